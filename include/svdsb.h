@@ -1,0 +1,263 @@
+/*
+ * svdsb.h -- C ABI of the B200-native PHSVDS hot path (libsvdsb.so).
+ *
+ * Everything below is plain C: opaque handles, raw pointers, 64-bit sizes,
+ * int status codes.  No torch / C++ types cross this boundary, so the same
+ * library can be bound from ctypes (what the Python package does), cgo, JNI
+ * or N-API.  See INTEGRATION.md for the binding stubs.
+ *
+ * Conventions (PRIMME's, fixed as stable API by the reference spec,
+ * /root/reference/SPEC.md:183 and PAPER.md:701-709):
+ *   - dense blocks are column-major fp64 with an explicit leading dimension
+ *     (x, ldx): element (i, j) lives at x[i + j*ldx];
+ *   - every pointer named x/y/v/w/... is a DEVICE pointer unless the
+ *     parameter name ends in _host;
+ *   - every call is asynchronous on the caller's CUDA stream (`stream`,
+ *     a cudaStream_t passed as void*; NULL = legacy default stream) unless
+ *     documented otherwise;
+ *   - return value 0 = success, < 0 = error; svdsb_last_error() returns the
+ *     message of the last failure on the calling thread.
+ *
+ * Reference interfaces each entry point replaces are cited per function
+ * (paths relative to /root/reference).
+ */
+#ifndef SVDSB_H
+#define SVDSB_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVDSB_OK 0
+#define SVDSB_ERR_ARG (-1)      /* invalid argument (maps to ValueError)   */
+#define SVDSB_ERR_CUDA (-2)     /* CUDA runtime failure                    */
+#define SVDSB_ERR_ALLOC (-3)    /* device/host allocation failure          */
+#define SVDSB_ERR_RANGE (-4)    /* size beyond the int32-index device layout */
+
+typedef struct svdsb_ctx svdsb_ctx;  /* per-stream workspace for reductions */
+typedef struct svdsb_csr svdsb_csr;  /* device CSR of A plus stored A^T     */
+
+/* ------------------------------------------------------------------ */
+/* library / context                                                   */
+
+int svdsb_version(void);
+const char *svdsb_last_error(void);
+/* Number of kernels this library launched since load (the bench's
+ * gpu_launches evidence). */
+int64_t svdsb_launch_count(void);
+
+/* A context owns the device workspace used by the deterministic two-level
+ * reductions (per-CTA partials + a ticket counter).  One context per stream
+ * in flight. */
+int svdsb_ctx_create(int device, svdsb_ctx **out);
+int svdsb_ctx_destroy(svdsb_ctx *ctx);
+
+/* ------------------------------------------------------------------ */
+/* sparse matrix: replaces SparseMatrixCsr (pkg/src/itersvd/matio.py:22-123) */
+
+#define SVDSB_CSR_TRANSPOSE 1   /* also build CSR(A^T) on device          */
+
+/* Upload a host CSR in the reference layout (int64 row_ptr[m+1], int64
+ * col_idx[nnz] strictly increasing per row, fp64 values[nnz]); validates
+ * like SparseMatrixCsr.__init__ (matio.py:35-52), stores int32 indices on
+ * device, and with SVDSB_CSR_TRANSPOSE builds CSR(A^T) equal bit for bit to
+ * SparseMatrixCsr.from_coo(n, m, col_idx, rows, values) (matio.py:63-92).
+ * Synchronises `stream` before returning. */
+int svdsb_csr_create_host(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nnz,
+                          const int64_t *row_ptr_host,
+                          const int64_t *col_idx_host,
+                          const double *values_host, int flags, void *stream,
+                          svdsb_csr **out);
+/* Assemble from COO triplets already on device (int64 rows/cols, fp64
+ * vals) with SparseMatrixCsr.from_coo semantics (matio.py:63-92): entries
+ * sorted by (row, col), duplicates summed in ascending input order. */
+int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n,
+                                int64_t ntrip, const int64_t *rows,
+                                const int64_t *cols, const double *vals,
+                                int flags, void *stream, svdsb_csr **out);
+int svdsb_csr_destroy(svdsb_csr *a);
+int svdsb_csr_shape(const svdsb_csr *a, int64_t *m, int64_t *n, int64_t *nnz);
+/* Copy CSR(A) (transpose = 0) or CSR(A^T) (transpose = 1) back to host in
+ * the reference's int64/fp64 layout (bit-exactness checks).  Synchronous. */
+int svdsb_csr_export_host(const svdsb_csr *a, int transpose,
+                          int64_t *row_ptr_host, int64_t *col_idx_host,
+                          double *values_host);
+
+/* Borrow the device arrays of CSR(A) (transpose = 0) or CSR(A^T): int32
+ * row_ptr[rows+1], int32 col[nnz], fp64 val[nnz].  Valid until destroy. */
+int svdsb_csr_device_arrays(const svdsb_csr *a, int transpose,
+                            const int **row_ptr, const int **col,
+                            const double **val);
+
+/* y = op(A) x for a block of `block` columns: the PRIMME matrixMatvec
+ * contract; replaces spmv_block (matio.py:126-155) and
+ * SvdOperator.apply / apply_t (operators.py:117-129).
+ * transpose = 0: x is n x block, y is m x block; transpose = 1: A^T.
+ * Summation order per output element reproduces the reference bit for bit
+ * for rows that fit one tile: forward = p0 + numpy-pairwise(p1..) of the
+ * rounded products (np.add.reduceat), transpose = left-to-right over
+ * ascending rows (np.add.at).  Rows longer than a tile use a deterministic
+ * chunked reduction instead. */
+int svdsb_matvec(svdsb_ctx *ctx, const svdsb_csr *a, int transpose,
+                 const double *x, int64_t ldx, double *y, int64_t ldy,
+                 int block, void *stream);
+/* Normal-equations operator without forming it (make_normal_operator,
+ * operators.py:163-172): side 0 -> y = A^T (A x) (dimension n),
+ * side 1 -> y = A (A^T x) (dimension m).  tmp: scratch of the inner
+ * dimension x block (ldtmp). */
+int svdsb_apply_normal(svdsb_ctx *ctx, const svdsb_csr *a, int side,
+                       const double *x, int64_t ldx, double *y, int64_t ldy,
+                       int block, double *tmp, int64_t ldtmp, void *stream);
+/* Augmented operator [0 A^T; A 0] on stacked [v (n); u (m)] vectors
+ * (make_augmented_operator, operators.py:175-190): y[:n] = A^T x[n:],
+ * y[n:] = A x[:n]. */
+int svdsb_apply_augmented(svdsb_ctx *ctx, const svdsb_csr *a, const double *x,
+                          int64_t ldx, double *y, int64_t ldy, int block,
+                          void *stream);
+
+/* Point-Jacobi diagonal (jacobi_precond_on_normal, operators.py:225-249):
+ * side 0 -> squared column norms (column_sq_norms, matio.py:115-118),
+ * side 1 -> squared row norms (row_sq_norms, matio.py:120-123); each clamped
+ * below at EPS * max.  d has n (side 0) or m (side 1) entries. Bit-exact. */
+int svdsb_precond_diag(svdsb_ctx *ctx, const svdsb_csr *a, int side,
+                       double *d, void *stream);
+/* y = x ./ d (applyPreconditioner; the lambda at
+ * operators.py:249).  y may alias x. */
+int svdsb_diag_solve(int64_t dim, const double *d, const double *x,
+                     int64_t ldx, double *y, int64_t ldy, int block,
+                     void *stream);
+
+/* ------------------------------------------------------------------ */
+/* tall-skinny fp64 kernels (kernels.py, eigensolver.py dense work).      */
+/* Up to SVDSB_MAX_BLOCKS column blocks can be passed as one concatenated */
+/* operand [X_0 | X_1 | ...] (the `against` lists of kernels.py:47-51).   */
+
+#define SVDSB_MAX_BLOCKS 4
+
+/* C (ldc) = [X_0|X_1|..]^T Y : (sum cols) x b, deterministic two-level
+ * reduction.  Replaces b.T @ v (kernels.py:50), V^T W (eigensolver.py:351,
+ * :690).  If norms2 != NULL also writes ||Y[:,j]||^2 (before anything). */
+int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs,
+               const int64_t *ldxs, const int *cols, const double *y,
+               int64_t ldy, int b, double *c, int64_t ldc, double *norms2,
+               void *stream);
+/* Y -= [X_0|X_1|..] C  (C device, (sum cols) x b, ldc); then, if norms2
+ * != NULL, norms2[j] = ||Y[:,j]||^2 of the updated block.  One classical
+ * Gram-Schmidt projection (kernels.py:47-51 / :497-499). */
+int svdsb_project_out(svdsb_ctx *ctx, int64_t dim, int nblk,
+                      const double *const *xs, const int64_t *ldxs,
+                      const int *cols, const double *c, int64_t ldc, double *y,
+                      int64_t ldy, int b, double *norms2, void *stream);
+/* Y = alpha * X C + beta * Y ; X dim x g, C (device) g x s.  Y must not
+ * alias X.  Replaces V @ coefs (eigensolver.py:526-527), V @ y (:390,
+ * :710, :760).  beta == 0 never reads Y. */
+int svdsb_ts_gemm(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx,
+                  int g, const double *c, int64_t ldc, int s, double alpha,
+                  double beta, double *y, int64_t ldy, void *stream);
+/* Fused Ritz candidates (eigensolver.py:385-394): for j < p
+ *   X[:,j] = V Yc[:,j], OX[:,j] = W Yc[:,j], R[:,j] = OX[:,j] - lam[j] X[:,j]
+ * writes R (and X / OX when non-NULL) and rn2[j] = ||R[:,j]||^2.
+ * lam, yc, rn2 are device arrays. */
+int svdsb_ritz_residual(svdsb_ctx *ctx, int64_t dim, const double *v,
+                        int64_t ldv, const double *w, int64_t ldw, int g,
+                        const double *yc, int64_t ldyc, const double *lam,
+                        int p, double *r, int64_t ldr, double *x, int64_t ldx,
+                        double *ox, int64_t ldox, double *rn2, void *stream);
+/* out[j] = ||X[:,j]||^2 (deterministic). */
+int svdsb_col_norms2(svdsb_ctx *ctx, int64_t dim, const double *x,
+                     int64_t ldx, int b, double *out, void *stream);
+/* Column dot products out[j] = X[:,j] . Y[:,j]. */
+int svdsb_col_dots(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx,
+                   const double *y, int64_t ldy, int b, double *out,
+                   void *stream);
+/* Y[:,j] = X[:,j] * f(s[j]) with s a DEVICE array: mode 0 multiply,
+ * mode 1 divide, mode 2 divide by sqrt (normalise from a squared norm).
+ * Columns whose factor is 0 (mode 1/2) are left untouched.  Y may alias X. */
+int svdsb_scale_cols(int64_t dim, const double *x, int64_t ldx, int b,
+                     const double *s, int mode, double *y, int64_t ldy,
+                     void *stream);
+/* Y = alpha X + beta Y elementwise on dim x b. */
+int svdsb_axpby(int64_t dim, int b, double alpha, const double *x,
+                int64_t ldx, double beta, double *y, int64_t ldy,
+                void *stream);
+/* Stage-2 split statistics of candidate vectors on the stacked layout
+ * [v (nsplit); u (dim-nsplit)] (hybrid.py:226-241, :413-423): for each
+ * column j writes 6 sums to out[6j..6j+5]:
+ *   ||r_v||^2, r_v.x_v, ||x_v||^2, ||r_u||^2, r_u.x_u, ||x_u||^2 */
+int svdsb_split_stats(svdsb_ctx *ctx, int64_t dim, int64_t nsplit,
+                      const double *r, int64_t ldr, const double *x,
+                      int64_t ldx, int b, double *out, void *stream);
+
+/* Exact stage-2 split residual from the split statistics (hybrid.py:
+ * 226-241): with nv = ||x_v||, nu = ||x_u||, sigma = |lam[j]| (lam device),
+ *   e1 = r_u/nv + (lam/nv - sigma/nu) x_u   (= A v^ - sigma u^)
+ *   e2 = r_v/nu + (lam/nu - sigma/nv) x_v   (= A^T u^ - sigma v^)
+ * out[j] = ||e1||^2 + ||e2||^2, formed elementwise (no cancellation).
+ * stats: the 6-per-column output of svdsb_split_stats (device).  Columns
+ * with nv == 0 or nu == 0 get out[j] = +inf. */
+int svdsb_split_residual(svdsb_ctx *ctx, int64_t dim, int64_t nsplit,
+                         const double *r, int64_t ldr, const double *x,
+                         int64_t ldx, int b, const double *lam,
+                         const double *stats, double *out, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* small dense kernels (one CTA; g <= SVDSB_SMALL_MAX)                     */
+
+#define SVDSB_SMALL_MAX 64
+
+#define SVDSB_ORDER_ASC 0       /* np.linalg.eigh order                     */
+#define SVDSB_ORDER_DESC 1      /* argsort(-lams, stable)  (eigensolver.py:256) */
+#define SVDSB_ORDER_INTERIOR 2  /* _interior_order (eigensolver.py:148-154) */
+
+/* Symmetric eigendecomposition of the g x g matrix H (ldh), reordered per
+ * `order` (shift used by INTERIOR): w[g] values, Y (ldy) orthonormal
+ * eigenvector columns.  Replaces sym_eig (kernels.py:136-145) +
+ * extract_rayleigh_ritz (eigensolver.py:362-367).  Cyclic Jacobi in fp64. */
+int svdsb_syev_small(int g, const double *h, int64_t ldh, int order,
+                     double shift, double *w, double *y, int64_t ldy,
+                     void *stream);
+/* Refined extraction (eigensolver.py:369-380): y = right singular vector
+ * of the smallest singular value of the g x g matrix R (ldr), lam = y^T H y.
+ * One-sided Jacobi SVD.  sv (optional, g) receives singular values desc. */
+int svdsb_refined_small(int g, const double *r, int64_t ldr, const double *h,
+                        int64_t ldh, double *y, double *lam, double *sv,
+                        void *stream);
+/* Thick-restart coefficient selection (eigensolver.py:485-515 with
+ * _coef_gs :438-459 and _padded_prev :461-469): the priority list
+ * [yfirst (optional)] + the ny ordered Ritz coefficient columns of yall
+ * is orthonormalised in order against `exclude` (optional g-vector),
+ * 2 modified Gram-Schmidt passes, dropping norms <= 1e-8, keeping at most
+ * `retain`; then up to max(min(plus_k, gmax-1-kept), 0) previous
+ * coefficient columns (prev, prev_g x nprev, zero padded to g; skipped
+ * when prev_g > g) against [exclude] + kept.  Result g x s in out (ldo);
+ * s written to count_dev[0] (device int). */
+int svdsb_restart_coefs(int g, int gmax, const double *yfirst,
+                        const double *yall, int64_t ldy, int ny, int retain,
+                        const double *exclude, const double *prev,
+                        int64_t ldp, int nprev, int prev_g, int plus_k,
+                        double *out, int64_t ldo, int *count_dev,
+                        void *stream);
+/* Hout (s x s) = sym(C^T H C), C g x s (eigensolver.py:528-531). */
+int svdsb_project_small(int g, int s, const double *h, int64_t ldh,
+                        const double *c, int64_t ldc, double *hout,
+                        int64_t ldho, void *stream);
+/* Thin QR of M = R Y (R g x g, Y g x s) with nonnegative diag:
+ * qy (g x s), ry (s x s)  (qr_restart, kernels.py:225-242). */
+int svdsb_qr_small(int g, int s, const double *r, int64_t ldr,
+                   const double *yc, int64_t ldy, double *qy, int64_t ldq,
+                   double *ry, int64_t ldry, void *stream);
+/* Insert the Gram block hc ((g+b) x b, ldhc) as new columns g..g+b-1 of the
+ * symmetric projection H (eigensolver.py:690-694). */
+int svdsb_h_insert(int g, int b, const double *hc, int64_t ldhc, double *h,
+                   int64_t ldh, void *stream);
+/* H (g x g) = sym(G) (eigensolver.py:349-352). */
+int svdsb_h_symmetrize(int g, const double *gm, int64_t ldg, double *h,
+                       int64_t ldh, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVDSB_H */

@@ -1,0 +1,149 @@
+"""ctypes binding of libsvdsb.so (the C ABI declared in include/svdsb.h).
+
+This is the only place the package touches native code.  There is no CPU
+fallback: if the shared library is missing, or CUDA is unavailable when a
+device operation is requested, the call raises.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libsvdsb.so")
+
+c_double_p = ctypes.POINTER(ctypes.c_double)
+c_int64_p = ctypes.POINTER(ctypes.c_int64)
+c_int_p = ctypes.POINTER(ctypes.c_int)
+c_void_p = ctypes.c_void_p
+i64 = ctypes.c_int64
+i32 = ctypes.c_int
+f64 = ctypes.c_double
+vp = ctypes.c_void_p
+
+# (name, restype, argtypes)
+_PROTOS = [
+    ("svdsb_version", i32, []),
+    ("svdsb_last_error", ctypes.c_char_p, []),
+    ("svdsb_launch_count", i64, []),
+    ("svdsb_ctx_create", i32, [i32, ctypes.POINTER(vp)]),
+    ("svdsb_ctx_destroy", i32, [vp]),
+    ("svdsb_csr_create_host", i32, [vp, i64, i64, i64, vp, vp, vp, i32, vp, ctypes.POINTER(vp)]),
+    ("svdsb_csr_create_coo_device", i32, [vp, i64, i64, i64, vp, vp, vp, i32, vp, ctypes.POINTER(vp)]),
+    ("svdsb_csr_destroy", i32, [vp]),
+    ("svdsb_csr_shape", i32, [vp, c_int64_p, c_int64_p, c_int64_p]),
+    ("svdsb_csr_export_host", i32, [vp, i32, vp, vp, vp]),
+    ("svdsb_csr_device_arrays", i32, [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)]),
+    ("svdsb_matvec", i32, [vp, vp, i32, vp, i64, vp, i64, i32, vp]),
+    ("svdsb_apply_normal", i32, [vp, vp, i32, vp, i64, vp, i64, i32, vp, i64, vp]),
+    ("svdsb_apply_augmented", i32, [vp, vp, vp, i64, vp, i64, i32, vp]),
+    ("svdsb_precond_diag", i32, [vp, vp, i32, vp, vp]),
+    ("svdsb_diag_solve", i32, [i64, vp, vp, i64, vp, i64, i32, vp]),
+    ("svdsb_gram", i32, [vp, i64, i32, vp, vp, vp, vp, i64, i32, vp, i64, vp, vp]),
+    ("svdsb_project_out", i32, [vp, i64, i32, vp, vp, vp, vp, i64, vp, i64, i32, vp, vp]),
+    ("svdsb_ts_gemm", i32, [vp, i64, vp, i64, i32, vp, i64, i32, f64, f64, vp, i64, vp]),
+    ("svdsb_ritz_residual", i32, [vp, i64, vp, i64, vp, i64, i32, vp, i64, vp, i32, vp, i64, vp, i64,
+                                  vp, i64, vp, vp]),
+    ("svdsb_col_norms2", i32, [vp, i64, vp, i64, i32, vp, vp]),
+    ("svdsb_col_dots", i32, [vp, i64, vp, i64, vp, i64, i32, vp, vp]),
+    ("svdsb_scale_cols", i32, [i64, vp, i64, i32, vp, i32, vp, i64, vp]),
+    ("svdsb_axpby", i32, [i64, i32, f64, vp, i64, f64, vp, i64, vp]),
+    ("svdsb_split_stats", i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp]),
+    ("svdsb_split_residual", i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp, vp, vp]),
+    ("svdsb_syev_small", i32, [i32, vp, i64, i32, f64, vp, vp, i64, vp]),
+    ("svdsb_refined_small", i32, [i32, vp, i64, vp, i64, vp, vp, vp, vp]),
+    ("svdsb_restart_coefs", i32, [i32, i32, vp, vp, i64, i32, i32, vp, vp, i64, i32, i32, i32, vp, i64,
+                                  vp, vp]),
+    ("svdsb_project_small", i32, [i32, i32, vp, i64, vp, i64, vp, i64, vp]),
+    ("svdsb_qr_small", i32, [i32, i32, vp, i64, vp, i64, vp, i64, vp, i64, vp]),
+    ("svdsb_h_insert", i32, [i32, i32, vp, i64, vp, i64, vp]),
+    ("svdsb_h_symmetrize", i32, [i32, vp, i64, vp, i64, vp]),
+]
+
+EXPORTED = [p[0] for p in _PROTOS]
+
+SVDSB_CSR_TRANSPOSE = 1
+ORDER_ASC, ORDER_DESC, ORDER_INTERIOR = 0, 1, 2
+SMALL_MAX = 64
+MAX_BLOCKS = 4
+
+
+class NativeError(RuntimeError):
+    """A libsvdsb call failed (CUDA error or invalid device state)."""
+
+
+_lib = None
+
+
+def load():
+    """Load libsvdsb.so once; raise loudly when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            "libsvdsb.so not found at %s; build it with "
+            "`python -m paper_1607_01404_b200.build` (nvcc, sm_100a)" % LIB_PATH)
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, res, args in _PROTOS:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error():
+    return load().svdsb_last_error().decode(errors="replace")
+
+
+def check(rc, what=""):
+    if rc == 0:
+        return
+    msg = last_error()
+    if rc in (-1, -4):
+        raise ValueError(msg or what)
+    raise NativeError("%s failed (%d): %s" % (what, rc, msg))
+
+
+def call(name, *args):
+    rc = getattr(load(), name)(*args)
+    check(rc, name)
+
+
+def launch_count():
+    return int(load().svdsb_launch_count())
+
+
+def np_ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def ptr_array(ptrs):
+    arr = (ctypes.c_void_p * MAX_BLOCKS)()
+    for i, p in enumerate(ptrs):
+        arr[i] = p
+    return arr
+
+
+def i64_array(vals):
+    arr = (ctypes.c_int64 * MAX_BLOCKS)()
+    for i, v in enumerate(vals):
+        arr[i] = int(v)
+    return arr
+
+
+def int_array(vals):
+    arr = (ctypes.c_int * MAX_BLOCKS)()
+    for i, v in enumerate(vals):
+        arr[i] = int(v)
+    return arr
+
+
+def as_i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def as_f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)

@@ -1,0 +1,761 @@
+// Device CSR of A with a stored transpose, and the block SpMV kernels.
+//
+// Reference: SparseMatrixCsr / spmv_block (pkg/src/itersvd/matio.py:22-155).
+// The reference keeps no transpose and scatters with np.add.at; here A^T is
+// stored as its own CSR (a stable counting/radix sort by column, bit-exact
+// with SparseMatrixCsr.from_coo(n, m, col_idx, rows, values)) so both
+// products are row-gathers with coalesced index/value streams.
+//
+// Kernel design (HBM-bound, ~0.17 flop/byte):
+//  * short rows: "CSR-stream" tiles of <= 256 rows / <= 2048 nnz per CTA.
+//    Values and indices stream in coalesced, the gathered products land in
+//    shared memory, then one thread per row folds its products in the exact
+//    order the reference's NumPy code uses, so results are bit-identical:
+//      forward  : p0 + pairwise(p1..)   (np.add.reduceat, matio.py:146-149)
+//      transpose: ((0 + p0) + p1) + ... (np.add.at, matio.py:150-154)
+//    Products are rounded before the add (no FMA contraction).
+//  * long rows (> 2048 nnz, e.g. the Zipf head columns of config 4's A^T):
+//    split into 8192-nnz chunks, one CTA each, fixed-order in-CTA tree then a
+//    fix-up kernel summing the chunk partials in chunk order: deterministic,
+//    not bit-identical to a serial sum.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace svdsb {
+
+constexpr int kTileThreads = 256;
+constexpr int kTileNnz = 2048;                    // 8 per thread
+constexpr int kTileRows = 256;
+constexpr int kLongChunk = 8192;                  // 32 per thread
+constexpr int kPerThread = kTileNnz / kTileThreads;
+
+struct CsrPart {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  int *row_ptr = nullptr;   // rows+1
+  int *col = nullptr;       // nnz
+  double *val = nullptr;    // nnz
+  // short-row tiles: [tile_r0[i], tile_r1[i])
+  int ntile = 0;
+  int *tile_r = nullptr;    // 2*ntile
+  // long rows, split in chunks
+  int nlong = 0;
+  int *long_row = nullptr;  // nlong
+  int *long_cptr = nullptr; // nlong+1 : chunk range of each long row
+  int nchunk = 0;
+  int *chunk_nz = nullptr;  // 2*nchunk : [nz0, nz1)
+  double *chunk_part = nullptr;  // nchunk * kMaxB partial sums
+  std::vector<int> host_row_ptr;
+};
+
+constexpr int kMaxB = 64;   // largest block handled by one matvec call
+
+}  // namespace svdsb
+
+struct svdsb_csr {
+  int device;
+  svdsb::CsrPart a, at;
+  bool has_t;
+};
+
+namespace svdsb {
+
+// ---------------------------------------------------------------- helpers
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+
+// NumPy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// DOUBLE_pairwise_sum) as used by np.add.reduceat for the tail of a segment.
+__device__ double np_pairwise(const double *a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = dadd(r, a[i]);
+    return r;
+  } else if (n <= 128) {
+    double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3];
+    double r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+      r0 = dadd(r0, a[i + 0]); r1 = dadd(r1, a[i + 1]);
+      r2 = dadd(r2, a[i + 2]); r3 = dadd(r3, a[i + 3]);
+      r4 = dadd(r4, a[i + 4]); r5 = dadd(r5, a[i + 5]);
+      r6 = dadd(r6, a[i + 6]); r7 = dadd(r7, a[i + 7]);
+    }
+    double res = dadd(dadd(dadd(r0, r1), dadd(r2, r3)), dadd(dadd(r4, r5), dadd(r6, r7)));
+    for (; i < n; ++i) res = dadd(res, a[i]);
+    return res;
+  } else {
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return dadd(np_pairwise(a, n2), np_pairwise(a + n2, n - n2));
+  }
+}
+
+// ORDER 0: forward (reduceat) ; ORDER 1: sequential (add.at)
+template <int ORDER>
+__device__ __forceinline__ double fold_row(const double *p, int len) {
+  if (ORDER == 0) {
+    if (len == 0) return 0.0;
+    if (len == 1) return p[0];
+    return dadd(p[0], np_pairwise(p + 1, len - 1));
+  } else {
+    double s = 0.0;
+    for (int i = 0; i < len; ++i) s = dadd(s, p[i]);
+    return s;
+  }
+}
+
+template <int ORDER>
+__global__ void __launch_bounds__(kTileThreads)
+csr_tile_kernel(const int *__restrict__ tile_r, const int *__restrict__ row_ptr,
+                const int *__restrict__ col, const double *__restrict__ val,
+                const double *__restrict__ x, int64_t ldx, double *__restrict__ y,
+                int64_t ldy, int b) {
+  __shared__ double prod[kTileNnz];
+  __shared__ int rp[kTileRows + 1];
+  const int t = threadIdx.x;
+  const int r0 = tile_r[2 * blockIdx.x], r1 = tile_r[2 * blockIdx.x + 1];
+  const int nrows = r1 - r0;
+  for (int i = t; i <= nrows; i += kTileThreads) rp[i] = row_ptr[r0 + i];
+  __syncthreads();
+  const int nz0 = rp[0], nnz = rp[nrows] - nz0;
+  double v[kPerThread];
+  int c[kPerThread];
+#pragma unroll
+  for (int i = 0; i < kPerThread; ++i) {
+    int k = t + i * kTileThreads;
+    if (k < nnz) {
+      v[i] = __ldg(val + nz0 + k);
+      c[i] = __ldg(col + nz0 + k);
+    } else {
+      v[i] = 0.0;
+      c[i] = 0;
+    }
+  }
+  int my0 = 0, mylen = 0;
+  if (t < nrows) {
+    my0 = rp[t] - nz0;
+    mylen = rp[t + 1] - rp[t];
+  }
+  for (int cc = 0; cc < b; ++cc) {
+    const double *xc = x + cc * ldx;
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) {
+      int k = t + i * kTileThreads;
+      if (k < nnz) prod[k] = dmul(v[i], __ldg(xc + c[i]));
+    }
+    __syncthreads();
+    if (t < nrows) y[(int64_t)(r0 + t) + cc * ldy] = fold_row<ORDER>(prod + my0, mylen);
+    __syncthreads();
+  }
+}
+
+// One CTA per chunk of a long row: partial sums of b columns.
+__global__ void __launch_bounds__(kTileThreads)
+csr_chunk_kernel(const int *__restrict__ chunk_nz, const int *__restrict__ col,
+                 const double *__restrict__ val, const double *__restrict__ x,
+                 int64_t ldx, int b, double *__restrict__ part) {
+  __shared__ double red[kTileThreads / 32];
+  const int nz0 = chunk_nz[2 * blockIdx.x], nz1 = chunk_nz[2 * blockIdx.x + 1];
+  const int t = threadIdx.x;
+  for (int cc = 0; cc < b; ++cc) {
+    const double *xc = x + cc * ldx;
+    double s = 0.0;
+    for (int k = nz0 + t; k < nz1; k += kTileThreads) s = fma(__ldg(val + k), __ldg(xc + __ldg(col + k)), s);
+    s = warp_sum(s);
+    if ((t & 31) == 0) red[t >> 5] = s;
+    __syncthreads();
+    if (t == 0) {
+      double acc = 0.0;
+      for (int w = 0; w < kTileThreads / 32; ++w) acc += red[w];
+      part[(int64_t)blockIdx.x * kMaxB + cc] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void csr_long_fixup_kernel(int nlong, const int *__restrict__ long_row,
+                                      const int *__restrict__ long_cptr,
+                                      const double *__restrict__ part, int b,
+                                      double *__restrict__ y, int64_t ldy) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nlong * b) return;
+  int li = i / b, cc = i % b;
+  double s = 0.0;
+  for (int ch = long_cptr[li]; ch < long_cptr[li + 1]; ++ch) s += part[(int64_t)ch * kMaxB + cc];
+  y[(int64_t)long_row[li] + cc * ldy] = s;
+}
+
+// ---------------------------------------------------------------- partition
+
+static void free_part(CsrPart &p) {
+  cudaFree(p.row_ptr);
+  cudaFree(p.col);
+  cudaFree(p.val);
+  cudaFree(p.tile_r);
+  cudaFree(p.long_row);
+  cudaFree(p.long_cptr);
+  cudaFree(p.chunk_nz);
+  cudaFree(p.chunk_part);
+  p = CsrPart();
+}
+
+template <typename T>
+static int upload(T **dst, const std::vector<T> &src, cudaStream_t st) {
+  size_t n = std::max<size_t>(src.size(), 1);
+  SVDSB_CUDA(cudaMalloc(dst, n * sizeof(T)));
+  if (!src.empty())
+    SVDSB_CUDA(cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  return SVDSB_OK;
+}
+
+// Tile the rows (host; row_ptr already on host in p.host_row_ptr).
+static int build_partition(CsrPart &p, cudaStream_t st) {
+  const std::vector<int> &rp = p.host_row_ptr;
+  std::vector<int> tiles, lrows, lcptr, cnz;
+  int open = -1, nrows = 0, nnz_blk = 0;
+  auto close = [&](int r_end) {
+    if (open >= 0) {
+      tiles.push_back(open);
+      tiles.push_back(r_end);
+    }
+    open = -1;
+    nrows = 0;
+    nnz_blk = 0;
+  };
+  lcptr.push_back(0);
+  for (int64_t r = 0; r < p.rows; ++r) {
+    int len = rp[r + 1] - rp[r];
+    if (len > kTileNnz) {
+      close((int)r);
+      lrows.push_back((int)r);
+      for (int z = rp[r]; z < rp[r + 1]; z += kLongChunk) {
+        cnz.push_back(z);
+        cnz.push_back(std::min(z + kLongChunk, rp[r + 1]));
+      }
+      lcptr.push_back((int)(cnz.size() / 2));
+      continue;
+    }
+    if (open >= 0 && (nrows == kTileRows || nnz_blk + len > kTileNnz)) close((int)r);
+    if (open < 0) open = (int)r;
+    nrows += 1;
+    nnz_blk += len;
+  }
+  close((int)p.rows);
+  p.ntile = (int)(tiles.size() / 2);
+  p.nlong = (int)lrows.size();
+  p.nchunk = (int)(cnz.size() / 2);
+  int rc;
+  if ((rc = upload(&p.tile_r, tiles, st))) return rc;
+  if ((rc = upload(&p.long_row, lrows, st))) return rc;
+  if ((rc = upload(&p.long_cptr, lcptr, st))) return rc;
+  if ((rc = upload(&p.chunk_nz, cnz, st))) return rc;
+  SVDSB_CUDA(cudaMalloc(&p.chunk_part, sizeof(double) * kMaxB * std::max(p.nchunk, 1)));
+  return SVDSB_OK;
+}
+
+// y = P x for one orientation.
+template <int ORDER>
+static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, double *y,
+                       int64_t ldy, int b, cudaStream_t st) {
+  if (p.rows == 0) return SVDSB_OK;
+  for (int c0 = 0; c0 < b; c0 += kMaxB) {
+    int bb = std::min(kMaxB, b - c0);
+    const double *xc = x + (int64_t)c0 * ldx;
+    double *yc = y + (int64_t)c0 * ldy;
+    if (p.ntile > 0) {
+      csr_tile_kernel<ORDER><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, xc,
+                                                               ldx, yc, ldy, bb);
+      SVDSB_LAUNCHED();
+    }
+    if (p.nlong > 0) {
+      csr_chunk_kernel<<<p.nchunk, kTileThreads, 0, st>>>(p.chunk_nz, p.col, p.val, xc, ldx, bb,
+                                                          p.chunk_part);
+      SVDSB_LAUNCHED();
+      int tot = p.nlong * bb;
+      csr_long_fixup_kernel<<<(tot + 255) / 256, 256, 0, st>>>(p.nlong, p.long_row, p.long_cptr,
+                                                               p.chunk_part, bb, yc, ldy);
+      SVDSB_LAUNCHED();
+    }
+  }
+  return SVDSB_OK;
+}
+
+// ---------------------------------------------------------------- transpose
+
+__global__ void expand_rows_kernel(int64_t m, const int *__restrict__ row_ptr, int *__restrict__ rows) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  for (int k = row_ptr[r]; k < row_ptr[r + 1]; ++k) rows[k] = (int)r;
+}
+
+__global__ void iota_kernel(int64_t n, int *__restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (int)i;
+}
+
+__global__ void count_kernel(int64_t nnz, const int *__restrict__ keys, int *__restrict__ counts) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nnz) atomicAdd(counts + keys[i], 1);
+}
+
+__global__ void gather_t_kernel(int64_t nnz, const int *__restrict__ perm, const int *__restrict__ rows,
+                                const double *__restrict__ val, int *__restrict__ tcol,
+                                double *__restrict__ tval) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  int k = perm[i];
+  tcol[i] = rows[k];
+  tval[i] = val[k];
+}
+
+static int bits_for(int64_t n) {
+  int b = 1;
+  while (b < 63 && ((int64_t)1 << b) < n) ++b;
+  return b;
+}
+
+static inline unsigned grid1(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+// Build at = CSR(A^T) from a (both on device).  Stable LSD radix sort by
+// column keeps ascending row order inside each column, which is exactly the
+// (col, row) lexsort of from_coo (matio.py:80-81) on a duplicate-free input.
+static int build_transpose(const CsrPart &a, CsrPart &at, cudaStream_t st) {
+  at.rows = a.cols;
+  at.cols = a.rows;
+  at.nnz = a.nnz;
+  const int64_t nnz = a.nnz;
+  SVDSB_CUDA(cudaMalloc(&at.row_ptr, sizeof(int) * (at.rows + 1)));
+  SVDSB_CUDA(cudaMalloc(&at.col, sizeof(int) * std::max<int64_t>(nnz, 1)));
+  SVDSB_CUDA(cudaMalloc(&at.val, sizeof(double) * std::max<int64_t>(nnz, 1)));
+  SVDSB_CUDA(cudaMemsetAsync(at.row_ptr, 0, sizeof(int) * (at.rows + 1), st));
+  if (nnz > 0) {
+    int *rows = nullptr, *idx = nullptr, *keys_out = nullptr, *perm = nullptr, *counts = nullptr;
+    SVDSB_CUDA(cudaMalloc(&rows, sizeof(int) * nnz));
+    SVDSB_CUDA(cudaMalloc(&idx, sizeof(int) * nnz));
+    SVDSB_CUDA(cudaMalloc(&keys_out, sizeof(int) * nnz));
+    SVDSB_CUDA(cudaMalloc(&perm, sizeof(int) * nnz));
+    SVDSB_CUDA(cudaMalloc(&counts, sizeof(int) * (at.rows + 1)));
+    SVDSB_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * (at.rows + 1), st));
+    expand_rows_kernel<<<grid1(a.rows), 256, 0, st>>>(a.rows, a.row_ptr, rows);
+    SVDSB_LAUNCHED();
+    iota_kernel<<<grid1(nnz), 256, 0, st>>>(nnz, idx);
+    SVDSB_LAUNCHED();
+    size_t tmp_bytes = 0;
+    int nbits = bits_for(a.cols);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, a.col, keys_out, idx, perm, (int)nnz, 0, nbits, st);
+    void *tmp = nullptr;
+    SVDSB_CUDA(cudaMalloc(&tmp, tmp_bytes));
+    SVDSB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, a.col, keys_out, idx, perm, (int)nnz, 0,
+                                               nbits, st));
+    bump_launches();
+    gather_t_kernel<<<grid1(nnz), 256, 0, st>>>(nnz, perm, rows, a.val, at.col, at.val);
+    SVDSB_LAUNCHED();
+    // row_ptr of A^T: counts per column, exclusive scan into [0, rows]
+    count_kernel<<<grid1(nnz), 256, 0, st>>>(nnz, a.col, counts);
+    SVDSB_LAUNCHED();
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts, at.row_ptr, (int)(at.rows + 1), st);
+    void *scan_tmp = nullptr;
+    SVDSB_CUDA(cudaMalloc(&scan_tmp, scan_bytes));
+    SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, at.row_ptr, (int)(at.rows + 1), st));
+    bump_launches();
+    SVDSB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(rows);
+    cudaFree(idx);
+    cudaFree(keys_out);
+    cudaFree(perm);
+    cudaFree(counts);
+    cudaFree(tmp);
+    cudaFree(scan_tmp);
+  }
+  at.host_row_ptr.resize(at.rows + 1);
+  SVDSB_CUDA(cudaMemcpyAsync(at.host_row_ptr.data(), at.row_ptr, sizeof(int) * (at.rows + 1),
+                             cudaMemcpyDeviceToHost, st));
+  SVDSB_CUDA(cudaStreamSynchronize(st));
+  return build_partition(at, st);
+}
+
+// ---------------------------------------------------------------- COO build
+
+__global__ void coo_keys_kernel(int64_t nt, int64_t n, const int64_t *__restrict__ r,
+                                const int64_t *__restrict__ c, unsigned long long *__restrict__ key,
+                                int *__restrict__ idx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  key[i] = (unsigned long long)(r[i] * n + c[i]);
+  idx[i] = (int)i;
+}
+
+__global__ void coo_first_kernel(int64_t nt, const unsigned long long *__restrict__ key, int *__restrict__ first) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  first[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+}
+
+// seg[i] = exclusive scan of first; segment s starts where first==1
+__global__ void coo_sum_kernel(int64_t nt, int64_t n, const unsigned long long *__restrict__ key,
+                               const int *__restrict__ perm, const int *__restrict__ first,
+                               const int *__restrict__ seg, const double *__restrict__ vals,
+                               int *__restrict__ col, double *__restrict__ val, int *__restrict__ rowcnt) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nt || !first[i]) return;
+  // np.add.at into zeros, ascending input order (stable sort keeps it)
+  double s = 0.0;
+  int64_t j = i;
+  do {
+    s = __dadd_rn(s, vals[perm[j]]);
+    ++j;
+  } while (j < nt && !first[j]);
+  int o = seg[i];
+  unsigned long long k = key[i];
+  int64_t r = (int64_t)(k / (unsigned long long)n);
+  col[o] = (int)(k - (unsigned long long)r * (unsigned long long)n);
+  val[o] = s;
+  atomicAdd(rowcnt + r, 1);
+}
+
+}  // namespace svdsb
+
+using namespace svdsb;
+
+extern "C" {
+
+int svdsb_csr_destroy(svdsb_csr *a) {
+  if (!a) return SVDSB_OK;
+  free_part(a->a);
+  free_part(a->at);
+  delete a;
+  return SVDSB_OK;
+}
+
+int svdsb_csr_shape(const svdsb_csr *a, int64_t *m, int64_t *n, int64_t *nnz) {
+  SVDSB_CHECK_ARG(a != nullptr, "svdsb_csr_shape: NULL handle");
+  if (m) *m = a->a.rows;
+  if (n) *n = a->a.cols;
+  if (nnz) *nnz = a->a.nnz;
+  return SVDSB_OK;
+}
+
+static int finish_create(svdsb_csr *h, int flags, cudaStream_t st) {
+  int rc = build_partition(h->a, st);
+  if (rc) return rc;
+  if (flags & SVDSB_CSR_TRANSPOSE) {
+    rc = build_transpose(h->a, h->at, st);
+    if (rc) return rc;
+    h->has_t = true;
+  }
+  SVDSB_CUDA(cudaStreamSynchronize(st));
+  return SVDSB_OK;
+}
+
+int svdsb_csr_create_host(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nnz, const int64_t *row_ptr_host,
+                          const int64_t *col_idx_host, const double *values_host, int flags, void *stream,
+                          svdsb_csr **out) {
+  (void)ctx;
+  SVDSB_CHECK_ARG(out != nullptr, "svdsb_csr_create_host: out is NULL");
+  SVDSB_CHECK_ARG(m >= 0 && n >= 0, "negative matrix dimension");
+  if (m >= INT32_MAX || n >= INT32_MAX || nnz >= INT32_MAX) {
+    set_error("matrix exceeds the int32-indexed device layout (m=%lld n=%lld nnz=%lld)", (long long)m,
+              (long long)n, (long long)nnz);
+    return SVDSB_ERR_RANGE;
+  }
+  SVDSB_CHECK_ARG(row_ptr_host != nullptr, "row_ptr is NULL");
+  // validation mirrors SparseMatrixCsr.__init__ (matio.py:41-52)
+  SVDSB_CHECK_ARG(row_ptr_host[0] == 0 && row_ptr_host[m] == nnz, "row_ptr endpoints inconsistent with nnz");
+  std::vector<int> rp(m + 1), ci(nnz);
+  for (int64_t r = 0; r <= m; ++r) {
+    if (r > 0 && row_ptr_host[r] < row_ptr_host[r - 1]) {
+      set_error("row_ptr must be nondecreasing");
+      return SVDSB_ERR_ARG;
+    }
+    rp[r] = (int)row_ptr_host[r];
+  }
+  for (int64_t k = 0; k < nnz; ++k) {
+    int64_t c = col_idx_host[k];
+    if (c < 0 || c >= n) {
+      set_error("column index out of range");
+      return SVDSB_ERR_ARG;
+    }
+    ci[k] = (int)c;
+  }
+  cudaStream_t st = as_stream(stream);
+  svdsb_csr *h = new svdsb_csr();
+  cudaGetDevice(&h->device);
+  h->has_t = false;
+  CsrPart &p = h->a;
+  p.rows = m;
+  p.cols = n;
+  p.nnz = nnz;
+  int rc;
+  if ((rc = upload(&p.row_ptr, rp, st)) || (rc = upload(&p.col, ci, st))) {
+    svdsb_csr_destroy(h);
+    return rc;
+  }
+  if (cudaMalloc(&p.val, sizeof(double) * std::max<int64_t>(nnz, 1)) != cudaSuccess) {
+    svdsb_csr_destroy(h);
+    set_error("cudaMalloc values failed");
+    return SVDSB_ERR_ALLOC;
+  }
+  if (nnz) cudaMemcpyAsync(p.val, values_host, sizeof(double) * nnz, cudaMemcpyHostToDevice, st);
+  p.host_row_ptr = std::move(rp);
+  rc = finish_create(h, flags, st);
+  if (rc) {
+    svdsb_csr_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return SVDSB_OK;
+}
+
+int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt, const int64_t *rows,
+                                const int64_t *cols, const double *vals, int flags, void *stream,
+                                svdsb_csr **out) {
+  (void)ctx;
+  SVDSB_CHECK_ARG(out != nullptr, "svdsb_csr_create_coo_device: out is NULL");
+  SVDSB_CHECK_ARG(m >= 0 && n >= 0 && nt >= 0, "negative size");
+  if (m >= INT32_MAX || n >= INT32_MAX || nt >= INT32_MAX) {
+    set_error("COO exceeds the int32-indexed device layout");
+    return SVDSB_ERR_RANGE;
+  }
+  cudaStream_t st = as_stream(stream);
+  svdsb_csr *h = new svdsb_csr();
+  cudaGetDevice(&h->device);
+  h->has_t = false;
+  CsrPart &p = h->a;
+  p.rows = m;
+  p.cols = n;
+  SVDSB_CUDA(cudaMalloc(&p.row_ptr, sizeof(int) * (m + 1)));
+  SVDSB_CUDA(cudaMemsetAsync(p.row_ptr, 0, sizeof(int) * (m + 1), st));
+  int64_t nnz = 0;
+  if (nt > 0) {
+    unsigned long long *key = nullptr, *key_s = nullptr;
+    int *idx = nullptr, *perm = nullptr, *first = nullptr, *seg = nullptr, *rowcnt = nullptr;
+    SVDSB_CUDA(cudaMalloc(&key, 8 * nt));
+    SVDSB_CUDA(cudaMalloc(&key_s, 8 * nt));
+    SVDSB_CUDA(cudaMalloc(&idx, 4 * nt));
+    SVDSB_CUDA(cudaMalloc(&perm, 4 * nt));
+    SVDSB_CUDA(cudaMalloc(&first, 4 * nt));
+    SVDSB_CUDA(cudaMalloc(&seg, 4 * (nt + 1)));
+    SVDSB_CUDA(cudaMalloc(&rowcnt, 4 * (m + 1)));
+    SVDSB_CUDA(cudaMemsetAsync(rowcnt, 0, 4 * (m + 1), st));
+    coo_keys_kernel<<<grid1(nt), 256, 0, st>>>(nt, n, rows, cols, key, idx);
+    SVDSB_LAUNCHED();
+    int nbits = bits_for(std::max<int64_t>(m * n, 2));
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key_s, idx, perm, (int)nt, 0, nbits, st);
+    void *tmp = nullptr;
+    SVDSB_CUDA(cudaMalloc(&tmp, tb));
+    SVDSB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key_s, idx, perm, (int)nt, 0, nbits, st));
+    bump_launches();
+    coo_first_kernel<<<grid1(nt), 256, 0, st>>>(nt, key_s, first);
+    SVDSB_LAUNCHED();
+    size_t sb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, sb, first, seg, (int)nt, st);
+    void *stmp = nullptr;
+    SVDSB_CUDA(cudaMalloc(&stmp, sb));
+    SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(stmp, sb, first, seg, (int)nt, st));
+    bump_launches();
+    int last_seg = 0, last_first = 0;
+    SVDSB_CUDA(cudaMemcpyAsync(&last_seg, seg + nt - 1, 4, cudaMemcpyDeviceToHost, st));
+    SVDSB_CUDA(cudaMemcpyAsync(&last_first, first + nt - 1, 4, cudaMemcpyDeviceToHost, st));
+    SVDSB_CUDA(cudaStreamSynchronize(st));
+    nnz = (int64_t)last_seg + last_first;
+    SVDSB_CUDA(cudaMalloc(&p.col, 4 * nnz));
+    SVDSB_CUDA(cudaMalloc(&p.val, 8 * nnz));
+    coo_sum_kernel<<<grid1(nt), 256, 0, st>>>(nt, n, key_s, perm, first, seg, vals, p.col, p.val, rowcnt);
+    SVDSB_LAUNCHED();
+    size_t sb2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, sb2, rowcnt, p.row_ptr, (int)(m + 1), st);
+    void *stmp2 = nullptr;
+    SVDSB_CUDA(cudaMalloc(&stmp2, sb2));
+    SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(stmp2, sb2, rowcnt, p.row_ptr, (int)(m + 1), st));
+    bump_launches();
+    SVDSB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(key);
+    cudaFree(key_s);
+    cudaFree(idx);
+    cudaFree(perm);
+    cudaFree(first);
+    cudaFree(seg);
+    cudaFree(rowcnt);
+    cudaFree(tmp);
+    cudaFree(stmp);
+    cudaFree(stmp2);
+  } else {
+    SVDSB_CUDA(cudaMalloc(&p.col, 4));
+    SVDSB_CUDA(cudaMalloc(&p.val, 8));
+  }
+  p.nnz = nnz;
+  p.host_row_ptr.resize(m + 1);
+  SVDSB_CUDA(cudaMemcpyAsync(p.host_row_ptr.data(), p.row_ptr, 4 * (m + 1), cudaMemcpyDeviceToHost, st));
+  SVDSB_CUDA(cudaStreamSynchronize(st));
+  int rc = finish_create(h, flags, st);
+  if (rc) {
+    svdsb_csr_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return SVDSB_OK;
+}
+
+int svdsb_csr_export_host(const svdsb_csr *a, int transpose, int64_t *row_ptr_host, int64_t *col_idx_host,
+                          double *values_host) {
+  SVDSB_CHECK_ARG(a != nullptr, "NULL handle");
+  SVDSB_CHECK_ARG(!transpose || a->has_t, "transpose was not built");
+  const CsrPart &p = transpose ? a->at : a->a;
+  std::vector<int> rp(p.rows + 1), ci(p.nnz);
+  SVDSB_CUDA(cudaMemcpy(rp.data(), p.row_ptr, 4 * (p.rows + 1), cudaMemcpyDeviceToHost));
+  if (p.nnz) {
+    SVDSB_CUDA(cudaMemcpy(ci.data(), p.col, 4 * p.nnz, cudaMemcpyDeviceToHost));
+    SVDSB_CUDA(cudaMemcpy(values_host, p.val, 8 * p.nnz, cudaMemcpyDeviceToHost));
+  }
+  for (int64_t i = 0; i <= p.rows; ++i) row_ptr_host[i] = rp[i];
+  for (int64_t k = 0; k < p.nnz; ++k) col_idx_host[k] = ci[k];
+  return SVDSB_OK;
+}
+
+int svdsb_csr_device_arrays(const svdsb_csr *a, int transpose, const int **row_ptr, const int **col,
+                            const double **val) {
+  SVDSB_CHECK_ARG(a != nullptr, "NULL handle");
+  SVDSB_CHECK_ARG(!transpose || a->has_t, "transpose was not built");
+  const CsrPart &p = transpose ? a->at : a->a;
+  if (row_ptr) *row_ptr = p.row_ptr;
+  if (col) *col = p.col;
+  if (val) *val = p.val;
+  return SVDSB_OK;
+}
+
+int svdsb_matvec(svdsb_ctx *ctx, const svdsb_csr *a, int transpose, const double *x, int64_t ldx, double *y,
+                 int64_t ldy, int block, void *stream) {
+  (void)ctx;
+  SVDSB_CHECK_ARG(a != nullptr, "svdsb_matvec: NULL handle");
+  SVDSB_CHECK_ARG(block >= 0, "svdsb_matvec: negative block");
+  if (block == 0) return SVDSB_OK;
+  cudaStream_t st = as_stream(stream);
+  if (!transpose) {
+    SVDSB_CHECK_ARG(ldx >= a->a.cols && ldy >= a->a.rows, "svdsb_matvec: leading dimension too small");
+    return part_matvec<0>(a->a, x, ldx, y, ldy, block, st);
+  }
+  SVDSB_CHECK_ARG(a->has_t, "svdsb_matvec: transpose requested but CSR(A^T) was not built");
+  SVDSB_CHECK_ARG(ldx >= a->at.cols && ldy >= a->at.rows, "svdsb_matvec: leading dimension too small");
+  return part_matvec<1>(a->at, x, ldx, y, ldy, block, st);
+}
+
+int svdsb_apply_normal(svdsb_ctx *ctx, const svdsb_csr *a, int side, const double *x, int64_t ldx, double *y,
+                       int64_t ldy, int block, double *tmp, int64_t ldtmp, void *stream) {
+  int rc;
+  if (side == 0) {
+    if ((rc = svdsb_matvec(ctx, a, 0, x, ldx, tmp, ldtmp, block, stream))) return rc;
+    return svdsb_matvec(ctx, a, 1, tmp, ldtmp, y, ldy, block, stream);
+  }
+  if ((rc = svdsb_matvec(ctx, a, 1, x, ldx, tmp, ldtmp, block, stream))) return rc;
+  return svdsb_matvec(ctx, a, 0, tmp, ldtmp, y, ldy, block, stream);
+}
+
+int svdsb_apply_augmented(svdsb_ctx *ctx, const svdsb_csr *a, const double *x, int64_t ldx, double *y,
+                          int64_t ldy, int block, void *stream) {
+  SVDSB_CHECK_ARG(a != nullptr, "NULL handle");
+  const int64_t n = a->a.cols;
+  int rc;
+  // y[:n] = A^T x[n:] ; y[n:] = A x[:n]
+  if ((rc = svdsb_matvec(ctx, a, 1, x + n, ldx, y, ldy, block, stream))) return rc;
+  return svdsb_matvec(ctx, a, 0, x, ldx, y + n, ldy, block, stream);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- precond
+
+namespace svdsb {
+
+// d[r] = sum over row r of v*v, left to right (np.bincount order over the
+// rows of the chosen orientation).
+__global__ void row_sq_kernel(int64_t rows, const int *__restrict__ rp, const double *__restrict__ val,
+                              double *__restrict__ d) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double s = 0.0;
+  for (int k = rp[r]; k < rp[r + 1]; ++k) {
+    double v = val[k];
+    s = __dadd_rn(s, __dmul_rn(v, v));
+  }
+  d[r] = s;
+}
+
+__global__ void max_kernel(int64_t n, const double *__restrict__ d, double *__restrict__ out,
+                           unsigned int *ticket, double *partials) {
+  __shared__ double red[8];
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, d[i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mm = fmax(mm, red[w]);
+    partials[blockIdx.x] = mm;
+  }
+  if (last_cta(ticket) && threadIdx.x == 0) {
+    double mm = partials[0];
+    for (unsigned b = 1; b < gridDim.x; ++b) mm = fmax(mm, partials[b]);
+    *out = mm;
+  }
+}
+
+__global__ void clamp_kernel(int64_t n, double *__restrict__ d, const double *__restrict__ mx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double f = __dmul_rn(kEps, *mx);
+  d[i] = fmax(d[i], f);
+}
+
+__global__ void diag_solve_kernel(int64_t dim, int b, const double *__restrict__ d, const double *x, int64_t ldx,
+                                  double *y, int64_t ldy) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= dim) return;
+  double di = d[i];
+  for (int c = 0; c < b; ++c) y[i + c * ldy] = __ddiv_rn(x[i + c * ldx], di);
+}
+
+}  // namespace svdsb
+
+extern "C" {
+
+int svdsb_precond_diag(svdsb_ctx *ctx, const svdsb_csr *a, int side, double *d, void *stream) {
+  SVDSB_CHECK_ARG(ctx && a && d, "svdsb_precond_diag: NULL argument");
+  SVDSB_CHECK_ARG(side == 0 || side == 1, "side must be 0 (cols) or 1 (rows)");
+  SVDSB_CHECK_ARG(a->a.nnz > 0, "empty matrix has no usable diagonal");
+  const CsrPart *p;
+  if (side == 0) {
+    SVDSB_CHECK_ARG(a->has_t, "column norms need CSR(A^T)");
+    p = &a->at;
+  } else {
+    p = &a->a;
+  }
+  cudaStream_t st = as_stream(stream);
+  row_sq_kernel<<<grid1(p->rows), 256, 0, st>>>(p->rows, p->row_ptr, p->val, d);
+  SVDSB_LAUNCHED();
+  int g = (int)std::min<int64_t>(grid1(p->rows), 2 * kNumSMs);
+  double *mx = ctx->partials + kMaxPartials - 1;
+  max_kernel<<<g, 256, 0, st>>>(p->rows, d, mx, take_ticket(ctx), ctx->partials);
+  SVDSB_LAUNCHED();
+  clamp_kernel<<<grid1(p->rows), 256, 0, st>>>(p->rows, d, mx);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+int svdsb_diag_solve(int64_t dim, const double *d, const double *x, int64_t ldx, double *y, int64_t ldy, int block,
+                     void *stream) {
+  if (dim == 0 || block == 0) return SVDSB_OK;
+  diag_solve_kernel<<<grid1(dim), 256, 0, as_stream(stream)>>>(dim, block, d, x, ldx, y, ldy);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+}  // extern "C"

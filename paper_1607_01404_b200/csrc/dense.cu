@@ -1,0 +1,611 @@
+// Tall-skinny fp64 kernels for the Davidson basis (HBM-bound streaming).
+//
+// All operands are column-major with an explicit leading dimension.  Every
+// kernel streams rows: CTA `bx` owns a contiguous row range, each thread
+// walks rows `tid, tid+256, ...` of it and touches all the columns it needs
+// for that row (coalesced 256-byte warp accesses per column).  Reductions
+// (Gram entries, norms) are two-level: warp shuffle + CTA fold into a
+// per-CTA partial, then the last CTA to finish (ticket) folds the partials
+// in CTA order.  The grid depends only on the row count, so results are
+// bit-reproducible run to run.
+//
+// Reference operations (pkg/src/itersvd): kernels.py:47-51 (_project_out),
+// :104-111 (norms), :497-499 (qr_append projection), eigensolver.py:349-352
+// (V^T W), :385-394 (_candidates), :526-527 (restart V @ coefs),
+// :690 (H column), hybrid.py:226-241 (stage-2 split residual).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace svdsb {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxCtas = 4 * kNumSMs;
+constexpr int kMinRowsPerCta = 1024;
+
+struct ColSet {
+  const double *base[SVDSB_MAX_BLOCKS];
+  int64_t ld[SVDSB_MAX_BLOCKS];
+  int cols[SVDSB_MAX_BLOCKS];
+  int nblk;
+  int total;
+};
+
+__device__ __forceinline__ const double *colset_ptr(const ColSet &s, int i) {
+  int k = 0;
+  while (k < s.nblk - 1 && i >= s.cols[k]) {
+    i -= s.cols[k];
+    ++k;
+  }
+  return s.base[k] + (int64_t)i * s.ld[k];
+}
+
+struct RowRange {
+  int64_t r0, r1;
+};
+
+__device__ __forceinline__ RowRange cta_rows(int64_t dim) {
+  int64_t per = (dim + gridDim.x - 1) / gridDim.x;
+  int64_t r0 = (int64_t)blockIdx.x * per;
+  int64_t r1 = min(dim, r0 + per);
+  return {r0, r1};
+}
+
+// Fold NACC per-thread accumulators over the CTA into part[0..nvalid).
+template <int NACC>
+__device__ __forceinline__ void cta_fold(double (&acc)[NACC], int nvalid, double *part) {
+  __shared__ double red[kWarps][NACC];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) {
+    double v = warp_sum(acc[k]);
+    if (lane == 0) red[w][k] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nvalid; k += kThreads) {
+    double s = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) s += red[ww][k];
+    part[k] = s;
+  }
+}
+
+static inline int grid_rows(int64_t dim) { return stream_grid(dim, kMinRowsPerCta, kMaxCtas); }
+
+// ------------------------------------------------------------------ gram
+
+template <int AT, int BT>
+__global__ void __launch_bounds__(kThreads)
+gram_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t ldy, int b, double *c, int64_t ldc,
+            double *norms2, double *partials, unsigned int *ticket) {
+  __shared__ const double *xp[AT];
+  const int ty = blockIdx.y, tz = blockIdx.z;
+  const int i0 = ty * AT, j0 = tz * BT;
+  const int na = min(AT, xs.total - i0), nb = min(BT, b - j0);
+  const bool want_norm = (norms2 != nullptr) && ty == 0;
+  if (threadIdx.x < AT && (int)threadIdx.x < na) xp[threadIdx.x] = colset_ptr(xs, i0 + threadIdx.x);
+  __syncthreads();
+  double acc[AT * BT + BT];
+#pragma unroll
+  for (int k = 0; k < AT * BT + BT; ++k) acc[k] = 0.0;
+  RowRange rr = cta_rows(dim);
+  for (int64_t r = rr.r0 + threadIdx.x; r < rr.r1; r += kThreads) {
+    double yv[BT];
+#pragma unroll
+    for (int j = 0; j < BT; ++j) yv[j] = (j < nb) ? __ldg(y + r + (int64_t)(j0 + j) * ldy) : 0.0;
+#pragma unroll
+    for (int i = 0; i < AT; ++i) {
+      if (i < na) {
+        double xv = __ldg(xp[i] + r);
+#pragma unroll
+        for (int j = 0; j < BT; ++j) acc[i * BT + j] = fma(xv, yv[j], acc[i * BT + j]);
+      }
+    }
+    if (want_norm) {
+#pragma unroll
+      for (int j = 0; j < BT; ++j) acc[AT * BT + j] = fma(yv[j], yv[j], acc[AT * BT + j]);
+    }
+  }
+  constexpr int NOUT = AT * BT + BT;
+  const int tile = ty * gridDim.z + tz;
+  double *part = partials + ((int64_t)tile * gridDim.x + blockIdx.x) * NOUT;
+  cta_fold<NOUT>(acc, NOUT, part);
+  if (!last_cta(ticket)) return;
+  const int ntile = gridDim.y * gridDim.z;
+  for (int o = threadIdx.x; o < ntile * NOUT; o += kThreads) {
+    const int t = o / NOUT, k = o % NOUT;
+    const int tyy = t / gridDim.z, tzz = t % gridDim.z;
+    double s = 0.0;
+    const double *pp = partials + (int64_t)t * gridDim.x * NOUT + k;
+    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * NOUT];
+    if (k < AT * BT) {
+      int i = tyy * AT + k / BT, j = tzz * BT + k % BT;
+      if (i < xs.total && j < b) c[i + (int64_t)j * ldc] = s;
+    } else if (norms2 != nullptr && tyy == 0) {
+      int j = tzz * BT + (k - AT * BT);
+      if (j < b) norms2[j] = s;
+    }
+  }
+}
+
+// ------------------------------------------------------------ project out
+
+template <int BT>
+__global__ void __launch_bounds__(kThreads)
+project_kernel(int64_t dim, ColSet xs, const double *__restrict__ cmat, int64_t ldc, double *y, int64_t ldy,
+               int b, double *norms2, double *partials, unsigned int *ticket) {
+  extern __shared__ double csh[];  // total x BT
+  __shared__ const double *xp[256];
+  const int na = xs.total;
+  for (int i = threadIdx.x; i < na; i += kThreads) xp[i] = colset_ptr(xs, i);
+  for (int k = threadIdx.x; k < na * BT; k += kThreads) {
+    int i = k / BT, j = k % BT;
+    csh[k] = (j < b) ? cmat[i + (int64_t)j * ldc] : 0.0;
+  }
+  __syncthreads();
+  double nacc[BT];
+#pragma unroll
+  for (int j = 0; j < BT; ++j) nacc[j] = 0.0;
+  RowRange rr = cta_rows(dim);
+  for (int64_t r = rr.r0 + threadIdx.x; r < rr.r1; r += kThreads) {
+    double yv[BT];
+#pragma unroll
+    for (int j = 0; j < BT; ++j) yv[j] = (j < b) ? y[r + (int64_t)j * ldy] : 0.0;
+    for (int i = 0; i < na; ++i) {
+      double xv = __ldg(xp[i] + r);
+#pragma unroll
+      for (int j = 0; j < BT; ++j) yv[j] = fma(-xv, csh[i * BT + j], yv[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < BT; ++j) {
+      if (j < b) {
+        y[r + (int64_t)j * ldy] = yv[j];
+        nacc[j] = fma(yv[j], yv[j], nacc[j]);
+      }
+    }
+  }
+  if (norms2 == nullptr) return;
+  double *part = partials + (int64_t)blockIdx.x * BT;
+  cta_fold<BT>(nacc, BT, part);
+  if (!last_cta(ticket)) return;
+  for (int j = threadIdx.x; j < b; j += kThreads) {
+    double s = 0.0;
+    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += partials[(int64_t)bx * BT + j];
+    norms2[j] = s;
+  }
+}
+
+// ---------------------------------------------------------------- ts_gemm
+
+template <int ST>
+__global__ void __launch_bounds__(kThreads)
+ts_gemm_kernel(int64_t dim, const double *__restrict__ x, int64_t ldx, int g, const double *__restrict__ cmat,
+               int64_t ldc, int s, double alpha, double beta, double *__restrict__ y, int64_t ldy) {
+  extern __shared__ double csh[];  // g x ST (row i: csh[i*ST + j])
+  const int j0 = blockIdx.y * ST;
+  const int ns = min(ST, s - j0);
+  for (int k = threadIdx.x; k < g * ST; k += kThreads) {
+    int i = k / ST, j = k % ST;
+    csh[k] = (j < ns) ? cmat[i + (int64_t)(j0 + j) * ldc] : 0.0;
+  }
+  __syncthreads();
+  RowRange rr = cta_rows(dim);
+  for (int64_t r = rr.r0 + threadIdx.x; r < rr.r1; r += kThreads) {
+    double acc[ST];
+#pragma unroll
+    for (int j = 0; j < ST; ++j) acc[j] = 0.0;
+    for (int i = 0; i < g; ++i) {
+      double xv = __ldg(x + r + (int64_t)i * ldx);
+#pragma unroll
+      for (int j = 0; j < ST; ++j) acc[j] = fma(xv, csh[i * ST + j], acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < ST; ++j) {
+      if (j < ns) {
+        double *yp = y + r + (int64_t)(j0 + j) * ldy;
+        double out = alpha * acc[j];
+        if (beta != 0.0) out = fma(beta, *yp, out);
+        *yp = out;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------- ritz residual
+
+template <int PT>
+__global__ void __launch_bounds__(kThreads)
+ritz_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const double *__restrict__ w, int64_t ldw,
+            int g, const double *__restrict__ yc, int64_t ldyc, const double *__restrict__ lam, int p,
+            double *__restrict__ r, int64_t ldr, double *__restrict__ xo, int64_t ldx, double *__restrict__ oxo,
+            int64_t ldox, double *rn2, double *partials, unsigned int *ticket) {
+  extern __shared__ double ysh[];  // g x PT
+  __shared__ double lsh[PT];
+  const int j0 = blockIdx.y * PT;
+  const int np = min(PT, p - j0);
+  for (int k = threadIdx.x; k < g * PT; k += kThreads) {
+    int i = k / PT, j = k % PT;
+    ysh[k] = (j < np) ? yc[i + (int64_t)(j0 + j) * ldyc] : 0.0;
+  }
+  if (threadIdx.x < PT) lsh[threadIdx.x] = ((int)threadIdx.x < np) ? lam[j0 + threadIdx.x] : 0.0;
+  __syncthreads();
+  double nacc[PT];
+#pragma unroll
+  for (int j = 0; j < PT; ++j) nacc[j] = 0.0;
+  RowRange rr = cta_rows(dim);
+  for (int64_t row = rr.r0 + threadIdx.x; row < rr.r1; row += kThreads) {
+    double ax[PT], aw[PT];
+#pragma unroll
+    for (int j = 0; j < PT; ++j) {
+      ax[j] = 0.0;
+      aw[j] = 0.0;
+    }
+    for (int i = 0; i < g; ++i) {
+      double vv = __ldg(v + row + (int64_t)i * ldv);
+      double ww = __ldg(w + row + (int64_t)i * ldw);
+#pragma unroll
+      for (int j = 0; j < PT; ++j) {
+        double cf = ysh[i * PT + j];
+        ax[j] = fma(vv, cf, ax[j]);
+        aw[j] = fma(ww, cf, aw[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PT; ++j) {
+      if (j < np) {
+        double res = aw[j] - ax[j] * lsh[j];
+        r[row + (int64_t)(j0 + j) * ldr] = res;
+        if (xo) xo[row + (int64_t)(j0 + j) * ldx] = ax[j];
+        if (oxo) oxo[row + (int64_t)(j0 + j) * ldox] = aw[j];
+        nacc[j] = fma(res, res, nacc[j]);
+      }
+    }
+  }
+  double *part = partials + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * PT;
+  cta_fold<PT>(nacc, PT, part);
+  if (!last_cta(ticket)) return;
+  for (int o = threadIdx.x; o < (int)gridDim.y * PT; o += kThreads) {
+    int ty = o / PT, j = o % PT;
+    if (ty * PT + j >= p) continue;
+    double s = 0.0;
+    const double *pp = partials + (int64_t)ty * gridDim.x * PT + j;
+    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * PT];
+    rn2[ty * PT + j] = s;
+  }
+}
+
+// -------------------------------------------------------- norms and dots
+
+template <int BT>
+__global__ void __launch_bounds__(kThreads)
+coldot_kernel(int64_t dim, const double *__restrict__ x, int64_t ldx, const double *__restrict__ y, int64_t ldy,
+              int b, double *out, double *partials, unsigned int *ticket) {
+  const int j0 = blockIdx.y * BT;
+  const int nb = min(BT, b - j0);
+  double acc[BT];
+#pragma unroll
+  for (int j = 0; j < BT; ++j) acc[j] = 0.0;
+  RowRange rr = cta_rows(dim);
+  for (int64_t r = rr.r0 + threadIdx.x; r < rr.r1; r += kThreads) {
+#pragma unroll
+    for (int j = 0; j < BT; ++j)
+      if (j < nb) acc[j] = fma(__ldg(x + r + (int64_t)(j0 + j) * ldx), __ldg(y + r + (int64_t)(j0 + j) * ldy), acc[j]);
+  }
+  double *part = partials + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * BT;
+  cta_fold<BT>(acc, BT, part);
+  if (!last_cta(ticket)) return;
+  for (int o = threadIdx.x; o < (int)gridDim.y * BT; o += kThreads) {
+    int ty = o / BT, j = o % BT;
+    if (ty * BT + j >= b) continue;
+    double s = 0.0;
+    const double *pp = partials + (int64_t)ty * gridDim.x * BT + j;
+    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * BT];
+    out[ty * BT + j] = s;
+  }
+}
+
+template <int BT>
+__global__ void __launch_bounds__(kThreads)
+split_kernel(int64_t dim, int64_t nsplit, const double *__restrict__ r, int64_t ldr, const double *__restrict__ x,
+             int64_t ldx, int b, double *out, double *partials, unsigned int *ticket) {
+  const int j0 = blockIdx.y * BT;
+  const int nb = min(BT, b - j0);
+  double acc[6 * BT];
+#pragma unroll
+  for (int k = 0; k < 6 * BT; ++k) acc[k] = 0.0;
+  RowRange rr = cta_rows(dim);
+  for (int64_t row = rr.r0 + threadIdx.x; row < rr.r1; row += kThreads) {
+    const int off = (row < nsplit) ? 0 : 3;
+#pragma unroll
+    for (int j = 0; j < BT; ++j) {
+      if (j < nb) {
+        double rv = __ldg(r + row + (int64_t)(j0 + j) * ldr);
+        double xv = __ldg(x + row + (int64_t)(j0 + j) * ldx);
+        acc[6 * j + off + 0] = fma(rv, rv, acc[6 * j + off + 0]);
+        acc[6 * j + off + 1] = fma(rv, xv, acc[6 * j + off + 1]);
+        acc[6 * j + off + 2] = fma(xv, xv, acc[6 * j + off + 2]);
+      }
+    }
+  }
+  double *part = partials + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 6 * BT;
+  cta_fold<6 * BT>(acc, 6 * BT, part);
+  if (!last_cta(ticket)) return;
+  for (int o = threadIdx.x; o < (int)gridDim.y * 6 * BT; o += kThreads) {
+    int ty = o / (6 * BT), k = o % (6 * BT);
+    if (ty * BT + k / 6 >= b) continue;
+    double s = 0.0;
+    const double *pp = partials + (int64_t)ty * gridDim.x * 6 * BT + k;
+    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * 6 * BT];
+    out[ty * 6 * BT + k] = s;
+  }
+}
+
+template <int BT>
+__global__ void __launch_bounds__(kThreads)
+split_res_kernel(int64_t dim, int64_t nsplit, const double *__restrict__ r, int64_t ldr, const double *__restrict__ x,
+                 int64_t ldx, int b, const double *__restrict__ lam, const double *__restrict__ stats, double *out,
+                 double *partials, unsigned int *ticket) {
+  const int j0 = blockIdx.y * BT;
+  const int nb = min(BT, b - j0);
+  __shared__ double coef[BT][4];  // 1/nv, alpha, 1/nu, beta
+  if (threadIdx.x < BT) {
+    int j = threadIdx.x;
+    if (j < nb) {
+      const double *st = stats + 6 * (j0 + j);
+      double nv = sqrt(st[2]), nu = sqrt(st[5]);
+      double l = lam[j0 + j], sg = fabs(l);
+      bool ok = nv > 0.0 && nu > 0.0;
+      coef[j][0] = ok ? 1.0 / nv : 0.0;
+      coef[j][1] = ok ? (l / nv - sg / nu) : 0.0;
+      coef[j][2] = ok ? 1.0 / nu : 0.0;
+      coef[j][3] = ok ? (l / nu - sg / nv) : 0.0;
+    }
+  }
+  __syncthreads();
+  double acc[BT];
+#pragma unroll
+  for (int j = 0; j < BT; ++j) acc[j] = 0.0;
+  RowRange rr = cta_rows(dim);
+  for (int64_t row = rr.r0 + threadIdx.x; row < rr.r1; row += kThreads) {
+    const bool is_v = row < nsplit;
+#pragma unroll
+    for (int j = 0; j < BT; ++j) {
+      if (j < nb) {
+        double rv = __ldg(r + row + (int64_t)(j0 + j) * ldr);
+        double xv = __ldg(x + row + (int64_t)(j0 + j) * ldx);
+        // rows of the v part contribute to e2 = r_v/nu + beta x_v,
+        // rows of the u part to e1 = r_u/nv + alpha x_u
+        double e = is_v ? fma(coef[j][3], xv, rv * coef[j][2]) : fma(coef[j][1], xv, rv * coef[j][0]);
+        acc[j] = fma(e, e, acc[j]);
+      }
+    }
+  }
+  double *part = partials + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * BT;
+  cta_fold<BT>(acc, BT, part);
+  if (!last_cta(ticket)) return;
+  for (int o = threadIdx.x; o < (int)gridDim.y * BT; o += kThreads) {
+    int ty = o / BT, j = o % BT;
+    int jj = ty * BT + j;
+    if (jj >= b) continue;
+    double s = 0.0;
+    const double *pp = partials + (int64_t)ty * gridDim.x * BT + j;
+    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * BT];
+    const double *st = stats + 6 * jj;
+    out[jj] = (st[2] > 0.0 && st[5] > 0.0) ? s : __longlong_as_double(0x7ff0000000000000LL);
+  }
+}
+
+__global__ void scale_kernel(int64_t dim, const double *x, int64_t ldx, int b, const double *__restrict__ s, int mode,
+                             double *y, int64_t ldy) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= dim) return;
+  for (int j = 0; j < b; ++j) {
+    double f = s[j];
+    double xv = x[i + (int64_t)j * ldx];
+    double out;
+    if (mode == 0) {
+      out = xv * f;
+    } else {
+      if (f == 0.0) {
+        out = xv;
+      } else {
+        double d = (mode == 2) ? sqrt(f) : f;
+        out = xv / d;
+      }
+    }
+    y[i + (int64_t)j * ldy] = out;
+  }
+}
+
+__global__ void axpby_kernel(int64_t dim, int b, double alpha, const double *x, int64_t ldx, double beta, double *y,
+                             int64_t ldy) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= dim) return;
+  for (int j = 0; j < b; ++j) {
+    double *yp = y + i + (int64_t)j * ldy;
+    double out = alpha * x[i + (int64_t)j * ldx];
+    if (beta != 0.0) out = fma(beta, *yp, out);
+    *yp = out;
+  }
+}
+
+static int make_colset(ColSet &s, int nblk, const double *const *xs, const int64_t *ldxs, const int *cols) {
+  SVDSB_CHECK_ARG(nblk >= 1 && nblk <= SVDSB_MAX_BLOCKS, "between 1 and SVDSB_MAX_BLOCKS column blocks");
+  s.nblk = 0;
+  s.total = 0;
+  for (int k = 0; k < nblk; ++k) {
+    if (cols[k] <= 0) continue;
+    s.base[s.nblk] = xs[k];
+    s.ld[s.nblk] = ldxs[k];
+    s.cols[s.nblk] = cols[k];
+    s.total += cols[k];
+    s.nblk++;
+  }
+  if (s.nblk == 0) {
+    s.base[0] = nullptr;
+    s.ld[0] = 1;
+    s.cols[0] = 0;
+    s.nblk = 1;
+  }
+  return SVDSB_OK;
+}
+
+}  // namespace svdsb
+
+using namespace svdsb;
+
+extern "C" {
+
+int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs, const int *cols,
+               const double *y, int64_t ldy, int b, double *c, int64_t ldc, double *norms2, void *stream) {
+  SVDSB_CHECK_ARG(ctx != nullptr, "svdsb_gram: NULL ctx");
+  ColSet s;
+  int rc = make_colset(s, nblk, xs, ldxs, cols);
+  if (rc) return rc;
+  if (b <= 0) return SVDSB_OK;
+  SVDSB_CHECK_ARG(s.total <= 4 * SVDSB_SMALL_MAX, "svdsb_gram: too many columns");
+  cudaStream_t st = as_stream(stream);
+  const int gx = grid_rows(dim);
+  if (s.total == 0) {
+    if (norms2) return svdsb_col_norms2(ctx, dim, y, ldy, b, norms2, stream);
+    return SVDSB_OK;
+  }
+  if (b == 1) {
+    constexpr int AT = 32, BT = 1;
+    dim3 grid(gx, (s.total + AT - 1) / AT, 1);
+    SVDSB_CHECK_ARG((int64_t)grid.x * grid.y * (AT * BT + BT) <= kMaxPartials, "gram: workspace too small");
+    gram_kernel<AT, BT><<<grid, kThreads, 0, st>>>(dim, s, y, ldy, b, c, ldc, norms2, ctx->partials,
+                                                   take_ticket(ctx));
+  } else {
+    constexpr int AT = 16, BT = 4;
+    dim3 grid(gx, (s.total + AT - 1) / AT, (b + BT - 1) / BT);
+    SVDSB_CHECK_ARG((int64_t)grid.x * grid.y * grid.z * (AT * BT + BT) <= kMaxPartials, "gram: workspace too small");
+    gram_kernel<AT, BT><<<grid, kThreads, 0, st>>>(dim, s, y, ldy, b, c, ldc, norms2, ctx->partials,
+                                                   take_ticket(ctx));
+  }
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+int svdsb_project_out(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs,
+                      const int *cols, const double *c, int64_t ldc, double *y, int64_t ldy, int b, double *norms2,
+                      void *stream) {
+  SVDSB_CHECK_ARG(ctx != nullptr, "svdsb_project_out: NULL ctx");
+  ColSet s;
+  int rc = make_colset(s, nblk, xs, ldxs, cols);
+  if (rc) return rc;
+  if (b <= 0) return SVDSB_OK;
+  SVDSB_CHECK_ARG(s.total <= 256, "svdsb_project_out: at most 256 columns");
+  cudaStream_t st = as_stream(stream);
+  for (int j0 = 0; j0 < b; j0 += 8) {
+    int bb = std::min(8, b - j0);
+    const int gx = grid_rows(dim);
+    double *yy = y + (int64_t)j0 * ldy;
+    const double *cc = c + (int64_t)j0 * ldc;
+    double *nn = norms2 ? norms2 + j0 : nullptr;
+    if (bb == 1) {
+      size_t sh = sizeof(double) * std::max(s.total, 1) * 1;
+      project_kernel<1><<<gx, kThreads, sh, st>>>(dim, s, cc, ldc, yy, ldy, bb, nn, ctx->partials, take_ticket(ctx));
+    } else {
+      size_t sh = sizeof(double) * std::max(s.total, 1) * 8;
+      project_kernel<8><<<gx, kThreads, sh, st>>>(dim, s, cc, ldc, yy, ldy, bb, nn, ctx->partials, take_ticket(ctx));
+    }
+    SVDSB_LAUNCHED();
+  }
+  return SVDSB_OK;
+}
+
+int svdsb_ts_gemm(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx, int g, const double *c, int64_t ldc,
+                  int s, double alpha, double beta, double *y, int64_t ldy, void *stream) {
+  (void)ctx;
+  if (s <= 0 || dim == 0) return SVDSB_OK;
+  SVDSB_CHECK_ARG(g >= 0 && g <= 256, "svdsb_ts_gemm: g out of range");
+  cudaStream_t st = as_stream(stream);
+  if (g == 0) {
+    // Y = beta Y
+    return svdsb_axpby(dim, s, 0.0, y, ldy, beta, y, ldy, stream);
+  }
+  constexpr int ST = 16;
+  dim3 grid(grid_rows(dim), (s + ST - 1) / ST);
+  size_t sh = sizeof(double) * g * ST;
+  ts_gemm_kernel<ST><<<grid, kThreads, sh, st>>>(dim, x, ldx, g, c, ldc, s, alpha, beta, y, ldy);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+int svdsb_ritz_residual(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const double *w, int64_t ldw,
+                        int g, const double *yc, int64_t ldyc, const double *lam, int p, double *r, int64_t ldr,
+                        double *x, int64_t ldx, double *ox, int64_t ldox, double *rn2, void *stream) {
+  SVDSB_CHECK_ARG(ctx != nullptr, "svdsb_ritz_residual: NULL ctx");
+  if (p <= 0) return SVDSB_OK;
+  SVDSB_CHECK_ARG(g >= 1 && g <= 256, "svdsb_ritz_residual: g out of range");
+  cudaStream_t st = as_stream(stream);
+  constexpr int PT = 12;
+  dim3 grid(grid_rows(dim), (p + PT - 1) / PT);
+  size_t sh = sizeof(double) * g * PT;
+  ritz_kernel<PT><<<grid, kThreads, sh, st>>>(dim, v, ldv, w, ldw, g, yc, ldyc, lam, p, r, ldr, x, ldx, ox, ldox, rn2,
+                                              ctx->partials, take_ticket(ctx));
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+int svdsb_col_norms2(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx, int b, double *out, void *stream) {
+  return svdsb_col_dots(ctx, dim, x, ldx, x, ldx, b, out, stream);
+}
+
+int svdsb_col_dots(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx, const double *y, int64_t ldy, int b,
+                   double *out, void *stream) {
+  SVDSB_CHECK_ARG(ctx != nullptr, "svdsb_col_dots: NULL ctx");
+  if (b <= 0) return SVDSB_OK;
+  constexpr int BT = 8;
+  dim3 grid(grid_rows(dim), (b + BT - 1) / BT);
+  coldot_kernel<BT><<<grid, kThreads, 0, as_stream(stream)>>>(dim, x, ldx, y, ldy, b, out, ctx->partials,
+                                                              take_ticket(ctx));
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+int svdsb_split_stats(svdsb_ctx *ctx, int64_t dim, int64_t nsplit, const double *r, int64_t ldr, const double *x,
+                      int64_t ldx, int b, double *out, void *stream) {
+  SVDSB_CHECK_ARG(ctx != nullptr, "svdsb_split_stats: NULL ctx");
+  if (b <= 0) return SVDSB_OK;
+  constexpr int BT = 4;
+  dim3 grid(grid_rows(dim), (b + BT - 1) / BT);
+  split_kernel<BT><<<grid, kThreads, 0, as_stream(stream)>>>(dim, nsplit, r, ldr, x, ldx, b, out, ctx->partials,
+                                                             take_ticket(ctx));
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+int svdsb_split_residual(svdsb_ctx *ctx, int64_t dim, int64_t nsplit, const double *r, int64_t ldr,
+                         const double *x, int64_t ldx, int b, const double *lam, const double *stats, double *out,
+                         void *stream) {
+  SVDSB_CHECK_ARG(ctx != nullptr, "svdsb_split_residual: NULL ctx");
+  if (b <= 0) return SVDSB_OK;
+  constexpr int BT = 4;
+  dim3 grid(grid_rows(dim), (b + BT - 1) / BT);
+  split_res_kernel<BT><<<grid, kThreads, 0, as_stream(stream)>>>(dim, nsplit, r, ldr, x, ldx, b, lam, stats, out,
+                                                                 ctx->partials, take_ticket(ctx));
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+int svdsb_scale_cols(int64_t dim, const double *x, int64_t ldx, int b, const double *s, int mode, double *y,
+                     int64_t ldy, void *stream) {
+  if (dim == 0 || b <= 0) return SVDSB_OK;
+  SVDSB_CHECK_ARG(mode >= 0 && mode <= 2, "svdsb_scale_cols: bad mode");
+  scale_kernel<<<(unsigned)((dim + 255) / 256), 256, 0, as_stream(stream)>>>(dim, x, ldx, b, s, mode, y, ldy);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+int svdsb_axpby(int64_t dim, int b, double alpha, const double *x, int64_t ldx, double beta, double *y, int64_t ldy,
+                void *stream) {
+  if (dim == 0 || b <= 0) return SVDSB_OK;
+  axpby_kernel<<<(unsigned)((dim + 255) / 256), 256, 0, as_stream(stream)>>>(dim, b, alpha, x, ldx, beta, y, ldy);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// Library plumbing: error strings, launch counter, context (workspace).
+#include <stdarg.h>
+#include <atomic>
+
+#include "common.cuh"
+
+namespace svdsb {
+
+static thread_local char g_err[1024] = "";
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int64_t bump_launches(int n) { return g_launches.fetch_add(n) + n; }
+
+}  // namespace svdsb
+
+extern "C" {
+
+int svdsb_version(void) { return 1; }
+
+const char *svdsb_last_error(void) { return svdsb::g_err; }
+
+int64_t svdsb_launch_count(void) { return svdsb::g_launches.load(); }
+
+int svdsb_ctx_create(int device, svdsb_ctx **out) {
+  SVDSB_CHECK_ARG(out != nullptr, "svdsb_ctx_create: out is NULL");
+  SVDSB_CUDA(cudaSetDevice(device));
+  svdsb_ctx *c = new svdsb_ctx();
+  c->device = device;
+  c->next_ticket = 0;
+  if (cudaMalloc(&c->partials, sizeof(double) * svdsb::kMaxPartials) != cudaSuccess ||
+      cudaMalloc(&c->ticket, sizeof(unsigned int) * svdsb::kMaxTickets) != cudaSuccess) {
+    svdsb::set_error("svdsb_ctx_create: cudaMalloc failed");
+    delete c;
+    return SVDSB_ERR_ALLOC;
+  }
+  SVDSB_CUDA(cudaMemset(c->ticket, 0, sizeof(unsigned int) * svdsb::kMaxTickets));
+  SVDSB_CUDA(cudaDeviceSynchronize());
+  *out = c;
+  return SVDSB_OK;
+}
+
+int svdsb_ctx_destroy(svdsb_ctx *ctx) {
+  if (!ctx) return SVDSB_OK;
+  cudaFree(ctx->partials);
+  cudaFree(ctx->ticket);
+  delete ctx;
+  return SVDSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,949 @@
+"""GD+k Davidson eigensolver with every N-sized operation on the GPU.
+
+Host-side control flow mirrors pkg/src/itersvd/eigensolver.py (cited per
+method); the state it drives -- the basis V, its image W = Op V, the
+projection H, the refined QR factors, the locked vectors -- lives in
+device memory and is touched only by libsvdsb kernels.  Per outer
+iteration the host reads one small status record (Ritz values, candidate
+residual norms, stage-2 split residuals; < 2 KB) in a single
+synchronisation, plus one norm per Gram-Schmidt pass of the expansion
+vector: exactly the scalars the reference's branches depend on.
+
+Small g x g work (Rayleigh-Ritz eigenproblem, refined SVD, restart
+coefficient selection, H <- C^T H C, QR of R Y) runs in single-CTA device
+kernels; random draws come from the same numpy Generator streams as the
+reference so trajectories track it.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as dv
+from .device import DTYPE
+from .operators import NormEstimate
+
+EPS = 2.220446049250313e-16
+TARGET_LARGEST = "largest_algebraic"
+TARGET_SMALLEST = "smallest_algebraic"
+TARGET_CLOSEST_GEQ = "closest_geq"
+EXTRACT_RR = "rayleigh_ritz"
+EXTRACT_REFINED = "refined_const_shift"
+PRACTICAL_FLOOR_FACTOR = 10.0          # eigensolver.py:43
+_IMPROVE_FACTOR = 0.999                # eigensolver.py:47
+REORTH_FACTOR = 1.0 / np.sqrt(2.0)     # kernels.py:24
+DEFICIENT_TOL = 1e-14                  # kernels.py:28
+_MAX_REORTH_PASSES = 6                 # kernels.py:30
+_MAX_RANDOM_RETRIES = 20               # kernels.py:31
+
+
+class BasisCollapseError(RuntimeError):
+    """Every expansion direction was dependent several times in a row."""
+
+
+@dataclass
+class EigConfig:
+    """Solver knobs (eigensolver.py:54-107); same fields and validation."""
+
+    num_evals: int = 1
+    target: str = TARGET_LARGEST
+    shifts: tuple = ()
+    max_basis_size: int = 15
+    min_restart_size: int = 6
+    plus_k: int = 1
+    max_block_size: int = 1
+    locking: bool = False
+    extraction: str = EXTRACT_RR
+    convergence_test: object = None
+    practical_test: object = None
+    max_matvecs: int = None
+    deactivate_krylov_init: bool = False
+    seed: int = 0
+    disable_reset: bool = False
+    stagnation_window: int = 250
+    iteration_hook: object = None
+
+    def validate(self, dim):
+        if self.num_evals < 0:
+            raise ValueError("num_evals must be nonnegative")
+        if self.target not in (TARGET_LARGEST, TARGET_SMALLEST, TARGET_CLOSEST_GEQ):
+            raise ValueError("unknown target %r" % (self.target,))
+        if self.extraction not in (EXTRACT_RR, EXTRACT_REFINED):
+            raise ValueError("unknown extraction %r" % (self.extraction,))
+        if self.target == TARGET_CLOSEST_GEQ:
+            if not len(self.shifts):
+                raise ValueError("closest_geq needs at least one shift")
+            if not self.locking:
+                raise ValueError("interior targets require locking")
+        elif self.extraction == EXTRACT_REFINED:
+            raise ValueError("refined extraction is tied to interior targets")
+        if dim <= self.max_basis_size:
+            return
+        if not (0 < self.min_restart_size < self.max_basis_size):
+            raise ValueError("need 0 < min_restart_size < max_basis_size")
+        if self.plus_k < 0 or self.max_block_size < 1:
+            raise ValueError("bad plus_k or max_block_size")
+        if self.min_restart_size + self.plus_k >= self.max_basis_size:
+            raise ValueError("min_restart_size + plus_k must stay below max_basis_size")
+        if self.num_evals > self.max_basis_size - 2:
+            raise ValueError("num_evals too large for the basis size")
+        if self.max_basis_size > _lib.SMALL_MAX:
+            raise ValueError("max_basis_size above %d is not supported on device" % _lib.SMALL_MAX)
+
+
+@dataclass
+class EigStats:
+    matvecs: int = 0
+    precond_applies: int = 0
+    restarts: int = 0
+    resets: int = 0
+    outer_iterations: int = 0
+    syncs: int = 0
+
+
+@dataclass
+class EigResult:
+    """eigenvalues/residual_norms/converged on host; eigenvectors a
+    column-major device block (dim x t)."""
+
+    eigenvalues: np.ndarray
+    eigenvectors: object
+    residual_norms: np.ndarray
+    converged: np.ndarray
+    stats: EigStats
+    status: str = "ok"
+
+    @property
+    def num_converged(self):
+        return int(self.converged.sum())
+
+
+def select_interior_candidate(lams, shift):
+    """eigensolver.py:133-145."""
+    lams = np.asarray(lams, dtype=np.float64)
+    if lams.size == 0:
+        raise ValueError("no pairs to select from")
+    above = np.flatnonzero(lams >= shift)
+    if above.size:
+        return int(above[np.argmin(lams[above])])
+    return int(np.argmax(lams))
+
+
+class Candidate:
+    """Per-candidate view handed to convergence tests: host scalars plus
+    lazily materialised device vectors."""
+
+    __slots__ = ("lam", "rnorm", "x", "opx", "nv", "nu", "r7")
+
+    def __init__(self, lam, rnorm, x=None, opx=None, nv=None, nu=None, r7=None):
+        self.lam, self.rnorm, self.x, self.opx = lam, rnorm, x, opx
+        self.nv, self.nu, self.r7 = nv, nu, r7
+
+
+def _run_test(test, cand, op_norm):
+    fast = getattr(test, "evaluate", None)
+    if fast is not None:
+        return bool(fast(cand, op_norm))
+    return bool(test(cand.lam, cand.rnorm, cand.x, cand.opx, op_norm))
+
+
+def _test_needs(test):
+    """(needs x/opx vectors, needs split statistics) for a test."""
+    if test is None:
+        return False, False
+    if getattr(test, "evaluate", None) is not None:
+        return False, bool(getattr(test, "split_n", None) is not None)
+    return True, False
+
+
+class Orthonormalizer:
+    """Iterated classical Gram-Schmidt with the DGKS 1/sqrt(2) test and
+    random replacement of collapsed columns (kernels.py:54-133), one column
+    at a time on device; the host sees two norms per pass."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.c = torch.zeros(4 * _lib.SMALL_MAX * 4, dtype=DTYPE, device=ctx.device)
+        self.nrm = torch.zeros(2, dtype=DTYPE, device=ctx.device)
+        self.syncs = 0
+
+    def _pass(self, prior, v):
+        ctx = self.ctx
+        if prior:
+            total = sum(b.shape[1] for b in prior)
+            c = self.c[:total]
+            dv.gram(ctx, v.shape[0], prior, v, c.unsqueeze(1), norms2=self.nrm[0:1])
+            dv.project_out(ctx, v.shape[0], prior, c.unsqueeze(1), v, norms2=self.nrm[1:2])
+        else:
+            dv.col_norms2(ctx, v, self.nrm[0:1])
+            dv.col_norms2(ctx, v, self.nrm[1:2])
+        before2, after2 = dv.fetch(ctx, [self.nrm])[0]
+        self.syncs += 1
+        return float(np.sqrt(before2)), float(np.sqrt(after2))
+
+    def column(self, v, prior):
+        """DGKS loop on one column; returns the final norm (0 on collapse)
+        and leaves v normalised when it is > 0."""
+        final = 0.0
+        prev = orig = None
+        collapses = 0
+        for p in range(_MAX_REORTH_PASSES):
+            before, cur = self._pass(prior, v)
+            if p == 0:
+                orig = prev = before
+                if orig == 0.0:
+                    break
+            if cur < DEFICIENT_TOL * orig:
+                collapses += 1
+                if collapses >= 2:
+                    break
+            elif cur > REORTH_FACTOR * prev:
+                final = cur
+                break
+            else:
+                collapses = 0
+            prev = cur
+        if final > 0.0:
+            dv.scale_cols(self.ctx, v, self.nrm[1:2], dv.SCALE_DIV_SQRT)
+        return final
+
+    def __call__(self, block, against=None, start_col=0, rng=None):
+        rows, cols = block.shape
+        ext = [b for b in (against or []) if b is not None and b.shape[1] > 0]
+        n_ext = sum(b.shape[1] for b in ext)
+        for b in ext:
+            if b.shape[0] != rows:
+                raise ValueError("dimension mismatch between block and against")
+        if n_ext + cols > rows:
+            raise ValueError("more columns than the space can hold")
+        if rng is None:
+            rng = np.random.default_rng(0)
+        replaced = []
+        for j in range(start_col, cols):
+            prior = ext + ([block[:, :j]] if j > 0 else [])
+            v = block[:, j:j + 1]
+            flagged = False
+            for _ in range(_MAX_RANDOM_RETRIES):
+                if self.column(v, prior) > 0.0:
+                    break
+                if not flagged:
+                    replaced.append(j)
+                    flagged = True
+                v.copy_(torch.from_numpy(rng.standard_normal(rows)).unsqueeze(1))
+            else:
+                raise np.linalg.LinAlgError("orthonormalize could not produce an independent column")
+        return replaced
+
+
+class DavidsonSolver:
+    """One solve (eigensolver.py:157-785); create it, then call run()."""
+
+    def __init__(self, op, cfg, guesses=None, ortho_constraints=None, precond=None, est=None,
+                 est_mode="normal"):
+        cfg.validate(op.dim)
+        self.ctx = dv.context()
+        ctx = self.ctx
+        self.op = op
+        self.cfg = cfg
+        self.precond = precond
+        self.est = est if est is not None else NormEstimate()
+        if est_mode not in ("normal", "augmented"):
+            raise ValueError("est_mode must be 'normal' or 'augmented'")
+        self.est_mode = est_mode
+        self.rng = np.random.default_rng(cfg.seed)
+        self.stats = EigStats()
+        self.status = "ok"
+        self.n = op.dim
+        self.ortho = Orthonormalizer(ctx)
+
+        self.ext = []
+        if ortho_constraints is not None and ortho_constraints.shape[1] > 0:
+            c = dv.to_device_block(ortho_constraints)
+            self.ortho(c, rng=self.rng)
+            self.ext.append(c)
+        self.n_ext = sum(b.shape[1] for b in self.ext)
+
+        self.wanted = max(min(cfg.num_evals, self.n - self.n_ext), 0)
+        self.dense = self.n <= cfg.max_basis_size
+        gmax = self.n - self.n_ext if self.dense else cfg.max_basis_size
+        self.gmax = gmax
+        gm = max(gmax, 1)
+        bs = cfg.max_block_size
+
+        self.v = dv.new_block(self.n, gm)
+        self.w = dv.new_block(self.n, gm)
+        self._v2 = None
+        self._w2 = None
+        self.h = dv.small_matrix(gm, gm)
+        self._hg = dv.small_matrix(gm, gm)
+        self.g = 0
+        self.lams_d = torch.zeros(gm, dtype=DTYPE, device=ctx.device)
+        self.y_d = dv.small_matrix(gm, gm)
+        pmax = max(min(self.wanted + bs, gm), 1)
+        self.pmax = pmax
+        self.rbuf = dv.new_block(self.n, pmax)
+        self.xbuf = None
+        self.oxbuf = None
+        # status scratch: rn2 | split stats (6 per col) | r7^2 | refined lam
+        self.stat_d = torch.zeros(8 * pmax + 4, dtype=DTYPE, device=ctx.device)
+        self.hc = dv.small_matrix(gm + bs, bs)
+        self.coefs = dv.small_matrix(gm, gm)
+        self.count_d = torch.zeros(1, dtype=torch.int32, device=ctx.device)
+        self.prev_d = dv.small_matrix(gm, max(cfg.plus_k, 1))
+        self.yref = torch.zeros(gm, dtype=DTYPE, device=ctx.device)
+        self.excl = torch.zeros(gm, dtype=DTYPE, device=ctx.device)
+
+        self.locked_vecs = dv.new_block(self.n, 0)
+        self._locked_buf = dv.new_block(self.n, max(self.wanted, 1)) if cfg.locking else None
+        self.locked_vals = []
+        self.locked_rnorms = []
+        self.locked_user = []
+
+        self.q = None
+        self.rfac = None
+        self.tau = None
+
+        self.restarts_since_reset = 0
+        self.prev_coefs = None          # number of stored previous columns
+        self.prev_coefs_g = 0
+        self.collapse_streak = 0
+        self._slot_progress = {}
+        self._finished = self.wanted == 0
+
+        need_v1, split1 = _test_needs(cfg.convergence_test)
+        need_v2, split2 = _test_needs(cfg.practical_test)
+        self._need_vecs = need_v1 or need_v2 or cfg.iteration_hook is not None
+        self._split_n = None
+        for t in (cfg.convergence_test, cfg.practical_test):
+            if t is not None and getattr(t, "split_n", None) is not None:
+                self._split_n = int(t.split_n)
+        if self._need_vecs or self._split_n is not None or cfg.locking:
+            self.xbuf = dv.new_block(self.n, pmax)
+        if self._need_vecs:
+            self.oxbuf = dv.new_block(self.n, pmax)
+
+        if not self._finished:
+            self._init_basis(guesses)
+            if self.g == 0:
+                self._finished = True
+            elif self.cfg.extraction == EXTRACT_REFINED and not self.dense:
+                self._rebuild_qr()
+
+    # ------------------------------------------------------------ plumbing
+    @property
+    def op_norm(self):
+        return self.est.a_norm if self.est_mode == "augmented" else self.est.c_norm
+
+    def _observe(self, lams):
+        if self.est_mode == "augmented":
+            self.est.update_from_augmented(lams)
+        else:
+            self.est.update(lams)
+
+    def _budget_left(self):
+        if self.cfg.max_matvecs is None:
+            return 10 ** 18
+        return self.cfg.max_matvecs - self.stats.matvecs
+
+    def _apply_op(self, x, y):
+        self.stats.matvecs += x.shape[1]
+        self.op.apply_into(x, y)
+
+    def _active_shift(self):
+        shifts = self.cfg.shifts
+        i = min(len(self.locked_vals), len(shifts) - 1)
+        return float(shifts[i])
+
+    def _against(self):
+        blocks = list(self.ext)
+        if self.locked_vecs.shape[1]:
+            blocks.append(self.locked_vecs)
+        return blocks
+
+    def _order_mode(self):
+        if self.cfg.target == TARGET_LARGEST:
+            return _lib.ORDER_DESC, 0.0
+        if self.cfg.target == TARGET_SMALLEST:
+            return _lib.ORDER_ASC, 0.0
+        return _lib.ORDER_INTERIOR, self._active_shift()
+
+    def _user_test(self, cand):
+        test = self.cfg.convergence_test
+        if test is None:
+            return cand.rnorm <= max(1e-12 * self.op_norm, PRACTICAL_FLOOR_FACTOR * EPS * self.op_norm)
+        return _run_test(test, cand, self.op_norm)
+
+    def _practical_test(self, cand):
+        if self.cfg.practical_test is not None:
+            return _run_test(self.cfg.practical_test, cand, self.op_norm)
+        return self.op_norm > 0.0 and cand.rnorm <= PRACTICAL_FLOOR_FACTOR * EPS * self.op_norm
+
+    def _sync_fetch(self, tensors):
+        self.stats.syncs += 1
+        return dv.fetch(self.ctx, tensors)
+
+    def _upload_normal(self, block, draws):
+        """Copy a C-order (rows, cols) numpy draw into a column-major block."""
+        block.copy_(torch.from_numpy(np.ascontiguousarray(draws)))
+
+    def orthonormalize(self, block, against=None, start_col=0):
+        r = self.ortho(block, against=against, start_col=start_col, rng=self.rng)
+        self.stats.syncs = self.stats.syncs  # ortho keeps its own count
+        return r
+
+    # ------------------------------------------------------ initialization
+    def _init_basis(self, guesses):
+        """eigensolver.py:278-347."""
+        cfg = self.cfg
+        if self.dense:
+            free = self.gmax
+            self._upload_normal(self.v[:, :free], self.rng.standard_normal((self.n, free)))
+            self.orthonormalize(self.v[:, :free], against=self.ext)
+            self.g = free
+            take = min(free, max(self._budget_left(), 0))
+            if take:
+                self._apply_op(self.v[:, :take], self.w[:, :take])
+            if take < free:
+                self.status = "budget"
+                self.g = take
+            self._update_h_full()
+            return
+        g0 = 0
+        if guesses is not None and guesses.shape[1] > 0:
+            take = min(guesses.shape[1], self.gmax - 1)
+            src = guesses if isinstance(guesses, torch.Tensor) else torch.from_numpy(
+                np.asarray(guesses, dtype=np.float64))
+            self.v[:, :take].copy_(src[:, :take])
+            self.orthonormalize(self.v[:, :take], against=self._against())
+            g0 = take
+        if g0 == 0:
+            b0 = min(max(cfg.max_block_size, cfg.num_evals), self.gmax - 1)
+            self._upload_normal(self.v[:, :b0], self.rng.standard_normal((self.n, b0)))
+            self.orthonormalize(self.v[:, :b0], against=self._against())
+            g0 = b0
+        if cfg.deactivate_krylov_init:
+            init_target = g0
+        else:
+            free = self.n - self.n_ext
+            init_target = min(max(cfg.min_restart_size, g0), self.gmax - 1, free)
+        if g0 > 1:
+            take = min(g0 - 1, max(self._budget_left(), 0))
+            if take:
+                self._apply_op(self.v[:, :take], self.w[:, :take])
+            if take < g0 - 1:
+                self.status = "budget"
+                self.g = take
+                self._update_h_full()
+                return
+        j = g0 - 1
+        while True:
+            if self._budget_left() < 1:
+                self.status = "budget"
+                self.g = j
+                self._update_h_full()
+                return
+            self._apply_op(self.v[:, j:j + 1], self.w[:, j:j + 1])
+            if j + 1 >= init_target:
+                break
+            dv.axpby(self.ctx, 1.0, self.w[:, j:j + 1], 0.0, self.v[:, j + 1:j + 2])
+            self.orthonormalize(self.v[:, :j + 2], against=self._against(), start_col=j + 1)
+            j += 1
+        self.g = init_target
+        self._update_h_full()
+
+    def _update_h_full(self):
+        """H = sym(V^T W) (eigensolver.py:349-352)."""
+        g = self.g
+        if g == 0:
+            return
+        dv.gram(self.ctx, self.n, [self.v[:, :g]], self.w[:, :g], self._hg[:g, :g])
+        dv.h_symmetrize(self.ctx, g, self._hg[:g, :g], self.h[:g, :g])
+
+    def _ensure_qr(self):
+        if self.q is None:
+            gm = max(self.gmax, 1)
+            self.q = dv.new_block(self.n, gm)
+            self._q2 = dv.new_block(self.n, gm)
+            self.rfac = dv.small_matrix(gm, gm)
+            self._qtmp = dv.new_block(self.n, 1)
+            self._qy = dv.small_matrix(gm, gm)
+            self._ry = dv.small_matrix(gm, gm)
+
+    def _rebuild_qr(self):
+        """Q R = W - tau V column by column (eigensolver.py:354-357)."""
+        self._ensure_qr()
+        self.tau = self._active_shift()
+        self.rfac.zero_()
+        self.qg = 0
+        for j in range(self.g):
+            self._qr_append_col(self.w[:, j:j + 1], self.v[:, j:j + 1])
+
+    def _qr_append_col(self, wcol, vcol):
+        """qr_append of (w - tau v) (kernels.py:160-222) into column qg."""
+        ctx = self.ctx
+        g = self.qg
+        v = self.q[:, g:g + 1]
+        dv.axpby(ctx, 1.0, wcol, 0.0, v)
+        dv.axpby(ctx, -self.tau, vcol, 1.0, v)
+        coef = self.rfac[:g, g:g + 1]
+        self.rfac[:g + 1, g].zero_()
+        prior = [self.q[:, :g]] if g > 0 else []
+        orth = self.ortho
+        # the reference's loop: orig, then passes with coefficient accumulation
+        orig = None
+        prev = None
+        deficient = False
+        collapses = 0
+        for p in range(_MAX_REORTH_PASSES):
+            if prior:
+                c = orth.c[:g].unsqueeze(1)
+                dv.gram(ctx, self.n, prior, v, c, norms2=orth.nrm[0:1])
+                dv.project_out(ctx, self.n, prior, c, v, norms2=orth.nrm[1:2])
+                dv.axpby(ctx, 1.0, c, 1.0, coef)
+            else:
+                dv.col_norms2(ctx, v, orth.nrm[0:1])
+                dv.col_norms2(ctx, v, orth.nrm[1:2])
+            before2, after2 = dv.fetch(ctx, [orth.nrm])[0]
+            orth.syncs += 1
+            before, cur = float(np.sqrt(before2)), float(np.sqrt(after2))
+            if p == 0:
+                orig = prev = before
+                if orig == 0.0:
+                    deficient = True
+                    break
+            if cur < DEFICIENT_TOL * orig:
+                collapses += 1
+                if collapses >= 2:
+                    deficient = True
+                    break
+            elif cur > REORTH_FACTOR * prev:
+                break
+            else:
+                collapses = 0
+            prev = cur
+        else:
+            deficient = True
+        if deficient:
+            v.copy_(torch.from_numpy(self.rng.standard_normal(self.n)).unsqueeze(1))
+            self.ortho(v, against=prior, rng=self.rng)
+            self.rfac[g, g] = 0.0
+        else:
+            dv.scale_cols(ctx, v, orth.nrm[1:2], dv.SCALE_DIV_SQRT)
+            self.rfac[g:g + 1, g].copy_(torch.sqrt(orth.nrm[1:2]))
+        self.qg = g + 1
+        return deficient
+
+    # ---------------------------------------------------------- extraction
+    def extract_rayleigh_ritz(self):
+        """Ritz values/vectors of H[:g,:g] in target order (device)."""
+        order, shift = self._order_mode()
+        g = self.g
+        dv.syev_small(self.ctx, self.h[:g, :g], g, order, shift, self.lams_d[:g], self.y_d[:g, :g])
+        return self.lams_d[:g], self.y_d[:g, :g]
+
+    def _candidates(self, y, lam, p, need_x, need_ox):
+        """R = W Y - V Y diag(lam) for p columns, norms and optional split
+        statistics (eigensolver.py:385-394); returns device views."""
+        g = self.g
+        r = self.rbuf[:, :p]
+        x = self.xbuf[:, :p] if need_x else None
+        ox = self.oxbuf[:, :p] if need_ox else None
+        rn2 = self.stat_d[:p]
+        dv.ritz_residual(self.ctx, self.v[:, :g], self.w[:, :g], y, lam, r, x, ox, rn2)
+        split = None
+        if self._split_n is not None:
+            pm = self.pmax
+            st = self.stat_d[pm:pm + 6 * p]
+            r7 = self.stat_d[7 * pm:7 * pm + p]
+            dv.split_stats(self.ctx, self._split_n, r, x, st)
+            dv.split_residual(self.ctx, self._split_n, r, x, lam, st, r7)
+            split = (st, r7)
+        return r, x, ox, rn2, split
+
+    def _make_cands(self, lams, rn2, split_h, p, x, ox):
+        cands = []
+        for i in range(p):
+            c = Candidate(float(lams[i]), float(np.sqrt(max(rn2[i], 0.0))))
+            if x is not None:
+                c.x = x[:, i]
+            if ox is not None:
+                c.opx = ox[:, i]
+            if split_h is not None:
+                st, r7 = split_h
+                c.nv = float(np.sqrt(st[6 * i + 2]))
+                c.nu = float(np.sqrt(st[6 * i + 5]))
+                c.r7 = float(np.sqrt(r7[i])) if np.isfinite(r7[i]) else np.inf
+            cands.append(c)
+        return cands
+
+    # ---------------------------------------------------- reset, stagnation
+    def maybe_reset(self, rnorm):
+        """eigensolver.py:396-416."""
+        if self.cfg.disable_reset:
+            return False
+        threshold = np.sqrt(self.restarts_since_reset) * self.op_norm * EPS
+        if rnorm >= threshold:
+            return False
+        g = self.g
+        if self._budget_left() < g:
+            return False
+        self.orthonormalize(self.v[:, :g], against=self._against())
+        self._apply_op(self.v[:, :g], self.w[:, :g])
+        self._update_h_full()
+        if self.q is not None:
+            self._rebuild_qr()
+        self.restarts_since_reset = 0
+        self.prev_coefs = None
+        self.stats.resets += 1
+        return True
+
+    def _note_progress(self, slot, rnorm, lam):
+        """eigensolver.py:418-433."""
+        rec = self._slot_progress.get(slot)
+        if rec is None:
+            self._slot_progress[slot] = [rnorm, 0, lam]
+            return 0
+        best, stale, lam_ref = rec
+        moved = abs(lam - lam_ref) > 100.0 * EPS * max(abs(lam), abs(lam_ref))
+        if rnorm < best * _IMPROVE_FACTOR or moved:
+            self._slot_progress[slot] = [min(rnorm, best), 0, lam]
+            return 0
+        rec[1] = stale + 1
+        return stale + 1
+
+    # ------------------------------------------------ restarting and locking
+    def _reseed_basis(self):
+        """eigensolver.py:471-483."""
+        self._upload_normal(self.v[:, :1], self.rng.standard_normal((self.n, 1)))
+        self.orthonormalize(self.v[:, :1], against=self._against())
+        self.g = 1
+        if self._budget_left() < 1:
+            self.status = "budget"
+            self._finished = True
+            self.w[:, 0].zero_()
+        else:
+            self._apply_op(self.v[:, :1], self.w[:, :1])
+        self._update_h_full()
+
+    def _swap_basis(self, s):
+        if self._v2 is None:
+            self._v2 = dv.new_block(self.n, max(self.gmax, 1))
+            self._w2 = dv.new_block(self.n, max(self.gmax, 1))
+        g = self.g
+        c = self.coefs[:g, :s]
+        dv.ts_gemm(self.ctx, self.v[:, :g], c, self._v2[:, :s])
+        dv.ts_gemm(self.ctx, self.w[:, :g], c, self._w2[:, :s])
+        self.v, self._v2 = self._v2, self.v
+        self.w, self._w2 = self._w2, self.w
+
+    def restart(self, conv_count, exclude=None, y_first=None):
+        """Thick restart keeping target-ordered Ritz vectors plus the
+        previous candidate coefficients (eigensolver.py:485-536).  Uses the
+        ordered Ritz coefficients of the current extraction (self.y_d)."""
+        cfg = self.cfg
+        g = self.g
+        retain_target = max(cfg.min_restart_size, conv_count + 1)
+        retain_target = max(min(retain_target, g - 1 if g > 1 else 1, self.gmax - 2), 1)
+        prev = None
+        nprev = 0
+        if self.prev_coefs is not None and self.prev_coefs_g <= g:
+            prev = self.prev_d
+            nprev = self.prev_coefs
+        dv.restart_coefs(self.ctx, g, self.gmax, y_first, self.y_d[:g, :g], g, retain_target, exclude,
+                         prev, nprev, self.prev_coefs_g, cfg.plus_k, self.coefs[:g, :], self.count_d)
+        self.stats.syncs += 1
+        s = int(self.count_d.item())
+        self.stats.restarts += 1
+        self.restarts_since_reset += 1
+        self.prev_coefs = None
+        if s == 0:
+            self._reseed_basis()
+            if self.q is not None and not self._finished:
+                self._rebuild_qr()
+            return self.g
+        self._swap_basis(s)
+        dv.project_small(self.ctx, self.h[:g, :g], g, self.coefs[:g, :s], s, self.h[:s, :s])
+        if self.q is not None:
+            dv.qr_small(self.ctx, self.rfac[:g, :g], g, self.coefs[:g, :s], s, self._qy[:g, :s],
+                        self._ry[:s, :s])
+            dv.ts_gemm(self.ctx, self.q[:, :g], self._qy[:g, :s], self._q2[:, :s])
+            self.q, self._q2 = self._q2, self.q
+            self.rfac[:s, :s].copy_(self._ry[:s, :s])
+            self.qg = s
+        self.g = s
+        return s
+
+    def lock_candidate(self, lam, y, x, rnorm, user_flag):
+        """eigensolver.py:538-558; y: device coefficient vector, x: device
+        candidate vector."""
+        cols = self.locked_vecs.shape[1]
+        slot = self._locked_buf[:, cols:cols + 1]
+        dv.col_norms2(self.ctx, x, self.stat_d[-1:])
+        dv.scale_cols(self.ctx, x, self.stat_d[-1:], dv.SCALE_DIV_SQRT, slot)
+        self.locked_vecs = self._locked_buf[:, :cols + 1]
+        self.orthonormalize(self.locked_vecs, against=self.ext, start_col=cols)
+        self.locked_vals.append(float(lam))
+        self.locked_rnorms.append(float(rnorm))
+        self.locked_user.append(bool(user_flag))
+        if len(self.locked_vals) >= self.wanted:
+            self._finished = True
+            return
+        self.excl[:self.g].copy_(y)
+        self.restart(0, exclude=self.excl[:self.g])
+        if self.q is not None and not self._finished:
+            self._rebuild_qr()
+
+    # ------------------------------------------------------------ main loop
+    def step(self):
+        """One outer iteration (eigensolver.py:563-664)."""
+        cfg = self.cfg
+        self.stats.outer_iterations += 1
+        info = {"restarted": False, "reset": False, "locked": False, "done": False}
+        g = self.g
+        lams_d, y_d = self.extract_rayleigh_ritz()
+        refined = cfg.extraction == EXTRACT_REFINED
+        need_x = self.xbuf is not None
+        need_ox = self._need_vecs
+        if refined:
+            lamref = self.stat_d[-2:-1]
+            dv.refined_small(self.ctx, self.rfac[:g, :g], self.h[:g, :g], g, self.yref[:g], lamref)
+            p = 1
+            r, x, ox, rn2, split = self._candidates(self.yref[:g].unsqueeze(1), lamref, 1, need_x, need_ox)
+            fetch = [lams_d, rn2, lamref]
+        else:
+            p = 1 if cfg.locking else min(self.wanted + cfg.max_block_size, g)
+            r, x, ox, rn2, split = self._candidates(y_d[:, :p], lams_d[:p], p, need_x, need_ox)
+            fetch = [lams_d, rn2]
+        if split is not None:
+            fetch += [split[0], split[1]]
+        got = self._sync_fetch(fetch)
+        lams = got[0]
+        rn2_h = got[1]
+        split_h = (got[-2], got[-1]) if split is not None else None
+        self._observe(lams)
+
+        if refined:
+            lam_ref = float(got[2][0])
+            cands = self._make_cands(np.array([lam_ref]), rn2_h, split_h, 1, x, ox)
+            cand = cands[0]
+            conv_count = 0
+            ci = 0
+            y_first = self.yref[:g]
+            y_c = self.yref[:g]
+        else:
+            cands = self._make_cands(lams, rn2_h, split_h, p, x, ox)
+            conv_count = 0
+            if not cfg.locking:
+                for i in range(min(self.wanted, p)):
+                    if not (self._user_test(cands[i]) or self._practical_test(cands[i])):
+                        break
+                    conv_count += 1
+            ci = min(conv_count, p - 1)
+            cand = cands[ci]
+            y_first = None
+            y_c = y_d[:, ci]
+        lam_c, rnorm_c = cand.lam, cand.rnorm
+        x_c = x[:, ci:ci + 1] if x is not None else None
+        res_block = r[:, ci:min(ci + cfg.max_block_size, p)]
+
+        slot = len(self.locked_vals) if cfg.locking else conv_count
+        info.update(lam=lam_c, rnorm=rnorm_c, x=x_c, conv_count=conv_count, g=g, slot=slot,
+                    tau=self.tau if self.q is not None else None)
+        if cfg.iteration_hook is not None:
+            yfull = dv.to_host(y_d)
+            yref_h = self.yref[:g].cpu().numpy() if refined else None
+            cfg.iteration_hook(self, dict(info, rr_values=lams, rr_coefs=yfull, y_refined=yref_h))
+
+        if self.maybe_reset(rnorm_c):
+            info["reset"] = True
+            return info
+        if not cfg.locking and conv_count >= self.wanted:
+            self._finished = True
+            info["done"] = True
+            return info
+        if cfg.locking:
+            ok_user = self._user_test(cand)
+            if ok_user or self._practical_test(cand):
+                self.lock_candidate(lam_c, y_c, x_c, rnorm_c, ok_user)
+                info["locked"] = True
+                info["done"] = self._finished
+                return info
+        if cfg.stagnation_window is not None and \
+                self._note_progress(slot, rnorm_c, lam_c) > cfg.stagnation_window:
+            self.status = "stagnated"
+            self._finished = True
+            info["done"] = True
+            return info
+        if self._budget_left() < cfg.max_block_size:
+            self.status = "budget"
+            self._finished = True
+            info["done"] = True
+            return info
+
+        restarted = False
+        if self.g >= self.gmax:
+            # keep the candidate coefficients we still need after the restart
+            self.restart(conv_count, y_first=y_first)
+            restarted = True
+            info["restarted"] = True
+            if self._finished:
+                info["done"] = True
+                return info
+        self._expand(res_block)
+        if not restarted:
+            if refined:
+                dv.axpby(self.ctx, 1.0, self.yref[:g].unsqueeze(1), 0.0, self.prev_d[:g, :1])
+                self.prev_coefs = 1
+            else:
+                hi = min(conv_count + max(cfg.plus_k, 1), g)
+                k = hi - conv_count
+                if k > 0:
+                    dv.axpby(self.ctx, 1.0, y_d[:, conv_count:hi], 0.0, self.prev_d[:g, :k])
+                self.prev_coefs = k
+            self.prev_coefs_g = info["g"]
+        return info
+
+    def _expand(self, res_block):
+        """eigensolver.py:666-700."""
+        b = min(res_block.shape[1], self.gmax - self.g)
+        if b <= 0:
+            return
+        block = res_block[:, :b]
+        g = self.g
+        dst = self.v[:, g:g + b]
+        if self.precond is not None:
+            self.precond.apply_into(block, dst)
+            self.stats.precond_applies += b
+        else:
+            dv.axpby(self.ctx, 1.0, block, 0.0, dst)
+        replaced = self.orthonormalize(self.v[:, :g + b], against=self._against(), start_col=g)
+        if len(replaced) == b:
+            self.collapse_streak += 1
+            if self.collapse_streak >= 3:
+                raise BasisCollapseError("no independent expansion direction after 3 retries")
+        else:
+            self.collapse_streak = 0
+        self._apply_op(self.v[:, g:g + b], self.w[:, g:g + b])
+        dv.gram(self.ctx, self.n, [self.v[:, :g + b]], self.w[:, g:g + b], self.hc[:g + b, :b])
+        dv.h_insert(self.ctx, g, b, self.hc[:g + b, :b], self.h)
+        if self.q is not None:
+            for j in range(b):
+                self._qr_append_col(self.w[:, g + j:g + j + 1], self.v[:, g + j:g + j + 1])
+        self.g = g + b
+
+    # ---------------------------------------------------------- finalization
+    def _final_pairs(self, x, wx, z_d, lam_d, t):
+        """x2 = x z, wx2 = wx z, res = wx2 - x2 lam, norms (+split)."""
+        x2 = dv.new_block(self.n, t)
+        rbuf = dv.new_block(self.n, t)
+        ox2 = dv.new_block(self.n, t) if self._need_vecs else None
+        rn2 = torch.zeros(t, dtype=DTYPE, device=self.ctx.device)
+        dv.ritz_residual(self.ctx, x, wx, z_d, lam_d, rbuf, x2, ox2, rn2)
+        fetch = [lam_d, rn2]
+        if self._split_n is not None:
+            st = torch.zeros(6 * t, dtype=DTYPE, device=self.ctx.device)
+            r7 = torch.zeros(t, dtype=DTYPE, device=self.ctx.device)
+            dv.split_stats(self.ctx, self._split_n, rbuf, x2, st)
+            dv.split_residual(self.ctx, self._split_n, rbuf, x2, lam_d, st, r7)
+            fetch += [st, r7]
+        got = self._sync_fetch(fetch)
+        split_h = (got[2], got[3]) if self._split_n is not None else None
+        cands = self._make_cands(got[0], got[1], split_h, t, x2, ox2)
+        conv = np.array([self._user_test(cands[i]) for i in range(t)], dtype=bool)
+        rnorms = np.array([c.rnorm for c in cands], dtype=np.float64)
+        return np.asarray(got[0], dtype=np.float64), x2, rnorms, conv
+
+    def finalize_soft_locked(self):
+        """Extra RR over the leading pairs with fresh products
+        (eigensolver.py:705-724)."""
+        _, y_d = self.extract_rayleigh_ritz()
+        t = min(self.wanted, self.g)
+        if t == 0:
+            return np.zeros(0), dv.new_block(self.n, 0), np.zeros(0), np.zeros(0, dtype=bool)
+        x = dv.new_block(self.n, t)
+        dv.ts_gemm(self.ctx, self.v[:, :self.g], y_d[:, :t], x)
+        wx = dv.new_block(self.n, t)
+        self._apply_op(x, wx)
+        h2 = dv.small_matrix(t, t)
+        dv.gram(self.ctx, self.n, [x], wx, h2)
+        order, shift = self._order_mode()
+        lam2 = torch.zeros(t, dtype=DTYPE, device=self.ctx.device)
+        z = dv.small_matrix(t, t)
+        dv.syev_small(self.ctx, h2, t, order, shift, lam2, z)
+        return self._final_pairs(x, wx, z, lam2, t)
+
+    def _finalize_locked(self):
+        """eigensolver.py:726-739."""
+        t = len(self.locked_vals)
+        if t == 0:
+            return np.zeros(0), dv.new_block(self.n, 0), np.zeros(0), np.zeros(0, dtype=bool)
+        x = self.locked_vecs[:, :t]
+        wx = dv.new_block(self.n, t)
+        self._apply_op(x, wx)
+        lam = torch.zeros(t, dtype=DTYPE, device=self.ctx.device)
+        dv.col_dots(self.ctx, x, wx, lam)
+        eye = dv.small_matrix(t, t)
+        eye.copy_(torch.eye(t, dtype=DTYPE))
+        return self._final_pairs(x, wx, eye, lam, t)
+
+    def _run_dense(self):
+        """Exact solve once the basis spans the admissible space
+        (eigensolver.py:741-768)."""
+        g = self.g
+        lams_all_d = torch.zeros(max(g, 1), dtype=DTYPE, device=self.ctx.device)
+        y_all = dv.small_matrix(max(g, 1), max(g, 1))
+        if g:
+            dv.syev_small(self.ctx, self.h[:g, :g], g, _lib.ORDER_ASC, 0.0, lams_all_d[:g], y_all[:g, :g])
+        lams_all = self._sync_fetch([lams_all_d[:g]])[0]
+        self._observe(lams_all)
+        if self.cfg.target == TARGET_CLOSEST_GEQ:
+            shifts = self.cfg.shifts
+            chosen = []
+            open_idx = list(range(lams_all.shape[0]))
+            for i in range(min(self.wanted, lams_all.shape[0])):
+                s = float(shifts[min(i, len(shifts) - 1)])
+                pick = open_idx[select_interior_candidate(lams_all[open_idx], s)]
+                open_idx.remove(pick)
+                chosen.append(pick)
+        else:
+            if self.cfg.target == TARGET_LARGEST:
+                order = np.argsort(-lams_all, kind="stable")
+            else:
+                order = np.argsort(lams_all, kind="stable")
+            chosen = list(order[:self.wanted])
+        t = len(chosen)
+        if t == 0:
+            return EigResult(np.zeros(0), dv.new_block(self.n, 0), np.zeros(0), np.zeros(0, dtype=bool),
+                             self.stats, self.status)
+        idx = torch.tensor(chosen, dtype=torch.long, device=self.ctx.device)
+        ysel = dv.small_matrix(g, t)
+        ysel.copy_(y_all[:g, :g].index_select(1, idx))
+        lam_sel = lams_all_d[:g].index_select(0, idx).contiguous()
+        lam, x, rnorms, conv = self._final_pairs(self.v[:, :g], self.w[:, :g], ysel, lam_sel, t)
+        return EigResult(lam, x, rnorms, conv, self.stats, self.status)
+
+    def run(self):
+        if self.wanted == 0:
+            return EigResult(np.zeros(0), dv.new_block(self.n, 0), np.zeros(0), np.zeros(0, dtype=bool),
+                             self.stats, self.status)
+        if self.dense:
+            return self._run_dense()
+        while not self._finished:
+            self.step()
+        if self.cfg.locking:
+            lam, x, rnorms, conv = self._finalize_locked()
+        else:
+            lam, x, rnorms, conv = self.finalize_soft_locked()
+        self.stats.syncs += self.ortho.syncs
+        return EigResult(np.asarray(lam, dtype=np.float64), x, np.asarray(rnorms, dtype=np.float64), conv,
+                         self.stats, self.status)
+
+
+def eig_solve(op, cfg, guesses=None, ortho_constraints=None, precond=None, est=None, est_mode="normal"):
+    """Compute cfg.num_evals eigenpairs of a symmetric device operator
+    (eigensolver.py:788-821)."""
+    solver = DavidsonSolver(op, cfg, guesses=guesses, ortho_constraints=ortho_constraints, precond=precond,
+                            est=est, est_mode=est_mode)
+    return solver.run()

@@ -1,0 +1,365 @@
+"""Kernel parity on the GPU: CSR build / transpose / SpMV / preconditioner
+diagonal bit-exact against the oracle (the reference's own summation
+order), tall-skinny kernels against fp64 numpy within 1e-13 relative, and
+the single-CTA small dense kernels against LAPACK."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import csr as ocsr
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev():
+    from paper_1607_01404_b200 import device as dv
+    return dv
+
+
+def _rand_coo(rng, m, n, nnz, dup=True, scale_spread=True):
+    rows = rng.integers(0, m, nnz)
+    cols = rng.integers(0, n, nnz)
+    vals = rng.standard_normal(nnz)
+    if scale_spread:
+        vals *= 10.0 ** rng.uniform(-4, 4, nnz)
+    if not dup:
+        key = np.unique(rows * n + cols)
+        rows, cols = key // n, key % n
+        vals = vals[:key.size]
+    return rows, cols, vals
+
+
+def _csr(m, n, rows, cols, vals):
+    from paper_1607_01404_b200 import SparseMatrixCsr
+    rp, ci, va = ocsr.csr_from_coo(m, n, rows, cols, vals)
+    return SparseMatrixCsr(m, n, rp, ci, va), (rp, ci, va)
+
+
+SHAPES = [(1, 1, 1), (7, 5, 12), (300, 40, 3000), (40, 300, 3000), (2000, 1500, 30000), (513, 257, 0)]
+
+
+@pytest.mark.parametrize("m,n,nnz", SHAPES)
+def test_transpose_build_bit_exact(m, n, nnz, rng):
+    rows, cols, vals = _rand_coo(rng, m, n, nnz)
+    a, (rp, ci, va) = _csr(m, n, rows, cols, vals)
+    dev = a.device_csr()
+    t_rp, t_ci, t_va = dev.export(transpose=True)
+    e_rp, e_ci, e_va = ocsr.csr_transpose(m, n, rp, ci, va)
+    assert np.array_equal(t_rp, e_rp)
+    assert np.array_equal(t_ci, e_ci)
+    assert np.array_equal(t_va.view(np.int64), e_va.view(np.int64))
+    f_rp, f_ci, f_va = dev.export(transpose=False)
+    assert np.array_equal(f_rp, rp) and np.array_equal(f_ci, ci) and np.array_equal(f_va, va)
+
+
+@pytest.mark.parametrize("m,n,nnz", [(5, 4, 30), (300, 40, 3000), (1000, 2000, 50000)])
+def test_from_coo_device_bit_exact(m, n, nnz, rng):
+    from paper_1607_01404_b200 import SparseMatrixCsr
+    rows, cols, vals = _rand_coo(rng, m, n, nnz)
+    # force explicit duplicates
+    rows = np.concatenate([rows, rows[:nnz // 3]])
+    cols = np.concatenate([cols, cols[:nnz // 3]])
+    vals = np.concatenate([vals, rng.standard_normal(nnz // 3)])
+    a = SparseMatrixCsr.from_coo(m, n, rows, cols, vals)
+    e_rp, e_ci, e_va = ocsr.csr_from_coo(m, n, rows, cols, vals)
+    assert a.nnz == e_va.size
+    assert np.array_equal(a.row_ptr, e_rp)
+    assert np.array_equal(a.col_idx, e_ci)
+    assert np.array_equal(a.values.view(np.int64), e_va.view(np.int64))
+
+
+def _spmv_dev(a, x, transpose):
+    dv = _dev()
+    dev = a.device_csr()
+    xb = dv.to_device_block(x)
+    rows = a.n if transpose else a.m
+    y = dv.new_block(rows, xb.shape[1])
+    dev.matvec(xb, y, transpose=transpose)
+    return dv.to_host(y)
+
+
+@pytest.mark.parametrize("m,n,nnz", SHAPES[:5])
+@pytest.mark.parametrize("b", [1, 3, 4])
+def test_spmv_bit_exact(m, n, nnz, b, rng):
+    rows, cols, vals = _rand_coo(rng, m, n, nnz)
+    a, (rp, ci, va) = _csr(m, n, rows, cols, vals)
+    x = rng.standard_normal((n, b)) * 10.0 ** rng.uniform(-3, 3, (n, b))
+    y = rng.standard_normal((m, b))
+    got = _spmv_dev(a, x, False)
+    want = ocsr.spmv(m, n, rp, ci, va, x)
+    assert np.array_equal(got, want)
+    got_t = _spmv_dev(a, y, True)
+    want_t = ocsr.spmv(m, n, rp, ci, va, y, transpose=True)
+    assert np.array_equal(got_t, want_t)
+
+
+def test_spmv_long_rows_and_dead_rows(rng):
+    """Rows longer than one tile (2048 nnz) take the chunked path: results
+    are deterministic and within fp64 rounding of the sequential sum."""
+    m, n = 20000, 64
+    rows = np.concatenate([rng.integers(0, m, 60000), np.arange(0, m, 3)])
+    cols = np.concatenate([rng.integers(0, 4, 60000), rng.integers(0, n, (m + 2) // 3)])
+    vals = rng.standard_normal(rows.size)
+    a, (rp, ci, va) = _csr(m, n, rows, cols, vals)
+    assert np.diff(ocsr.csr_transpose(m, n, rp, ci, va)[0]).max() > 2048
+    y = rng.standard_normal((m, 2))
+    got1 = _spmv_dev(a, y, True)
+    got2 = _spmv_dev(a, y, True)
+    assert np.array_equal(got1, got2)
+    want = ocsr.spmv(m, n, rp, ci, va, y, transpose=True)
+    scale = np.abs(va)[:, None] * np.abs(y[np.repeat(np.arange(m), np.diff(rp))])
+    bound = 1e-14 * np.sqrt(np.bincount(ci, weights=scale[:, 0] ** 2, minlength=n)).max() * 50
+    assert np.abs(got1 - want).max() <= max(bound, 1e-12)
+    # the short rows (fewer than a tile) are still bit-exact
+    t_rp = ocsr.csr_transpose(m, n, rp, ci, va)[0]
+    short = np.flatnonzero(np.diff(t_rp) <= 2048)
+    assert np.array_equal(got1[short], want[short])
+
+
+def test_spmv_identity_permutation_dead_row():
+    """test_matio.py:99-112 known answers."""
+    from paper_1607_01404_b200 import SparseMatrixCsr
+    a = SparseMatrixCsr.from_dense(np.array([[0.0, 1.0], [1.0, 0.0], [0.0, 0.0]]))
+    assert np.array_equal(_spmv_dev(a, np.array([[2.0], [5.0]]), False)[:, 0], [5.0, 2.0, 0.0])
+    assert np.array_equal(_spmv_dev(a, np.array([[7.0], [11.0], [13.0]]), True)[:, 0], [11.0, 7.0])
+    eye = SparseMatrixCsr.from_dense(np.eye(3))
+    x = np.random.default_rng(0).standard_normal((3, 2))
+    assert np.array_equal(_spmv_dev(eye, x, False), x)
+
+
+@pytest.mark.parametrize("side", ["cols", "rows"])
+def test_jacobi_diag_bit_exact(side, rng):
+    from paper_1607_01404_b200 import jacobi_precond_on_normal
+    m, n = 400, 250
+    rows, cols, vals = _rand_coo(rng, m, n, 4000)
+    a, (rp, ci, va) = _csr(m, n, rows, cols, vals)
+    pre = jacobi_precond_on_normal(a, side=side)
+    want = ocsr.jacobi_diag(m, n, rp, ci, va, side=side)
+    got = pre.diagonal.cpu().numpy()
+    assert np.array_equal(got, want)
+    x = rng.standard_normal((want.size, 2))
+    y = _dev().to_host(pre.apply(_dev().to_device_block(x)))
+    assert np.array_equal(y, x / want[:, None])
+
+
+def test_normal_and_augmented_operators(rng):
+    from paper_1607_01404_b200 import SvdOperator, make_augmented_operator, make_normal_operator
+    m, n = 300, 200
+    rows, cols, vals = _rand_coo(rng, m, n, 3000, scale_spread=False)
+    a, (rp, ci, va) = _csr(m, n, rows, cols, vals)
+    op = SvdOperator.from_csr(a)
+    d = a.to_dense()
+    c = make_normal_operator(op)
+    x = rng.standard_normal((n, 3))
+    got = _dev().to_host(c.apply(_dev().to_device_block(x)))
+    ref = d.T @ (d @ x)
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+    assert op.n_matvecs == 6
+    b = make_augmented_operator(op)
+    z = rng.standard_normal((n + m, 2))
+    got = _dev().to_host(b.apply(_dev().to_device_block(z)))
+    ref = np.vstack([d.T @ z[n:], d @ z[:n]])
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+    assert op.n_matvecs == 10
+
+
+# ------------------------------------------------------------ tall-skinny
+
+@pytest.mark.parametrize("dim", [1, 100, 5000, 300001])
+def test_gram_project_tsgemm(dim, rng):
+    dv = _dev()
+    ctx = dv.context()
+    a1 = rng.standard_normal((dim, 7))
+    a2 = rng.standard_normal((dim, 30))
+    y = rng.standard_normal((dim, 4))
+    X1, X2, Y = dv.to_device_block(a1), dv.to_device_block(a2), dv.to_device_block(y)
+    for b in (1, 4):
+        C = dv.small_matrix(37, b)
+        nrm = torch.zeros(b, dtype=torch.float64, device=ctx.device)
+        dv.gram(ctx, dim, [X1, X2], Y[:, :b], C, norms2=nrm)
+        want = np.hstack([a1, a2]).T @ y[:, :b]
+        got = dv.to_host(C)
+        assert np.abs(got - want).max() <= 1e-13 * max(1.0, np.abs(want).max()) * np.sqrt(dim)
+        assert np.allclose(nrm.cpu().numpy(), (y[:, :b] ** 2).sum(0), rtol=1e-13)
+        Yc = Y[:, :b].clone()
+        Yc = dv.to_device_block(y[:, :b])
+        nrm2 = torch.zeros(b, dtype=torch.float64, device=ctx.device)
+        dv.project_out(ctx, dim, [X1, X2], C, Yc, norms2=nrm2)
+        want_y = y[:, :b] - np.hstack([a1, a2]) @ got
+        assert np.abs(dv.to_host(Yc) - want_y).max() <= 1e-12 * max(1.0, np.abs(want_y).max())
+        assert np.allclose(nrm2.cpu().numpy(), (want_y ** 2).sum(0), rtol=1e-10, atol=1e-20)
+    cm = rng.standard_normal((30, 15))
+    out = dv.new_block(dim, 15)
+    dv.ts_gemm(ctx, X2, dv.to_device_block(cm), out)
+    want = a2 @ cm
+    assert np.abs(dv.to_host(out) - want).max() <= 1e-13 * np.abs(want).max() * 4
+
+
+@pytest.mark.parametrize("dim", [50, 100003])
+@pytest.mark.parametrize("p", [1, 11, 24])
+def test_ritz_residual(dim, p, rng):
+    dv = _dev()
+    ctx = dv.context()
+    g = 35
+    v = rng.standard_normal((dim, g))
+    w = rng.standard_normal((dim, g))
+    yc = rng.standard_normal((g, p))
+    lam = rng.standard_normal(p)
+    V, W = dv.to_device_block(v), dv.to_device_block(w)
+    R, X, OX = dv.new_block(dim, p), dv.new_block(dim, p), dv.new_block(dim, p)
+    rn2 = torch.zeros(p, dtype=torch.float64, device=ctx.device)
+    dv.ritz_residual(ctx, V, W, dv.to_device_block(yc), torch.as_tensor(lam, device=ctx.device), R, X, OX, rn2)
+    x = v @ yc
+    ox = w @ yc
+    r = ox - x * lam
+    tol = 1e-13 * np.abs(ox).max() * 4
+    assert np.abs(dv.to_host(X) - x).max() <= tol
+    assert np.abs(dv.to_host(OX) - ox).max() <= tol
+    assert np.abs(dv.to_host(R) - r).max() <= tol * 4
+    assert np.allclose(rn2.cpu().numpy(), (r ** 2).sum(0), rtol=1e-12)
+
+
+def test_split_residual_matches_direct(rng):
+    dv = _dev()
+    ctx = dv.context()
+    n, m, p = 700, 1100, 3
+    x = rng.standard_normal((n + m, p))
+    x[:n] *= 0.8
+    lam = np.array([1.5, -0.7, 2.0])
+    r = rng.standard_normal((n + m, p)) * 1e-3
+    R, X = dv.to_device_block(r), dv.to_device_block(x)
+    lam_d = torch.as_tensor(lam, device=ctx.device)
+    st = torch.zeros(6 * p, dtype=torch.float64, device=ctx.device)
+    out = torch.zeros(p, dtype=torch.float64, device=ctx.device)
+    dv.split_stats(ctx, n, R, X, st)
+    dv.split_residual(ctx, n, R, X, lam_d, st, out)
+    bx = r + x * lam
+    for j in range(p):
+        nv, nu = np.linalg.norm(x[:n, j]), np.linalg.norm(x[n:, j])
+        sg = abs(lam[j])
+        e1 = bx[n:, j] / nv - sg * x[n:, j] / nu
+        e2 = bx[:n, j] / nu - sg * x[:n, j] / nv
+        want = e1 @ e1 + e2 @ e2
+        assert abs(out[j].item() - want) <= 1e-12 * max(want, 1e-300) + 1e-26
+        s = st[6 * j:6 * j + 6].cpu().numpy()
+        assert np.allclose(s[[2, 5]], [nv ** 2, nu ** 2], rtol=1e-13)
+
+
+# ------------------------------------------------------------ small dense
+
+@pytest.mark.parametrize("g", [1, 2, 3, 15, 35, 64])
+def test_syev_small(g, rng):
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    a = rng.standard_normal((g, g))
+    h = a + a.T
+    if g > 3:
+        h[0, 0] = h[1, 1]  # some structure
+    H = dv.to_device_block(h)
+    w = torch.zeros(g, dtype=torch.float64, device=ctx.device)
+    Y = dv.small_matrix(g, g)
+    ref_w, ref_v = np.linalg.eigh(h)
+    for order, expect in ((_lib.ORDER_ASC, np.arange(g)), (_lib.ORDER_DESC, np.argsort(-ref_w, kind="stable"))):
+        dv.syev_small(ctx, H, g, order, 0.0, w, Y)
+        got_w = w.cpu().numpy()
+        got_y = dv.to_host(Y)
+        assert np.abs(got_w - ref_w[expect]).max() <= 1e-13 * np.abs(ref_w).max() * g
+        assert np.abs(got_y.T @ got_y - np.eye(g)).max() <= 1e-13 * g
+        res = h @ got_y - got_y * got_w
+        assert np.abs(res).max() <= 1e-13 * np.abs(ref_w).max() * g
+    shift = float(np.median(ref_w)) + 1e-3
+    dv.syev_small(ctx, H, g, _lib.ORDER_INTERIOR, shift, w, Y)
+    below = ref_w < shift
+    key = np.where(below, shift - ref_w, ref_w - shift)
+    expect = np.lexsort((key, below.astype(np.int64)))
+    assert np.abs(w.cpu().numpy() - ref_w[expect]).max() <= 1e-13 * np.abs(ref_w).max() * g
+
+
+@pytest.mark.parametrize("g", [2, 9, 35])
+def test_refined_small(g, rng):
+    dv = _dev()
+    ctx = dv.context()
+    r = np.triu(rng.standard_normal((g, g)))
+    r[g - 1, g - 1] = 1e-9
+    h = rng.standard_normal((g, g))
+    h = h + h.T
+    y = torch.zeros(g, dtype=torch.float64, device=ctx.device)
+    lam = torch.zeros(1, dtype=torch.float64, device=ctx.device)
+    sv = torch.zeros(g, dtype=torch.float64, device=ctx.device)
+    dv.refined_small(ctx, dv.to_device_block(r), dv.to_device_block(h), g, y, lam, sv)
+    _, s, vt = np.linalg.svd(r)
+    yv = y.cpu().numpy()
+    assert abs(abs(yv @ vt[-1]) - 1.0) <= 1e-10
+    assert np.allclose(sv.cpu().numpy(), s, rtol=1e-12, atol=1e-14 * s[0])
+    assert abs(lam.item() - yv @ h @ yv) <= 1e-12 * np.abs(h).max() * g
+
+
+@pytest.mark.parametrize("g,s", [(5, 3), (35, 15), (20, 20)])
+def test_qr_small(g, s, rng):
+    dv = _dev()
+    ctx = dv.context()
+    r = np.triu(rng.standard_normal((g, g)))
+    yc, _ = np.linalg.qr(rng.standard_normal((g, s)))
+    qy = dv.small_matrix(g, s)
+    ry = dv.small_matrix(s, s)
+    dv.qr_small(ctx, dv.to_device_block(r), g, dv.to_device_block(yc), s, qy, ry)
+    qw, rw = np.linalg.qr(r @ yc)
+    sign = np.where(np.diag(rw) < 0.0, -1.0, 1.0)
+    qw, rw = qw * sign, rw * sign[:, None]
+    assert np.abs(dv.to_host(qy) - qw).max() <= 1e-12
+    assert np.abs(dv.to_host(ry) - rw).max() <= 1e-12 * np.abs(rw).max()
+
+
+def _coef_gs_ref(columns, limit, against):
+    kept = []
+    for col in columns:
+        if len(kept) >= limit:
+            break
+        c = np.array(col, dtype=np.float64, copy=True)
+        for _ in range(2):
+            for b in against:
+                c -= b * (b @ c)
+            for b in kept:
+                c -= b * (b @ c)
+        nrm = np.linalg.norm(c)
+        if nrm > 1e-8:
+            kept.append(c / nrm)
+    return kept
+
+
+def test_restart_coefs(rng):
+    dv = _dev()
+    ctx = dv.context()
+    g, gmax = 35, 35
+    h = rng.standard_normal((g, g))
+    _, y = np.linalg.eigh(h + h.T)
+    yfirst = rng.standard_normal(g)
+    yfirst /= np.linalg.norm(yfirst)
+    excl = y[:, 3].copy()
+    prev = rng.standard_normal((30, 1))
+    out = dv.small_matrix(g, g)
+    cnt = torch.zeros(1, dtype=torch.int32, device=ctx.device)
+    dv.restart_coefs(ctx, g, gmax, torch.as_tensor(yfirst, device=ctx.device), dv.to_device_block(y), g, 14,
+                     torch.as_tensor(excl, device=ctx.device), dv.to_device_block(prev), 1, 30, 1, out, cnt)
+    s = int(cnt.item())
+    sel = _coef_gs_ref([yfirst] + [y[:, j] for j in range(g)], 14, [excl])
+    padded = np.zeros(g)
+    padded[:30] = prev[:, 0]
+    plus = _coef_gs_ref([padded], 1, [excl] + sel)
+    want = np.array(sel + plus).T
+    assert s == want.shape[1] == 15
+    assert np.abs(dv.to_host(out)[:, :s] - want).max() <= 1e-12
+
+
+def test_launch_counter_moves():
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    before = _lib.launch_count()
+    x = dv.to_device_block(np.ones((10, 1)))
+    out = torch.zeros(1, dtype=torch.float64, device=ctx.device)
+    dv.col_norms2(ctx, x, out)
+    assert _lib.launch_count() == before + 1
+    assert out.item() == 10.0

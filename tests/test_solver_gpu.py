@@ -1,0 +1,140 @@
+"""End-to-end parity of the device PHSVDS solve against the reference's
+golden values (tests/golden/fixtures.json, solves.json) and host-side
+recomputed residuals (Eq. 7)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+from oracle import csr as ocsr
+from oracle import gen as ogen
+
+pytestmark = pytest.mark.gpu
+
+
+def _mat(m, n, rp, ci, va):
+    from paper_1607_01404_b200 import SparseMatrixCsr
+    return SparseMatrixCsr(m, n, rp, ci, va)
+
+
+def _host_r7(m, n, rp, ci, va, sigma, u, v):
+    out = []
+    for i in range(sigma.size):
+        av = ocsr.spmv(m, n, rp, ci, va, v[:, i])
+        atu = ocsr.spmv(m, n, rp, ci, va, u[:, i], transpose=True)
+        out.append(np.sqrt(np.linalg.norm(av - sigma[i] * u[:, i]) ** 2 +
+                           np.linalg.norm(atu - sigma[i] * v[:, i]) ** 2))
+    return np.array(out)
+
+
+def _angle(a, b):
+    """Largest principal angle between the column spans of a and b."""
+    qa, _ = np.linalg.qr(a)
+    qb, _ = np.linalg.qr(b)
+    s = np.linalg.svd(qa.T @ qb, compute_uv=False)
+    return float(np.arccos(min(1.0, s.min())))
+
+
+@pytest.mark.parametrize("seed", [1000, 1003, 1007, 1011, 1019])
+@pytest.mark.parametrize("target", ["largest", "smallest"])
+@pytest.mark.parametrize("eps", [1e-6, 1e-12])
+def test_sparse_oracle_criterion1(seed, target, eps):
+    """Criterion 1 (test_acceptance.py:66-97) on device."""
+    from paper_1607_01404_b200 import SvdsConfig, svds_solve
+    recs = {r["seed"]: r for r in load_golden("fixtures.json")["sparse_oracle.json"]}
+    rec = recs[seed]
+    m, n, rp, ci, va = ogen.build_sparse(seed)
+    a = _mat(m, n, rp, ci, va)
+    res = svds_solve(a, cfg=SvdsConfig(num_svals=5, target=target, eps=eps, seed=seed))
+    oracle = np.array(rec[target + "5"])
+    a_norm = rec["sigma_max"]
+    assert res.converged.all(), (res.rnorms, res.status)
+    assert np.abs(res.sigma - oracle).max() <= a_norm * eps * 10
+    r7 = _host_r7(m, n, rp, ci, va, res.sigma, res.u, res.v)
+    assert r7.max() < a_norm * eps
+
+
+def test_clustered_engages_stage2():
+    """Five clustered smallest values at 1e-12 need stage 2
+    (test_hybrid.py:64-80)."""
+    from paper_1607_01404_b200 import SvdsConfig, svds_solve
+    fx = load_golden("fixtures.json")["clustered300x200.json"]
+    m, n, rp, ci, va = ogen.build_clustered()
+    a = _mat(m, n, rp, ci, va)
+    res = svds_solve(a, cfg=SvdsConfig(num_svals=5, target="smallest", eps=1e-12, seed=0))
+    assert res.stats.stage2_matvecs > 0
+    assert res.converged.all(), (res.rnorms, res.status)
+    oracle = np.array(fx["smallest5"])
+    assert np.abs(res.sigma - oracle).max() <= fx["sigma_max"] * 1e-12 * 10
+    r7 = _host_r7(m, n, rp, ci, va, res.sigma, res.u, res.v)
+    assert r7.max() < fx["sigma_max"] * 1e-12
+
+
+@pytest.mark.parametrize("target", ["smallest", "largest"])
+def test_criterion2_synth_tight(target):
+    from paper_1607_01404_b200 import SvdsConfig, svds_solve
+    sigma = np.geomspace(1e-3, 1.0, 60)[::-1].copy()
+    m, n = 90, 60
+    rp, ci, va = ogen.synth_csr(sigma, m, n, 2200)
+    a = _mat(m, n, rp, ci, va)
+    res = svds_solve(a, cfg=SvdsConfig(num_svals=5, target=target, eps=1e-12, seed=2200))
+    want = np.sort(sigma)[:5] if target == "smallest" else np.sort(sigma)[::-1][:5]
+    assert res.converged.all()
+    assert np.abs(res.sigma - want).max() <= 1e-11
+    r7 = _host_r7(m, n, rp, ci, va, res.sigma, res.u, res.v)
+    assert r7.max() < 1e-12
+
+
+def test_config1_full_against_reference():
+    """BASELINE config 1 (64x64 conv-diff, k=10 largest, tol 1e-10) against
+    the reference's own solve (solves.json)."""
+    from paper_1607_01404_b200 import SvdsConfig, svds_solve, workloads
+    gold = load_golden("solves.json")["c1"]
+    m, n, r, c, v = workloads.c1_coo()
+    rp, ci, va = ocsr.csr_from_coo(m, n, r, c, v)
+    a = _mat(m, n, rp, ci, va)
+    res = svds_solve(a, cfg=SvdsConfig(num_svals=10, target="largest", eps=1e-10, seed=0))
+    want = np.array(gold["sigma"])
+    smax = want[0]
+    assert res.converged.all()
+    assert np.abs(res.sigma - want).max() <= max(1e-10 * smax, 1e-10 * smax)
+    r7 = _host_r7(m, n, rp, ci, va, res.sigma, res.u, res.v)
+    assert r7.max() <= 1e-10 * smax
+    # matvec count tracks the reference's trajectory
+    assert abs(res.stats.stage1_matvecs - gold["stage1_matvecs"]) <= 0.25 * gold["stage1_matvecs"]
+
+
+def test_pysvds_dense_and_coo():
+    from paper_1607_01404_b200.pysvds import PySvdsError, svds
+    sigma, u, v, rnorms, stats = svds(np.diag([1.0, 2.0, 3.0]), k=1, which="S")
+    assert abs(sigma[0] - 1.0) < 1e-12 and rnorms[0] < 1e-11
+    assert stats["converged"] == [True] and stats["status"] == "ok"
+    m, n, rp, ci, va = ogen.build_rect50x30()
+    rows = np.repeat(np.arange(m), np.diff(rp))
+    fx = load_golden("fixtures.json")["rect50x30_expected.json"]
+    s5 = svds((rows, ci, va, (m, n)), k=5, which="L", tol=1e-10)[0]
+    assert np.abs(s5 - np.array(fx["largest5"])).max() <= 1e-9
+    with pytest.raises(PySvdsError):
+        svds(np.eye(3), k=1, which="X")
+    with pytest.raises(PySvdsError):
+        svds(np.eye(3), k=1, eps=1e-3)
+
+
+def test_eig_solve_diag_largest_and_locking():
+    from paper_1607_01404_b200 import EigConfig, LinearOperator, eig_solve
+    d = torch.arange(1.0, 41.0, dtype=torch.float64, device="cuda")
+
+    def diag_op(vals):
+        return LinearOperator(vals.numel(), lambda x: vals[:, None] * x, device=True)
+
+    res = eig_solve(diag_op(d), EigConfig(num_evals=2, target="largest_algebraic", max_basis_size=10,
+                                          min_restart_size=4,
+                                          convergence_test=lambda lam, rn, x, ox, c: rn <= 1e-10, seed=1))
+    assert np.allclose(res.eigenvalues, [40.0, 39.0], atol=1e-9)
+    assert res.converged.all()
+    res = eig_solve(diag_op(d), EigConfig(num_evals=3, target="smallest_algebraic", locking=True, max_basis_size=8,
+                                          min_restart_size=3,
+                                          convergence_test=lambda lam, rn, x, ox, c: rn <= 1e-10, seed=7))
+    assert res.converged.all()
+    assert np.allclose(res.eigenvalues, [1.0, 2.0, 3.0], atol=1e-8)
