@@ -1,0 +1,341 @@
+"""Benchmark: time-to-k-triplets of the device PHSVDS solve on BASELINE
+config 2 (200,000 x 100,000 random sparse, 8 N(0,1) per row + unit
+diagonal, k=5 smallest, tol 1e-10, point-Jacobi preconditioner).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2]
+
+One "step" is one full svds_solve (both stages as needed) with the matrix
+and preconditioner already resident in HBM; value = mean seconds per solve
+(max over ranks; lower is better).  ``e2e`` is the same solve through the
+reference-facing binding (pysvds.svds) from host COO arrays, host->device
+and device->host copies included.  ``roofline`` is the CSR SpMV kernel
+(A x and A^T y), timed with CUDA events on the launching stream around
+every SpMV launch inside the timed region.  ``cpu_baseline`` is the CPU
+oracle port (oracle/phsvds.py, bit-identical to the reference) on a
+bounded sample of the same workload.
+
+With --gpus N > 1 (torchrun) each rank solves its own replica; see
+DESIGN.md for the row-sharded path.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "time-to-k-triplets"
+UNIT = "s"
+PEAKS_FILE = os.path.join(REPO, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+REF_SAMPLE_MATVECS = 150     # budget of one bounded reference step
+CPU_BASELINE_MATVECS = 300   # budget of the cpu_baseline sample
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(key):
+    from paper_1607_01404_b200 import workloads
+    wl = workloads.CONFIGS[key]
+    return wl, wl.build()
+
+
+def config_json(wl, m, n, nnz, world):
+    return {"workload": "BASELINE config %s: %s" % (wl.name[1], wl.note), "m": m, "n": n, "nnz": nnz,
+            "k": wl.k, "which": wl.which, "tol": wl.tol, "block": wl.block,
+            "precond": "jacobi" if wl.precond else None, "seed_matrix": int(wl.name[1]), "seed_solver": 0,
+            "parallelism": "replicas%d" % world if world > 1 else "single",
+            "l2": "flushed before every timed step (256 MiB write); working set (~60 MB) is L2-resident "
+                  "within a solve"}
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- our arm
+
+def spmv_bytes(m, n, nnz, b, transpose):
+    """Algorithmic bytes of one CSR SpMV launch: values +
+    int32 indices + row pointers + gathered x + written y."""
+    rows = n if transpose else m
+    return 12 * nnz + 4 * (rows + 1) + 8 * b * (m + n)
+
+
+def peak_hbm():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_1607_01404_b200 import (SparseMatrixCsr, SvdsConfig, _lib, jacobi_precond_on_normal, matrix,
+                                       svds_solve)
+    from paper_1607_01404_b200 import pysvds
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    wl, (m, n, r, c, v) = workload(args.config)
+    a = SparseMatrixCsr.from_coo(m, n, r, c, v)
+    pre = jacobi_precond_on_normal(a, side="auto") if wl.precond else None
+    cfg = lambda: SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0)  # noqa
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        res = svds_solve(a, precond=pre, cfg=cfg(), return_device=True)
+    step_ms = []
+    prof_all = []
+    launches0 = _lib.launch_count()
+    res = None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            barrier()
+            prof = []
+            matrix.SPMV_PROFILER = prof
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            res = svds_solve(a, precond=pre, cfg=cfg(), return_device=True)
+            e1.record()
+            matrix.SPMV_PROFILER = None
+            barrier()
+            step_ms.append(e0.elapsed_time(e1))
+            prof_all.append(prof)
+    launches = _lib.launch_count() - launches0
+    local_mean = float(np.mean(step_ms))
+    t = torch.tensor([local_mean], dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # SpMV roofline from the events recorded around every launch
+    fwd, adj = [], []
+    for prof in prof_all:
+        for tr, b, s0, s1 in prof:
+            (adj if tr else fwd).append((b, s0.elapsed_time(s1)))
+    nnz = a.nnz
+    tot_bytes = sum(spmv_bytes(m, n, nnz, b, False) for b, _ in fwd) + \
+        sum(spmv_bytes(m, n, nnz, b, True) for b, _ in adj)
+    tot_ms = sum(t for _, t in fwd) + sum(t for _, t in adj)
+    nl = len(fwd) + len(adj)
+    peak, peak_kind = peak_hbm()
+    achieved = (tot_bytes / nl) / (tot_ms / nl * 1e-3) / 1e9 if nl else 0.0
+    spmv_share = tot_ms / float(np.sum(step_ms)) if step_ms else 0.0
+    traffic = None
+    tf = os.path.join(REPO, "profiles", "spmv_traffic_%s.json" % args.config)
+    if os.path.exists(tf):
+        with open(tf) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator of BASELINE config %s)" %
+        wl.name[1], "config": config_json(wl, m, n, nnz, world),
+        "result": {"sigma": [float(s) for s in res.sigma], "rnorms_max": float(res.rnorms.max()),
+                   "converged": bool(res.converged.all()), "status": res.status,
+                   "stage1_matvecs": res.stats.stage1_matvecs, "stage2_matvecs": res.stats.stage2_matvecs,
+                   "outer_iterations": res.stats.outer_iterations, "host_syncs": res.stats.syncs},
+        "roofline": {"kernel": "csr_tile_kernel (SpMV A x / A^T y, b=%d)" % wl.block, "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": tot_bytes / nl if nl else None,
+                     "avg_launch_us": tot_ms / nl * 1e3 if nl else None, "launches_timed": nl,
+                     "share_of_step": spmv_share,
+                     "note": "CSR of config 2 (~20 MB) stays L2-resident within a solve, so this kernel is "
+                             "L2-fed after the first touch"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+
+    if not args.no_e2e:
+        line["e2e"] = e2e(args, wl, m, n, r, c, v, pysvds, barrier)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(wl, m, n, r, c, v, res.stats.stage1_matvecs + res.stats.stage2_matvecs,
+                                            CPU_BASELINE_MATVECS)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def e2e(args, wl, m, n, r, c, v, pysvds, barrier):
+    """Same solve through the reference-facing binding from host COO:
+    pysvds.svds((rows, cols, vals, shape), ...) with the Jacobi
+    preconditioner; host->device copy of the triplets, device CSR assembly,
+    the solve and the device->host read of (sigma, u, v, rnorms) inside the
+    timed region."""
+    import torch
+    from paper_1607_01404_b200 import SparseMatrixCsr, jacobi_precond_on_normal
+    rows_p = torch.from_numpy(r).pin_memory()
+    cols_p = torch.from_numpy(c).pin_memory()
+    vals_p = torch.from_numpy(v).pin_memory()
+    times = []
+    h2d = int(r.nbytes + c.nbytes + v.nbytes)
+    d2h = 0
+    for i in range(args.steps + 1):
+        barrier()
+        t0 = time.perf_counter()
+        a = SparseMatrixCsr.from_coo(m, n, rows_p, cols_p, vals_p)
+        pre = jacobi_precond_on_normal(a, side="auto") if wl.precond else None
+        sigma, u, vv, rn, stats = pysvds.svds(a, k=wl.k, which="S" if wl.which == "smallest" else "L",
+                                              tol=wl.tol, seed=0, precond=pre, max_block_size=wl.block)
+        barrier()
+        dt = time.perf_counter() - t0
+        d2h = int(sigma.nbytes + u.nbytes + vv.nbytes + rn.nbytes)
+        if i > 0:  # first call warms allocator / CUB temp buffers
+            times.append(dt)
+    return {"value": float(np.mean(times)), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": "paper_1607_01404_b200.pysvds.svds(SparseMatrixCsr.from_coo(host COO), precond=jacobi)",
+            "steps": len(times)}
+
+
+# ----------------------------------------------------------- CPU oracle
+
+def _oracle_solve(wl, m, n, r, c, v, budget):
+    from oracle import csr as ocsr
+    from oracle import phsvds
+    rp, ci, va = ocsr.csr_from_coo(m, n, r, c, v)
+    mat = phsvds.Csr(m, n, rp, ci, va)
+    pre = phsvds.Jacobi(mat, "auto") if wl.precond else None
+    t0 = time.perf_counter()
+    out = phsvds.svds(mat, wl.k, wl.which, wl.tol, seed=0, block=wl.block, precond=pre, max_matvecs=budget)
+    return time.perf_counter() - t0, out
+
+
+def cpu_baseline(wl, m, n, r, c, v, full_matvecs, budget):
+    sec, out = _oracle_solve(wl, m, n, r, c, v, budget)
+    used = out["stage1_matvecs"] + out["stage2_matvecs"]
+    return {"value": sec * full_matvecs / used, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": "oracle/phsvds.py (bit-identical restatement of the reference) on the full config-%s matrix "
+                      "with max_matvecs=%d: %.2f s for %d matvecs, scaled to the %d matvecs of the full solve "
+                      "(single-threaded NumPy SpMV, OpenBLAS on up to %d threads for dense ops)"
+                      % (wl.name[1], budget, sec, used, full_matvecs, os.cpu_count())}
+
+
+FULL_MATVECS = {"c2": 950, "c1": 1792}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (the oracle port)
+    on the host cores, rank 0 only, each step a bounded sample."""
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    wl, (m, n, r, c, v) = workload(args.config)
+    full = FULL_MATVECS.get(args.config)
+    vals = []
+    samples = []
+    for i in range(args.warmup + args.steps):
+        sec, out = _oracle_solve(wl, m, n, r, c, v, REF_SAMPLE_MATVECS)
+        used = out["stage1_matvecs"] + out["stage2_matvecs"]
+        est = sec * (full if full else used) / used
+        if i >= args.warmup:
+            vals.append(est)
+            samples.append((sec, used))
+    value = float(np.mean(vals))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator of BASELINE config %s)"
+            % wl.name[1], "config": config_json(wl, m, n, len(v), 1), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": "each step: oracle/phsvds.py on the full matrix with max_matvecs=%d "
+                                       "(mean %.2f s for %d matvecs), scaled to the full solve's %s matvecs"
+                                       % (REF_SAMPLE_MATVECS, float(np.mean([s for s, _ in samples])),
+                                          samples[0][1], full)},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

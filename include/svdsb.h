@@ -219,6 +219,17 @@ int svdsb_split_residual(svdsb_ctx *ctx, int64_t dim, int64_t nsplit,
 int svdsb_syev_small(int g, const double *h, int64_t ldh, int order,
                      double shift, double *w, double *y, int64_t ldy,
                      void *stream);
+/* Warm-started version of svdsb_syev_small for a projection that grew by b
+ * bordering rows/columns: given H[:g0,:g0] = Y0 diag(l0) Y0^T (y0 g0 x g0,
+ * l0 g0; y0 == NULL means Y0 = I and l0 = diag(H), the state right after a
+ * thick restart that kept Ritz vectors), returns the eigendecomposition of
+ * H[:g0+b,:g0+b] ordered like svdsb_syev_small.  Each border is absorbed as
+ * an arrowhead matrix through its secular equation (deflation + Gu-Eisenstat
+ * couplings), O(g^2) per border.  y / w may alias y0 / l0. */
+int svdsb_syev_update(int g0, int b, const double *h, int64_t ldh,
+                      const double *y0, int64_t ldy0, const double *l0,
+                      int order, double shift, double *w, double *y,
+                      int64_t ldy, void *stream);
 /* Refined extraction (eigensolver.py:369-380): y = right singular vector
  * of the smallest singular value of the g x g matrix R (ldr), lam = y^T H y.
  * One-sided Jacobi SVD.  sv (optional, g) receives singular values desc. */

@@ -52,7 +52,8 @@ _PROTOS = [
     ("svdsb_split_stats", i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp]),
     ("svdsb_split_residual", i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp, vp, vp]),
     ("svdsb_syev_small", i32, [i32, vp, i64, i32, f64, vp, vp, i64, vp]),
-    ("svdsb_refined_small", i32, [i32, vp, i64, vp, i64, vp, vp, vp, vp]),
+    ("svdsb_syev_update", i32, [i32, i32, vp, i64, vp, i64, vp, i32, f64, vp, vp, i64, vp]),
+    ("svdsb_refined_small",i32, [i32, vp, i64, vp, i64, vp, vp, vp, vp]),
     ("svdsb_restart_coefs", i32, [i32, i32, vp, vp, i64, i32, i32, vp, vp, i64, i32, i32, i32, vp, i64,
                                   vp, vp]),
     ("svdsb_project_small", i32, [i32, i32, vp, i64, vp, i64, vp, i64, vp]),

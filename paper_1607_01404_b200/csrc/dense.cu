@@ -21,8 +21,8 @@ namespace svdsb {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxCtas = 4 * kNumSMs;
-constexpr int kMinRowsPerCta = 1024;
+constexpr int kMaxCtas = 8 * kNumSMs;
+constexpr int kMinRowsPerCta = 256;
 
 struct ColSet {
   const double *base[SVDSB_MAX_BLOCKS];

@@ -227,6 +227,11 @@ def syev_small(ctx, h, g, order, shift, w, y):
          ctx.stream)
 
 
+def syev_update(ctx, h, g0, b, y0, l0, order, shift, w, y):
+    call("svdsb_syev_update", int(g0), int(b), P(h), ld_of(h), P(y0), ld_of(y0) if y0 is not None else 1,
+         P(l0), int(order), float(shift), P(w), P(y), ld_of(y), ctx.stream)
+
+
 def refined_small(ctx, r, h, g, y, lam, sv=None):
     call("svdsb_refined_small", int(g), P(r), ld_of(r), P(h), ld_of(h), P(y), P(lam), P(sv),
          ctx.stream)

@@ -311,6 +311,8 @@ class DavidsonSolver:
         self.collapse_streak = 0
         self._slot_progress = {}
         self._finished = self.wanted == 0
+        self._warm = None           # (kind, g0) of the last known decomposition of H
+        self.warm_start = True
 
         need_v1, split1 = _test_needs(cfg.convergence_test)
         need_v2, split2 = _test_needs(cfg.practical_test)
@@ -456,6 +458,7 @@ class DavidsonSolver:
     def _update_h_full(self):
         """H = sym(V^T W) (eigensolver.py:349-352)."""
         g = self.g
+        self._warm = None
         if g == 0:
             return
         dv.gram(self.ctx, self.n, [self.v[:, :g]], self.w[:, :g], self._hg[:g, :g])
@@ -537,10 +540,23 @@ class DavidsonSolver:
 
     # ---------------------------------------------------------- extraction
     def extract_rayleigh_ritz(self):
-        """Ritz values/vectors of H[:g,:g] in target order (device)."""
+        """Ritz values/vectors of H[:g,:g] in target order (device).
+
+        Warm path: when H only grew by bordering columns since the last
+        extraction (or since a Ritz-vector restart left it diagonal), the
+        new decomposition is an O(g^2) secular-equation update of the known
+        one; otherwise a cold Jacobi solve."""
         order, shift = self._order_mode()
         g = self.g
-        dv.syev_small(self.ctx, self.h[:g, :g], g, order, shift, self.lams_d[:g], self.y_d[:g, :g])
+        warm = self._warm if self.warm_start else None
+        if warm is not None and 0 < g - warm[1] <= 8:
+            kind, g0 = warm
+            y0 = self.y_d[:g0, :g0] if kind == "prev" else None
+            l0 = self.lams_d[:g0] if kind == "prev" else None
+            dv.syev_update(self.ctx, self.h, g0, g - g0, y0, l0, order, shift, self.lams_d[:g], self.y_d[:g, :g])
+        else:
+            dv.syev_small(self.ctx, self.h[:g, :g], g, order, shift, self.lams_d[:g], self.y_d[:g, :g])
+        self._warm = ("prev", g)
         return self.lams_d[:g], self.y_d[:g, :g]
 
     def _candidates(self, y, lam, p, need_x, need_ox):
@@ -665,6 +681,11 @@ class DavidsonSolver:
             return self.g
         self._swap_basis(s)
         dv.project_small(self.ctx, self.h[:g, :g], g, self.coefs[:g, :s], s, self.h[:s, :s])
+        # Kept Ritz vectors plus a +k direction orthogonal to them make
+        # C^T H C diagonal (to rounding): the next extraction starts from
+        # (diag(H), I).  A refined head vector or an excluded direction breaks
+        # that, so those restarts fall back to a cold solve.
+        self._warm = ("diag", s) if (y_first is None and exclude is None) else None
         if self.q is not None:
             dv.qr_small(self.ctx, self.rfac[:g, :g], g, self.coefs[:g, :s], s, self._qy[:g, :s],
                         self._ry[:s, :s])

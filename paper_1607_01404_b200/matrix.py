@@ -18,6 +18,10 @@ import torch
 from . import _lib
 from .device import context, require_cuda
 
+# When set to a list, every SpMV appends (transpose, block, start_event,
+# end_event) recorded on the launching stream (bench.py's roofline probe).
+SPMV_PROFILER = None
+
 
 class DeviceCsr:
     """Owning handle to a libsvdsb CSR (A and A^T) on one device."""
@@ -90,8 +94,16 @@ class DeviceCsr:
         matrixMatvec)."""
         from .device import P, ld_of, as_block
         x, y = as_block(x), as_block(y)
+        prof = SPMV_PROFILER
+        if prof is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
         _lib.call("svdsb_matvec", self.ctx.handle, self.handle, int(bool(transpose)), P(x), ld_of(x),
                   P(y), ld_of(y), x.shape[1], self.ctx.stream)
+        if prof is not None:
+            e1.record()
+            prof.append((bool(transpose), int(x.shape[1]), e0, e1))
 
     def precond_diag(self, side, out):
         from .device import P

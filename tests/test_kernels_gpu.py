@@ -363,3 +363,44 @@ def test_launch_counter_moves():
     dv.col_norms2(ctx, x, out)
     assert _lib.launch_count() == before + 1
     assert out.item() == 10.0
+
+
+@pytest.mark.parametrize("g0,b", [(0, 1), (1, 1), (14, 1), (34, 1), (20, 4), (30, 5), (60, 4)])
+@pytest.mark.parametrize("kind", ["prev", "diag", "degenerate"])
+def test_syev_update_matches_eigh(g0, b, kind, rng):
+    """Warm arrowhead update of a bordered projection vs LAPACK."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    g = g0 + b
+    a = rng.standard_normal((g, g))
+    h = a + a.T
+    if kind == "degenerate" and g0 >= 4:
+        # repeated leading eigenvalues and an (almost) decoupled direction
+        w0, q0 = np.linalg.eigh(h[:g0, :g0])
+        w0[1] = w0[0]
+        w0[3] = w0[2] + 1e-17
+        h[:g0, :g0] = (q0 * w0) @ q0.T
+        h[:g0, g0] = q0[:, 0] * 1e-20 + h[:g0, g0] * (np.arange(g0) % 2)
+        h[g0, :g0] = h[:g0, g0]
+    if kind == "diag":
+        h[:g0, :g0] = np.diag(np.sort(rng.standard_normal(g0)))
+    H = dv.to_device_block(h)
+    w = torch.zeros(g, dtype=torch.float64, device=ctx.device)
+    Y = dv.small_matrix(g, g)
+    if kind == "diag" or g0 == 0:
+        y0 = l0 = None
+    else:
+        l0h, y0h = np.linalg.eigh(h[:g0, :g0])
+        y0 = dv.to_device_block(y0h)
+        l0 = torch.as_tensor(l0h, device=ctx.device)
+    ref_w = np.linalg.eigh(h)[0]
+    scale = max(1.0, np.abs(ref_w).max())
+    for order in (_lib.ORDER_ASC, _lib.ORDER_DESC):
+        dv.syev_update(ctx, H, g0, b, y0, l0, order, 0.0, w, Y)
+        got_w = w.cpu().numpy()
+        got_y = dv.to_host(Y)
+        exp = ref_w if order == _lib.ORDER_ASC else ref_w[::-1]
+        assert np.abs(got_w - exp).max() <= 1e-13 * scale * g
+        assert np.abs(got_y.T @ got_y - np.eye(g)).max() <= 1e-13 * g
+        assert np.abs(h @ got_y - got_y * got_w).max() <= 1e-13 * scale * g

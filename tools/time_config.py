@@ -1,0 +1,27 @@
+"""Time one config solve on the GPU (development helper)."""
+import sys, time, json
+import numpy as np, torch
+sys.path.insert(0, '.')
+from paper_1607_01404_b200 import SparseMatrixCsr, SvdsConfig, svds_solve, jacobi_precond_on_normal, workloads, _lib
+
+key = sys.argv[1]
+small = len(sys.argv) > 2 and sys.argv[2] == 'small'
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+wl = workloads.CONFIGS[key]
+t0 = time.perf_counter()
+m, n, r, c, v = wl.build(**(workloads.SMALL[key] if small else {}))
+t1 = time.perf_counter()
+a = SparseMatrixCsr.from_coo(m, n, r, c, v)
+torch.cuda.synchronize(); t2 = time.perf_counter()
+print(f"{key} m={m} n={n} nnz={a.nnz} gen {t1-t0:.2f}s build {t2-t1:.2f}s", flush=True)
+for rep in range(reps):
+    pre = jacobi_precond_on_normal(a, side='auto') if wl.precond else None
+    cfg = SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0)
+    l0 = _lib.launch_count()
+    torch.cuda.synchronize(); t = time.perf_counter()
+    res = svds_solve(a, precond=pre, cfg=cfg, return_device=True)
+    torch.cuda.synchronize(); dt = time.perf_counter() - t
+    s = res.stats
+    print(json.dumps({"rep": rep, "sec": round(dt, 4), "sigma": res.sigma.tolist(), "rnorms_max": float(res.rnorms.max()),
+        "conv": bool(res.converged.all()), "status": res.status, "mv1": s.stage1_matvecs, "mv2": s.stage2_matvecs,
+        "restarts": s.restarts, "iters": s.outer_iterations, "syncs": s.syncs, "launches": _lib.launch_count() - l0}), flush=True)
