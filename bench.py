@@ -190,15 +190,18 @@ def run_ours(args):
     ms = float(t.item())
 
     # SpMV roofline from the events recorded around every launch
-    fwd, adj = [], []
+    tot_bytes, tot_ms, nl = 0.0, 0.0, 0
     for prof in prof_all:
-        for tr, b, s0, s1 in prof:
-            (adj if tr else fwd).append((b, s0.elapsed_time(s1)))
+        for kind, b, s0, s1 in prof:
+            if kind == "normal":
+                byt = spmv_bytes(m, n, a.nnz, b, False) + spmv_bytes(m, n, a.nnz, b, True)
+                nl += 2
+            else:
+                byt = spmv_bytes(m, n, a.nnz, b, kind == "adj")
+                nl += 1
+            tot_bytes += byt
+            tot_ms += s0.elapsed_time(s1)
     nnz = a.nnz
-    tot_bytes = sum(spmv_bytes(m, n, nnz, b, False) for b, _ in fwd) + \
-        sum(spmv_bytes(m, n, nnz, b, True) for b, _ in adj)
-    tot_ms = sum(t for _, t in fwd) + sum(t for _, t in adj)
-    nl = len(fwd) + len(adj)
     peak, peak_kind = peak_hbm()
     achieved = (tot_bytes / nl) / (tot_ms / nl * 1e-3) / 1e9 if nl else 0.0
     spmv_share = tot_ms / float(np.sum(step_ms)) if step_ms else 0.0

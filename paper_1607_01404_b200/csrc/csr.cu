@@ -41,6 +41,7 @@ struct CsrPart {
   // short-row tiles: [tile_r0[i], tile_r1[i])
   int ntile = 0;
   int *tile_r = nullptr;    // 2*ntile
+  int4 *tile_info = nullptr;  // ntile x {r0, r1, nz0, nz1}
   // long rows, split in chunks
   int nlong = 0;
   int *long_row = nullptr;  // nlong
@@ -59,6 +60,10 @@ struct svdsb_csr {
   int device;
   svdsb::CsrPart a, at;
   bool has_t;
+  // row-major staging for block products (2 <= b <= 4): packed input and
+  // the inner product of the normal operator; grown on demand
+  double *scratch[2] = {nullptr, nullptr};
+  size_t scratch_cap[2] = {0, 0};
 };
 
 namespace svdsb {
@@ -95,13 +100,23 @@ __device__ double np_pairwise(const double *a, int n) {
   }
 }
 
+// Out-of-line copy for the rare long tails (>= 8 terms) so the common fold
+// stays register-light.
+__device__ __noinline__ double np_pairwise_long(const double *a, int n) { return np_pairwise(a, n); }
+
 // ORDER 0: forward (reduceat) ; ORDER 1: sequential (add.at)
 template <int ORDER>
 __device__ __forceinline__ double fold_row(const double *p, int len) {
   if (ORDER == 0) {
     if (len == 0) return 0.0;
-    if (len == 1) return p[0];
-    return dadd(p[0], np_pairwise(p + 1, len - 1));
+    double s = p[0];
+    if (len == 1) return s;
+    if (len <= 8) {  // tail < 8 terms: numpy sums them left to right from 0
+      double r = 0.0;
+      for (int i = 1; i < len; ++i) r = dadd(r, p[i]);
+      return dadd(s, r);
+    }
+    return dadd(s, np_pairwise_long(p + 1, len - 1));
   } else {
     double s = 0.0;
     for (int i = 0; i < len; ++i) s = dadd(s, p[i]);
@@ -109,8 +124,21 @@ __device__ __forceinline__ double fold_row(const double *p, int len) {
   }
 }
 
-template <int ORDER>
-__global__ void __launch_bounds__(kTileThreads)
+__device__ __forceinline__ double ld_stream(const double *p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_stream(const int *p) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// XROW: x is row-major with row stride b (one 8*b-byte gather per nonzero);
+// otherwise column-major with leading dimension ldx.  YROW likewise for y.
+template <int ORDER, int XROW, int YROW, int BMAX>
+__global__ void __launch_bounds__(kTileThreads, 3)
 csr_tile_kernel(const int *__restrict__ tile_r, const int *__restrict__ row_ptr,
                 const int *__restrict__ col, const double *__restrict__ val,
                 const double *__restrict__ x, int64_t ldx, double *__restrict__ y,
@@ -129,8 +157,8 @@ csr_tile_kernel(const int *__restrict__ tile_r, const int *__restrict__ row_ptr,
   for (int i = 0; i < kPerThread; ++i) {
     int k = t + i * kTileThreads;
     if (k < nnz) {
-      v[i] = __ldg(val + nz0 + k);
-      c[i] = __ldg(col + nz0 + k);
+      v[i] = ld_stream(val + nz0 + k);
+      c[i] = ld_stream(col + nz0 + k);
     } else {
       v[i] = 0.0;
       c[i] = 0;
@@ -141,53 +169,358 @@ csr_tile_kernel(const int *__restrict__ tile_r, const int *__restrict__ row_ptr,
     my0 = rp[t] - nz0;
     mylen = rp[t + 1] - rp[t];
   }
-  for (int cc = 0; cc < b; ++cc) {
-    const double *xc = x + cc * ldx;
+  if (XROW) {
+    // gather whole x rows (b <= BMAX doubles) once per nonzero
+    double xv[kPerThread][BMAX];
 #pragma unroll
     for (int i = 0; i < kPerThread; ++i) {
       int k = t + i * kTileThreads;
-      if (k < nnz) prod[k] = dmul(v[i], __ldg(xc + c[i]));
+#pragma unroll
+      for (int cc = 0; cc < BMAX; ++cc) xv[i][cc] = (k < nnz && cc < b) ? __ldg(x + (int64_t)c[i] * b + cc) : 0.0;
     }
-    __syncthreads();
-    if (t < nrows) y[(int64_t)(r0 + t) + cc * ldy] = fold_row<ORDER>(prod + my0, mylen);
-    __syncthreads();
+#pragma unroll
+    for (int cc = 0; cc < BMAX; ++cc) {
+      if (cc >= b) break;
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) {
+        int k = t + i * kTileThreads;
+        if (k < nnz) prod[k] = dmul(v[i], xv[i][cc]);
+      }
+      __syncthreads();
+      if (t < nrows) {
+        double s = fold_row<ORDER>(prod + my0, mylen);
+        if (YROW)
+          y[(int64_t)(r0 + t) * b + cc] = s;
+        else
+          y[(int64_t)(r0 + t) + cc * ldy] = s;
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int cc = 0; cc < b; ++cc) {
+      const double *xc = x + cc * ldx;
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) {
+        int k = t + i * kTileThreads;
+        if (k < nnz) prod[k] = dmul(v[i], __ldg(xc + c[i]));
+      }
+      __syncthreads();
+      if (t < nrows) {
+        double s = fold_row<ORDER>(prod + my0, mylen);
+        if (YROW)
+          y[(int64_t)(r0 + t) * b + cc] = s;
+        else
+          y[(int64_t)(r0 + t) + cc * ldy] = s;
+      }
+      __syncthreads();
+    }
   }
 }
 
-// One CTA per chunk of a long row: partial sums of b columns.
+// Persistent, software-pipelined b = 1 variant: while a CTA gathers and
+// folds tile t, the value / index / row-pointer loads of its next tile are
+// already in flight; products are double-buffered in shared memory so one
+// barrier per tile suffices.  Same per-row summation order as above.
+template <int ORDER>
+__global__ void __launch_bounds__(kTileThreads, 3)
+csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__restrict__ row_ptr,
+                     const int *__restrict__ col, const double *__restrict__ val, const double *__restrict__ x,
+                     double *__restrict__ y) {
+  __shared__ double prod[2][kTileNnz];
+  __shared__ int rps[2][kTileRows + 1];
+  const int t = threadIdx.x;
+  int tile = blockIdx.x;
+  if (tile >= ntile) return;
+  // stage A: loads for `tile`
+  int4 cur = info[tile];
+  double v[kPerThread];
+  int c[kPerThread];
+  int rpa, rpb;
+  auto issue = [&](const int4 &ti, double (&vv)[kPerThread], int (&cc)[kPerThread], int &ra, int &rb) {
+    const int nnz = ti.w - ti.z, nrows = ti.y - ti.x;
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) {
+      int k = t + i * kTileThreads;
+      if (k < nnz) {
+        vv[i] = ld_stream(val + ti.z + k);
+        cc[i] = ld_stream(col + ti.z + k);
+      } else {
+        vv[i] = 0.0;
+        cc[i] = 0;
+      }
+    }
+    ra = (t <= nrows) ? __ldg(row_ptr + ti.x + t) : 0;
+    rb = (t == 0 && nrows >= kTileThreads) ? __ldg(row_ptr + ti.x + kTileThreads) : 0;
+  };
+  issue(cur, v, c, rpa, rpb);
+  int buf = 0;
+  while (true) {
+    const int next_tile = tile + gridDim.x;
+    int4 nxt = make_int4(0, 0, 0, 0);
+    double vn[kPerThread];
+    int cn[kPerThread];
+    int rna = 0, rnb = 0;
+    if (next_tile < ntile) {
+      nxt = info[next_tile];
+      issue(nxt, vn, cn, rna, rnb);
+    }
+    // gather + products of the current tile
+    const int nnz = cur.w - cur.z, nrows = cur.y - cur.x;
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) {
+      int k = t + i * kTileThreads;
+      if (k < nnz) prod[buf][k] = dmul(v[i], __ldg(x + c[i]));
+    }
+    if (t <= nrows) rps[buf][t] = rpa;
+    if (t == 0 && nrows >= kTileThreads) rps[buf][kTileThreads] = rpb;
+    __syncthreads();
+    if (t < nrows) {
+      const int s0 = rps[buf][t] - cur.z;
+      const int len = rps[buf][t + 1] - rps[buf][t];
+      y[cur.x + t] = fold_row<ORDER>(prod[buf] + s0, len);
+    }
+    if (next_tile >= ntile) break;
+    tile = next_tile;
+    cur = nxt;
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) {
+      v[i] = vn[i];
+      c[i] = cn[i];
+    }
+    rpa = rna;
+    rpb = rnb;
+    buf ^= 1;
+  }
+}
+
+// Pipelined variant for row-major block operands (2 <= b <= 4): one x-row
+// gather per nonzero, products of all b columns staged in shared memory,
+// then (row, column) pairs folded in parallel, each column in the
+// reference's order.
+template <int ORDER, int YROW>
+__global__ void __launch_bounds__(kTileThreads, 2)
+csr_tile_pipe_rows_kernel(int ntile, const int4 *__restrict__ info, const int *__restrict__ row_ptr,
+                          const int *__restrict__ col, const double *__restrict__ val,
+                          const double *__restrict__ x, double *__restrict__ y, int64_t ldy, int b) {
+  extern __shared__ double dsm[];
+  double *prod = dsm;                                        // 4 x kTileNnz
+  int *rps = reinterpret_cast<int *>(dsm + 4 * kTileNnz);     // kTileRows + 1
+  const int t = threadIdx.x;
+  int tile = blockIdx.x;
+  if (tile >= ntile) return;
+  int4 cur = info[tile];
+  double v[kPerThread];
+  int c[kPerThread];
+  int rpa, rpb;
+  auto issue = [&](const int4 &ti, double (&vv)[kPerThread], int (&cc)[kPerThread], int &ra, int &rb) {
+    const int nnz = ti.w - ti.z, nrows = ti.y - ti.x;
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) {
+      int k = t + i * kTileThreads;
+      if (k < nnz) {
+        vv[i] = ld_stream(val + ti.z + k);
+        cc[i] = ld_stream(col + ti.z + k);
+      } else {
+        vv[i] = 0.0;
+        cc[i] = 0;
+      }
+    }
+    ra = (t <= nrows) ? __ldg(row_ptr + ti.x + t) : 0;
+    rb = (t == 0 && nrows >= kTileThreads) ? __ldg(row_ptr + ti.x + kTileThreads) : 0;
+  };
+  issue(cur, v, c, rpa, rpb);
+  while (true) {
+    const int next_tile = tile + gridDim.x;
+    int4 nxt = make_int4(0, 0, 0, 0);
+    double vn[kPerThread];
+    int cn[kPerThread];
+    int rna = 0, rnb = 0;
+    if (next_tile < ntile) {
+      nxt = info[next_tile];
+      issue(nxt, vn, cn, rna, rnb);
+    }
+    const int nnz = cur.w - cur.z, nrows = cur.y - cur.x;
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) {
+      int k = t + i * kTileThreads;
+      if (k < nnz) {
+        const double *xr = x + (int64_t)c[i] * b;
+        double x0 = __ldg(xr), x1 = __ldg(xr + 1);
+        prod[k] = dmul(v[i], x0);
+        prod[kTileNnz + k] = dmul(v[i], x1);
+        if (b > 2) prod[2 * kTileNnz + k] = dmul(v[i], __ldg(xr + 2));
+        if (b > 3) prod[3 * kTileNnz + k] = dmul(v[i], __ldg(xr + 3));
+      }
+    }
+    if (t <= nrows) rps[t] = rpa;
+    if (t == 0 && nrows >= kTileThreads) rps[kTileThreads] = rpb;
+    __syncthreads();
+    for (int q = t; q < nrows * b; q += kTileThreads) {
+      const int row = q % nrows, cc = q / nrows;
+      const int s0 = rps[row] - cur.z;
+      const int len = rps[row + 1] - rps[row];
+      double sres = fold_row<ORDER>(prod + cc * kTileNnz + s0, len);
+      if (YROW)
+        y[(int64_t)(cur.x + row) * b + cc] = sres;
+      else
+        y[(int64_t)(cur.x + row) + cc * ldy] = sres;
+    }
+    if (next_tile >= ntile) break;
+    __syncthreads();  // prod / rps are single-buffered
+    tile = next_tile;
+    cur = nxt;
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) {
+      v[i] = vn[i];
+      c[i] = cn[i];
+    }
+    rpa = rna;
+    rpb = rnb;
+  }
+}
+
+static int pipe_rows_grid(const void *kernel, size_t smem) {
+  static const void *which[4] = {nullptr, nullptr, nullptr, nullptr};
+  static int cap[4] = {0, 0, 0, 0};
+  for (int i = 0; i < 4; ++i)
+    if (which[i] == kernel) return cap[i];
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kTileThreads, smem);
+  if (occ < 1) occ = 1;
+  for (int i = 0; i < 4; ++i)
+    if (!which[i]) {
+      which[i] = kernel;
+      cap[i] = occ * kNumSMs;
+      break;
+    }
+  return occ * kNumSMs;
+}
+
+static int pipe_grid(const void *kernel) {
+  static int cap[2] = {0, 0};
+  static const void *which[2] = {nullptr, nullptr};
+  for (int i = 0; i < 2; ++i)
+    if (which[i] == kernel) return cap[i];
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kTileThreads, 0);
+  if (occ < 1) occ = 1;
+  for (int i = 0; i < 2; ++i)
+    if (!which[i]) {
+      which[i] = kernel;
+      cap[i] = occ * kNumSMs;
+      break;
+    }
+  return occ * kNumSMs;
+}
+
+// column-major (ld) -> row-major (stride b) and back
+__global__ void pack_rows_kernel(int64_t rows, int b, const double *__restrict__ x, int64_t ldx,
+                                 double *__restrict__ xr) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * b) return;
+  int64_t r = i / b;
+  int cc = (int)(i - r * b);
+  xr[i] = x[r + cc * ldx];
+}
+
+__global__ void unpack_rows_kernel(int64_t rows, int b, const double *__restrict__ xr, double *__restrict__ y,
+                                   int64_t ldy) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * b) return;
+  int64_t r = i / b;
+  int cc = (int)(i - r * b);
+  y[r + cc * ldy] = xr[i];
+}
+
+// One CTA per chunk of a long row: partial sums of b columns.  x is
+// row-major (stride b) when xrow, else column-major (ldx).
 __global__ void __launch_bounds__(kTileThreads)
 csr_chunk_kernel(const int *__restrict__ chunk_nz, const int *__restrict__ col,
                  const double *__restrict__ val, const double *__restrict__ x,
-                 int64_t ldx, int b, double *__restrict__ part) {
-  __shared__ double red[kTileThreads / 32];
+                 int64_t ldx, int xrow, int b, double *__restrict__ part) {
+  __shared__ double red[kTileThreads / 32][4];
   const int nz0 = chunk_nz[2 * blockIdx.x], nz1 = chunk_nz[2 * blockIdx.x + 1];
   const int t = threadIdx.x;
+  if ((xrow || b == 1) && b <= 4) {
+    // one pass over the chunk for all b columns; 4-deep unroll for MLP
+    // (b == 1: column- and row-major coincide)
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    int k = nz0 + t;
+    for (; k + 3 * kTileThreads < nz1; k += 4 * kTileThreads) {
+      int64_t c0 = ld_stream(col + k), c1 = ld_stream(col + k + kTileThreads);
+      int64_t c2 = ld_stream(col + k + 2 * kTileThreads), c3 = ld_stream(col + k + 3 * kTileThreads);
+      double v0 = ld_stream(val + k), v1 = ld_stream(val + k + kTileThreads);
+      double v2 = ld_stream(val + k + 2 * kTileThreads), v3 = ld_stream(val + k + 3 * kTileThreads);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        if (cc < b) {
+          s[cc] = fma(v0, __ldg(x + c0 * b + cc), s[cc]);
+          s[cc] = fma(v1, __ldg(x + c1 * b + cc), s[cc]);
+          s[cc] = fma(v2, __ldg(x + c2 * b + cc), s[cc]);
+          s[cc] = fma(v3, __ldg(x + c3 * b + cc), s[cc]);
+        }
+      }
+    }
+    for (; k < nz1; k += kTileThreads) {
+      int64_t c0 = ld_stream(col + k);
+      double v0 = ld_stream(val + k);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc)
+        if (cc < b) s[cc] = fma(v0, __ldg(x + c0 * b + cc), s[cc]);
+    }
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      double w = warp_sum(s[cc]);
+      if ((t & 31) == 0) red[t >> 5][cc] = w;
+    }
+    __syncthreads();
+    if (t < b) {
+      double acc = 0.0;
+      for (int w = 0; w < kTileThreads / 32; ++w) acc += red[w][t];
+      part[(int64_t)blockIdx.x * kMaxB + t] = acc;
+    }
+    return;
+  }
   for (int cc = 0; cc < b; ++cc) {
-    const double *xc = x + cc * ldx;
     double s = 0.0;
-    for (int k = nz0 + t; k < nz1; k += kTileThreads) s = fma(__ldg(val + k), __ldg(xc + __ldg(col + k)), s);
+    for (int k = nz0 + t; k < nz1; k += kTileThreads) {
+      int64_t cix = ld_stream(col + k);
+      double xv = xrow ? __ldg(x + cix * b + cc) : __ldg(x + cix + cc * ldx);
+      s = fma(ld_stream(val + k), xv, s);
+    }
     s = warp_sum(s);
-    if ((t & 31) == 0) red[t >> 5] = s;
+    if ((t & 31) == 0) red[t >> 5][0] = s;
     __syncthreads();
     if (t == 0) {
       double acc = 0.0;
-      for (int w = 0; w < kTileThreads / 32; ++w) acc += red[w];
+      for (int w = 0; w < kTileThreads / 32; ++w) acc += red[w][0];
       part[(int64_t)blockIdx.x * kMaxB + cc] = acc;
     }
     __syncthreads();
   }
 }
 
+// One warp per (long row, column): lanes take chunks l, l+32, ... and a
+// fixed shuffle tree combines them (deterministic for a given chunking).
 __global__ void csr_long_fixup_kernel(int nlong, const int *__restrict__ long_row,
                                       const int *__restrict__ long_cptr,
                                       const double *__restrict__ part, int b,
-                                      double *__restrict__ y, int64_t ldy) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nlong * b) return;
-  int li = i / b, cc = i % b;
+                                      double *__restrict__ y, int64_t ldy, int yrow) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= nlong * b) return;
+  const int li = warp / b, cc = warp % b;
   double s = 0.0;
-  for (int ch = long_cptr[li]; ch < long_cptr[li + 1]; ++ch) s += part[(int64_t)ch * kMaxB + cc];
-  y[(int64_t)long_row[li] + cc * ldy] = s;
+  for (int ch = long_cptr[li] + lane; ch < long_cptr[li + 1]; ch += 32) s += part[(int64_t)ch * kMaxB + cc];
+  s = warp_sum(s);
+  if (lane == 0) {
+    int64_t r = long_row[li];
+    if (yrow)
+      y[r * b + cc] = s;
+    else
+      y[r + cc * ldy] = s;
+  }
 }
 
 // ---------------------------------------------------------------- partition
@@ -197,6 +530,7 @@ static void free_part(CsrPart &p) {
   cudaFree(p.col);
   cudaFree(p.val);
   cudaFree(p.tile_r);
+  cudaFree(p.tile_info);
   cudaFree(p.long_row);
   cudaFree(p.long_cptr);
   cudaFree(p.chunk_nz);
@@ -249,7 +583,16 @@ static int build_partition(CsrPart &p, cudaStream_t st) {
   p.ntile = (int)(tiles.size() / 2);
   p.nlong = (int)lrows.size();
   p.nchunk = (int)(cnz.size() / 2);
+  std::vector<int> info;
+  info.reserve(4 * p.ntile);
+  for (int i = 0; i < p.ntile; ++i) {
+    info.push_back(tiles[2 * i]);
+    info.push_back(tiles[2 * i + 1]);
+    info.push_back(rp[tiles[2 * i]]);
+    info.push_back(rp[tiles[2 * i + 1]]);
+  }
   int rc;
+  if ((rc = upload(reinterpret_cast<int **>(&p.tile_info), info, st))) return rc;
   if ((rc = upload(&p.tile_r, tiles, st))) return rc;
   if ((rc = upload(&p.long_row, lrows, st))) return rc;
   if ((rc = upload(&p.long_cptr, lcptr, st))) return rc;
@@ -258,27 +601,71 @@ static int build_partition(CsrPart &p, cudaStream_t st) {
   return SVDSB_OK;
 }
 
-// y = P x for one orientation.
+// y = P x for one orientation.  xrow / yrow: operands row-major with
+// stride b (only for 2 <= b <= 4); otherwise column-major with ld.
 template <int ORDER>
-static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, double *y,
-                       int64_t ldy, int b, cudaStream_t st) {
+static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow, double *y, int64_t ldy, int yrow,
+                       int b, cudaStream_t st) {
   if (p.rows == 0) return SVDSB_OK;
+  if (b == 1) xrow = yrow = 0;
+  if (xrow || yrow) {
+    if (b > 4) {
+      set_error("row-major SpMV operands need block <= 4");
+      return SVDSB_ERR_ARG;
+    }
+    if (p.ntile > 0 && xrow) {
+      const size_t sm = sizeof(double) * 4 * kTileNnz + sizeof(int) * (kTileRows + 1);
+      if (yrow) {
+        auto k = csr_tile_pipe_rows_kernel<ORDER, 1>;
+        const int g = std::min(p.ntile, pipe_rows_grid(reinterpret_cast<const void *>(k), sm));
+        k<<<g, kTileThreads, sm, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, x, y, ldy, b);
+      } else {
+        auto k = csr_tile_pipe_rows_kernel<ORDER, 0>;
+        const int g = std::min(p.ntile, pipe_rows_grid(reinterpret_cast<const void *>(k), sm));
+        k<<<g, kTileThreads, sm, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, x, y, ldy, b);
+      }
+      SVDSB_LAUNCHED();
+    } else if (p.ntile > 0) {
+      if (xrow && yrow)
+        csr_tile_kernel<ORDER, 1, 1, 4><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, x, ldx,
+                                                                         y, ldy, b);
+      else if (xrow)
+        csr_tile_kernel<ORDER, 1, 0, 4><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, x, ldx,
+                                                                         y, ldy, b);
+      else
+        csr_tile_kernel<ORDER, 0, 1, 4><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, x, ldx,
+                                                                         y, ldy, b);
+      SVDSB_LAUNCHED();
+    }
+    if (p.nlong > 0) {
+      csr_chunk_kernel<<<p.nchunk, kTileThreads, 0, st>>>(p.chunk_nz, p.col, p.val, x, ldx, xrow, b, p.chunk_part);
+      SVDSB_LAUNCHED();
+      int tot = p.nlong * b;
+      csr_long_fixup_kernel<<<(tot * 32 + 255) / 256, 256, 0, st>>>(p.nlong, p.long_row, p.long_cptr, p.chunk_part, b, y,
+                                                               ldy, yrow);
+      SVDSB_LAUNCHED();
+    }
+    return SVDSB_OK;
+  }
   for (int c0 = 0; c0 < b; c0 += kMaxB) {
     int bb = std::min(kMaxB, b - c0);
     const double *xc = x + (int64_t)c0 * ldx;
     double *yc = y + (int64_t)c0 * ldy;
-    if (p.ntile > 0) {
-      csr_tile_kernel<ORDER><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, xc,
-                                                               ldx, yc, ldy, bb);
+    if (p.ntile > 0 && bb == 1) {
+      const int g = std::min(p.ntile, pipe_grid(reinterpret_cast<const void *>(csr_tile_pipe_kernel<ORDER>)));
+      csr_tile_pipe_kernel<ORDER><<<g, kTileThreads, 0, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc);
+      SVDSB_LAUNCHED();
+    } else if (p.ntile > 0) {
+      csr_tile_kernel<ORDER, 0, 0, 1><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, xc, ldx,
+                                                                       yc, ldy, bb);
       SVDSB_LAUNCHED();
     }
     if (p.nlong > 0) {
-      csr_chunk_kernel<<<p.nchunk, kTileThreads, 0, st>>>(p.chunk_nz, p.col, p.val, xc, ldx, bb,
-                                                          p.chunk_part);
+      csr_chunk_kernel<<<p.nchunk, kTileThreads, 0, st>>>(p.chunk_nz, p.col, p.val, xc, ldx, 0, bb, p.chunk_part);
       SVDSB_LAUNCHED();
       int tot = p.nlong * bb;
-      csr_long_fixup_kernel<<<(tot + 255) / 256, 256, 0, st>>>(p.nlong, p.long_row, p.long_cptr,
-                                                               p.chunk_part, bb, yc, ldy);
+      csr_long_fixup_kernel<<<(tot * 32 + 255) / 256, 256, 0, st>>>(p.nlong, p.long_row, p.long_cptr, p.chunk_part, bb,
+                                                               yc, ldy, 0);
       SVDSB_LAUNCHED();
     }
   }
@@ -429,6 +816,8 @@ int svdsb_csr_destroy(svdsb_csr *a) {
   if (!a) return SVDSB_OK;
   free_part(a->a);
   free_part(a->at);
+  cudaFree(a->scratch[0]);
+  cudaFree(a->scratch[1]);
   delete a;
   return SVDSB_OK;
 }
@@ -630,6 +1019,28 @@ int svdsb_csr_device_arrays(const svdsb_csr *a, int transpose, const int **row_p
   return SVDSB_OK;
 }
 
+static double *scratch_get(const svdsb_csr *ca, int slot, size_t n) {
+  svdsb_csr *a = const_cast<svdsb_csr *>(ca);
+  if (a->scratch_cap[slot] < n) {
+    cudaFree(a->scratch[slot]);
+    a->scratch[slot] = nullptr;
+    a->scratch_cap[slot] = 0;
+    if (cudaMalloc(&a->scratch[slot], n * sizeof(double)) != cudaSuccess) return nullptr;
+    a->scratch_cap[slot] = n;
+  }
+  return a->scratch[slot];
+}
+
+static int pack(const double *x, int64_t rows, int64_t ldx, int b, double *xr, cudaStream_t st) {
+  int64_t tot = rows * b;
+  if (tot == 0) return SVDSB_OK;
+  pack_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(rows, b, x, ldx, xr);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+static inline bool packed_block(int b) { return b >= 2 && b <= 4; }
+
 int svdsb_matvec(svdsb_ctx *ctx, const svdsb_csr *a, int transpose, const double *x, int64_t ldx, double *y,
                  int64_t ldy, int block, void *stream) {
   (void)ctx;
@@ -637,17 +1048,49 @@ int svdsb_matvec(svdsb_ctx *ctx, const svdsb_csr *a, int transpose, const double
   SVDSB_CHECK_ARG(block >= 0, "svdsb_matvec: negative block");
   if (block == 0) return SVDSB_OK;
   cudaStream_t st = as_stream(stream);
-  if (!transpose) {
-    SVDSB_CHECK_ARG(ldx >= a->a.cols && ldy >= a->a.rows, "svdsb_matvec: leading dimension too small");
-    return part_matvec<0>(a->a, x, ldx, y, ldy, block, st);
+  SVDSB_CHECK_ARG(!transpose || a->has_t, "svdsb_matvec: transpose requested but CSR(A^T) was not built");
+  const CsrPart &p = transpose ? a->at : a->a;
+  SVDSB_CHECK_ARG(ldx >= p.cols && ldy >= p.rows, "svdsb_matvec: leading dimension too small");
+  if (packed_block(block)) {
+    double *xr = scratch_get(a, 0, (size_t)p.cols * block);
+    if (!xr) {
+      set_error("svdsb_matvec: scratch allocation failed");
+      return SVDSB_ERR_ALLOC;
+    }
+    int rc = pack(x, p.cols, ldx, block, xr, st);
+    if (rc) return rc;
+    return transpose ? part_matvec<1>(p, xr, block, 1, y, ldy, 0, block, st)
+                     : part_matvec<0>(p, xr, block, 1, y, ldy, 0, block, st);
   }
-  SVDSB_CHECK_ARG(a->has_t, "svdsb_matvec: transpose requested but CSR(A^T) was not built");
-  SVDSB_CHECK_ARG(ldx >= a->at.cols && ldy >= a->at.rows, "svdsb_matvec: leading dimension too small");
-  return part_matvec<1>(a->at, x, ldx, y, ldy, block, st);
+  return transpose ? part_matvec<1>(p, x, ldx, 0, y, ldy, 0, block, st)
+                   : part_matvec<0>(p, x, ldx, 0, y, ldy, 0, block, st);
 }
 
 int svdsb_apply_normal(svdsb_ctx *ctx, const svdsb_csr *a, int side, const double *x, int64_t ldx, double *y,
                        int64_t ldy, int block, double *tmp, int64_t ldtmp, void *stream) {
+  SVDSB_CHECK_ARG(a != nullptr && a->has_t, "svdsb_apply_normal: needs CSR(A) and CSR(A^T)");
+  SVDSB_CHECK_ARG(side == 0 || side == 1, "svdsb_apply_normal: side must be 0 or 1");
+  if (block == 0) return SVDSB_OK;
+  cudaStream_t st = as_stream(stream);
+  const CsrPart &first = side == 0 ? a->a : a->at;    // inner product
+  const CsrPart &second = side == 0 ? a->at : a->a;
+  if (packed_block(block)) {
+    // x packed once; the inner result stays row-major for the second gather
+    double *xr = scratch_get(a, 0, (size_t)first.cols * block);
+    double *tr = scratch_get(a, 1, (size_t)first.rows * block);
+    if (!xr || !tr) {
+      set_error("svdsb_apply_normal: scratch allocation failed");
+      return SVDSB_ERR_ALLOC;
+    }
+    int rc = pack(x, first.cols, ldx, block, xr, st);
+    if (rc) return rc;
+    rc = side == 0 ? part_matvec<0>(first, xr, block, 1, tr, block, 1, block, st)
+                   : part_matvec<1>(first, xr, block, 1, tr, block, 1, block, st);
+    if (rc) return rc;
+    return side == 0 ? part_matvec<1>(second, tr, block, 1, y, ldy, 0, block, st)
+                     : part_matvec<0>(second, tr, block, 1, y, ldy, 0, block, st);
+  }
+  SVDSB_CHECK_ARG(tmp != nullptr && ldtmp >= first.rows, "svdsb_apply_normal: tmp too small");
   int rc;
   if (side == 0) {
     if ((rc = svdsb_matvec(ctx, a, 0, x, ldx, tmp, ldtmp, block, stream))) return rc;

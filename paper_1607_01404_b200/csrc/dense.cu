@@ -73,6 +73,30 @@ __device__ __forceinline__ void cta_fold(double (&acc)[NACC], int nvalid, double
 
 static inline int grid_rows(int64_t dim) { return stream_grid(dim, kMinRowsPerCta, kMaxCtas); }
 
+// Persistent-style grid: one wave of resident CTAs (occupancy x 148 SMs),
+// each looping over its contiguous row range.  Cached per (kernel, smem).
+template <typename K>
+static int grid_for(K kernel, int64_t dim, size_t smem) {
+  struct Entry {
+    const void *k;
+    size_t smem;
+    int cap;
+  };
+  static Entry cache[64];
+  static int ncache = 0;
+  const void *kp = reinterpret_cast<const void *>(kernel);
+  int cap = 0;
+  for (int i = 0; i < ncache; ++i)
+    if (cache[i].k == kp && cache[i].smem == smem) cap = cache[i].cap;
+  if (cap == 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+    cap = occ * kNumSMs;
+    if (ncache < 64) cache[ncache++] = {kp, smem, cap};
+  }
+  return stream_grid(dim, kMinRowsPerCta, cap);
+}
+
 // ------------------------------------------------------------------ gram
 
 template <int AT, int BT>
@@ -430,6 +454,256 @@ __global__ void axpby_kernel(int64_t dim, int b, double alpha, const double *x, 
   }
 }
 
+// ------------------------------------------------- 2-row vectorised paths
+// Each thread owns row pairs (r, r+1): every column access is one 16-byte
+// load, twice the bytes in flight per instruction of the scalar kernels.
+// Used when every base pointer is 16-byte aligned and every leading
+// dimension is even (always true for blocks allocated by the package).
+
+__device__ __forceinline__ RowRange cta_rows_even(int64_t dim) {
+  int64_t per = (dim + gridDim.x - 1) / gridDim.x;
+  per += per & 1;
+  int64_t r0 = (int64_t)blockIdx.x * per;
+  int64_t r1 = min(dim, r0 + per);
+  return {r0, r1};
+}
+
+__device__ __forceinline__ double2 ldg2(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
+
+template <int AT>
+__global__ void __launch_bounds__(kThreads)
+gram1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, double *c, double *norms2, double *partials,
+                 unsigned int *ticket) {
+  __shared__ const double *xp[AT];
+  const int ty = blockIdx.y;
+  const int i0 = ty * AT;
+  const int na = min(AT, xs.total - i0);
+  const bool want_norm = norms2 != nullptr && ty == 0;
+  if (threadIdx.x < AT && (int)threadIdx.x < na) xp[threadIdx.x] = colset_ptr(xs, i0 + threadIdx.x);
+  __syncthreads();
+  double acc[AT + 1];
+#pragma unroll
+  for (int k = 0; k <= AT; ++k) acc[k] = 0.0;
+  RowRange rr = cta_rows_even(dim);
+  int64_t r = rr.r0 + 2 * threadIdx.x;
+  for (; r + 1 < rr.r1; r += 2 * kThreads) {
+    double2 yv = ldg2(y + r);
+#pragma unroll
+    for (int i = 0; i < AT; ++i) {
+      if (i < na) {
+        double2 xv = ldg2(xp[i] + r);
+        acc[i] = fma(xv.x, yv.x, fma(xv.y, yv.y, acc[i]));
+      }
+    }
+    if (want_norm) acc[AT] = fma(yv.x, yv.x, fma(yv.y, yv.y, acc[AT]));
+  }
+  if (r < rr.r1) {  // odd tail row
+    double yv = __ldg(y + r);
+#pragma unroll
+    for (int i = 0; i < AT; ++i)
+      if (i < na) acc[i] = fma(__ldg(xp[i] + r), yv, acc[i]);
+    if (want_norm) acc[AT] = fma(yv, yv, acc[AT]);
+  }
+  constexpr int NOUT = AT + 1;
+  double *part = partials + ((int64_t)ty * gridDim.x + blockIdx.x) * NOUT;
+  cta_fold<NOUT>(acc, NOUT, part);
+  if (!last_cta(ticket)) return;
+  for (int o = threadIdx.x; o < (int)gridDim.y * NOUT; o += kThreads) {
+    const int t = o / NOUT, k = o % NOUT;
+    double s = 0.0;
+    const double *pp = partials + (int64_t)t * gridDim.x * NOUT + k;
+    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * NOUT];
+    if (k < AT) {
+      int i = t * AT + k;
+      if (i < xs.total) c[i] = s;
+    } else if (norms2 != nullptr && t == 0) {
+      norms2[0] = s;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+project1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ cvec, double *y, double *norms2,
+                    double *partials, unsigned int *ticket) {
+  extern __shared__ double csh[];
+  __shared__ const double *xp[256];
+  const int na = xs.total;
+  for (int i = threadIdx.x; i < na; i += kThreads) {
+    xp[i] = colset_ptr(xs, i);
+    csh[i] = cvec[i];
+  }
+  __syncthreads();
+  double nacc = 0.0;
+  RowRange rr = cta_rows_even(dim);
+  int64_t r = rr.r0 + 2 * threadIdx.x;
+  for (; r + 1 < rr.r1; r += 2 * kThreads) {
+    double2 yv = *reinterpret_cast<const double2 *>(y + r);
+    int i = 0;
+    for (; i + 4 <= na; i += 4) {
+      double2 a0 = ldg2(xp[i] + r), a1 = ldg2(xp[i + 1] + r), a2 = ldg2(xp[i + 2] + r), a3 = ldg2(xp[i + 3] + r);
+      yv.x = fma(-a0.x, csh[i], yv.x);
+      yv.y = fma(-a0.y, csh[i], yv.y);
+      yv.x = fma(-a1.x, csh[i + 1], yv.x);
+      yv.y = fma(-a1.y, csh[i + 1], yv.y);
+      yv.x = fma(-a2.x, csh[i + 2], yv.x);
+      yv.y = fma(-a2.y, csh[i + 2], yv.y);
+      yv.x = fma(-a3.x, csh[i + 3], yv.x);
+      yv.y = fma(-a3.y, csh[i + 3], yv.y);
+    }
+    for (; i < na; ++i) {
+      double2 a0 = ldg2(xp[i] + r);
+      yv.x = fma(-a0.x, csh[i], yv.x);
+      yv.y = fma(-a0.y, csh[i], yv.y);
+    }
+    *reinterpret_cast<double2 *>(y + r) = yv;
+    nacc = fma(yv.x, yv.x, fma(yv.y, yv.y, nacc));
+  }
+  if (r < rr.r1) {
+    double yv = y[r];
+    for (int i = 0; i < na; ++i) yv = fma(-__ldg(xp[i] + r), csh[i], yv);
+    y[r] = yv;
+    nacc = fma(yv, yv, nacc);
+  }
+  if (norms2 == nullptr) return;
+  double accs[1] = {nacc};
+  cta_fold<1>(accs, 1, partials + blockIdx.x);
+  if (!last_cta(ticket)) return;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += partials[bx];
+    norms2[0] = s;
+  }
+}
+
+// R = W Y - V Y diag(lam) for p <= PT candidates in one pass over V, W.
+template <int PT>
+__global__ void __launch_bounds__(kThreads)
+ritz_wide_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const double *__restrict__ w, int64_t ldw,
+                 int g, const double *__restrict__ yc, int64_t ldyc, const double *__restrict__ lam, int p,
+                 double *__restrict__ r, int64_t ldr, double *__restrict__ xo, int64_t ldx, double *__restrict__ oxo,
+                 int64_t ldox, double *rn2, double *partials, unsigned int *ticket) {
+  extern __shared__ double ysh[];  // g x PT
+  __shared__ double lsh[PT];
+  for (int k = threadIdx.x; k < g * PT; k += kThreads) {
+    int i = k / PT, j = k % PT;
+    ysh[k] = (j < p) ? yc[i + (int64_t)j * ldyc] : 0.0;
+  }
+  if (threadIdx.x < PT) lsh[threadIdx.x] = ((int)threadIdx.x < p) ? lam[threadIdx.x] : 0.0;
+  __syncthreads();
+  double nacc[PT];
+#pragma unroll
+  for (int j = 0; j < PT; ++j) nacc[j] = 0.0;
+  RowRange rr = cta_rows(dim);
+  for (int64_t row = rr.r0 + threadIdx.x; row < rr.r1; row += kThreads) {
+    double ax[PT], aw[PT];
+#pragma unroll
+    for (int j = 0; j < PT; ++j) {
+      ax[j] = 0.0;
+      aw[j] = 0.0;
+    }
+    for (int i = 0; i < g; ++i) {
+      double vv = __ldg(v + row + (int64_t)i * ldv);
+      double ww = __ldg(w + row + (int64_t)i * ldw);
+      const double2 *yrow = reinterpret_cast<const double2 *>(ysh + i * PT);
+#pragma unroll
+      for (int j = 0; j < PT / 2; ++j) {
+        double2 cf = yrow[j];
+        ax[2 * j] = fma(vv, cf.x, ax[2 * j]);
+        aw[2 * j] = fma(ww, cf.x, aw[2 * j]);
+        ax[2 * j + 1] = fma(vv, cf.y, ax[2 * j + 1]);
+        aw[2 * j + 1] = fma(ww, cf.y, aw[2 * j + 1]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PT; ++j) {
+      if (j < p) {
+        double res = aw[j] - ax[j] * lsh[j];
+        r[row + (int64_t)j * ldr] = res;
+        if (xo) xo[row + (int64_t)j * ldx] = ax[j];
+        if (oxo) oxo[row + (int64_t)j * ldox] = aw[j];
+        nacc[j] = fma(res, res, nacc[j]);
+      }
+    }
+  }
+  double *part = partials + (int64_t)blockIdx.x * PT;
+  cta_fold<PT>(nacc, PT, part);
+  if (!last_cta(ticket)) return;
+  for (int j = threadIdx.x; j < p; j += kThreads) {
+    double s = 0.0;
+    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += partials[(int64_t)bx * PT + j];
+    rn2[j] = s;
+  }
+}
+
+// Y = alpha X C + beta Y, two rows per thread, s <= ST.
+template <int ST>
+__global__ void __launch_bounds__(kThreads)
+ts_gemm_vec_kernel(int64_t dim, const double *__restrict__ x, int64_t ldx, int g, const double *__restrict__ cmat,
+                   int64_t ldc, int s, double alpha, double beta, double *__restrict__ y, int64_t ldy) {
+  extern __shared__ double csh[];  // g x ST
+  for (int k = threadIdx.x; k < g * ST; k += kThreads) {
+    int i = k / ST, j = k % ST;
+    csh[k] = (j < s) ? cmat[i + (int64_t)j * ldc] : 0.0;
+  }
+  __syncthreads();
+  RowRange rr = cta_rows_even(dim);
+  int64_t r = rr.r0 + 2 * threadIdx.x;
+  for (; r < rr.r1; r += 2 * kThreads) {
+    const bool pair = r + 1 < rr.r1;
+    double a0[ST], a1[ST];
+#pragma unroll
+    for (int j = 0; j < ST; ++j) {
+      a0[j] = 0.0;
+      a1[j] = 0.0;
+    }
+    for (int i = 0; i < g; ++i) {
+      double2 xv;
+      if (pair) {
+        xv = ldg2(x + r + (int64_t)i * ldx);
+      } else {
+        xv.x = __ldg(x + r + (int64_t)i * ldx);
+        xv.y = 0.0;
+      }
+      const double2 *crow = reinterpret_cast<const double2 *>(csh + i * ST);
+#pragma unroll
+      for (int j = 0; j < ST / 2; ++j) {
+        double2 cf = crow[j];
+        a0[2 * j] = fma(xv.x, cf.x, a0[2 * j]);
+        a1[2 * j] = fma(xv.y, cf.x, a1[2 * j]);
+        a0[2 * j + 1] = fma(xv.x, cf.y, a0[2 * j + 1]);
+        a1[2 * j + 1] = fma(xv.y, cf.y, a1[2 * j + 1]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < ST; ++j) {
+      if (j < s) {
+        double *yp = y + r + (int64_t)j * ldy;
+        if (pair) {
+          double2 out = make_double2(alpha * a0[j], alpha * a1[j]);
+          if (beta != 0.0) {
+            double2 old = *reinterpret_cast<double2 *>(yp);
+            out.x = fma(beta, old.x, out.x);
+            out.y = fma(beta, old.y, out.y);
+          }
+          *reinterpret_cast<double2 *>(yp) = out;
+        } else {
+          double out = alpha * a0[j];
+          if (beta != 0.0) out = fma(beta, *yp, out);
+          *yp = out;
+        }
+      }
+    }
+  }
+}
+
+static inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static bool colset_vec_ok(const ColSet &s) {
+  for (int k = 0; k < s.nblk; ++k)
+    if (s.cols[k] > 0 && (!aligned16(s.base[k]) || (s.ld[k] & 1))) return false;
+  return true;
+}
+
 static int make_colset(ColSet &s, int nblk, const double *const *xs, const int64_t *ldxs, const int *cols) {
   SVDSB_CHECK_ARG(nblk >= 1 && nblk <= SVDSB_MAX_BLOCKS, "between 1 and SVDSB_MAX_BLOCKS column blocks");
   s.nblk = 0;
@@ -471,7 +745,16 @@ int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, c
     if (norms2) return svdsb_col_norms2(ctx, dim, y, ldy, b, norms2, stream);
     return SVDSB_OK;
   }
-  if (b == 1) {
+  if (b == 1 && colset_vec_ok(s) && aligned16(y)) {
+    if (s.total <= 16) {
+      dim3 grid(grid_for(gram1_vec_kernel<16>, dim, 0), 1, 1);
+      gram1_vec_kernel<16><<<grid, kThreads, 0, st>>>(dim, s, y, c, norms2, ctx->partials, take_ticket(ctx));
+    } else {
+      constexpr int AT = 40;
+      dim3 grid(grid_for(gram1_vec_kernel<AT>, dim, 0), (s.total + AT - 1) / AT, 1);
+      gram1_vec_kernel<AT><<<grid, kThreads, 0, st>>>(dim, s, y, c, norms2, ctx->partials, take_ticket(ctx));
+    }
+  } else if (b == 1) {
     constexpr int AT = 32, BT = 1;
     dim3 grid(gx, (s.total + AT - 1) / AT, 1);
     SVDSB_CHECK_ARG((int64_t)grid.x * grid.y * (AT * BT + BT) <= kMaxPartials, "gram: workspace too small");
@@ -504,7 +787,10 @@ int svdsb_project_out(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const
     double *yy = y + (int64_t)j0 * ldy;
     const double *cc = c + (int64_t)j0 * ldc;
     double *nn = norms2 ? norms2 + j0 : nullptr;
-    if (bb == 1) {
+    if (bb == 1 && colset_vec_ok(s) && aligned16(yy)) {
+      size_t sh = sizeof(double) * std::max(s.total, 1);
+      project1_vec_kernel<<<grid_for(project1_vec_kernel, dim, sh), kThreads, sh, st>>>(dim, s, cc, yy, nn, ctx->partials, take_ticket(ctx));
+    } else if (bb == 1) {
       size_t sh = sizeof(double) * std::max(s.total, 1) * 1;
       project_kernel<1><<<gx, kThreads, sh, st>>>(dim, s, cc, ldc, yy, ldy, bb, nn, ctx->partials, take_ticket(ctx));
     } else {
@@ -527,6 +813,12 @@ int svdsb_ts_gemm(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx, int
     return svdsb_axpby(dim, s, 0.0, y, ldy, beta, y, ldy, stream);
   }
   constexpr int ST = 16;
+  if (s <= ST && aligned16(x) && aligned16(y) && !(ldx & 1) && !(ldy & 1)) {
+    size_t sh = sizeof(double) * g * ST;
+    ts_gemm_vec_kernel<ST><<<grid_for(ts_gemm_vec_kernel<ST>, dim, sh), kThreads, sh, st>>>(dim, x, ldx, g, c, ldc, s, alpha, beta, y, ldy);
+    SVDSB_LAUNCHED();
+    return SVDSB_OK;
+  }
   dim3 grid(grid_rows(dim), (s + ST - 1) / ST);
   size_t sh = sizeof(double) * g * ST;
   ts_gemm_kernel<ST><<<grid, kThreads, sh, st>>>(dim, x, ldx, g, c, ldc, s, alpha, beta, y, ldy);
@@ -541,6 +833,27 @@ int svdsb_ritz_residual(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ld
   if (p <= 0) return SVDSB_OK;
   SVDSB_CHECK_ARG(g >= 1 && g <= 256, "svdsb_ritz_residual: g out of range");
   cudaStream_t st = as_stream(stream);
+  if (p <= 32) {
+    auto *tk = take_ticket(ctx);
+#define SVDSB_RITZ_WIDE(PTV)                                                                                  \
+  ritz_wide_kernel<PTV><<<grid_for(ritz_wide_kernel<PTV>, dim, sizeof(double) * g * PTV), kThreads, sizeof(double) * g * PTV, st>>>(dim, v, ldv, w, ldw, g, yc, ldyc, lam, p, r, \
+                                                                         ldr, x, ldx, ox, ldox, rn2, ctx->partials, tk)
+    if (p <= 4)
+      SVDSB_RITZ_WIDE(4);
+    else if (p <= 8)
+      SVDSB_RITZ_WIDE(8);
+    else if (p <= 12)
+      SVDSB_RITZ_WIDE(12);
+    else if (p <= 16)
+      SVDSB_RITZ_WIDE(16);
+    else if (p <= 24)
+      SVDSB_RITZ_WIDE(24);
+    else
+      SVDSB_RITZ_WIDE(32);
+#undef SVDSB_RITZ_WIDE
+    SVDSB_LAUNCHED();
+    return SVDSB_OK;
+  }
   constexpr int PT = 12;
   dim3 grid(grid_rows(dim), (p + PT - 1) / PT);
   size_t sh = sizeof(double) * g * PT;

@@ -18,8 +18,8 @@ import torch
 from . import _lib
 from .device import context, require_cuda
 
-# When set to a list, every SpMV appends (transpose, block, start_event,
-# end_event) recorded on the launching stream (bench.py's roofline probe).
+# When set to a list, every SpMV appends (kind, block, start_event,
+# end_event) with kind in fwd / adj / normal (both products) recorded on the launching stream (bench.py's roofline probe).
 SPMV_PROFILER = None
 
 
@@ -103,7 +103,7 @@ class DeviceCsr:
                   P(y), ld_of(y), x.shape[1], self.ctx.stream)
         if prof is not None:
             e1.record()
-            prof.append((bool(transpose), int(x.shape[1]), e0, e1))
+            prof.append(("adj" if transpose else "fwd", int(x.shape[1]), e0, e1))
 
     def precond_diag(self, side, out):
         from .device import P

@@ -103,9 +103,11 @@ class SvdOperator:
     @classmethod
     def from_csr(cls, a, check=True, device=None):
         dev = a.device_csr(device)
-        return cls(a.m, a.n, explicit=a, check=check,
-                   into=lambda x, y: dev.matvec(x, y, transpose=False),
-                   into_t=lambda x, y: dev.matvec(x, y, transpose=True))
+        op = cls(a.m, a.n, explicit=a, check=check,
+                 into=lambda x, y: dev.matvec(x, y, transpose=False),
+                 into_t=lambda x, y: dev.matvec(x, y, transpose=True))
+        op._csr_dev = dev
+        return op
 
     @classmethod
     def from_dense(cls, arr, check=True):
@@ -252,6 +254,35 @@ def make_normal_operator(a):
     (operators.py:163-172).  Two matvecs per column; the inner m x b (or
     n x b) product goes through a cached scratch block in HBM."""
     scratch = _Scratch()
+    base = a.base if isinstance(a, _TransposedSvdOperator) else a
+    dev = getattr(base, "_csr_dev", None)
+    if dev is not None:
+        # one C call: both products, block operands staged row-major inside
+        side = 0 if (a.m >= a.n) == (base is a) else 1
+        dim = a.n if a.m >= a.n else a.m
+        inner = a.m if a.m >= a.n else a.n
+
+        def into_native(x, y):
+            from . import _lib
+            from . import matrix
+            b = x.shape[1]
+            base.n_matvecs += 2 * b
+            t = scratch.get("t", inner, b, x.device)
+            prof = matrix.SPMV_PROFILER
+            if prof is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            _lib.call("svdsb_apply_normal", dev.ctx.handle, dev.handle, side, dv.P(x), dv.ld_of(x), dv.P(y),
+                      dv.ld_of(y), b, dv.P(t), dv.ld_of(t), dev.ctx.stream)
+            if prof is not None:
+                e1.record()
+                prof.append(("normal", b, e0, e1))
+
+        op = LinearOperator(dim, into=into_native)
+        op.svd_op = a
+        op.kind = "normal"
+        return op
     if a.m >= a.n:
         def into(x, y):
             t = scratch.get("t", a.m, x.shape[1], x.device)

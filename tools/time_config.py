@@ -7,6 +7,7 @@ from paper_1607_01404_b200 import SparseMatrixCsr, SvdsConfig, svds_solve, jacob
 key = sys.argv[1]
 small = len(sys.argv) > 2 and sys.argv[2] == 'small'
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+budget = int(sys.argv[4]) if len(sys.argv) > 4 else None
 wl = workloads.CONFIGS[key]
 t0 = time.perf_counter()
 m, n, r, c, v = wl.build(**(workloads.SMALL[key] if small else {}))
@@ -16,7 +17,7 @@ torch.cuda.synchronize(); t2 = time.perf_counter()
 print(f"{key} m={m} n={n} nnz={a.nnz} gen {t1-t0:.2f}s build {t2-t1:.2f}s", flush=True)
 for rep in range(reps):
     pre = jacobi_precond_on_normal(a, side='auto') if wl.precond else None
-    cfg = SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0)
+    cfg = SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0, max_matvecs=budget)
     l0 = _lib.launch_count()
     torch.cuda.synchronize(); t = time.perf_counter()
     res = svds_solve(a, precond=pre, cfg=cfg, return_device=True)
