@@ -161,13 +161,28 @@ def _test_needs(test):
 class Orthonormalizer:
     """Iterated classical Gram-Schmidt with the DGKS 1/sqrt(2) test and
     random replacement of collapsed columns (kernels.py:54-133), one column
-    at a time on device; the host sees two norms per pass."""
+    at a time on device; the host sees two norms per pass.
 
-    def __init__(self, ctx):
+    Distributed: block rows are this rank's slice of the global vectors;
+    every partial inner product is finished by ``comm.allreduce_`` (the
+    globalSum of PAPER.md:727), and replacement draws are global-length
+    draws sliced by ``local_slice`` so all ranks agree."""
+
+    def __init__(self, ctx, comm=None, global_rows=None, local_slice=None):
+        from .dist import LOCAL
         self.ctx = ctx
+        self.comm = comm if comm is not None else LOCAL
+        self.global_rows = global_rows
+        self.local_slice = local_slice
         self.c = torch.zeros(4 * _lib.SMALL_MAX * 4, dtype=DTYPE, device=ctx.device)
         self.nrm = torch.zeros(2, dtype=DTYPE, device=ctx.device)
         self.syncs = 0
+
+    def draw(self, rng, rows):
+        """A standard-normal column of the GLOBAL length, this rank's rows."""
+        if self.local_slice is None or self.global_rows is None:
+            return rng.standard_normal(rows)
+        return self.local_slice(rng.standard_normal(self.global_rows))
 
     def _pass(self, prior, v):
         ctx = self.ctx
@@ -175,10 +190,16 @@ class Orthonormalizer:
             total = sum(b.shape[1] for b in prior)
             c = self.c[:total]
             dv.gram(ctx, v.shape[0], prior, v, c.unsqueeze(1), norms2=self.nrm[0:1])
+            if self.comm.distributed:
+                self.comm.allreduce_(self.c[:total])
             dv.project_out(ctx, v.shape[0], prior, c.unsqueeze(1), v, norms2=self.nrm[1:2])
         else:
             dv.col_norms2(ctx, v, self.nrm[0:1])
             dv.col_norms2(ctx, v, self.nrm[1:2])
+        if self.comm.distributed:
+            # nrm[0] reduced before the projection was already summed only
+            # locally; one reduction finishes both entries
+            self.comm.allreduce_(self.nrm)
         before2, after2 = dv.fetch(ctx, [self.nrm])[0]
         self.syncs += 1
         return float(np.sqrt(before2)), float(np.sqrt(after2))
@@ -216,7 +237,8 @@ class Orthonormalizer:
         for b in ext:
             if b.shape[0] != rows:
                 raise ValueError("dimension mismatch between block and against")
-        if n_ext + cols > rows:
+        grows = self.global_rows if self.global_rows is not None else rows
+        if n_ext + cols > grows:
             raise ValueError("more columns than the space can hold")
         if rng is None:
             rng = np.random.default_rng(0)
@@ -231,7 +253,7 @@ class Orthonormalizer:
                 if not flagged:
                     replaced.append(j)
                     flagged = True
-                v.copy_(torch.from_numpy(rng.standard_normal(rows)).unsqueeze(1))
+                v.copy_(torch.from_numpy(np.ascontiguousarray(self.draw(rng, rows))).unsqueeze(1))
             else:
                 raise np.linalg.LinAlgError("orthonormalize could not produce an independent column")
         return replaced
@@ -256,17 +278,27 @@ class DavidsonSolver:
         self.stats = EigStats()
         self.status = "ok"
         self.n = op.dim
-        self.ortho = Orthonormalizer(ctx)
+        # distributed operators expose the global length and the slicing of
+        # a global host vector to this rank's rows; single-GPU is the
+        # identity
+        from .dist import LOCAL
+        self.comm = getattr(op, "comm", LOCAL)
+        self.n_global = int(getattr(op, "dim_global", self.n))
+        self._slice = getattr(op, "local_slice", None)
+        self.ortho = Orthonormalizer(ctx, self.comm, self.n_global, self._slice)
 
         self.ext = []
         if ortho_constraints is not None and ortho_constraints.shape[1] > 0:
-            c = dv.to_device_block(ortho_constraints)
+            c = ortho_constraints if isinstance(ortho_constraints, torch.Tensor) else \
+                dv.to_device_block(self._local_rows(np.asarray(ortho_constraints, dtype=np.float64)))
             self.ortho(c, rng=self.rng)
             self.ext.append(c)
         self.n_ext = sum(b.shape[1] for b in self.ext)
 
-        self.wanted = max(min(cfg.num_evals, self.n - self.n_ext), 0)
-        self.dense = self.n <= cfg.max_basis_size
+        self.wanted = max(min(cfg.num_evals, self.n_global - self.n_ext), 0)
+        self.dense = self.n_global <= cfg.max_basis_size
+        if self.dense and self.comm.distributed:
+            raise ValueError("problems smaller than the basis are not distributed")
         gmax = self.n - self.n_ext if self.dense else cfg.max_basis_size
         self.gmax = gmax
         gm = max(gmax, 1)
@@ -321,6 +353,8 @@ class DavidsonSolver:
         for t in (cfg.convergence_test, cfg.practical_test):
             if t is not None and getattr(t, "split_n", None) is not None:
                 self._split_n = int(t.split_n)
+        if self._split_n is not None and hasattr(op, "split_local"):
+            self._split_n = int(op.split_local)
         if self._need_vecs or self._split_n is not None or cfg.locking:
             self.xbuf = dv.new_block(self.n, pmax)
         if self._need_vecs:
@@ -390,6 +424,20 @@ class DavidsonSolver:
         """Copy a C-order (rows, cols) numpy draw into a column-major block."""
         block.copy_(torch.from_numpy(np.ascontiguousarray(draws)))
 
+    def _local_rows(self, arr):
+        return arr if self._slice is None else self._slice(arr)
+
+    def _draw(self, cols):
+        """rng.standard_normal((N, cols)) of the GLOBAL length N (the same
+        stream on every rank), this rank's rows."""
+        return self._local_rows(self.rng.standard_normal((self.n_global, cols)))
+
+    def _red(self, *tensors):
+        """Finish local partial sums across ranks (globalSum)."""
+        if self.comm.distributed:
+            for t in tensors:
+                self.comm.allreduce_(t)
+
     def orthonormalize(self, block, against=None, start_col=0):
         r = self.ortho(block, against=against, start_col=start_col, rng=self.rng)
         self.stats.syncs = self.stats.syncs  # ortho keeps its own count
@@ -401,7 +449,7 @@ class DavidsonSolver:
         cfg = self.cfg
         if self.dense:
             free = self.gmax
-            self._upload_normal(self.v[:, :free], self.rng.standard_normal((self.n, free)))
+            self._upload_normal(self.v[:, :free], self._draw(free))
             self.orthonormalize(self.v[:, :free], against=self.ext)
             self.g = free
             take = min(free, max(self._budget_left(), 0))
@@ -416,19 +464,19 @@ class DavidsonSolver:
         if guesses is not None and guesses.shape[1] > 0:
             take = min(guesses.shape[1], self.gmax - 1)
             src = guesses if isinstance(guesses, torch.Tensor) else torch.from_numpy(
-                np.asarray(guesses, dtype=np.float64))
+                np.ascontiguousarray(self._local_rows(np.asarray(guesses, dtype=np.float64))))
             self.v[:, :take].copy_(src[:, :take])
             self.orthonormalize(self.v[:, :take], against=self._against())
             g0 = take
         if g0 == 0:
             b0 = min(max(cfg.max_block_size, cfg.num_evals), self.gmax - 1)
-            self._upload_normal(self.v[:, :b0], self.rng.standard_normal((self.n, b0)))
+            self._upload_normal(self.v[:, :b0], self._draw(b0))
             self.orthonormalize(self.v[:, :b0], against=self._against())
             g0 = b0
         if cfg.deactivate_krylov_init:
             init_target = g0
         else:
-            free = self.n - self.n_ext
+            free = self.n_global - self.n_ext
             init_target = min(max(cfg.min_restart_size, g0), self.gmax - 1, free)
         if g0 > 1:
             take = min(g0 - 1, max(self._budget_left(), 0))
@@ -461,8 +509,10 @@ class DavidsonSolver:
         self._warm = None
         if g == 0:
             return
-        dv.gram(self.ctx, self.n, [self.v[:, :g]], self.w[:, :g], self._hg[:g, :g])
-        dv.h_symmetrize(self.ctx, g, self._hg[:g, :g], self.h[:g, :g])
+        hg = dv.small_matrix(g, g)
+        dv.gram(self.ctx, self.n, [self.v[:, :g]], self.w[:, :g], hg)
+        self._red(hg)
+        dv.h_symmetrize(self.ctx, g, hg, self.h[:g, :g])
 
     def _ensure_qr(self):
         if self.q is None:
@@ -503,11 +553,13 @@ class DavidsonSolver:
             if prior:
                 c = orth.c[:g].unsqueeze(1)
                 dv.gram(ctx, self.n, prior, v, c, norms2=orth.nrm[0:1])
+                self._red(orth.c[:g])
                 dv.project_out(ctx, self.n, prior, c, v, norms2=orth.nrm[1:2])
                 dv.axpby(ctx, 1.0, c, 1.0, coef)
             else:
                 dv.col_norms2(ctx, v, orth.nrm[0:1])
                 dv.col_norms2(ctx, v, orth.nrm[1:2])
+            self._red(orth.nrm)
             before2, after2 = dv.fetch(ctx, [orth.nrm])[0]
             orth.syncs += 1
             before, cur = float(np.sqrt(before2)), float(np.sqrt(after2))
@@ -529,7 +581,7 @@ class DavidsonSolver:
         else:
             deficient = True
         if deficient:
-            v.copy_(torch.from_numpy(self.rng.standard_normal(self.n)).unsqueeze(1))
+            v.copy_(torch.from_numpy(np.ascontiguousarray(self._draw(1))))
             self.ortho(v, against=prior, rng=self.rng)
             self.rfac[g, g] = 0.0
         else:
@@ -568,13 +620,16 @@ class DavidsonSolver:
         ox = self.oxbuf[:, :p] if need_ox else None
         rn2 = self.stat_d[:p]
         dv.ritz_residual(self.ctx, self.v[:, :g], self.w[:, :g], y, lam, r, x, ox, rn2)
+        self._red(rn2)
         split = None
         if self._split_n is not None:
             pm = self.pmax
             st = self.stat_d[pm:pm + 6 * p]
             r7 = self.stat_d[7 * pm:7 * pm + p]
             dv.split_stats(self.ctx, self._split_n, r, x, st)
+            self._red(st)
             dv.split_residual(self.ctx, self._split_n, r, x, lam, st, r7)
+            self._red(r7)
             split = (st, r7)
         return r, x, ox, rn2, split
 
@@ -632,7 +687,7 @@ class DavidsonSolver:
     # ------------------------------------------------ restarting and locking
     def _reseed_basis(self):
         """eigensolver.py:471-483."""
-        self._upload_normal(self.v[:, :1], self.rng.standard_normal((self.n, 1)))
+        self._upload_normal(self.v[:, :1], self._draw(1))
         self.orthonormalize(self.v[:, :1], against=self._against())
         self.g = 1
         if self._budget_left() < 1:
@@ -702,6 +757,7 @@ class DavidsonSolver:
         cols = self.locked_vecs.shape[1]
         slot = self._locked_buf[:, cols:cols + 1]
         dv.col_norms2(self.ctx, x, self.stat_d[-1:])
+        self._red(self.stat_d[-1:])
         dv.scale_cols(self.ctx, x, self.stat_d[-1:], dv.SCALE_DIV_SQRT, slot)
         self.locked_vecs = self._locked_buf[:, :cols + 1]
         self.orthonormalize(self.locked_vecs, against=self.ext, start_col=cols)
@@ -847,8 +903,10 @@ class DavidsonSolver:
         else:
             self.collapse_streak = 0
         self._apply_op(self.v[:, g:g + b], self.w[:, g:g + b])
-        dv.gram(self.ctx, self.n, [self.v[:, :g + b]], self.w[:, g:g + b], self.hc[:g + b, :b])
-        dv.h_insert(self.ctx, g, b, self.hc[:g + b, :b], self.h)
+        hc = dv.small_matrix(g + b, b)
+        dv.gram(self.ctx, self.n, [self.v[:, :g + b]], self.w[:, g:g + b], hc)
+        self._red(hc)
+        dv.h_insert(self.ctx, g, b, hc, self.h)
         if self.q is not None:
             for j in range(b):
                 self._qr_append_col(self.w[:, g + j:g + j + 1], self.v[:, g + j:g + j + 1])
@@ -862,12 +920,15 @@ class DavidsonSolver:
         ox2 = dv.new_block(self.n, t) if self._need_vecs else None
         rn2 = torch.zeros(t, dtype=DTYPE, device=self.ctx.device)
         dv.ritz_residual(self.ctx, x, wx, z_d, lam_d, rbuf, x2, ox2, rn2)
+        self._red(rn2)
         fetch = [lam_d, rn2]
         if self._split_n is not None:
             st = torch.zeros(6 * t, dtype=DTYPE, device=self.ctx.device)
             r7 = torch.zeros(t, dtype=DTYPE, device=self.ctx.device)
             dv.split_stats(self.ctx, self._split_n, rbuf, x2, st)
+            self._red(st)
             dv.split_residual(self.ctx, self._split_n, rbuf, x2, lam_d, st, r7)
+            self._red(r7)
             fetch += [st, r7]
         got = self._sync_fetch(fetch)
         split_h = (got[2], got[3]) if self._split_n is not None else None
@@ -889,6 +950,7 @@ class DavidsonSolver:
         self._apply_op(x, wx)
         h2 = dv.small_matrix(t, t)
         dv.gram(self.ctx, self.n, [x], wx, h2)
+        self._red(h2)
         order, shift = self._order_mode()
         lam2 = torch.zeros(t, dtype=DTYPE, device=self.ctx.device)
         z = dv.small_matrix(t, t)
@@ -905,6 +967,7 @@ class DavidsonSolver:
         self._apply_op(x, wx)
         lam = torch.zeros(t, dtype=DTYPE, device=self.ctx.device)
         dv.col_dots(self.ctx, x, wx, lam)
+        self._red(lam)
         eye = dv.small_matrix(t, t)
         eye.copy_(torch.eye(t, dtype=DTYPE))
         return self._final_pairs(x, wx, eye, lam, t)

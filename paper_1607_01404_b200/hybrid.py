@@ -211,8 +211,31 @@ def stage1_convergence_test(lam, rnorm, est, delta):
 
 # ------------------------------------------------------------- utilities
 
+def _comm(op):
+    from .dist import LOCAL
+    return getattr(op, "comm", LOCAL)
+
+
+def _red(op, *tensors):
+    c = _comm(op)
+    if c.distributed:
+        for t in tensors:
+            c.allreduce_(t)
+
+
+def _local_n(op):
+    return getattr(op, "n_loc", op.n)
+
+
+def _local_m(op):
+    return getattr(op, "m_loc", op.m)
+
+
 def orient_problem(a):
     """Rows >= cols; hybrid.py:197-203."""
+    from .dist import DistSvdOperator
+    if isinstance(a, DistSvdOperator):
+        return a, False   # sharded operators are built oriented
     a = SvdOperator.wrap(a)
     if a.m < a.n:
         return a.transposed(), True
@@ -229,18 +252,20 @@ def _svd_residual_block(ctx, a, sigma_d, u, v):
     """r7^2 per column: ||A v - s u||^2 + ||A^T u - s v||^2 (2 matvecs per
     column, hybrid.py:206-211) -> device vector."""
     k = u.shape[1]
-    av = dv.new_block(a.m, k, zero=False)
-    atu = dv.new_block(a.n, k, zero=False)
+    ml, nl = _local_m(a), _local_n(a)
+    av = dv.new_block(ml, k, zero=False)
+    atu = dv.new_block(nl, k, zero=False)
     a.apply_into(v, av)
     a.apply_t_into(u, atu)
     eye = dv.small_matrix(k, k)
     eye.copy_(torch.eye(k, dtype=DTYPE))
-    r1 = dv.new_block(a.m, k, zero=False)
-    r2 = dv.new_block(a.n, k, zero=False)
+    r1 = dv.new_block(ml, k, zero=False)
+    r2 = dv.new_block(nl, k, zero=False)
     n1 = torch.zeros(k, dtype=DTYPE, device=ctx.device)
     n2 = torch.zeros(k, dtype=DTYPE, device=ctx.device)
     dv.ritz_residual(ctx, u, av, eye, sigma_d, r1, rn2=n1)
     dv.ritz_residual(ctx, v, atu, eye, sigma_d, r2, rn2=n2)
+    _red(a, n1, n2)
     return n1, n2
 
 
@@ -262,13 +287,17 @@ def stage1_postprocess(eig, a, est, k=None, rng=None):
     if rng is None:
         rng = np.random.default_rng(0)
     m, n = a.m, a.n
+    ml, nl = _local_m(a), _local_n(a)
+    comm = _comm(a)
+    m_slice = getattr(a, "m_slice", lambda full: full)
+    n_slice = getattr(a, "n_slice", lambda full: full)
     got = eig.eigenvalues.shape[0]
     if k is None:
         k = got
     t = min(got, k)
     sigma = np.zeros(k)
-    u = dv.new_block(m, k)
-    v = dv.new_block(n, k)
+    u = dv.new_block(ml, k)
+    v = dv.new_block(nl, k)
     rc = np.full(k, np.inf)
     r7 = np.full(k, np.inf)
     tiny = np.zeros(k, dtype=bool)
@@ -278,13 +307,15 @@ def stage1_postprocess(eig, a, est, k=None, rng=None):
         x = eig.eigenvectors[:, :t]
         nrm = torch.zeros(t, dtype=DTYPE, device=ctx.device)
         dv.col_norms2(ctx, x, nrm)
+        _red(a, nrm)
         dv.scale_cols(ctx, x, nrm, dv.SCALE_DIV_SQRT, v[:, :t])
         lam = eig.eigenvalues[:t]
         sig = np.sqrt(np.maximum(lam, 0.0))
-        av = dv.new_block(m, t, zero=False)
+        av = dv.new_block(ml, t, zero=False)
         a.apply_into(v[:, :t], av)
         nav_d = torch.zeros(t, dtype=DTYPE, device=ctx.device)
         dv.col_norms2(ctx, av, nav_d)
+        _red(a, nav_d)
         nav = np.sqrt(dv.fetch(ctx, [nav_d])[0])
         dv.scale_cols(ctx, av, nav_d, dv.SCALE_DIV_SQRT, u[:, :t])
         for i in range(t):
@@ -292,38 +323,40 @@ def stage1_postprocess(eig, a, est, k=None, rng=None):
                 tiny[i] = True
                 sigma[i] = 0.0
                 if not nav[i] > 0.0:
-                    u[:, i].copy_(torch.from_numpy(rng.standard_normal(m)))
+                    u[:, i].copy_(torch.from_numpy(np.ascontiguousarray(m_slice(rng.standard_normal(m)))))
                     from .eigensolver import Orthonormalizer
-                    Orthonormalizer(ctx)(u[:, :i + 1], start_col=i, rng=rng)
+                    Orthonormalizer(ctx, comm, m, m_slice)(u[:, :i + 1], start_col=i, rng=rng)
             else:
                 sigma[i] = sig[i]
         sig_d = torch.as_tensor(sigma[:t], dtype=DTYPE, device=ctx.device)
-        atu = dv.new_block(n, t, zero=False)
+        atu = dv.new_block(nl, t, zero=False)
         a.apply_t_into(u[:, :t], atu)
         eye = dv.small_matrix(t, t)
         eye.copy_(torch.eye(t, dtype=DTYPE))
-        r1 = dv.new_block(m, t, zero=False)
-        r2 = dv.new_block(n, t, zero=False)
+        r1 = dv.new_block(ml, t, zero=False)
+        r2 = dv.new_block(nl, t, zero=False)
         n1 = torch.zeros(t, dtype=DTYPE, device=ctx.device)
         n2 = torch.zeros(t, dtype=DTYPE, device=ctx.device)
         dv.ritz_residual(ctx, u[:, :t], av, eye, sig_d, r1, rn2=n1)
         dv.ritz_residual(ctx, v[:, :t], atu, eye, sig_d, r2, rn2=n2)
+        _red(a, n1, n2)
         h1, h2 = dv.fetch(ctx, [n1, n2])
         r7[:t] = np.sqrt(h1 + h2)
         rc[:t] = eig.residual_norms[:t]
         conv[:t] = eig.converged[:t]
     if t < k:
         from .eigensolver import Orthonormalizer
-        orth = Orthonormalizer(ctx)
+        orth_v = Orthonormalizer(ctx, comm, n, n_slice)
+        orth_u = Orthonormalizer(ctx, comm, m, m_slice)
         for i in range(t, k):
-            v[:, i].copy_(torch.from_numpy(rng.standard_normal(n)))
-            u[:, i].copy_(torch.from_numpy(rng.standard_normal(m)))
-            orth(v[:, :i + 1], start_col=i, rng=rng)
-            orth(u[:, :i + 1], start_col=i, rng=rng)
-    guesses = dv.new_block(n + m, k)
+            v[:, i].copy_(torch.from_numpy(np.ascontiguousarray(n_slice(rng.standard_normal(n)))))
+            u[:, i].copy_(torch.from_numpy(np.ascontiguousarray(m_slice(rng.standard_normal(m)))))
+            orth_v(v[:, :i + 1], start_col=i, rng=rng)
+            orth_u(u[:, :i + 1], start_col=i, rng=rng)
+    guesses = dv.new_block(nl + ml, k)
     s2 = 1.0 / np.sqrt(2.0)
-    dv.axpby(ctx, s2, v, 0.0, guesses[:n, :])
-    dv.axpby(ctx, s2, u, 0.0, guesses[n:, :])
+    dv.axpby(ctx, s2, v, 0.0, guesses[:nl, :])
+    dv.axpby(ctx, s2, u, 0.0, guesses[nl:, :])
     bridge = StageBridge(sigma_tilde=sigma.copy(), rc_norms=rc, guesses=guesses, tiny=tiny)
     prov = _Provisional(sigma=sigma, u=u, v=v, r7=r7, conv=conv)
     return bridge, prov
@@ -356,9 +389,18 @@ def _random_bridge(op, k, rng):
     """hybrid.py:367-373."""
     from .eigensolver import Orthonormalizer
     m, n = op.m, op.n
-    guesses = dv.new_block(n + m, k)
-    guesses.copy_(torch.from_numpy(rng.standard_normal((n + m, k))))
-    Orthonormalizer(dv.context())(guesses, rng=rng)
+    nl, ml = _local_n(op), _local_m(op)
+    draw = rng.standard_normal((n + m, k))
+    if _comm(op).distributed:
+        draw = np.concatenate([draw[op.c0:op.c1], draw[n + op.r0:n + op.r1]], axis=0)
+
+        def sl(full):
+            return np.concatenate([full[op.c0:op.c1], full[n + op.r0:n + op.r1]], axis=0)
+    else:
+        sl = None
+    guesses = dv.new_block(nl + ml, k)
+    guesses.copy_(torch.from_numpy(np.ascontiguousarray(draw)))
+    Orthonormalizer(dv.context(), _comm(op), n + m, sl)(guesses, rng=rng)
     return StageBridge(sigma_tilde=np.zeros(k), rc_norms=np.full(k, np.inf), guesses=guesses,
                        tiny=np.zeros(k, dtype=bool))
 
@@ -445,7 +487,9 @@ def svds_solve(a, precond=None, cfg=None, return_device=False):
     """
     t0 = time.perf_counter()
     cfg = cfg if cfg is not None else SvdsConfig()
-    a = SvdOperator.wrap(a)
+    from .dist import DistSvdOperator
+    if not isinstance(a, DistSvdOperator):
+        a = SvdOperator.wrap(a)
     cfg.validate(a.m, a.n)
     ctx = dv.context()
     stats = SvdsStats()
@@ -461,6 +505,18 @@ def svds_solve(a, precond=None, cfg=None, return_device=False):
 
     op, swapped = orient_problem(a)
     m, n = op.m, op.n
+    nl, ml = _local_n(op), _local_m(op)
+    comm = _comm(op)
+
+    def _dev_n(x):  # host guesses / constraints of global length -> local rows
+        if isinstance(x, torch.Tensor):
+            return _dev(x)
+        return _dev(getattr(op, "n_slice", lambda f: f)(np.asarray(x, dtype=np.float64)))
+
+    def _dev_m(x):
+        if isinstance(x, torch.Tensor):
+            return _dev(x)
+        return _dev(getattr(op, "m_slice", lambda f: f)(np.asarray(x, dtype=np.float64)))
     delta = float(cfg.eps)
     est = NormEstimate(cfg.a_norm)
     rng = np.random.default_rng(np.random.SeedSequence([cfg.seed, 0x5fd]))
@@ -487,8 +543,8 @@ def svds_solve(a, precond=None, cfg=None, return_device=False):
         e1 = _stage1_eig_config(cfg, delta, mbs, mrs, ops_left())
         pre1 = select_preconditioner(precond, "AAt" if swapped else "AtA")
         pre1_before = pre1.n_applies if pre1 is not None else 0
-        guess = _dev(right_g) if right_g is not None else None
-        ortho = _dev(ortho_r) if ortho_r is not None else None
+        guess = _dev_n(right_g) if right_g is not None else None
+        ortho = _dev_n(ortho_r) if ortho_r is not None else None
         r1 = eig_solve(c_op, e1, guesses=guess, ortho_constraints=ortho, precond=pre1, est=est,
                        est_mode="normal")
         statuses.append(r1.status)
@@ -498,7 +554,7 @@ def svds_solve(a, precond=None, cfg=None, return_device=False):
         bridge, prov = stage1_postprocess(r1, op, est, k=k, rng=rng)
     else:
         bridge = _random_bridge(op, k, rng)
-        prov = _Provisional(sigma=np.zeros(k), u=dv.new_block(m, k), v=dv.new_block(n, k),
+        prov = _Provisional(sigma=np.zeros(k), u=dv.new_block(ml, k), v=dv.new_block(nl, k),
                             r7=np.full(k, np.inf), conv=np.zeros(k, dtype=bool))
     stats.stage1_matvecs = op.n_matvecs - mv0
 
@@ -520,20 +576,20 @@ def svds_solve(a, precond=None, cfg=None, return_device=False):
             pre2_before = pre2.n_applies if pre2 is not None else 0
             frozen = []
             if ortho_l is not None and ortho_l.shape[1] > 0:
-                frozen.append(_stack_pairs(ctx, _dev(ortho_r), _dev(ortho_l)))
+                frozen.append(_stack_pairs(ctx, _dev_n(ortho_r), _dev_m(ortho_l)))
             fz = np.flatnonzero(bridge.tiny | passed)
             if fz.size:
                 frozen.append(_colsel(bridge.guesses, torch.as_tensor(fz, device=ctx.device)))
             ortho_b = None
             if frozen:
                 tot = sum(f.shape[1] for f in frozen)
-                ortho_b = dv.new_block(n + m, tot)
+                ortho_b = dv.new_block(nl + ml, tot)
                 c0 = 0
                 for f in frozen:
                     ortho_b[:, c0:c0 + f.shape[1]].copy_(f)
                     c0 += f.shape[1]
             shifts2 = bridge.shifts[active] if bridge.shifts is not None else ()
-            e2 = _stage2_eig_config(cfg, delta, n, mbs, mrs, active.size, shifts2, ops_left())
+            e2 = _stage2_eig_config(cfg, delta, nl, mbs, mrs, active.size, shifts2, ops_left())
             guesses2 = _colsel(bridge.guesses, torch.as_tensor(active, device=ctx.device))
             r2 = eig_solve(b_op, e2, guesses=guesses2, ortho_constraints=ortho_b, precond=pre2, est=est,
                            est_mode="augmented")
@@ -548,15 +604,18 @@ def svds_solve(a, precond=None, cfg=None, return_device=False):
                 x = r2.eigenvectors[:, :nj]
                 nvd = torch.zeros(nj, dtype=DTYPE, device=ctx.device)
                 nud = torch.zeros(nj, dtype=DTYPE, device=ctx.device)
-                dv.col_norms2(ctx, x[:n, :], nvd)
-                dv.col_norms2(ctx, x[n:, :], nud)
+                dv.col_norms2(ctx, x[:nl, :], nvd)
+                dv.col_norms2(ctx, x[nl:, :], nud)
+                _red(op, nvd, nud)
                 nv2, nu2 = dv.fetch(ctx, [nvd, nud])
                 keep = [j for j in range(nj) if nv2[j] > 0.0 and nu2[j] > 0.0]
                 for j in keep:
                     slot = active[j]
                     prov.sigma[slot] = abs(float(r2.eigenvalues[j]))
-                    dv.scale_cols(ctx, x[:n, j:j + 1], nvd[j:j + 1], dv.SCALE_DIV_SQRT, prov.v[:, slot:slot + 1])
-                    dv.scale_cols(ctx, x[n:, j:j + 1], nud[j:j + 1], dv.SCALE_DIV_SQRT, prov.u[:, slot:slot + 1])
+                    dv.scale_cols(ctx, x[:nl, j:j + 1], nvd[j:j + 1], dv.SCALE_DIV_SQRT,
+                                  prov.v[:, slot:slot + 1])
+                    dv.scale_cols(ctx, x[nl:, j:j + 1], nud[j:j + 1], dv.SCALE_DIV_SQRT,
+                                  prov.u[:, slot:slot + 1])
                 if keep:
                     slots = torch.as_tensor(active[keep], dtype=torch.long, device=ctx.device)
                     us = _colsel(prov.u, slots)
@@ -594,6 +653,10 @@ def svds_solve(a, precond=None, cfg=None, return_device=False):
         u, v = v, u
     if not return_device:
         u, v = dv.to_host(u), dv.to_host(v)
+        if comm.distributed:
+            # local row chunks, rank order == row order
+            u = np.asfortranarray(comm.allgather_host(np.ascontiguousarray(u)))
+            v = np.asfortranarray(comm.allgather_host(np.ascontiguousarray(v)))
     else:
         torch.cuda.current_stream(ctx.device).synchronize()
     stats.seconds = time.perf_counter() - t0

@@ -254,6 +254,16 @@ def make_normal_operator(a):
     (operators.py:163-172).  Two matvecs per column; the inner m x b (or
     n x b) product goes through a cached scratch block in HBM."""
     scratch = _Scratch()
+    from .dist import DistSvdOperator
+    if isinstance(a, DistSvdOperator):
+        # row-sharded: all-gather, two local products, reduce-scatter
+        op = LinearOperator(a.n_loc, into=lambda x, y: a.normal_into(x, y))
+        op.svd_op = a
+        op.kind = "normal"
+        op.comm = a.comm
+        op.dim_global = a.n
+        op.local_slice = a.n_slice
+        return op
     base = a.base if isinstance(a, _TransposedSvdOperator) else a
     dev = getattr(base, "_csr_dev", None)
     if dev is not None:
@@ -304,6 +314,23 @@ def make_normal_operator(a):
 def make_augmented_operator(a):
     """Stacked operator on [v (n); u (m)]: [A^T u; A v]
     (operators.py:175-190, layout SPEC.md:174)."""
+    from .dist import DistSvdOperator
+    if isinstance(a, DistSvdOperator):
+        # local stacked layout: [v rows of this rank (n_loc); u rows (m_loc)]
+        nl, ml = a.n_loc, a.m_loc
+
+        def into_d(x, y):
+            a.apply_t_into(x[nl:, :], y[:nl, :])
+            a.apply_into(x[:nl, :], y[nl:, :])
+
+        op = LinearOperator(nl + ml, into=into_d)
+        op.svd_op = a
+        op.kind = "augmented"
+        op.comm = a.comm
+        op.dim_global = a.n + a.m
+        op.local_slice = lambda full: np.concatenate([full[a.c0:a.c1], full[a.n + a.r0:a.n + a.r1]], axis=0)
+        op.split_local = nl
+        return op
     n, m = a.n, a.m
 
     def into(x, y):
@@ -313,6 +340,7 @@ def make_augmented_operator(a):
     op = LinearOperator(n + m, into=into)
     op.svd_op = a
     op.kind = "augmented"
+    op.split_local = n
     return op
 
 
