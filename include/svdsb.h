@@ -49,6 +49,12 @@ const char *svdsb_last_error(void);
  * gpu_launches evidence). */
 int64_t svdsb_launch_count(void);
 
+/* Status plumbing: asynchronous device->host copy on `stream` (dst should be
+ * pinned) and a stream synchronisation -- the single per-iteration host
+ * round trip of the solver. */
+int svdsb_d2h(void *dst_host, const void *src, size_t bytes, void *stream);
+int svdsb_stream_sync(void *stream);
+
 /* A context owns the device workspace used by the deterministic two-level
  * reductions (per-CTA partials + a ticket counter).  One context per stream
  * in flight. */
@@ -198,6 +204,19 @@ int svdsb_split_stats(svdsb_ctx *ctx, int64_t dim, int64_t nsplit,
  * out[j] = ||e1||^2 + ||e2||^2, formed elementwise (no cancellation).
  * stats: the 6-per-column output of svdsb_split_stats (device).  Columns
  * with nv == 0 or nu == 0 get out[j] = +inf. */
+/* Device-resident iterated CGS for ONE new column v (kernels.py:54-133
+ * without the host round trip).  state: 8 doubles [active, pass,
+ * collapses, orig, prev, final, |v|^2 before, |v|^2 after];
+ * svdsb_dgks_begin arms it, every svdsb_cgs_pass (Gram + projection, the
+ * second kernel's last CTA applies the DGKS 1/sqrt(2) / collapse rule)
+ * is a no-op once the column is final, so a caller queues a fixed number
+ * of passes and checks state later.  cwork: >= sum(cols) doubles.
+ * Operands must be 16-byte aligned with even leading dimensions. */
+int svdsb_dgks_begin(double *state, void *stream);
+int svdsb_cgs_pass(svdsb_ctx *ctx, int64_t dim, int nblk,
+                   const double *const *xs, const int64_t *ldxs,
+                   const int *cols, double *v, double *cwork, double *state,
+                   int first_pass, void *stream);
 int svdsb_split_residual(svdsb_ctx *ctx, int64_t dim, int64_t nsplit,
                          const double *r, int64_t ldr, const double *x,
                          int64_t ldx, int b, const double *lam,

@@ -27,6 +27,8 @@ _PROTOS = [
     ("svdsb_version", i32, []),
     ("svdsb_last_error", ctypes.c_char_p, []),
     ("svdsb_launch_count", i64, []),
+    ("svdsb_d2h", i32, [vp, vp, ctypes.c_size_t, vp]),
+    ("svdsb_stream_sync", i32, [vp]),
     ("svdsb_ctx_create", i32, [i32, ctypes.POINTER(vp)]),
     ("svdsb_ctx_destroy", i32, [vp]),
     ("svdsb_csr_create_host", i32, [vp, i64, i64, i64, vp, vp, vp, i32, vp, ctypes.POINTER(vp)]),
@@ -50,7 +52,9 @@ _PROTOS = [
     ("svdsb_scale_cols", i32, [i64, vp, i64, i32, vp, i32, vp, i64, vp]),
     ("svdsb_axpby", i32, [i64, i32, f64, vp, i64, f64, vp, i64, vp]),
     ("svdsb_split_stats", i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp]),
-    ("svdsb_split_residual", i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp, vp, vp]),
+    ("svdsb_dgks_begin", i32, [vp, vp]),
+    ("svdsb_cgs_pass", i32, [vp, i64, i32, vp, vp, vp, vp, vp, vp, i32, vp]),
+    ("svdsb_split_residual",i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp, vp, vp]),
     ("svdsb_syev_small", i32, [i32, vp, i64, i32, f64, vp, vp, i64, vp]),
     ("svdsb_syev_update", i32, [i32, i32, vp, i64, vp, i64, vp, i32, f64, vp, vp, i64, vp]),
     ("svdsb_refined_small",i32, [i32, vp, i64, vp, i64, vp, vp, vp, vp]),

@@ -473,7 +473,8 @@ __device__ __forceinline__ double2 ldg2(const double *p) { return __ldg(reinterp
 template <int AT>
 __global__ void __launch_bounds__(kThreads)
 gram1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, double *c, double *norms2, double *partials,
-                 unsigned int *ticket) {
+                 unsigned int *ticket, const double *gate) {
+  if (gate != nullptr && gate[0] == 0.0) return;  // device-side DGKS: column already final
   __shared__ const double *xp[AT];
   const int ty = blockIdx.y;
   const int i0 = ty * AT;
@@ -522,9 +523,47 @@ gram1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, double *c
   }
 }
 
+// One step of the iterated-CGS decision of kernels.py:115-127, on device.
+// st: [active, pass, collapses, orig, prev, final, |v|^2 before, |v|^2 after]
+__device__ __forceinline__ void dgks_decide(double *st) {
+  const double before = sqrt(st[6]), cur = sqrt(st[7]);
+  double p = st[1], coll = st[2], orig = st[3], prev = st[4], fin = 0.0;
+  bool active = true;
+  if (p == 0.0) {
+    orig = before;
+    prev = before;
+    if (!(orig > 0.0)) active = false;
+  }
+  if (active) {
+    if (cur < 1e-14 * orig) {
+      coll += 1.0;
+      if (coll >= 2.0) active = false;
+    } else if (cur > 0.70710678118654752440 * prev) {
+      fin = cur;
+      active = false;
+    } else {
+      coll = 0.0;
+    }
+    prev = cur;
+  }
+  p += 1.0;
+  if (active && p >= 6.0) active = false;
+  st[0] = active ? 1.0 : 0.0;
+  st[1] = p;
+  st[2] = coll;
+  st[3] = orig;
+  st[4] = prev;
+  st[5] = fin;
+}
+
+__global__ void dgks_begin_kernel(double *st) {
+  if (threadIdx.x < 8) st[threadIdx.x] = (threadIdx.x == 0) ? 1.0 : 0.0;
+}
+
 __global__ void __launch_bounds__(kThreads)
 project1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ cvec, double *y, double *norms2,
-                    double *partials, unsigned int *ticket) {
+                    double *partials, unsigned int *ticket, double *dgks) {
+  if (dgks != nullptr && dgks[0] == 0.0) return;
   extern __shared__ double csh[];
   __shared__ const double *xp[256];
   const int na = xs.total;
@@ -572,6 +611,7 @@ project1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ cvec, dou
     double s = 0.0;
     for (unsigned bx = 0; bx < gridDim.x; ++bx) s += partials[bx];
     norms2[0] = s;
+    if (dgks != nullptr) dgks_decide(dgks);
   }
 }
 
@@ -748,11 +788,11 @@ int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, c
   if (b == 1 && colset_vec_ok(s) && aligned16(y)) {
     if (s.total <= 16) {
       dim3 grid(grid_for(gram1_vec_kernel<16>, dim, 0), 1, 1);
-      gram1_vec_kernel<16><<<grid, kThreads, 0, st>>>(dim, s, y, c, norms2, ctx->partials, take_ticket(ctx));
+      gram1_vec_kernel<16><<<grid, kThreads, 0, st>>>(dim, s, y, c, norms2, ctx->partials, take_ticket(ctx), nullptr);
     } else {
       constexpr int AT = 40;
       dim3 grid(grid_for(gram1_vec_kernel<AT>, dim, 0), (s.total + AT - 1) / AT, 1);
-      gram1_vec_kernel<AT><<<grid, kThreads, 0, st>>>(dim, s, y, c, norms2, ctx->partials, take_ticket(ctx));
+      gram1_vec_kernel<AT><<<grid, kThreads, 0, st>>>(dim, s, y, c, norms2, ctx->partials, take_ticket(ctx), nullptr);
     }
   } else if (b == 1) {
     constexpr int AT = 32, BT = 1;
@@ -789,7 +829,8 @@ int svdsb_project_out(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const
     double *nn = norms2 ? norms2 + j0 : nullptr;
     if (bb == 1 && colset_vec_ok(s) && aligned16(yy)) {
       size_t sh = sizeof(double) * std::max(s.total, 1);
-      project1_vec_kernel<<<grid_for(project1_vec_kernel, dim, sh), kThreads, sh, st>>>(dim, s, cc, yy, nn, ctx->partials, take_ticket(ctx));
+      project1_vec_kernel<<<grid_for(project1_vec_kernel, dim, sh), kThreads, sh, st>>>(dim, s, cc, yy, nn, ctx->partials,
+                                                                                 take_ticket(ctx), nullptr);
     } else if (bb == 1) {
       size_t sh = sizeof(double) * std::max(s.total, 1) * 1;
       project_kernel<1><<<gx, kThreads, sh, st>>>(dim, s, cc, ldc, yy, ldy, bb, nn, ctx->partials, take_ticket(ctx));
@@ -917,6 +958,39 @@ int svdsb_axpby(int64_t dim, int b, double alpha, const double *x, int64_t ldx, 
                 void *stream) {
   if (dim == 0 || b <= 0) return SVDSB_OK;
   axpby_kernel<<<(unsigned)((dim + 255) / 256), 256, 0, as_stream(stream)>>>(dim, b, alpha, x, ldx, beta, y, ldy);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+int svdsb_dgks_begin(double *state, void *stream) {
+  dgks_begin_kernel<<<1, 32, 0, as_stream(stream)>>>(state);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+int svdsb_cgs_pass(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs,
+                   const int *cols, double *v, double *cwork, double *state, int first_pass, void *stream) {
+  SVDSB_CHECK_ARG(ctx != nullptr && state != nullptr, "svdsb_cgs_pass: NULL argument");
+  ColSet s;
+  int rc = make_colset(s, nblk, xs, ldxs, cols);
+  if (rc) return rc;
+  SVDSB_CHECK_ARG(s.total >= 1 && s.total <= 256, "svdsb_cgs_pass: 1..256 prior columns");
+  SVDSB_CHECK_ARG(colset_vec_ok(s) && aligned16(v), "svdsb_cgs_pass: operands must be 16-byte aligned");
+  cudaStream_t st = as_stream(stream);
+  double *n0 = first_pass ? state + 6 : nullptr;
+  if (s.total <= 16) {
+    dim3 grid(grid_for(gram1_vec_kernel<16>, dim, 0), 1, 1);
+    gram1_vec_kernel<16><<<grid, kThreads, 0, st>>>(dim, s, v, cwork, n0, ctx->partials, take_ticket(ctx), state);
+  } else {
+    constexpr int AT = 40;
+    dim3 grid(grid_for(gram1_vec_kernel<AT>, dim, 0), (s.total + AT - 1) / AT, 1);
+    gram1_vec_kernel<AT><<<grid, kThreads, 0, st>>>(dim, s, v, cwork, n0, ctx->partials, take_ticket(ctx), state);
+  }
+  SVDSB_LAUNCHED();
+  size_t sh = sizeof(double) * s.total;
+  project1_vec_kernel<<<grid_for(project1_vec_kernel, dim, sh), kThreads, sh, st>>>(dim, s, cwork, v, state + 7,
+                                                                                   ctx->partials, take_ticket(ctx),
+                                                                                   state);
   SVDSB_LAUNCHED();
   return SVDSB_OK;
 }

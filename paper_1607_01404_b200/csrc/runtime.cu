@@ -28,6 +28,17 @@ const char *svdsb_last_error(void) { return svdsb::g_err; }
 
 int64_t svdsb_launch_count(void) { return svdsb::g_launches.load(); }
 
+int svdsb_d2h(void *dst_host, const void *src, size_t bytes, void *stream) {
+  if (bytes == 0) return SVDSB_OK;
+  SVDSB_CUDA(cudaMemcpyAsync(dst_host, src, bytes, cudaMemcpyDeviceToHost, svdsb::as_stream(stream)));
+  return SVDSB_OK;
+}
+
+int svdsb_stream_sync(void *stream) {
+  SVDSB_CUDA(cudaStreamSynchronize(svdsb::as_stream(stream)));
+  return SVDSB_OK;
+}
+
 int svdsb_ctx_create(int device, svdsb_ctx **out) {
   SVDSB_CHECK_ARG(out != nullptr, "svdsb_ctx_create: out is NULL");
   SVDSB_CUDA(cudaSetDevice(device));

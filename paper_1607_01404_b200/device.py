@@ -42,9 +42,18 @@ class DeviceContext:
         # pinned staging for the per-iteration status read
         self._pinned = torch.empty(8192, dtype=DTYPE, pin_memory=True)
 
+        self._stream = None
+        self.refresh_stream()
+
+    def refresh_stream(self):
+        """Bind libsvdsb launches to torch's current stream on this device
+        (looked up once per solve; per-call lookups cost ~8 us each)."""
+        self._stream = int(torch.cuda.current_stream(self.device).cuda_stream) or None
+        return self._stream
+
     @property
     def stream(self):
-        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        return self._stream
 
     def __del__(self):
         try:
@@ -109,7 +118,7 @@ def as_block(t):
 
 
 def P(t):
-    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+    return t.data_ptr() if t is not None else None
 
 
 def to_device_block(x, device=None):
@@ -270,18 +279,27 @@ def small_matrix(rows, cols, device=None):
 
 def fetch(ctx, tensors):
     """Copy small 1-D device tensors to host with ONE stream
-    synchronisation (the per-iteration status read).  Returns numpy
-    arrays (copies)."""
+    synchronisation (the per-iteration status read): one cudaMemcpyAsync
+    per tensor into pinned memory, then a stream sync, all through
+    libsvdsb.  Returns numpy arrays (copies)."""
     sizes = [int(t.numel()) for t in tensors]
     total = sum(sizes)
     if total > ctx._pinned.numel():
         ctx._pinned = torch.empty(total * 2, dtype=DTYPE, pin_memory=True)
+    base = ctx._pinned.data_ptr()
+    lib = _lib.load()
     off = 0
     for t, n in zip(tensors, sizes):
         if n:
-            ctx._pinned[off:off + n].copy_(t.reshape(-1), non_blocking=True)
+            if not t.is_contiguous():
+                t = t.contiguous()
+            rc = lib.svdsb_d2h(base + 8 * off, t.data_ptr(), 8 * n, ctx._stream)
+            if rc:
+                _lib.check(rc, "svdsb_d2h")
         off += n
-    torch.cuda.current_stream(ctx.device).synchronize()
+    rc = lib.svdsb_stream_sync(ctx._stream)
+    if rc:
+        _lib.check(rc, "svdsb_stream_sync")
     host = ctx._pinned[:total].numpy().copy()
     out = []
     off = 0

@@ -230,6 +230,28 @@ class Orthonormalizer:
             dv.scale_cols(self.ctx, v, self.nrm[1:2], dv.SCALE_DIV_SQRT)
         return final
 
+    def resume(self, v, prior, st):
+        """Continue a DGKS loop started on device (state st, see
+        svdsb_cgs_pass) with host-checked passes; returns the final norm."""
+        p, collapses, orig, prev = int(st[1]), int(st[2]), float(st[3]), float(st[4])
+        final = 0.0
+        while p < _MAX_REORTH_PASSES:
+            _, cur = self._pass(prior, v)
+            p += 1
+            if cur < DEFICIENT_TOL * orig:
+                collapses += 1
+                if collapses >= 2:
+                    break
+            elif cur > REORTH_FACTOR * prev:
+                final = cur
+                break
+            else:
+                collapses = 0
+            prev = cur
+        if final > 0.0:
+            dv.scale_cols(self.ctx, v, self.nrm[1:2], dv.SCALE_DIV_SQRT)
+        return final
+
     def __call__(self, block, against=None, start_col=0, rng=None):
         rows, cols = block.shape
         ext = [b for b in (against or []) if b is not None and b.shape[1] > 0]
@@ -267,6 +289,8 @@ class DavidsonSolver:
         cfg.validate(op.dim)
         self.ctx = dv.context()
         ctx = self.ctx
+        if hasattr(ctx, "refresh_stream"):
+            ctx.refresh_stream()
         self.op = op
         self.cfg = cfg
         self.precond = precond
@@ -345,6 +369,9 @@ class DavidsonSolver:
         self._finished = self.wanted == 0
         self._warm = None           # (kind, g0) of the last known decomposition of H
         self.warm_start = True
+        self.speculate = True       # device-decided DGKS for single-column expansions
+        self._spec = None
+        self._dgks_state = torch.zeros(8, dtype=DTYPE, device=ctx.device)
 
         need_v1, split1 = _test_needs(cfg.convergence_test)
         need_v2, split2 = _test_needs(cfg.practical_test)
@@ -795,7 +822,16 @@ class DavidsonSolver:
             fetch = [lams_d, rn2]
         if split is not None:
             fetch += [split[0], split[1]]
+        spec = self._spec is not None
+        if spec:
+            fetch.append(self._dgks_state)
         got = self._sync_fetch(fetch)
+        if spec:
+            st = got.pop()
+            if not self._resolve_speculation(st):
+                # the previous expansion was redone: extract again
+                self.stats.outer_iterations -= 1
+                return self.step()
         lams = got[0]
         rn2_h = got[1]
         split_h = (got[-2], got[-1]) if split is not None else None
@@ -882,12 +918,95 @@ class DavidsonSolver:
             self.prev_coefs_g = info["g"]
         return info
 
+    # ------------------------------------------------ speculative expansion
+    # A single new column is orthonormalised by device-decided CGS passes
+    # (svdsb_cgs_pass) and the iteration proceeds without waiting for the
+    # pass norms; the DGKS state rides along with the next status read.  In
+    # the rare case the column collapsed (or needs more than SPEC_PASSES
+    # passes) the expansion is rolled back and redone on the host path,
+    # which reproduces the reference's random-replacement sequence.
+    SPEC_PASSES = 3
+
+    def _can_speculate(self, b):
+        return (b == 1 and self.speculate and self.q is None and not self.comm.distributed
+                and self.g >= 1 and getattr(self.ctx, "handle", None) is not None)
+
+    def _expand_speculative(self, block):
+        g = self.g
+        dst = self.v[:, g:g + 1]
+        if self.precond is not None:
+            self.precond.apply_into(block, dst)
+            self.stats.precond_applies += 1
+        else:
+            dv.axpby(self.ctx, 1.0, block, 0.0, dst)
+        st = self._dgks_state
+        _lib.call("svdsb_dgks_begin", dv.P(st), self.ctx.stream)
+        prior = [b for b in self._against()] + [self.v[:, :g]]
+        n, ptrs, lds, cols, total = dv._blk_args(prior)
+        for p in range(self.SPEC_PASSES):
+            _lib.call("svdsb_cgs_pass", self.ctx.handle, self.n, n, ptrs, lds, cols, dv.P(dst),
+                      dv.P(self.ortho.c), dv.P(st), 1 if p == 0 else 0, self.ctx.stream)
+        dv.scale_cols(self.ctx, dst, st[5:6], dv.SCALE_DIV)
+        self._apply_op(dst, self.w[:, g:g + 1])
+        hc = dv.small_matrix(g + 1, 1)
+        dv.gram(self.ctx, self.n, [self.v[:, :g + 1]], self.w[:, g:g + 1], hc)
+        dv.h_insert(self.ctx, g, 1, hc, self.h)
+        self._spec = {"g0": g}
+        self.g = g + 1
+
+    def _resolve_speculation(self, st):
+        """Called with the fetched DGKS state; True if the speculative
+        expansion stands, else it has been redone on the host path."""
+        spec, self._spec = self._spec, None
+        if st[0] == 0.0 and st[5] > 0.0:
+            self.collapse_streak = 0
+            return True
+        # roll back the product of the speculative column
+        g = spec["g0"]
+        self.g = g
+        self.stats.matvecs -= 1
+        self.op.n_applies -= 1
+        svd_op = getattr(self.op, "svd_op", None)
+        if svd_op is not None:
+            getattr(svd_op, "base", svd_op).n_matvecs -= 2
+        v = self.v[:, g:g + 1]
+        prior = self._against() + [self.v[:, :g]]
+        replaced = False
+        final = 0.0
+        if st[0] != 0.0:
+            # still iterating after SPEC_PASSES: continue the same DGKS loop
+            final = self.ortho.resume(v, prior, st)
+        if final == 0.0:
+            replaced = True
+            for _ in range(_MAX_RANDOM_RETRIES):
+                v.copy_(torch.from_numpy(np.ascontiguousarray(self._draw(1))))
+                if self.ortho.column(v, prior) > 0.0:
+                    break
+            else:
+                raise np.linalg.LinAlgError("orthonormalize could not produce an independent column")
+        if replaced:
+            self.collapse_streak += 1
+            if self.collapse_streak >= 3:
+                raise BasisCollapseError("no independent expansion direction after 3 retries")
+        else:
+            self.collapse_streak = 0
+        self._apply_op(v, self.w[:, g:g + 1])
+        hc = dv.small_matrix(g + 1, 1)
+        dv.gram(self.ctx, self.n, [self.v[:, :g + 1]], self.w[:, g:g + 1], hc)
+        dv.h_insert(self.ctx, g, 1, hc, self.h)
+        self.g = g + 1
+        self._warm = None
+        return False
+
     def _expand(self, res_block):
         """eigensolver.py:666-700."""
         b = min(res_block.shape[1], self.gmax - self.g)
         if b <= 0:
             return
         block = res_block[:, :b]
+        if self._can_speculate(b):
+            self._expand_speculative(block)
+            return
         g = self.g
         dst = self.v[:, g:g + b]
         if self.precond is not None:
