@@ -21,7 +21,7 @@
 
 namespace svdsb {
 
-constexpr int kAT = 256;          // threads
+constexpr int kAT = 576;          // threads: 72 eight-lane root groups
 constexpr int kAN = SVDSB_SMALL_MAX;  // max dimension
 
 struct ArrowSmem {
@@ -30,6 +30,8 @@ struct ArrowSmem {
   int sidx[kAN];                   // original index of sorted pole
   int defl[kAN];                   // deflated flag per original index
   double tau[kAN + 1];             // root offsets
+  double tau2[kAN + 1];            // per-column scratch (eigenvector scaling)
+  int rank[kAN + 1];               // ascending rank of each eigenvalue
   int korg[kAN + 1];               // root origin (sorted pole index)
   double zhat[kAN];
   double newd[kAN + 1];            // eigenvalues in output column order
@@ -40,39 +42,57 @@ struct ArrowSmem {
   double alpha, tol, znorm;
 };
 
-// f(tau) with origin pole K (sorted index), also its derivative parts.
-__device__ __forceinline__ void secular_eval(const ArrowSmem &s, int K, double tau, double &f, double &h,
-                                             double &hp, double &fscale) {
+// f(tau) with origin pole K (sorted index), also the pieces of h = tau*f
+// without the K pole.  Evaluated by an 8-lane group (lane l sums terms
+// l, l+8, ...), combined with a fixed xor tree so every lane of the group
+// holds identical values; one reciprocal per term.
+constexpr int kGroup = 8;
+
+__device__ __forceinline__ double group_sum(double v, unsigned mask) {
+  v += __shfl_xor_sync(mask, v, 1);
+  v += __shfl_xor_sync(mask, v, 2);
+  v += __shfl_xor_sync(mask, v, 4);
+  return v;
+}
+
+__device__ __forceinline__ void secular_eval(const ArrowSmem &s, int K, double tau, int lane, unsigned mask,
+                                             double &f, double &h, double &hp, double &fscale) {
   const double dK = s.sd[K];
-  double sum = 0.0, sum_nk = 0.0, dsum_nk = 0.0, scale = fabs(dK - s.alpha) + fabs(tau);
-  for (int i = 0; i < s.np; ++i) {
-    double del = s.sd[i] - dK;                // delta_i (0 for K)
-    double den = tau - del;                   // lam - d_i
-    double zz = s.sz[i] * s.sz[i];
-    double t = zz / den;
+  double sum = 0.0, sum_nk = 0.0, dsum_nk = 0.0, scale = 0.0;
+  for (int i = lane; i < s.np; i += kGroup) {
+    const double den = tau - (s.sd[i] - dK);   // lam - d_i
+    const double inv = 1.0 / den;
+    const double zz = s.sz[i] * s.sz[i];
+    const double t = zz * inv;
     sum += t;
     scale += fabs(t);
     if (i != K) {
       sum_nk += t;
-      dsum_nk += t / den;
+      dsum_nk += t * inv;
     }
   }
+  sum = group_sum(sum, mask);
+  scale = group_sum(scale, mask) + fabs(dK - s.alpha) + fabs(tau);
+  sum_nk = group_sum(sum_nk, mask);
+  dsum_nk = group_sum(dsum_nk, mask);
   f = (dK - s.alpha) + tau - sum;
-  // h = tau * f without the K pole: tau*(dK - alpha) + tau^2 - zK^2 - tau*sum_nk
   const double zK2 = s.sz[K] * s.sz[K];
   h = tau * ((dK - s.alpha) + tau - sum_nk) - zK2;
   hp = (dK - s.alpha) + 2.0 * tau - sum_nk + tau * dsum_nk;
   fscale = scale;
 }
 
-__device__ void arrow_roots(ArrowSmem &s, int j) {
-  // root j of np+1 roots, sorted ascending; interval (sd[j-1], sd[j])
+// Root j of np+1 (ascending; interval (sd[j-1], sd[j])), solved by the
+// 8-lane group `lane`/`mask`; lane 0 stores the result.
+__device__ void arrow_roots(ArrowSmem &s, int j, int lane, unsigned mask) {
   const int np = s.np;
   int K;
   double lo, hi;
   if (np == 0) {
-    s.korg[j] = -1;
-    s.tau[j] = s.alpha;
+    if (lane == 0) {
+      s.korg[j] = -1;
+      s.tau[j] = s.alpha;
+    }
     return;
   }
   if (j == 0) {
@@ -88,9 +108,8 @@ __device__ void arrow_roots(ArrowSmem &s, int j) {
   } else {
     const double a = s.sd[j - 1], b = s.sd[j];
     const double half = 0.5 * (b - a);
-    // f at the midpoint, measured from the left pole
     double f, h, hp, sc;
-    secular_eval(s, j - 1, half, f, h, hp, sc);
+    secular_eval(s, j - 1, half, lane, mask, f, h, hp, sc);
     if (f >= 0.0) {
       K = j - 1;
       lo = 0.0;
@@ -104,7 +123,7 @@ __device__ void arrow_roots(ArrowSmem &s, int j) {
   double tau = 0.5 * (lo + hi);
   for (int it = 0; it < 200; ++it) {
     double f, h, hp, sc;
-    secular_eval(s, K, tau, f, h, hp, sc);
+    secular_eval(s, K, tau, lane, mask, f, h, hp, sc);
     if (f == 0.0) break;
     if (f > 0.0)
       hi = tau;
@@ -123,8 +142,10 @@ __device__ void arrow_roots(ArrowSmem &s, int j) {
     }
     tau = nt;
   }
-  s.korg[j] = K;
-  s.tau[j] = tau;
+  if (lane == 0) {
+    s.korg[j] = K;
+    s.tau[j] = tau;
+  }
 }
 
 // lam_j - d_i for sorted pole i
@@ -195,7 +216,12 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
   }
   __syncthreads();
   const int np = s.np;
-  for (int j = tid; j <= np; j += nt) arrow_roots(s, j);
+  {
+    // one 8-lane group per root; groups of a warp run independently
+    const int lane = tid & (kGroup - 1);
+    const unsigned mask = 0xffu << (tid & 31 & ~(kGroup - 1));
+    for (int j = tid / kGroup; j <= np; j += nt / kGroup) arrow_roots(s, j, lane, mask);
+  }
   __syncthreads();
   // Gu-Eisenstat couplings
   for (int i = tid; i < np; i += nt) {
@@ -227,20 +253,29 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
   }
   __syncthreads();
   const int ndefl = n - np;
-  for (int j = tid; j <= np; j += nt) {
-    double *pc = P + (ndefl + j) * ldp;
-    double nrm2 = 1.0;
-    if (np == 0) {
-      pc[n] = 1.0;
-    } else {
-      for (int i = 0; i < np; ++i) {
-        double v = s.zhat[i] / lam_minus_pole(s, j, i);
-        pc[s.sidx[i]] = v;
-        nrm2 += v * v;
-      }
-      double inv = 1.0 / sqrt(nrm2);
-      for (int i = 0; i < np; ++i) pc[s.sidx[i]] *= inv;
-      pc[n] = inv;
+  if (np == 0) {
+    if (tid == 0) P[n + ndefl * ldp] = 1.0;
+  } else {
+    // element-parallel: v_i = zhat_i / (lam_j - d_i), then column norms
+    for (int e = tid; e < (np + 1) * np; e += nt) {
+      const int j = e / np, i = e % np;
+      P[s.sidx[i] + (ndefl + j) * ldp] = s.zhat[i] / lam_minus_pole(s, j, i);
+    }
+    __syncthreads();
+    for (int j = tid; j <= np; j += nt) {
+      double *pc = P + (ndefl + j) * ldp;
+      double nrm2 = 1.0;
+      for (int i = 0; i < np; ++i) nrm2 += pc[s.sidx[i]] * pc[s.sidx[i]];
+      s.tau2[j] = 1.0 / sqrt(nrm2);
+    }
+    __syncthreads();
+    for (int e = tid; e < (np + 1) * (np + 1); e += nt) {
+      const int j = e / (np + 1), i = e % (np + 1);
+      double *pc = P + (ndefl + j) * ldp;
+      if (i < np)
+        pc[s.sidx[i]] *= s.tau2[j];
+      else
+        pc[n] = s.tau2[j];
     }
   }
   __syncthreads();
@@ -311,37 +346,38 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
     }
     __syncthreads();
   }
-  // ordering as in syev_jacobi_kernel
-  if (tid < G) {
-    const int i = tid;
+  // ordering as in syev_jacobi_kernel: ascending ranks first (ties by
+  // index), then each value's position under the target rule, O(G) each
+  for (int i = tid; i < G; i += nt) {
     const double wi = lam[i];
     int rank = 0;
     for (int j = 0; j < G; ++j) {
-      double wj = lam[j];
+      const double wj = lam[j];
       if (wj < wi || (wj == wi && j < i)) ++rank;
     }
+    s.rank[i] = rank;
+  }
+  __syncthreads();
+  for (int i = tid; i < G; i += nt) {
+    const double wi = lam[i];
+    const int rank = s.rank[i];
     int pos = 0;
     if (order == SVDSB_ORDER_ASC) {
       pos = rank;
+    } else if (order == SVDSB_ORDER_DESC) {
+      for (int j = 0; j < G; ++j) {
+        const double wj = lam[j];
+        if (j != i && ((wj > wi) || (wj == wi && s.rank[j] < rank))) ++pos;
+      }
     } else {
+      const int bi = wi < shift;
+      const double ki = bi ? shift - wi : wi - shift;
       for (int j = 0; j < G; ++j) {
         if (j == i) continue;
-        double wj = lam[j];
-        int rj = 0;
-        for (int k = 0; k < G; ++k) {
-          double wk = lam[k];
-          if (wk < wj || (wk == wj && k < j)) ++rj;
-        }
-        bool before;
-        if (order == SVDSB_ORDER_DESC) {
-          before = (wj > wi) || (wj == wi && rj < rank);
-        } else {
-          int bi = wi < shift, bj = wj < shift;
-          double ki = bi ? shift - wi : wi - shift;
-          double kj = bj ? shift - wj : wj - shift;
-          before = (bj < bi) || (bj == bi && (kj < ki || (kj == ki && rj < rank)));
-        }
-        if (before) ++pos;
+        const double wj = lam[j];
+        const int bj = wj < shift;
+        const double kj = bj ? shift - wj : wj - shift;
+        if ((bj < bi) || (bj == bi && (kj < ki || (kj == ki && s.rank[j] < rank)))) ++pos;
       }
     }
     w_out[pos] = wi;
