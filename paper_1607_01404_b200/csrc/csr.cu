@@ -64,6 +64,10 @@ struct svdsb_csr {
   // the inner product of the normal operator; grown on demand
   double *scratch[2] = {nullptr, nullptr};
   size_t scratch_cap[2] = {0, 0};
+  // A^T split by row blocks of A (tall, scattered matrices): local column
+  // ids, block k covers rows [atb_r0[k], atb_r0[k+1]) of A
+  std::vector<svdsb::CsrPart> atb;
+  std::vector<int64_t> atb_r0;
 };
 
 namespace svdsb {
@@ -122,6 +126,14 @@ __device__ __forceinline__ double fold_row(const double *p, int len) {
     for (int i = 0; i < len; ++i) s = dadd(s, p[i]);
     return s;
   }
+}
+
+// Sequential fold continuing from a running value: a row split over column
+// blocks of A^T (processed in ascending row order) keeps np.add.at's exact
+// left-to-right order.
+__device__ __forceinline__ double fold_row_from(double s, const double *p, int len) {
+  for (int i = 0; i < len; ++i) s = dadd(s, p[i]);
+  return s;
 }
 
 __device__ __forceinline__ double ld_stream(const double *p) {
@@ -225,7 +237,7 @@ template <int ORDER>
 __global__ void __launch_bounds__(kTileThreads, 3)
 csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__restrict__ row_ptr,
                      const int *__restrict__ col, const double *__restrict__ val, const double *__restrict__ x,
-                     double *__restrict__ y) {
+                     double *__restrict__ y, int accumulate) {
   __shared__ double prod[2][kTileNnz];
   __shared__ int rps[2][kTileRows + 1];
   const int t = threadIdx.x;
@@ -277,7 +289,8 @@ csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
     if (t < nrows) {
       const int s0 = rps[buf][t] - cur.z;
       const int len = rps[buf][t + 1] - rps[buf][t];
-      y[cur.x + t] = fold_row<ORDER>(prod[buf] + s0, len);
+      y[cur.x + t] = accumulate ? fold_row_from(y[cur.x + t], prod[buf] + s0, len)
+                                : fold_row<ORDER>(prod[buf] + s0, len);
     }
     if (next_tile >= ntile) break;
     tile = next_tile;
@@ -301,7 +314,8 @@ template <int ORDER, int YROW>
 __global__ void __launch_bounds__(kTileThreads, 2)
 csr_tile_pipe_rows_kernel(int ntile, const int4 *__restrict__ info, const int *__restrict__ row_ptr,
                           const int *__restrict__ col, const double *__restrict__ val,
-                          const double *__restrict__ x, double *__restrict__ y, int64_t ldy, int b) {
+                          const double *__restrict__ x, double *__restrict__ y, int64_t ldy, int b,
+                          int accumulate) {
   extern __shared__ double dsm[];
   double *prod = dsm;                                        // 4 x kTileNnz
   int *rps = reinterpret_cast<int *>(dsm + 4 * kTileNnz);     // kTileRows + 1
@@ -345,11 +359,23 @@ csr_tile_pipe_rows_kernel(int ntile, const int4 *__restrict__ info, const int *_
       int k = t + i * kTileThreads;
       if (k < nnz) {
         const double *xr = x + (int64_t)c[i] * b;
-        double x0 = __ldg(xr), x1 = __ldg(xr + 1);
-        prod[k] = dmul(v[i], x0);
-        prod[kTileNnz + k] = dmul(v[i], x1);
-        if (b > 2) prod[2 * kTileNnz + k] = dmul(v[i], __ldg(xr + 2));
-        if (b > 3) prod[3 * kTileNnz + k] = dmul(v[i], __ldg(xr + 3));
+        if (b == 4) {
+          // one 256-bit gather per nonzero (rows are 32-byte aligned)
+          double x0, x1, x2, x3;
+          asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(x0), "=d"(x1), "=d"(x2), "=d"(x3) : "l"(xr));
+          prod[k] = dmul(v[i], x0);
+          prod[kTileNnz + k] = dmul(v[i], x1);
+          prod[2 * kTileNnz + k] = dmul(v[i], x2);
+          prod[3 * kTileNnz + k] = dmul(v[i], x3);
+        } else if (b == 2) {
+          double2 xv = __ldg(reinterpret_cast<const double2 *>(xr));
+          prod[k] = dmul(v[i], xv.x);
+          prod[kTileNnz + k] = dmul(v[i], xv.y);
+        } else {
+          prod[k] = dmul(v[i], __ldg(xr));
+          prod[kTileNnz + k] = dmul(v[i], __ldg(xr + 1));
+          prod[2 * kTileNnz + k] = dmul(v[i], __ldg(xr + 2));
+        }
       }
     }
     if (t <= nrows) rps[t] = rpa;
@@ -359,11 +385,9 @@ csr_tile_pipe_rows_kernel(int ntile, const int4 *__restrict__ info, const int *_
       const int row = q % nrows, cc = q / nrows;
       const int s0 = rps[row] - cur.z;
       const int len = rps[row + 1] - rps[row];
-      double sres = fold_row<ORDER>(prod + cc * kTileNnz + s0, len);
-      if (YROW)
-        y[(int64_t)(cur.x + row) * b + cc] = sres;
-      else
-        y[(int64_t)(cur.x + row) + cc * ldy] = sres;
+      double *yp = YROW ? y + (int64_t)(cur.x + row) * b + cc : y + (int64_t)(cur.x + row) + cc * ldy;
+      *yp = accumulate ? fold_row_from(*yp, prod + cc * kTileNnz + s0, len)
+                       : fold_row<ORDER>(prod + cc * kTileNnz + s0, len);
     }
     if (next_tile >= ntile) break;
     __syncthreads();  // prod / rps are single-buffered
@@ -433,6 +457,22 @@ __global__ void unpack_rows_kernel(int64_t rows, int b, const double *__restrict
   y[r + cc * ldy] = xr[i];
 }
 
+// s[cc] += v * xr[cc] for cc < b, one 256-bit gather when b == 4.
+__device__ __forceinline__ void gather_acc(const double *xr, int b, double v, double (&s)[4]) {
+  if (b == 4) {
+    double x0, x1, x2, x3;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(x0), "=d"(x1), "=d"(x2), "=d"(x3) : "l"(xr));
+    s[0] = fma(v, x0, s[0]);
+    s[1] = fma(v, x1, s[1]);
+    s[2] = fma(v, x2, s[2]);
+    s[3] = fma(v, x3, s[3]);
+  } else {
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+      if (cc < b) s[cc] = fma(v, __ldg(xr + cc), s[cc]);
+  }
+}
+
 // One CTA per chunk of a long row: partial sums of b columns.  x is
 // row-major (stride b) when xrow, else column-major (ldx).
 __global__ void __launch_bounds__(kTileThreads)
@@ -452,22 +492,15 @@ csr_chunk_kernel(const int *__restrict__ chunk_nz, const int *__restrict__ col,
       int64_t c2 = ld_stream(col + k + 2 * kTileThreads), c3 = ld_stream(col + k + 3 * kTileThreads);
       double v0 = ld_stream(val + k), v1 = ld_stream(val + k + kTileThreads);
       double v2 = ld_stream(val + k + 2 * kTileThreads), v3 = ld_stream(val + k + 3 * kTileThreads);
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        if (cc < b) {
-          s[cc] = fma(v0, __ldg(x + c0 * b + cc), s[cc]);
-          s[cc] = fma(v1, __ldg(x + c1 * b + cc), s[cc]);
-          s[cc] = fma(v2, __ldg(x + c2 * b + cc), s[cc]);
-          s[cc] = fma(v3, __ldg(x + c3 * b + cc), s[cc]);
-        }
-      }
+      gather_acc(x + c0 * b, b, v0, s);
+      gather_acc(x + c1 * b, b, v1, s);
+      gather_acc(x + c2 * b, b, v2, s);
+      gather_acc(x + c3 * b, b, v3, s);
     }
     for (; k < nz1; k += kTileThreads) {
       int64_t c0 = ld_stream(col + k);
       double v0 = ld_stream(val + k);
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc)
-        if (cc < b) s[cc] = fma(v0, __ldg(x + c0 * b + cc), s[cc]);
+      gather_acc(x + c0 * b, b, v0, s);
     }
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
@@ -506,7 +539,7 @@ csr_chunk_kernel(const int *__restrict__ chunk_nz, const int *__restrict__ col,
 __global__ void csr_long_fixup_kernel(int nlong, const int *__restrict__ long_row,
                                       const int *__restrict__ long_cptr,
                                       const double *__restrict__ part, int b,
-                                      double *__restrict__ y, int64_t ldy, int yrow) {
+                                      double *__restrict__ y, int64_t ldy, int yrow, int accumulate) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= nlong * b) return;
@@ -516,10 +549,8 @@ __global__ void csr_long_fixup_kernel(int nlong, const int *__restrict__ long_ro
   s = warp_sum(s);
   if (lane == 0) {
     int64_t r = long_row[li];
-    if (yrow)
-      y[r * b + cc] = s;
-    else
-      y[r + cc * ldy] = s;
+    double *yp = yrow ? y + r * b + cc : y + r + cc * ldy;
+    *yp = accumulate ? *yp + s : s;
   }
 }
 
@@ -605,7 +636,7 @@ static int build_partition(CsrPart &p, cudaStream_t st) {
 // stride b (only for 2 <= b <= 4); otherwise column-major with ld.
 template <int ORDER>
 static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow, double *y, int64_t ldy, int yrow,
-                       int b, cudaStream_t st) {
+                       int b, cudaStream_t st, int acc = 0) {
   if (p.rows == 0) return SVDSB_OK;
   if (b == 1) xrow = yrow = 0;
   if (xrow || yrow) {
@@ -618,34 +649,35 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
       if (yrow) {
         auto k = csr_tile_pipe_rows_kernel<ORDER, 1>;
         const int g = std::min(p.ntile, pipe_rows_grid(reinterpret_cast<const void *>(k), sm));
-        k<<<g, kTileThreads, sm, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, x, y, ldy, b);
+        k<<<g, kTileThreads, sm, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, x, y, ldy, b, acc);
       } else {
         auto k = csr_tile_pipe_rows_kernel<ORDER, 0>;
         const int g = std::min(p.ntile, pipe_rows_grid(reinterpret_cast<const void *>(k), sm));
-        k<<<g, kTileThreads, sm, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, x, y, ldy, b);
+        k<<<g, kTileThreads, sm, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, x, y, ldy, b, acc);
       }
       SVDSB_LAUNCHED();
     } else if (p.ntile > 0) {
-      if (xrow && yrow)
-        csr_tile_kernel<ORDER, 1, 1, 4><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, x, ldx,
-                                                                         y, ldy, b);
-      else if (xrow)
-        csr_tile_kernel<ORDER, 1, 0, 4><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, x, ldx,
-                                                                         y, ldy, b);
-      else
-        csr_tile_kernel<ORDER, 0, 1, 4><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, x, ldx,
-                                                                         y, ldy, b);
+      if (acc) {
+        set_error("accumulating SpMV needs row-major input");
+        return SVDSB_ERR_ARG;
+      }
+      csr_tile_kernel<ORDER, 0, 1, 4><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, x, ldx, y,
+                                                                       ldy, b);
       SVDSB_LAUNCHED();
     }
     if (p.nlong > 0) {
       csr_chunk_kernel<<<p.nchunk, kTileThreads, 0, st>>>(p.chunk_nz, p.col, p.val, x, ldx, xrow, b, p.chunk_part);
       SVDSB_LAUNCHED();
       int tot = p.nlong * b;
-      csr_long_fixup_kernel<<<(tot * 32 + 255) / 256, 256, 0, st>>>(p.nlong, p.long_row, p.long_cptr, p.chunk_part, b, y,
-                                                               ldy, yrow);
+      csr_long_fixup_kernel<<<(tot * 32 + 255) / 256, 256, 0, st>>>(p.nlong, p.long_row, p.long_cptr, p.chunk_part, b,
+                                                                    y, ldy, yrow, acc);
       SVDSB_LAUNCHED();
     }
     return SVDSB_OK;
+  }
+  if (acc && b != 1) {
+    set_error("accumulating SpMV needs block 1 or row-major operands");
+    return SVDSB_ERR_ARG;
   }
   for (int c0 = 0; c0 < b; c0 += kMaxB) {
     int bb = std::min(kMaxB, b - c0);
@@ -653,7 +685,8 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
     double *yc = y + (int64_t)c0 * ldy;
     if (p.ntile > 0 && bb == 1) {
       const int g = std::min(p.ntile, pipe_grid(reinterpret_cast<const void *>(csr_tile_pipe_kernel<ORDER>)));
-      csr_tile_pipe_kernel<ORDER><<<g, kTileThreads, 0, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc);
+      csr_tile_pipe_kernel<ORDER><<<g, kTileThreads, 0, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc,
+                                                              acc);
       SVDSB_LAUNCHED();
     } else if (p.ntile > 0) {
       csr_tile_kernel<ORDER, 0, 0, 1><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, xc, ldx,
@@ -665,9 +698,24 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
       SVDSB_LAUNCHED();
       int tot = p.nlong * bb;
       csr_long_fixup_kernel<<<(tot * 32 + 255) / 256, 256, 0, st>>>(p.nlong, p.long_row, p.long_cptr, p.chunk_part, bb,
-                                                               yc, ldy, 0);
+                                                                    yc, ldy, 0, acc);
       SVDSB_LAUNCHED();
     }
+  }
+  return SVDSB_OK;
+}
+
+// A^T y through the column blocks of A^T (rows of A in [r0_k, r0_{k+1}))
+// in ascending order, each block continuing the running sums of the last:
+// y blocks stay L2-resident while the Zipf head rows sweep them.
+template <int XROW>
+static int blocked_adj(const svdsb_csr *a, const double *x, int64_t ldx, double *y, int64_t ldy, int yrow, int b,
+                       cudaStream_t st) {
+  for (size_t k = 0; k < a->atb.size(); ++k) {
+    const int64_t r0 = a->atb_r0[k];
+    const double *xk = XROW ? x + r0 * b : x + r0;
+    int rc = part_matvec<1>(a->atb[k], xk, ldx, XROW, y, ldy, yrow, b, st, k > 0 ? 1 : 0);
+    if (rc) return rc;
   }
   return SVDSB_OK;
 }
@@ -816,6 +864,7 @@ int svdsb_csr_destroy(svdsb_csr *a) {
   if (!a) return SVDSB_OK;
   free_part(a->a);
   free_part(a->at);
+  for (auto &p : a->atb) free_part(p);
   cudaFree(a->scratch[0]);
   cudaFree(a->scratch[1]);
   delete a;
@@ -830,6 +879,91 @@ int svdsb_csr_shape(const svdsb_csr *a, int64_t *m, int64_t *n, int64_t *nnz) {
   return SVDSB_OK;
 }
 
+// Column blocks of A^T for tall matrices whose A^T gathers would sweep a y
+// block larger than L2 (config 4: m = 10 M rows).  Same nonzeros, regrouped
+// by row block of A; built once on device.
+constexpr int64_t kBlockRows = 2 << 20;   // 2 Mi rows: y block <= 64 MB at b = 4
+
+__global__ void seg_bounds_kernel(int64_t n, const int *__restrict__ rp, const int *__restrict__ col, int r0, int r1,
+                                  int *__restrict__ lo_out, int *__restrict__ len_out) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  auto lower = [&](int key) {
+    int lo = rp[j], hi = rp[j + 1];
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (col[mid] < key)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    return lo;
+  };
+  int a = lower(r0), b = lower(r1);
+  lo_out[j] = a;
+  len_out[j] = b - a;
+}
+
+__global__ void seg_copy_kernel(int64_t n, const int *__restrict__ col, const double *__restrict__ val,
+                                const int *__restrict__ lo, const int *__restrict__ rpk, int r0, int *__restrict__ colk,
+                                double *__restrict__ valk) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int src = lo[j], dst = rpk[j], len = rpk[j + 1] - rpk[j];
+  for (int i = 0; i < len; ++i) {
+    colk[dst + i] = col[src + i] - r0;
+    valk[dst + i] = val[src + i];
+  }
+}
+
+static int build_blocked_transpose(svdsb_csr *h, cudaStream_t st) {
+  const CsrPart &at = h->at;
+  const int64_t m = h->a.rows, n = h->a.cols;
+  int64_t block_rows = kBlockRows;
+  bool forced = false;
+  if (const char *env = getenv("SVDSB_T_BLOCK_ROWS")) {  // tuning / test knob
+    block_rows = std::max<int64_t>(1, atoll(env));
+    forced = true;
+  }
+  if (!forced && !(m > block_rows && m >= 4 * n)) return SVDSB_OK;
+  int *lo = nullptr, *len = nullptr;
+  SVDSB_CUDA(cudaMalloc(&lo, sizeof(int) * (n + 1)));
+  SVDSB_CUDA(cudaMalloc(&len, sizeof(int) * (n + 1)));
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, len, lo, (int)(n + 1), st);
+  void *scan_tmp = nullptr;
+  SVDSB_CUDA(cudaMalloc(&scan_tmp, scan_bytes));
+  for (int64_t r0 = 0; r0 < m; r0 += block_rows) {
+    const int64_t r1 = std::min(m, r0 + block_rows);
+    CsrPart p;
+    p.rows = n;
+    p.cols = r1 - r0;
+    SVDSB_CUDA(cudaMalloc(&p.row_ptr, sizeof(int) * (n + 1)));
+    SVDSB_CUDA(cudaMemsetAsync(len + n, 0, sizeof(int), st));
+    seg_bounds_kernel<<<grid1(n), 256, 0, st>>>(n, at.row_ptr, at.col, (int)r0, (int)r1, lo, len);
+    SVDSB_LAUNCHED();
+    SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, len, p.row_ptr, (int)(n + 1), st));
+    bump_launches();
+    p.host_row_ptr.resize(n + 1);
+    SVDSB_CUDA(cudaMemcpyAsync(p.host_row_ptr.data(), p.row_ptr, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, st));
+    SVDSB_CUDA(cudaStreamSynchronize(st));
+    p.nnz = p.host_row_ptr[n];
+    SVDSB_CUDA(cudaMalloc(&p.col, sizeof(int) * std::max<int64_t>(p.nnz, 1)));
+    SVDSB_CUDA(cudaMalloc(&p.val, sizeof(double) * std::max<int64_t>(p.nnz, 1)));
+    seg_copy_kernel<<<grid1(n), 256, 0, st>>>(n, at.col, at.val, lo, p.row_ptr, (int)r0, p.col, p.val);
+    SVDSB_LAUNCHED();
+    int rc = build_partition(p, st);
+    if (rc) return rc;
+    h->atb.push_back(std::move(p));
+    h->atb_r0.push_back(r0);
+  }
+  SVDSB_CUDA(cudaStreamSynchronize(st));
+  cudaFree(lo);
+  cudaFree(len);
+  cudaFree(scan_tmp);
+  return SVDSB_OK;
+}
+
 static int finish_create(svdsb_csr *h, int flags, cudaStream_t st) {
   int rc = build_partition(h->a, st);
   if (rc) return rc;
@@ -837,6 +971,8 @@ static int finish_create(svdsb_csr *h, int flags, cudaStream_t st) {
     rc = build_transpose(h->a, h->at, st);
     if (rc) return rc;
     h->has_t = true;
+    rc = build_blocked_transpose(h, st);
+    if (rc) return rc;
   }
   SVDSB_CUDA(cudaStreamSynchronize(st));
   return SVDSB_OK;
@@ -1059,9 +1195,11 @@ int svdsb_matvec(svdsb_ctx *ctx, const svdsb_csr *a, int transpose, const double
     }
     int rc = pack(x, p.cols, ldx, block, xr, st);
     if (rc) return rc;
+    if (transpose && !a->atb.empty()) return blocked_adj<1>(a, xr, block, y, ldy, 0, block, st);
     return transpose ? part_matvec<1>(p, xr, block, 1, y, ldy, 0, block, st)
                      : part_matvec<0>(p, xr, block, 1, y, ldy, 0, block, st);
   }
+  if (transpose && block == 1 && !a->atb.empty()) return blocked_adj<0>(a, x, ldx, y, ldy, 0, 1, st);
   return transpose ? part_matvec<1>(p, x, ldx, 0, y, ldy, 0, block, st)
                    : part_matvec<0>(p, x, ldx, 0, y, ldy, 0, block, st);
 }
@@ -1087,6 +1225,7 @@ int svdsb_apply_normal(svdsb_ctx *ctx, const svdsb_csr *a, int side, const doubl
     rc = side == 0 ? part_matvec<0>(first, xr, block, 1, tr, block, 1, block, st)
                    : part_matvec<1>(first, xr, block, 1, tr, block, 1, block, st);
     if (rc) return rc;
+    if (side == 0 && !a->atb.empty()) return blocked_adj<1>(a, tr, block, y, ldy, 0, block, st);
     return side == 0 ? part_matvec<1>(second, tr, block, 1, y, ldy, 0, block, st)
                      : part_matvec<0>(second, tr, block, 1, y, ldy, 0, block, st);
   }

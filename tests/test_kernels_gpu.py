@@ -404,3 +404,31 @@ def test_syev_update_matches_eigh(g0, b, kind, rng):
         assert np.abs(got_w - exp).max() <= 1e-13 * scale * g
         assert np.abs(got_y.T @ got_y - np.eye(g)).max() <= 1e-13 * g
         assert np.abs(h @ got_y - got_y * got_w).max() <= 1e-13 * scale * g
+
+
+@pytest.mark.parametrize("b", [1, 2, 4])
+def test_column_blocked_transpose(b, rng, monkeypatch):
+    """A^T through row blocks of A (tall scattered matrices) keeps the
+    reference's left-to-right order across blocks: bit-exact for short rows,
+    deterministic within rounding for long (chunked) rows."""
+    monkeypatch.setenv("SVDSB_T_BLOCK_ROWS", "997")
+    from paper_1607_01404_b200 import SparseMatrixCsr, SvdOperator, make_normal_operator
+    m, n = 5000, 300
+    rows = np.concatenate([np.repeat(np.arange(m), 3), rng.integers(0, m, 6000)])
+    cols = np.concatenate([rng.integers(0, n, 3 * m), rng.integers(0, 3, 6000)])  # 3 heavy columns
+    vals = rng.standard_normal(rows.size)
+    rp, ci, va = ocsr.csr_from_coo(m, n, rows, cols, vals)
+    a = SparseMatrixCsr(m, n, rp, ci, va)
+    y = rng.standard_normal((m, b))
+    got = _spmv_dev(a, y, True)
+    want = ocsr.spmv(m, n, rp, ci, va, y, transpose=True)
+    t_rp = ocsr.csr_transpose(m, n, rp, ci, va)[0]
+    long_rows = np.flatnonzero(np.diff(t_rp) > 2048)
+    short = np.setdiff1d(np.arange(n), long_rows)
+    assert np.array_equal(got[short], want[short])
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+    op = make_normal_operator(SvdOperator.from_csr(a, check=False))
+    x = rng.standard_normal((n, b))
+    c = _dev().to_host(op.apply(_dev().to_device_block(x)))
+    ref = ocsr.spmv(m, n, rp, ci, va, ocsr.spmv(m, n, rp, ci, va, x), transpose=True)
+    assert np.abs(c - ref).max() <= 1e-12 * np.abs(ref).max()
