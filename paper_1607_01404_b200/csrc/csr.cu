@@ -50,6 +50,7 @@ struct CsrPart {
   int *chunk_nz = nullptr;  // 2*nchunk : [nz0, nz1)
   double *chunk_part = nullptr;  // nchunk * kMaxB partial sums
   std::vector<int> host_row_ptr;
+  int maxlen = 0;             // longest row handled by the tiles
 };
 
 constexpr int kMaxB = 64;   // largest block handled by one matvec call
@@ -108,9 +109,17 @@ __device__ double np_pairwise(const double *a, int n) {
 // stays register-light.
 __device__ __noinline__ double np_pairwise_long(const double *a, int n) { return np_pairwise(a, n); }
 
-// ORDER 0: forward (reduceat) ; ORDER 1: sequential (add.at)
-template <int ORDER>
+// ORDER 0: forward (reduceat) ; ORDER 1: sequential (add.at).  SHORT: the
+// caller guarantees len <= 8 (stencil-like matrices), which keeps the fold
+// register-light.
+template <int ORDER, bool SHORT = false>
 __device__ __forceinline__ double fold_row(const double *p, int len) {
+  if (ORDER == 0 && SHORT) {
+    if (len == 0) return 0.0;
+    double r = 0.0;
+    for (int i = 1; i < len; ++i) r = dadd(r, p[i]);
+    return len == 1 ? p[0] : dadd(p[0], r);
+  }
   if (ORDER == 0) {
     if (len == 0) return 0.0;
     double s = p[0];
@@ -119,6 +128,21 @@ __device__ __forceinline__ double fold_row(const double *p, int len) {
       double r = 0.0;
       for (int i = 1; i < len; ++i) r = dadd(r, p[i]);
       return dadd(s, r);
+    }
+    if (len <= 129) {  // tail of 8..128 terms: numpy's 8-accumulator block, inline
+      const double *a = p + 1;
+      const int n = len - 1;
+      double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+      int i = 8;
+      for (; i < n - (n % 8); i += 8) {
+        r0 = dadd(r0, a[i + 0]); r1 = dadd(r1, a[i + 1]);
+        r2 = dadd(r2, a[i + 2]); r3 = dadd(r3, a[i + 3]);
+        r4 = dadd(r4, a[i + 4]); r5 = dadd(r5, a[i + 5]);
+        r6 = dadd(r6, a[i + 6]); r7 = dadd(r7, a[i + 7]);
+      }
+      double res = dadd(dadd(dadd(r0, r1), dadd(r2, r3)), dadd(dadd(r4, r5), dadd(r6, r7)));
+      for (; i < n; ++i) res = dadd(res, a[i]);
+      return dadd(s, res);
     }
     return dadd(s, np_pairwise_long(p + 1, len - 1));
   } else {
@@ -233,7 +257,7 @@ csr_tile_kernel(const int *__restrict__ tile_r, const int *__restrict__ row_ptr,
 // folds tile t, the value / index / row-pointer loads of its next tile are
 // already in flight; products are double-buffered in shared memory so one
 // barrier per tile suffices.  Same per-row summation order as above.
-template <int ORDER>
+template <int ORDER, bool SHORT>
 __global__ void __launch_bounds__(kTileThreads, 3)
 csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__restrict__ row_ptr,
                      const int *__restrict__ col, const double *__restrict__ val, const double *__restrict__ x,
@@ -290,7 +314,7 @@ csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
       const int s0 = rps[buf][t] - cur.z;
       const int len = rps[buf][t + 1] - rps[buf][t];
       y[cur.x + t] = accumulate ? fold_row_from(y[cur.x + t], prod[buf] + s0, len)
-                                : fold_row<ORDER>(prod[buf] + s0, len);
+                                : fold_row<ORDER, SHORT>(prod[buf] + s0, len);
     }
     if (next_tile >= ntile) break;
     tile = next_tile;
@@ -422,14 +446,14 @@ static int pipe_rows_grid(const void *kernel, size_t smem) {
 }
 
 static int pipe_grid(const void *kernel) {
-  static int cap[2] = {0, 0};
-  static const void *which[2] = {nullptr, nullptr};
-  for (int i = 0; i < 2; ++i)
+  static int cap[8] = {0};
+  static const void *which[8] = {nullptr};
+  for (int i = 0; i < 8; ++i)
     if (which[i] == kernel) return cap[i];
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kTileThreads, 0);
   if (occ < 1) occ = 1;
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 8; ++i)
     if (!which[i]) {
       which[i] = kernel;
       cap[i] = occ * kNumSMs;
@@ -609,6 +633,7 @@ static int build_partition(CsrPart &p, cudaStream_t st) {
     if (open < 0) open = (int)r;
     nrows += 1;
     nnz_blk += len;
+    p.maxlen = std::max(p.maxlen, len);
   }
   close((int)p.rows);
   p.ntile = (int)(tiles.size() / 2);
@@ -684,9 +709,15 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
     const double *xc = x + (int64_t)c0 * ldx;
     double *yc = y + (int64_t)c0 * ldy;
     if (p.ntile > 0 && bb == 1) {
-      const int g = std::min(p.ntile, pipe_grid(reinterpret_cast<const void *>(csr_tile_pipe_kernel<ORDER>)));
-      csr_tile_pipe_kernel<ORDER><<<g, kTileThreads, 0, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc,
-                                                              acc);
+      if (p.maxlen <= 8) {
+        auto k = csr_tile_pipe_kernel<ORDER, true>;
+        const int g = std::min(p.ntile, pipe_grid(reinterpret_cast<const void *>(k)));
+        k<<<g, kTileThreads, 0, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc, acc);
+      } else {
+        auto k = csr_tile_pipe_kernel<ORDER, false>;
+        const int g = std::min(p.ntile, pipe_grid(reinterpret_cast<const void *>(k)));
+        k<<<g, kTileThreads, 0, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc, acc);
+      }
       SVDSB_LAUNCHED();
     } else if (p.ntile > 0) {
       csr_tile_kernel<ORDER, 0, 0, 1><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, xc, ldx,
