@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-scale", action="store_true", help="skip the config-3 kernel roofline section")
     return ap.parse_args()
 
 
@@ -233,7 +234,7 @@ def run_ours(args):
                    "converged": bool(res.converged.all()), "status": res.status,
                    "stage1_matvecs": res.stats.stage1_matvecs, "stage2_matvecs": res.stats.stage2_matvecs,
                    "outer_iterations": res.stats.outer_iterations, "host_syncs": res.stats.syncs},
-        "roofline": {"kernel": "csr_tile_kernel (SpMV A x / A^T y, b=%d)" % wl.block, "bound": "hbm",
+        "roofline": {"kernel": "csr_tile_pipe_kernel (CSR SpMV A x / A^T y, b=%d)" % wl.block, "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": tot_bytes / nl if nl else None,
@@ -247,6 +248,8 @@ def run_ours(args):
 
     if not args.no_e2e and world == 1:
         line["e2e"] = e2e(args, wl, m, n, r, c, v, pysvds, barrier)
+    if world == 1 and not args.no_scale:
+        line["kernels_at_hbm_scale"] = kernels_at_scale(peak)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(wl, m, n, r, c, v, res.stats.stage1_matvecs + res.stats.stage2_matvecs,
                                             CPU_BASELINE_MATVECS)
@@ -255,6 +258,73 @@ def run_ours(args):
         tdist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def kernels_at_scale(peak):
+    """The hot kernels at BASELINE config 3 size (160^3 7-point, N = 4.1 M,
+    nnz 28.5 M; every operand larger than L2), CUDA-event timed on the
+    launching stream with L2 flushed between launches: the HBM roofline
+    fractions the north star gates on (SpMV and orthogonalisation >= 60%)."""
+    import torch
+    from paper_1607_01404_b200 import SparseMatrixCsr, SvdOperator, make_normal_operator, workloads
+    from paper_1607_01404_b200 import device as dv
+    m, n, r, c, v = workloads.c3_coo()
+    a = SparseMatrixCsr.from_coo(m, n, r, c, v)
+    del r, c, v
+    dev = a.device_csr()
+    ctx = dv.context()
+    ctx.refresh_stream()
+    nnz = a.nnz
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    def timed(fn, reps=10):
+        for _ in range(2):
+            fn()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        return float(np.median(ts))
+
+    g, p = 35, 11
+    x = dv.new_block(n, 1)
+    x.copy_(torch.randn(1, n, dtype=torch.float64, device="cuda").t())
+    y = dv.new_block(m, 1)
+    z = dv.new_block(n, 1)
+    V = dv.new_block(n, g)
+    V.copy_(torch.randn(g, n, dtype=torch.float64, device="cuda").t())
+    W = dv.new_block(n, g)
+    W.copy_(torch.randn(g, n, dtype=torch.float64, device="cuda").t())
+    Y = dv.to_device_block(np.linalg.qr(np.random.default_rng(2).standard_normal((g, g)))[0])
+    lam = torch.randn(g, dtype=torch.float64, device="cuda")
+    R = dv.new_block(n, p)
+    rn2 = torch.zeros(p, dtype=torch.float64, device="cuda")
+    C = dv.small_matrix(g, 1)
+    nr = torch.zeros(1, dtype=torch.float64, device="cuda")
+    op = make_normal_operator(SvdOperator.from_csr(a, check=False))
+    cases = {
+        "spmv_Ax": (lambda: dev.matvec(x, y, False), spmv_bytes(m, n, nnz, 1, False)),
+        "spmv_ATy": (lambda: dev.matvec(y, z, True), spmv_bytes(m, n, nnz, 1, True)),
+        "normal_apply_AtAx": (lambda: op.apply_into(x, z),
+                              spmv_bytes(m, n, nnz, 1, False) + spmv_bytes(m, n, nnz, 1, True)),
+        "ritz_residual_g35_p11": (lambda: dv.ritz_residual(ctx, V, W, Y[:, :p], lam[:p], R, rn2=rn2),
+                                  8 * n * (2 * g + p)),
+        "cgs_gram_g35": (lambda: dv.gram(ctx, n, [V], x, C, norms2=nr), 8 * n * (g + 1)),
+        "cgs_project_g35": (lambda: dv.project_out(ctx, n, [V], C, x, norms2=nr), 8 * n * (g + 2)),
+    }
+    out = {"workload": "BASELINE config 3 matrix (160^3, N=4096000, nnz=%d), basis g=35" % nnz,
+           "peak_gbs": peak}
+    for name, (fn, byt) in cases.items():
+        t = timed(fn)
+        out[name] = {"us": t * 1e6, "gbs": byt / t / 1e9, "frac": byt / t / 1e9 / peak,
+                     "algorithmic_bytes": byt}
+    return out
 
 
 def e2e(args, wl, m, n, r, c, v, pysvds, barrier):
@@ -322,6 +392,8 @@ def run_reference(args):
         return
     wl, (m, n, r, c, v) = workload(args.config)
     full = FULL_MATVECS.get(args.config)
+    from oracle import csr as ocsr
+    nnz_dedup = int(ocsr.csr_from_coo(m, n, r, c, v)[0][-1])
     vals = []
     samples = []
     for i in range(args.warmup + args.steps):
@@ -335,7 +407,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator of BASELINE config %s)"
-            % wl.name[1], "config": config_json(wl, m, n, len(v), 1), "impl": "reference",
+            % wl.name[1], "config": config_json(wl, m, n, nnz_dedup, 1), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                              "sample": "each step: oracle/phsvds.py on the full matrix with max_matvecs=%d "
                                        "(mean %.2f s for %d matvecs), scaled to the full solve's %s matvecs"
