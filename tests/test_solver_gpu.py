@@ -105,6 +105,59 @@ def test_config1_full_against_reference():
     assert abs(res.stats.stage1_matvecs - gold["stage1_matvecs"]) <= 0.25 * gold["stage1_matvecs"]
 
 
+@pytest.mark.parametrize("key", ["c2", "c3L", "c3S", "c4", "c5"])
+def test_downscaled_configs_against_reference(key):
+    """Down-scaled instances of every BASELINE config (same generators,
+    SURVEY 8(d)) against the reference's own solves (solves.json): sigma
+    within max(tol*||A||, 1e-10*sigma_max), residuals recomputed on the host
+    with the oracle's SpMV <= tol*||A||, and the matvec count close to the
+    reference's trajectory."""
+    from paper_1607_01404_b200 import SparseMatrixCsr, SvdsConfig, jacobi_precond_on_normal, svds_solve, workloads
+    gold = load_golden("solves.json")[key]
+    wl = workloads.CONFIGS[key]
+    m, n, r, c, v = wl.build(**workloads.SMALL[key])
+    rp, ci, va = ocsr.csr_from_coo(m, n, r, c, v)
+    a = _mat(m, n, rp, ci, va)
+    pre = jacobi_precond_on_normal(a, side="auto") if wl.precond else None
+    res = svds_solve(a, precond=pre, cfg=SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol,
+                                                     max_block_size=wl.block, seed=0, max_matvecs=60000))
+    want = np.array(gold["sigma"])
+    assert res.converged.all(), (res.status, res.rnorms)
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    a_norm = float(spla.svds(sp.csr_matrix((va, ci, rp), shape=(m, n)), k=1, return_singular_vectors=False)[0])
+    tol = max(wl.tol * a_norm, 1e-10 * want.max())
+    assert np.abs(res.sigma - want).max() <= tol
+    r7 = _host_r7(m, n, rp, ci, va, res.sigma, res.u, res.v)
+    assert r7.max() <= wl.tol * a_norm
+    assert abs(res.stats.stage1_matvecs - gold["stage1_matvecs"]) <= 0.3 * gold["stage1_matvecs"] + 10
+
+
+def test_subspace_angles_against_oracle_port():
+    """Principal angles between the device singular subspaces and the oracle
+    port's (bit-identical to the reference) <= 1e-6."""
+    from oracle import phsvds
+    from paper_1607_01404_b200 import SvdsConfig, svds_solve, workloads
+    m, n, r, c, v = workloads.c3_coo(nx=16)
+    rp, ci, va = ocsr.csr_from_coo(m, n, r, c, v)
+    ref = phsvds.svds(phsvds.Csr(m, n, rp, ci, va), 6, "largest", 1e-10, seed=0)
+    res = svds_solve(_mat(m, n, rp, ci, va), cfg=SvdsConfig(num_svals=6, target="largest", eps=1e-10, seed=0))
+    assert np.abs(res.sigma - ref["sigma"]).max() <= 1e-10 * ref["sigma"][0]
+    # group clustered values so the angle is taken between invariant subspaces
+    s = ref["sigma"]
+    groups, cur = [], [0]
+    for i in range(1, len(s)):
+        if abs(s[i] - s[i - 1]) <= 1e-6 * s[0]:
+            cur.append(i)
+        else:
+            groups.append(cur)
+            cur = [i]
+    groups.append(cur)
+    for gidx in groups:
+        assert _angle(res.v[:, gidx], ref["v"][:, gidx]) <= 1e-6
+        assert _angle(res.u[:, gidx], ref["u"][:, gidx]) <= 1e-6
+
+
 def test_pysvds_dense_and_coo():
     from paper_1607_01404_b200.pysvds import PySvdsError, svds
     sigma, u, v, rnorms, stats = svds(np.diag([1.0, 2.0, 3.0]), k=1, which="S")
