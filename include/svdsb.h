@@ -48,6 +48,9 @@ const char *svdsb_last_error(void);
 /* Number of kernels this library launched since load (the bench's
  * gpu_launches evidence). */
 int64_t svdsb_launch_count(void);
+/* Adds n to that counter: a CUDA-graph replay of n captured library kernels
+ * is n launches the host no longer makes one by one. */
+int64_t svdsb_note_launches(int64_t n);
 
 /* Status plumbing: asynchronous device->host copy on `stream` (dst should be
  * pinned) and a stream synchronisation -- the single per-iteration host

@@ -28,6 +28,8 @@ const char *svdsb_last_error(void) { return svdsb::g_err; }
 
 int64_t svdsb_launch_count(void) { return svdsb::g_launches.load(); }
 
+int64_t svdsb_note_launches(int64_t n) { return svdsb::bump_launches((int)n); }
+
 int svdsb_d2h(void *dst_host, const void *src, size_t bytes, void *stream) {
   if (bytes == 0) return SVDSB_OK;
   SVDSB_CUDA(cudaMemcpyAsync(dst_host, src, bytes, cudaMemcpyDeviceToHost, svdsb::as_stream(stream)));

@@ -15,6 +15,7 @@ kernels; random draws come from the same numpy Generator streams as the
 reference so trajectories track it.
 """
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -101,6 +102,7 @@ class EigStats:
     resets: int = 0
     outer_iterations: int = 0
     syncs: int = 0
+    graphs_captured: int = 0
 
 
 @dataclass
@@ -281,8 +283,60 @@ class Orthonormalizer:
         return replaced
 
 
+class _Workspace:
+    """Device buffers of one solver shape, pooled per device so repeated
+    solves of the same shape reuse memory -- and with it the CUDA graphs
+    captured for their iterations (graphs bake device pointers)."""
+
+    def __init__(self, key, n, gm, pmax, bs, plus_k):
+        self.key = key
+        self.v = dv.new_block(n, gm)
+        self.w = dv.new_block(n, gm)
+        self.v2 = dv.new_block(n, gm)
+        self.w2 = dv.new_block(n, gm)
+        self.h = dv.small_matrix(gm, gm)
+        self.lams = torch.zeros(gm, dtype=DTYPE, device=dv.context().device)
+        self.y = dv.small_matrix(gm, gm)
+        self.rbuf = dv.new_block(n, pmax)
+        self.stat = torch.zeros(8 * pmax + 4, dtype=DTYPE, device=dv.context().device)
+        self.coefs = dv.small_matrix(gm, gm)
+        self.count = torch.zeros(1, dtype=torch.int32, device=dv.context().device)
+        self.prev = dv.small_matrix(gm, max(plus_k, 1))
+        self.yref = torch.zeros(gm, dtype=DTYPE, device=dv.context().device)
+        self.excl = torch.zeros(gm, dtype=DTYPE, device=dv.context().device)
+        self.dgks = torch.zeros(8, dtype=DTYPE, device=dv.context().device)
+        self.hc1 = dv.small_matrix(gm + 1, 1)
+        self.res1 = dv.new_block(n, 1)
+        self.orthoc = torch.zeros(4 * _lib.SMALL_MAX * 4, dtype=DTYPE, device=dv.context().device)
+        self.status = torch.zeros(2 * gm + 32, dtype=DTYPE, pin_memory=True)
+        self.graphs = {}
+
+    def reset(self):
+        self.h.zero_()
+
+
+_POOL = {}
+
+
+def _acquire_workspace(n, gm, pmax, bs, plus_k):
+    ctx = dv.context()
+    key = (ctx.index, int(n), int(gm), int(pmax), int(bs), int(plus_k))
+    free = _POOL.setdefault(key, [])
+    ws = free.pop() if free else _Workspace(key, n, gm, pmax, bs, plus_k)
+    ws.reset()
+    return ws
+
+
+def _release_workspace(ws):
+    if ws is not None:
+        _POOL.setdefault(ws.key, []).append(ws)
+
+
 class DavidsonSolver:
     """One solve (eigensolver.py:157-785); create it, then call run()."""
+
+    # capture single-column iterations as CUDA graphs (SVDSB_GRAPHS=0 disables)
+    use_graphs = os.environ.get("SVDSB_GRAPHS", "1") != "0"
 
     def __init__(self, op, cfg, guesses=None, ortho_constraints=None, precond=None, est=None,
                  est_mode="normal"):
@@ -328,28 +382,36 @@ class DavidsonSolver:
         gm = max(gmax, 1)
         bs = cfg.max_block_size
 
-        self.v = dv.new_block(self.n, gm)
-        self.w = dv.new_block(self.n, gm)
-        self._v2 = None
-        self._w2 = None
-        self.h = dv.small_matrix(gm, gm)
-        self._hg = dv.small_matrix(gm, gm)
-        self.g = 0
-        self.lams_d = torch.zeros(gm, dtype=DTYPE, device=ctx.device)
-        self.y_d = dv.small_matrix(gm, gm)
         pmax = max(min(self.wanted + bs, gm), 1)
         self.pmax = pmax
-        self.rbuf = dv.new_block(self.n, pmax)
+        self._ws = None
+        if getattr(ctx, "handle", None) is not None:
+            ws = self._ws = _acquire_workspace(self.n, gm, pmax, bs, cfg.plus_k)
+            self.v, self.w, self._v2, self._w2 = ws.v, ws.w, ws.v2, ws.w2
+            self.h, self.lams_d, self.y_d = ws.h, ws.lams, ws.y
+            self.rbuf, self.stat_d, self.coefs, self.count_d = ws.rbuf, ws.stat, ws.coefs, ws.count
+            self.prev_d, self.yref, self.excl = ws.prev, ws.yref, ws.excl
+            self.ortho.c = ws.orthoc
+        else:
+            self.v = dv.new_block(self.n, gm)
+            self.w = dv.new_block(self.n, gm)
+            self._v2 = None
+            self._w2 = None
+            self.h = dv.small_matrix(gm, gm)
+            self.lams_d = torch.zeros(gm, dtype=DTYPE, device=ctx.device)
+            self.y_d = dv.small_matrix(gm, gm)
+            self.rbuf = dv.new_block(self.n, pmax)
+            # status scratch: rn2 | split stats (6 per col) | r7^2 | refined lam
+            self.stat_d = torch.zeros(8 * pmax + 4, dtype=DTYPE, device=ctx.device)
+            self.coefs = dv.small_matrix(gm, gm)
+            self.count_d = torch.zeros(1, dtype=torch.int32, device=ctx.device)
+            self.prev_d = dv.small_matrix(gm, max(cfg.plus_k, 1))
+            self.yref = torch.zeros(gm, dtype=DTYPE, device=ctx.device)
+            self.excl = torch.zeros(gm, dtype=DTYPE, device=ctx.device)
+        self.g = 0
         self.xbuf = None
         self.oxbuf = None
-        # status scratch: rn2 | split stats (6 per col) | r7^2 | refined lam
-        self.stat_d = torch.zeros(8 * pmax + 4, dtype=DTYPE, device=ctx.device)
-        self.hc = dv.small_matrix(gm + bs, bs)
-        self.coefs = dv.small_matrix(gm, gm)
-        self.count_d = torch.zeros(1, dtype=torch.int32, device=ctx.device)
-        self.prev_d = dv.small_matrix(gm, max(cfg.plus_k, 1))
-        self.yref = torch.zeros(gm, dtype=DTYPE, device=ctx.device)
-        self.excl = torch.zeros(gm, dtype=DTYPE, device=ctx.device)
+        self._pending = None
 
         self.locked_vecs = dv.new_block(self.n, 0)
         self._locked_buf = dv.new_block(self.n, max(self.wanted, 1)) if cfg.locking else None
@@ -371,7 +433,8 @@ class DavidsonSolver:
         self.warm_start = True
         self.speculate = True       # device-decided DGKS for single-column expansions
         self._spec = None
-        self._dgks_state = torch.zeros(8, dtype=DTYPE, device=ctx.device)
+        self._dgks_state = self._ws.dgks if self._ws is not None else torch.zeros(8, dtype=DTYPE,
+                                                                                   device=ctx.device)
 
         need_v1, split1 = _test_needs(cfg.convergence_test)
         need_v2, split2 = _test_needs(cfg.practical_test)
@@ -806,10 +869,25 @@ class DavidsonSolver:
         self.stats.outer_iterations += 1
         info = {"restarted": False, "reset": False, "locked": False, "done": False}
         g = self.g
-        lams_d, y_d = self.extract_rayleigh_ritz()
         refined = cfg.extraction == EXTRACT_REFINED
         need_x = self.xbuf is not None
         need_ox = self._need_vecs
+        if self._pending is not None:
+            # extraction, candidates and the status copy were queued (graph)
+            # together with the previous expansion; only wait for them
+            pend, self._pending = self._pending, None
+            p = pend["p"]
+            lams_d, y_d = self.lams_d[:g], self.y_d[:g, :g]
+            r, x, ox, split = self.rbuf[:, :p], None, None, None
+            got = self._wait_status(g, p)
+            st = got.pop()
+            if not self._resolve_speculation(st):
+                self.stats.outer_iterations -= 1
+                return self.step()
+            lams, rn2_h, split_h = got[0], got[1], None
+            self._observe(lams)
+            return self._step_decide(info, g, lams, y_d, rn2_h, split_h, r, x, ox, p, refined)
+        lams_d, y_d = self.extract_rayleigh_ritz()
         if refined:
             lamref = self.stat_d[-2:-1]
             dv.refined_small(self.ctx, self.rfac[:g, :g], self.h[:g, :g], g, self.yref[:g], lamref)
@@ -836,9 +914,16 @@ class DavidsonSolver:
         rn2_h = got[1]
         split_h = (got[-2], got[-1]) if split is not None else None
         self._observe(lams)
+        self._lam_ref_h = float(got[2][0]) if refined else None
+        return self._step_decide(info, g, lams, y_d, rn2_h, split_h, r, x, ox, p, refined)
 
+    def _step_decide(self, info, g, lams, y_d, rn2_h, split_h, r, x, ox, p, refined):
+        """Host half of an outer iteration: convergence tests, reset,
+        locking, stagnation, budget, restart and expansion
+        (eigensolver.py:586-664) on the fetched status."""
+        cfg = self.cfg
         if refined:
-            lam_ref = float(got[2][0])
+            lam_ref = self._lam_ref_h
             cands = self._make_cands(np.array([lam_ref]), rn2_h, split_h, 1, x, ox)
             cand = cands[0]
             conv_count = 0
@@ -904,8 +989,9 @@ class DavidsonSolver:
             if self._finished:
                 info["done"] = True
                 return info
-        self._expand(res_block)
         if not restarted:
+            # saved before the expansion: a graphed expansion also runs the
+            # next extraction, which overwrites the Ritz coefficients
             if refined:
                 dv.axpby(self.ctx, 1.0, self.yref[:g].unsqueeze(1), 0.0, self.prev_d[:g, :1])
                 self.prev_coefs = 1
@@ -916,6 +1002,7 @@ class DavidsonSolver:
                     dv.axpby(self.ctx, 1.0, y_d[:, conv_count:hi], 0.0, self.prev_d[:g, :k])
                 self.prev_coefs = k
             self.prev_coefs_g = info["g"]
+        self._expand(res_block, ci)
         return info
 
     # ------------------------------------------------ speculative expansion
@@ -998,12 +1085,125 @@ class DavidsonSolver:
         self._warm = None
         return False
 
-    def _expand(self, res_block):
+    # ------------------------------------------------- graphed iterations
+    # The device work between two host decisions of a plain single-column
+    # Rayleigh-Ritz iteration -- expansion (preconditioner, device-decided
+    # CGS passes, the C-apply, the H column), the next warm extraction, the
+    # candidate residuals and the status copy -- depends only on (g, ci, p,
+    # warm state, buffers).  It is captured once as a CUDA graph and
+    # replayed: one launch instead of ~15, no Python in between.
+
+    def _graph_ok(self, b):
+        return (self.use_graphs and self._can_speculate(b) and self._ws is not None
+                and not self.cfg.locking and self.cfg.extraction == EXTRACT_RR
+                and self._split_n is None and not self._need_vecs and self.cfg.iteration_hook is None
+                and not self.ext and self.locked_vecs.shape[1] == 0 and self.warm_start
+                and self._warm is not None and getattr(self.op, "graph_key", None) is not None
+                and (self.precond is None or getattr(self.precond, "graph_key", None) is not None))
+
+    def _iter_device(self, g, ci, kind, g0, p, order, shift):
+        """Launch-only body of a graphed iteration (no host bookkeeping)."""
+        ctx = self.ctx
+        ws = self._ws
+        dst = self.v[:, g:g + 1]
+        res = ws.res1   # the chosen residual column, copied in before replay
+        if self.precond is not None:
+            self.precond._into(res, dst)
+        else:
+            dv.axpby(ctx, 1.0, res, 0.0, dst)
+        st = ws.dgks
+        _lib.call("svdsb_dgks_begin", dv.P(st), ctx.stream)
+        n_, ptrs, lds, cols, _ = dv._blk_args([self.v[:, :g]])
+        for p_ in range(self.SPEC_PASSES):
+            _lib.call("svdsb_cgs_pass", ctx.handle, self.n, n_, ptrs, lds, cols, dv.P(dst), dv.P(self.ortho.c),
+                      dv.P(st), 1 if p_ == 0 else 0, ctx.stream)
+        dv.scale_cols(ctx, dst, st[5:6], dv.SCALE_DIV)
+        self.op.raw_into(dst, self.w[:, g:g + 1])
+        hc = ws.hc1[:g + 1, :]
+        dv.gram(ctx, self.n, [self.v[:, :g + 1]], self.w[:, g:g + 1], hc)
+        dv.h_insert(ctx, g, 1, hc, self.h)
+        gn = g + 1
+        y0 = self.y_d[:g0, :g0] if kind == "prev" else None
+        l0 = self.lams_d[:g0] if kind == "prev" else None
+        dv.syev_update(ctx, self.h, g0, gn - g0, y0, l0, order, shift, self.lams_d[:gn], self.y_d[:gn, :gn])
+        dv.ritz_residual(ctx, self.v[:, :gn], self.w[:, :gn], self.y_d[:gn, :p], self.lams_d[:p],
+                         self.rbuf[:, :p], rn2=self.stat_d[:p])
+        lib = _lib.load()
+        base = ws.status.data_ptr()
+        lib.svdsb_d2h(base, self.lams_d.data_ptr(), 8 * gn, ctx.stream)
+        lib.svdsb_d2h(base + 8 * gn, self.stat_d.data_ptr(), 8 * p, ctx.stream)
+        lib.svdsb_d2h(base + 8 * (gn + p), st.data_ptr(), 64, ctx.stream)
+
+    def _capture(self, fn):
+        ctx = self.ctx
+        graph = torch.cuda.CUDAGraph()
+        cur = torch.cuda.current_stream(ctx.device)
+        cap = torch.cuda.Stream(ctx.device)
+        cap.wait_stream(cur)
+        old = ctx._stream
+        try:
+            with torch.cuda.stream(cap):
+                ctx._stream = cap.cuda_stream
+                graph.capture_begin()
+                try:
+                    fn()
+                finally:
+                    graph.capture_end()
+        finally:
+            ctx._stream = old
+        cur.wait_stream(cap)
+        return graph
+
+    def _expand_graphed(self, ci):
+        g = self.g
+        kind, g0 = self._warm
+        p = min(self.wanted + self.cfg.max_block_size, g + 1)
+        order, shift = self._order_mode()
+        key = (self.v.data_ptr(), self.w.data_ptr(), kind, g0, g, p, order, shift, self.op.graph_key(),
+               None if self.precond is None else self.precond.graph_key)
+        graphs = self._ws.graphs
+        entry = graphs.get(key)
+        if entry is None:
+            before = _lib.launch_count()
+            graph = self._capture(lambda: self._iter_device(g, ci, kind, g0, p, order, shift))
+            entry = (graph, _lib.launch_count() - before)
+            graphs[key] = entry
+            self.stats.graphs_captured += 1
+        # the residual column the host chose goes to the graph's fixed slot
+        dv.axpby(self.ctx, 1.0, self.rbuf[:, ci:ci + 1], 0.0, self._ws.res1)
+        entry[0].replay()
+        _lib.load().svdsb_note_launches(entry[1])
+        # host bookkeeping of what the graph did
+        if self.precond is not None:
+            self.precond.n_applies += 1
+            self.stats.precond_applies += 1
+        self.stats.matvecs += 1
+        self.op.n_applies += 1
+        self.op.count_svd_matvecs(1)
+        self._spec = {"g0": g}
+        self.g = g + 1
+        self._warm = ("prev", g + 1)
+        self._pending = {"p": p}
+
+    def _wait_status(self, g, p):
+        """Synchronise with the queued iteration and read its status."""
+        lib = _lib.load()
+        rc = lib.svdsb_stream_sync(self.ctx._stream)
+        if rc:
+            _lib.check(rc, "svdsb_stream_sync")
+        self.stats.syncs += 1
+        host = self._ws.status.numpy()
+        return [host[:g].copy(), host[g:g + p].copy(), host[g + p:g + p + 8].copy()]
+
+    def _expand(self, res_block, ci=0):
         """eigensolver.py:666-700."""
         b = min(res_block.shape[1], self.gmax - self.g)
         if b <= 0:
             return
         block = res_block[:, :b]
+        if self._graph_ok(b):
+            self._expand_graphed(ci)
+            return
         if self._can_speculate(b):
             self._expand_speculative(block)
             return
@@ -1149,4 +1349,11 @@ def eig_solve(op, cfg, guesses=None, ortho_constraints=None, precond=None, est=N
     (eigensolver.py:788-821)."""
     solver = DavidsonSolver(op, cfg, guesses=guesses, ortho_constraints=ortho_constraints, precond=precond,
                             est=est, est_mode=est_mode)
-    return solver.run()
+    try:
+        return solver.run()
+    finally:
+        # results never alias the pooled buffers (finalisation writes fresh
+        # blocks), so the workspace -- and its captured graphs -- can serve
+        # the next solve of the same shape
+        _release_workspace(solver._ws)
+        solver._ws = None

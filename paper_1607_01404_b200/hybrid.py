@@ -94,6 +94,7 @@ class SvdsStats:
     seconds: float = 0.0
     outer_iterations: int = 0
     syncs: int = 0
+    graphs_captured: int = 0
 
 
 @dataclass
@@ -476,6 +477,7 @@ def _add_stats(stats, r):
     stats.resets += r.stats.resets
     stats.outer_iterations += r.stats.outer_iterations
     stats.syncs += r.stats.syncs
+    stats.graphs_captured += r.stats.graphs_captured
 
 
 def svds_solve(a, precond=None, cfg=None, return_device=False):

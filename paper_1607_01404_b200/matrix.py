@@ -105,6 +105,19 @@ class DeviceCsr:
             e1.record()
             prof.append(("adj" if transpose else "fwd", int(x.shape[1]), e0, e1))
 
+    def scratch(self, rows, cols):
+        """Grow-only column-major scratch block owned by the matrix (the
+        inner product of the normal operator)."""
+        from .device import new_block
+        # single columns get their own never-reallocated buffer: captured
+        # CUDA graphs of the one-column iteration bake its address in
+        attr = "_scratch1" if cols <= 1 else "_scratch"
+        buf = getattr(self, attr, None)
+        if buf is None or buf.shape[0] != rows or buf.shape[1] < cols:
+            buf = new_block(rows, max(cols, 1), device=self.ctx.device, zero=False)
+            setattr(self, attr, buf)
+        return buf[:, :cols]
+
     def precond_diag(self, side, out):
         from .device import P
         _lib.call("svdsb_precond_diag", self.ctx.handle, self.handle, int(side), P(out),

@@ -272,26 +272,36 @@ def make_normal_operator(a):
         dim = a.n if a.m >= a.n else a.m
         inner = a.m if a.m >= a.n else a.n
 
-        def into_native(x, y):
+        # the inner m x b (or n x b) product lives with the matrix, so its
+        # address is stable across solves (graphs captured by the solver
+        # bake it in)
+        def raw_into(x, y):
             from . import _lib
-            from . import matrix
             b = x.shape[1]
-            base.n_matvecs += 2 * b
-            t = scratch.get("t", inner, b, x.device)
+            t = dev.scratch(inner, b)
+            _lib.call("svdsb_apply_normal", dev.ctx.handle, dev.handle, side, dv.P(x), dv.ld_of(x), dv.P(y),
+                      dv.ld_of(y), b, dv.P(t), dv.ld_of(t), dev.ctx.stream)
+
+        def into_native(x, y):
+            from . import matrix
+            base.n_matvecs += 2 * x.shape[1]
             prof = matrix.SPMV_PROFILER
             if prof is not None:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record()
-            _lib.call("svdsb_apply_normal", dev.ctx.handle, dev.handle, side, dv.P(x), dv.ld_of(x), dv.P(y),
-                      dv.ld_of(y), b, dv.P(t), dv.ld_of(t), dev.ctx.stream)
+            raw_into(x, y)
             if prof is not None:
                 e1.record()
-                prof.append(("normal", b, e0, e1))
+                prof.append(("normal", x.shape[1], e0, e1))
 
         op = LinearOperator(dim, into=into_native)
         op.svd_op = a
         op.kind = "normal"
+        op.raw_into = raw_into
+        # evaluated at capture / replay time: includes the scratch address
+        op.graph_key = lambda: ("normal", dev.handle.value, side, dev.scratch(inner, 1).data_ptr())
+        op.count_svd_matvecs = lambda cols: setattr(base, "n_matvecs", base.n_matvecs + 2 * cols)
         return op
     if a.m >= a.n:
         def into(x, y):
@@ -408,6 +418,7 @@ def jacobi_precond_on_normal(a, side="cols"):
 
     pre = Preconditioner(mode, into=into)
     pre.diagonal = d
+    pre.graph_key = ("jacobi", d.data_ptr())
     return pre
 
 

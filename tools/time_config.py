@@ -15,8 +15,8 @@ t1 = time.perf_counter()
 a = SparseMatrixCsr.from_coo(m, n, r, c, v)
 torch.cuda.synchronize(); t2 = time.perf_counter()
 print(f"{key} m={m} n={n} nnz={a.nnz} gen {t1-t0:.2f}s build {t2-t1:.2f}s", flush=True)
+pre = jacobi_precond_on_normal(a, side='auto') if wl.precond else None
 for rep in range(reps):
-    pre = jacobi_precond_on_normal(a, side='auto') if wl.precond else None
     cfg = SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0, max_matvecs=budget)
     l0 = _lib.launch_count()
     torch.cuda.synchronize(); t = time.perf_counter()
@@ -25,4 +25,4 @@ for rep in range(reps):
     s = res.stats
     print(json.dumps({"rep": rep, "sec": round(dt, 4), "sigma": res.sigma.tolist(), "rnorms_max": float(res.rnorms.max()),
         "conv": bool(res.converged.all()), "status": res.status, "mv1": s.stage1_matvecs, "mv2": s.stage2_matvecs,
-        "restarts": s.restarts, "iters": s.outer_iterations, "syncs": s.syncs, "launches": _lib.launch_count() - l0}), flush=True)
+        "restarts": s.restarts, "iters": s.outer_iterations, "syncs": s.syncs, "graphs": s.graphs_captured, "launches": _lib.launch_count() - l0}), flush=True)
