@@ -160,9 +160,11 @@ int svdsb_project_out(svdsb_ctx *ctx, int64_t dim, int nblk,
                       const double *const *xs, const int64_t *ldxs,
                       const int *cols, const double *c, int64_t ldc, double *y,
                       int64_t ldy, int b, double *norms2, void *stream);
-/* Y = alpha * X C + beta * Y ; X dim x g, C (device) g x s.  Y must not
- * alias X.  Replaces V @ coefs (eigensolver.py:526-527), V @ y (:390,
- * :710, :760).  beta == 0 never reads Y. */
+/* Y = alpha * X C + beta * Y ; X dim x g, C (device) g x s.  Replaces
+ * V @ coefs (eigensolver.py:526-527), V @ y (:390, :710, :760).  beta == 0
+ * never reads Y.  Y may alias X only exactly (y == x, ldy == ldx: the
+ * in-place restart V <- V C) with s <= min(g, 32), alpha 1, beta 0; any
+ * other overlap is undefined. */
 int svdsb_ts_gemm(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx,
                   int g, const double *c, int64_t ldc, int s, double alpha,
                   double beta, double *y, int64_t ldy, void *stream);

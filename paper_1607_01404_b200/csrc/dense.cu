@@ -736,6 +736,41 @@ ts_gemm_vec_kernel(int64_t dim, const double *__restrict__ x, int64_t ldx, int g
   }
 }
 
+// In-place Y[:, :s] = X[:, :g] C (Y aliases X, s <= g): every output row
+// depends only on the same input row, so one thread reads its whole row
+// before it writes any of it and no other thread touches that row.  No
+// __restrict__ / read-only cache on the aliased block.
+template <int ST>
+__global__ void __launch_bounds__(kThreads)
+ts_gemm_inplace_kernel(int64_t dim, double *x, int64_t ldx, int g, const double *__restrict__ cmat, int64_t ldc,
+                       int s) {
+  extern __shared__ double csh[];  // g x ST
+  for (int k = threadIdx.x; k < g * ST; k += kThreads) {
+    int i = k / ST, j = k % ST;
+    csh[k] = (j < s) ? cmat[i + (int64_t)j * ldc] : 0.0;
+  }
+  __syncthreads();
+  RowRange rr = cta_rows(dim);
+  for (int64_t r = rr.r0 + threadIdx.x; r < rr.r1; r += kThreads) {
+    double acc[ST];
+#pragma unroll
+    for (int j = 0; j < ST; ++j) acc[j] = 0.0;
+    for (int i = 0; i < g; ++i) {
+      double xv = x[r + (int64_t)i * ldx];
+      const double2 *crow = reinterpret_cast<const double2 *>(csh + i * ST);
+#pragma unroll
+      for (int j = 0; j < ST / 2; ++j) {
+        double2 cf = crow[j];
+        acc[2 * j] = fma(xv, cf.x, acc[2 * j]);
+        acc[2 * j + 1] = fma(xv, cf.y, acc[2 * j + 1]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < ST; ++j)
+      if (j < s) x[r + (int64_t)j * ldx] = acc[j];
+  }
+}
+
 static inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 static bool colset_vec_ok(const ColSet &s) {
@@ -852,6 +887,20 @@ int svdsb_ts_gemm(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx, int
   if (g == 0) {
     // Y = beta Y
     return svdsb_axpby(dim, s, 0.0, y, ldy, beta, y, ldy, stream);
+  }
+  if (x == y) {
+    SVDSB_CHECK_ARG(ldx == ldy && s <= g && s <= 32 && alpha == 1.0 && beta == 0.0,
+                    "svdsb_ts_gemm: in-place needs ldy == ldx, s <= min(g, 32), alpha 1, beta 0");
+    size_t sh = sizeof(double) * g * 32;
+    static bool attr = false;
+    if (!attr) {
+      SVDSB_CUDA(cudaFuncSetAttribute(ts_gemm_inplace_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(double) * 256 * 32)));
+      attr = true;
+    }
+    ts_gemm_inplace_kernel<32><<<grid_rows(dim), kThreads, sh, st>>>(dim, y, ldy, g, c, ldc, s);
+    SVDSB_LAUNCHED();
+    return SVDSB_OK;
   }
   constexpr int ST = 16;
   if (s <= ST && aligned16(x) && aligned16(y) && !(ldx & 1) && !(ldy & 1)) {

@@ -310,6 +310,7 @@ class _Workspace:
         self.orthoc = torch.zeros(4 * _lib.SMALL_MAX * 4, dtype=DTYPE, device=dv.context().device)
         self.status = torch.zeros(2 * gm + 32, dtype=DTYPE, pin_memory=True)
         self.graphs = {}
+        self.graph_owner = None
 
     def reset(self):
         self.h.zero_()
@@ -392,6 +393,13 @@ class DavidsonSolver:
             self.rbuf, self.stat_d, self.coefs, self.count_d = ws.rbuf, ws.stat, ws.coefs, ws.count
             self.prev_d, self.yref, self.excl = ws.prev, ws.yref, ws.excl
             self.ortho.c = ws.orthoc
+            # a workspace keeps the graphs of one operator: a new operator
+            # drops them (they reference its device arrays)
+            gk = getattr(op, "graph_key", None)
+            owner = gk() if gk is not None else None
+            if ws.graph_owner != owner:
+                ws.graphs.clear()
+                ws.graph_owner = owner
         else:
             self.v = dv.new_block(self.n, gm)
             self.w = dv.new_block(self.n, gm)
@@ -789,11 +797,17 @@ class DavidsonSolver:
         self._update_h_full()
 
     def _swap_basis(self, s):
+        g = self.g
+        c = self.coefs[:g, :s]
+        if s <= 32:
+            # row-local in-place V <- V C: the basis keeps its address, so the
+            # captured iteration graphs do not come in two copies
+            dv.ts_gemm(self.ctx, self.v[:, :g], c, self.v[:, :s])
+            dv.ts_gemm(self.ctx, self.w[:, :g], c, self.w[:, :s])
+            return
         if self._v2 is None:
             self._v2 = dv.new_block(self.n, max(self.gmax, 1))
             self._w2 = dv.new_block(self.n, max(self.gmax, 1))
-        g = self.g
-        c = self.coefs[:g, :s]
         dv.ts_gemm(self.ctx, self.v[:, :g], c, self._v2[:, :s])
         dv.ts_gemm(self.ctx, self.w[:, :g], c, self._w2[:, :s])
         self.v, self._v2 = self._v2, self.v

@@ -11,6 +11,7 @@ lazily only when someone asks for them.
 """
 
 import ctypes
+import itertools
 
 import numpy as np
 import torch
@@ -22,11 +23,16 @@ from .device import context, require_cuda
 # end_event) with kind in fwd / adj / normal (both products) recorded on the launching stream (bench.py's roofline probe).
 SPMV_PROFILER = None
 
+_UIDS = itertools.count(1)
+
 
 class DeviceCsr:
     """Owning handle to a libsvdsb CSR (A and A^T) on one device."""
 
     def __init__(self, handle, ctx, m, n, nnz):
+        # process-unique id: a freed handle's address can be reused by the
+        # next matrix, so captured graphs are keyed by this instead
+        self.uid = next(_UIDS)
         self.handle = handle
         self.ctx = ctx
         self.m, self.n, self.nnz = int(m), int(n), int(nnz)

@@ -300,7 +300,7 @@ def make_normal_operator(a):
         op.kind = "normal"
         op.raw_into = raw_into
         # evaluated at capture / replay time: includes the scratch address
-        op.graph_key = lambda: ("normal", dev.handle.value, side, dev.scratch(inner, 1).data_ptr())
+        op.graph_key = lambda: ("normal", dev.uid, side, dev.scratch(inner, 1).data_ptr())
         op.count_svd_matvecs = lambda cols: setattr(base, "n_matvecs", base.n_matvecs + 2 * cols)
         return op
     if a.m >= a.n:

@@ -196,6 +196,27 @@ def test_gram_project_tsgemm(dim, rng):
     assert np.abs(dv.to_host(out) - want).max() <= 1e-13 * np.abs(want).max() * 4
 
 
+@pytest.mark.parametrize("dim", [7, 100003])
+@pytest.mark.parametrize("g,s", [(35, 15), (40, 32), (3, 1)])
+def test_ts_gemm_inplace_matches_out_of_place(dim, g, s, rng):
+    """The in-place restart V <- V C is bit-identical to the out-of-place
+    product (same fma order per row)."""
+    dv = _dev()
+    ctx = dv.context()
+    a = rng.standard_normal((dim, g))
+    cm = dv.to_device_block(rng.standard_normal((g, s)))
+    x = dv.to_device_block(a)
+    ref = dv.new_block(dim, s)
+    dv.ts_gemm(ctx, x, cm, ref)
+    dv.ts_gemm(ctx, x, cm, x[:, :s])
+    assert np.array_equal(dv.to_host(x[:, :s]), dv.to_host(ref))
+    assert np.array_equal(dv.to_host(x[:, s:]), a[:, s:])
+    if g >= 3:
+        # in place with more outputs than inputs is rejected, not raced
+        with pytest.raises(ValueError):
+            dv.ts_gemm(ctx, x[:, :2], dv.to_device_block(rng.standard_normal((2, 3))), x[:, :3])
+
+
 @pytest.mark.parametrize("dim", [50, 100003])
 @pytest.mark.parametrize("p", [1, 11, 24])
 def test_ritz_residual(dim, p, rng):

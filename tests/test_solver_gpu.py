@@ -191,3 +191,34 @@ def test_eig_solve_diag_largest_and_locking():
                                           convergence_test=lambda lam, rn, x, ox, c: rn <= 1e-10, seed=7))
     assert res.converged.all()
     assert np.allclose(res.eigenvalues, [1.0, 2.0, 3.0], atol=1e-8)
+
+
+def test_graph_cache_across_matrices_and_repeats():
+    """Captured iteration graphs bake device addresses: solving a sequence of
+    freshly assembled matrices of one shape (addresses get reused) and
+    repeating a solve must give exactly the graph-free result every time."""
+    from paper_1607_01404_b200 import SparseMatrixCsr, SvdsConfig, jacobi_precond_on_normal, svds_solve, workloads
+    from paper_1607_01404_b200.eigensolver import DavidsonSolver
+    wl = workloads.CONFIGS["c2"]
+    m, n, r, c, v = wl.build(**workloads.SMALL["c2"])
+    cfg = dict(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0)
+
+    def solve(scale):
+        a = SparseMatrixCsr.from_coo(m, n, r, c, v * scale)
+        pre = jacobi_precond_on_normal(a, side="auto")
+        res = svds_solve(a, precond=pre, cfg=SvdsConfig(**cfg))
+        return res.sigma.copy(), res.stats.stage1_matvecs, res.stats.graphs_captured
+
+    saved = DavidsonSolver.use_graphs
+    try:
+        DavidsonSolver.use_graphs = False
+        plain = [solve(s)[:2] for s in (1.0, 2.0)]
+        DavidsonSolver.use_graphs = True
+        runs = [solve(s) for s in (1.0, 2.0, 1.0, 2.0)]
+    finally:
+        DavidsonSolver.use_graphs = saved
+    assert any(g > 0 for _, _, g in runs)
+    for i, (sig, mv, _) in enumerate(runs):
+        want_sig, want_mv = plain[i % 2]
+        assert mv == want_mv
+        assert np.array_equal(sig, want_sig)

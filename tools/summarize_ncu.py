@@ -11,7 +11,8 @@ def launches(path, top=25):
         if len(r) <= mv: continue
         try: v = float(r[mv].replace(',', ''))
         except ValueError: continue
-        scale = {'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3, 'second': 1e6}.get(r[mu], 1.0)
+        scale = {'ns': 1e-3, 'nsecond': 1e-3, 'us': 1.0, 'usecond': 1.0, 'ms': 1e3, 'msecond': 1e3,
+                 's': 1e6, 'second': 1e6}[r[mu]]
         name = r[ki].split('(')[0].replace('void ', '')
         tot[name] += v * scale; cnt[name] += 1
     T = sum(tot.values())
