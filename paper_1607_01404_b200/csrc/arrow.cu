@@ -35,6 +35,7 @@ struct ArrowSmem {
   int korg[kAN + 1];               // root origin (sorted pole index)
   double zhat[kAN];
   double newd[kAN + 1];            // eigenvalues in output column order
+  double hcol[kAN + 1];            // bordering column of H, staged once
   // Givens rotations from type-2 deflation (original index pairs)
   int ra[kAN], rb[kAN];
   double rc[kAN], rs[kAN];
@@ -305,6 +306,8 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
   double *T = P + G * ld;      // product scratch
   double *lam = T + G * ld;    // current eigenvalues
   const int tid = threadIdx.x, nt = blockDim.x;
+  pdl_wait();
+  pdl_trigger();
   for (int e = tid; e < G * G; e += nt) {
     int i = e % G, j = e / G;
     double v = 0.0;
@@ -315,14 +318,17 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
   __syncthreads();
   for (int j = 0; j < b; ++j) {
     const int sdim = g0 + j;  // current size; new index sdim
-    // z = Y^T H[:sdim, sdim]
+    // one parallel global read of the border column, then z = Y^T H[:sdim, sdim]
+    // from shared memory (a k-loop over global loads is a latency chain)
+    for (int k = tid; k <= sdim; k += nt) s.hcol[k] = h[k + (int64_t)sdim * ldh];
+    __syncthreads();
     for (int i = tid; i < sdim; i += nt) {
       double acc = 0.0;
-      for (int k = 0; k < sdim; ++k) acc = fma(Y[k + i * ld], h[k + (int64_t)sdim * ldh], acc);
+      for (int k = 0; k < sdim; ++k) acc = fma(Y[k + i * ld], s.hcol[k], acc);
       s.z[i] = acc;
       s.d[i] = lam[i];
     }
-    if (tid == 0) s.alpha = h[sdim + (int64_t)sdim * ldh];
+    if (tid == 0) s.alpha = s.hcol[sdim];
     __syncthreads();
     arrow_solve(s, sdim, P, ld);
     // Y <- blkdiag(Y, 1) P   (size sdim+1)
@@ -402,7 +408,7 @@ extern "C" int svdsb_syev_update(int g0, int b, const double *h, int64_t ldh, co
   }
   const int G = g0 + b;
   size_t sh = sizeof(double) * (3 * G * (G + 1) + G + 1);
-  syev_update_kernel<<<1, kAT, sh, as_stream(stream)>>>(g0, b, h, ldh, y0, ldy0, l0, order, shift, w, y, ldy);
-  SVDSB_LAUNCHED();
+  SVDSB_LAUNCH_PDL(syev_update_kernel, 1, kAT, sh, as_stream(stream), g0, b, h, ldh, y0, ldy0, l0, order, shift, w, y,
+                   ldy);
   return SVDSB_OK;
 }

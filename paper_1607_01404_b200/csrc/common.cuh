@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string>
+#include <utility>
 
 #include "../../include/svdsb.h"
 
@@ -49,6 +50,48 @@ int64_t bump_launches(int n = 1);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Programmatic dependent launch.  The per-iteration kernels are launched
+// with programmatic stream serialisation so a kernel's launch overlaps the
+// tail of the one before it (also inside captured graphs).  Every kernel
+// launched through launch_k() calls pdl_wait() before it touches memory --
+// that blocks until the preceding grid has completed and its writes are
+// visible -- and may call pdl_trigger() once its own main loop is done to let
+// the next grid's CTAs be scheduled early.  SVDSB_PDL=0 turns the attribute
+// off (plain stream order; pdl_wait() is then a no-op).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_on();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// Launch through launch_k and account for it (use inside int-returning
+// C-ABI functions).
+#define SVDSB_LAUNCH_PDL(...)                                             \
+  do {                                                                    \
+    cudaError_t e_ = ::svdsb::launch_k(__VA_ARGS__);                      \
+    if (e_ != cudaSuccess) {                                              \
+      ::svdsb::set_error("%s:%d launch: %s", __FILE__, __LINE__,          \
+                         cudaGetErrorString(e_));                         \
+      return SVDSB_ERR_CUDA;                                              \
+    }                                                                     \
+    ::svdsb::bump_launches();                                             \
+  } while (0)
+
 }  // namespace svdsb
 
 // Reduction workspace: per-CTA partial sums then a ticket so the last CTA
@@ -77,6 +120,25 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Last-CTA fold of per-CTA partials laid out as
+//   partials[(t * nparts + bx) * per + k],  output o = t * per + k < nout,
+// by the whole CTA: one warp per output, lanes take a fixed strided subset of
+// the nparts CTAs and a fixed xor tree combines them, so the result is
+// deterministic and the load chain is nparts / 32 deep instead of nparts.
+// emit(o, t, k, sum) is called by lane 0 of the owning warp.
+template <typename Emit>
+__device__ __forceinline__ void fold_parts(const double *partials, unsigned nparts, int per, int nout, Emit emit) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = w; o < nout; o += nw) {
+    const int t = o / per, k = o % per;
+    const double *pp = partials + (int64_t)t * nparts * per + k;
+    double s = 0.0;
+    for (unsigned bx = lane; bx < nparts; bx += 32) s += pp[(int64_t)bx * per];
+    s = warp_sum(s);
+    if (lane == 0) emit(o, t, k, s);
+  }
 }
 
 // Returns true in exactly one CTA: the last to arrive at the ticket.  All

@@ -289,6 +289,7 @@ csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
     rb = (t == 0 && nrows >= kTileThreads) ? __ldg(row_ptr + ti.x + kTileThreads) : 0;
   };
   issue(cur, v, c, rpa, rpb);
+  pdl_wait();  // matrix data is immutable after assembly; x / y are not
   int buf = 0;
   while (true) {
     const int next_tile = tile + gridDim.x;
@@ -328,6 +329,7 @@ csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
     rpb = rnb;
     buf ^= 1;
   }
+  pdl_trigger();
 }
 
 // Pipelined variant for row-major block operands (2 <= b <= 4): one x-row
@@ -367,6 +369,7 @@ csr_tile_pipe_rows_kernel(int ntile, const int4 *__restrict__ info, const int *_
     rb = (t == 0 && nrows >= kTileThreads) ? __ldg(row_ptr + ti.x + kTileThreads) : 0;
   };
   issue(cur, v, c, rpa, rpb);
+  pdl_wait();
   while (true) {
     const int next_tile = tile + gridDim.x;
     int4 nxt = make_int4(0, 0, 0, 0);
@@ -503,6 +506,7 @@ __global__ void __launch_bounds__(kTileThreads)
 csr_chunk_kernel(const int *__restrict__ chunk_nz, const int *__restrict__ col,
                  const double *__restrict__ val, const double *__restrict__ x,
                  int64_t ldx, int xrow, int b, double *__restrict__ part) {
+  pdl_wait();
   __shared__ double red[kTileThreads / 32][4];
   const int nz0 = chunk_nz[2 * blockIdx.x], nz1 = chunk_nz[2 * blockIdx.x + 1];
   const int t = threadIdx.x;
@@ -564,6 +568,7 @@ __global__ void csr_long_fixup_kernel(int nlong, const int *__restrict__ long_ro
                                       const int *__restrict__ long_cptr,
                                       const double *__restrict__ part, int b,
                                       double *__restrict__ y, int64_t ldy, int yrow, int accumulate) {
+  pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= nlong * b) return;
@@ -674,13 +679,12 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
       if (yrow) {
         auto k = csr_tile_pipe_rows_kernel<ORDER, 1>;
         const int g = std::min(p.ntile, pipe_rows_grid(reinterpret_cast<const void *>(k), sm));
-        k<<<g, kTileThreads, sm, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, x, y, ldy, b, acc);
+        SVDSB_LAUNCH_PDL(k, g, kTileThreads, sm, st, p.ntile, p.tile_info, p.row_ptr, p.col, p.val, x, y, ldy, b, acc);
       } else {
         auto k = csr_tile_pipe_rows_kernel<ORDER, 0>;
         const int g = std::min(p.ntile, pipe_rows_grid(reinterpret_cast<const void *>(k), sm));
-        k<<<g, kTileThreads, sm, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, x, y, ldy, b, acc);
+        SVDSB_LAUNCH_PDL(k, g, kTileThreads, sm, st, p.ntile, p.tile_info, p.row_ptr, p.col, p.val, x, y, ldy, b, acc);
       }
-      SVDSB_LAUNCHED();
     } else if (p.ntile > 0) {
       if (acc) {
         set_error("accumulating SpMV needs row-major input");
@@ -691,12 +695,11 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
       SVDSB_LAUNCHED();
     }
     if (p.nlong > 0) {
-      csr_chunk_kernel<<<p.nchunk, kTileThreads, 0, st>>>(p.chunk_nz, p.col, p.val, x, ldx, xrow, b, p.chunk_part);
-      SVDSB_LAUNCHED();
+      SVDSB_LAUNCH_PDL(csr_chunk_kernel, p.nchunk, kTileThreads, 0, st, p.chunk_nz, p.col, p.val, x, ldx, xrow, b,
+                       p.chunk_part);
       int tot = p.nlong * b;
-      csr_long_fixup_kernel<<<(tot * 32 + 255) / 256, 256, 0, st>>>(p.nlong, p.long_row, p.long_cptr, p.chunk_part, b,
-                                                                    y, ldy, yrow, acc);
-      SVDSB_LAUNCHED();
+      SVDSB_LAUNCH_PDL(csr_long_fixup_kernel, (tot * 32 + 255) / 256, 256, 0, st, p.nlong, p.long_row, p.long_cptr,
+                       p.chunk_part, b, y, ldy, yrow, acc);
     }
     return SVDSB_OK;
   }
@@ -712,25 +715,23 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
       if (p.maxlen <= 8) {
         auto k = csr_tile_pipe_kernel<ORDER, true>;
         const int g = std::min(p.ntile, pipe_grid(reinterpret_cast<const void *>(k)));
-        k<<<g, kTileThreads, 0, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc, acc);
+        SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc, acc);
       } else {
         auto k = csr_tile_pipe_kernel<ORDER, false>;
         const int g = std::min(p.ntile, pipe_grid(reinterpret_cast<const void *>(k)));
-        k<<<g, kTileThreads, 0, st>>>(p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc, acc);
+        SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc, acc);
       }
-      SVDSB_LAUNCHED();
     } else if (p.ntile > 0) {
       csr_tile_kernel<ORDER, 0, 0, 1><<<p.ntile, kTileThreads, 0, st>>>(p.tile_r, p.row_ptr, p.col, p.val, xc, ldx,
                                                                        yc, ldy, bb);
       SVDSB_LAUNCHED();
     }
     if (p.nlong > 0) {
-      csr_chunk_kernel<<<p.nchunk, kTileThreads, 0, st>>>(p.chunk_nz, p.col, p.val, xc, ldx, 0, bb, p.chunk_part);
-      SVDSB_LAUNCHED();
+      SVDSB_LAUNCH_PDL(csr_chunk_kernel, p.nchunk, kTileThreads, 0, st, p.chunk_nz, p.col, p.val, xc, ldx, 0, bb,
+                       p.chunk_part);
       int tot = p.nlong * bb;
-      csr_long_fixup_kernel<<<(tot * 32 + 255) / 256, 256, 0, st>>>(p.nlong, p.long_row, p.long_cptr, p.chunk_part, bb,
-                                                                    yc, ldy, 0, acc);
-      SVDSB_LAUNCHED();
+      SVDSB_LAUNCH_PDL(csr_long_fixup_kernel, (tot * 32 + 255) / 256, 256, 0, st, p.nlong, p.long_row, p.long_cptr,
+                       p.chunk_part, bb, yc, ldy, 0, acc);
     }
   }
   return SVDSB_OK;
@@ -1330,6 +1331,7 @@ __global__ void clamp_kernel(int64_t n, double *__restrict__ d, const double *__
 
 __global__ void diag_solve_kernel(int64_t dim, int b, const double *__restrict__ d, const double *x, int64_t ldx,
                                   double *y, int64_t ldy) {
+  pdl_wait();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= dim) return;
   double di = d[i];
@@ -1366,8 +1368,7 @@ int svdsb_precond_diag(svdsb_ctx *ctx, const svdsb_csr *a, int side, double *d, 
 int svdsb_diag_solve(int64_t dim, const double *d, const double *x, int64_t ldx, double *y, int64_t ldy, int block,
                      void *stream) {
   if (dim == 0 || block == 0) return SVDSB_OK;
-  diag_solve_kernel<<<grid1(dim), 256, 0, as_stream(stream)>>>(dim, block, d, x, ldx, y, ldy);
-  SVDSB_LAUNCHED();
+  SVDSB_LAUNCH_PDL(diag_solve_kernel, grid1(dim), 256, 0, as_stream(stream), dim, block, d, x, ldx, y, ldy);
   return SVDSB_OK;
 }
 

@@ -137,12 +137,8 @@ gram_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t ldy, i
   cta_fold<NOUT>(acc, NOUT, part);
   if (!last_cta(ticket)) return;
   const int ntile = gridDim.y * gridDim.z;
-  for (int o = threadIdx.x; o < ntile * NOUT; o += kThreads) {
-    const int t = o / NOUT, k = o % NOUT;
+  fold_parts(partials, gridDim.x, NOUT, ntile * NOUT, [&](int, int t, int k, double s) {
     const int tyy = t / gridDim.z, tzz = t % gridDim.z;
-    double s = 0.0;
-    const double *pp = partials + (int64_t)t * gridDim.x * NOUT + k;
-    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * NOUT];
     if (k < AT * BT) {
       int i = tyy * AT + k / BT, j = tzz * BT + k % BT;
       if (i < xs.total && j < b) c[i + (int64_t)j * ldc] = s;
@@ -150,7 +146,7 @@ gram_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t ldy, i
       int j = tzz * BT + (k - AT * BT);
       if (j < b) norms2[j] = s;
     }
-  }
+  });
 }
 
 // ------------------------------------------------------------ project out
@@ -193,11 +189,7 @@ project_kernel(int64_t dim, ColSet xs, const double *__restrict__ cmat, int64_t 
   double *part = partials + (int64_t)blockIdx.x * BT;
   cta_fold<BT>(nacc, BT, part);
   if (!last_cta(ticket)) return;
-  for (int j = threadIdx.x; j < b; j += kThreads) {
-    double s = 0.0;
-    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += partials[(int64_t)bx * BT + j];
-    norms2[j] = s;
-  }
+  fold_parts(partials, gridDim.x, BT, b, [&](int j, int, int, double s) { norms2[j] = s; });
 }
 
 // ---------------------------------------------------------------- ts_gemm
@@ -289,14 +281,9 @@ ritz_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const double
   double *part = partials + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * PT;
   cta_fold<PT>(nacc, PT, part);
   if (!last_cta(ticket)) return;
-  for (int o = threadIdx.x; o < (int)gridDim.y * PT; o += kThreads) {
-    int ty = o / PT, j = o % PT;
-    if (ty * PT + j >= p) continue;
-    double s = 0.0;
-    const double *pp = partials + (int64_t)ty * gridDim.x * PT + j;
-    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * PT];
-    rn2[ty * PT + j] = s;
-  }
+  fold_parts(partials, gridDim.x, PT, (int)gridDim.y * PT, [&](int o, int, int, double s) {
+    if (o < p) rn2[o] = s;
+  });
 }
 
 // -------------------------------------------------------- norms and dots
@@ -319,14 +306,9 @@ coldot_kernel(int64_t dim, const double *__restrict__ x, int64_t ldx, const doub
   double *part = partials + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * BT;
   cta_fold<BT>(acc, BT, part);
   if (!last_cta(ticket)) return;
-  for (int o = threadIdx.x; o < (int)gridDim.y * BT; o += kThreads) {
-    int ty = o / BT, j = o % BT;
-    if (ty * BT + j >= b) continue;
-    double s = 0.0;
-    const double *pp = partials + (int64_t)ty * gridDim.x * BT + j;
-    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * BT];
-    out[ty * BT + j] = s;
-  }
+  fold_parts(partials, gridDim.x, BT, (int)gridDim.y * BT, [&](int o, int, int, double s) {
+    if (o < b) out[o] = s;
+  });
 }
 
 template <int BT>
@@ -355,14 +337,9 @@ split_kernel(int64_t dim, int64_t nsplit, const double *__restrict__ r, int64_t 
   double *part = partials + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 6 * BT;
   cta_fold<6 * BT>(acc, 6 * BT, part);
   if (!last_cta(ticket)) return;
-  for (int o = threadIdx.x; o < (int)gridDim.y * 6 * BT; o += kThreads) {
-    int ty = o / (6 * BT), k = o % (6 * BT);
-    if (ty * BT + k / 6 >= b) continue;
-    double s = 0.0;
-    const double *pp = partials + (int64_t)ty * gridDim.x * 6 * BT + k;
-    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * 6 * BT];
-    out[ty * 6 * BT + k] = s;
-  }
+  fold_parts(partials, gridDim.x, 6 * BT, (int)gridDim.y * 6 * BT, [&](int o, int ty, int k, double s) {
+    if (ty * BT + k / 6 < b) out[o] = s;
+  });
 }
 
 template <int BT>
@@ -408,20 +385,16 @@ split_res_kernel(int64_t dim, int64_t nsplit, const double *__restrict__ r, int6
   double *part = partials + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * BT;
   cta_fold<BT>(acc, BT, part);
   if (!last_cta(ticket)) return;
-  for (int o = threadIdx.x; o < (int)gridDim.y * BT; o += kThreads) {
-    int ty = o / BT, j = o % BT;
-    int jj = ty * BT + j;
-    if (jj >= b) continue;
-    double s = 0.0;
-    const double *pp = partials + (int64_t)ty * gridDim.x * BT + j;
-    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * BT];
+  fold_parts(partials, gridDim.x, BT, (int)gridDim.y * BT, [&](int jj, int, int, double s) {
+    if (jj >= b) return;
     const double *st = stats + 6 * jj;
     out[jj] = (st[2] > 0.0 && st[5] > 0.0) ? s : __longlong_as_double(0x7ff0000000000000LL);
-  }
+  });
 }
 
 __global__ void scale_kernel(int64_t dim, const double *x, int64_t ldx, int b, const double *__restrict__ s, int mode,
                              double *y, int64_t ldy) {
+  pdl_wait();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= dim) return;
   for (int j = 0; j < b; ++j) {
@@ -444,6 +417,7 @@ __global__ void scale_kernel(int64_t dim, const double *x, int64_t ldx, int b, c
 
 __global__ void axpby_kernel(int64_t dim, int b, double alpha, const double *x, int64_t ldx, double beta, double *y,
                              int64_t ldy) {
+  pdl_wait();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= dim) return;
   for (int j = 0; j < b; ++j) {
@@ -474,6 +448,7 @@ template <int AT>
 __global__ void __launch_bounds__(kThreads)
 gram1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, double *c, double *norms2, double *partials,
                  unsigned int *ticket, const double *gate) {
+  pdl_wait();
   if (gate != nullptr && gate[0] == 0.0) return;  // device-side DGKS: column already final
   __shared__ const double *xp[AT];
   const int ty = blockIdx.y;
@@ -505,22 +480,19 @@ gram1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, double *c
       if (i < na) acc[i] = fma(__ldg(xp[i] + r), yv, acc[i]);
     if (want_norm) acc[AT] = fma(yv, yv, acc[AT]);
   }
+  pdl_trigger();
   constexpr int NOUT = AT + 1;
   double *part = partials + ((int64_t)ty * gridDim.x + blockIdx.x) * NOUT;
   cta_fold<NOUT>(acc, NOUT, part);
   if (!last_cta(ticket)) return;
-  for (int o = threadIdx.x; o < (int)gridDim.y * NOUT; o += kThreads) {
-    const int t = o / NOUT, k = o % NOUT;
-    double s = 0.0;
-    const double *pp = partials + (int64_t)t * gridDim.x * NOUT + k;
-    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += pp[(int64_t)bx * NOUT];
+  fold_parts(partials, gridDim.x, NOUT, (int)gridDim.y * NOUT, [&](int, int t, int k, double s) {
     if (k < AT) {
       int i = t * AT + k;
       if (i < xs.total) c[i] = s;
     } else if (norms2 != nullptr && t == 0) {
       norms2[0] = s;
     }
-  }
+  });
 }
 
 // One step of the iterated-CGS decision of kernels.py:115-127, on device.
@@ -557,12 +529,15 @@ __device__ __forceinline__ void dgks_decide(double *st) {
 }
 
 __global__ void dgks_begin_kernel(double *st) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x < 8) st[threadIdx.x] = (threadIdx.x == 0) ? 1.0 : 0.0;
 }
 
 __global__ void __launch_bounds__(kThreads)
 project1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ cvec, double *y, double *norms2,
                     double *partials, unsigned int *ticket, double *dgks) {
+  pdl_wait();
   if (dgks != nullptr && dgks[0] == 0.0) return;
   extern __shared__ double csh[];
   __shared__ const double *xp[256];
@@ -603,16 +578,15 @@ project1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ cvec, dou
     y[r] = yv;
     nacc = fma(yv, yv, nacc);
   }
+  pdl_trigger();
   if (norms2 == nullptr) return;
   double accs[1] = {nacc};
   cta_fold<1>(accs, 1, partials + blockIdx.x);
   if (!last_cta(ticket)) return;
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += partials[bx];
+  fold_parts(partials, gridDim.x, 1, 1, [&](int, int, int, double s) {
     norms2[0] = s;
     if (dgks != nullptr) dgks_decide(dgks);
-  }
+  });
 }
 
 // R = W Y - V Y diag(lam) for p <= PT candidates in one pass over V, W.
@@ -622,6 +596,7 @@ ritz_wide_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const d
                  int g, const double *__restrict__ yc, int64_t ldyc, const double *__restrict__ lam, int p,
                  double *__restrict__ r, int64_t ldr, double *__restrict__ xo, int64_t ldx, double *__restrict__ oxo,
                  int64_t ldox, double *rn2, double *partials, unsigned int *ticket) {
+  pdl_wait();
   extern __shared__ double ysh[];  // g x PT
   __shared__ double lsh[PT];
   for (int k = threadIdx.x; k < g * PT; k += kThreads) {
@@ -665,14 +640,11 @@ ritz_wide_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const d
       }
     }
   }
+  pdl_trigger();
   double *part = partials + (int64_t)blockIdx.x * PT;
   cta_fold<PT>(nacc, PT, part);
   if (!last_cta(ticket)) return;
-  for (int j = threadIdx.x; j < p; j += kThreads) {
-    double s = 0.0;
-    for (unsigned bx = 0; bx < gridDim.x; ++bx) s += partials[(int64_t)bx * PT + j];
-    rn2[j] = s;
-  }
+  fold_parts(partials, gridDim.x, PT, p, [&](int j, int, int, double s) { rn2[j] = s; });
 }
 
 // Y = alpha X C + beta Y, two rows per thread, s <= ST.
@@ -823,12 +795,15 @@ int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, c
   if (b == 1 && colset_vec_ok(s) && aligned16(y)) {
     if (s.total <= 16) {
       dim3 grid(grid_for(gram1_vec_kernel<16>, dim, 0), 1, 1);
-      gram1_vec_kernel<16><<<grid, kThreads, 0, st>>>(dim, s, y, c, norms2, ctx->partials, take_ticket(ctx), nullptr);
+      SVDSB_LAUNCH_PDL(gram1_vec_kernel<16>, grid, kThreads, 0, st, dim, s, y, c, norms2, ctx->partials,
+                       take_ticket(ctx), nullptr);
     } else {
       constexpr int AT = 40;
       dim3 grid(grid_for(gram1_vec_kernel<AT>, dim, 0), (s.total + AT - 1) / AT, 1);
-      gram1_vec_kernel<AT><<<grid, kThreads, 0, st>>>(dim, s, y, c, norms2, ctx->partials, take_ticket(ctx), nullptr);
+      SVDSB_LAUNCH_PDL(gram1_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, y, c, norms2, ctx->partials,
+                       take_ticket(ctx), nullptr);
     }
+    return SVDSB_OK;
   } else if (b == 1) {
     constexpr int AT = 32, BT = 1;
     dim3 grid(gx, (s.total + AT - 1) / AT, 1);
@@ -864,8 +839,9 @@ int svdsb_project_out(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const
     double *nn = norms2 ? norms2 + j0 : nullptr;
     if (bb == 1 && colset_vec_ok(s) && aligned16(yy)) {
       size_t sh = sizeof(double) * std::max(s.total, 1);
-      project1_vec_kernel<<<grid_for(project1_vec_kernel, dim, sh), kThreads, sh, st>>>(dim, s, cc, yy, nn, ctx->partials,
-                                                                                 take_ticket(ctx), nullptr);
+      SVDSB_LAUNCH_PDL(project1_vec_kernel, grid_for(project1_vec_kernel, dim, sh), kThreads, sh, st, dim, s, cc, yy,
+                       nn, ctx->partials, take_ticket(ctx), (double *)nullptr);
+      continue;
     } else if (bb == 1) {
       size_t sh = sizeof(double) * std::max(s.total, 1) * 1;
       project_kernel<1><<<gx, kThreads, sh, st>>>(dim, s, cc, ldc, yy, ldy, bb, nn, ctx->partials, take_ticket(ctx));
@@ -926,8 +902,9 @@ int svdsb_ritz_residual(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ld
   if (p <= 32) {
     auto *tk = take_ticket(ctx);
 #define SVDSB_RITZ_WIDE(PTV)                                                                                  \
-  ritz_wide_kernel<PTV><<<grid_for(ritz_wide_kernel<PTV>, dim, sizeof(double) * g * PTV), kThreads, sizeof(double) * g * PTV, st>>>(dim, v, ldv, w, ldw, g, yc, ldyc, lam, p, r, \
-                                                                         ldr, x, ldx, ox, ldox, rn2, ctx->partials, tk)
+  SVDSB_LAUNCH_PDL(ritz_wide_kernel<PTV>, grid_for(ritz_wide_kernel<PTV>, dim, sizeof(double) * g * PTV), kThreads,  \
+                   sizeof(double) * g * PTV, st, dim, v, ldv, w, ldw, g, yc, ldyc, lam, p, r, ldr, x, ldx, ox, ldox, \
+                   rn2, ctx->partials, tk)
     if (p <= 4)
       SVDSB_RITZ_WIDE(4);
     else if (p <= 8)
@@ -941,7 +918,6 @@ int svdsb_ritz_residual(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ld
     else
       SVDSB_RITZ_WIDE(32);
 #undef SVDSB_RITZ_WIDE
-    SVDSB_LAUNCHED();
     return SVDSB_OK;
   }
   constexpr int PT = 12;
@@ -998,22 +974,21 @@ int svdsb_scale_cols(int64_t dim, const double *x, int64_t ldx, int b, const dou
                      int64_t ldy, void *stream) {
   if (dim == 0 || b <= 0) return SVDSB_OK;
   SVDSB_CHECK_ARG(mode >= 0 && mode <= 2, "svdsb_scale_cols: bad mode");
-  scale_kernel<<<(unsigned)((dim + 255) / 256), 256, 0, as_stream(stream)>>>(dim, x, ldx, b, s, mode, y, ldy);
-  SVDSB_LAUNCHED();
+  SVDSB_LAUNCH_PDL(scale_kernel, (unsigned)((dim + 255) / 256), 256, 0, as_stream(stream), dim, x, ldx, b, s, mode, y,
+                   ldy);
   return SVDSB_OK;
 }
 
 int svdsb_axpby(int64_t dim, int b, double alpha, const double *x, int64_t ldx, double beta, double *y, int64_t ldy,
                 void *stream) {
   if (dim == 0 || b <= 0) return SVDSB_OK;
-  axpby_kernel<<<(unsigned)((dim + 255) / 256), 256, 0, as_stream(stream)>>>(dim, b, alpha, x, ldx, beta, y, ldy);
-  SVDSB_LAUNCHED();
+  SVDSB_LAUNCH_PDL(axpby_kernel, (unsigned)((dim + 255) / 256), 256, 0, as_stream(stream), dim, b, alpha, x, ldx, beta,
+                   y, ldy);
   return SVDSB_OK;
 }
 
 int svdsb_dgks_begin(double *state, void *stream) {
-  dgks_begin_kernel<<<1, 32, 0, as_stream(stream)>>>(state);
-  SVDSB_LAUNCHED();
+  SVDSB_LAUNCH_PDL(dgks_begin_kernel, 1, 32, 0, as_stream(stream), state);
   return SVDSB_OK;
 }
 
@@ -1029,18 +1004,17 @@ int svdsb_cgs_pass(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *x
   double *n0 = first_pass ? state + 6 : nullptr;
   if (s.total <= 16) {
     dim3 grid(grid_for(gram1_vec_kernel<16>, dim, 0), 1, 1);
-    gram1_vec_kernel<16><<<grid, kThreads, 0, st>>>(dim, s, v, cwork, n0, ctx->partials, take_ticket(ctx), state);
+    SVDSB_LAUNCH_PDL(gram1_vec_kernel<16>, grid, kThreads, 0, st, dim, s, v, cwork, n0, ctx->partials,
+                     take_ticket(ctx), state);
   } else {
     constexpr int AT = 40;
     dim3 grid(grid_for(gram1_vec_kernel<AT>, dim, 0), (s.total + AT - 1) / AT, 1);
-    gram1_vec_kernel<AT><<<grid, kThreads, 0, st>>>(dim, s, v, cwork, n0, ctx->partials, take_ticket(ctx), state);
+    SVDSB_LAUNCH_PDL(gram1_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, v, cwork, n0, ctx->partials,
+                     take_ticket(ctx), state);
   }
-  SVDSB_LAUNCHED();
   size_t sh = sizeof(double) * s.total;
-  project1_vec_kernel<<<grid_for(project1_vec_kernel, dim, sh), kThreads, sh, st>>>(dim, s, cwork, v, state + 7,
-                                                                                   ctx->partials, take_ticket(ctx),
-                                                                                   state);
-  SVDSB_LAUNCHED();
+  SVDSB_LAUNCH_PDL(project1_vec_kernel, grid_for(project1_vec_kernel, dim, sh), kThreads, sh, st, dim, s, cwork, v,
+                   state + 7, ctx->partials, take_ticket(ctx), state);
   return SVDSB_OK;
 }
 

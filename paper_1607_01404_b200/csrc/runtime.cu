@@ -1,5 +1,6 @@
 // Library plumbing: error strings, launch counter, context (workspace).
 #include <stdarg.h>
+#include <stdlib.h>
 #include <atomic>
 
 #include "common.cuh"
@@ -17,6 +18,15 @@ void set_error(const char *fmt, ...) {
 }
 
 int64_t bump_launches(int n) { return g_launches.fetch_add(n) + n; }
+
+bool pdl_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("SVDSB_PDL");
+    on = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
 
 }  // namespace svdsb
 

@@ -447,6 +447,8 @@ __global__ void qr_small_kernel(int g, int s, const double *__restrict__ r, int6
 // ------------------------------------------------------- H bookkeeping
 
 __global__ void h_insert_kernel(int g, int b, const double *__restrict__ hc, int64_t ldhc, double *h, int64_t ldh) {
+  pdl_wait();
+  pdl_trigger();
   const int gb = g + b;
   for (int e = threadIdx.x; e < gb * b; e += blockDim.x) {
     int i = e % gb, j = e / gb;  // hc(i, j) -> H(i, g+j)
@@ -555,8 +557,7 @@ int svdsb_qr_small(int g, int s, const double *r, int64_t ldr, const double *yc,
 
 int svdsb_h_insert(int g, int b, const double *hc, int64_t ldhc, double *h, int64_t ldh, void *stream) {
   if (b <= 0) return SVDSB_OK;
-  h_insert_kernel<<<1, 256, 0, as_stream(stream)>>>(g, b, hc, ldhc, h, ldh);
-  SVDSB_LAUNCHED();
+  SVDSB_LAUNCH_PDL(h_insert_kernel, 1, 256, 0, as_stream(stream), g, b, hc, ldhc, h, ldh);
   return SVDSB_OK;
 }
 
