@@ -194,6 +194,17 @@ int svdsb_scale_cols(int64_t dim, const double *x, int64_t ldx, int b,
 int svdsb_axpby(int64_t dim, int b, double alpha, const double *x,
                 int64_t ldx, double beta, double *y, int64_t ldy,
                 void *stream);
+/* Device-indexed column gather: with f = *first (a device int),
+ * Y[:, c] = X[:, f + c] (divided elementwise by d when d != NULL, exactly
+ * as svdsb_diag_solve) for c < ncols and f + c < limit.  The column index
+ * lives on the device so captured iteration graphs need not be re-captured
+ * when the selected Ritz candidate changes (eigensolver.py:598-607 picks
+ * the first unconverged one; :520-527 keeps its +k neighbours). */
+int svdsb_gather_cols(int64_t dim, const double *x, int64_t ldx,
+                      const int *first, int ncols, int limit,
+                      const double *d, double *y, int64_t ldy, void *stream);
+/* *dst = v on the stream (stream-ordered scalar update for the above). */
+int svdsb_set_int(int *dst, int v, void *stream);
 /* Stage-2 split statistics of candidate vectors on the stacked layout
  * [v (nsplit); u (dim-nsplit)] (hybrid.py:226-241, :413-423): for each
  * column j writes 6 sums to out[6j..6j+5]:

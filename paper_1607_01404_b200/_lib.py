@@ -52,7 +52,9 @@ _PROTOS = [
     ("svdsb_col_dots", i32, [vp, i64, vp, i64, vp, i64, i32, vp, vp]),
     ("svdsb_scale_cols", i32, [i64, vp, i64, i32, vp, i32, vp, i64, vp]),
     ("svdsb_axpby", i32, [i64, i32, f64, vp, i64, f64, vp, i64, vp]),
-    ("svdsb_split_stats", i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp]),
+    ("svdsb_gather_cols", i32, [i64, vp, i64, vp, i32, i32, vp, vp, i64, vp]),
+    ("svdsb_set_int", i32, [vp, i32, vp]),
+    ("svdsb_split_stats",i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp]),
     ("svdsb_dgks_begin", i32, [vp, vp]),
     ("svdsb_cgs_pass", i32, [vp, i64, i32, vp, vp, vp, vp, vp, vp, i32, vp]),
     ("svdsb_split_residual",i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp, vp, vp]),

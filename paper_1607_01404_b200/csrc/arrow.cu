@@ -49,6 +49,18 @@ struct ArrowSmem {
 // holds identical values; one reciprocal per term.
 constexpr int kGroup = 8;
 
+// Development probe (tools/arrow_phases.py): per-phase SM clock stamps of
+// thread 0, compiled in only with -DSVDSB_PHASE_CLOCKS.
+#ifdef SVDSB_PHASE_CLOCKS
+__device__ long long g_arrow_clk[16];
+#define SVDSB_PHASE(k) \
+  if (threadIdx.x == 0) g_arrow_clk[k] = clock64()
+#else
+#define SVDSB_PHASE(k) \
+  do {                 \
+  } while (0)
+#endif
+
 __device__ __forceinline__ double group_sum(double v, unsigned mask) {
   v += __shfl_xor_sync(mask, v, 1);
   v += __shfl_xor_sync(mask, v, 2);
@@ -170,6 +182,7 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
     s.tol = 8.0 * kEps * fmax(dm, zn);
   }
   __syncthreads();
+  SVDSB_PHASE(3);
   for (int i = tid; i < n; i += nt) s.defl[i] = (fabs(s.z[i]) <= s.tol) ? 1 : 0;
   __syncthreads();
   // sort the surviving poles ascending (stable by index)
@@ -182,6 +195,7 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
     s.sidx[r] = i;
   }
   __syncthreads();
+  SVDSB_PHASE(4);
   if (tid == 0) {
     int np = 0;
     for (int i = 0; i < n; ++i) np += !s.defl[i];
@@ -216,6 +230,7 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
     }
   }
   __syncthreads();
+  SVDSB_PHASE(5);
   const int np = s.np;
   {
     // one 8-lane group per root; groups of a warp run independently
@@ -224,6 +239,7 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
     for (int j = tid / kGroup; j <= np; j += nt / kGroup) arrow_roots(s, j, lane, mask);
   }
   __syncthreads();
+  SVDSB_PHASE(6);
   // Gu-Eisenstat couplings
   for (int i = tid; i < np; i += nt) {
     double prod = lam_minus_pole(s, i, i) * lam_minus_pole(s, i + 1, i);
@@ -236,6 +252,7 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
     s.zhat[i] = (s.sz[i] >= 0.0) ? zh : -zh;
   }
   __syncthreads();
+  SVDSB_PHASE(7);
   // eigenvector columns: first the deflated original indices, then roots
   const int N1 = n + 1;
   for (int e = tid; e < N1 * N1; e += nt) P[(e % N1) + (e / N1) * ldp] = 0.0;
@@ -280,6 +297,7 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
     }
   }
   __syncthreads();
+  SVDSB_PHASE(8);
   // undo the deflation rotations (last created first): v = G_1 ... G_r v'
   for (int c = tid; c < N1; c += nt) {
     double *pc = P + c * ldp;
@@ -291,6 +309,7 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
     }
   }
   __syncthreads();
+  SVDSB_PHASE(9);
 }
 
 __global__ void __launch_bounds__(kAT)
@@ -308,6 +327,7 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
   const int tid = threadIdx.x, nt = blockDim.x;
   pdl_wait();
   pdl_trigger();
+  SVDSB_PHASE(0);
   for (int e = tid; e < G * G; e += nt) {
     int i = e % G, j = e / G;
     double v = 0.0;
@@ -316,6 +336,7 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
   }
   for (int i = tid; i < g0; i += nt) lam[i] = l0 ? l0[i] : h[i + (int64_t)i * ldh];
   __syncthreads();
+  SVDSB_PHASE(1);
   for (int j = 0; j < b; ++j) {
     const int sdim = g0 + j;  // current size; new index sdim
     // one parallel global read of the border column, then z = Y^T H[:sdim, sdim]
@@ -330,6 +351,7 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
     }
     if (tid == 0) s.alpha = s.hcol[sdim];
     __syncthreads();
+    SVDSB_PHASE(2);
     arrow_solve(s, sdim, P, ld);
     // Y <- blkdiag(Y, 1) P   (size sdim+1)
     const int n1 = sdim + 1;
@@ -346,11 +368,13 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
     }
     for (int c = tid; c < n1; c += nt) lam[c] = s.newd[c];
     __syncthreads();
+    SVDSB_PHASE(10);
     for (int e = tid; e < n1 * n1; e += nt) {
       int r = e % n1, c = e / n1;
       Y[r + c * ld] = T[r + c * ld];
     }
     __syncthreads();
+    SVDSB_PHASE(11);
   }
   // ordering as in syev_jacobi_kernel: ascending ranks first (ties by
   // index), then each value's position under the target rule, O(G) each
@@ -364,6 +388,7 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
     s.rank[i] = rank;
   }
   __syncthreads();
+  SVDSB_PHASE(12);
   for (int i = tid; i < G; i += nt) {
     const double wi = lam[i];
     const int rank = s.rank[i];
@@ -389,6 +414,10 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
     w_out[pos] = wi;
     for (int r = 0; r < G; ++r) y_out[r + (int64_t)pos * ldy] = Y[r + i * ld];
   }
+#ifdef SVDSB_PHASE_CLOCKS
+  __syncthreads();
+  SVDSB_PHASE(13);
+#endif
 }
 
 static bool g_arrow_attr = false;
@@ -396,6 +425,13 @@ static bool g_arrow_attr = false;
 }  // namespace svdsb
 
 using namespace svdsb;
+
+#ifdef SVDSB_PHASE_CLOCKS
+extern "C" int svdsb_dbg_arrow_clocks(long long *out) {
+  SVDSB_CUDA(cudaMemcpyFromSymbol(out, g_arrow_clk, sizeof(long long) * 16));
+  return SVDSB_OK;
+}
+#endif
 
 extern "C" int svdsb_syev_update(int g0, int b, const double *h, int64_t ldh, const double *y0, int64_t ldy0,
                                  const double *l0, int order, double shift, double *w, double *y, int64_t ldy,

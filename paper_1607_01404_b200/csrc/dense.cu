@@ -415,6 +415,24 @@ __global__ void scale_kernel(int64_t dim, const double *x, int64_t ldx, int b, c
   }
 }
 
+__global__ void gather_cols_kernel(int64_t dim, const double *x, int64_t ldx, const int *first, int ncols, int limit,
+                                   const double *__restrict__ d, double *y, int64_t ldy) {
+  pdl_wait();
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= dim) return;
+  const int f = *first;
+  const double di = d ? d[i] : 1.0;
+  for (int c = 0; c < ncols && f + c < limit; ++c) {
+    const double v = x[i + (int64_t)(f + c) * ldx];
+    y[i + (int64_t)c * ldy] = d ? __ddiv_rn(v, di) : v;
+  }
+}
+
+__global__ void set_int_kernel(int *dst, int v) {
+  pdl_wait();
+  if (threadIdx.x == 0) *dst = v;
+}
+
 __global__ void axpby_kernel(int64_t dim, int b, double alpha, const double *x, int64_t ldx, double beta, double *y,
                              int64_t ldy) {
   pdl_wait();
@@ -984,6 +1002,21 @@ int svdsb_axpby(int64_t dim, int b, double alpha, const double *x, int64_t ldx, 
   if (dim == 0 || b <= 0) return SVDSB_OK;
   SVDSB_LAUNCH_PDL(axpby_kernel, (unsigned)((dim + 255) / 256), 256, 0, as_stream(stream), dim, b, alpha, x, ldx, beta,
                    y, ldy);
+  return SVDSB_OK;
+}
+
+int svdsb_gather_cols(int64_t dim, const double *x, int64_t ldx, const int *first, int ncols, int limit,
+                      const double *d, double *y, int64_t ldy, void *stream) {
+  SVDSB_CHECK_ARG(first != nullptr, "svdsb_gather_cols: NULL index");
+  if (dim == 0 || ncols <= 0) return SVDSB_OK;
+  SVDSB_LAUNCH_PDL(gather_cols_kernel, (unsigned)((dim + 255) / 256), 256, 0, as_stream(stream), dim, x, ldx, first,
+                   ncols, limit, d, y, ldy);
+  return SVDSB_OK;
+}
+
+int svdsb_set_int(int *dst, int v, void *stream) {
+  SVDSB_CHECK_ARG(dst != nullptr, "svdsb_set_int: NULL destination");
+  SVDSB_LAUNCH_PDL(set_int_kernel, 1, 32, 0, as_stream(stream), dst, v);
   return SVDSB_OK;
 }
 

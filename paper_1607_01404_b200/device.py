@@ -219,6 +219,18 @@ def axpby(ctx, alpha, x, beta, y):
          ld_of(y), ctx.stream)
 
 
+def gather_cols(ctx, x, first, ncols, limit, y, d=None):
+    """y[:, c] = x[:, *first + c] (/ d) for c < ncols, *first + c < limit;
+    ``first`` is a one-element int32 device tensor."""
+    x, y = as_block(x), as_block(y)
+    call("svdsb_gather_cols", y.shape[0], P(x), ld_of(x), P(first), int(ncols), int(limit),
+         None if d is None else P(d), P(y), ld_of(y), ctx.stream)
+
+
+def set_int(ctx, dst, v):
+    call("svdsb_set_int", P(dst), int(v), ctx.stream)
+
+
 def split_stats(ctx, nsplit, r, x, out):
     r, x = as_block(r), as_block(x)
     call("svdsb_split_stats", ctx.handle, r.shape[0], int(nsplit), P(r), ld_of(r), P(x), ld_of(x),

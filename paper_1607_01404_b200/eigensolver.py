@@ -286,29 +286,39 @@ class Orthonormalizer:
 class _Workspace:
     """Device buffers of one solver shape, pooled per device so repeated
     solves of the same shape reuse memory -- and with it the CUDA graphs
-    captured for their iterations (graphs bake device pointers)."""
+    captured for their iterations (graphs bake device pointers).
+
+    The per-iteration outputs (Ritz values and coefficients, candidate
+    residuals, status scalars, DGKS state, the pinned status copy) come in
+    two slots: a graphed iteration reads slot s and writes slot 1 - s, so
+    the next iteration can be queued before the host has decided on the
+    current one (see DavidsonSolver._expand_graphed)."""
 
     def __init__(self, key, n, gm, pmax, bs, plus_k):
+        dev = dv.context().device
         self.key = key
         self.v = dv.new_block(n, gm)
         self.w = dv.new_block(n, gm)
         self.v2 = dv.new_block(n, gm)
         self.w2 = dv.new_block(n, gm)
         self.h = dv.small_matrix(gm, gm)
-        self.lams = torch.zeros(gm, dtype=DTYPE, device=dv.context().device)
-        self.y = dv.small_matrix(gm, gm)
-        self.rbuf = dv.new_block(n, pmax)
-        self.stat = torch.zeros(8 * pmax + 4, dtype=DTYPE, device=dv.context().device)
+        self.lams = [torch.zeros(gm, dtype=DTYPE, device=dev) for _ in range(2)]
+        self.y = [dv.small_matrix(gm, gm) for _ in range(2)]
+        self.rbuf = [dv.new_block(n, pmax) for _ in range(2)]
+        self.stat = [torch.zeros(8 * pmax + 4, dtype=DTYPE, device=dev) for _ in range(2)]
+        self.dgks = [torch.zeros(8, dtype=DTYPE, device=dev) for _ in range(2)]
+        self.status = [torch.zeros(2 * gm + 32, dtype=DTYPE, pin_memory=True) for _ in range(2)]
+        self.events = [torch.cuda.Event() for _ in range(2)]
         self.coefs = dv.small_matrix(gm, gm)
-        self.count = torch.zeros(1, dtype=torch.int32, device=dv.context().device)
+        self.count = torch.zeros(1, dtype=torch.int32, device=dev)
         self.prev = dv.small_matrix(gm, max(plus_k, 1))
-        self.yref = torch.zeros(gm, dtype=DTYPE, device=dv.context().device)
-        self.excl = torch.zeros(gm, dtype=DTYPE, device=dv.context().device)
-        self.dgks = torch.zeros(8, dtype=DTYPE, device=dv.context().device)
+        self.yref = torch.zeros(gm, dtype=DTYPE, device=dev)
+        self.excl = torch.zeros(gm, dtype=DTYPE, device=dev)
+        self.dgks_eager = torch.zeros(8, dtype=DTYPE, device=dev)
         self.hc1 = dv.small_matrix(gm + 1, 1)
-        self.res1 = dv.new_block(n, 1)
-        self.orthoc = torch.zeros(4 * _lib.SMALL_MAX * 4, dtype=DTYPE, device=dv.context().device)
-        self.status = torch.zeros(2 * gm + 32, dtype=DTYPE, pin_memory=True)
+        self.ci = torch.zeros(1, dtype=torch.int32, device=dev)   # selected candidate (device copy)
+        self.ci_host = None                                        # its value in stream order
+        self.orthoc = torch.zeros(4 * _lib.SMALL_MAX * 4, dtype=DTYPE, device=dev)
         self.graphs = {}
         self.graph_owner = None
 
@@ -389,9 +399,11 @@ class DavidsonSolver:
         if getattr(ctx, "handle", None) is not None:
             ws = self._ws = _acquire_workspace(self.n, gm, pmax, bs, cfg.plus_k)
             self.v, self.w, self._v2, self._w2 = ws.v, ws.w, ws.v2, ws.w2
-            self.h, self.lams_d, self.y_d = ws.h, ws.lams, ws.y
-            self.rbuf, self.stat_d, self.coefs, self.count_d = ws.rbuf, ws.stat, ws.coefs, ws.count
+            self.h = ws.h
+            self._use_slot(0)
+            self.coefs, self.count_d = ws.coefs, ws.count
             self.prev_d, self.yref, self.excl = ws.prev, ws.yref, ws.excl
+            ws.ci_host = None
             self.ortho.c = ws.orthoc
             # a workspace keeps the graphs of one operator: a new operator
             # drops them (they reference its device arrays)
@@ -419,7 +431,9 @@ class DavidsonSolver:
         self.g = 0
         self.xbuf = None
         self.oxbuf = None
-        self._pending = None
+        self._pending = None   # graphed iteration queued, status not yet read
+        self._ahead = None     # next graphed iteration queued speculatively
+        self._ahead_used = False
 
         self.locked_vecs = dv.new_block(self.n, 0)
         self._locked_buf = dv.new_block(self.n, max(self.wanted, 1)) if cfg.locking else None
@@ -441,8 +455,8 @@ class DavidsonSolver:
         self.warm_start = True
         self.speculate = True       # device-decided DGKS for single-column expansions
         self._spec = None
-        self._dgks_state = self._ws.dgks if self._ws is not None else torch.zeros(8, dtype=DTYPE,
-                                                                                   device=ctx.device)
+        self._dgks_state = self._ws.dgks_eager if self._ws is not None else torch.zeros(8, dtype=DTYPE,
+                                                                                         device=ctx.device)
 
         need_v1, split1 = _test_needs(cfg.convergence_test)
         need_v2, split2 = _test_needs(cfg.practical_test)
@@ -466,6 +480,12 @@ class DavidsonSolver:
                 self._rebuild_qr()
 
     # ------------------------------------------------------------ plumbing
+    def _use_slot(self, s):
+        """Point the per-iteration buffers at workspace slot s."""
+        ws = self._ws
+        self._slot = s
+        self.lams_d, self.y_d, self.rbuf, self.stat_d = ws.lams[s], ws.y[s], ws.rbuf[s], ws.stat[s]
+
     @property
     def op_norm(self):
         return self.est.a_norm if self.est_mode == "augmented" else self.est.c_norm
@@ -891,16 +911,26 @@ class DavidsonSolver:
             # together with the previous expansion; only wait for them
             pend, self._pending = self._pending, None
             p = pend["p"]
+            self._use_slot(pend["slot"])
             lams_d, y_d = self.lams_d[:g], self.y_d[:g, :g]
             r, x, ox, split = self.rbuf[:, :p], None, None, None
-            got = self._wait_status(g, p)
+            got = self._wait_status(g, p, pend["slot"])
             st = got.pop()
             if not self._resolve_speculation(st):
+                # the queued next iteration was built on the collapsed column
+                self._ahead = None
                 self.stats.outer_iterations -= 1
                 return self.step()
             lams, rn2_h, split_h = got[0], got[1], None
             self._observe(lams)
-            return self._step_decide(info, g, lams, y_d, rn2_h, split_h, r, x, ox, p, refined)
+            self._ahead_used = False
+            try:
+                return self._step_decide(info, g, lams, y_d, rn2_h, split_h, r, x, ox, p, refined)
+            finally:
+                if not self._ahead_used:
+                    # the host decided differently from the speculation: the
+                    # queued iteration only wrote buffers nobody reads now
+                    self._ahead = None
         lams_d, y_d = self.extract_rayleigh_ritz()
         if refined:
             lamref = self.stat_d[-2:-1]
@@ -1012,11 +1042,14 @@ class DavidsonSolver:
             else:
                 hi = min(conv_count + max(cfg.plus_k, 1), g)
                 k = hi - conv_count
-                if k > 0:
+                # a graphed expansion copies the same columns on device
+                # (selected by the device-side candidate index)
+                if k > 0 and not (ci == conv_count and self._graph_ok(min(res_block.shape[1],
+                                                                          self.gmax - self.g))):
                     dv.axpby(self.ctx, 1.0, y_d[:, conv_count:hi], 0.0, self.prev_d[:g, :k])
                 self.prev_coefs = k
             self.prev_coefs_g = info["g"]
-        self._expand(res_block, ci)
+        self._expand(res_block, ci, graph=refined or ci == conv_count)
         return info
 
     # ------------------------------------------------ speculative expansion
@@ -1103,9 +1136,21 @@ class DavidsonSolver:
     # The device work between two host decisions of a plain single-column
     # Rayleigh-Ritz iteration -- expansion (preconditioner, device-decided
     # CGS passes, the C-apply, the H column), the next warm extraction, the
-    # candidate residuals and the status copy -- depends only on (g, ci, p,
-    # warm state, buffers).  It is captured once as a CUDA graph and
-    # replayed: one launch instead of ~15, no Python in between.
+    # candidate residuals and the status copy -- depends only on (g, p, warm
+    # state, buffers); the selected candidate is a device-side index.  It is
+    # captured once as a CUDA graph and replayed: one launch instead of ~17,
+    # no Python in between.
+    #
+    # Iterations are also queued one ahead: right after iteration k's graph,
+    # iteration k+1's graph is launched on the guess that the host will
+    # decide on k the way it usually does (no new convergence, no reset, no
+    # stop -- so the same candidate index, and no restart since the basis is
+    # not full).  The host then decides on k while the GPU already runs k+1.
+    # k+1 reads slot s and writes slot 1-s, so a wrong guess costs only the
+    # wasted GPU work: nothing the host path reads was overwritten, and the
+    # counters are only advanced when the queued iteration is accepted.
+
+    run_ahead = os.environ.get("SVDSB_AHEAD", "1") != "0"
 
     def _graph_ok(self, b):
         return (self.use_graphs and self._can_speculate(b) and self._ws is not None
@@ -1113,19 +1158,23 @@ class DavidsonSolver:
                 and self._split_n is None and not self._need_vecs and self.cfg.iteration_hook is None
                 and not self.ext and self.locked_vecs.shape[1] == 0 and self.warm_start
                 and self._warm is not None and getattr(self.op, "graph_key", None) is not None
-                and (self.precond is None or getattr(self.precond, "graph_key", None) is not None))
+                and (self.precond is None or getattr(self.precond, "diagonal", None) is not None))
 
-    def _iter_device(self, g, ci, kind, g0, p, order, shift):
-        """Launch-only body of a graphed iteration (no host bookkeeping)."""
+    def _iter_device(self, g, kind, g0, p, order, shift, sin, sout):
+        """Launch-only body of a graphed iteration (no host bookkeeping):
+        expand with candidate *ws.ci of slot sin, extract into slot sout."""
         ctx = self.ctx
         ws = self._ws
         dst = self.v[:, g:g + 1]
-        res = ws.res1   # the chosen residual column, copied in before replay
-        if self.precond is not None:
-            self.precond._into(res, dst)
-        else:
-            dv.axpby(ctx, 1.0, res, 0.0, dst)
-        st = ws.dgks
+        y_in, l_in = ws.y[sin], ws.lams[sin]
+        y_out, l_out, r_out, s_out = ws.y[sout], ws.lams[sout], ws.rbuf[sout], ws.stat[sout]
+        # +k coefficients kept for the next restart (eigensolver.py:520-527)
+        kk = max(self.cfg.plus_k, 1)
+        dv.gather_cols(ctx, y_in[:g, :g], ws.ci, kk, g, self.prev_d[:g, :kk])
+        # the selected residual, preconditioned (x ./ d as svdsb_diag_solve)
+        d = self.precond.diagonal if self.precond is not None else None
+        dv.gather_cols(ctx, ws.rbuf[sin], ws.ci, 1, self.pmax, dst, d=d)
+        st = ws.dgks[sout]
         _lib.call("svdsb_dgks_begin", dv.P(st), ctx.stream)
         n_, ptrs, lds, cols, _ = dv._blk_args([self.v[:, :g]])
         for p_ in range(self.SPEC_PASSES):
@@ -1137,15 +1186,15 @@ class DavidsonSolver:
         dv.gram(ctx, self.n, [self.v[:, :g + 1]], self.w[:, g:g + 1], hc)
         dv.h_insert(ctx, g, 1, hc, self.h)
         gn = g + 1
-        y0 = self.y_d[:g0, :g0] if kind == "prev" else None
-        l0 = self.lams_d[:g0] if kind == "prev" else None
-        dv.syev_update(ctx, self.h, g0, gn - g0, y0, l0, order, shift, self.lams_d[:gn], self.y_d[:gn, :gn])
-        dv.ritz_residual(ctx, self.v[:, :gn], self.w[:, :gn], self.y_d[:gn, :p], self.lams_d[:p],
-                         self.rbuf[:, :p], rn2=self.stat_d[:p])
+        y0 = y_in[:g0, :g0] if kind == "prev" else None
+        l0 = l_in[:g0] if kind == "prev" else None
+        dv.syev_update(ctx, self.h, g0, gn - g0, y0, l0, order, shift, l_out[:gn], y_out[:gn, :gn])
+        dv.ritz_residual(ctx, self.v[:, :gn], self.w[:, :gn], y_out[:gn, :p], l_out[:p],
+                         r_out[:, :p], rn2=s_out[:p])
         lib = _lib.load()
-        base = ws.status.data_ptr()
-        lib.svdsb_d2h(base, self.lams_d.data_ptr(), 8 * gn, ctx.stream)
-        lib.svdsb_d2h(base + 8 * gn, self.stat_d.data_ptr(), 8 * p, ctx.stream)
+        base = ws.status[sout].data_ptr()
+        lib.svdsb_d2h(base, l_out.data_ptr(), 8 * gn, ctx.stream)
+        lib.svdsb_d2h(base + 8 * gn, s_out.data_ptr(), 8 * p, ctx.stream)
         lib.svdsb_d2h(base + 8 * (gn + p), st.data_ptr(), 64, ctx.stream)
 
     def _capture(self, fn):
@@ -1168,26 +1217,44 @@ class DavidsonSolver:
         cur.wait_stream(cap)
         return graph
 
-    def _expand_graphed(self, ci):
-        g = self.g
-        kind, g0 = self._warm
+    def _launch_iter(self, g, kind, g0, sin, ci):
+        """Replay (capturing on first use) the iteration graph that expands
+        a basis of size g from slot sin; returns the queued-iteration
+        record."""
+        ws = self._ws
+        sout = 1 - sin
         p = min(self.wanted + self.cfg.max_block_size, g + 1)
         order, shift = self._order_mode()
-        key = (self.v.data_ptr(), self.w.data_ptr(), kind, g0, g, p, order, shift, self.op.graph_key(),
-               None if self.precond is None else self.precond.graph_key)
-        graphs = self._ws.graphs
-        entry = graphs.get(key)
+        key = (self.v.data_ptr(), self.w.data_ptr(), kind, g0, g, p, sin, order, shift, self.op.graph_key(),
+               None if self.precond is None else self.precond.diagonal.data_ptr())
+        entry = ws.graphs.get(key)
         if entry is None:
             before = _lib.launch_count()
-            graph = self._capture(lambda: self._iter_device(g, ci, kind, g0, p, order, shift))
+            graph = self._capture(lambda: self._iter_device(g, kind, g0, p, order, shift, sin, sout))
             entry = (graph, _lib.launch_count() - before)
-            graphs[key] = entry
+            ws.graphs[key] = entry
             self.stats.graphs_captured += 1
-        # the residual column the host chose goes to the graph's fixed slot
-        dv.axpby(self.ctx, 1.0, self.rbuf[:, ci:ci + 1], 0.0, self._ws.res1)
         entry[0].replay()
+        ws.events[sout].record()
         _lib.load().svdsb_note_launches(entry[1])
-        # host bookkeeping of what the graph did
+        return {"p": p, "slot": sout, "sin": sin, "g": g, "ci": ci}
+
+    def _expand_graphed(self, ci):
+        ws = self._ws
+        g = self.g
+        sin = self._slot
+        ahead, self._ahead = self._ahead, None
+        self._ahead_used = True
+        if ahead is not None and ahead["g"] == g and ahead["ci"] == ci and ahead["sin"] == sin \
+                and self._warm == ("prev", g):
+            pend = ahead          # already running: the guess was right
+        else:
+            if ws.ci_host != ci:
+                dv.set_int(self.ctx, ws.ci, ci)
+                ws.ci_host = ci
+            kind, g0 = self._warm
+            pend = self._launch_iter(g, kind, g0, sin, ci)
+        # host bookkeeping of what the graph does
         if self.precond is not None:
             self.precond.n_applies += 1
             self.stats.precond_applies += 1
@@ -1197,25 +1264,28 @@ class DavidsonSolver:
         self._spec = {"g0": g}
         self.g = g + 1
         self._warm = ("prev", g + 1)
-        self._pending = {"p": p}
+        self._pending = pend
+        # queue the next iteration on the usual decision; with a full basis
+        # the host would restart instead, so only while g + 1 < gmax
+        if self.run_ahead and g + 1 < self.gmax:
+            self._ahead = self._launch_iter(g + 1, "prev", g + 1, pend["slot"], ci)
 
-    def _wait_status(self, g, p):
-        """Synchronise with the queued iteration and read its status."""
-        lib = _lib.load()
-        rc = lib.svdsb_stream_sync(self.ctx._stream)
-        if rc:
-            _lib.check(rc, "svdsb_stream_sync")
+    def _wait_status(self, g, p, slot):
+        """Wait for the queued iteration that writes `slot` (not for a
+        later one queued behind it) and read its status."""
+        ws = self._ws
+        ws.events[slot].synchronize()
         self.stats.syncs += 1
-        host = self._ws.status.numpy()
+        host = ws.status[slot].numpy()
         return [host[:g].copy(), host[g:g + p].copy(), host[g + p:g + p + 8].copy()]
 
-    def _expand(self, res_block, ci=0):
+    def _expand(self, res_block, ci=0, graph=True):
         """eigensolver.py:666-700."""
         b = min(res_block.shape[1], self.gmax - self.g)
         if b <= 0:
             return
         block = res_block[:, :b]
-        if self._graph_ok(b):
+        if graph and self._graph_ok(b):
             self._expand_graphed(ci)
             return
         if self._can_speculate(b):

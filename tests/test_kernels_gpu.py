@@ -453,3 +453,30 @@ def test_column_blocked_transpose(b, rng, monkeypatch):
     c = _dev().to_host(op.apply(_dev().to_device_block(x)))
     ref = ocsr.spmv(m, n, rp, ci, va, ocsr.spmv(m, n, rp, ci, va, x), transpose=True)
     assert np.abs(c - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("dim", [5, 100003])
+def test_gather_cols_device_index(dim, rng):
+    """Device-indexed column gather: plain copy, and divided by a diagonal
+    bit-identically to svdsb_diag_solve; the limit clips the column range."""
+    import torch
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    x = rng.standard_normal((dim, 6))
+    d = rng.uniform(0.5, 2.0, dim)
+    X = dv.to_device_block(x)
+    D = torch.from_numpy(d).cuda()
+    first = torch.tensor([2], dtype=torch.int32, device="cuda")
+    Y = dv.new_block(dim, 3)
+    dv.gather_cols(ctx, X, first, 3, 4, Y)
+    got = dv.to_host(Y)
+    assert np.array_equal(got[:, :2], x[:, 2:4])
+    assert np.all(got[:, 2] == 0.0)           # column 4 is past the limit
+    dv.set_int(ctx, first, 5)
+    dv.gather_cols(ctx, X, first, 1, 6, Y[:, :1], d=D)
+    ref = dv.new_block(dim, 1)
+    _lib.call("svdsb_diag_solve", dim, dv.P(D), dv.P(X[:, 5:6]), dv.ld_of(X), dv.P(ref), dv.ld_of(ref), 1,
+              ctx.stream)
+    assert np.array_equal(dv.to_host(Y[:, :1]), dv.to_host(ref))
+    assert np.array_equal(dv.to_host(ref)[:, 0], x[:, 5] / d)

@@ -209,14 +209,17 @@ def test_graph_cache_across_matrices_and_repeats():
         res = svds_solve(a, precond=pre, cfg=SvdsConfig(**cfg))
         return res.sigma.copy(), res.stats.stage1_matvecs, res.stats.graphs_captured
 
-    saved = DavidsonSolver.use_graphs
+    saved = DavidsonSolver.use_graphs, DavidsonSolver.run_ahead
     try:
         DavidsonSolver.use_graphs = False
         plain = [solve(s)[:2] for s in (1.0, 2.0)]
         DavidsonSolver.use_graphs = True
-        runs = [solve(s) for s in (1.0, 2.0, 1.0, 2.0)]
+        DavidsonSolver.run_ahead = False
+        runs = [solve(s) for s in (1.0, 2.0)]
+        DavidsonSolver.run_ahead = True
+        runs += [solve(s) for s in (1.0, 2.0, 1.0, 2.0)]
     finally:
-        DavidsonSolver.use_graphs = saved
+        DavidsonSolver.use_graphs, DavidsonSolver.run_ahead = saved
     assert any(g > 0 for _, _, g in runs)
     for i, (sig, mv, _) in enumerate(runs):
         want_sig, want_mv = plain[i % 2]
