@@ -6,12 +6,17 @@
 // the basis blkdiag(Y0, I_b) the new projection is an arrowhead matrix per
 // border.  Each border is absorbed exactly with the secular equation
 //     f(lam) = lam - alpha - sum_i z_i^2 / (lam - d_i) = 0,
-// one thread per root (safeguarded Newton on f*(lam - d_K) about the nearest
+// one warp per root (safeguarded Newton on f*(lam - d_K) about the nearest
 // pole K), deflation of tiny couplings and of (nearly) equal poles by Givens
 // rotations, and Gu-Eisenstat recomputed couplings z^ so the computed
 // eigenvectors are orthogonal to working precision.  Cost is O(g^2) per
-// border on one CTA (a few microseconds) instead of the O(g^3) sweeps of a
-// cold Jacobi solve.
+// border on one CTA instead of the O(g^3) sweeps of a cold Jacobi solve.
+//
+// Latency is what matters here (g <= 64, one CTA, on the critical path of
+// every Davidson iteration), so every O(g) loop is spread over a warp or
+// the CTA: the secular sums and the Gu-Eisenstat products are warp-wide with
+// fixed xor trees (deterministic), the type-2 deflation scan only runs
+// serially when two poles actually coincide.
 //
 // Replaces, on the warm path, the per-iteration dense eigh of
 // extract_rayleigh_ritz (pkg/src/itersvd/eigensolver.py:362-367).
@@ -21,7 +26,7 @@
 
 namespace svdsb {
 
-constexpr int kAT = 576;          // threads: 72 eight-lane root groups
+constexpr int kAT = 1024;             // threads: 32 warps, one secular root each
 constexpr int kAN = SVDSB_SMALL_MAX;  // max dimension
 
 struct ArrowSmem {
@@ -32,6 +37,7 @@ struct ArrowSmem {
   double tau[kAN + 1];             // root offsets
   double tau2[kAN + 1];            // per-column scratch (eigenvector scaling)
   int rank[kAN + 1];               // ascending rank of each eigenvalue
+  int perm[kAN + 1];               // output column -> eigenvalue index
   int korg[kAN + 1];               // root origin (sorted pole index)
   double zhat[kAN];
   double newd[kAN + 1];            // eigenvalues in output column order
@@ -42,12 +48,6 @@ struct ArrowSmem {
   int nrot, np;
   double alpha, tol, znorm;
 };
-
-// f(tau) with origin pole K (sorted index), also the pieces of h = tau*f
-// without the K pole.  Evaluated by an 8-lane group (lane l sums terms
-// l, l+8, ...), combined with a fixed xor tree so every lane of the group
-// holds identical values; one reciprocal per term.
-constexpr int kGroup = 8;
 
 // Development probe (tools/arrow_phases.py): per-phase SM clock stamps of
 // thread 0, compiled in only with -DSVDSB_PHASE_CLOCKS.
@@ -61,20 +61,34 @@ __device__ long long g_arrow_clk[16];
   } while (0)
 #endif
 
-__device__ __forceinline__ double group_sum(double v, unsigned mask) {
-  v += __shfl_xor_sync(mask, v, 1);
-  v += __shfl_xor_sync(mask, v, 2);
-  v += __shfl_xor_sync(mask, v, 4);
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-__device__ __forceinline__ void secular_eval(const ArrowSmem &s, int K, double tau, int lane, unsigned mask,
-                                             double &f, double &h, double &hp, double &fscale) {
+// 1/x from the MUFU seed and two Newton steps (~1 ulp; the secular sums do
+// not need a correctly rounded reciprocal, and the FP64 divide sequence is
+// what bounds this single-CTA kernel).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// f(tau) with origin pole K (sorted index), also the pieces of h = tau*f
+// without the K pole.  Evaluated by one warp (lane l sums terms l, l+32),
+// combined with a fixed xor tree so every lane holds identical values.
+__device__ __forceinline__ void secular_eval(const ArrowSmem &s, int K, double tau, int lane, double &f,
+                                             double &h, double &hp, double &fscale) {
   const double dK = s.sd[K];
   double sum = 0.0, sum_nk = 0.0, dsum_nk = 0.0, scale = 0.0;
-  for (int i = lane; i < s.np; i += kGroup) {
+  for (int i = lane; i < s.np; i += 32) {
     const double den = tau - (s.sd[i] - dK);   // lam - d_i
-    const double inv = 1.0 / den;
+    const double inv = fast_rcp(den);
     const double zz = s.sz[i] * s.sz[i];
     const double t = zz * inv;
     sum += t;
@@ -84,10 +98,10 @@ __device__ __forceinline__ void secular_eval(const ArrowSmem &s, int K, double t
       dsum_nk += t * inv;
     }
   }
-  sum = group_sum(sum, mask);
-  scale = group_sum(scale, mask) + fabs(dK - s.alpha) + fabs(tau);
-  sum_nk = group_sum(sum_nk, mask);
-  dsum_nk = group_sum(dsum_nk, mask);
+  sum = wsum(sum);
+  scale = wsum(scale) + fabs(dK - s.alpha) + fabs(tau);
+  sum_nk = wsum(sum_nk);
+  dsum_nk = wsum(dsum_nk);
   f = (dK - s.alpha) + tau - sum;
   const double zK2 = s.sz[K] * s.sz[K];
   h = tau * ((dK - s.alpha) + tau - sum_nk) - zK2;
@@ -95,9 +109,9 @@ __device__ __forceinline__ void secular_eval(const ArrowSmem &s, int K, double t
   fscale = scale;
 }
 
-// Root j of np+1 (ascending; interval (sd[j-1], sd[j])), solved by the
-// 8-lane group `lane`/`mask`; lane 0 stores the result.
-__device__ void arrow_roots(ArrowSmem &s, int j, int lane, unsigned mask) {
+// Root j of np+1 (ascending; interval (sd[j-1], sd[j])), solved by one warp;
+// lane 0 stores the result.
+__device__ void arrow_roots(ArrowSmem &s, int j, int lane) {
   const int np = s.np;
   int K;
   double lo, hi;
@@ -122,7 +136,7 @@ __device__ void arrow_roots(ArrowSmem &s, int j, int lane, unsigned mask) {
     const double a = s.sd[j - 1], b = s.sd[j];
     const double half = 0.5 * (b - a);
     double f, h, hp, sc;
-    secular_eval(s, j - 1, half, lane, mask, f, h, hp, sc);
+    secular_eval(s, j - 1, half, lane, f, h, hp, sc);
     if (f >= 0.0) {
       K = j - 1;
       lo = 0.0;
@@ -134,9 +148,48 @@ __device__ void arrow_roots(ArrowSmem &s, int j, int lane, unsigned mask) {
     }
   }
   double tau = 0.5 * (lo + hi);
-  for (int it = 0; it < 200; ++it) {
+  {
+    // Starting point: zero of the model that keeps pole K and the pole N at
+    // the other end of the interval exactly and freezes the remaining terms
+    // (and, for interior roots, the linear term) at the interval midpoint.
+    // Newton on h then needs a few steps instead of working down from the
+    // midpoint.
+    const double dK = s.sd[K];
+    const int N = (j == 0 || j == np) ? -1 : (K == j - 1 ? j : j - 1);
+    double so = 0.0;
+    for (int i = lane; i < np; i += 32) {
+      if (i == K || i == N) continue;
+      so += s.sz[i] * s.sz[i] * fast_rcp(tau - (s.sd[i] - dK));
+    }
+    so = wsum(so);
+    const double zK2 = s.sz[K] * s.sz[K];
+    double guess;
+    if (N < 0) {
+      // (c + t) t - zK2 = 0, the positive root right of all poles, the
+      // negative one left of them (cancellation-free forms)
+      const double c = dK - s.alpha - so;
+      const double sq = sqrt(c * c + 4.0 * zK2);
+      if (j == np)
+        guess = (c <= 0.0) ? 0.5 * (sq - c) : 2.0 * zK2 / (sq + c);
+      else
+        guess = (c >= 0.0) ? -0.5 * (sq + c) : -2.0 * zK2 / (sq - c);
+    } else {
+      // c t (t - dN) - zK2 (t - dN) - zN2 t = 0 has one zero in (lo, hi)
+      const double dN = s.sd[N] - dK;
+      const double zN2 = s.sz[N] * s.sz[N];
+      const double c = dK - s.alpha + tau - so;
+      const double A = c, B = -(c * dN + zK2 + zN2), C = zK2 * dN;
+      const double q = -0.5 * (B + copysign(sqrt(fmax(B * B - 4.0 * A * C, 0.0)), B));
+      const double t1 = (A != 0.0) ? q / A : lo;
+      const double t2 = (q != 0.0) ? C / q : lo;
+      guess = (t1 > lo && t1 < hi) ? t1 : t2;
+    }
+    if (guess > lo && guess < hi) tau = guess;
+  }
+  int it = 0;
+  for (; it < 200; ++it) {
     double f, h, hp, sc;
-    secular_eval(s, K, tau, lane, mask, f, h, hp, sc);
+    secular_eval(s, K, tau, lane, f, h, hp, sc);
     if (f == 0.0) break;
     if (f > 0.0)
       hi = tau;
@@ -155,6 +208,12 @@ __device__ void arrow_roots(ArrowSmem &s, int j, int lane, unsigned mask) {
     }
     tau = nt;
   }
+#ifdef SVDSB_PHASE_CLOCKS
+  if (lane == 0) {
+    atomicMax(reinterpret_cast<unsigned long long *>(&g_arrow_clk[14]), (unsigned long long)it);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&g_arrow_clk[15]), (unsigned long long)it);
+  }
+#endif
   if (lane == 0) {
     s.korg[j] = K;
     s.tau[j] = tau;
@@ -168,18 +227,26 @@ __device__ __forceinline__ double lam_minus_pole(const ArrowSmem &s, int j, int 
 
 // Solve one arrowhead [[diag(d[0..n-1)), z],[z^T, alpha]] of size n+1.
 // Outputs newd[0..n] and P ((n+1) x (n+1), column-major, ld = ldp) in the
-// original coordinates (border coordinate n).
+// original coordinates (border coordinate n).  n < kAN <= blockDim.x.
 __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  if (tid == 0) {
-    double dm = fabs(s.alpha), zn = 0.0;
-    for (int i = 0; i < n; ++i) {
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  if (warp == 0) {
+    double dm = 0.0, zn = 0.0;
+    for (int i = lane; i < n; i += 32) {
       dm = fmax(dm, fabs(s.d[i]));
-      zn += s.z[i] * s.z[i];
+      zn = fma(s.z[i], s.z[i], zn);
     }
-    zn = sqrt(zn);
-    s.znorm = zn;
-    s.tol = 8.0 * kEps * fmax(dm, zn);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+      zn += __shfl_xor_sync(0xffffffffu, zn, o);
+    }
+    if (lane == 0) {
+      zn = sqrt(zn);
+      s.znorm = zn;
+      s.tol = 8.0 * kEps * fmax(fmax(dm, fabs(s.alpha)), zn);
+    }
   }
   __syncthreads();
   SVDSB_PHASE(3);
@@ -194,83 +261,89 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
       if (!s.defl[k] && (s.d[k] < di || (s.d[k] == di && k < i))) ++r;
     s.sidx[r] = i;
   }
-  __syncthreads();
+  const int np0 = __syncthreads_count(tid < n && !s.defl[tid]);
   SVDSB_PHASE(4);
-  if (tid == 0) {
-    int np = 0;
-    for (int i = 0; i < n; ++i) np += !s.defl[i];
-    // type-2 deflation: (nearly) equal neighbouring poles
-    int nrot = 0;
-    int w = 0;  // write cursor of compacted survivors
-    int prev = -1;
-    for (int r = 0; r < np; ++r) {
-      int i = s.sidx[r];
-      if (prev >= 0 && s.d[i] - s.d[prev] <= s.tol) {
-        double za = s.z[prev], zb = s.z[i];
-        double rr = hypot(za, zb);
-        double c = zb / rr, sn = za / rr;
-        s.ra[nrot] = prev;
-        s.rb[nrot] = i;
-        s.rc[nrot] = c;
-        s.rs[nrot] = sn;
-        ++nrot;
-        s.z[prev] = 0.0;
-        s.z[i] = rr;
-        s.defl[prev] = 1;
-        --w;  // prev leaves the survivor list
+  // type-2 deflation: (nearly) equal neighbouring poles.  The scan chains
+  // through the survivors, so it runs on one thread -- only when needed.
+  const bool close = tid >= 1 && tid < np0 && (s.d[s.sidx[tid]] - s.d[s.sidx[tid - 1]] <= s.tol);
+  if (__syncthreads_or(close)) {
+    if (tid == 0) {
+      int nrot = 0;
+      int w = 0;  // write cursor of compacted survivors
+      int prev = -1;
+      for (int r = 0; r < np0; ++r) {
+        int i = s.sidx[r];
+        if (prev >= 0 && s.d[i] - s.d[prev] <= s.tol) {
+          double za = s.z[prev], zb = s.z[i];
+          double rr = hypot(za, zb);
+          double c = zb / rr, sn = za / rr;
+          s.ra[nrot] = prev;
+          s.rb[nrot] = i;
+          s.rc[nrot] = c;
+          s.rs[nrot] = sn;
+          ++nrot;
+          s.z[prev] = 0.0;
+          s.z[i] = rr;
+          s.defl[prev] = 1;
+          --w;  // prev leaves the survivor list
+        }
+        s.sidx[w++] = i;
+        prev = i;
       }
-      s.sidx[w++] = i;
-      prev = i;
+      s.np = w;
+      s.nrot = nrot;
+      for (int r = 0; r < w; ++r) {
+        s.sd[r] = s.d[s.sidx[r]];
+        s.sz[r] = s.z[s.sidx[r]];
+      }
     }
-    s.np = w;
-    s.nrot = nrot;
-    for (int r = 0; r < w; ++r) {
-      s.sd[r] = s.d[s.sidx[r]];
-      s.sz[r] = s.z[s.sidx[r]];
+  } else {
+    if (tid < np0) {
+      s.sd[tid] = s.d[s.sidx[tid]];
+      s.sz[tid] = s.z[s.sidx[tid]];
+    }
+    if (tid == 0) {
+      s.np = np0;
+      s.nrot = 0;
     }
   }
   __syncthreads();
   SVDSB_PHASE(5);
   const int np = s.np;
-  {
-    // one 8-lane group per root; groups of a warp run independently
-    const int lane = tid & (kGroup - 1);
-    const unsigned mask = 0xffu << (tid & 31 & ~(kGroup - 1));
-    for (int j = tid / kGroup; j <= np; j += nt / kGroup) arrow_roots(s, j, lane, mask);
-  }
+  for (int j = warp; j <= np; j += nwarp) arrow_roots(s, j, lane);
   __syncthreads();
   SVDSB_PHASE(6);
-  // Gu-Eisenstat couplings
-  for (int i = tid; i < np; i += nt) {
-    double prod = lam_minus_pole(s, i, i) * lam_minus_pole(s, i + 1, i);
-    for (int k = 0; k < np; ++k) {
+  // Gu-Eisenstat couplings: one warp per pole, lane-strided partial
+  // products of the ratios, fixed xor-tree product
+  for (int i = warp; i < np; i += nwarp) {
+    double prod = 1.0;
+    for (int k = lane; k < np; k += 32) {
       if (k == i) continue;
       double num = (k < i) ? lam_minus_pole(s, k, i) : lam_minus_pole(s, k + 1, i);
       prod *= num / (s.sd[k] - s.sd[i]);
     }
-    double zh = sqrt(fabs(prod));
-    s.zhat[i] = (s.sz[i] >= 0.0) ? zh : -zh;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) prod *= __shfl_xor_sync(0xffffffffu, prod, o);
+    if (lane == 0) {
+      prod *= lam_minus_pole(s, i, i) * lam_minus_pole(s, i + 1, i);
+      double zh = sqrt(fabs(prod));
+      s.zhat[i] = (s.sz[i] >= 0.0) ? zh : -zh;
+    }
   }
-  __syncthreads();
-  SVDSB_PHASE(7);
   // eigenvector columns: first the deflated original indices, then roots
   const int N1 = n + 1;
   for (int e = tid; e < N1 * N1; e += nt) P[(e % N1) + (e / N1) * ldp] = 0.0;
   __syncthreads();
-  if (tid == 0) {
-    int col = 0;
-    for (int i = 0; i < n; ++i)
-      if (s.defl[i]) {
-        P[i + col * ldp] = 1.0;
-        s.newd[col] = s.d[i];
-        ++col;
-      }
-    for (int j = 0; j <= np; ++j) {
-      s.newd[col + j] = (np == 0) ? s.alpha : s.sd[s.korg[j]] + s.tau[j];
-    }
-  }
-  __syncthreads();
+  SVDSB_PHASE(7);
   const int ndefl = n - np;
+  for (int i = tid; i < n; i += nt) {
+    if (!s.defl[i]) continue;
+    int col = 0;
+    for (int k = 0; k < i; ++k) col += s.defl[k];
+    P[i + col * ldp] = 1.0;
+    s.newd[col] = s.d[i];
+  }
+  for (int j = tid; j <= np; j += nt) s.newd[ndefl + j] = (np == 0) ? s.alpha : s.sd[s.korg[j]] + s.tau[j];
   if (np == 0) {
     if (tid == 0) P[n + ndefl * ldp] = 1.0;
   } else {
@@ -280,11 +353,15 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
       P[s.sidx[i] + (ndefl + j) * ldp] = s.zhat[i] / lam_minus_pole(s, j, i);
     }
     __syncthreads();
-    for (int j = tid; j <= np; j += nt) {
-      double *pc = P + (ndefl + j) * ldp;
-      double nrm2 = 1.0;
-      for (int i = 0; i < np; ++i) nrm2 += pc[s.sidx[i]] * pc[s.sidx[i]];
-      s.tau2[j] = 1.0 / sqrt(nrm2);
+    for (int j = warp; j <= np; j += nwarp) {
+      const double *pc = P + (ndefl + j) * ldp;
+      double a = 0.0;
+      for (int i = lane; i < np; i += 32) {
+        const double v = pc[s.sidx[i]];
+        a = fma(v, v, a);
+      }
+      a = wsum(a);
+      if (lane == 0) s.tau2[j] = 1.0 / sqrt(1.0 + a);
     }
     __syncthreads();
     for (int e = tid; e < (np + 1) * (np + 1); e += nt) {
@@ -299,16 +376,18 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
   __syncthreads();
   SVDSB_PHASE(8);
   // undo the deflation rotations (last created first): v = G_1 ... G_r v'
-  for (int c = tid; c < N1; c += nt) {
-    double *pc = P + c * ldp;
-    for (int k = s.nrot - 1; k >= 0; --k) {
-      int a = s.ra[k], b = s.rb[k];
-      double va = pc[a], vb = pc[b];
-      pc[a] = s.rc[k] * va + s.rs[k] * vb;
-      pc[b] = -s.rs[k] * va + s.rc[k] * vb;
+  if (s.nrot > 0) {
+    for (int c = tid; c < N1; c += nt) {
+      double *pc = P + c * ldp;
+      for (int k = s.nrot - 1; k >= 0; --k) {
+        int a = s.ra[k], b = s.rb[k];
+        double va = pc[a], vb = pc[b];
+        pc[a] = s.rc[k] * va + s.rs[k] * vb;
+        pc[b] = -s.rs[k] * va + s.rc[k] * vb;
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
   SVDSB_PHASE(9);
 }
 
@@ -322,7 +401,7 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
   const int ld = G + 1;
   double *Y = dyn;             // G x G current eigvecs (in V coordinates)
   double *P = Y + G * ld;      // arrowhead eigvecs
-  double *T = P + G * ld;      // product scratch
+  double *T = P + G * ld;      // product buffer (swapped with Y)
   double *lam = T + G * ld;    // current eigenvalues
   const int tid = threadIdx.x, nt = blockDim.x;
   pdl_wait();
@@ -353,7 +432,7 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
     __syncthreads();
     SVDSB_PHASE(2);
     arrow_solve(s, sdim, P, ld);
-    // Y <- blkdiag(Y, 1) P   (size sdim+1)
+    // T <- blkdiag(Y, 1) P   (size sdim+1), then T becomes Y
     const int n1 = sdim + 1;
     for (int e = tid; e < n1 * n1; e += nt) {
       int r = e % n1, c = e / n1;
@@ -369,11 +448,9 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
     for (int c = tid; c < n1; c += nt) lam[c] = s.newd[c];
     __syncthreads();
     SVDSB_PHASE(10);
-    for (int e = tid; e < n1 * n1; e += nt) {
-      int r = e % n1, c = e / n1;
-      Y[r + c * ld] = T[r + c * ld];
-    }
-    __syncthreads();
+    double *tmp = Y;
+    Y = T;
+    T = tmp;
     SVDSB_PHASE(11);
   }
   // ordering as in syev_jacobi_kernel: ascending ranks first (ties by
@@ -412,7 +489,13 @@ syev_update_kernel(int g0, int b, const double *__restrict__ h, int64_t ldh, con
       }
     }
     w_out[pos] = wi;
-    for (int r = 0; r < G; ++r) y_out[r + (int64_t)pos * ldy] = Y[r + i * ld];
+    s.perm[pos] = i;
+  }
+  __syncthreads();
+  // coalesced write-out of the permuted eigenvectors
+  for (int e = tid; e < G * G; e += nt) {
+    const int r = e % G, c = e / G;
+    y_out[r + (int64_t)c * ldy] = Y[r + s.perm[c] * ld];
   }
 #ifdef SVDSB_PHASE_CLOCKS
   __syncthreads();

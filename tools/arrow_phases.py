@@ -66,6 +66,7 @@ def run(g):
     w = np.linalg.eigvalsh(h0)
     print("max |w - eigvalsh| = %.2e" % np.abs(np.sort(W[:g + 1].cpu().numpy()) - w).max())
     last = rows[-1]
+    print("root iterations: max %d, total %d (accumulated over %d calls)" % (clk[14], clk[15], len(rows)))
     tot = last[-1] - last[0]
     print("G = %d, total %d cycles (%.1f us at 1.965 GHz)" % (g + 1, tot, tot / 1965.0))
     for i, name in enumerate(PHASES):
