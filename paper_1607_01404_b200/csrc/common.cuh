@@ -128,16 +128,46 @@ __device__ __forceinline__ double warp_sum(double v) {
 // the nparts CTAs and a fixed xor tree combines them, so the result is
 // deterministic and the load chain is nparts / 32 deep instead of nparts.
 // emit(o, t, k, sum) is called by lane 0 of the owning warp.
+// Wide partial vectors (per >= 16) are read by (k, slice) thread pairs
+// instead -- consecutive threads take consecutive k, so every warp load is
+// coalesced -- and the slices are combined in shared memory in fixed order.
+// Must be called by every thread of the CTA (it synchronises).
 template <typename Emit>
 __device__ __forceinline__ void fold_parts(const double *partials, unsigned nparts, int per, int nout, Emit emit) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nt = blockDim.x;
+  if (per >= 16 && per <= nt) {
+    __shared__ double red[1024];
+    const int S = nt / per;
+    const int k = threadIdx.x % per, sl = threadIdx.x / per;
+    const int ntile = (nout + per - 1) / per;
+    for (int t = 0; t < ntile; ++t) {
+      const double *pp = partials + (int64_t)t * nparts * per + k;
+      double acc = 0.0;
+      if (sl < S) {
+#pragma unroll 8
+        for (unsigned bx = sl; bx < nparts; bx += S) acc += pp[(int64_t)bx * per];
+      }
+      red[threadIdx.x] = acc;
+      __syncthreads();
+      if (threadIdx.x < per) {
+        double s = 0.0;
+        for (int q = 0; q < S; ++q) s += red[q * per + threadIdx.x];
+        const int o = t * per + threadIdx.x;
+        if (o < nout) emit(o, t, (int)threadIdx.x, s);
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = nt >> 5;
   for (int o = w; o < nout; o += nw) {
-    const int t = o / per, k = o % per;
-    const double *pp = partials + (int64_t)t * nparts * per + k;
+    const int t = o / per, kk = o % per;
+    const double *pp = partials + (int64_t)t * nparts * per + kk;
     double s = 0.0;
+#pragma unroll 4
     for (unsigned bx = lane; bx < nparts; bx += 32) s += pp[(int64_t)bx * per];
     s = warp_sum(s);
-    if (lane == 0) emit(o, t, k, s);
+    if (lane == 0) emit(o, t, kk, s);
   }
 }
 
