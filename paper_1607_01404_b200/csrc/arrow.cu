@@ -6,7 +6,7 @@
 // the basis blkdiag(Y0, I_b) the new projection is an arrowhead matrix per
 // border.  Each border is absorbed exactly with the secular equation
 //     f(lam) = lam - alpha - sum_i z_i^2 / (lam - d_i) = 0,
-// one warp per root (safeguarded Newton on f*(lam - d_K) about the nearest
+// one lane group per root (safeguarded Newton on f*(lam - d_K) about the nearest
 // pole K), deflation of tiny couplings and of (nearly) equal poles by Givens
 // rotations, and Gu-Eisenstat recomputed couplings z^ so the computed
 // eigenvectors are orthogonal to working precision.  Cost is O(g^2) per
@@ -61,6 +61,19 @@ __device__ long long g_arrow_clk[16];
   } while (0)
 #endif
 
+// Lanes per secular root: a small group keeps the FP64 work per Newton step
+// low (one SM executes every root), a wide one shortens each step's chain.
+#ifndef SVDSB_ARROW_GROUP
+#define SVDSB_ARROW_GROUP 16
+#endif
+constexpr int kRG = SVDSB_ARROW_GROUP;
+
+__device__ __forceinline__ double gsum(double v, unsigned mask) {
+#pragma unroll
+  for (int o = 1; o < kRG; o <<= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -80,13 +93,14 @@ __device__ __forceinline__ double fast_rcp(double x) {
 }
 
 // f(tau) with origin pole K (sorted index), also the pieces of h = tau*f
-// without the K pole.  Evaluated by one warp (lane l sums terms l, l+32),
-// combined with a fixed xor tree so every lane holds identical values.
-__device__ __forceinline__ void secular_eval(const ArrowSmem &s, int K, double tau, int lane, double &f,
-                                             double &h, double &hp, double &fscale) {
+// without the K pole.  Evaluated by a kRG-lane group (lane l sums terms l,
+// l+kRG, ...), combined with a fixed xor tree so every lane of the group
+// holds identical values.
+__device__ __forceinline__ void secular_eval(const ArrowSmem &s, int K, double tau, int lane, unsigned mask,
+                                             double &f, double &h, double &hp, double &fscale) {
   const double dK = s.sd[K];
   double sum = 0.0, sum_nk = 0.0, dsum_nk = 0.0, scale = 0.0;
-  for (int i = lane; i < s.np; i += 32) {
+  for (int i = lane; i < s.np; i += kRG) {
     const double den = tau - (s.sd[i] - dK);   // lam - d_i
     const double inv = fast_rcp(den);
     const double zz = s.sz[i] * s.sz[i];
@@ -98,10 +112,10 @@ __device__ __forceinline__ void secular_eval(const ArrowSmem &s, int K, double t
       dsum_nk += t * inv;
     }
   }
-  sum = wsum(sum);
-  scale = wsum(scale) + fabs(dK - s.alpha) + fabs(tau);
-  sum_nk = wsum(sum_nk);
-  dsum_nk = wsum(dsum_nk);
+  sum = gsum(sum, mask);
+  scale = gsum(scale, mask) + fabs(dK - s.alpha) + fabs(tau);
+  sum_nk = gsum(sum_nk, mask);
+  dsum_nk = gsum(dsum_nk, mask);
   f = (dK - s.alpha) + tau - sum;
   const double zK2 = s.sz[K] * s.sz[K];
   h = tau * ((dK - s.alpha) + tau - sum_nk) - zK2;
@@ -111,7 +125,7 @@ __device__ __forceinline__ void secular_eval(const ArrowSmem &s, int K, double t
 
 // Root j of np+1 (ascending; interval (sd[j-1], sd[j])), solved by one warp;
 // lane 0 stores the result.
-__device__ void arrow_roots(ArrowSmem &s, int j, int lane) {
+__device__ void arrow_roots(ArrowSmem &s, int j, int lane, unsigned mask) {
   const int np = s.np;
   int K;
   double lo, hi;
@@ -136,7 +150,7 @@ __device__ void arrow_roots(ArrowSmem &s, int j, int lane) {
     const double a = s.sd[j - 1], b = s.sd[j];
     const double half = 0.5 * (b - a);
     double f, h, hp, sc;
-    secular_eval(s, j - 1, half, lane, f, h, hp, sc);
+    secular_eval(s, j - 1, half, lane, mask, f, h, hp, sc);
     if (f >= 0.0) {
       K = j - 1;
       lo = 0.0;
@@ -157,11 +171,11 @@ __device__ void arrow_roots(ArrowSmem &s, int j, int lane) {
     const double dK = s.sd[K];
     const int N = (j == 0 || j == np) ? -1 : (K == j - 1 ? j : j - 1);
     double so = 0.0;
-    for (int i = lane; i < np; i += 32) {
+    for (int i = lane; i < np; i += kRG) {
       if (i == K || i == N) continue;
       so += s.sz[i] * s.sz[i] * fast_rcp(tau - (s.sd[i] - dK));
     }
-    so = wsum(so);
+    so = gsum(so, mask);
     const double zK2 = s.sz[K] * s.sz[K];
     double guess;
     if (N < 0) {
@@ -189,14 +203,14 @@ __device__ void arrow_roots(ArrowSmem &s, int j, int lane) {
   int it = 0;
   for (; it < 200; ++it) {
     double f, h, hp, sc;
-    secular_eval(s, K, tau, lane, f, h, hp, sc);
+    secular_eval(s, K, tau, lane, mask, f, h, hp, sc);
     if (f == 0.0) break;
     if (f > 0.0)
       hi = tau;
     else
       lo = tau;
     if (fabs(f) <= 4.0 * kEps * sc) break;
-    double nt = (hp != 0.0) ? tau - h / hp : 0.5 * (lo + hi);
+    double nt = (hp != 0.0) ? tau - h * fast_rcp(hp) : 0.5 * (lo + hi);
     if (!(nt > lo && nt < hi)) nt = 0.5 * (lo + hi);
     if (nt == tau || fabs(nt - tau) <= 2.0 * kEps * fabs(nt)) {
       tau = nt;
@@ -310,7 +324,11 @@ __device__ void arrow_solve(ArrowSmem &s, int n, double *P, int ldp) {
   __syncthreads();
   SVDSB_PHASE(5);
   const int np = s.np;
-  for (int j = warp; j <= np; j += nwarp) arrow_roots(s, j, lane);
+  {
+    const int gl = tid & (kRG - 1);
+    const unsigned gmask = (kRG == 32) ? 0xffffffffu : (((1u << kRG) - 1u) << ((tid & 31) & ~(kRG - 1)));
+    for (int j = tid / kRG; j <= np; j += nt / kRG) arrow_roots(s, j, gl, gmask);
+  }
   __syncthreads();
   SVDSB_PHASE(6);
   // Gu-Eisenstat couplings: one warp per pole, lane-strided partial

@@ -15,7 +15,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 sys.path.insert(0, REPO)
-OUT = os.path.join(HERE, "_dbg", "libsvdsb_phase.so")
+GROUP = os.environ.get("ARROW_GROUP", "")
+OUT = os.path.join(HERE, "_dbg", "libsvdsb_phase%s.so" % GROUP)
 
 PHASES = ["load Y0/lam", "border column + z", "norms (tid 0)", "defl + sort", "type-2 deflation (tid 0)",
           "secular roots", "Gu-Eisenstat", "eigvec fill/normalise", "rotations", "Y <- Y P", "copy T->Y",
@@ -28,8 +29,8 @@ def build():
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     objs = []
     for src in ("runtime.cu", "arrow.cu"):
-        obj = os.path.join(os.path.dirname(OUT), src.replace(".cu", ".o"))
-        cmd = [b.NVCC, *b.ARCH, *[f for f in b.FLAGS if f != "-v" and f != "-Xptxas"], "-DSVDSB_PHASE_CLOCKS",
+        obj = os.path.join(os.path.dirname(OUT), src.replace(".cu", GROUP + ".o"))
+        cmd = [b.NVCC, *b.ARCH, *[f for f in b.FLAGS if f != "-v" and f != "-Xptxas"], "-DSVDSB_PHASE_CLOCKS", *(["-DSVDSB_ARROW_GROUP=" + GROUP] if GROUP else []),
                "-I", os.path.join(REPO, "include"), "-c", os.path.join(b.CSRC, src), "-o", obj]
         subprocess.run(cmd, check=True)
         objs.append(obj)
