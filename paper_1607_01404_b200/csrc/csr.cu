@@ -23,6 +23,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace svdsb {
@@ -430,16 +432,146 @@ csr_tile_pipe_rows_kernel(int ntile, const int4 *__restrict__ info, const int *_
   }
 }
 
+// ------------------------------------------------ bulk-copy tile pipeline
+// b = 1 SpMV with the matrix stream moved by the copy engine: each tile's
+// val / col / row_ptr ranges go global -> shared with cp.async.bulk
+// (16-byte granules, completion counted on one mbarrier per stage) into a
+// kBulkStages-deep ring, so up to kBulkStages - 1 tiles are in flight per
+// CTA without holding them in registers.  Threads only gather x, form the
+// products in place and fold each row in the reference's order -- the same
+// arithmetic as csr_tile_pipe_kernel, bit for bit.
+constexpr int kBulkStages = 2;
+
+struct __align__(128) BulkStage {
+  double val[kTileNnz + 2];
+  int col[kTileNnz + 4];
+  int rp[kTileRows + 1 + 8];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n"
+               " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+template <int ORDER, bool SHORT>
+__global__ void __launch_bounds__(kTileThreads, 2)
+csr_tile_bulk_kernel(int ntile, const int4 *__restrict__ info, const int *__restrict__ row_ptr,
+                     const int *__restrict__ col, const double *__restrict__ val, const double *__restrict__ x,
+                     double *__restrict__ y, int accumulate) {
+  extern __shared__ __align__(128) unsigned char bulk_smem[];
+  BulkStage *stg = reinterpret_cast<BulkStage *>(bulk_smem);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(bulk_smem + kBulkStages * sizeof(BulkStage));
+  __shared__ int4 tinfo[kBulkStages];
+  const int t = threadIdx.x;
+  if (blockIdx.x >= ntile) return;
+  if (t == 0) {
+    for (int k = 0; k < kBulkStages; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(bar + k)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // thread 0: arm stage k's barrier with the byte count and start the copies
+  auto issue = [&](int tile, int k) {
+    const int4 ti = info[tile];
+    tinfo[k] = ti;
+    const int v0 = ti.z & ~1, v1 = (ti.w + 1) & ~1;
+    const int c0 = ti.z & ~3, c1 = (ti.w + 3) & ~3;
+    const int r0 = ti.x & ~3, r1 = (ti.y + 4) & ~3;
+    const unsigned bytes = 8u * (v1 - v0) + 4u * (c1 - c0) + 4u * (r1 - r0);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar + k)), "r"(bytes)
+                 : "memory");
+    if (v1 > v0) bulk_g2s(stg[k].val, val + v0, 8u * (v1 - v0), bar + k);
+    if (c1 > c0) bulk_g2s(stg[k].col, col + c0, 4u * (c1 - c0), bar + k);
+    bulk_g2s(stg[k].rp, row_ptr + r0, 4u * (r1 - r0), bar + k);
+  };
+  // the matrix is immutable after assembly: start streaming it before the
+  // producer of x has finished
+  if (t == 0)
+    for (int k = 0; k < kBulkStages; ++k) {
+      const int tk = blockIdx.x + k * gridDim.x;
+      if (tk < ntile) issue(tk, k);
+    }
+  pdl_wait();
+  int k = 0;
+  unsigned phase = 0;
+  for (int tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    mbar_wait(bar + k, phase);
+    const int4 ti = tinfo[k];
+    const int nnz = ti.w - ti.z, nrows = ti.y - ti.x;
+    double *pv = stg[k].val + (ti.z & 1);
+    const int *pc = stg[k].col + (ti.z & 3);
+    const int *prp = stg[k].rp + (ti.x & 3);
+    if (SHORT) {
+      // rows of <= 8 nonzeros: each thread gathers and folds its own row,
+      // so no CTA barrier separates the gathers from the folds
+      if (t < nrows) {
+        const int s0 = prp[t] - ti.z;
+        const int len = prp[t + 1] - prp[t];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < len) pv[s0 + j] = dmul(pv[s0 + j], __ldg(x + pc[s0 + j]));
+        y[ti.x + t] = accumulate ? fold_row_from(y[ti.x + t], pv + s0, len) : fold_row<ORDER, SHORT>(pv + s0, len);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) {
+        const int e = t + i * kTileThreads;
+        if (e < nnz) pv[e] = dmul(pv[e], __ldg(x + pc[e]));
+      }
+      __syncthreads();
+      if (t < nrows) {
+        const int s0 = prp[t] - ti.z;
+        const int len = prp[t + 1] - prp[t];
+        y[ti.x + t] = accumulate ? fold_row_from(y[ti.x + t], pv + s0, len) : fold_row<ORDER, SHORT>(pv + s0, len);
+      }
+    }
+    __syncthreads();  // stage k consumed
+    if (t == 0) {
+      const int nt = tile + kBulkStages * gridDim.x;
+      if (nt < ntile) {
+        // generic-proxy writes (the products) precede the copy engine's
+        // next writes into this stage
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(nt, k);
+      }
+    }
+    if (++k == kBulkStages) {
+      k = 0;
+      phase ^= 1u;
+    }
+  }
+  pdl_trigger();
+}
+
+static bool spmv_bulk_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("SVDSB_SPMV_BULK");
+    on = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 static int pipe_rows_grid(const void *kernel, size_t smem) {
-  static const void *which[4] = {nullptr, nullptr, nullptr, nullptr};
-  static int cap[4] = {0, 0, 0, 0};
-  for (int i = 0; i < 4; ++i)
+  static const void *which[8] = {nullptr};
+  static int cap[8] = {0};
+  for (int i = 0; i < 8; ++i)
     if (which[i] == kernel) return cap[i];
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kTileThreads, smem);
   if (occ < 1) occ = 1;
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 8; ++i)
     if (!which[i]) {
       which[i] = kernel;
       cap[i] = occ * kNumSMs;
@@ -598,10 +730,19 @@ static void free_part(CsrPart &p) {
   p = CsrPart();
 }
 
+// Device arrays of a CSR part carry kAllocPad bytes of slack: the bulk-copy
+// SpMV moves whole 16-byte granules, which can reach past the last element.
+constexpr size_t kAllocPad = 64;
+
+template <typename T>
+static cudaError_t alloc_pad(T **dst, size_t n) {
+  return cudaMalloc(dst, n * sizeof(T) + kAllocPad);
+}
+
 template <typename T>
 static int upload(T **dst, const std::vector<T> &src, cudaStream_t st) {
   size_t n = std::max<size_t>(src.size(), 1);
-  SVDSB_CUDA(cudaMalloc(dst, n * sizeof(T)));
+  SVDSB_CUDA(alloc_pad(dst, n));
   if (!src.empty())
     SVDSB_CUDA(cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st));
   return SVDSB_OK;
@@ -711,7 +852,12 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
     int bb = std::min(kMaxB, b - c0);
     const double *xc = x + (int64_t)c0 * ldx;
     double *yc = y + (int64_t)c0 * ldy;
-    if (p.ntile > 0 && bb == 1) {
+    if (p.ntile > 0 && bb == 1 && spmv_bulk_on()) {
+      const size_t sm = kBulkStages * sizeof(BulkStage) + kBulkStages * sizeof(uint64_t);
+      auto k = p.maxlen <= 8 ? csr_tile_bulk_kernel<ORDER, true> : csr_tile_bulk_kernel<ORDER, false>;
+      const int g = std::min(p.ntile, pipe_rows_grid(reinterpret_cast<const void *>(k), sm));
+      SVDSB_LAUNCH_PDL(k, g, kTileThreads, sm, st, p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc, acc);
+    } else if (p.ntile > 0 && bb == 1) {
       if (p.maxlen <= 8) {
         auto k = csr_tile_pipe_kernel<ORDER, true>;
         const int g = std::min(p.ntile, pipe_grid(reinterpret_cast<const void *>(k)));
@@ -796,9 +942,9 @@ static int build_transpose(const CsrPart &a, CsrPart &at, cudaStream_t st) {
   at.cols = a.rows;
   at.nnz = a.nnz;
   const int64_t nnz = a.nnz;
-  SVDSB_CUDA(cudaMalloc(&at.row_ptr, sizeof(int) * (at.rows + 1)));
-  SVDSB_CUDA(cudaMalloc(&at.col, sizeof(int) * std::max<int64_t>(nnz, 1)));
-  SVDSB_CUDA(cudaMalloc(&at.val, sizeof(double) * std::max<int64_t>(nnz, 1)));
+  SVDSB_CUDA(alloc_pad(&at.row_ptr, at.rows + 1));
+  SVDSB_CUDA(alloc_pad(&at.col, std::max<int64_t>(nnz, 1)));
+  SVDSB_CUDA(alloc_pad(&at.val, std::max<int64_t>(nnz, 1)));
   SVDSB_CUDA(cudaMemsetAsync(at.row_ptr, 0, sizeof(int) * (at.rows + 1), st));
   if (nnz > 0) {
     int *rows = nullptr, *idx = nullptr, *keys_out = nullptr, *perm = nullptr, *counts = nullptr;
@@ -970,7 +1116,7 @@ static int build_blocked_transpose(svdsb_csr *h, cudaStream_t st) {
     CsrPart p;
     p.rows = n;
     p.cols = r1 - r0;
-    SVDSB_CUDA(cudaMalloc(&p.row_ptr, sizeof(int) * (n + 1)));
+    SVDSB_CUDA(alloc_pad(&p.row_ptr, n + 1));
     SVDSB_CUDA(cudaMemsetAsync(len + n, 0, sizeof(int), st));
     seg_bounds_kernel<<<grid1(n), 256, 0, st>>>(n, at.row_ptr, at.col, (int)r0, (int)r1, lo, len);
     SVDSB_LAUNCHED();
@@ -980,8 +1126,8 @@ static int build_blocked_transpose(svdsb_csr *h, cudaStream_t st) {
     SVDSB_CUDA(cudaMemcpyAsync(p.host_row_ptr.data(), p.row_ptr, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, st));
     SVDSB_CUDA(cudaStreamSynchronize(st));
     p.nnz = p.host_row_ptr[n];
-    SVDSB_CUDA(cudaMalloc(&p.col, sizeof(int) * std::max<int64_t>(p.nnz, 1)));
-    SVDSB_CUDA(cudaMalloc(&p.val, sizeof(double) * std::max<int64_t>(p.nnz, 1)));
+    SVDSB_CUDA(alloc_pad(&p.col, std::max<int64_t>(p.nnz, 1)));
+    SVDSB_CUDA(alloc_pad(&p.val, std::max<int64_t>(p.nnz, 1)));
     seg_copy_kernel<<<grid1(n), 256, 0, st>>>(n, at.col, at.val, lo, p.row_ptr, (int)r0, p.col, p.val);
     SVDSB_LAUNCHED();
     int rc = build_partition(p, st);
@@ -1053,7 +1199,7 @@ int svdsb_csr_create_host(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nnz, con
     svdsb_csr_destroy(h);
     return rc;
   }
-  if (cudaMalloc(&p.val, sizeof(double) * std::max<int64_t>(nnz, 1)) != cudaSuccess) {
+  if (alloc_pad(&p.val, std::max<int64_t>(nnz, 1)) != cudaSuccess) {
     svdsb_csr_destroy(h);
     set_error("cudaMalloc values failed");
     return SVDSB_ERR_ALLOC;
@@ -1086,7 +1232,7 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
   CsrPart &p = h->a;
   p.rows = m;
   p.cols = n;
-  SVDSB_CUDA(cudaMalloc(&p.row_ptr, sizeof(int) * (m + 1)));
+  SVDSB_CUDA(alloc_pad(&p.row_ptr, m + 1));
   SVDSB_CUDA(cudaMemsetAsync(p.row_ptr, 0, sizeof(int) * (m + 1), st));
   int64_t nnz = 0;
   if (nt > 0) {
@@ -1122,8 +1268,8 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     SVDSB_CUDA(cudaMemcpyAsync(&last_first, first + nt - 1, 4, cudaMemcpyDeviceToHost, st));
     SVDSB_CUDA(cudaStreamSynchronize(st));
     nnz = (int64_t)last_seg + last_first;
-    SVDSB_CUDA(cudaMalloc(&p.col, 4 * nnz));
-    SVDSB_CUDA(cudaMalloc(&p.val, 8 * nnz));
+    SVDSB_CUDA(alloc_pad(&p.col, std::max<int64_t>(nnz, 1)));
+    SVDSB_CUDA(alloc_pad(&p.val, std::max<int64_t>(nnz, 1)));
     coo_sum_kernel<<<grid1(nt), 256, 0, st>>>(nt, n, key_s, perm, first, seg, vals, p.col, p.val, rowcnt);
     SVDSB_LAUNCHED();
     size_t sb2 = 0;
