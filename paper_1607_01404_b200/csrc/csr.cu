@@ -463,7 +463,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
                " @!p bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
-template <int ORDER, bool SHORT>
+// ROWS: 0 = every tile row has <= 8 nonzeros, 1 = <= 32 (both: one thread
+// gathers and folds one row), 2 = longer rows (strided gathers, CTA barrier,
+// then the per-row folds).
+template <int ORDER, int ROWS>
 __global__ void __launch_bounds__(kTileThreads, 2)
 csr_tile_bulk_kernel(int ntile, const int4 *__restrict__ info, const int *__restrict__ row_ptr,
                      const int *__restrict__ col, const double *__restrict__ val, const double *__restrict__ x,
@@ -511,16 +514,20 @@ csr_tile_bulk_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
     double *pv = stg[k].val + (ti.z & 1);
     const int *pc = stg[k].col + (ti.z & 3);
     const int *prp = stg[k].rp + (ti.x & 3);
-    if (SHORT) {
-      // rows of <= 8 nonzeros: each thread gathers and folds its own row,
-      // so no CTA barrier separates the gathers from the folds
+    if (ROWS < 2) {
+      // short rows: each thread gathers (8 independent loads at a time) and
+      // folds its own row, so no CTA barrier separates gathers and folds
       if (t < nrows) {
         const int s0 = prp[t] - ti.z;
         const int len = prp[t + 1] - prp[t];
+        for (int j0 = 0; j0 < len; j0 += 8) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < len) pv[s0 + j] = dmul(pv[s0 + j], __ldg(x + pc[s0 + j]));
-        y[ti.x + t] = accumulate ? fold_row_from(y[ti.x + t], pv + s0, len) : fold_row<ORDER, SHORT>(pv + s0, len);
+          for (int j = 0; j < 8; ++j)
+            if (j0 + j < len) pv[s0 + j0 + j] = dmul(pv[s0 + j0 + j], __ldg(x + pc[s0 + j0 + j]));
+          if (ROWS == 0) break;
+        }
+        y[ti.x + t] = accumulate ? fold_row_from(y[ti.x + t], pv + s0, len)
+                                 : fold_row<ORDER, ROWS == 0>(pv + s0, len);
       }
     } else {
 #pragma unroll
@@ -532,7 +539,7 @@ csr_tile_bulk_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
       if (t < nrows) {
         const int s0 = prp[t] - ti.z;
         const int len = prp[t + 1] - prp[t];
-        y[ti.x + t] = accumulate ? fold_row_from(y[ti.x + t], pv + s0, len) : fold_row<ORDER, SHORT>(pv + s0, len);
+        y[ti.x + t] = accumulate ? fold_row_from(y[ti.x + t], pv + s0, len) : fold_row<ORDER, false>(pv + s0, len);
       }
     }
     __syncthreads();  // stage k consumed
@@ -854,7 +861,9 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
     double *yc = y + (int64_t)c0 * ldy;
     if (p.ntile > 0 && bb == 1 && spmv_bulk_on()) {
       const size_t sm = kBulkStages * sizeof(BulkStage) + kBulkStages * sizeof(uint64_t);
-      auto k = p.maxlen <= 8 ? csr_tile_bulk_kernel<ORDER, true> : csr_tile_bulk_kernel<ORDER, false>;
+      // (the per-row path pays off only for the shortest rows: longer ones
+      // serialise a thread's gathers, measured slower on configs 2 and 4)
+      auto k = p.maxlen <= 8 ? csr_tile_bulk_kernel<ORDER, 0> : csr_tile_bulk_kernel<ORDER, 2>;
       const int g = std::min(p.ntile, pipe_rows_grid(reinterpret_cast<const void *>(k), sm));
       SVDSB_LAUNCH_PDL(k, g, kTileThreads, sm, st, p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc, acc);
     } else if (p.ntile > 0 && bb == 1) {
