@@ -452,9 +452,13 @@ __device__ __forceinline__ unsigned smem_u32(const void *p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+// The matrix streams through L2 once per product: mark it evict-first so
+// the gathered vector x stays L2-resident.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar,
+                                         uint64_t policy) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+               " [%0], [%1], %2, [%3], %4;"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
@@ -483,6 +487,8 @@ csr_tile_bulk_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  uint64_t policy = 0;
+  if (t == 0) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
   // thread 0: arm stage k's barrier with the byte count and start the copies
   auto issue = [&](int tile, int k) {
     const int4 ti = info[tile];
@@ -493,9 +499,9 @@ csr_tile_bulk_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
     const unsigned bytes = 8u * (v1 - v0) + 4u * (c1 - c0) + 4u * (r1 - r0);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar + k)), "r"(bytes)
                  : "memory");
-    if (v1 > v0) bulk_g2s(stg[k].val, val + v0, 8u * (v1 - v0), bar + k);
-    if (c1 > c0) bulk_g2s(stg[k].col, col + c0, 4u * (c1 - c0), bar + k);
-    bulk_g2s(stg[k].rp, row_ptr + r0, 4u * (r1 - r0), bar + k);
+    if (v1 > v0) bulk_g2s(stg[k].val, val + v0, 8u * (v1 - v0), bar + k, policy);
+    if (c1 > c0) bulk_g2s(stg[k].col, col + c0, 4u * (c1 - c0), bar + k, policy);
+    bulk_g2s(stg[k].rp, row_ptr + r0, 4u * (r1 - r0), bar + k, policy);
   };
   // the matrix is immutable after assembly: start streaming it before the
   // producer of x has finished
@@ -569,12 +575,13 @@ static bool spmv_bulk_on() {
   return on == 1;
 }
 
-static int pipe_rows_grid(const void *kernel, size_t smem) {
+static int pipe_rows_grid(const void *kernel, size_t smem, bool bulk = false) {
   static const void *which[8] = {nullptr};
   static int cap[8] = {0};
   for (int i = 0; i < 8; ++i)
     if (which[i] == kernel) return cap[i];
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  (void)bulk;  // the default carveout keeps L1 for the gathered vector
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kTileThreads, smem);
   if (occ < 1) occ = 1;
@@ -864,7 +871,7 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
       // (the per-row path pays off only for the shortest rows: longer ones
       // serialise a thread's gathers, measured slower on configs 2 and 4)
       auto k = p.maxlen <= 8 ? csr_tile_bulk_kernel<ORDER, 0> : csr_tile_bulk_kernel<ORDER, 2>;
-      const int g = std::min(p.ntile, pipe_rows_grid(reinterpret_cast<const void *>(k), sm));
+      const int g = std::min(p.ntile, pipe_rows_grid(reinterpret_cast<const void *>(k), sm, true));
       SVDSB_LAUNCH_PDL(k, g, kTileThreads, sm, st, p.ntile, p.tile_info, p.row_ptr, p.col, p.val, xc, yc, acc);
     } else if (p.ntile > 0 && bb == 1) {
       if (p.maxlen <= 8) {
