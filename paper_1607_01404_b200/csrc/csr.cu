@@ -441,6 +441,7 @@ csr_tile_pipe_rows_kernel(int ntile, const int4 *__restrict__ info, const int *_
 // products in place and fold each row in the reference's order -- the same
 // arithmetic as csr_tile_pipe_kernel, bit for bit.
 constexpr int kBulkStages = 2;
+constexpr int64_t kBulkMinBytes = 64ll << 20;  // half of the 126 MB L2
 
 struct __align__(128) BulkStage {
   double val[kTileNnz + 2];
@@ -866,7 +867,10 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
     int bb = std::min(kMaxB, b - c0);
     const double *xc = x + (int64_t)c0 * ldx;
     double *yc = y + (int64_t)c0 * ldy;
-    if (p.ntile > 0 && bb == 1 && spmv_bulk_on()) {
+    // bulk-copy ring for matrices that stream from HBM; L2-resident ones
+    // (configs 1 and 2) are faster on the register-staged pipeline, which
+    // runs more CTAs per SM
+    if (p.ntile > 0 && bb == 1 && spmv_bulk_on() && 12 * p.nnz >= kBulkMinBytes) {
       const size_t sm = kBulkStages * sizeof(BulkStage) + kBulkStages * sizeof(uint64_t);
       // (the per-row path pays off only for the shortest rows: longer ones
       // serialise a thread's gathers, measured slower on configs 2 and 4)
