@@ -94,6 +94,29 @@ def test_spmv_bit_exact(m, n, nnz, b, rng):
     assert np.array_equal(got_t, want_t)
 
 
+def test_spmv_bulk_copy_path_bit_exact(rng):
+    """Matrices of >= 64 MB stream through the cp.async.bulk tile ring
+    (csr_tile_bulk_kernel); it must reproduce the reference's summation
+    order bit for bit like the register pipeline: a 100^3 7-point stencil
+    (1M rows, 6.9M nnz, 83 MB) for A x and A^T y, plus a scattered
+    rectangular matrix whose tiles take the strided path."""
+    from paper_1607_01404_b200 import workloads
+    m, n, r, c, v = workloads.c3_coo(nx=100)
+    a, (rp, ci, va) = _csr(m, n, r, c, v)
+    assert 12 * va.size >= 64 << 20
+    x = rng.standard_normal((n, 1))
+    assert np.array_equal(_spmv_dev(a, x, False), ocsr.spmv(m, n, rp, ci, va, x))
+    y = rng.standard_normal((m, 1))
+    assert np.array_equal(_spmv_dev(a, y, True), ocsr.spmv(m, n, rp, ci, va, y, transpose=True))
+    m2, n2 = 600000, 50000
+    rows = np.repeat(np.arange(m2), 12)
+    cols = rng.integers(0, n2, rows.size)
+    a2, (rp2, ci2, va2) = _csr(m2, n2, rows, cols, rng.standard_normal(rows.size))
+    assert 12 * va2.size >= 64 << 20
+    x2 = rng.standard_normal((n2, 1))
+    assert np.array_equal(_spmv_dev(a2, x2, False), ocsr.spmv(m2, n2, rp2, ci2, va2, x2))
+
+
 def test_spmv_long_rows_and_dead_rows(rng):
     """Rows longer than one tile (2048 nnz) take the chunked path: results
     are deterministic and within fp64 rounding of the sequential sum."""
