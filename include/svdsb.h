@@ -220,6 +220,21 @@ int svdsb_split_stats(svdsb_ctx *ctx, int64_t dim, int64_t nsplit,
  * out[j] = ||e1||^2 + ||e2||^2, formed elementwise (no cancellation).
  * stats: the 6-per-column output of svdsb_split_stats (device).  Columns
  * with nv == 0 or nu == 0 get out[j] = +inf. */
+/* The whole single-column expansion orthonormalisation in one launch (basis
+ * of <= 40 columns): x = R[:, *ci] (./ d when d != NULL, as
+ * svdsb_diag_solve), the +k coefficient copy prev[:g, :kk] = Y[:g, *ci ...]
+ * (when prev != NULL), then up to `passes` device-decided CGS passes as
+ * svdsb_cgs_pass and x /= final norm; `state` receives the DGKS record
+ * (svdsb_dgks_begin layout).  Replaces the orthonormalize / _expand
+ * sequence of eigensolver.py:666-700 + kernels.py:54-133 for one column.
+ * Uses a software grid barrier: the grid is at most one CTA per SM. */
+int svdsb_cgs_fused(svdsb_ctx *ctx, int64_t dim, int nblk,
+                    const double *const *xs, const int64_t *ldxs,
+                    const int *cols, const double *rsrc, int64_t ldr,
+                    const int *ci, const double *d, double *x,
+                    const double *yin, int64_t ldyin, int g, int kk,
+                    double *prev, int64_t ldprev, int passes, double *state,
+                    void *stream);
 /* Device-resident iterated CGS for ONE new column v (kernels.py:54-133
  * without the host round trip).  state: 8 doubles [active, pass,
  * collapses, orig, prev, final, |v|^2 before, |v|^2 after];

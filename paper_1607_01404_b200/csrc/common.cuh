@@ -101,6 +101,7 @@ struct svdsb_ctx {
   double *partials;      // kMaxPartials doubles
   unsigned int *ticket;  // kMaxTickets counters, always left at 0
   int next_ticket;
+  unsigned int *gbar;    // software grid barrier: {arrival count, generation}
 };
 
 namespace svdsb {

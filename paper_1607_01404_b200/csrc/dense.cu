@@ -761,6 +761,170 @@ ts_gemm_inplace_kernel(int64_t dim, double *x, int64_t ldx, int g, const double 
   }
 }
 
+
+// ------------------------------------------------ fused single-column CGS
+// The whole orthonormalisation of one expansion vector in ONE launch, for a
+// basis of <= 40 columns: select the residual column by the device index and
+// precondition it (x ./ d), the +k coefficient copy (CTA 0), then up to
+// `passes` iterated-CGS passes -- Gram, projection and the DGKS decision of
+// kernels.py:115-127 -- and the final normalisation.  A pass needs two
+// grid-wide reductions; between them the CTAs meet at a software grid
+// barrier and EVERY CTA folds the per-CTA partials itself in the same fixed
+// order, so all CTAs hold identical c, norms and DGKS state with no second
+// barrier and no serial fold.  One 512-thread CTA per SM, grid <= #SMs, so
+// every CTA is resident (the barrier's requirement); the kernel never
+// triggers its dependants early.  Each thread owns the same row pairs in
+// every phase, so x is read back only by the thread that wrote it.
+constexpr int kCgsThreads = 512;
+constexpr int kCgsMaxCols = 40;
+
+__device__ __forceinline__ void grid_barrier(unsigned int *bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int *gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int NACC>
+__device__ __forceinline__ void cta_fold_wide(double (&acc)[NACC], double *part) {
+  __shared__ double red[kCgsThreads / 32][NACC];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) {
+    double v = warp_sum(acc[k]);
+    if (lane == 0) red[w][k] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < NACC; k += blockDim.x) {
+    double s = 0.0;
+    for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) s += red[ww][k];
+    part[k] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kCgsThreads, 1)
+cgs_fused_kernel(int64_t dim, ColSet xs, const double *rsrc, int64_t ldr, const int *ci,
+                 const double *__restrict__ d, double *x, const double *yin, int64_t ldyin, int g, int kk,
+                 double *prev, int64_t ldprev, int passes, double *st_out, double *partials,
+                 unsigned int *bar) {
+  constexpr int AT = kCgsMaxCols;
+  constexpr int NACC = AT + 1;
+  pdl_wait();
+  __shared__ const double *xp[AT];
+  __shared__ double csh[NACC];
+  __shared__ double st[8];
+  const int tid = threadIdx.x;
+  const int na = xs.total;
+  if (tid < na) xp[tid] = colset_ptr(xs, tid);
+  if (tid < 8) st[tid] = (tid == 0) ? 1.0 : 0.0;
+  const int cidx = *ci;
+  if (blockIdx.x == 0 && prev != nullptr) {
+    for (int e = tid; e < g * kk; e += blockDim.x) {
+      const int r = e % g, j = e / g;
+      if (cidx + j < g) prev[r + (int64_t)j * ldprev] = yin[r + (int64_t)(cidx + j) * ldyin];
+    }
+  }
+  __syncthreads();
+  RowRange rr = cta_rows_even(dim);
+  const int64_t step = 2 * (int64_t)blockDim.x;
+  const int64_t rbeg = rr.r0 + 2 * tid;
+  {
+    const double *src = rsrc + (int64_t)cidx * ldr;
+    for (int64_t r = rbeg; r < rr.r1; r += step) {
+      const int64_t r2 = min(r + 2, rr.r1);
+      for (int64_t q = r; q < r2; ++q) {
+        const double v = src[q];
+        x[q] = d ? __ddiv_rn(v, d[q]) : v;
+      }
+    }
+  }
+  double *part_c = partials;
+  double *part_n = partials + (int64_t)gridDim.x * NACC;
+  for (int pass = 0; pass < passes; ++pass) {
+    // Gram c = X^T x (+ |x|^2 on the first pass)
+    double acc[NACC];
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+    for (int64_t r = rbeg; r < rr.r1; r += step) {
+      if (r + 1 < rr.r1) {
+        const double2 xv = *reinterpret_cast<const double2 *>(x + r);
+#pragma unroll
+        for (int i = 0; i < AT; ++i)
+          if (i < na) {
+            const double2 vv = ldg2(xp[i] + r);
+            acc[i] = fma(vv.x, xv.x, fma(vv.y, xv.y, acc[i]));
+          }
+        if (pass == 0) acc[AT] = fma(xv.x, xv.x, fma(xv.y, xv.y, acc[AT]));
+      } else {
+        const double xv = x[r];
+#pragma unroll
+        for (int i = 0; i < AT; ++i)
+          if (i < na) acc[i] = fma(__ldg(xp[i] + r), xv, acc[i]);
+        if (pass == 0) acc[AT] = fma(xv, xv, acc[AT]);
+      }
+    }
+    cta_fold_wide<NACC>(acc, part_c + (int64_t)blockIdx.x * NACC);
+    grid_barrier(bar, gridDim.x);
+    fold_parts(part_c, gridDim.x, NACC, NACC, [&](int o, int, int, double sum) { csh[o] = sum; });
+    __syncthreads();
+    if (pass == 0 && tid == 0) st[6] = csh[AT];
+    // projection x -= X c, |x|^2
+    double nacc = 0.0;
+    for (int64_t r = rbeg; r < rr.r1; r += step) {
+      if (r + 1 < rr.r1) {
+        double2 xv = *reinterpret_cast<const double2 *>(x + r);
+#pragma unroll
+        for (int i = 0; i < AT; ++i)
+          if (i < na) {
+            const double2 vv = ldg2(xp[i] + r);
+            xv.x = fma(-vv.x, csh[i], xv.x);
+            xv.y = fma(-vv.y, csh[i], xv.y);
+          }
+        *reinterpret_cast<double2 *>(x + r) = xv;
+        nacc = fma(xv.x, xv.x, fma(xv.y, xv.y, nacc));
+      } else {
+        double xv = x[r];
+#pragma unroll
+        for (int i = 0; i < AT; ++i)
+          if (i < na) xv = fma(-__ldg(xp[i] + r), csh[i], xv);
+        x[r] = xv;
+        nacc = fma(xv, xv, nacc);
+      }
+    }
+    {
+      double a1[1] = {nacc};
+      cta_fold_wide<1>(a1, part_n + blockIdx.x);
+    }
+    grid_barrier(bar, gridDim.x);
+    fold_parts(part_n, gridDim.x, 1, 1, [&](int, int, int, double sum) {
+      st[7] = sum;
+      dgks_decide(st);
+    });
+    __syncthreads();
+    if (st[0] == 0.0) break;
+  }
+  // normalise by the accepted norm (the host path handles collapses)
+  const double fin = st[5];
+  if (st[0] == 0.0 && fin > 0.0) {
+    for (int64_t r = rbeg; r < rr.r1; r += step) {
+      const int64_t r2 = min(r + 2, rr.r1);
+      for (int64_t q = r; q < r2; ++q) x[q] = x[q] / fin;
+    }
+  }
+  if (blockIdx.x == 0 && tid < 8) st_out[tid] = st[tid];
+}
+
 static inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 static bool colset_vec_ok(const ColSet &s) {
@@ -1022,6 +1186,36 @@ int svdsb_set_int(int *dst, int v, void *stream) {
 
 int svdsb_dgks_begin(double *state, void *stream) {
   SVDSB_LAUNCH_PDL(dgks_begin_kernel, 1, 32, 0, as_stream(stream), state);
+  return SVDSB_OK;
+}
+
+int svdsb_cgs_fused(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs,
+                    const int *cols, const double *rsrc, int64_t ldr, const int *ci, const double *d, double *x,
+                    const double *yin, int64_t ldyin, int g, int kk, double *prev, int64_t ldprev, int passes,
+                    double *state, void *stream) {
+  SVDSB_CHECK_ARG(ctx != nullptr && state != nullptr && ci != nullptr && rsrc != nullptr && x != nullptr,
+                  "svdsb_cgs_fused: NULL argument");
+  ColSet s;
+  int rc = make_colset(s, nblk, xs, ldxs, cols);
+  if (rc) return rc;
+  SVDSB_CHECK_ARG(s.total >= 1 && s.total <= kCgsMaxCols, "svdsb_cgs_fused: 1..40 prior columns");
+  SVDSB_CHECK_ARG(colset_vec_ok(s) && aligned16(x), "svdsb_cgs_fused: operands must be 16-byte aligned");
+  SVDSB_CHECK_ARG(passes >= 1 && passes <= 6, "svdsb_cgs_fused: 1..6 passes");
+  if (dim == 0) return SVDSB_OK;
+  static int cap = 0;
+  if (cap == 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cgs_fused_kernel, kCgsThreads, 0) != cudaSuccess ||
+        occ < 1) {
+      set_error("svdsb_cgs_fused: kernel does not fit on an SM");
+      return SVDSB_ERR_CUDA;
+    }
+    cap = kNumSMs;  // one CTA per SM: all resident for the grid barrier
+  }
+  const int grid = stream_grid(dim, 2 * kCgsThreads, cap);
+  SVDSB_CHECK_ARG((int64_t)grid * (kCgsMaxCols + 2) <= kMaxPartials, "svdsb_cgs_fused: workspace too small");
+  SVDSB_LAUNCH_PDL(cgs_fused_kernel, grid, kCgsThreads, 0, as_stream(stream), dim, s, rsrc, ldr, ci, d, x, yin,
+                   ldyin, g, kk, prev, ldprev, passes, state, ctx->partials, ctx->gbar);
   return SVDSB_OK;
 }
 

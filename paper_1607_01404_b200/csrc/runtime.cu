@@ -58,12 +58,14 @@ int svdsb_ctx_create(int device, svdsb_ctx **out) {
   c->device = device;
   c->next_ticket = 0;
   if (cudaMalloc(&c->partials, sizeof(double) * svdsb::kMaxPartials) != cudaSuccess ||
-      cudaMalloc(&c->ticket, sizeof(unsigned int) * svdsb::kMaxTickets) != cudaSuccess) {
+      cudaMalloc(&c->ticket, sizeof(unsigned int) * svdsb::kMaxTickets) != cudaSuccess ||
+      cudaMalloc(&c->gbar, sizeof(unsigned int) * 2) != cudaSuccess) {
     svdsb::set_error("svdsb_ctx_create: cudaMalloc failed");
     delete c;
     return SVDSB_ERR_ALLOC;
   }
   SVDSB_CUDA(cudaMemset(c->ticket, 0, sizeof(unsigned int) * svdsb::kMaxTickets));
+  SVDSB_CUDA(cudaMemset(c->gbar, 0, sizeof(unsigned int) * 2));
   SVDSB_CUDA(cudaDeviceSynchronize());
   *out = c;
   return SVDSB_OK;
@@ -73,6 +75,7 @@ int svdsb_ctx_destroy(svdsb_ctx *ctx) {
   if (!ctx) return SVDSB_OK;
   cudaFree(ctx->partials);
   cudaFree(ctx->ticket);
+  cudaFree(ctx->gbar);
   delete ctx;
   return SVDSB_OK;
 }

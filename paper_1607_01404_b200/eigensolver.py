@@ -317,6 +317,7 @@ class _Workspace:
         self.dgks_eager = torch.zeros(8, dtype=DTYPE, device=dev)
         self.hc1 = dv.small_matrix(gm + 1, 1)
         self.ci = torch.zeros(1, dtype=torch.int32, device=dev)   # selected candidate (device copy)
+        self.zero_i = torch.zeros(1, dtype=torch.int32, device=dev)
         self.ci_host = None                                        # its value in stream order
         self.orthoc = torch.zeros(4 * _lib.SMALL_MAX * 4, dtype=DTYPE, device=dev)
         self.graphs = {}
@@ -1068,6 +1069,29 @@ class DavidsonSolver:
     def _expand_speculative(self, block):
         g = self.g
         dst = self.v[:, g:g + 1]
+        prior = [b for b in self._against()] + [self.v[:, :g]]
+        total = sum(b.shape[1] for b in prior)
+        ws = self._ws
+        d = getattr(self.precond, "diagonal", None) if self.precond is not None else None
+        if (self.fused_cgs and ws is not None and total <= 40 and len(prior) <= _lib.MAX_BLOCKS
+                and (self.precond is None or d is not None)):
+            # same single launch as the graphed iterations (bit-identical)
+            if self.precond is not None:
+                self.precond.n_applies += 1
+                self.stats.precond_applies += 1
+            st = self._dgks_state
+            n, ptrs, lds, cols, _ = dv._blk_args(prior)
+            blk = dv.as_block(block)
+            _lib.call("svdsb_cgs_fused", self.ctx.handle, self.n, n, ptrs, lds, cols, dv.P(blk), dv.ld_of(blk),
+                      dv.P(ws.zero_i), None if d is None else dv.P(d), dv.P(dst), None, 1, g, 1, None, 1,
+                      self.SPEC_PASSES, dv.P(st), self.ctx.stream)
+            self._apply_op(dst, self.w[:, g:g + 1])
+            hc = dv.small_matrix(g + 1, 1)
+            dv.gram(self.ctx, self.n, [self.v[:, :g + 1]], self.w[:, g:g + 1], hc)
+            dv.h_insert(self.ctx, g, 1, hc, self.h)
+            self._spec = {"g0": g}
+            self.g = g + 1
+            return
         if self.precond is not None:
             self.precond.apply_into(block, dst)
             self.stats.precond_applies += 1
@@ -1151,6 +1175,7 @@ class DavidsonSolver:
     # counters are only advanced when the queued iteration is accepted.
 
     run_ahead = os.environ.get("SVDSB_AHEAD", "1") != "0"
+    fused_cgs = os.environ.get("SVDSB_CGS_FUSED", "1") != "0"
 
     def _graph_ok(self, b):
         return (self.use_graphs and self._can_speculate(b) and self._ws is not None
@@ -1168,19 +1193,27 @@ class DavidsonSolver:
         dst = self.v[:, g:g + 1]
         y_in, l_in = ws.y[sin], ws.lams[sin]
         y_out, l_out, r_out, s_out = ws.y[sout], ws.lams[sout], ws.rbuf[sout], ws.stat[sout]
-        # +k coefficients kept for the next restart (eigensolver.py:520-527)
         kk = max(self.cfg.plus_k, 1)
-        dv.gather_cols(ctx, y_in[:g, :g], ws.ci, kk, g, self.prev_d[:g, :kk])
-        # the selected residual, preconditioned (x ./ d as svdsb_diag_solve)
         d = self.precond.diagonal if self.precond is not None else None
-        dv.gather_cols(ctx, ws.rbuf[sin], ws.ci, 1, self.pmax, dst, d=d)
         st = ws.dgks[sout]
-        _lib.call("svdsb_dgks_begin", dv.P(st), ctx.stream)
         n_, ptrs, lds, cols, _ = dv._blk_args([self.v[:, :g]])
-        for p_ in range(self.SPEC_PASSES):
-            _lib.call("svdsb_cgs_pass", ctx.handle, self.n, n_, ptrs, lds, cols, dv.P(dst), dv.P(self.ortho.c),
-                      dv.P(st), 1 if p_ == 0 else 0, ctx.stream)
-        dv.scale_cols(ctx, dst, st[5:6], dv.SCALE_DIV)
+        if self.fused_cgs and g <= 40:
+            # select + precondition + +k copy + device-decided CGS passes +
+            # normalise, one launch (svdsb_cgs_fused)
+            rin, yb = ws.rbuf[sin], y_in[:g, :g]
+            _lib.call("svdsb_cgs_fused", ctx.handle, self.n, n_, ptrs, lds, cols, dv.P(rin), dv.ld_of(rin),
+                      dv.P(ws.ci), None if d is None else dv.P(d), dv.P(dst), dv.P(yb), dv.ld_of(yb), g, kk,
+                      dv.P(self.prev_d), dv.ld_of(self.prev_d), self.SPEC_PASSES, dv.P(st), ctx.stream)
+        else:
+            # +k coefficients kept for the next restart (eigensolver.py:520-527)
+            dv.gather_cols(ctx, y_in[:g, :g], ws.ci, kk, g, self.prev_d[:g, :kk])
+            # the selected residual, preconditioned (x ./ d as svdsb_diag_solve)
+            dv.gather_cols(ctx, ws.rbuf[sin], ws.ci, 1, self.pmax, dst, d=d)
+            _lib.call("svdsb_dgks_begin", dv.P(st), ctx.stream)
+            for p_ in range(self.SPEC_PASSES):
+                _lib.call("svdsb_cgs_pass", ctx.handle, self.n, n_, ptrs, lds, cols, dv.P(dst),
+                          dv.P(self.ortho.c), dv.P(st), 1 if p_ == 0 else 0, ctx.stream)
+            dv.scale_cols(ctx, dst, st[5:6], dv.SCALE_DIV)
         self.op.raw_into(dst, self.w[:, g:g + 1])
         hc = ws.hc1[:g + 1, :]
         dv.gram(ctx, self.n, [self.v[:, :g + 1]], self.w[:, g:g + 1], hc)

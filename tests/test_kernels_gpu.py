@@ -503,3 +503,48 @@ def test_gather_cols_device_index(dim, rng):
               ctx.stream)
     assert np.array_equal(dv.to_host(Y[:, :1]), dv.to_host(ref))
     assert np.array_equal(dv.to_host(ref)[:, 0], x[:, 5] / d)
+
+
+@pytest.mark.parametrize("dim,g", [(7, 3), (5000, 30), (300001, 40), (300001, 1)])
+@pytest.mark.parametrize("precond", [False, True])
+def test_cgs_fused_matches_pass_by_pass(dim, g, precond, rng):
+    """svdsb_cgs_fused (one launch, software grid barrier) against the
+    pass-by-pass kernels: same selected column, +k copy, DGKS pass count and
+    orthonormalised vector to rounding."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    q, _ = np.linalg.qr(rng.standard_normal((dim, g)))
+    V = dv.to_device_block(q)
+    R = dv.to_device_block(rng.standard_normal((dim, 3)) + 0.5 * q[:, :1])
+    d = torch.from_numpy(rng.uniform(0.5, 2.0, dim)).cuda() if precond else None
+    ci = torch.tensor([1], dtype=torch.int32, device="cuda")
+    Y = dv.to_device_block(rng.standard_normal((g, g)))
+    kk = 2
+    n_, ptrs, lds, cols, _ = dv._blk_args([V])
+    outs = []
+    for fused in (True, False):
+        x = dv.new_block(dim, 1)
+        prev = dv.small_matrix(g, kk)
+        st = torch.zeros(8, dtype=torch.float64, device="cuda")
+        if fused:
+            _lib.call("svdsb_cgs_fused", ctx.handle, dim, n_, ptrs, lds, cols, dv.P(R), dv.ld_of(R), dv.P(ci),
+                      None if d is None else dv.P(d), dv.P(x), dv.P(Y), dv.ld_of(Y), g, kk, dv.P(prev),
+                      dv.ld_of(prev), 3, dv.P(st), ctx.stream)
+        else:
+            cw = torch.zeros(256, dtype=torch.float64, device="cuda")
+            dv.gather_cols(ctx, Y, ci, kk, g, prev)
+            dv.gather_cols(ctx, R, ci, 1, 3, x, d=d)
+            _lib.call("svdsb_dgks_begin", dv.P(st), ctx.stream)
+            for p in range(3):
+                _lib.call("svdsb_cgs_pass", ctx.handle, dim, n_, ptrs, lds, cols, dv.P(x), dv.P(cw), dv.P(st),
+                          1 if p == 0 else 0, ctx.stream)
+            dv.scale_cols(ctx, x, st[5:6], dv.SCALE_DIV)
+        outs.append((dv.to_host(x)[:, 0], dv.to_host(prev), st.cpu().numpy()))
+    (xf, pf, sf), (xr, pr, sr) = outs
+    assert np.array_equal(pf[:, :1], pr[:, :1]) and np.array_equal(pf, pr)
+    assert sf[0] == sr[0] == 0.0 and sf[1] == sr[1] and sf[5] > 0.0
+    assert abs(sf[5] - sr[5]) <= 1e-12 * sr[5]
+    assert np.abs(xf - xr).max() <= 1e-12
+    assert abs(np.linalg.norm(xf) - 1.0) <= 1e-13
+    assert np.abs(q.T @ xf).max() <= 1e-13
