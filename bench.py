@@ -9,9 +9,12 @@ One "step" is one full svds_solve (both stages as needed) with the matrix
 and preconditioner already resident in HBM; value = mean seconds per solve
 (max over ranks; lower is better).  ``e2e`` is the same solve through the
 reference-facing binding (pysvds.svds) from host COO arrays, host->device
-and device->host copies included.  ``roofline`` is the CSR SpMV kernel
-(A x and A^T y), timed with CUDA events on the launching stream around
-every SpMV launch inside the timed region.  ``cpu_baseline`` is the CPU
+and device->host copies included.  ``roofline`` is the dominant kernel of
+the graphed iteration (``iteration_kernels`` lists every kernel with its
+per-launch time -- a CUDA graph of 100 back-to-back launches on this
+workload's matrix, timed with CUDA events on the launching stream -- and
+its share of the step); ``kernels_at_hbm_scale`` repeats the hot kernels at
+config-3 size where every operand streams from HBM.  ``cpu_baseline`` is the CPU
 oracle port (oracle/phsvds.py, bit-identical to the reference) on a
 bounded sample of the same workload.
 
@@ -350,14 +353,30 @@ def iteration_kernels(a, pre, wl, peak, iters, step_ms, g=25):
     spmv_f = spmv_bytes(m, n, nnz, 1, False)
     spmv_t = spmv_bytes(m, n, nnz, 1, True)
     # (name, per-launch us, launches per iteration, algorithmic bytes per launch)
-    rows = [
-        ("gather_cols (residual select + precond, +k copy)",
-         timeit(lambda: dv.gather_cols(ctx, R, ci, 1, p, col, d=d)), 2, 8 * N * (3 if d is not None else 2)),
-        ("dgks_begin", timeit(lambda: _lib.call("svdsb_dgks_begin", dv.P(st), ctx.stream)), 1, 0),
-        ("cgs pass, active (gram1_vec + project1_vec)", timeit(lambda: cgs(True)) - t_copy, 2,
-         8 * N * (2 * g + 3)),
-        ("cgs pass, gated off", timeit(lambda: cgs(False)) - t_copy, 1, 0),
-        ("scale_cols (normalise)", timeit(lambda: dv.scale_cols(ctx, col, nrm, dv.SCALE_DIV)), 1, 16 * N),
+    if g <= 40 and 8 * N * g <= (64 << 20):
+        # the solver's one-launch CGS (select, precondition, +k copy,
+        # device-decided passes, normalise) -- what configs 1/2 run
+        prev = dv.small_matrix(g, 2)
+
+        def fused():
+            _lib.call("svdsb_cgs_fused", ctx.handle, N, n_, ptrs, lds, cols, dv.P(R), dv.ld_of(R), dv.P(ci),
+                      None if d is None else dv.P(d), dv.P(col), dv.P(Y0), dv.ld_of(Y0), g, 2, dv.P(prev),
+                      dv.ld_of(prev), 3, dv.P(st), ctx.stream)
+        us = timeit(fused)
+        passes = int(st[1].item())
+        rows = [("cgs_fused_kernel (select + precondition + %d CGS passes + normalise)" % passes, us, 1,
+                 8 * N * ((3 if d is not None else 2) + passes * (2 * g + 3) + 2))]
+    else:
+        rows = [
+            ("gather_cols (residual select + precond, +k copy)",
+             timeit(lambda: dv.gather_cols(ctx, R, ci, 1, p, col, d=d)), 2, 8 * N * (3 if d is not None else 2)),
+            ("dgks_begin", timeit(lambda: _lib.call("svdsb_dgks_begin", dv.P(st), ctx.stream)), 1, 0),
+            ("cgs pass, active (gram1_vec + project1_vec)", timeit(lambda: cgs(True)) - t_copy, 2,
+             8 * N * (2 * g + 3)),
+            ("cgs pass, gated off", timeit(lambda: cgs(False)) - t_copy, 1, 0),
+            ("scale_cols (normalise)", timeit(lambda: dv.scale_cols(ctx, col, nrm, dv.SCALE_DIV)), 1, 16 * N),
+        ]
+    rows += [
         ("csr SpMV (first of the C-apply)", timeit(lambda: dev.matvec(col, tmp, tr)), 1,
          spmv_t if tr else spmv_f),
         ("csr SpMV (second of the C-apply)", timeit(lambda: dev.matvec(tmp, W[:, g:g + 1], not tr)), 1,

@@ -1066,6 +1066,12 @@ class DavidsonSolver:
         return (b == 1 and self.speculate and self.q is None and not self.comm.distributed
                 and self.g >= 1 and getattr(self.ctx, "handle", None) is not None)
 
+    def _use_fused_cgs(self, cols):
+        """The one-launch CGS wins while the basis is L2-resident (latency
+        bound: configs 1 and 2); HBM-streamed bases run the separate
+        Gram / projection kernels, which stream at 82-86 % of HBM."""
+        return self.fused_cgs and cols <= 40 and 8 * self.n * cols <= (64 << 20)
+
     def _expand_speculative(self, block):
         g = self.g
         dst = self.v[:, g:g + 1]
@@ -1073,7 +1079,7 @@ class DavidsonSolver:
         total = sum(b.shape[1] for b in prior)
         ws = self._ws
         d = getattr(self.precond, "diagonal", None) if self.precond is not None else None
-        if (self.fused_cgs and ws is not None and total <= 40 and len(prior) <= _lib.MAX_BLOCKS
+        if (ws is not None and self._use_fused_cgs(total) and len(prior) <= _lib.MAX_BLOCKS
                 and (self.precond is None or d is not None)):
             # same single launch as the graphed iterations (bit-identical)
             if self.precond is not None:
@@ -1197,7 +1203,7 @@ class DavidsonSolver:
         d = self.precond.diagonal if self.precond is not None else None
         st = ws.dgks[sout]
         n_, ptrs, lds, cols, _ = dv._blk_args([self.v[:, :g]])
-        if self.fused_cgs and g <= 40:
+        if self._use_fused_cgs(g):
             # select + precondition + +k copy + device-decided CGS passes +
             # normalise, one launch (svdsb_cgs_fused)
             rin, yb = ws.rbuf[sin], y_in[:g, :g]
