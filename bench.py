@@ -505,6 +505,7 @@ def e2e(args, wl, m, n, r, c, v, pysvds, barrier):
         if i > 0:  # first call warms allocator / CUB temp buffers
             times.append(dt)
     return {"value": float(np.mean(times)), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "per_step_s": [round(t, 4) for t in times],
             "api": "paper_1607_01404_b200.pysvds.svds(SparseMatrixCsr.from_coo(host COO), precond=jacobi)",
             "steps": len(times)}
 
