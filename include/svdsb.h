@@ -203,6 +203,12 @@ int svdsb_axpby(int64_t dim, int b, double alpha, const double *x,
 int svdsb_gather_cols(int64_t dim, const double *x, int64_t ldx,
                       const int *first, int ncols, int limit,
                       const double *d, double *y, int64_t ldy, void *stream);
+/* Iteration status straight into pinned (UVA-mapped) host memory:
+ * host_dst[0:gn] = lams, [gn:gn+p] = rn2, [gn+p:gn+p+8] = state; the host
+ * reads it after an event on `stream` (the per-iteration status read of
+ * eigensolver.py:563-607). */
+int svdsb_status_pack(const double *lams, int gn, const double *rn2, int p,
+                      const double *state, double *host_dst, void *stream);
 /* *dst = v on the stream (stream-ordered scalar update for the above). */
 int svdsb_set_int(int *dst, int v, void *stream);
 /* Stage-2 split statistics of candidate vectors on the stacked layout

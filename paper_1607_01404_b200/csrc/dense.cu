@@ -428,6 +428,26 @@ __global__ void gather_cols_kernel(int64_t dim, const double *x, int64_t ldx, co
   }
 }
 
+// One kernel writes the iteration status straight into pinned host memory
+// (mapped under UVA): Ritz values, candidate residual norms, DGKS state.
+// Replaces three small device->host copies at the end of every graphed
+// iteration.
+__global__ void status_pack_kernel(const double *__restrict__ lams, int gn, const double *__restrict__ rn2, int p,
+                                   const double *__restrict__ st, double *host) {
+  pdl_wait();
+  for (int i = threadIdx.x; i < gn + p + 8; i += blockDim.x) {
+    double v;
+    if (i < gn)
+      v = lams[i];
+    else if (i < gn + p)
+      v = rn2[i - gn];
+    else
+      v = st[i - gn - p];
+    host[i] = v;
+  }
+  __threadfence_system();
+}
+
 __global__ void set_int_kernel(int *dst, int v) {
   pdl_wait();
   if (threadIdx.x == 0) *dst = v;
@@ -1175,6 +1195,14 @@ int svdsb_gather_cols(int64_t dim, const double *x, int64_t ldx, const int *firs
   if (dim == 0 || ncols <= 0) return SVDSB_OK;
   SVDSB_LAUNCH_PDL(gather_cols_kernel, (unsigned)((dim + 255) / 256), 256, 0, as_stream(stream), dim, x, ldx, first,
                    ncols, limit, d, y, ldy);
+  return SVDSB_OK;
+}
+
+int svdsb_status_pack(const double *lams, int gn, const double *rn2, int p, const double *state,
+                       double *host_dst, void *stream) {
+  SVDSB_CHECK_ARG(lams != nullptr && rn2 != nullptr && state != nullptr && host_dst != nullptr,
+                  "svdsb_status_pack: NULL argument");
+  SVDSB_LAUNCH_PDL(status_pack_kernel, 1, 128, 0, as_stream(stream), lams, gn, rn2, p, state, host_dst);
   return SVDSB_OK;
 }
 

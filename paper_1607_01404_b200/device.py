@@ -48,7 +48,8 @@ class DeviceContext:
     def refresh_stream(self):
         """Bind libsvdsb launches to torch's current stream on this device
         (looked up once per solve; per-call lookups cost ~8 us each)."""
-        self._stream = int(torch.cuda.current_stream(self.device).cuda_stream) or None
+        self.torch_stream = torch.cuda.current_stream(self.device)
+        self._stream = int(self.torch_stream.cuda_stream) or None
         return self._stream
 
     @property

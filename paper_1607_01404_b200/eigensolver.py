@@ -435,6 +435,8 @@ class DavidsonSolver:
         self._pending = None   # graphed iteration queued, status not yet read
         self._ahead = None     # next graphed iteration queued speculatively
         self._ahead_used = False
+        self._graph_base = None
+        self._graph_static = None
 
         self.locked_vecs = dv.new_block(self.n, 0)
         self._locked_buf = dv.new_block(self.n, max(self.wanted, 1)) if cfg.locking else None
@@ -754,8 +756,10 @@ class DavidsonSolver:
 
     def _make_cands(self, lams, rn2, split_h, p, x, ox):
         cands = []
+        rn = np.sqrt(np.maximum(rn2[:p], 0.0)).tolist()
+        lv = lams[:p].tolist()
         for i in range(p):
-            c = Candidate(float(lams[i]), float(np.sqrt(max(rn2[i], 0.0))))
+            c = Candidate(lv[i], rn[i])
             if x is not None:
                 c.x = x[:, i]
             if ox is not None:
@@ -1184,12 +1188,18 @@ class DavidsonSolver:
     fused_cgs = os.environ.get("SVDSB_CGS_FUSED", "1") != "0"
 
     def _graph_ok(self, b):
-        return (self.use_graphs and self._can_speculate(b) and self._ws is not None
+        static = self._graph_static
+        if static is None:
+            # the parts fixed for the whole solve, evaluated once
+            static = self._graph_static = bool(
+                self.use_graphs and self._ws is not None and not self.comm.distributed
+                and getattr(self.ctx, "handle", None) is not None
                 and not self.cfg.locking and self.cfg.extraction == EXTRACT_RR
                 and self._split_n is None and not self._need_vecs and self.cfg.iteration_hook is None
-                and not self.ext and self.locked_vecs.shape[1] == 0 and self.warm_start
-                and self._warm is not None and getattr(self.op, "graph_key", None) is not None
+                and not self.ext and getattr(self.op, "graph_key", None) is not None
                 and (self.precond is None or getattr(self.precond, "diagonal", None) is not None))
+        return (static and b == 1 and self.speculate and self.q is None and self.g >= 1 and self.warm_start
+                and self._warm is not None and self.locked_vecs.shape[1] == 0)
 
     def _iter_device(self, g, kind, g0, p, order, shift, sin, sout):
         """Launch-only body of a graphed iteration (no host bookkeeping):
@@ -1230,11 +1240,9 @@ class DavidsonSolver:
         dv.syev_update(ctx, self.h, g0, gn - g0, y0, l0, order, shift, l_out[:gn], y_out[:gn, :gn])
         dv.ritz_residual(ctx, self.v[:, :gn], self.w[:, :gn], y_out[:gn, :p], l_out[:p],
                          r_out[:, :p], rn2=s_out[:p])
-        lib = _lib.load()
-        base = ws.status[sout].data_ptr()
-        lib.svdsb_d2h(base, l_out.data_ptr(), 8 * gn, ctx.stream)
-        lib.svdsb_d2h(base + 8 * gn, s_out.data_ptr(), 8 * p, ctx.stream)
-        lib.svdsb_d2h(base + 8 * (gn + p), st.data_ptr(), 64, ctx.stream)
+        # status straight into the pinned host slot (one kernel, no copies)
+        _lib.call("svdsb_status_pack", dv.P(l_out), gn, dv.P(s_out), p, dv.P(st), ws.status[sout].data_ptr(),
+                  ctx.stream)
 
     def _capture(self, fn):
         ctx = self.ctx
@@ -1264,8 +1272,12 @@ class DavidsonSolver:
         sout = 1 - sin
         p = min(self.wanted + self.cfg.max_block_size, g + 1)
         order, shift = self._order_mode()
-        key = (self.v.data_ptr(), self.w.data_ptr(), kind, g0, g, p, sin, order, shift, self.op.graph_key(),
-               None if self.precond is None else self.precond.diagonal.data_ptr())
+        base = self._graph_base
+        if base is None:
+            # operator / preconditioner identity: fixed for the solve
+            base = self._graph_base = (self.op.graph_key(),
+                                       None if self.precond is None else self.precond.diagonal.data_ptr())
+        key = (self.v.data_ptr(), self.w.data_ptr(), kind, g0, g, p, sin, order, shift, base)
         entry = ws.graphs.get(key)
         if entry is None:
             before = _lib.launch_count()
@@ -1274,7 +1286,7 @@ class DavidsonSolver:
             ws.graphs[key] = entry
             self.stats.graphs_captured += 1
         entry[0].replay()
-        ws.events[sout].record()
+        ws.events[sout].record(self.ctx.torch_stream)
         _lib.load().svdsb_note_launches(entry[1])
         return {"p": p, "slot": sout, "sin": sin, "g": g, "ci": ci}
 
@@ -1323,10 +1335,10 @@ class DavidsonSolver:
         b = min(res_block.shape[1], self.gmax - self.g)
         if b <= 0:
             return
-        block = res_block[:, :b]
         if graph and self._graph_ok(b):
             self._expand_graphed(ci)
             return
+        block = res_block[:, :b]
         if self._can_speculate(b):
             self._expand_speculative(block)
             return
