@@ -400,8 +400,18 @@ def iteration_kernels(a, pre, wl, peak, iters, step_ms, g=25):
     modeled = sum(t["share_of_step"] for t in table)
     dom = max((t for t in table if t["algorithmic_bytes"]), key=lambda t: t["share_of_step"])
     achieved = dom["gbs"]
+    traffic = None
+    tf = os.path.join(REPO, "profiles", "traffic_%s.json" % wl.name)
+    if os.path.exists(tf):
+        with open(tf) as f:
+            per = json.load(f).get("dram_bytes_per_launch", {})
+        for kname, byt in per.items():
+            if kname in dom["kernel"]:
+                traffic = byt
     roof = {"kernel": dom["kernel"], "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None,
+            "frac": achieved / peak, "traffic": traffic,
+            "traffic_note": "ncu dram read+write per launch, cold L2 (profiles/traffic_%s.json); inside a "
+                            "solve the basis is L2-resident" % wl.name,
             "algorithmic_bytes_per_launch": dom["algorithmic_bytes"], "avg_launch_us": dom["us_per_launch"],
             "share_of_step": dom["share_of_step"],
             "method": "CUDA events around a graph of %d back-to-back launches at basis size g=%d on this "
