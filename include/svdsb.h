@@ -58,6 +58,15 @@ int64_t svdsb_note_launches(int64_t n);
 int svdsb_d2h(void *dst_host, const void *src, size_t bytes, void *stream);
 int svdsb_stream_sync(void *stream);
 
+/* CUDA-graph capture of a launch sequence on a non-default `stream`
+ * (thread-local capture mode), instantiation + upload, replay and release.
+ * The solver captures the device work of one Davidson iteration once per
+ * shape and replays it (eigensolver.py:563-700's per-iteration kernels). */
+int svdsb_graph_begin(void *stream);
+int svdsb_graph_end(void *stream, void **exec_out);
+int svdsb_graph_launch(void *exec, void *stream);
+int svdsb_graph_destroy(void *exec);
+
 /* A context owns the device workspace used by the deterministic two-level
  * reductions (per-CTA partials + a ticket counter).  One context per stream
  * in flight. */

@@ -30,6 +30,10 @@ _PROTOS = [
     ("svdsb_note_launches", i64, [i64]),
     ("svdsb_d2h", i32, [vp, vp, ctypes.c_size_t, vp]),
     ("svdsb_stream_sync", i32, [vp]),
+    ("svdsb_graph_begin", i32, [vp]),
+    ("svdsb_graph_end", i32, [vp, ctypes.POINTER(vp)]),
+    ("svdsb_graph_launch", i32, [vp, vp]),
+    ("svdsb_graph_destroy", i32, [vp]),
     ("svdsb_ctx_create", i32, [i32, ctypes.POINTER(vp)]),
     ("svdsb_ctx_destroy", i32, [vp]),
     ("svdsb_csr_create_host", i32, [vp, i64, i64, i64, vp, vp, vp, i32, vp, ctypes.POINTER(vp)]),

@@ -51,6 +51,37 @@ int svdsb_stream_sync(void *stream) {
   return SVDSB_OK;
 }
 
+// Stream capture / replay of the per-iteration launch sequence, without
+// the framework's graph bookkeeping (private memory pools etc.): nothing
+// is allocated inside a capture, only libsvdsb kernels are recorded.
+int svdsb_graph_begin(void *stream) {
+  SVDSB_CHECK_ARG(stream != nullptr, "svdsb_graph_begin: capture needs a non-default stream");
+  SVDSB_CUDA(cudaStreamBeginCapture(svdsb::as_stream(stream), cudaStreamCaptureModeThreadLocal));
+  return SVDSB_OK;
+}
+
+int svdsb_graph_end(void *stream, void **exec_out) {
+  SVDSB_CHECK_ARG(exec_out != nullptr, "svdsb_graph_end: NULL output");
+  cudaGraph_t g = nullptr;
+  SVDSB_CUDA(cudaStreamEndCapture(svdsb::as_stream(stream), &g));
+  cudaGraphExec_t e = nullptr;
+  cudaError_t rc = cudaGraphInstantiateWithFlags(&e, g, 0);
+  cudaGraphDestroy(g);
+  SVDSB_CUDA(rc);
+  *exec_out = e;
+  return SVDSB_OK;
+}
+
+int svdsb_graph_launch(void *exec, void *stream) {
+  SVDSB_CUDA(cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(exec), svdsb::as_stream(stream)));
+  return SVDSB_OK;
+}
+
+int svdsb_graph_destroy(void *exec) {
+  if (exec) cudaGraphExecDestroy(reinterpret_cast<cudaGraphExec_t>(exec));
+  return SVDSB_OK;
+}
+
 int svdsb_ctx_create(int device, svdsb_ctx **out) {
   SVDSB_CHECK_ARG(out != nullptr, "svdsb_ctx_create: out is NULL");
   SVDSB_CUDA(cudaSetDevice(device));

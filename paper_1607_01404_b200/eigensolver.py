@@ -15,6 +15,7 @@ kernels; random draws come from the same numpy Generator streams as the
 reference so trajectories track it.
 """
 
+import ctypes
 import os
 from dataclasses import dataclass
 
@@ -281,6 +282,28 @@ class Orthonormalizer:
             else:
                 raise np.linalg.LinAlgError("orthonormalize could not produce an independent column")
         return replaced
+
+
+class _NativeGraph:
+    """An instantiated CUDA graph (svdsb_graph_end), replayed with
+    svdsb_graph_launch on the solver's stream."""
+
+    __slots__ = ("exec",)
+
+    def __init__(self, ex):
+        self.exec = ex
+
+    def replay(self, stream):
+        rc = _lib.load().svdsb_graph_launch(self.exec, stream)
+        if rc:
+            _lib.check(rc, "svdsb_graph_launch")
+
+    def __del__(self):
+        try:
+            if self.exec and _lib._lib is not None:
+                _lib._lib.svdsb_graph_destroy(self.exec)
+        except Exception:
+            pass
 
 
 class _Workspace:
@@ -1245,24 +1268,24 @@ class DavidsonSolver:
                   ctx.stream)
 
     def _capture(self, fn):
+        """Record fn's libsvdsb launches as a CUDA graph on a side stream
+        (capture needs a non-default stream) and instantiate it."""
         ctx = self.ctx
-        graph = torch.cuda.CUDAGraph()
-        cur = torch.cuda.current_stream(ctx.device)
-        cap = torch.cuda.Stream(ctx.device)
-        cap.wait_stream(cur)
+        cap = getattr(ctx, "capture_stream", None)
+        if cap is None:
+            cap = ctx.capture_stream = torch.cuda.Stream(ctx.device)
         old = ctx._stream
+        lib = _lib.load()
+        _lib.check(lib.svdsb_graph_begin(cap.cuda_stream), "svdsb_graph_begin")
+        ex = ctypes.c_void_p()
         try:
-            with torch.cuda.stream(cap):
-                ctx._stream = cap.cuda_stream
-                graph.capture_begin()
-                try:
-                    fn()
-                finally:
-                    graph.capture_end()
+            ctx._stream = cap.cuda_stream
+            fn()
         finally:
             ctx._stream = old
-        cur.wait_stream(cap)
-        return graph
+            rc = lib.svdsb_graph_end(cap.cuda_stream, ctypes.byref(ex))
+        _lib.check(rc, "svdsb_graph_end")
+        return _NativeGraph(ex.value)
 
     def _launch_iter(self, g, kind, g0, sin, ci):
         """Replay (capturing on first use) the iteration graph that expands
@@ -1285,7 +1308,7 @@ class DavidsonSolver:
             entry = (graph, _lib.launch_count() - before)
             ws.graphs[key] = entry
             self.stats.graphs_captured += 1
-        entry[0].replay()
+        entry[0].replay(self.ctx._stream)
         ws.events[sout].record(self.ctx.torch_stream)
         _lib.load().svdsb_note_launches(entry[1])
         return {"p": p, "slot": sout, "sin": sin, "g": g, "ci": ci}

@@ -37,12 +37,12 @@ for ws_list in es._POOL.values():
     for ws in ws_list:
         for k, (graph, nl) in ws.graphs.items():
             s = torch.cuda.current_stream()
-            graph.replay()
+            graph.replay(torch.cuda.current_stream().cuda_stream)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(s)
             for _ in range(reps):
-                graph.replay()
+                graph.replay(torch.cuda.current_stream().cuda_stream)
             e1.record(s)
             e1.synchronize()
             rows.append((k[3], k[2], nl, e0.elapsed_time(e1) * 1e3 / reps))
