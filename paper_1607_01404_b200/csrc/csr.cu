@@ -732,32 +732,65 @@ __global__ void csr_long_fixup_kernel(int nlong, const int *__restrict__ long_ro
 
 // ---------------------------------------------------------------- partition
 
-static void free_part(CsrPart &p) {
-  cudaFree(p.row_ptr);
-  cudaFree(p.col);
-  cudaFree(p.val);
-  cudaFree(p.tile_r);
-  cudaFree(p.tile_info);
-  cudaFree(p.long_row);
-  cudaFree(p.long_cptr);
-  cudaFree(p.chunk_nz);
-  cudaFree(p.chunk_part);
-  p = CsrPart();
-}
-
 // Device arrays of a CSR part carry kAllocPad bytes of slack: the bulk-copy
 // SpMV moves whole 16-byte granules, which can reach past the last element.
 constexpr size_t kAllocPad = 64;
 
+// Stream-ordered allocations from the device's default memory pool, which
+// keeps freed memory (release threshold = max): assembling a matrix
+// allocates and frees a dozen temporaries, and plain cudaMalloc / cudaFree
+// synchronise the device and remap pages each time (5-200 ms per matrix).
+static cudaError_t pool_init() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool;
+  e = cudaDeviceGetDefaultMemPool(&pool, dev);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = UINT64_MAX;
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  if (e != cudaSuccess) return e;
+  done = true;
+  return cudaSuccess;
+}
+
 template <typename T>
-static cudaError_t alloc_pad(T **dst, size_t n) {
-  return cudaMalloc(dst, n * sizeof(T) + kAllocPad);
+static cudaError_t palloc(T **p, size_t bytes, cudaStream_t st) {
+  cudaError_t e = pool_init();
+  if (e != cudaSuccess) return e;
+  return cudaMallocAsync(reinterpret_cast<void **>(p), bytes, st);
+}
+
+static void pfree(void *p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
+template <typename T>
+static cudaError_t alloc_pad(T **dst, size_t n, cudaStream_t st) {
+  return palloc(dst, n * sizeof(T) + kAllocPad, st);
+}
+
+static void free_part(CsrPart &p) {
+  // pool memory: returned in legacy-stream order (svdsb_csr_destroy has
+  // synchronised the device first)
+  pfree(p.row_ptr, nullptr);
+  pfree(p.col, nullptr);
+  pfree(p.val, nullptr);
+  pfree(p.tile_r, nullptr);
+  pfree(p.tile_info, nullptr);
+  pfree(p.long_row, nullptr);
+  pfree(p.long_cptr, nullptr);
+  pfree(p.chunk_nz, nullptr);
+  pfree(p.chunk_part, nullptr);
+  p = CsrPart();
 }
 
 template <typename T>
 static int upload(T **dst, const std::vector<T> &src, cudaStream_t st) {
   size_t n = std::max<size_t>(src.size(), 1);
-  SVDSB_CUDA(alloc_pad(dst, n));
+  SVDSB_CUDA(alloc_pad(dst, n, st));
   if (!src.empty())
     SVDSB_CUDA(cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st));
   return SVDSB_OK;
@@ -814,7 +847,7 @@ static int build_partition(CsrPart &p, cudaStream_t st) {
   if ((rc = upload(&p.long_row, lrows, st))) return rc;
   if ((rc = upload(&p.long_cptr, lcptr, st))) return rc;
   if ((rc = upload(&p.chunk_nz, cnz, st))) return rc;
-  SVDSB_CUDA(cudaMalloc(&p.chunk_part, sizeof(double) * kMaxB * std::max(p.nchunk, 1)));
+  SVDSB_CUDA(palloc(&p.chunk_part, sizeof(double) * kMaxB * std::max(p.nchunk, 1), st));
   return SVDSB_OK;
 }
 
@@ -962,17 +995,17 @@ static int build_transpose(const CsrPart &a, CsrPart &at, cudaStream_t st) {
   at.cols = a.rows;
   at.nnz = a.nnz;
   const int64_t nnz = a.nnz;
-  SVDSB_CUDA(alloc_pad(&at.row_ptr, at.rows + 1));
-  SVDSB_CUDA(alloc_pad(&at.col, std::max<int64_t>(nnz, 1)));
-  SVDSB_CUDA(alloc_pad(&at.val, std::max<int64_t>(nnz, 1)));
+  SVDSB_CUDA(alloc_pad(&at.row_ptr, at.rows + 1, st));
+  SVDSB_CUDA(alloc_pad(&at.col, std::max<int64_t>(nnz, 1), st));
+  SVDSB_CUDA(alloc_pad(&at.val, std::max<int64_t>(nnz, 1), st));
   SVDSB_CUDA(cudaMemsetAsync(at.row_ptr, 0, sizeof(int) * (at.rows + 1), st));
   if (nnz > 0) {
     int *rows = nullptr, *idx = nullptr, *keys_out = nullptr, *perm = nullptr, *counts = nullptr;
-    SVDSB_CUDA(cudaMalloc(&rows, sizeof(int) * nnz));
-    SVDSB_CUDA(cudaMalloc(&idx, sizeof(int) * nnz));
-    SVDSB_CUDA(cudaMalloc(&keys_out, sizeof(int) * nnz));
-    SVDSB_CUDA(cudaMalloc(&perm, sizeof(int) * nnz));
-    SVDSB_CUDA(cudaMalloc(&counts, sizeof(int) * (at.rows + 1)));
+    SVDSB_CUDA(palloc(&rows, sizeof(int) * nnz, st));
+    SVDSB_CUDA(palloc(&idx, sizeof(int) * nnz, st));
+    SVDSB_CUDA(palloc(&keys_out, sizeof(int) * nnz, st));
+    SVDSB_CUDA(palloc(&perm, sizeof(int) * nnz, st));
+    SVDSB_CUDA(palloc(&counts, sizeof(int) * (at.rows + 1), st));
     SVDSB_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * (at.rows + 1), st));
     expand_rows_kernel<<<grid1(a.rows), 256, 0, st>>>(a.rows, a.row_ptr, rows);
     SVDSB_LAUNCHED();
@@ -982,7 +1015,7 @@ static int build_transpose(const CsrPart &a, CsrPart &at, cudaStream_t st) {
     int nbits = bits_for(a.cols);
     cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, a.col, keys_out, idx, perm, (int)nnz, 0, nbits, st);
     void *tmp = nullptr;
-    SVDSB_CUDA(cudaMalloc(&tmp, tmp_bytes));
+    SVDSB_CUDA(palloc(&tmp, tmp_bytes, st));
     SVDSB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, a.col, keys_out, idx, perm, (int)nnz, 0,
                                                nbits, st));
     bump_launches();
@@ -994,17 +1027,17 @@ static int build_transpose(const CsrPart &a, CsrPart &at, cudaStream_t st) {
     size_t scan_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts, at.row_ptr, (int)(at.rows + 1), st);
     void *scan_tmp = nullptr;
-    SVDSB_CUDA(cudaMalloc(&scan_tmp, scan_bytes));
+    SVDSB_CUDA(palloc(&scan_tmp, scan_bytes, st));
     SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, at.row_ptr, (int)(at.rows + 1), st));
     bump_launches();
     SVDSB_CUDA(cudaStreamSynchronize(st));
-    cudaFree(rows);
-    cudaFree(idx);
-    cudaFree(keys_out);
-    cudaFree(perm);
-    cudaFree(counts);
-    cudaFree(tmp);
-    cudaFree(scan_tmp);
+    pfree(rows, st);
+    pfree(idx, st);
+    pfree(keys_out, st);
+    pfree(perm, st);
+    pfree(counts, st);
+    pfree(tmp, st);
+    pfree(scan_tmp, st);
   }
   at.host_row_ptr.resize(at.rows + 1);
   SVDSB_CUDA(cudaMemcpyAsync(at.host_row_ptr.data(), at.row_ptr, sizeof(int) * (at.rows + 1),
@@ -1060,6 +1093,7 @@ extern "C" {
 
 int svdsb_csr_destroy(svdsb_csr *a) {
   if (!a) return SVDSB_OK;
+  cudaDeviceSynchronize();
   free_part(a->a);
   free_part(a->at);
   for (auto &p : a->atb) free_part(p);
@@ -1125,18 +1159,18 @@ static int build_blocked_transpose(svdsb_csr *h, cudaStream_t st) {
   }
   if (!forced && !(m > block_rows && m >= 4 * n)) return SVDSB_OK;
   int *lo = nullptr, *len = nullptr;
-  SVDSB_CUDA(cudaMalloc(&lo, sizeof(int) * (n + 1)));
-  SVDSB_CUDA(cudaMalloc(&len, sizeof(int) * (n + 1)));
+  SVDSB_CUDA(palloc(&lo, sizeof(int) * (n + 1), st));
+  SVDSB_CUDA(palloc(&len, sizeof(int) * (n + 1), st));
   size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, len, lo, (int)(n + 1), st);
   void *scan_tmp = nullptr;
-  SVDSB_CUDA(cudaMalloc(&scan_tmp, scan_bytes));
+  SVDSB_CUDA(palloc(&scan_tmp, scan_bytes, st));
   for (int64_t r0 = 0; r0 < m; r0 += block_rows) {
     const int64_t r1 = std::min(m, r0 + block_rows);
     CsrPart p;
     p.rows = n;
     p.cols = r1 - r0;
-    SVDSB_CUDA(alloc_pad(&p.row_ptr, n + 1));
+    SVDSB_CUDA(alloc_pad(&p.row_ptr, n + 1, st));
     SVDSB_CUDA(cudaMemsetAsync(len + n, 0, sizeof(int), st));
     seg_bounds_kernel<<<grid1(n), 256, 0, st>>>(n, at.row_ptr, at.col, (int)r0, (int)r1, lo, len);
     SVDSB_LAUNCHED();
@@ -1146,8 +1180,8 @@ static int build_blocked_transpose(svdsb_csr *h, cudaStream_t st) {
     SVDSB_CUDA(cudaMemcpyAsync(p.host_row_ptr.data(), p.row_ptr, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, st));
     SVDSB_CUDA(cudaStreamSynchronize(st));
     p.nnz = p.host_row_ptr[n];
-    SVDSB_CUDA(alloc_pad(&p.col, std::max<int64_t>(p.nnz, 1)));
-    SVDSB_CUDA(alloc_pad(&p.val, std::max<int64_t>(p.nnz, 1)));
+    SVDSB_CUDA(alloc_pad(&p.col, std::max<int64_t>(p.nnz, 1), st));
+    SVDSB_CUDA(alloc_pad(&p.val, std::max<int64_t>(p.nnz, 1), st));
     seg_copy_kernel<<<grid1(n), 256, 0, st>>>(n, at.col, at.val, lo, p.row_ptr, (int)r0, p.col, p.val);
     SVDSB_LAUNCHED();
     int rc = build_partition(p, st);
@@ -1156,9 +1190,9 @@ static int build_blocked_transpose(svdsb_csr *h, cudaStream_t st) {
     h->atb_r0.push_back(r0);
   }
   SVDSB_CUDA(cudaStreamSynchronize(st));
-  cudaFree(lo);
-  cudaFree(len);
-  cudaFree(scan_tmp);
+  pfree(lo, st);
+  pfree(len, st);
+  pfree(scan_tmp, st);
   return SVDSB_OK;
 }
 
@@ -1219,7 +1253,7 @@ int svdsb_csr_create_host(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nnz, con
     svdsb_csr_destroy(h);
     return rc;
   }
-  if (alloc_pad(&p.val, std::max<int64_t>(nnz, 1)) != cudaSuccess) {
+  if (alloc_pad(&p.val, std::max<int64_t>(nnz, 1), st) != cudaSuccess) {
     svdsb_csr_destroy(h);
     set_error("cudaMalloc values failed");
     return SVDSB_ERR_ALLOC;
@@ -1252,19 +1286,19 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
   CsrPart &p = h->a;
   p.rows = m;
   p.cols = n;
-  SVDSB_CUDA(alloc_pad(&p.row_ptr, m + 1));
+  SVDSB_CUDA(alloc_pad(&p.row_ptr, m + 1, st));
   SVDSB_CUDA(cudaMemsetAsync(p.row_ptr, 0, sizeof(int) * (m + 1), st));
   int64_t nnz = 0;
   if (nt > 0) {
     unsigned long long *key = nullptr, *key_s = nullptr;
     int *idx = nullptr, *perm = nullptr, *first = nullptr, *seg = nullptr, *rowcnt = nullptr;
-    SVDSB_CUDA(cudaMalloc(&key, 8 * nt));
-    SVDSB_CUDA(cudaMalloc(&key_s, 8 * nt));
-    SVDSB_CUDA(cudaMalloc(&idx, 4 * nt));
-    SVDSB_CUDA(cudaMalloc(&perm, 4 * nt));
-    SVDSB_CUDA(cudaMalloc(&first, 4 * nt));
-    SVDSB_CUDA(cudaMalloc(&seg, 4 * (nt + 1)));
-    SVDSB_CUDA(cudaMalloc(&rowcnt, 4 * (m + 1)));
+    SVDSB_CUDA(palloc(&key, 8 * nt, st));
+    SVDSB_CUDA(palloc(&key_s, 8 * nt, st));
+    SVDSB_CUDA(palloc(&idx, 4 * nt, st));
+    SVDSB_CUDA(palloc(&perm, 4 * nt, st));
+    SVDSB_CUDA(palloc(&first, 4 * nt, st));
+    SVDSB_CUDA(palloc(&seg, 4 * (nt + 1), st));
+    SVDSB_CUDA(palloc(&rowcnt, 4 * (m + 1), st));
     SVDSB_CUDA(cudaMemsetAsync(rowcnt, 0, 4 * (m + 1), st));
     coo_keys_kernel<<<grid1(nt), 256, 0, st>>>(nt, n, rows, cols, key, idx);
     SVDSB_LAUNCHED();
@@ -1272,7 +1306,7 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key_s, idx, perm, (int)nt, 0, nbits, st);
     void *tmp = nullptr;
-    SVDSB_CUDA(cudaMalloc(&tmp, tb));
+    SVDSB_CUDA(palloc(&tmp, tb, st));
     SVDSB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key_s, idx, perm, (int)nt, 0, nbits, st));
     bump_launches();
     coo_first_kernel<<<grid1(nt), 256, 0, st>>>(nt, key_s, first);
@@ -1280,7 +1314,7 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     size_t sb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb, first, seg, (int)nt, st);
     void *stmp = nullptr;
-    SVDSB_CUDA(cudaMalloc(&stmp, sb));
+    SVDSB_CUDA(palloc(&stmp, sb, st));
     SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(stmp, sb, first, seg, (int)nt, st));
     bump_launches();
     int last_seg = 0, last_first = 0;
@@ -1288,30 +1322,30 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     SVDSB_CUDA(cudaMemcpyAsync(&last_first, first + nt - 1, 4, cudaMemcpyDeviceToHost, st));
     SVDSB_CUDA(cudaStreamSynchronize(st));
     nnz = (int64_t)last_seg + last_first;
-    SVDSB_CUDA(alloc_pad(&p.col, std::max<int64_t>(nnz, 1)));
-    SVDSB_CUDA(alloc_pad(&p.val, std::max<int64_t>(nnz, 1)));
+    SVDSB_CUDA(alloc_pad(&p.col, std::max<int64_t>(nnz, 1), st));
+    SVDSB_CUDA(alloc_pad(&p.val, std::max<int64_t>(nnz, 1), st));
     coo_sum_kernel<<<grid1(nt), 256, 0, st>>>(nt, n, key_s, perm, first, seg, vals, p.col, p.val, rowcnt);
     SVDSB_LAUNCHED();
     size_t sb2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb2, rowcnt, p.row_ptr, (int)(m + 1), st);
     void *stmp2 = nullptr;
-    SVDSB_CUDA(cudaMalloc(&stmp2, sb2));
+    SVDSB_CUDA(palloc(&stmp2, sb2, st));
     SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(stmp2, sb2, rowcnt, p.row_ptr, (int)(m + 1), st));
     bump_launches();
     SVDSB_CUDA(cudaStreamSynchronize(st));
-    cudaFree(key);
-    cudaFree(key_s);
-    cudaFree(idx);
-    cudaFree(perm);
-    cudaFree(first);
-    cudaFree(seg);
-    cudaFree(rowcnt);
-    cudaFree(tmp);
-    cudaFree(stmp);
-    cudaFree(stmp2);
+    pfree(key, st);
+    pfree(key_s, st);
+    pfree(idx, st);
+    pfree(perm, st);
+    pfree(first, st);
+    pfree(seg, st);
+    pfree(rowcnt, st);
+    pfree(tmp, st);
+    pfree(stmp, st);
+    pfree(stmp2, st);
   } else {
-    SVDSB_CUDA(cudaMalloc(&p.col, 4));
-    SVDSB_CUDA(cudaMalloc(&p.val, 8));
+    SVDSB_CUDA(palloc(&p.col, 4, st));
+    SVDSB_CUDA(palloc(&p.val, 8, st));
   }
   p.nnz = nnz;
   p.host_row_ptr.resize(m + 1);
