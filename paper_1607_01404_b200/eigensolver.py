@@ -1327,6 +1327,12 @@ class DavidsonSolver:
                 dv.set_int(self.ctx, ws.ci, ci)
                 ws.ci_host = ci
             kind, g0 = self._warm
+            if kind == "diag" and sin == 1:
+                # a restart cycle always starts from slot 0 (the diag-warm
+                # iteration reads only the chosen residual), so each basis
+                # size maps to one slot and half as many graphs get captured
+                dv.axpby(self.ctx, 1.0, ws.rbuf[1][:, ci:ci + 1], 0.0, ws.rbuf[0][:, ci:ci + 1])
+                sin = 0
             pend = self._launch_iter(g, kind, g0, sin, ci)
         # host bookkeeping of what the graph does
         if self.precond is not None:
