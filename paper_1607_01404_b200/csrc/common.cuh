@@ -172,6 +172,28 @@ __device__ __forceinline__ void fold_parts(const double *partials, unsigned npar
   }
 }
 
+// Software grid barrier (arrival counter + generation).  Every CTA of the
+// grid must be resident at once: callers size the grid to at most the
+// occupancy-limited number of co-resident CTAs and never trigger their
+// dependants before the last barrier.
+__device__ __forceinline__ void grid_barrier(unsigned int *bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int *gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // Returns true in exactly one CTA: the last to arrive at the ticket.  All
 // partial writes of this CTA must precede the call.  Resets the ticket.
 __device__ __forceinline__ bool last_cta(unsigned int *ticket) {

@@ -259,16 +259,22 @@ csr_tile_kernel(const int *__restrict__ tile_r, const int *__restrict__ row_ptr,
 // folds tile t, the value / index / row-pointer loads of its next tile are
 // already in flight; products are double-buffered in shared memory so one
 // barrier per tile suffices.  Same per-row summation order as above.
-template <int ORDER, bool SHORT>
-__global__ void __launch_bounds__(kTileThreads, 3)
-csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__restrict__ row_ptr,
-                     const int *__restrict__ col, const double *__restrict__ val, const double *__restrict__ x,
-                     double *__restrict__ y, int accumulate) {
-  __shared__ double prod[2][kTileNnz];
-  __shared__ int rps[2][kTileRows + 1];
+// The tile loop itself, shared with the fused normal-operator kernel.
+// CG: gather x with ld.global.cg (L2 only) -- required when x was written
+// earlier in the same kernel by other CTAs; prewait: prefetch the first
+// tile's immutable matrix data, then wait for the producer of x.
+template <int ORDER, bool SHORT, bool CG>
+__device__ __forceinline__ void pipe_tiles(int ntile, const int4 *__restrict__ info, const int *__restrict__ row_ptr,
+                                           const int *__restrict__ col, const double *__restrict__ val,
+                                           const double *x, double *y, int accumulate,
+                                           double (&prod)[2][kTileNnz], int (&rps)[2][kTileRows + 1],
+                                           bool prewait) {
   const int t = threadIdx.x;
   int tile = blockIdx.x;
-  if (tile >= ntile) return;
+  if (tile >= ntile) {
+    if (prewait) pdl_wait();
+    return;
+  }
   // stage A: loads for `tile`
   int4 cur = info[tile];
   double v[kPerThread];
@@ -291,7 +297,7 @@ csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
     rb = (t == 0 && nrows >= kTileThreads) ? __ldg(row_ptr + ti.x + kTileThreads) : 0;
   };
   issue(cur, v, c, rpa, rpb);
-  pdl_wait();  // matrix data is immutable after assembly; x / y are not
+  if (prewait) pdl_wait();  // matrix data is immutable after assembly; x / y are not
   int buf = 0;
   while (true) {
     const int next_tile = tile + gridDim.x;
@@ -308,7 +314,7 @@ csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
 #pragma unroll
     for (int i = 0; i < kPerThread; ++i) {
       int k = t + i * kTileThreads;
-      if (k < nnz) prod[buf][k] = dmul(v[i], __ldg(x + c[i]));
+      if (k < nnz) prod[buf][k] = dmul(v[i], CG ? __ldcg(x + c[i]) : __ldg(x + c[i]));
     }
     if (t <= nrows) rps[buf][t] = rpa;
     if (t == 0 && nrows >= kTileThreads) rps[buf][kTileThreads] = rpb;
@@ -331,6 +337,16 @@ csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
     rpb = rnb;
     buf ^= 1;
   }
+}
+
+template <int ORDER, bool SHORT>
+__global__ void __launch_bounds__(kTileThreads, 3)
+csr_tile_pipe_kernel(int ntile, const int4 *__restrict__ info, const int *__restrict__ row_ptr,
+                     const int *__restrict__ col, const double *__restrict__ val, const double *__restrict__ x,
+                     double *__restrict__ y, int accumulate) {
+  __shared__ double prod[2][kTileNnz];
+  __shared__ int rps[2][kTileRows + 1];
+  pipe_tiles<ORDER, SHORT, false>(ntile, info, row_ptr, col, val, x, y, accumulate, prod, rps, true);
   pdl_trigger();
 }
 

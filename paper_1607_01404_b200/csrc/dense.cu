@@ -798,24 +798,6 @@ ts_gemm_inplace_kernel(int64_t dim, double *x, int64_t ldx, int g, const double 
 constexpr int kCgsThreads = 512;
 constexpr int kCgsMaxCols = 40;
 
-__device__ __forceinline__ void grid_barrier(unsigned int *bar, unsigned int nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned int *gen = bar + 1;
-    const unsigned int g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 template <int NACC>
 __device__ __forceinline__ void cta_fold_wide(double (&acc)[NACC], double *part) {
   __shared__ double red[kCgsThreads / 32][NACC];
