@@ -36,6 +36,8 @@ extern "C" {
 #define SVDSB_ERR_CUDA (-2)     /* CUDA runtime failure                    */
 #define SVDSB_ERR_ALLOC (-3)    /* device/host allocation failure          */
 #define SVDSB_ERR_RANGE (-4)    /* size beyond the int32-index device layout */
+#define SVDSB_ERR_FORMAT (-5)   /* malformed Matrix Market input (MatrixMarketError) */
+#define SVDSB_ERR_IO (-6)       /* file cannot be opened / read / written (OSError) */
 
 typedef struct svdsb_ctx svdsb_ctx;  /* per-stream workspace for reductions */
 typedef struct svdsb_csr svdsb_csr;  /* device CSR of A plus stored A^T     */
@@ -332,6 +334,31 @@ int svdsb_h_insert(int g, int b, const double *hc, int64_t ldhc, double *h,
 /* H (g x g) = sym(G) (eigensolver.py:349-352). */
 int svdsb_h_symmetrize(int g, const double *gm, int64_t ldg, double *h,
                        int64_t ldh, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* Matrix Market ingestion (host side; replaces read_matrix_market /     */
+/* write_matrix_market / write_dense_market, matio.py:170-258).          */
+/* The reader is two calls: the header (shape, stored entry count,       */
+/* layout), then the entries into caller-owned host arrays of exactly    */
+/* `entries` elements (0-based rows/cols; array files column-major).     */
+/* A malformed file returns SVDSB_ERR_FORMAT with *err_line = the        */
+/* 1-based line the reference names and the reference's message in      */
+/* svdsb_last_error().  Symmetric expansion and device assembly are the  */
+/* caller's (svdsb_csr_create_coo_device sums duplicates in input order).*/
+
+int svdsb_mm_read_header(const char *path, int64_t *m, int64_t *n,
+                         int64_t *entries, int *is_array, int *symmetric,
+                         int64_t *err_line);
+int svdsb_mm_read_entries(const char *path, int64_t entries,
+                          int64_t *rows_host, int64_t *cols_host,
+                          double *vals_host, int64_t *err_line);
+/* "coordinate real general", values as %.17g (matio.py:244-251). */
+int svdsb_mm_write_coo(const char *path, int64_t m, int64_t n, int64_t nnz,
+                       const int64_t *row_ptr_host, const int64_t *col_host,
+                       const double *vals_host);
+/* "array real general", column-major (matio.py:254-262). */
+int svdsb_mm_write_array(const char *path, int64_t m, int64_t n,
+                         const double *a_host, int64_t lda);
 
 #ifdef __cplusplus
 }

@@ -111,3 +111,28 @@ def csr_digest(row_ptr, col_idx, values):
     for arr in (np.asarray(row_ptr, np.int64), np.asarray(col_idx, np.int64), np.asarray(values, np.float64)):
         h.update(np.ascontiguousarray(arr).tobytes())
     return h.hexdigest()
+
+
+def build_spec(spec):
+    """Host CSR (m, n, row_ptr, col_idx, values) of a spec."""
+    k = spec["kind"]
+    if k == "crit9":
+        inner = np.linspace(0.3, 0.7, 38)
+        sigma = np.sort(np.concatenate([[1.0 / spec["kappa"]], inner, [1.0]]))[::-1].copy()
+        return (60, 40) + synth_csr(sigma, 60, 40, spec["seed"])
+    if k == "synth":
+        sigma = np.geomspace(spec["lo"], 1.0, spec["p"])[::-1].copy()
+        return (spec["m"], spec["n"]) + synth_csr(sigma, spec["m"], spec["n"], spec["seed"])
+    if k == "diag":
+        d = np.asarray(spec["d"])
+        n = d.shape[0]
+        return (n, n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int64), d.astype(np.float64))
+    if k == "zero_col":
+        rng = np.random.default_rng(spec["seed"])
+        dense = rng.standard_normal((spec["m"], spec["n"]))
+        dense[:, spec["col"]] = 0.0
+        rows, cols = np.nonzero(dense)
+        return (spec["m"], spec["n"]) + ocsr.csr_from_coo(spec["m"], spec["n"], rows, cols, dense[rows, cols])
+    if k == "sparse":
+        return build_sparse(spec["seed"])
+    raise ValueError(k)

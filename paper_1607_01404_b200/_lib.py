@@ -74,6 +74,11 @@ _PROTOS = [
     ("svdsb_qr_small", i32, [i32, i32, vp, i64, vp, i64, vp, i64, vp, i64, vp]),
     ("svdsb_h_insert", i32, [i32, i32, vp, i64, vp, i64, vp]),
     ("svdsb_h_symmetrize", i32, [i32, vp, i64, vp, i64, vp]),
+    ("svdsb_mm_read_header", i32, [ctypes.c_char_p, c_int64_p, c_int64_p, c_int64_p, c_int_p, c_int_p,
+                                    c_int64_p]),
+    ("svdsb_mm_read_entries", i32, [ctypes.c_char_p, i64, vp, vp, vp, c_int64_p]),
+    ("svdsb_mm_write_coo", i32, [ctypes.c_char_p, i64, i64, i64, vp, vp, vp]),
+    ("svdsb_mm_write_array", i32, [ctypes.c_char_p, i64, i64, vp, i64]),
 ]
 
 EXPORTED = [p[0] for p in _PROTOS]
@@ -119,6 +124,8 @@ def check(rc, what=""):
     msg = last_error()
     if rc in (-1, -4):
         raise ValueError(msg or what)
+    if rc == -6:
+        raise OSError(msg or what)
     raise NativeError("%s failed (%d): %s" % (what, rc, msg))
 
 

@@ -18,7 +18,7 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libsvdsb.so")
 REPO = os.path.dirname(HERE)
 
-SOURCES = ["runtime.cu", "csr.cu", "dense.cu", "small.cu", "arrow.cu"]
+SOURCES = ["runtime.cu", "csr.cu", "dense.cu", "small.cu", "arrow.cu", "mmio.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -47,7 +47,7 @@ def build(force=False, verbose=False):
     os.makedirs(OUT_DIR, exist_ok=True)
     objs = []
     for src in SOURCES:
-        obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
+        obj = os.path.join(OUT_DIR, os.path.splitext(src)[0] + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(REPO, "include"),
                "-c", os.path.join(CSRC, src), "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)

@@ -664,3 +664,111 @@ def svds_solve(a, precond=None, cfg=None, return_device=False):
     stats.seconds = time.perf_counter() - t0
     return SvdsResult(sigma=sigma, u=u, v=v, rnorms=rnorms, converged=conv, stats=stats,
                       status=_status_merge(statuses, bool(conv.all())), stage1_rnorms=stage1_r7)
+
+
+# ------------------------------------------------- condition-number mode
+
+@dataclass
+class CondResult:
+    """hybrid.py:187-194."""
+
+    kappa: float
+    sigma_max: float
+    sigma_min: float
+    infinite: bool
+    lower_bound: bool
+    stats: SvdsStats
+
+
+class _RelativeTest:
+    """||r_C|| <= rel_tol |lam| (the loose rule of hybrid.py:667-668)."""
+
+    split_n = None
+
+    def __init__(self, rel_tol):
+        self.rel_tol = float(rel_tol)
+
+    def evaluate(self, cand, op_norm):
+        return cand.rnorm <= abs(cand.lam) * self.rel_tol
+
+    def __call__(self, lam, rnorm, x, opx, op_norm):
+        return rnorm <= abs(lam) * self.rel_tol
+
+
+def estimate_condition_number(a, precond=None, cfg=None, rel_tol=0.1):
+    """sigma_max / sigma_min from two loose one-pair GD+k solves on the
+    normal operator, largest then smallest (hybrid.py:634-701).  A smallest
+    squared value at or below ||C|| eps max(m, n) reports kappa = inf; a
+    smallest solve cut off by the budget marks the estimate a lower bound."""
+    t0 = time.perf_counter()
+    cfg = cfg if cfg is not None else SvdsConfig()
+    from .dist import DistSvdOperator
+    if not isinstance(a, DistSvdOperator):
+        a = SvdOperator.wrap(a)
+    if not 0.0 < rel_tol < 1.0:
+        raise ValueError("rel_tol must lie in (0, 1)")
+    stats = SvdsStats()
+    op, swapped = orient_problem(a)
+    est = NormEstimate(cfg.a_norm)
+    c_op = make_normal_operator(op)
+    pre = select_preconditioner(precond, "AAt" if swapped else "AtA")
+    budget = cfg.max_matvecs
+    mv0 = op.n_matvecs
+
+    def ops_left():
+        if budget is None:
+            return None
+        return max((budget - (op.n_matvecs - mv0)) // 2, 0)
+
+    test = _RelativeTest(rel_tol)
+
+    def one(target, seed, mbs, mrs):
+        e = EigConfig(num_evals=1, target=target, max_basis_size=mbs, min_restart_size=mrs, plus_k=1,
+                      max_block_size=1, convergence_test=test, max_matvecs=ops_left(), seed=seed)
+        return eig_solve(c_op, e, precond=pre, est=est, est_mode="normal")
+
+    pre_before = pre.n_applies if pre is not None else 0
+    r_hi = one(TARGET_LARGEST, cfg.seed, *_BASIS_SMALL)
+    stats.stage1_matvecs = op.n_matvecs - mv0
+    mv1 = op.n_matvecs
+    r_lo = one(TARGET_SMALLEST, cfg.seed + 1, *_BASIS_LARGE)
+    stats.stage2_matvecs = op.n_matvecs - mv1
+    stats.restarts = r_hi.stats.restarts + r_lo.stats.restarts
+    stats.resets = r_hi.stats.resets + r_lo.stats.resets
+    if pre is not None:
+        stats.precond_applies = pre.n_applies - pre_before
+    sigma_max = float(np.sqrt(max(r_hi.eigenvalues[0], 0.0))) if r_hi.eigenvalues.size else 0.0
+    lam_min = float(r_lo.eigenvalues[0]) if r_lo.eigenvalues.size else 0.0
+    sigma_min = float(np.sqrt(max(lam_min, 0.0)))
+    infinite = lam_min <= est.c_norm * EPS * max(op.m, op.n)
+    lower_bound = (not infinite) and (r_lo.status != "ok" or not bool(np.all(r_lo.converged)))
+    kappa = np.inf if infinite else sigma_max / sigma_min
+    stats.seconds = time.perf_counter() - t0
+    return CondResult(kappa=kappa, sigma_max=sigma_max, sigma_min=sigma_min, infinite=infinite,
+                      lower_bound=lower_bound, stats=stats)
+
+
+def stage2_convergence_test(lam, x, a, est, delta):
+    """Two-level stage-2 acceptance on the stacked vector x = [v; u]
+    (hybrid.py:244-260): the eigenresidual test, then Eq. (7) on the
+    normalised halves; a zero-norm half is rejected.  ``x`` may be a host
+    array or a device vector; the two products run on device (counted)."""
+    a = SvdOperator.wrap(a)
+    n = a.n
+    xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, dtype=np.float64).copy())
+    xt = xt.to(device=dv.context().device, dtype=DTYPE).reshape(-1)
+    xv, xu = xt[:n].contiguous(), xt[n:].contiguous()
+    av = a.apply(xv).reshape(-1)
+    atu = a.apply_t(xu).reshape(-1)
+    lam = float(lam)
+    rnorm = float(torch.sqrt(torch.sum((atu - lam * xv) ** 2) + torch.sum((av - lam * xu) ** 2)))
+    a_norm = est.a_norm
+    if not rnorm < np.sqrt(2.0) * a_norm * delta:
+        return False
+    nv, nu = float(torch.linalg.vector_norm(xv)), float(torch.linalg.vector_norm(xu))
+    if nv == 0.0 or nu == 0.0:
+        return False
+    sigma = abs(lam)
+    r7 = np.sqrt(float(torch.sum((av / nv - sigma * xu / nu) ** 2)) +
+                 float(torch.sum((atu / nu - sigma * xv / nv) ** 2)))
+    return bool(r7 < a_norm * delta)

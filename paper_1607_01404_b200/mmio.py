@@ -1,0 +1,121 @@
+"""Matrix Market ingestion.
+
+Same functions, arguments, results and errors as the reference's
+pkg/src/itersvd/matio.py:158-276 (``read_matrix_market``,
+``write_matrix_market``, ``write_dense_market``, ``read_dense_market``,
+``MatrixMarketError``).  Parsing runs in the native library
+(csrc/mmio.cpp, one pass over the file in C++); the triplets then go to the
+device CSR assembly, which sums duplicates in input order exactly like the
+reference's ``SparseMatrixCsr.from_coo``.  ``read_matrix_market_coo``
+returns the parsed (and symmetric-expanded) triplets without assembling.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _lib
+from .matrix import SparseMatrixCsr
+
+
+class MatrixMarketError(ValueError):
+    """Malformed Matrix Market input; carries the offending line number
+    (matio.py:12-19)."""
+
+    def __init__(self, message, line=None):
+        if line is not None:
+            message = "line %d: %s" % (line, message)
+        super().__init__(message)
+        self.line = line
+
+
+def _path(path):
+    return os.fsencode(os.fspath(path))
+
+
+def _check(rc, err_line, what):
+    if rc == 0:
+        return
+    if rc == -5:
+        raise MatrixMarketError(_lib.last_error(), line=int(err_line.value))
+    _lib.check(rc, what)
+
+
+def read_matrix_market_coo(path):
+    """(m, n, rows, cols, vals, is_array) of a Matrix Market file: 0-based
+    int64 indices, symmetric storage expanded as the reference does
+    (stored entries first, then the mirrored off-diagonal ones), stored zeros
+    of array files dropped (matio.py:170-241)."""
+    lib = _lib.load()
+    m, n, entries = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    is_array, symmetric = ctypes.c_int(), ctypes.c_int()
+    err = ctypes.c_int64()
+    p = _path(path)
+    rc = lib.svdsb_mm_read_header(p, ctypes.byref(m), ctypes.byref(n), ctypes.byref(entries),
+                                  ctypes.byref(is_array), ctypes.byref(symmetric), ctypes.byref(err))
+    _check(rc, err, "svdsb_mm_read_header")
+    cnt = int(entries.value)
+    rows = np.empty(cnt, dtype=np.int64)
+    cols = np.empty(cnt, dtype=np.int64)
+    vals = np.empty(cnt, dtype=np.float64)
+    rc = lib.svdsb_mm_read_entries(p, cnt, _lib.np_ptr(rows), _lib.np_ptr(cols), _lib.np_ptr(vals),
+                                   ctypes.byref(err))
+    _check(rc, err, "svdsb_mm_read_entries")
+    if symmetric.value:
+        off = rows != cols
+        rows, cols, vals = (np.concatenate([rows, cols[off]]), np.concatenate([cols, rows[off]]),
+                            np.concatenate([vals, vals[off]]))
+    if is_array.value:
+        # dense storage forces zeros in; the reference drops them after
+        # assembly (no duplicates exist in array storage, so before is equal)
+        keep = vals != 0.0
+        if not keep.all():
+            rows, cols, vals = rows[keep], cols[keep], vals[keep]
+    return int(m.value), int(n.value), rows, cols, vals, bool(is_array.value)
+
+
+def read_matrix_market(path, device=None):
+    """Read a real Matrix Market file into a (device-assembled) CSR matrix
+    (matio.py:170-241).  ``coordinate real/integer/double general|symmetric``
+    and ``array real general``; anything else raises MatrixMarketError with
+    the reference's message and line number."""
+    m, n, rows, cols, vals, _ = read_matrix_market_coo(path)
+    if rows.size == 0 or m == 0 or n == 0:
+        return SparseMatrixCsr(m, n, np.zeros(m + 1, dtype=np.int64), np.zeros(0, dtype=np.int64),
+                               np.zeros(0, dtype=np.float64))
+    return SparseMatrixCsr.from_coo(m, n, rows, cols, vals, device=device)
+
+
+def write_matrix_market(path, a):
+    """``coordinate real general`` with %.17g values (matio.py:244-251)."""
+    rp = _lib.as_i64(a.row_ptr)
+    ci = _lib.as_i64(a.col_idx)
+    va = _lib.as_f64(a.values)
+    rc = _lib.load().svdsb_mm_write_coo(_path(path), int(a.m), int(a.n), int(va.shape[0]), _lib.np_ptr(rp),
+                                        _lib.np_ptr(ci), _lib.np_ptr(va))
+    _lib.check(rc, "svdsb_mm_write_coo")
+
+
+def write_dense_market(path, a):
+    """``array real general``, column major (matio.py:254-262); ``a`` may be
+    a host array or a device tensor."""
+    if hasattr(a, "detach"):
+        a = a.detach().cpu().numpy()
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    if a.ndim != 2:
+        raise ValueError("dense block must be two-dimensional")
+    rc = _lib.load().svdsb_mm_write_array(_path(path), int(a.shape[0]), int(a.shape[1]), _lib.np_ptr(a),
+                                          max(int(a.shape[0]), 1))
+    _lib.check(rc, "svdsb_mm_write_array")
+
+
+def read_dense_market(path):
+    """An ``array real general`` file as a dense column-major host block
+    (matio.py:265-268)."""
+    m, n, rows, cols, vals, _ = read_matrix_market_coo(path)
+    out = np.zeros((m, n), dtype=np.float64, order="F")
+    # duplicates only arise from coordinate files: summed in input order,
+    # as the reference's CSR assembly does before densifying
+    np.add.at(out, (rows, cols), vals)
+    return out

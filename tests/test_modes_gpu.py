@@ -1,0 +1,154 @@
+"""Drop-in modes beyond the two extreme targets, on device, against the
+reference's own outcomes (tests/golden/modes.json, made by
+tests/golden/make_modes_golden.py): the condition-number estimator
+(hybrid.py:634-701, pysvds cond_est), target="closest" solves
+(hybrid.py:385-387, 433-439), the stage-2 convergence test
+(hybrid.py:244-260), and Matrix Market files assembled on device."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import csr as ocsr
+from oracle import gen as ogen
+
+pytestmark = pytest.mark.gpu
+
+GOLD = load_golden("modes.json")
+
+
+def _mat(spec):
+    from paper_1607_01404_b200 import SparseMatrixCsr
+    m, n, rp, ci, va = ogen.build_spec(spec)
+    return SparseMatrixCsr(m, n, rp, ci, va), (m, n, rp, ci, va)
+
+
+@pytest.mark.parametrize("name", sorted(GOLD["cond"]))
+def test_condition_number_against_reference(name):
+    from paper_1607_01404_b200 import SvdsConfig, estimate_condition_number
+    g = GOLD["cond"][name]
+    a, _ = _mat(g["spec"])
+    r = estimate_condition_number(a, cfg=SvdsConfig(**g["cfg"]))
+    assert r.infinite == g["infinite"]
+    assert r.lower_bound == g["lower_bound"]
+    if g["infinite"]:
+        assert r.kappa == np.inf
+        return
+    # same GD+k trajectory (same seeded draws) -> the same loose estimate
+    assert abs(r.kappa - g["kappa"]) <= 1e-6 * g["kappa"]
+    assert abs(r.sigma_max - g["sigma_max"]) <= 1e-6 * g["sigma_max"]
+    if g["spec"]["kind"] == "crit9":
+        # criterion 9 (test_acceptance.py:295-311): within 10% of the truth
+        assert abs(r.kappa - g["spec"]["kappa"]) <= 0.1 * g["spec"]["kappa"]
+    tot = r.stats.stage1_matvecs + r.stats.stage2_matvecs
+    gtot = g["stats"]["stage1_matvecs"] + g["stats"]["stage2_matvecs"]
+    assert abs(tot - gtot) <= 0.2 * gtot + 4
+
+
+def test_cond_est_binding():
+    from paper_1607_01404_b200 import pysvds
+    g = GOLD["cond"]["sparse1003"]
+    _, (m, n, rp, ci, va) = _mat(g["spec"])
+    dense = np.zeros((m, n))
+    dense[np.repeat(np.arange(m), np.diff(rp)), ci] = va
+    k = pysvds.cond_est(dense, tol=0.1)
+    assert abs(k - g["kappa"]) <= 1e-6 * g["kappa"]
+    zc = GOLD["cond"]["zero_col_60x40"]
+    _, (m, n, rp, ci, va) = _mat(zc["spec"])
+    dense = np.zeros((m, n))
+    dense[np.repeat(np.arange(m), np.diff(rp)), ci] = va
+    assert pysvds.cond_est(dense) == float("inf")
+
+
+@pytest.mark.parametrize("name", sorted(GOLD["closest"]))
+def test_closest_target_against_reference(name):
+    from paper_1607_01404_b200 import SvdsConfig, svds_solve
+    g = GOLD["closest"][name]
+    a, (m, n, rp, ci, va) = _mat(g["spec"])
+    res = svds_solve(a, cfg=SvdsConfig(target="closest", **g["cfg"]))
+    want = np.array(g["sigma"])
+    assert res.status == g["status"]
+    assert list(res.converged) == g["converged"]
+    a_norm = float(np.linalg.svd(ogen_dense(m, n, rp, ci, va), compute_uv=False)[0])
+    eps = g["cfg"]["eps"]
+    assert np.abs(res.sigma - want).max() <= max(eps * a_norm, 1e-10 * want.max())
+    for i in range(want.size):
+        av = ocsr.spmv(m, n, rp, ci, va, res.v[:, i])
+        atu = ocsr.spmv(m, n, rp, ci, va, res.u[:, i], transpose=True)
+        r7 = np.sqrt(np.linalg.norm(av - res.sigma[i] * res.u[:, i]) ** 2 +
+                     np.linalg.norm(atu - res.sigma[i] * res.v[:, i]) ** 2)
+        assert r7 <= eps * a_norm
+
+
+def ogen_dense(m, n, rp, ci, va):
+    d = np.zeros((m, n))
+    d[np.repeat(np.arange(m), np.diff(rp)), ci] = va
+    return d
+
+
+def test_stage2_convergence_test_matches_host():
+    """stage2_convergence_test on device vs the same two-level test in
+    numpy on the host (hybrid.py:226-260), accept and reject cases."""
+    from paper_1607_01404_b200 import NormEstimate, SvdOperator, stage2_convergence_test
+    sigma = np.geomspace(1e-3, 1.0, 60)[::-1].copy()
+    m, n = 90, 60
+    rp, ci, va = ogen.synth_csr(sigma, m, n, 2200)
+    d = ogen_dense(m, n, rp, ci, va)
+    u, s, vt = np.linalg.svd(d, full_matrices=False)
+    from paper_1607_01404_b200 import SparseMatrixCsr
+    op = SvdOperator.wrap(SparseMatrixCsr(m, n, rp, ci, va))
+    est = NormEstimate(float(s[0]))
+    x = np.concatenate([vt[3], u[:, 3]]) / np.sqrt(2.0)
+    assert stage2_convergence_test(s[3], x, op, est, 1e-10)
+    assert op.n_matvecs == 2
+    # perturbed: fails the first level
+    y = x.copy()
+    y[5] += 1e-6
+    assert not stage2_convergence_test(s[3], y, op, est, 1e-10)
+    # null-space direction (u half zero): rejected even when level 1 holds
+    z = np.concatenate([np.zeros(n), u[:, 0] * 0.0])
+    z[0] = 1.0
+    assert not stage2_convergence_test(0.0, np.zeros(n + m) + z, op, NormEstimate(1e30), 1e-10)
+
+
+def test_matrix_market_device_assembly(tmp_path):
+    """read_matrix_market -> device CSR, exported bit-identical to the
+    oracle's from_coo of the same triplets (and a symmetric file expanded);
+    a solve on it equals the solve on the in-memory matrix."""
+    from paper_1607_01404_b200 import (SparseMatrixCsr, SvdsConfig, read_matrix_market, svds_solve,
+                                       write_matrix_market)
+    m, n, rp, ci, va = ogen.build_sparse(1003)
+    a0 = SparseMatrixCsr(m, n, rp, ci, va)
+    p = tmp_path / "a.mtx"
+    write_matrix_market(p, a0)
+    a1 = read_matrix_market(p)
+    rp1, ci1, va1 = a1.device_csr().export()
+    np.testing.assert_array_equal(rp1, rp)
+    np.testing.assert_array_equal(ci1, ci)
+    assert va1.tobytes() == va.tobytes()
+    cfg = lambda: SvdsConfig(num_svals=4, target="smallest", eps=1e-10, seed=3)  # noqa: E731
+    r0 = svds_solve(a0, cfg=cfg())
+    r1 = svds_solve(a1, cfg=cfg())
+    assert r0.sigma.tobytes() == r1.sigma.tobytes()
+    # symmetric storage: lower triangle stored, expanded on read
+    s = tmp_path / "s.mtx"
+    rng = np.random.default_rng(5)
+    k = 400
+    r = rng.integers(0, 50, k)
+    c = rng.integers(0, 50, k)
+    lo = np.maximum(r, c), np.minimum(r, c)
+    v = rng.standard_normal(k)
+    with open(s, "w") as f:
+        f.write("%%MatrixMarket matrix coordinate real symmetric\n")
+        f.write("50 50 %d\n" % k)
+        for i in range(k):
+            f.write("%d %d %.17g\n" % (lo[0][i] + 1, lo[1][i] + 1, v[i]))
+    a2 = read_matrix_market(s)
+    off = lo[0] != lo[1]
+    rows = np.concatenate([lo[0], lo[1][off]])
+    cols = np.concatenate([lo[1], lo[0][off]])
+    vals = np.concatenate([v, v[off]])
+    want = ocsr.csr_from_coo(50, 50, rows, cols, vals)
+    got = a2.device_csr().export()
+    for x, y in zip(got, want):
+        assert np.asarray(x).tobytes() == np.asarray(y).tobytes()
