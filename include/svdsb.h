@@ -336,6 +336,43 @@ int svdsb_h_symmetrize(int g, const double *gm, int64_t ldg, double *h,
                        int64_t ldh, void *stream);
 
 /* ------------------------------------------------------------------ */
+/* JDQMR inner solver (PRIMME's QMRs on the Jacobi-Davidson correction    */
+/* equation; the paper's stage-2 method, PAPER.md:765-767, 897 -- the      */
+/* reference runs GD+k only):                                */
+/*   P (Op - sigma I) P t = -r,  P = I - Q Q^T, Q (n x nq, nq <= 32)       */
+/* orthonormal, optional point-Jacobi K^-1 = 1 ./ dg applied as P K^-1 P.  */
+/* The caller owns every vector (device, length n, contiguous).  The      */
+/* operator product w = Op d is the caller's (the CSR SpMV entry points)  */
+/* between phase 0 and each phase 1:                                       */
+/*   phase 0: setup from r (state inputs SIGMA, RITZ, RNORM, MAXIT, TOL_E, */
+/*            ETOL_FRAC, LFAC must be written first, svdsb_jd_state_size() */
+/*            doubles);                                                     */
+/*   phase 1: one QMRs step after w = Op d: scalars, t/g updates, the     */
+/*            eigen-residual estimate of x + t and the device-side stop    */
+/*            test; `cond` (from svdsb_while_begin, or 0) is set to 0 when */
+/*            the inner solve is done.                                     */
+/* The solution accumulates in t.  State slots: 0 SIGMA, 14 ERES, 16 IT,   */
+/* 17 MAXIT, 18 TOL_E, 19 ETOL_FRAC, 20 STOP (reason), 21 RITZ, 22 RNORM,  */
+/* 25 LFAC (see csrc/jdqmr.cu).                                           */
+typedef struct svdsb_jd_vecs {
+  const double *r;   /* outer residual (input)                     */
+  const double *dg;  /* Jacobi diagonal or NULL                    */
+  double *rc, *g, *t, *dl, *z, *d, *w;  /* QMRs work vectors, t = solution */
+} svdsb_jd_vecs;
+
+int svdsb_jd_state_size(void);
+int svdsb_jd_phase(svdsb_ctx *ctx, int phase, int64_t n,
+                   const svdsb_jd_vecs *vecs, const double *q, int64_t ldq,
+                   int nq, double *state, uint64_t cond, void *stream);
+/* Capture a CUDA graph whose single node is a WHILE loop: launches made on
+ * `stream` between begin and end form the loop body, which repeats while
+ * the conditional handle *cond_out (pass it to svdsb_jd_phase) is nonzero;
+ * it is 1 at every launch of the instantiated graph.  PDL is off inside the
+ * body.  Launch / destroy with svdsb_graph_launch / svdsb_graph_destroy. */
+int svdsb_while_begin(void *stream, uint64_t *cond_out);
+int svdsb_while_end(void *stream, void **exec_out);
+
+/* ------------------------------------------------------------------ */
 /* Matrix Market ingestion (host side; replaces read_matrix_market /     */
 /* write_matrix_market / write_dense_market, matio.py:170-258).          */
 /* The reader is two calls: the header (shape, stored entry count,       */

@@ -74,6 +74,10 @@ _PROTOS = [
     ("svdsb_qr_small", i32, [i32, i32, vp, i64, vp, i64, vp, i64, vp, i64, vp]),
     ("svdsb_h_insert", i32, [i32, i32, vp, i64, vp, i64, vp]),
     ("svdsb_h_symmetrize", i32, [i32, vp, i64, vp, i64, vp]),
+    ("svdsb_jd_state_size", i32, []),
+    ("svdsb_jd_phase", i32, [vp, i32, i64, vp, vp, i64, i32, vp, ctypes.c_uint64, vp]),
+    ("svdsb_while_begin", i32, [vp, ctypes.POINTER(ctypes.c_uint64)]),
+    ("svdsb_while_end", i32, [vp, ctypes.POINTER(vp)]),
     ("svdsb_mm_read_header", i32, [ctypes.c_char_p, c_int64_p, c_int64_p, c_int64_p, c_int_p, c_int_p,
                                     c_int64_p]),
     ("svdsb_mm_read_entries", i32, [ctypes.c_char_p, i64, vp, vp, vp, c_int64_p]),

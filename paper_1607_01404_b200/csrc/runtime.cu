@@ -19,7 +19,12 @@ void set_error(const char *fmt, ...) {
 
 int64_t bump_launches(int n) { return g_launches.fetch_add(n) + n; }
 
+static thread_local bool g_pdl_suspended = false;
+
+void set_pdl_suspended(bool on) { g_pdl_suspended = on; }
+
 bool pdl_on() {
+  if (g_pdl_suspended) return false;
   static int on = -1;
   if (on < 0) {
     const char *e = getenv("SVDSB_PDL");

@@ -34,6 +34,8 @@ TARGET_CLOSEST_GEQ = "closest_geq"
 EXTRACT_RR = "rayleigh_ritz"
 EXTRACT_REFINED = "refined_const_shift"
 PRACTICAL_FLOOR_FACTOR = 10.0          # eigensolver.py:43
+METHOD_GDK = "GD+k"                    # the reference's method in both stages
+METHOD_JDQMR = "JDQMR"                 # PRIMME's JDQMR; jdqmr.py
 _IMPROVE_FACTOR = 0.999                # eigensolver.py:47
 REORTH_FACTOR = 1.0 / np.sqrt(2.0)     # kernels.py:24
 DEFICIENT_TOL = 1e-14                  # kernels.py:28
@@ -66,10 +68,20 @@ class EigConfig:
     disable_reset: bool = False
     stagnation_window: int = 250
     iteration_hook: object = None
+    # expansion method: GD+k (preconditioned residual, the reference's) or
+    # JDQMR (QMRs on the correction equation, device inner solver)
+    method: str = METHOD_GDK
+    max_inner_iterations: int = 200
+    inner_etol_frac: float = 0.0
+    inner_lfac: float = 0.1
 
     def validate(self, dim):
         if self.num_evals < 0:
             raise ValueError("num_evals must be nonnegative")
+        if self.method not in (METHOD_GDK, METHOD_JDQMR):
+            raise ValueError("method must be %r or %r" % (METHOD_GDK, METHOD_JDQMR))
+        if self.max_inner_iterations < 0 or not (0.0 <= self.inner_etol_frac < 1.0) or self.inner_lfac < 0.0:
+            raise ValueError("bad JDQMR inner-solver settings")
         if self.target not in (TARGET_LARGEST, TARGET_SMALLEST, TARGET_CLOSEST_GEQ):
             raise ValueError("unknown target %r" % (self.target,))
         if self.extraction not in (EXTRACT_RR, EXTRACT_REFINED):
@@ -104,6 +116,8 @@ class EigStats:
     outer_iterations: int = 0
     syncs: int = 0
     graphs_captured: int = 0
+    inner_iterations: int = 0
+    inner_solves: int = 0
 
 
 @dataclass
@@ -1077,8 +1091,78 @@ class DavidsonSolver:
                     dv.axpby(self.ctx, 1.0, y_d[:, conv_count:hi], 0.0, self.prev_d[:g, :k])
                 self.prev_coefs = k
             self.prev_coefs_g = info["g"]
+        if cfg.method == METHOD_JDQMR:
+            corr = self._jd_corrections(res_block, ci, cands, y_d, refined)
+            if corr is not None:
+                self._expand(corr, ci, graph=False, precondition=False)
+                return info
         self._expand(res_block, ci, graph=refined or ci == conv_count)
         return info
+
+    # ------------------------------------------------------------ JDQMR
+    def _jd_threshold(self, cand):
+        """Eigen-residual at which the candidate would pass the outer test
+        (the inner solve stops there)."""
+        test = self.cfg.convergence_test
+        if test is None:
+            return max(1e-12 * self.op_norm, PRACTICAL_FLOOR_FACTOR * EPS * self.op_norm)
+        fn = getattr(test, "threshold", None)
+        return float(fn(cand.lam, self.op_norm)) if fn is not None else 0.0
+
+    def _jd_corrections(self, res_block, ci, cands, y_d, refined):
+        """JDQMR expansion block: for each block column the device inner
+        solve of the correction equation of its Ritz pair (jdqmr.py);
+        None when a GD step is taken instead (nothing to correct)."""
+        from .jdqmr import JdqmrInner
+        cfg = self.cfg
+        b = min(res_block.shape[1], self.gmax - self.g)
+        if b <= 0:
+            return None
+        jd = getattr(self, "_jd", None)
+        if jd is None:
+            diag = getattr(self.precond, "diagonal", None) if self.precond is not None else None
+            if self.precond is not None and diag is None:
+                raise ValueError("JDQMR supports the point-Jacobi preconditioner or none")
+            jd = self._jd = JdqmrInner(self.ctx, self.op, self.n, diag=diag,
+                                       use_graph=self.use_graphs and not self.comm.distributed)
+            self._jd_x = dv.new_block(self.n, 1)
+            self._jd_out = dv.new_block(self.n, cfg.max_block_size)
+        if self.comm.distributed:
+            raise ValueError("JDQMR is single-GPU in this build")
+        g = self.g
+        out = self._jd_out[:, :b]
+        any_inner = False
+        for j in range(b):
+            if refined:
+                ycol, cand = self.yref[:g], cands[0]
+            else:
+                ycol, cand = y_d[:g, ci + j], cands[ci + j]
+            r = res_block[:, j:j + 1]
+            budget = self._budget_left() - (b - j)
+            maxit = max(min(cfg.max_inner_iterations, budget), 0)
+            if cand.rnorm <= 0.0 or maxit == 0:
+                dv.axpby(self.ctx, 1.0, r, 0.0, out[:, j:j + 1])
+                continue
+            dv.ts_gemm(self.ctx, self.v[:, :g], ycol.reshape(g, 1), self._jd_x)
+            t, info = jd.solve(self._jd_x, cand.lam, r, cand.rnorm, against=self._against(), maxit=maxit,
+                               tol_e=self._jd_threshold(cand), etol_frac=cfg.inner_etol_frac,
+                               lfac=cfg.inner_lfac)
+            it = info["iterations"]
+            self.stats.matvecs += it
+            self.stats.inner_iterations += it
+            self.stats.inner_solves += 1
+            if self.precond is not None:
+                self.precond.n_applies += it + 1
+                self.stats.precond_applies += it + 1
+            if it == 0:
+                # breakdown before the first step: plain residual
+                dv.axpby(self.ctx, 1.0, r, 0.0, out[:, j:j + 1])
+            else:
+                any_inner = True
+                dv.axpby(self.ctx, 1.0, t.unsqueeze(1), 0.0, out[:, j:j + 1])
+        if not any_inner and self.precond is not None:
+            return None
+        return out
 
     # ------------------------------------------------ speculative expansion
     # A single new column is orthonormalised by device-decided CGS passes
@@ -1099,17 +1183,18 @@ class DavidsonSolver:
         Gram / projection kernels, which stream at 82-86 % of HBM."""
         return self.fused_cgs and cols <= 40 and 8 * self.n * cols <= (64 << 20)
 
-    def _expand_speculative(self, block):
+    def _expand_speculative(self, block, precondition=True):
         g = self.g
         dst = self.v[:, g:g + 1]
         prior = [b for b in self._against()] + [self.v[:, :g]]
         total = sum(b.shape[1] for b in prior)
         ws = self._ws
-        d = getattr(self.precond, "diagonal", None) if self.precond is not None else None
+        pre = self.precond if precondition else None
+        d = getattr(pre, "diagonal", None) if pre is not None else None
         if (ws is not None and self._use_fused_cgs(total) and len(prior) <= _lib.MAX_BLOCKS
-                and (self.precond is None or d is not None)):
+                and (pre is None or d is not None)):
             # same single launch as the graphed iterations (bit-identical)
-            if self.precond is not None:
+            if pre is not None:
                 self.precond.n_applies += 1
                 self.stats.precond_applies += 1
             st = self._dgks_state
@@ -1125,8 +1210,8 @@ class DavidsonSolver:
             self._spec = {"g0": g}
             self.g = g + 1
             return
-        if self.precond is not None:
-            self.precond.apply_into(block, dst)
+        if pre is not None:
+            pre.apply_into(block, dst)
             self.stats.precond_applies += 1
         else:
             dv.axpby(self.ctx, 1.0, block, 0.0, dst)
@@ -1359,21 +1444,22 @@ class DavidsonSolver:
         host = ws.status[slot].numpy()
         return [host[:g].copy(), host[g:g + p].copy(), host[g + p:g + p + 8].copy()]
 
-    def _expand(self, res_block, ci=0, graph=True):
-        """eigensolver.py:666-700."""
+    def _expand(self, res_block, ci=0, graph=True, precondition=True):
+        """eigensolver.py:666-700.  precondition=False: the block is already
+        the expansion direction (JDQMR corrections)."""
         b = min(res_block.shape[1], self.gmax - self.g)
         if b <= 0:
             return
-        if graph and self._graph_ok(b):
+        if graph and precondition and self._graph_ok(b):
             self._expand_graphed(ci)
             return
         block = res_block[:, :b]
         if self._can_speculate(b):
-            self._expand_speculative(block)
+            self._expand_speculative(block, precondition)
             return
         g = self.g
         dst = self.v[:, g:g + b]
-        if self.precond is not None:
+        if self.precond is not None and precondition:
             self.precond.apply_into(block, dst)
             self.stats.precond_applies += b
         else:

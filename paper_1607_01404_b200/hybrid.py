@@ -95,6 +95,7 @@ class SvdsStats:
     outer_iterations: int = 0
     syncs: int = 0
     graphs_captured: int = 0
+    inner_iterations: int = 0
 
 
 @dataclass
@@ -169,6 +170,9 @@ class Stage1Test:
     def evaluate(self, cand, op_norm):
         return cand.rnorm <= max(np.sqrt(abs(cand.lam) * op_norm) * self.delta, EPS * op_norm)
 
+    def threshold(self, lam, op_norm):
+        return max(np.sqrt(abs(lam) * op_norm) * self.delta, EPS * op_norm)
+
     def __call__(self, lam, rnorm, x, opx, op_norm):
         return rnorm <= max(np.sqrt(abs(lam) * op_norm) * self.delta, EPS * op_norm)
 
@@ -181,6 +185,9 @@ class Stage2Test:
     def __init__(self, n, delta):
         self.split_n = int(n)
         self.delta = float(delta)
+
+    def threshold(self, lam, op_norm):
+        return np.sqrt(2.0) * op_norm * self.delta
 
     def evaluate(self, cand, op_norm):
         if not cand.rnorm < np.sqrt(2.0) * op_norm * self.delta:
@@ -478,6 +485,7 @@ def _add_stats(stats, r):
     stats.outer_iterations += r.stats.outer_iterations
     stats.syncs += r.stats.syncs
     stats.graphs_captured += r.stats.graphs_captured
+    stats.inner_iterations += r.stats.inner_iterations
 
 
 def svds_solve(a, precond=None, cfg=None, return_device=False):
@@ -690,6 +698,9 @@ class _RelativeTest:
 
     def evaluate(self, cand, op_norm):
         return cand.rnorm <= abs(cand.lam) * self.rel_tol
+
+    def threshold(self, lam, op_norm):
+        return abs(lam) * self.rel_tol
 
     def __call__(self, lam, rnorm, x, opx, op_norm):
         return rnorm <= abs(lam) * self.rel_tol
