@@ -15,11 +15,11 @@ tolerance (tests/test_jdqmr_gpu.py).
 import numpy as np
 
 STOP_NAMES = {1: "maxit", 2: "converged", 3: "etol", 4: "linear", 5: "stagnation", 6: "breakdown",
-              7: "empty"}
+              7: "empty", 8: "rq_reversal"}
 
 
 def qmrs_correction(op, x, theta, r, q=None, dg=None, maxit=100, tol_e=0.0, etol_frac=0.0, lfac=0.1,
-                    sigma=None):
+                    sigma=None, direction=0):
     """Approximate solution t of P (op - sigma) P t = -r, P = I - Q Q^T with
     Q = q (orthonormal columns, x among them), preconditioner P K^-1 P with
     K = diag(dg).  Returns (t, info)."""
@@ -52,6 +52,7 @@ def qmrs_correction(op, x, theta, r, q=None, dg=None, maxit=100, tol_e=0.0, etol
     it = 0
     stop = 0 if (bb > 0.0 and maxit > 0) else 7
     eres = rnorm
+    rq_prev = theta
     history = []
     while stop == 0:
         w = op(d) - sigma * d
@@ -103,10 +104,15 @@ def qmrs_correction(op, x, theta, r, q=None, dg=None, maxit=100, tol_e=0.0, etol
         else:
             stall += 1
         history.append(eres)
+        rqv = sigma + rq
+        reversed_ = direction * (rqv - rq_prev) < 0.0
+        rq_prev = rqv
         if stop:
             pass
         elif not np.isfinite(eres) or not np.isfinite(tt):
             stop = 6
+        elif reversed_:
+            stop = 8
         elif eres <= tol_e:
             stop = 2
         elif eres <= etol_frac * rnorm:

@@ -26,6 +26,9 @@
 //   (Op - sigma) y = (theta - sigma + r.t) x - g            (x^T Op t = r.t)
 //   rho(y) - sigma = ((theta - sigma + r.t) - g.t) / (1 + |t|^2)
 //   |res(y)|^2     = ((theta - sigma + r.t)^2 + |g|^2) / (1 + |t|^2) - (rho - sigma)^2
+// For an extreme target (DIR = -1 smallest, +1 largest) the inner solve also
+// stops as soon as rho(y) moves away from that end of the spectrum: past that
+// point the iterate converges toward another eigenpair (RQI behaviour).
 #include "common.cuh"
 
 namespace svdsb {
@@ -35,7 +38,7 @@ namespace jd {
 enum : int {
   SIGMA = 0, TAU, THETA_PREV, RHO_PREV, ALPHA, GAMMA, ETA, BETA, C2, S2,
   RT, TT, GT, GG, ERES, ERES_BEST, IT, MAXIT, TOL_E, ETOL_FRAC, STOP, RITZ, RNORM, STALL,
-  SIGP, LFAC, BNORM,
+  SIGP, LFAC, BNORM, DIR, RQ_PREV,
   QW = 32,   // Q^T w   (QMAX)
   QZ = 64,   // Q^T z   (QMAX)
   NSTATE = 96
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(jd::kThreads) jd_init_kernel(
     S[jd::STALL] = 0.0;
     S[jd::ERES] = S[jd::RNORM];
     S[jd::ERES_BEST] = S[jd::RNORM];
+    S[jd::RQ_PREV] = S[jd::RITZ];
     S[jd::STOP] = (bb > 0.0 && S[jd::MAXIT] > 0.0) ? 0.0 : 7.0;
     for (int k = 0; k < jd::kQMax; ++k) S[jd::QZ + k] = (PRE && k < nq) ? tot[k] : 0.0;
   }
@@ -286,7 +290,13 @@ __global__ void __launch_bounds__(jd::kThreads) jd_k3_kernel(
     } else {
       S[jd::STALL] += 1.0;
     }
+    // Rayleigh quotient of x + t moving away from the wanted end of the
+    // spectrum: the inner iterate heads for another eigenpair
+    const double rqv = S[jd::SIGMA] + rq;
+    const bool reversed = S[jd::DIR] * (rqv - S[jd::RQ_PREV]) < 0.0;
+    S[jd::RQ_PREV] = rqv;
     if (!isfinite(eres) || !isfinite(tt)) stop = 6.0;
+    else if (reversed) stop = 8.0;
     else if (eres <= S[jd::TOL_E]) stop = 2.0;                        // eigenpair would converge
     else if (eres <= S[jd::ETOL_FRAC] * S[jd::RNORM]) stop = 3.0;     // ETolerance reached
     else if (sqrt(gg) <= S[jd::LFAC] * eres) stop = 4.0;              // linear residual below the plateau

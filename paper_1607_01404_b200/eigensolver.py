@@ -36,6 +36,7 @@ EXTRACT_REFINED = "refined_const_shift"
 PRACTICAL_FLOOR_FACTOR = 10.0          # eigensolver.py:43
 METHOD_GDK = "GD+k"                    # the reference's method in both stages
 METHOD_JDQMR = "JDQMR"                 # PRIMME's JDQMR; jdqmr.py
+JD_LOG = None                          # diagnostics: a list collects every inner solve
 _IMPROVE_FACTOR = 0.999                # eigensolver.py:47
 REORTH_FACTOR = 1.0 / np.sqrt(2.0)     # kernels.py:24
 DEFICIENT_TOL = 1e-14                  # kernels.py:28
@@ -1100,6 +1101,13 @@ class DavidsonSolver:
         return info
 
     # ------------------------------------------------------------ JDQMR
+    def _jd_direction(self):
+        if self.cfg.target == TARGET_LARGEST:
+            return 1
+        if self.cfg.target == TARGET_SMALLEST:
+            return -1
+        return 0
+
     def _jd_threshold(self, cand):
         """Eigen-residual at which the candidate would pass the outer test
         (the inner solve stops there)."""
@@ -1125,6 +1133,7 @@ class DavidsonSolver:
                 raise ValueError("JDQMR supports the point-Jacobi preconditioner or none")
             jd = self._jd = JdqmrInner(self.ctx, self.op, self.n, diag=diag,
                                        use_graph=self.use_graphs and not self.comm.distributed)
+            jd.log = JD_LOG
             self._jd_x = dv.new_block(self.n, 1)
             self._jd_out = dv.new_block(self.n, cfg.max_block_size)
         if self.comm.distributed:
@@ -1146,7 +1155,7 @@ class DavidsonSolver:
             dv.ts_gemm(self.ctx, self.v[:, :g], ycol.reshape(g, 1), self._jd_x)
             t, info = jd.solve(self._jd_x, cand.lam, r, cand.rnorm, against=self._against(), maxit=maxit,
                                tol_e=self._jd_threshold(cand), etol_frac=cfg.inner_etol_frac,
-                               lfac=cfg.inner_lfac)
+                               lfac=cfg.inner_lfac, direction=self._jd_direction())
             it = info["iterations"]
             self.stats.matvecs += it
             self.stats.inner_iterations += it

@@ -21,8 +21,9 @@ of x + t is tracked exactly from device dot products; the inner solve stops
 when it would satisfy the outer convergence test, when it has dropped below
 ``etol_frac`` times the outer residual (PRIMME's JDQMR_ETol rule; 0 = off),
 when the QMR residual falls below ``lfac`` times it (further inner steps
-cannot lower it), after 3 steps without improvement, or at
-``max_inner_iterations``.
+cannot lower it), when the Rayleigh quotient of x + t moves away from the
+wanted end of the spectrum (extreme targets), after 3 steps without
+improvement, or at ``max_inner_iterations``.
 """
 
 import ctypes
@@ -35,11 +36,11 @@ from . import device as dv
 from .device import DTYPE
 
 # state slots (csrc/jdqmr.cu, namespace jd)
-SIGMA, ERES, IT, MAXIT, TOL_E, ETOL_FRAC, STOP, RITZ, RNORM, LFAC = 0, 14, 16, 17, 18, 19, 20, 21, 22, 25
+SIGMA, ERES, IT, MAXIT, TOL_E, ETOL_FRAC, STOP, RITZ, RNORM, LFAC, DIR = 0, 14, 16, 17, 18, 19, 20, 21, 22, 25, 27
 NSTATE = 96
 QMAX = 32
 STOP_NAMES = {1: "maxit", 2: "converged", 3: "etol", 4: "linear", 5: "stagnation", 6: "breakdown",
-              7: "empty"}
+              7: "empty", 8: "rq_reversal"}
 
 
 class _Vecs(ctypes.Structure):
@@ -92,6 +93,7 @@ class JdqmrInner:
         self._graphs = {}
         self._per_apply = None   # counter advance of one operator application
         self.solves = 0
+        self.log = None          # list -> (theta, rnorm, iterations, reason, eres) per solve
         self.inner_iterations = 0
         self.launches = 0
 
@@ -140,7 +142,7 @@ class JdqmrInner:
         return _NativeGraph(ex.value), _lib.launch_count() - l0
 
     # ------------------------------------------------------------- solve
-    def solve(self, x, theta, r, rnorm, against=(), maxit=100, tol_e=0.0, etol_frac=0.0, lfac=0.1):
+    def solve(self, x, theta, r, rnorm, against=(), maxit=100, tol_e=0.0, etol_frac=0.0, lfac=0.1, direction=0):
         """Correction for the Ritz pair (theta, x) with residual r (device
         columns of length n).  Returns (t, info); t is a view of an internal
         buffer, valid until the next solve."""
@@ -159,6 +161,7 @@ class JdqmrInner:
         inp[SIGMA], inp[RITZ], inp[RNORM] = float(theta), float(theta), float(rnorm)
         inp[MAXIT], inp[TOL_E], inp[ETOL_FRAC], inp[LFAC] = float(max(int(maxit), 0)), float(tol_e), \
             float(etol_frac), float(lfac)
+        inp[DIR] = float(np.sign(direction))
         # the previous solve ended with a stream sync, so the pinned image is
         # free to rewrite; phase 0 fills every other slot
         with torch.cuda.stream(self.ctx.torch_stream):
@@ -190,6 +193,8 @@ class JdqmrInner:
         self.inner_iterations += it
         info = {"iterations": it, "stop": int(self.status[STOP]), "eres": float(self.status[ERES])}
         info["reason"] = STOP_NAMES.get(info["stop"], "?")
+        if self.log is not None:
+            self.log.append((float(theta), float(rnorm), it, info["reason"], info["eres"]))
         return self.t, info
 
     def _read_status(self):

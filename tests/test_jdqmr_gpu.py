@@ -57,14 +57,16 @@ def test_inner_solve_matches_oracle(pre, which, locked):
     r = host_c(x) - th * x
     q = np.concatenate([lock, x[:, None]], axis=1)
     dg = np.diag(cmat).copy() if pre else None
-    t_ref, info_ref = qmrs_correction(host_c, x, th, r, q=q, dg=dg, maxit=60)
+    direction = 1 if which == "largest" else -1
+    t_ref, info_ref = qmrs_correction(host_c, x, th, r, q=q, dg=dg, maxit=60, direction=direction)
     ctx = dv.context()
     diag = torch.from_numpy(dg).cuda() if pre else None
     outs = []
     for use_graph in (True, False):
         jd = JdqmrInner(ctx, cop, n, diag=diag, use_graph=use_graph)
         against = [dv.to_device_block(lock)] if locked else []
-        t, info = jd.solve(_dev(x), th, _dev(r), float(np.linalg.norm(r)), against=against, maxit=60)
+        t, info = jd.solve(_dev(x), th, _dev(r), float(np.linalg.norm(r)), against=against, maxit=60,
+                           direction=direction)
         outs.append((t.cpu().numpy().copy(), info))
     (tg, ig), (te, ie) = outs
     assert tg.tobytes() == te.tobytes(), "graph and step-by-step paths differ"

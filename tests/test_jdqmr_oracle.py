@@ -54,3 +54,20 @@ def test_empty_rhs():
     a, w, v, x, th, r = _problem()
     t, info = qmrs_correction(lambda z: a @ z, x, th, np.zeros_like(r), q=x[:, None])
     assert info["reason"] == "empty" and info["iterations"] == 0 and not t.any()
+
+
+@pytest.mark.parametrize("which", [0, 299])
+def test_rq_reversal_stop(which):
+    """Extreme targets: the Rayleigh quotient of x + t only moves toward the
+    wanted end while the inner solve runs; it stops at the first reversal."""
+    a, w, v, x, th, r = _problem(which=which, noise=0.3)
+    direction = -1 if which == 0 else 1
+    t, info = qmrs_correction(lambda z: a @ z, x, th, r, q=x[:, None], maxit=300, lfac=0.0,
+                              direction=direction)
+    assert info["reason"] == "rq_reversal"
+    # the correction still expands the search space usefully: Rayleigh-Ritz
+    # on span{x, t} moves past theta toward the wanted end
+    qb, _ = np.linalg.qr(np.stack([x, t], axis=1))
+    ritz = np.linalg.eigvalsh(qb.T @ a @ qb)
+    best = ritz[0] if direction < 0 else ritz[-1]
+    assert direction * (best - th) > 0

@@ -16,8 +16,22 @@ a = SparseMatrixCsr.from_coo(m, n, r, c, v)
 torch.cuda.synchronize(); t2 = time.perf_counter()
 print(f"{key} m={m} n={n} nnz={a.nnz} gen {t1-t0:.2f}s build {t2-t1:.2f}s", flush=True)
 pre = jacobi_precond_on_normal(a, side='auto') if wl.precond else None
+import os
+jd = os.environ.get("JD", "")          # "1", "2" or "12": stages that run JDQMR
+jdo = {"method": "JDQMR"}
+if os.environ.get("ETOL"):
+    jdo["inner_etol_frac"] = float(os.environ["ETOL"])
+if os.environ.get("LFAC"):
+    jdo["inner_lfac"] = float(os.environ["LFAC"])
+if os.environ.get("MAXIN"):
+    jdo["max_inner_iterations"] = int(os.environ["MAXIN"])
+opts = {}
+if "1" in jd:
+    opts["stage1_opts"] = dict(jdo)
+if "2" in jd:
+    opts["stage2_opts"] = dict(jdo)
 for rep in range(reps):
-    cfg = SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0, max_matvecs=budget)
+    cfg = SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0, max_matvecs=budget, **opts)
     l0 = _lib.launch_count()
     torch.cuda.synchronize(); t = time.perf_counter()
     res = svds_solve(a, precond=pre, cfg=cfg, return_device=True)
@@ -25,4 +39,4 @@ for rep in range(reps):
     s = res.stats
     print(json.dumps({"rep": rep, "sec": round(dt, 4), "sigma": res.sigma.tolist(), "rnorms_max": float(res.rnorms.max()),
         "conv": bool(res.converged.all()), "status": res.status, "mv1": s.stage1_matvecs, "mv2": s.stage2_matvecs,
-        "restarts": s.restarts, "iters": s.outer_iterations, "syncs": s.syncs, "graphs": s.graphs_captured, "launches": _lib.launch_count() - l0}), flush=True)
+        "restarts": s.restarts, "iters": s.outer_iterations, "inner": s.inner_iterations, "jd": jd, "jdo": jdo, "syncs": s.syncs, "graphs": s.graphs_captured, "launches": _lib.launch_count() - l0}), flush=True)
