@@ -76,8 +76,9 @@ def config_json(wl, m, n, nnz, world):
             "precond": "jacobi" if wl.precond else None, "seed_matrix": int(wl.name[1]), "seed_solver": 0,
             "parallelism": "row-sharded x%d (NCCL all-reduce / all-gather / reduce-scatter)" % world
             if world > 1 else "single",
-            "l2": "flushed before every timed step (256 MiB write); working set (~60 MB) is L2-resident "
-                  "within a solve"}
+            "l2": "flushed before every timed step (256 MiB write); the solve's working set (CSR A + A^T "
+                  "41 MB, basis V/W 56 MB, ...) does not stay L2-resident: warm-cache ncu shows the basis "
+                  "kernels reading their algorithmic bytes from DRAM (profiles/r01_warm_c2.json)"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -410,8 +411,8 @@ def iteration_kernels(a, pre, wl, peak, iters, step_ms, g=25):
                 traffic = byt
     roof = {"kernel": dom["kernel"], "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
-            "traffic_note": "ncu dram read+write per launch, cold L2 (profiles/traffic_%s.json); inside a "
-                            "solve the basis is L2-resident" % wl.name,
+            "traffic_note": "ncu dram read+write per launch, cold L2 (profiles/traffic_%s.json); warm-cache "
+                            "values inside the solve in profiles/r01_warm_c2.json" % wl.name,
             "algorithmic_bytes_per_launch": dom["algorithmic_bytes"], "avg_launch_us": dom["us_per_launch"],
             "share_of_step": dom["share_of_step"],
             "method": "CUDA events around a graph of %d back-to-back launches at basis size g=%d on this "
