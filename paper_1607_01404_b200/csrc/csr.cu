@@ -237,10 +237,14 @@ csr_tile_kernel(const int *__restrict__ tile_r, const int *__restrict__ row_ptr,
   } else {
     for (int cc = 0; cc < b; ++cc) {
       const double *xc = x + cc * ldx;
+      // all gathers issued before the first use (c[i] = 0 past the tile)
+      double xv[kPerThread];
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) xv[i] = __ldg(xc + c[i]);
 #pragma unroll
       for (int i = 0; i < kPerThread; ++i) {
         int k = t + i * kTileThreads;
-        if (k < nnz) prod[k] = dmul(v[i], __ldg(xc + c[i]));
+        if (k < nnz) prod[k] = dmul(v[i], xv[i]);
       }
       __syncthreads();
       if (t < nrows) {
@@ -311,10 +315,15 @@ __device__ __forceinline__ void pipe_tiles(int ntile, const int4 *__restrict__ i
     }
     // gather + products of the current tile
     const int nnz = cur.w - cur.z, nrows = cur.y - cur.x;
+    // all gathers issued before the first use (c[i] = 0 past the tile), so
+    // a thread keeps kPerThread loads in flight instead of one
+    double xg[kPerThread];
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) xg[i] = CG ? __ldcg(x + c[i]) : __ldg(x + c[i]);
 #pragma unroll
     for (int i = 0; i < kPerThread; ++i) {
       int k = t + i * kTileThreads;
-      if (k < nnz) prod[buf][k] = dmul(v[i], CG ? __ldcg(x + c[i]) : __ldg(x + c[i]));
+      if (k < nnz) prod[buf][k] = dmul(v[i], xg[i]);
     }
     if (t <= nrows) rps[buf][t] = rpa;
     if (t == 0 && nrows >= kTileThreads) rps[buf][kTileThreads] = rpb;
@@ -399,20 +408,36 @@ csr_tile_pipe_rows_kernel(int ntile, const int4 *__restrict__ info, const int *_
       issue(nxt, vn, cn, rna, rnb);
     }
     const int nnz = cur.w - cur.z, nrows = cur.y - cur.x;
+    if (b == 4) {
+      // one 256-bit gather per nonzero (rows are 32-byte aligned), issued in
+      // groups of four before their products (c[i] = 0 past the tile)
+#pragma unroll
+      for (int h = 0; h < kPerThread; h += 4) {
+        double xg[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double *xr = x + (int64_t)c[h + i] * 4;
+          asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+              : "=d"(xg[i][0]), "=d"(xg[i][1]), "=d"(xg[i][2]), "=d"(xg[i][3]) : "l"(xr));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int k = t + (h + i) * kTileThreads;
+          if (k < nnz) {
+            prod[k] = dmul(v[h + i], xg[i][0]);
+            prod[kTileNnz + k] = dmul(v[h + i], xg[i][1]);
+            prod[2 * kTileNnz + k] = dmul(v[h + i], xg[i][2]);
+            prod[3 * kTileNnz + k] = dmul(v[h + i], xg[i][3]);
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int i = 0; i < kPerThread; ++i) {
       int k = t + i * kTileThreads;
-      if (k < nnz) {
+      if (b != 4 && k < nnz) {
         const double *xr = x + (int64_t)c[i] * b;
-        if (b == 4) {
-          // one 256-bit gather per nonzero (rows are 32-byte aligned)
-          double x0, x1, x2, x3;
-          asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(x0), "=d"(x1), "=d"(x2), "=d"(x3) : "l"(xr));
-          prod[k] = dmul(v[i], x0);
-          prod[kTileNnz + k] = dmul(v[i], x1);
-          prod[2 * kTileNnz + k] = dmul(v[i], x2);
-          prod[3 * kTileNnz + k] = dmul(v[i], x3);
-        } else if (b == 2) {
+        if (b == 2) {
           double2 xv = __ldg(reinterpret_cast<const double2 *>(xr));
           prod[k] = dmul(v[i], xv.x);
           prod[kTileNnz + k] = dmul(v[i], xv.y);
@@ -544,19 +569,36 @@ csr_tile_bulk_kernel(int ntile, const int4 *__restrict__ info, const int *__rest
         const int s0 = prp[t] - ti.z;
         const int len = prp[t + 1] - prp[t];
         for (int j0 = 0; j0 < len; j0 += 8) {
+          // indices first, then all gathers, then the products: 8 loads in
+          // flight per thread (index 0 stands in past the row)
+          int cj[8];
+          double xg[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) cj[j] = (j0 + j < len) ? pc[s0 + j0 + j] : 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) xg[j] = __ldg(x + cj[j]);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            if (j0 + j < len) pv[s0 + j0 + j] = dmul(pv[s0 + j0 + j], __ldg(x + pc[s0 + j0 + j]));
+            if (j0 + j < len) pv[s0 + j0 + j] = dmul(pv[s0 + j0 + j], xg[j]);
           if (ROWS == 0) break;
         }
         y[ti.x + t] = accumulate ? fold_row_from(y[ti.x + t], pv + s0, len)
                                  : fold_row<ORDER, ROWS == 0>(pv + s0, len);
       }
     } else {
+      int ce[kPerThread];
+      double xg[kPerThread];
 #pragma unroll
       for (int i = 0; i < kPerThread; ++i) {
         const int e = t + i * kTileThreads;
-        if (e < nnz) pv[e] = dmul(pv[e], __ldg(x + pc[e]));
+        ce[i] = e < nnz ? pc[e] : 0;
+      }
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) xg[i] = __ldg(x + ce[i]);
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i) {
+        const int e = t + i * kTileThreads;
+        if (e < nnz) pv[e] = dmul(pv[e], xg[i]);
       }
       __syncthreads();
       if (t < nrows) {
