@@ -213,6 +213,43 @@ __device__ __forceinline__ bool last_cta(unsigned int *ticket) {
   return am_last;
 }
 
+// ------------------------------------------------ bulk copies (TMA engine)
+// cp.async.bulk global -> shared with completion counted on an mbarrier
+// (the non-tensor form of TMA): one thread moves whole tiles while the CTA
+// computes on the previous stage.
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// Streamed operands (read once per launch) are marked evict-first.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar,
+                                         uint64_t policy) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+               " [%0], [%1], %2, [%3], %4;"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n"
+               " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t policy;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  return policy;
+}
+
 // Grid size for row-streaming kernels: enough CTAs to fill the chip a few
 // times, never more than rows warrant.  Fixed for a given dim so the
 // reduction order (and so the result) is reproducible.

@@ -490,25 +490,6 @@ struct __align__(128) BulkStage {
   int rp[kTileRows + 1 + 8];
 };
 
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-// The matrix streams through L2 once per product: mark it evict-first so
-// the gathered vector x stays L2-resident.
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar,
-                                         uint64_t policy) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-               " [%0], [%1], %2, [%3], %4;"
-               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n"
-               " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-               " @!p bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-
 // ROWS: 0 = every tile row has <= 8 nonzeros, 1 = <= 32 (both: one thread
 // gathers and folds one row), 2 = longer rows (strided gathers, CTA barrier,
 // then the per-row folds).

@@ -240,7 +240,7 @@ def test_ts_gemm_inplace_matches_out_of_place(dim, g, s, rng):
             dv.ts_gemm(ctx, x[:, :2], dv.to_device_block(rng.standard_normal((2, 3))), x[:, :3])
 
 
-@pytest.mark.parametrize("dim", [50, 100003])
+@pytest.mark.parametrize("dim", [50, 100003, 250001])   # 250001: HBM-streamed bulk-copy path
 @pytest.mark.parametrize("p", [1, 11, 24])
 def test_ritz_residual(dim, p, rng):
     dv = _dev()
