@@ -336,6 +336,36 @@ int svdsb_h_symmetrize(int g, const double *gm, int64_t ldg, double *h,
                        int64_t ldh, void *stream);
 
 /* ------------------------------------------------------------------ */
+/* One single-column GD+k iteration, all launches in one call (the body of */
+/* the solver's captured iteration graph; eigensolver.py:563-700): fused   */
+/* CGS expansion of the candidate *ci into V[:, g], W[:, g] = A^T A V[:, g] */
+/* (csr, side as svdsb_apply_normal), H column, warm RR update            */
+/* (svdsb_syev_update with g0 / y0 / l0), Ritz residuals of p candidates, */
+/* status into pinned host memory.  See csrc/gdk.cu.                       */
+typedef struct svdsb_gdk_iter_args {
+  int64_t n;
+  double *v; int64_t ldv;          /* basis, n x (g+1) used */
+  double *w; int64_t ldw;          /* its image */
+  int g;                            /* columns before the expansion */
+  const double *rsrc; int64_t ldr;  /* candidate residual block */
+  const int *ci;                    /* device candidate index */
+  const double *d;                  /* Jacobi diagonal or NULL */
+  const double *yin; int64_t ldyin; /* Ritz coefficients (for the +k copy) */
+  int kk; double *prev; int64_t ldprev;
+  int passes; double *dgks;         /* DGKS state (8 doubles) */
+  const svdsb_csr *csr; int side; double *tmp; int64_t ldtmp;
+  double *hc; int64_t ldhc; double *h; int64_t ldh;
+  int g0; const double *y0; int64_t ldy0; const double *l0;
+  int order; double shift;
+  double *lout; double *yout; int64_t ldyout;
+  int p; double *rout; int64_t ldrout; double *rn2;
+  double *status_host;
+} svdsb_gdk_iter_args;
+
+int svdsb_gdk_iteration(svdsb_ctx *ctx, const svdsb_gdk_iter_args *args,
+                        void *stream);
+
+/* ------------------------------------------------------------------ */
 /* JDQMR inner solver (PRIMME's QMRs on the Jacobi-Davidson correction    */
 /* equation; the paper's stage-2 method, PAPER.md:765-767, 897 -- the      */
 /* reference runs GD+k only):                                */

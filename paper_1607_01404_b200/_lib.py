@@ -74,6 +74,7 @@ _PROTOS = [
     ("svdsb_qr_small", i32, [i32, i32, vp, i64, vp, i64, vp, i64, vp, i64, vp]),
     ("svdsb_h_insert", i32, [i32, i32, vp, i64, vp, i64, vp]),
     ("svdsb_h_symmetrize", i32, [i32, vp, i64, vp, i64, vp]),
+    ("svdsb_gdk_iteration", i32, [vp, vp, vp]),
     ("svdsb_jd_state_size", i32, []),
     ("svdsb_jd_phase", i32, [vp, i32, i64, vp, vp, i64, i32, vp, ctypes.c_uint64, vp]),
     ("svdsb_while_begin", i32, [vp, ctypes.POINTER(ctypes.c_uint64)]),
@@ -91,6 +92,18 @@ SVDSB_CSR_TRANSPOSE = 1
 ORDER_ASC, ORDER_DESC, ORDER_INTERIOR = 0, 1, 2
 SMALL_MAX = 64
 MAX_BLOCKS = 4
+
+
+class GdkIterArgs(ctypes.Structure):
+    """svdsb_gdk_iter_args (include/svdsb.h)."""
+    _fields_ = [("n", i64), ("v", vp), ("ldv", i64), ("w", vp), ("ldw", i64), ("g", i32),
+                ("rsrc", vp), ("ldr", i64), ("ci", vp), ("d", vp), ("yin", vp), ("ldyin", i64),
+                ("kk", i32), ("prev", vp), ("ldprev", i64), ("passes", i32), ("dgks", vp),
+                ("csr", vp), ("side", i32), ("tmp", vp), ("ldtmp", i64),
+                ("hc", vp), ("ldhc", i64), ("h", vp), ("ldh", i64),
+                ("g0", i32), ("y0", vp), ("ldy0", i64), ("l0", vp), ("order", i32), ("shift", f64),
+                ("lout", vp), ("yout", vp), ("ldyout", i64),
+                ("p", i32), ("rout", vp), ("ldrout", i64), ("rn2", vp), ("status_host", vp)]
 
 
 class NativeError(RuntimeError):

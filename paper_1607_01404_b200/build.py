@@ -18,7 +18,7 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libsvdsb.so")
 REPO = os.path.dirname(HERE)
 
-SOURCES = ["runtime.cu", "csr.cu", "dense.cu", "small.cu", "arrow.cu", "jdqmr.cu", "mmio.cpp"]
+SOURCES = ["runtime.cu", "csr.cu", "dense.cu", "small.cu", "arrow.cu", "jdqmr.cu", "gdk.cu", "mmio.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

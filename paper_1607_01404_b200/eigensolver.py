@@ -1329,6 +1329,27 @@ class DavidsonSolver:
         kk = max(self.cfg.plus_k, 1)
         d = self.precond.diagonal if self.precond is not None else None
         st = ws.dgks[sout]
+        nat = getattr(self.op, "native_normal", None)
+        if nat is not None and self._use_fused_cgs(g):
+            # the whole launch sequence in one native call (csrc/gdk.cu)
+            dev, side, inner = nat
+            tmp = dev.scratch(inner, 1)
+            gn = g + 1
+            y0 = y_in if kind == "prev" else None
+            a = _lib.GdkIterArgs(
+                n=self.n, v=self.v.data_ptr(), ldv=dv.ld_of(self.v), w=self.w.data_ptr(), ldw=dv.ld_of(self.w), g=g,
+                rsrc=ws.rbuf[sin].data_ptr(), ldr=dv.ld_of(ws.rbuf[sin]), ci=ws.ci.data_ptr(),
+                d=None if d is None else d.data_ptr(), yin=y_in.data_ptr(), ldyin=dv.ld_of(y_in), kk=kk,
+                prev=self.prev_d.data_ptr(), ldprev=dv.ld_of(self.prev_d), passes=self.SPEC_PASSES,
+                dgks=st.data_ptr(), csr=dev.handle, side=side, tmp=tmp.data_ptr(), ldtmp=dv.ld_of(tmp),
+                hc=ws.hc1.data_ptr(), ldhc=dv.ld_of(ws.hc1), h=self.h.data_ptr(), ldh=dv.ld_of(self.h),
+                g0=g0, y0=None if y0 is None else y0.data_ptr(), ldy0=dv.ld_of(y0) if y0 is not None else 1,
+                l0=None if y0 is None else l_in.data_ptr(), order=int(order), shift=float(shift),
+                lout=l_out.data_ptr(), yout=y_out.data_ptr(), ldyout=dv.ld_of(y_out), p=p,
+                rout=r_out.data_ptr(), ldrout=dv.ld_of(r_out), rn2=s_out.data_ptr(),
+                status_host=ws.status[sout].data_ptr())
+            _lib.call("svdsb_gdk_iteration", ctx.handle, ctypes.byref(a), ctx.stream)
+            return
         n_, ptrs, lds, cols, _ = dv._blk_args([self.v[:, :g]])
         if self._use_fused_cgs(g):
             # select + precondition + +k copy + device-decided CGS passes +

@@ -299,6 +299,8 @@ def make_normal_operator(a):
         op.svd_op = a
         op.kind = "normal"
         op.raw_into = raw_into
+        # for the native iteration entry point (svdsb_gdk_iteration)
+        op.native_normal = (dev, side, inner)
         # evaluated at capture / replay time: includes the scratch address
         op.graph_key = lambda: ("normal", dev.uid, side, dev.scratch(inner, 1).data_ptr())
         op.count_svd_matvecs = lambda cols: setattr(base, "n_matvecs", base.n_matvecs + 2 * cols)
