@@ -148,8 +148,20 @@ __device__ __forceinline__ void fold_parts(const double *partials, unsigned npar
       const double *pp = partials + (int64_t)t * nparts * per + k;
       double acc = 0.0;
       if (sl < S) {
-#pragma unroll 8
-        for (unsigned bx = sl; bx < nparts; bx += S) acc += pp[(int64_t)bx * per];
+        // 16 independent loads in flight per thread, summed in the same
+        // order as a plain strided loop (bx = sl, sl + S, ...)
+        constexpr int CH = 16;
+        for (unsigned b0 = sl; b0 < nparts; b0 += CH * S) {
+          double tv[CH];
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            const unsigned bx = b0 + q * S;
+            tv[q] = bx < nparts ? pp[(int64_t)bx * per] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < CH; ++q)
+            if (b0 + q * S < nparts) acc += tv[q];
+        }
       }
       red[threadIdx.x] = acc;
       __syncthreads();
@@ -168,8 +180,18 @@ __device__ __forceinline__ void fold_parts(const double *partials, unsigned npar
     const int t = o / per, kk = o % per;
     const double *pp = partials + (int64_t)t * nparts * per + kk;
     double s = 0.0;
-#pragma unroll 4
-    for (unsigned bx = lane; bx < nparts; bx += 32) s += pp[(int64_t)bx * per];
+    constexpr int CH = 8;
+    for (unsigned b0 = lane; b0 < nparts; b0 += CH * 32) {
+      double tv[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const unsigned bx = b0 + q * 32;
+        tv[q] = bx < nparts ? pp[(int64_t)bx * per] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q)
+        if (b0 + q * 32 < nparts) s += tv[q];
+    }
     s = warp_sum(s);
     if (lane == 0) emit(o, t, kk, s);
   }
