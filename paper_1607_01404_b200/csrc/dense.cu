@@ -629,7 +629,7 @@ project1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ cvec, dou
 
 // R = W Y - V Y diag(lam) for p <= PT candidates in one pass over V, W.
 template <int PT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, PT <= 16 ? 2 : 1)
 ritz_wide_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const double *__restrict__ w, int64_t ldw,
                  int g, const double *__restrict__ yc, int64_t ldyc, const double *__restrict__ lam, int p,
                  double *__restrict__ r, int64_t ldr, double *__restrict__ xo, int64_t ldx, double *__restrict__ oxo,
@@ -654,7 +654,31 @@ ritz_wide_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const d
       ax[j] = 0.0;
       aw[j] = 0.0;
     }
-    for (int i = 0; i < g; ++i) {
+    // basis columns in groups of RU, every load of a group issued before
+    // its FMAs (same FMA order as one column at a time)
+    constexpr int RU = PT <= 8 ? 8 : (PT <= 12 ? 4 : (PT <= 16 ? 2 : 1));
+    int i = 0;
+    for (; i + RU <= g; i += RU) {
+      double vv[RU], ww[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        vv[u] = __ldg(v + row + (int64_t)(i + u) * ldv);
+        ww[u] = __ldg(w + row + (int64_t)(i + u) * ldw);
+      }
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const double2 *yrow = reinterpret_cast<const double2 *>(ysh + (i + u) * PT);
+#pragma unroll
+        for (int j = 0; j < PT / 2; ++j) {
+          double2 cf = yrow[j];
+          ax[2 * j] = fma(vv[u], cf.x, ax[2 * j]);
+          aw[2 * j] = fma(ww[u], cf.x, aw[2 * j]);
+          ax[2 * j + 1] = fma(vv[u], cf.y, ax[2 * j + 1]);
+          aw[2 * j + 1] = fma(ww[u], cf.y, aw[2 * j + 1]);
+        }
+      }
+    }
+    for (; i < g; ++i) {
       double vv = __ldg(v + row + (int64_t)i * ldv);
       double ww = __ldg(w + row + (int64_t)i * ldw);
       const double2 *yrow = reinterpret_cast<const double2 *>(ysh + i * PT);
