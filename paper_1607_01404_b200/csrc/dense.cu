@@ -1010,7 +1010,7 @@ int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, c
       // latency-bound sizes (L2-scale N): one CTA per SM halves the partials
       // the last CTA folds (measured 12.4 -> 9.9 us on config 2)
       int gxv = grid_for(gram1_vec_kernel<AT>, dim, 0);
-      if (dim < (1 << 20) && gxv > kNumSMs) gxv = kNumSMs;
+      if (dim <= (1 << 18) && gxv > kNumSMs) gxv = kNumSMs;
       dim3 grid(gxv, (s.total + AT - 1) / AT, 1);
       SVDSB_LAUNCH_PDL(gram1_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, y, c, norms2, ctx->partials,
                        take_ticket(ctx), nullptr);
