@@ -533,6 +533,71 @@ gram1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, double *c
   });
 }
 
+// b = 4 Gram C = X^T Y (+ |Y_j|^2): two rows per thread with 16-byte loads,
+// AT basis columns per CTA row of the grid; every load of a row pair is
+// issued before its FMAs (the generic gram_kernel keeps ~4 in flight).
+template <int AT>
+__global__ void __launch_bounds__(kThreads)
+gram4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t ldy, double *c, int64_t ldc,
+                 double *norms2, double *partials, unsigned int *ticket) {
+  pdl_wait();
+  __shared__ const double *xp[AT];
+  const int ty = blockIdx.y;
+  const int i0 = ty * AT;
+  const int na = min(AT, xs.total - i0);
+  const bool want_norm = norms2 != nullptr && ty == 0;
+  if (threadIdx.x < AT) xp[threadIdx.x] = colset_ptr(xs, i0 + min((int)threadIdx.x, na - 1));
+  __syncthreads();
+  constexpr int NOUT = AT * 4 + 4;
+  double acc[NOUT];
+#pragma unroll
+  for (int k = 0; k < NOUT; ++k) acc[k] = 0.0;
+  RowRange rr = cta_rows_even(dim);
+  int64_t r = rr.r0 + 2 * threadIdx.x;
+  for (; r + 1 < rr.r1; r += 2 * kThreads) {
+    double2 yv[4], xv[AT];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) yv[j] = ldg2(y + r + (int64_t)j * ldy);
+#pragma unroll
+    for (int i = 0; i < AT; ++i) xv[i] = ldg2(xp[i] + r);  // columns past na re-read the last one
+#pragma unroll
+    for (int i = 0; i < AT; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fma(xv[i].x, yv[j].x, fma(xv[i].y, yv[j].y, acc[i * 4 + j]));
+    if (want_norm) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[AT * 4 + j] = fma(yv[j].x, yv[j].x, fma(yv[j].y, yv[j].y, acc[AT * 4 + j]));
+    }
+  }
+  if (r < rr.r1) {  // odd tail row
+    double yv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) yv[j] = __ldg(y + r + (int64_t)j * ldy);
+#pragma unroll
+    for (int i = 0; i < AT; ++i) {
+      const double xv = __ldg(xp[i] + r);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i * 4 + j] = fma(xv, yv[j], acc[i * 4 + j]);
+    }
+    if (want_norm) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[AT * 4 + j] = fma(yv[j], yv[j], acc[AT * 4 + j]);
+    }
+  }
+  pdl_trigger();
+  double *part = partials + ((int64_t)ty * gridDim.x + blockIdx.x) * NOUT;
+  cta_fold<NOUT>(acc, NOUT, part);
+  if (!last_cta(ticket)) return;
+  fold_parts(partials, gridDim.x, NOUT, (int)gridDim.y * NOUT, [&](int, int t, int k, double sum) {
+    if (k < AT * 4) {
+      const int i = t * AT + k / 4, j = k % 4;
+      if (k / 4 < min(AT, xs.total - t * AT)) c[i + (int64_t)j * ldc] = sum;
+    } else if (norms2 != nullptr && t == 0) {
+      norms2[k - AT * 4] = sum;
+    }
+  });
+}
+
 // One step of the iterated-CGS decision of kernels.py:115-127, on device.
 // st: [active, pass, collapses, orig, prev, final, |v|^2 before, |v|^2 after]
 __device__ __forceinline__ void dgks_decide(double *st) {
@@ -1015,6 +1080,13 @@ int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, c
       SVDSB_LAUNCH_PDL(gram1_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, y, c, norms2, ctx->partials,
                        take_ticket(ctx), nullptr);
     }
+    return SVDSB_OK;
+  } else if (b == 4 && colset_vec_ok(s) && aligned16(y) && ldy % 2 == 0) {
+    constexpr int AT = 8;
+    dim3 grid(grid_for(gram4_vec_kernel<AT>, dim, 0), (s.total + AT - 1) / AT, 1);
+    SVDSB_CHECK_ARG((int64_t)grid.x * grid.y * (AT * 4 + 4) <= kMaxPartials, "gram: workspace too small");
+    SVDSB_LAUNCH_PDL(gram4_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, y, ldy, c, ldc, norms2, ctx->partials,
+                     take_ticket(ctx));
     return SVDSB_OK;
   } else if (b == 1) {
     constexpr int AT = 32, BT = 1;
