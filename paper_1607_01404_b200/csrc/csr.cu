@@ -473,6 +473,128 @@ csr_tile_pipe_rows_kernel(int ntile, const int4 *__restrict__ info, const int *_
   }
 }
 
+// Forward b = 4 product for matrices whose rows are all short (<= 129 nnz,
+// e.g. config 4's A with 7-20 per row): one thread per row, no shared
+// memory and no CTA barrier.  The row's x-rows are gathered four at a time
+// (one 256-bit load each) and folded on the fly into the exact order of
+// fold_row<0> -- p0 + numpy pairwise(rest): the first 8 tail products seed 8
+// accumulators, whole blocks of 8 follow, the remainder is added to the
+// tree sum -- for the four columns as independent chains.
+__device__ __forceinline__ void gather4(const double *x, int c, double (&o)[4]) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(x + (int64_t)c * 4));
+}
+
+template <int YROW>
+__global__ void __launch_bounds__(kTileThreads, 2)
+csr_rowlane4_kernel(int64_t nrows, const int *__restrict__ row_ptr, const int *__restrict__ col,
+                    const double *__restrict__ val, const double *__restrict__ x, double *__restrict__ y,
+                    int64_t ldy) {
+  pdl_wait();
+  for (int64_t row = blockIdx.x * (int64_t)kTileThreads + threadIdx.x; row < nrows;
+       row += (int64_t)gridDim.x * kTileThreads) {
+    const int k0 = __ldg(row_ptr + row), k1 = __ldg(row_ptr + row + 1);
+    const int n = k1 - k0 - 1;  // tail length
+    double out[4] = {0.0, 0.0, 0.0, 0.0};
+    if (n >= 0) {
+      double p0[4];
+      {
+        double xv[4];
+        gather4(x, ld_stream(col + k0), xv);
+        const double v = ld_stream(val + k0);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) p0[c] = dmul(v, xv[c]);
+      }
+      const int t0 = k0 + 1;  // first tail element
+      if (n < 8) {
+        // numpy: tail < 8 summed left to right from 0
+        double r[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int i0 = 0; i0 < n; i0 += 4) {
+          double xv[4][4], vv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = t0 + min(i0 + u, n - 1);
+            vv[u] = ld_stream(val + k);
+            gather4(x, ld_stream(col + k), xv[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i0 + u < n) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) r[c] = dadd(r[c], dmul(vv[u], xv[u][c]));
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out[c] = n == 0 ? p0[c] : dadd(p0[c], r[c]);
+      } else {
+        double acc[4][8];
+        const int nb = n - (n % 8);
+        // block 0 seeds the accumulators, blocks 8.. add in order
+        for (int b0 = 0; b0 < nb; b0 += 8) {
+#pragma unroll
+          for (int h = 0; h < 8; h += 4) {
+            double xv[4][4], vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int k = t0 + b0 + h + u;
+              vv[u] = ld_stream(val + k);
+              gather4(x, ld_stream(col + k), xv[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const double pr = dmul(vv[u], xv[u][c]);
+                acc[c][h + u] = b0 == 0 ? pr : dadd(acc[c][h + u], pr);
+              }
+          }
+        }
+        double res[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double *a = acc[c];
+          res[c] = dadd(dadd(dadd(a[0], a[1]), dadd(a[2], a[3])), dadd(dadd(a[4], a[5]), dadd(a[6], a[7])));
+        }
+        for (int i0 = nb; i0 < n; i0 += 4) {
+          double xv[4][4], vv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = t0 + min(i0 + u, n - 1);
+            vv[u] = ld_stream(val + k);
+            gather4(x, ld_stream(col + k), xv[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i0 + u < n) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) res[c] = dadd(res[c], dmul(vv[u], xv[u][c]));
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out[c] = dadd(p0[c], res[c]);
+      }
+    }
+    if (YROW) {
+      double *yp = y + row * 4;
+      asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" :: "l"(yp), "d"(out[0]), "d"(out[1]), "d"(out[2]),
+                   "d"(out[3]) : "memory");
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) y[row + c * ldy] = out[c];
+    }
+  }
+  pdl_trigger();
+}
+
+static bool rowlane_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("SVDSB_SPMV_ROWLANE");
+    on = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 // ------------------------------------------------ bulk-copy tile pipeline
 // b = 1 SpMV with the matrix stream moved by the copy engine: each tile's
 // val / col / row_ptr ranges go global -> shared with cp.async.bulk
@@ -901,6 +1023,14 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
     if (b > 4) {
       set_error("row-major SpMV operands need block <= 4");
       return SVDSB_ERR_ARG;
+    }
+    if (ORDER == 0 && b == 4 && xrow && !acc && p.nlong == 0 && p.maxlen <= 129 && rowlane_on()) {
+      const int g = (int)std::min<int64_t>((p.rows + kTileThreads - 1) / kTileThreads, 2 * kNumSMs * 4);
+      if (yrow)
+        SVDSB_LAUNCH_PDL(csr_rowlane4_kernel<1>, g, kTileThreads, 0, st, p.rows, p.row_ptr, p.col, p.val, x, y, ldy);
+      else
+        SVDSB_LAUNCH_PDL(csr_rowlane4_kernel<0>, g, kTileThreads, 0, st, p.rows, p.row_ptr, p.col, p.val, x, y, ldy);
+      return SVDSB_OK;
     }
     if (p.ntile > 0 && xrow) {
       const size_t sm = sizeof(double) * 4 * kTileNnz + sizeof(int) * (kTileRows + 1);
