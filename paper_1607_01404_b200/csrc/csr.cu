@@ -21,6 +21,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <vector>
 
 #include <stdlib.h>
@@ -893,6 +895,39 @@ __global__ void csr_long_fixup_kernel(int nlong, const int *__restrict__ long_ro
 
 // ---------------------------------------------------------------- partition
 
+
+// SVDSB_TRACE=<ms>: print the host-side phases of a matrix assembly that
+// took longer than <ms> (diagnoses stalls in the e2e path)
+struct CreateTrace {
+  const char *what[32];
+  std::chrono::steady_clock::time_point t[32];
+  int n = 0;
+  double limit_ms = -1.0;
+  CreateTrace() {
+    const char *e = getenv("SVDSB_TRACE");
+    if (e) limit_ms = atof(e);
+    mark("start");
+  }
+  void mark(const char *w) {
+    if (limit_ms >= 0 && n < 32) {
+      what[n] = w;
+      t[n++] = std::chrono::steady_clock::now();
+    }
+  }
+  ~CreateTrace() {
+    if (limit_ms < 0 || n < 2) return;
+    auto ms = [&](int a, int b) { return std::chrono::duration<double, std::milli>(t[b] - t[a]).count(); };
+    if (ms(0, n - 1) < limit_ms) return;
+    fprintf(stderr, "[svdsb create %.1f ms]", ms(0, n - 1));
+    for (int i = 1; i < n; ++i) fprintf(stderr, " %s %.2f", what[i], ms(i - 1, i));
+    fprintf(stderr, "\n");
+  }
+};
+static thread_local CreateTrace *g_trace = nullptr;
+static inline void tmark(const char *w) {
+  if (g_trace) g_trace->mark(w);
+}
+
 // Device arrays of a CSR part carry kAllocPad bytes of slack: the bulk-copy
 // SpMV moves whole 16-byte granules, which can reach past the last element.
 constexpr size_t kAllocPad = 64;
@@ -1199,7 +1234,9 @@ static int build_transpose(const CsrPart &a, CsrPart &at, cudaStream_t st) {
     SVDSB_CUDA(palloc(&scan_tmp, scan_bytes, st));
     SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, at.row_ptr, (int)(at.rows + 1), st));
     bump_launches();
+    tmark("T launch");
     SVDSB_CUDA(cudaStreamSynchronize(st));
+    tmark("T sync");
     pfree(rows, st);
     pfree(idx, st);
     pfree(keys_out, st);
@@ -1212,6 +1249,7 @@ static int build_transpose(const CsrPart &a, CsrPart &at, cudaStream_t st) {
   SVDSB_CUDA(cudaMemcpyAsync(at.host_row_ptr.data(), at.row_ptr, sizeof(int) * (at.rows + 1),
                              cudaMemcpyDeviceToHost, st));
   SVDSB_CUDA(cudaStreamSynchronize(st));
+  tmark("T row_ptr d2h");
   return build_partition(at, st);
 }
 
@@ -1366,16 +1404,21 @@ static int build_blocked_transpose(svdsb_csr *h, cudaStream_t st) {
 }
 
 static int finish_create(svdsb_csr *h, int flags, cudaStream_t st) {
+  tmark("assembled");
   int rc = build_partition(h->a, st);
+  tmark("partition A");
   if (rc) return rc;
   if (flags & SVDSB_CSR_TRANSPOSE) {
     rc = build_transpose(h->a, h->at, st);
+    tmark("transpose");
     if (rc) return rc;
     h->has_t = true;
     rc = build_blocked_transpose(h, st);
+    tmark("blocked transpose");
     if (rc) return rc;
   }
   SVDSB_CUDA(cudaStreamSynchronize(st));
+  tmark("final sync");
   return SVDSB_OK;
 }
 
@@ -1449,6 +1492,9 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     return SVDSB_ERR_RANGE;
   }
   cudaStream_t st = as_stream(stream);
+  CreateTrace trace;
+  g_trace = &trace;
+  struct Unset { ~Unset() { g_trace = nullptr; } } unset_trace;
   svdsb_csr *h = new svdsb_csr();
   cudaGetDevice(&h->device);
   h->has_t = false;
@@ -1469,6 +1515,7 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     SVDSB_CUDA(palloc(&seg, 4 * (nt + 1), st));
     SVDSB_CUDA(palloc(&rowcnt, 4 * (m + 1), st));
     SVDSB_CUDA(cudaMemsetAsync(rowcnt, 0, 4 * (m + 1), st));
+    tmark("alloc");
     coo_keys_kernel<<<grid1(nt), 256, 0, st>>>(nt, n, rows, cols, key, idx);
     SVDSB_LAUNCHED();
     int nbits = bits_for(std::max<int64_t>(m * n, 2));
@@ -1487,10 +1534,12 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(stmp, sb, first, seg, (int)nt, st));
     bump_launches();
     int last_seg = 0, last_first = 0;
+    tmark("sort+scan launch");
     SVDSB_CUDA(cudaMemcpyAsync(&last_seg, seg + nt - 1, 4, cudaMemcpyDeviceToHost, st));
     SVDSB_CUDA(cudaMemcpyAsync(&last_first, first + nt - 1, 4, cudaMemcpyDeviceToHost, st));
     SVDSB_CUDA(cudaStreamSynchronize(st));
     nnz = (int64_t)last_seg + last_first;
+    tmark("sync nnz");
     SVDSB_CUDA(alloc_pad(&p.col, std::max<int64_t>(nnz, 1), st));
     SVDSB_CUDA(alloc_pad(&p.val, std::max<int64_t>(nnz, 1), st));
     coo_sum_kernel<<<grid1(nt), 256, 0, st>>>(nt, n, key_s, perm, first, seg, vals, p.col, p.val, rowcnt);
@@ -1501,7 +1550,9 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     SVDSB_CUDA(palloc(&stmp2, sb2, st));
     SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(stmp2, sb2, rowcnt, p.row_ptr, (int)(m + 1), st));
     bump_launches();
+    tmark("sum+scan launch");
     SVDSB_CUDA(cudaStreamSynchronize(st));
+    tmark("sum sync");
     pfree(key, st);
     pfree(key_s, st);
     pfree(idx, st);
@@ -1518,8 +1569,10 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
   }
   p.nnz = nnz;
   p.host_row_ptr.resize(m + 1);
+  tmark("free temps");
   SVDSB_CUDA(cudaMemcpyAsync(p.host_row_ptr.data(), p.row_ptr, 4 * (m + 1), cudaMemcpyDeviceToHost, st));
   SVDSB_CUDA(cudaStreamSynchronize(st));
+  tmark("row_ptr d2h");
   int rc = finish_create(h, flags, st);
   if (rc) {
     svdsb_csr_destroy(h);
