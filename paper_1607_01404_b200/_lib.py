@@ -27,6 +27,7 @@ _PROTOS = [
     ("svdsb_version", i32, []),
     ("svdsb_last_error", ctypes.c_char_p, []),
     ("svdsb_launch_count", i64, []),
+    ("svdsb_tune_set", ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     ("svdsb_note_launches", i64, [i64]),
     ("svdsb_d2h", i32, [vp, vp, ctypes.c_size_t, vp]),
     ("svdsb_stream_sync", i32, [vp]),

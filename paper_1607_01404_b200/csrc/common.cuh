@@ -84,6 +84,14 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 
 // Launch through launch_k and account for it (use inside int-returning
 // C-ABI functions).
+// Kernel-variant knobs for measurement tools (svdsb_tune_set); 0 selects
+// the default everywhere.  Key 0: forward b = 4 SpMV of short-row matrices
+// (0 sliced ELL, 2 warp-staged CSR, 1 thread-per-row from global, 3 four
+// lanes per row).
+// Key 1: b = 4 Gram grid order (0 interleaved, 2 column groups outermost).
+constexpr int kTuneKeys = 8;
+inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0};
+
 #define SVDSB_LAUNCH_PDL(...)                                             \
   do {                                                                    \
     cudaError_t e_ = ::svdsb::launch_k(__VA_ARGS__);                      \

@@ -55,6 +55,13 @@ struct CsrPart {
   double *chunk_part = nullptr;  // nchunk * kMaxB partial sums
   std::vector<int> host_row_ptr;
   int maxlen = 0;             // longest row handled by the tiles
+  // sliced ELL copy (slices of 32 rows, element j of row t of a slice at
+  // sell_ptr[slice] + 32 j + t) for the b = 4 forward product; built on
+  // first use
+  int64_t nslice = 0;
+  int64_t *sell_ptr = nullptr;  // nslice + 1
+  int *sell_col = nullptr;
+  double *sell_val = nullptr;
 };
 
 constexpr int kMaxB = 64;   // largest block handled by one matvec call
@@ -487,105 +494,335 @@ __device__ __forceinline__ void gather4(const double *x, int c, double (&o)[4]) 
       : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(x + (int64_t)c * 4));
 }
 
+// One row's four products in the exact fold_row<0> order; `src` supplies
+// the row's values / column ids (global memory or a warp's shared stage).
+template <typename Src>
+__device__ __forceinline__ void row4_fold(const Src &src, int k0, int k1, const double *__restrict__ x,
+                                          double (&out)[4]) {
+  const int n = k1 - k0 - 1;  // tail length
+#pragma unroll
+  for (int c = 0; c < 4; ++c) out[c] = 0.0;
+  if (n < 0) return;
+  double p0[4];
+  {
+    double xv[4];
+    gather4(x, src.c(k0), xv);
+    const double v = src.v(k0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) p0[c] = dmul(v, xv[c]);
+  }
+  const int t0 = k0 + 1;  // first tail element
+  if (n < 8) {
+    // numpy: tail < 8 summed left to right from 0
+    double r[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i0 = 0; i0 < n; i0 += 4) {
+      double xv[4][4], vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = t0 + min(i0 + u, n - 1);
+        vv[u] = src.v(k);
+        gather4(x, src.c(k), xv[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u < n) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) r[c] = dadd(r[c], dmul(vv[u], xv[u][c]));
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) out[c] = n == 0 ? p0[c] : dadd(p0[c], r[c]);
+    return;
+  }
+  double acc[4][8];
+  const int nb = n - (n % 8);
+  // block 0 seeds the accumulators, blocks 8.. add in order
+  for (int b0 = 0; b0 < nb; b0 += 8) {
+#pragma unroll
+    for (int h = 0; h < 8; h += 4) {
+      double xv[4][4], vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = t0 + b0 + h + u;
+        vv[u] = src.v(k);
+        gather4(x, src.c(k), xv[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double pr = dmul(vv[u], xv[u][c]);
+          acc[c][h + u] = b0 == 0 ? pr : dadd(acc[c][h + u], pr);
+        }
+    }
+  }
+  double res[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double *a = acc[c];
+    res[c] = dadd(dadd(dadd(a[0], a[1]), dadd(a[2], a[3])), dadd(dadd(a[4], a[5]), dadd(a[6], a[7])));
+  }
+  for (int i0 = nb; i0 < n; i0 += 4) {
+    double xv[4][4], vv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = t0 + min(i0 + u, n - 1);
+      vv[u] = src.v(k);
+      gather4(x, src.c(k), xv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u < n) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) res[c] = dadd(res[c], dmul(vv[u], xv[u][c]));
+      }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) out[c] = dadd(p0[c], res[c]);
+}
+
+template <int YROW>
+__device__ __forceinline__ void store_row4(double *__restrict__ y, int64_t ldy, int64_t row, const double (&out)[4]) {
+  if (YROW) {
+    double *yp = y + row * 4;
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" :: "l"(yp), "d"(out[0]), "d"(out[1]), "d"(out[2]),
+                 "d"(out[3]) : "memory");
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) y[row + c * ldy] = out[c];
+  }
+}
+
+struct GlobalRowSrc {
+  const double *__restrict__ val;
+  const int *__restrict__ col;
+  __device__ __forceinline__ double v(int k) const { return ld_stream(val + k); }
+  __device__ __forceinline__ int c(int k) const { return ld_stream(col + k); }
+};
+
+// k indexes the global nonzero; the stage holds [base, base + cap)
+struct StagedRowSrc {
+  const double *val;
+  const int *col;
+  int base;
+  __device__ __forceinline__ double v(int k) const { return val[k - base]; }
+  __device__ __forceinline__ int c(int k) const { return col[k - base]; }
+};
+
 template <int YROW>
 __global__ void __launch_bounds__(kTileThreads, 2)
 csr_rowlane4_kernel(int64_t nrows, const int *__restrict__ row_ptr, const int *__restrict__ col,
                     const double *__restrict__ val, const double *__restrict__ x, double *__restrict__ y,
                     int64_t ldy) {
   pdl_wait();
+  const GlobalRowSrc src{val, col};
   for (int64_t row = blockIdx.x * (int64_t)kTileThreads + threadIdx.x; row < nrows;
        row += (int64_t)gridDim.x * kTileThreads) {
-    const int k0 = __ldg(row_ptr + row), k1 = __ldg(row_ptr + row + 1);
-    const int n = k1 - k0 - 1;  // tail length
-    double out[4] = {0.0, 0.0, 0.0, 0.0};
-    if (n >= 0) {
-      double p0[4];
-      {
-        double xv[4];
-        gather4(x, ld_stream(col + k0), xv);
-        const double v = ld_stream(val + k0);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) p0[c] = dmul(v, xv[c]);
-      }
-      const int t0 = k0 + 1;  // first tail element
-      if (n < 8) {
-        // numpy: tail < 8 summed left to right from 0
-        double r[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int i0 = 0; i0 < n; i0 += 4) {
-          double xv[4][4], vv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int k = t0 + min(i0 + u, n - 1);
-            vv[u] = ld_stream(val + k);
-            gather4(x, ld_stream(col + k), xv[u]);
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (i0 + u < n) {
-#pragma unroll
-              for (int c = 0; c < 4; ++c) r[c] = dadd(r[c], dmul(vv[u], xv[u][c]));
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) out[c] = n == 0 ? p0[c] : dadd(p0[c], r[c]);
-      } else {
-        double acc[4][8];
-        const int nb = n - (n % 8);
-        // block 0 seeds the accumulators, blocks 8.. add in order
-        for (int b0 = 0; b0 < nb; b0 += 8) {
-#pragma unroll
-          for (int h = 0; h < 8; h += 4) {
-            double xv[4][4], vv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int k = t0 + b0 + h + u;
-              vv[u] = ld_stream(val + k);
-              gather4(x, ld_stream(col + k), xv[u]);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                const double pr = dmul(vv[u], xv[u][c]);
-                acc[c][h + u] = b0 == 0 ? pr : dadd(acc[c][h + u], pr);
-              }
-          }
-        }
-        double res[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const double *a = acc[c];
-          res[c] = dadd(dadd(dadd(a[0], a[1]), dadd(a[2], a[3])), dadd(dadd(a[4], a[5]), dadd(a[6], a[7])));
-        }
-        for (int i0 = nb; i0 < n; i0 += 4) {
-          double xv[4][4], vv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int k = t0 + min(i0 + u, n - 1);
-            vv[u] = ld_stream(val + k);
-            gather4(x, ld_stream(col + k), xv[u]);
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (i0 + u < n) {
-#pragma unroll
-              for (int c = 0; c < 4; ++c) res[c] = dadd(res[c], dmul(vv[u], xv[u][c]));
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) out[c] = dadd(p0[c], res[c]);
+    double out[4];
+    row4_fold(src, __ldg(row_ptr + row), __ldg(row_ptr + row + 1), x, out);
+    store_row4<YROW>(y, ldy, row, out);
+  }
+  pdl_trigger();
+}
+
+// Warp-staged variant: a warp takes 32 consecutive rows, copies their
+// values / column ids global -> shared with coalesced loads (instead of
+// each thread walking its own row, which touches 32 sectors per warp load
+// and fetches every sector from L2 up to four times), then each lane folds
+// its row from the stage exactly as csr_rowlane4_kernel does.  Row groups
+// longer than the stage fall back to the global walk.
+constexpr int kWarpStage = 768;  // nonzeros per warp stage (9 KB)
+
+template <int YROW>
+__global__ void __launch_bounds__(kTileThreads, 2)
+csr_warprows4_kernel(int64_t nrows, const int *__restrict__ row_ptr, const int *__restrict__ col,
+                     const double *__restrict__ val, const double *__restrict__ x, double *__restrict__ y,
+                     int64_t ldy) {
+  extern __shared__ __align__(16) unsigned char wr_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double *sv = reinterpret_cast<double *>(wr_smem) + w * kWarpStage;
+  int *sc = reinterpret_cast<int *>(wr_smem + sizeof(double) * kWarpStage * (kTileThreads / 32)) + w * kWarpStage;
+  const int64_t ngroups = (nrows + 31) >> 5;
+  const int64_t wstride = (int64_t)gridDim.x * (kTileThreads / 32);
+  pdl_wait();
+  for (int64_t grp = blockIdx.x * (int64_t)(kTileThreads / 32) + w; grp < ngroups; grp += wstride) {
+    const int64_t row = (grp << 5) + lane;
+    const int64_t rcl = row < nrows ? row : nrows;
+    const int k0 = __ldg(row_ptr + rcl);
+    int k1 = __shfl_down_sync(0xffffffffu, k0, 1);
+    if (lane == 31) k1 = __ldg(row_ptr + (row + 1 < nrows ? row + 1 : nrows));
+    const int s = __shfl_sync(0xffffffffu, k0, 0);
+    const int e = __shfl_sync(0xffffffffu, k1, 31);
+    double out[4];
+    // a group longer than the stage is read straight from global memory
+    // (same fold; generic loads)
+    const bool staged = e - s <= kWarpStage;
+    if (staged) {
+      const int len = e - s;
+#pragma unroll 4
+      for (int k = lane; k < len; k += 32) {
+        sv[k] = ld_stream(val + s + k);
+        sc[k] = ld_stream(col + s + k);
       }
     }
-    if (YROW) {
-      double *yp = y + row * 4;
-      asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" :: "l"(yp), "d"(out[0]), "d"(out[1]), "d"(out[2]),
-                   "d"(out[3]) : "memory");
-    } else {
+    __syncwarp();
+    const StagedRowSrc src{staged ? sv : val, staged ? sc : col, staged ? s : 0};
+    if (row < nrows) {
+      row4_fold(src, k0, k1, x, out);
+      store_row4<YROW>(y, ldy, row, out);
+    }
+    __syncwarp();
+  }
+  pdl_trigger();
+}
+
+// Quad variant: four lanes per row, one block column each, eight rows per
+// warp.  The four lanes of a row gather the same 32-byte x row (one sector
+// per row per warp load) and each folds one column in the fold_row<0>
+// order with scalar registers, so the kernel runs at high occupancy and
+// keeps eight gathers in flight per lane.  Values / column ids of the
+// warp's eight rows are staged through shared memory with coalesced loads.
+constexpr int kQuadStage = 256;  // nonzeros per warp stage (8 rows)
+
+template <int YROW>
+__global__ void __launch_bounds__(kTileThreads, 3)
+csr_quad4_kernel(int64_t nrows, const int *__restrict__ row_ptr, const int *__restrict__ col,
+                 const double *__restrict__ val, const double *__restrict__ x, double *__restrict__ y,
+                 int64_t ldy) {
+  __shared__ double qv[kTileThreads / 32][kQuadStage];
+  __shared__ int qc[kTileThreads / 32][kQuadStage];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int rr = lane >> 2, cc = lane & 3;
+  const int64_t ngroups = (nrows + 7) >> 3;
+  const int64_t wstride = (int64_t)gridDim.x * (kTileThreads / 32);
+  const double *xc = x + cc;
+  pdl_wait();
+  for (int64_t grp = blockIdx.x * (int64_t)(kTileThreads / 32) + w; grp < ngroups; grp += wstride) {
+    const int64_t r0 = grp << 3;
+    int rpv = 0;
+    if (lane <= 8) rpv = __ldg(row_ptr + (r0 + lane < nrows ? r0 + lane : nrows));
+    const int k0 = __shfl_sync(0xffffffffu, rpv, rr);
+    const int k1 = __shfl_sync(0xffffffffu, rpv, rr + 1);
+    const int s = __shfl_sync(0xffffffffu, rpv, 0);
+    const int e = __shfl_sync(0xffffffffu, rpv, 8);
+    const bool staged = e - s <= kQuadStage;
+    if (staged) {
+      const int len = e - s;
+#pragma unroll 4
+      for (int k = lane; k < len; k += 32) {
+        qv[w][k] = ld_stream(val + s + k);
+        qc[w][k] = ld_stream(col + s + k);
+      }
+    }
+    __syncwarp();
+    // generic pointers: the stage, or global memory for an oversized group
+    const double *vp = staged ? &qv[w][0] : val + s;
+    const int *cp = staged ? &qc[w][0] : col + s;
+    const int a0 = k0 - s;           // row start within the group
+    const int n = k1 - k0 - 1;       // tail length
+    double out = 0.0;
+    if (n >= 0) {
+      const double p0 = dmul(vp[a0], __ldg(xc + (int64_t)cp[a0] * 4));
+      const int t0 = a0 + 1;
+      double res;
+      int i = 0;
+      if (n < 8) {
+        res = 0.0;
+      } else {
+        double acc[8];
+        const int nb = n - (n % 8);
+        for (; i < nb; i += 8) {
+          double xg[8], vv[8];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) y[row + c * ldy] = out[c];
+          for (int j = 0; j < 8; ++j) {
+            vv[j] = vp[t0 + i + j];
+            xg[j] = __ldg(xc + (int64_t)cp[t0 + i + j] * 4);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const double pr = dmul(vv[j], xg[j]);
+            acc[j] = i == 0 ? pr : dadd(acc[j], pr);
+          }
+        }
+        res = dadd(dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3])), dadd(dadd(acc[4], acc[5]), dadd(acc[6], acc[7])));
+      }
+      // remainder (< 8 terms) left to right -- the whole tail when n < 8
+      if (i < n) {
+        double xg[7], vv[7];
+#pragma unroll
+        for (int j = 0; j < 7; ++j) {
+          const int k = t0 + min(i + j, n - 1);
+          vv[j] = vp[k];
+          xg[j] = __ldg(xc + (int64_t)cp[k] * 4);
+        }
+#pragma unroll
+        for (int j = 0; j < 7; ++j)
+          if (i + j < n) res = dadd(res, dmul(vv[j], xg[j]));
+      }
+      out = n == 0 ? p0 : dadd(p0, res);
+    }
+    const int64_t row = r0 + rr;
+    if (row < nrows) {
+      if (YROW)
+        y[row * 4 + cc] = out;
+      else
+        y[row + cc * ldy] = out;
+    }
+    __syncwarp();
+  }
+  pdl_trigger();
+}
+
+// Sliced ELL (SELL-32) forward product for b = 4: lane t of a warp owns
+// row t of a 32-row slice and reads element j of its row at
+// base + 32 j + t, so every value / index load of the warp is one
+// contiguous 256 / 128-byte segment -- no shared-memory staging and no
+// bank conflicts.  The fold is row4_fold's, so results are bit-identical
+// to the CSR kernels.
+struct SellRowSrc {
+  const double *__restrict__ val;
+  const int *__restrict__ col;
+  int64_t base;  // slice base + t - 32 k0 (element k sits at base + 32 k)
+  __device__ __forceinline__ double v(int k) const { return ld_stream(val + base + 32 * (int64_t)k); }
+  __device__ __forceinline__ int c(int k) const { return ld_stream(col + base + 32 * (int64_t)k); }
+};
+
+template <int YROW>
+__global__ void __launch_bounds__(kTileThreads, 2)
+csr_sell4_kernel(int64_t nrows, int64_t nslice, const int *__restrict__ row_ptr, const int64_t *__restrict__ sell_ptr,
+                 const int *__restrict__ col, const double *__restrict__ val, const double *__restrict__ x,
+                 double *__restrict__ y, int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * (kTileThreads / 32);
+  pdl_wait();
+  for (int64_t sl = blockIdx.x * (int64_t)(kTileThreads / 32) + (threadIdx.x >> 5); sl < nslice; sl += wstride) {
+    const int64_t row = (sl << 5) + lane;
+    if (row < nrows) {
+      const int k0 = __ldg(row_ptr + row), k1 = __ldg(row_ptr + row + 1);
+      const SellRowSrc src{val, col, __ldg(sell_ptr + sl) + lane - 32 * (int64_t)k0};
+      double out[4];
+      row4_fold(src, k0, k1, x, out);
+      store_row4<YROW>(y, ldy, row, out);
     }
   }
   pdl_trigger();
+}
+
+__global__ void sell_fill_kernel(int64_t nrows, const int *__restrict__ row_ptr, const int *__restrict__ col,
+                                 const double *__restrict__ val, const int64_t *__restrict__ sell_ptr,
+                                 int *__restrict__ scol, double *__restrict__ sval) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= nrows) return;
+  const int64_t sl = row >> 5;
+  const int t = (int)(row & 31);
+  const int k0 = row_ptr[row], k1 = row_ptr[row + 1];
+  const int64_t base = sell_ptr[sl] + t;
+  const int w = (int)((sell_ptr[sl + 1] - sell_ptr[sl]) >> 5);
+  for (int j = 0; j < w; ++j) {
+    const bool in = k0 + j < k1;
+    scol[base + 32 * (int64_t)j] = in ? col[k0 + j] : 0;
+    sval[base + 32 * (int64_t)j] = in ? val[k0 + j] : 0.0;
+  }
 }
 
 static bool rowlane_on() {
@@ -980,6 +1217,9 @@ static void free_part(CsrPart &p) {
   pfree(p.long_cptr, nullptr);
   pfree(p.chunk_nz, nullptr);
   pfree(p.chunk_part, nullptr);
+  pfree(p.sell_ptr, nullptr);
+  pfree(p.sell_col, nullptr);
+  pfree(p.sell_val, nullptr);
   p = CsrPart();
 }
 
@@ -990,6 +1230,47 @@ static int upload(T **dst, const std::vector<T> &src, cudaStream_t st) {
   if (!src.empty())
     SVDSB_CUDA(cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, st));
   return SVDSB_OK;
+}
+
+// Sliced ELL copy of a part (see csr_sell4_kernel): slice widths from the
+// host row pointer, device fill.  Padding entries (column 0, value 0) are
+// never read: a lane stops at its row's length.
+static int build_sell(CsrPart &p, cudaStream_t st) {
+  const std::vector<int> &rp = p.host_row_ptr;
+  const int64_t ns = (p.rows + 31) / 32;
+  std::vector<int64_t> sp(ns + 1, 0);
+  for (int64_t sl = 0; sl < ns; ++sl) {
+    int w = 0;
+    for (int64_t r = 32 * sl; r < std::min(p.rows, 32 * sl + 32); ++r) w = std::max(w, rp[r + 1] - rp[r]);
+    sp[sl + 1] = sp[sl] + 32 * (int64_t)w;
+  }
+  int64_t *dsp = nullptr;
+  int rc;
+  if ((rc = upload(&dsp, sp, st))) return rc;
+  int *scol = nullptr;
+  double *sval = nullptr;
+  if (alloc_pad(&scol, std::max<int64_t>(sp[ns], 1), st) != cudaSuccess ||
+      alloc_pad(&sval, std::max<int64_t>(sp[ns], 1), st) != cudaSuccess) {
+    pfree(dsp, st);
+    pfree(scol, st);
+    set_error("sliced-ELL allocation failed");
+    return SVDSB_ERR_ALLOC;
+  }
+  if (p.rows > 0) {
+    sell_fill_kernel<<<(unsigned)((p.rows + 255) / 256), 256, 0, st>>>(p.rows, p.row_ptr, p.col, p.val, dsp, scol,
+                                                                       sval);
+    SVDSB_LAUNCHED();
+  }
+  p.nslice = ns;
+  p.sell_ptr = dsp;
+  p.sell_col = scol;
+  p.sell_val = sval;
+  return SVDSB_OK;
+}
+
+static bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
 }
 
 // Tile the rows (host; row_ptr already on host in p.host_row_ptr).
@@ -1058,6 +1339,37 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
     if (b > 4) {
       set_error("row-major SpMV operands need block <= 4");
       return SVDSB_ERR_ARG;
+    }
+    if (ORDER == 0 && b == 4 && xrow && !acc && p.nlong == 0 && p.maxlen <= 129 && rowlane_on() &&
+        g_tune[0] == 0) {
+      // sliced-ELL copy, built on the first uncaptured call
+      if (!p.sell_val && !capturing(st)) {
+        int rc = build_sell(const_cast<CsrPart &>(p), st);
+        if (rc) return rc;
+      }
+      if (p.sell_val) {
+        auto k = yrow ? csr_sell4_kernel<1> : csr_sell4_kernel<0>;
+        const int g = (int)std::min<int64_t>((p.nslice + 7) / 8, pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
+        SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.rows, p.nslice, p.row_ptr, p.sell_ptr, p.sell_col, p.sell_val, x,
+                         y, ldy);
+        return SVDSB_OK;
+      }
+    }
+    if (ORDER == 0 && b == 4 && xrow && !acc && p.nlong == 0 && p.maxlen <= 129 && rowlane_on() &&
+        g_tune[0] == 3) {  // measurement variant (slower on config 4)
+      auto k = yrow ? csr_quad4_kernel<1> : csr_quad4_kernel<0>;
+      const int g = (int)std::min<int64_t>((p.rows + 63) / 64, pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
+      SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.rows, p.row_ptr, p.col, p.val, x, y, ldy);
+      return SVDSB_OK;
+    }
+    if (ORDER == 0 && b == 4 && xrow && !acc && p.nlong == 0 && p.maxlen <= 129 && rowlane_on() &&
+        g_tune[0] != 1) {  // 2 (or no sliced-ELL copy); 1 selects the thread-per-row walk
+      const size_t sm = (sizeof(double) + sizeof(int)) * kWarpStage * (kTileThreads / 32);
+      auto k = yrow ? csr_warprows4_kernel<1> : csr_warprows4_kernel<0>;
+      const int g = (int)std::min<int64_t>((p.rows + kTileThreads - 1) / kTileThreads,
+                                           pipe_rows_grid(reinterpret_cast<const void *>(k), sm));
+      SVDSB_LAUNCH_PDL(k, g, kTileThreads, sm, st, p.rows, p.row_ptr, p.col, p.val, x, y, ldy);
+      return SVDSB_OK;
     }
     if (ORDER == 0 && b == 4 && xrow && !acc && p.nlong == 0 && p.maxlen <= 129 && rowlane_on()) {
       const int g = (int)std::min<int64_t>((p.rows + kTileThreads - 1) / kTileThreads, 2 * kNumSMs * 4);

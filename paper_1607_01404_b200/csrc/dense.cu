@@ -472,13 +472,14 @@ __global__ void axpby_kernel(int64_t dim, int b, double alpha, const double *x, 
 // Used when every base pointer is 16-byte aligned and every leading
 // dimension is even (always true for blocks allocated by the package).
 
-__device__ __forceinline__ RowRange cta_rows_even(int64_t dim) {
-  int64_t per = (dim + gridDim.x - 1) / gridDim.x;
+__device__ __forceinline__ RowRange cta_rows_even(int64_t dim, int bx, int nx) {
+  int64_t per = (dim + nx - 1) / nx;
   per += per & 1;
-  int64_t r0 = (int64_t)blockIdx.x * per;
+  int64_t r0 = (int64_t)bx * per;
   int64_t r1 = min(dim, r0 + per);
   return {r0, r1};
 }
+__device__ __forceinline__ RowRange cta_rows_even(int64_t dim) { return cta_rows_even(dim, blockIdx.x, gridDim.x); }
 
 __device__ __forceinline__ double2 ldg2(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
 
@@ -539,10 +540,15 @@ gram1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, double *c
 template <int AT>
 __global__ void __launch_bounds__(kThreads)
 gram4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t ldy, double *c, int64_t ldc,
-                 double *norms2, double *partials, unsigned int *ticket) {
+                 double *norms2, double *partials, unsigned int *ticket, int ny) {
   pdl_wait();
   __shared__ const double *xp[AT];
-  const int ty = blockIdx.y;
+  // ny > 0: one-dimensional grid with the ny column groups of a row range
+  // on consecutive CTAs, so they stream the same y rows together (L2 hits)
+  const int ty = ny ? blockIdx.x % ny : blockIdx.y;
+  const int bx = ny ? blockIdx.x / ny : blockIdx.x;
+  const int nx = ny ? gridDim.x / ny : gridDim.x;
+  const int nty = ny ? ny : gridDim.y;
   const int i0 = ty * AT;
   const int na = min(AT, xs.total - i0);
   const bool want_norm = norms2 != nullptr && ty == 0;
@@ -552,7 +558,7 @@ gram4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t l
   double acc[NOUT];
 #pragma unroll
   for (int k = 0; k < NOUT; ++k) acc[k] = 0.0;
-  RowRange rr = cta_rows_even(dim);
+  RowRange rr = cta_rows_even(dim, bx, nx);
   int64_t r = rr.r0 + 2 * threadIdx.x;
   for (; r + 1 < rr.r1; r += 2 * kThreads) {
     double2 yv[4], xv[AT];
@@ -585,10 +591,10 @@ gram4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t l
     }
   }
   pdl_trigger();
-  double *part = partials + ((int64_t)ty * gridDim.x + blockIdx.x) * NOUT;
+  double *part = partials + ((int64_t)ty * nx + bx) * NOUT;
   cta_fold<NOUT>(acc, NOUT, part);
   if (!last_cta(ticket)) return;
-  fold_parts(partials, gridDim.x, NOUT, (int)gridDim.y * NOUT, [&](int, int t, int k, double sum) {
+  fold_parts(partials, nx, NOUT, nty * NOUT, [&](int, int t, int k, double sum) {
     if (k < AT * 4) {
       const int i = t * AT + k / 4, j = k % 4;
       if (k / 4 < min(AT, xs.total - t * AT)) c[i + (int64_t)j * ldc] = sum;
@@ -1148,10 +1154,16 @@ int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, c
     return SVDSB_OK;
   } else if (b == 4 && colset_vec_ok(s) && aligned16(y) && ldy % 2 == 0) {
     constexpr int AT = 8;
-    dim3 grid(grid_for(gram4_vec_kernel<AT>, dim, 0), (s.total + AT - 1) / AT, 1);
+    const int ny = (s.total + AT - 1) / AT;
+    dim3 grid(grid_for(gram4_vec_kernel<AT>, dim, 0), ny, 1);
     SVDSB_CHECK_ARG((int64_t)grid.x * grid.y * (AT * 4 + 4) <= kMaxPartials, "gram: workspace too small");
-    SVDSB_LAUNCH_PDL(gram4_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, y, ldy, c, ldc, norms2, ctx->partials,
-                     take_ticket(ctx));
+    if (g_tune[1] != 2) {  // 2: column groups outermost (the slower order)
+      SVDSB_LAUNCH_PDL(gram4_vec_kernel<AT>, dim3(grid.x * ny, 1, 1), kThreads, 0, st, dim, s, y, ldy, c, ldc, norms2,
+                       ctx->partials, take_ticket(ctx), ny);
+    } else {
+      SVDSB_LAUNCH_PDL(gram4_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, y, ldy, c, ldc, norms2, ctx->partials,
+                       take_ticket(ctx), 0);
+    }
     return SVDSB_OK;
   } else if (b == 1) {
     constexpr int AT = 32, BT = 1;

@@ -45,6 +45,12 @@ int64_t svdsb_launch_count(void) { return svdsb::g_launches.load(); }
 
 int64_t svdsb_note_launches(int64_t n) { return svdsb::bump_launches((int)n); }
 
+int svdsb_tune_set(int key, int value) {
+  if (key < 0 || key >= svdsb::kTuneKeys) return SVDSB_ERR_ARG;
+  svdsb::g_tune[key] = value;
+  return SVDSB_OK;
+}
+
 int svdsb_d2h(void *dst_host, const void *src, size_t bytes, void *stream) {
   if (bytes == 0) return SVDSB_OK;
   SVDSB_CUDA(cudaMemcpyAsync(dst_host, src, bytes, cudaMemcpyDeviceToHost, svdsb::as_stream(stream)));

@@ -94,6 +94,54 @@ def test_spmv_bit_exact(m, n, nnz, b, rng):
     assert np.array_equal(got_t, want_t)
 
 
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_spmv_forward_b4_variants_bit_exact(variant, rng):
+    """Forward b = 4 products of short-row matrices (sliced ELL, warp-staged
+    CSR, thread-per-row, four lanes per row; svdsb_tune_set key 0) against
+    the oracle: ragged rows of 0..120 nonzeros (tails below, at and above
+    numpy's 8-term block), a row count that is not a multiple of 32, and
+    32-row groups larger than the warp stage (global fallback)."""
+    from paper_1607_01404_b200 import _lib
+    m, n = 4133, 3001
+    lens = rng.integers(0, 24, m)
+    lens[rng.random(m) < 0.02] = 0
+    lens[1000:1064] = rng.integers(90, 121, 64)
+    rows = np.repeat(np.arange(m), lens)
+    cols = rng.integers(0, n, rows.size)
+    vals = rng.standard_normal(rows.size) * 10.0 ** rng.uniform(-3, 3, rows.size)
+    a, (rp, ci, va) = _csr(m, n, rows, cols, vals)
+    x = rng.standard_normal((n, 4)) * 10.0 ** rng.uniform(-3, 3, (n, 4))
+    try:
+        _lib.call("svdsb_tune_set", 0, variant)
+        got = _spmv_dev(a, x, False)
+    finally:
+        _lib.call("svdsb_tune_set", 0, 0)
+    assert np.array_equal(got, ocsr.spmv(m, n, rp, ci, va, x))
+
+
+@pytest.mark.parametrize("order", [0, 2])
+def test_gram_b4_grid_orders(order, rng):
+    """b = 4 Gram in both grid orders (svdsb_tune_set key 1) against numpy,
+    column counts that leave a partial group of eight."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    dim = 200003
+    a = rng.standard_normal((dim, 35))
+    y = rng.standard_normal((dim, 4))
+    X, Y = dv.to_device_block(a), dv.to_device_block(y)
+    C = dv.small_matrix(35, 4)
+    nrm = torch.zeros(4, dtype=torch.float64, device=ctx.device)
+    try:
+        _lib.call("svdsb_tune_set", 1, order)
+        dv.gram(ctx, dim, [X], Y, C, norms2=nrm)
+    finally:
+        _lib.call("svdsb_tune_set", 1, 0)
+    want = a.T @ y
+    assert np.abs(dv.to_host(C) - want).max() <= 1e-13 * np.abs(want).max() * np.sqrt(dim)
+    assert np.allclose(nrm.cpu().numpy(), (y ** 2).sum(0), rtol=1e-13)
+
+
 def test_spmv_bulk_copy_path_bit_exact(rng):
     """Matrices of >= 64 MB stream through the cp.async.bulk tile ring
     (csr_tile_bulk_kernel); it must reproduce the reference's summation
