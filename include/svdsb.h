@@ -69,6 +69,11 @@ int svdsb_stream_sync(void *stream);
  * shape and replays it (eigensolver.py:563-700's per-iteration kernels). */
 int svdsb_graph_begin(void *stream);
 int svdsb_graph_end(void *stream, void **exec_out);
+/* Ends the capture and, when exec_in is not NULL, updates that executable
+ * graph in place with the captured one (same topology -- e.g. the same
+ * iteration on a new matrix of the same shape); falls back to a fresh
+ * instantiation (*exec_out != exec_in, the caller releases exec_in). */
+int svdsb_graph_end_update(void *stream, void *exec_in, void **exec_out);
 int svdsb_graph_launch(void *exec, void *stream);
 int svdsb_graph_destroy(void *exec);
 

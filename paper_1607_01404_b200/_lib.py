@@ -33,6 +33,7 @@ _PROTOS = [
     ("svdsb_stream_sync", i32, [vp]),
     ("svdsb_graph_begin", i32, [vp]),
     ("svdsb_graph_end", i32, [vp, ctypes.POINTER(vp)]),
+    ("svdsb_graph_end_update", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     ("svdsb_graph_launch", i32, [vp, vp]),
     ("svdsb_graph_destroy", i32, [vp]),
     ("svdsb_ctx_create", i32, [i32, ctypes.POINTER(vp)]),

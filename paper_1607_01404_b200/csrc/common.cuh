@@ -89,6 +89,8 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 // (0 sliced ELL, 2 warp-staged CSR, 1 thread-per-row from global, 3 four
 // lanes per row).
 // Key 1: b = 4 Gram grid order (0 interleaved, 2 column groups outermost).
+// Key 2: sliced-ELL b = 4 (0 grouped loads, 1 whole-row prefetch for rows
+// <= 20; slower on config 4).
 constexpr int kTuneKeys = 8;
 inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0};
 

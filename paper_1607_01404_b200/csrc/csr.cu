@@ -808,6 +808,93 @@ csr_sell4_kernel(int64_t nrows, int64_t nslice, const int *__restrict__ row_ptr,
   pdl_trigger();
 }
 
+// Sliced-ELL forward b = 4 for rows of at most kSellW nonzeros: a lane
+// issues every value / index load of its row at once (one DRAM round trip
+// per row instead of one per group of four), then folds the four columns
+// as two pairs (16-byte gathers; the same L1 wavefronts as one 32-byte
+// gather) in the fold_row<0> order: p0 + (tail < 8 ? left-to-right :
+// 8-accumulator blocks, tree, remainder).  Bit-identical to row4_fold.
+constexpr int kSellW = 20;
+
+__device__ __forceinline__ double2 ldg2c(const double *p) {
+  double2 v;
+  asm("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 pmul(double v, double2 x) { return make_double2(dmul(v, x.x), dmul(v, x.y)); }
+__device__ __forceinline__ double2 padd(double2 a, double2 b) { return make_double2(dadd(a.x, b.x), dadd(a.y, b.y)); }
+
+__device__ __forceinline__ double2 sell_pair_fold(const int (&cj)[kSellW], const double (&vj)[kSellW], int len,
+                                                  const double *__restrict__ xc) {
+  if (len == 0) return make_double2(0.0, 0.0);
+  const int n = len - 1;
+  const double2 p0 = pmul(vj[0], ldg2c(xc + (int64_t)cj[0] * 4));
+  if (n < 8) {
+    double2 g[7];
+#pragma unroll
+    for (int u = 0; u < 7; ++u) g[u] = ldg2c(xc + (int64_t)cj[1 + u] * 4);  // cj = 0 past the row
+    double2 r = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 7; ++u)
+      if (1 + u <= n) r = padd(r, pmul(vj[1 + u], g[u]));
+    return n == 0 ? p0 : padd(p0, r);
+  }
+  double2 acc[8], g[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) g[u] = ldg2c(xc + (int64_t)cj[1 + u] * 4);
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = pmul(vj[1 + u], g[u]);
+  const int nb = n - (n % 8);  // 8 or 16
+#pragma unroll
+  for (int u = 0; u < 8; ++u) g[u] = ldg2c(xc + (int64_t)cj[9 + u] * 4);
+  if (nb == 16) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = padd(acc[u], pmul(vj[9 + u], g[u]));
+  }
+  double2 res = padd(padd(padd(acc[0], acc[1]), padd(acc[2], acc[3])), padd(padd(acc[4], acc[5]), padd(acc[6], acc[7])));
+  if (nb == 8) {
+#pragma unroll
+    for (int u = 0; u < 7; ++u)
+      if (9 + u <= n) res = padd(res, pmul(vj[9 + u], g[u]));
+  } else {
+#pragma unroll
+    for (int u = 0; u < kSellW - 17; ++u) g[u] = ldg2c(xc + (int64_t)cj[17 + u] * 4);
+#pragma unroll
+    for (int u = 0; u < kSellW - 17; ++u)
+      if (17 + u <= n) res = padd(res, pmul(vj[17 + u], g[u]));
+  }
+  return padd(p0, res);
+}
+
+template <int YROW>
+__global__ void __launch_bounds__(kTileThreads, 2)
+csr_sell4w_kernel(int64_t nrows, int64_t nslice, const int *__restrict__ row_ptr, const int64_t *__restrict__ sell_ptr,
+                  const int *__restrict__ col, const double *__restrict__ val, const double *__restrict__ x,
+                  double *__restrict__ y, int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * (kTileThreads / 32);
+  pdl_wait();
+  for (int64_t sl = blockIdx.x * (int64_t)(kTileThreads / 32) + (threadIdx.x >> 5); sl < nslice; sl += wstride) {
+    const int64_t row = (sl << 5) + lane;
+    if (row < nrows) {
+      const int len = __ldg(row_ptr + row + 1) - __ldg(row_ptr + row);
+      const int64_t base = __ldg(sell_ptr + sl) + lane;
+      int cj[kSellW];
+      double vj[kSellW];
+#pragma unroll
+      for (int j = 0; j < kSellW; ++j) {
+        cj[j] = j < len ? ld_stream(col + base + 32 * j) : 0;
+        vj[j] = j < len ? ld_stream(val + base + 32 * j) : 0.0;
+      }
+      const double2 lo = sell_pair_fold(cj, vj, len, x);
+      const double2 hi = sell_pair_fold(cj, vj, len, x + 2);
+      const double out[4] = {lo.x, lo.y, hi.x, hi.y};
+      store_row4<YROW>(y, ldy, row, out);
+    }
+  }
+  pdl_trigger();
+}
+
 __global__ void sell_fill_kernel(int64_t nrows, const int *__restrict__ row_ptr, const int *__restrict__ col,
                                  const double *__restrict__ val, const int64_t *__restrict__ sell_ptr,
                                  int *__restrict__ scol, double *__restrict__ sval) {
@@ -1346,6 +1433,13 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
       if (!p.sell_val && !capturing(st)) {
         int rc = build_sell(const_cast<CsrPart &>(p), st);
         if (rc) return rc;
+      }
+      if (p.sell_val && p.maxlen <= kSellW && g_tune[2] == 1) {  // measured slower (register spills)
+        auto k = yrow ? csr_sell4w_kernel<1> : csr_sell4w_kernel<0>;
+        const int g = (int)std::min<int64_t>((p.nslice + 7) / 8, pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
+        SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.rows, p.nslice, p.row_ptr, p.sell_ptr, p.sell_col, p.sell_val, x,
+                         y, ldy);
+        return SVDSB_OK;
       }
       if (p.sell_val) {
         auto k = yrow ? csr_sell4_kernel<1> : csr_sell4_kernel<0>;

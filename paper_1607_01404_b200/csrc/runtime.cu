@@ -83,6 +83,27 @@ int svdsb_graph_end(void *stream, void **exec_out) {
   return SVDSB_OK;
 }
 
+int svdsb_graph_end_update(void *stream, void *exec_in, void **exec_out) {
+  SVDSB_CHECK_ARG(exec_out != nullptr, "svdsb_graph_end_update: NULL output");
+  cudaGraph_t g = nullptr;
+  SVDSB_CUDA(cudaStreamEndCapture(svdsb::as_stream(stream), &g));
+  if (exec_in != nullptr) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(reinterpret_cast<cudaGraphExec_t>(exec_in), g, &info) == cudaSuccess) {
+      cudaGraphDestroy(g);
+      *exec_out = exec_in;
+      return SVDSB_OK;
+    }
+    cudaGetLastError();  // clear the update failure; instantiate afresh
+  }
+  cudaGraphExec_t e = nullptr;
+  cudaError_t rc = cudaGraphInstantiateWithFlags(&e, g, 0);
+  cudaGraphDestroy(g);
+  SVDSB_CUDA(rc);
+  *exec_out = e;
+  return SVDSB_OK;
+}
+
 int svdsb_graph_launch(void *exec, void *stream) {
   SVDSB_CUDA(cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(exec), svdsb::as_stream(stream)));
   return SVDSB_OK;

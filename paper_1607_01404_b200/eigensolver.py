@@ -359,6 +359,7 @@ class _Workspace:
         self.ci_host = None                                        # its value in stream order
         self.orthoc = torch.zeros(4 * _lib.SMALL_MAX * 4, dtype=DTYPE, device=dev)
         self.graphs = {}
+        self.graph_shape = {}   # key without the operator identity -> current key
         self.graph_owner = None
 
     def reset(self):
@@ -444,13 +445,11 @@ class DavidsonSolver:
             self.prev_d, self.yref, self.excl = ws.prev, ws.yref, ws.excl
             ws.ci_host = None
             self.ortho.c = ws.orthoc
-            # a workspace keeps the graphs of one operator: a new operator
-            # drops them (they reference its device arrays)
+            # graphs of a previous operator stay as update targets: their
+            # keys carry that operator's identity, so they are never
+            # replayed for this one (_launch_iter updates them in place)
             gk = getattr(op, "graph_key", None)
-            owner = gk() if gk is not None else None
-            if ws.graph_owner != owner:
-                ws.graphs.clear()
-                ws.graph_owner = owner
+            ws.graph_owner = gk() if gk is not None else None
         else:
             self.v = dv.new_block(self.n, gm)
             self.w = dv.new_block(self.n, gm)
@@ -1382,9 +1381,12 @@ class DavidsonSolver:
         _lib.call("svdsb_status_pack", dv.P(l_out), gn, dv.P(s_out), p, dv.P(st), ws.status[sout].data_ptr(),
                   ctx.stream)
 
-    def _capture(self, fn):
+    def _capture(self, fn, reuse=None):
         """Record fn's libsvdsb launches as a CUDA graph on a side stream
-        (capture needs a non-default stream) and instantiate it."""
+        (capture needs a non-default stream) and instantiate it -- or, with
+        `reuse` (a _NativeGraph of the same iteration shape, e.g. captured
+        for the previous matrix), update that executable in place, which
+        costs a fraction of an instantiation."""
         ctx = self.ctx
         cap = getattr(ctx, "capture_stream", None)
         if cap is None:
@@ -1398,8 +1400,13 @@ class DavidsonSolver:
             fn()
         finally:
             ctx._stream = old
-            rc = lib.svdsb_graph_end(cap.cuda_stream, ctypes.byref(ex))
+            if reuse is None:
+                rc = lib.svdsb_graph_end(cap.cuda_stream, ctypes.byref(ex))
+            else:
+                rc = lib.svdsb_graph_end_update(cap.cuda_stream, reuse.exec, ctypes.byref(ex))
         _lib.check(rc, "svdsb_graph_end")
+        if reuse is not None and ex.value == reuse.exec:
+            reuse.exec = None   # ownership moves to the returned graph
         return _NativeGraph(ex.value)
 
     def _launch_iter(self, g, kind, g0, sin, ci):
@@ -1418,10 +1425,17 @@ class DavidsonSolver:
         key = (self.v.data_ptr(), self.w.data_ptr(), kind, g0, g, p, sin, order, shift, base)
         entry = ws.graphs.get(key)
         if entry is None:
+            # one graph per iteration shape: the one captured for another
+            # operator / preconditioner (a new matrix) is updated in place
+            skey = key[:-1]
+            old_key = ws.graph_shape.get(skey)
+            old = ws.graphs.pop(old_key, None) if old_key is not None else None
             before = _lib.launch_count()
-            graph = self._capture(lambda: self._iter_device(g, kind, g0, p, order, shift, sin, sout))
+            graph = self._capture(lambda: self._iter_device(g, kind, g0, p, order, shift, sin, sout),
+                                  reuse=None if old is None else old[0])
             entry = (graph, _lib.launch_count() - before)
             ws.graphs[key] = entry
+            ws.graph_shape[skey] = key
             self.stats.graphs_captured += 1
         entry[0].replay(self.ctx._stream)
         ws.events[sout].record(self.ctx.torch_stream)
