@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-scale", action="store_true", help="skip the config-3 kernel roofline section")
+    ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE",
+                    help="kernel-variant knob (svdsb_tune_set) for A/B measurements")
     return ap.parse_args()
 
 
@@ -153,6 +155,9 @@ def run_ours(args):
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
+    for kv in args.tune:
+        key, val = kv.split("=")
+        _lib.call("svdsb_tune_set", int(key), int(val))
     if world > 1:
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)

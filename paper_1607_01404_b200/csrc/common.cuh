@@ -84,6 +84,30 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 
 // Launch through launch_k and account for it (use inside int-returning
 // C-ABI functions).
+// Optional epilogues of the last CTA of a reduction kernel (the native
+// GD+k iteration, gdk.cu): write the Gram column straight into H (column
+// and row g, as svdsb_h_insert does for b = 1), and copy the status record
+// (Ritz values, residual norms, DGKS state) to pinned host memory after the
+// Ritz residual norms (as svdsb_status_pack).
+struct HInsert {
+  double *h = nullptr;
+  int64_t ldh = 0;
+  int g = 0;
+};
+struct StatusOut {
+  const double *lams = nullptr;
+  int gn = 0;
+  const double *st = nullptr;
+  double *host = nullptr;
+};
+
+// Reduction launches with the epilogues above (dense.cu), for gdk.cu.
+int gram_impl(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs, const int *cols,
+              const double *y, int64_t ldy, int b, double *c, int64_t ldc, double *norms2, void *stream, HInsert hi);
+int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const double *w, int64_t ldw, int g,
+              const double *yc, int64_t ldyc, const double *lam, int p, double *r, int64_t ldr, double *x,
+              int64_t ldx, double *ox, int64_t ldox, double *rn2, void *stream, StatusOut so);
+
 // Kernel-variant knobs for measurement tools (svdsb_tune_set); 0 selects
 // the default everywhere.  Key 0: forward b = 4 SpMV of short-row matrices
 // (0 sliced ELL, 2 warp-staged CSR, 1 thread-per-row from global, 3 four
@@ -91,6 +115,10 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 // Key 1: b = 4 Gram grid order (0 interleaved, 2 column groups outermost).
 // Key 2: sliced-ELL b = 4 (0 grouped loads, 1 whole-row prefetch for rows
 // <= 20; slower on config 4).
+// Key 3: Ritz residual (0: two threads per row for 16 < p <= 32, one
+// otherwise; 1: always one; 2: two also for 8 < p <= 16).
+// Key 4: native GD+k iteration (0 H-column / status epilogues, 1 separate
+// h_insert and status_pack launches).
 constexpr int kTuneKeys = 8;
 inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0};
 

@@ -486,7 +486,7 @@ __device__ __forceinline__ double2 ldg2(const double *p) { return __ldg(reinterp
 template <int AT>
 __global__ void __launch_bounds__(kThreads)
 gram1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, double *c, double *norms2, double *partials,
-                 unsigned int *ticket, const double *gate) {
+                 unsigned int *ticket, const double *gate, HInsert hi) {
   pdl_wait();
   if (gate != nullptr && gate[0] == 0.0) return;  // device-side DGKS: column already final
   __shared__ const double *xp[AT];
@@ -527,7 +527,13 @@ gram1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, double *c
   fold_parts(partials, gridDim.x, NOUT, (int)gridDim.y * NOUT, [&](int, int t, int k, double s) {
     if (k < AT) {
       int i = t * AT + k;
-      if (i < xs.total) c[i] = s;
+      if (i < xs.total) {
+        c[i] = s;
+        if (hi.h != nullptr && i <= hi.g) {  // H(i, g) = H(g, i); H(g, g) = (c_g + c_g) / 2 = c_g
+          hi.h[i + (int64_t)hi.g * hi.ldh] = s;
+          hi.h[hi.g + (int64_t)i * hi.ldh] = s;
+        }
+      }
     } else if (norms2 != nullptr && t == 0) {
       norms2[0] = s;
     }
@@ -769,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, PT <= 16 ? 2 : 1)
 ritz_wide_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const double *__restrict__ w, int64_t ldw,
                  int g, const double *__restrict__ yc, int64_t ldyc, const double *__restrict__ lam, int p,
                  double *__restrict__ r, int64_t ldr, double *__restrict__ xo, int64_t ldx, double *__restrict__ oxo,
-                 int64_t ldox, double *rn2, double *partials, unsigned int *ticket) {
+                 int64_t ldox, double *rn2, double *partials, unsigned int *ticket, StatusOut so) {
   pdl_wait();
   extern __shared__ double ysh[];  // g x PT
   __shared__ double lsh[PT];
@@ -843,6 +849,124 @@ ritz_wide_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const d
   cta_fold<PT>(nacc, PT, part);
   if (!last_cta(ticket)) return;
   fold_parts(partials, gridDim.x, PT, p, [&](int j, int, int, double s) { rn2[j] = s; });
+  if (so.host != nullptr) {
+    __syncthreads();  // this CTA's rn2 writes are visible to all its threads
+    for (int i = threadIdx.x; i < so.gn + p + 8; i += blockDim.x)
+      so.host[i] = i < so.gn ? so.lams[i] : (i < so.gn + p ? rn2[i - so.gn] : so.st[i - so.gn - p]);
+    __threadfence_system();
+  }
+}
+
+// Ritz residuals with SPLIT threads per row, each owning PQ consecutive
+// candidates: the same per-element fma order as ritz_wide_kernel (basis
+// index ascending), so R is bit-identical; fewer accumulators per thread
+// keep two CTAs per SM and RU loads in flight where ritz_wide_kernel<24/32>
+// ran one CTA with one load pair at a time.  The threads of a row read the
+// same V / W element (one sector per warp load, broadcast).
+template <int PQ, int SPLIT>
+__global__ void __launch_bounds__(kThreads, 2)
+ritz_split_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const double *__restrict__ w, int64_t ldw,
+                  int g, const double *__restrict__ yc, int64_t ldyc, const double *__restrict__ lam, int p,
+                  double *__restrict__ r, int64_t ldr, double *__restrict__ xo, int64_t ldx, double *__restrict__ oxo,
+                  int64_t ldox, double *rn2, double *partials, unsigned int *ticket, StatusOut so) {
+  constexpr int PT = PQ * SPLIT;
+  pdl_wait();
+  extern __shared__ double ysh[];  // g x PT
+  __shared__ double lsh[PT];
+  __shared__ double red[kWarps][PT];
+  for (int k = threadIdx.x; k < g * PT; k += kThreads) {
+    int i = k / PT, j = k % PT;
+    ysh[k] = (j < p) ? yc[i + (int64_t)j * ldyc] : 0.0;
+  }
+  if (threadIdx.x < PT) lsh[threadIdx.x] = ((int)threadIdx.x < p) ? lam[threadIdx.x] : 0.0;
+  __syncthreads();
+  const int part = threadIdx.x % SPLIT;
+  const int j0 = part * PQ;
+  double nacc[PQ];
+#pragma unroll
+  for (int j = 0; j < PQ; ++j) nacc[j] = 0.0;
+  RowRange rr = cta_rows(dim);
+  constexpr int RPP = kThreads / SPLIT;  // rows per pass of the CTA
+  for (int64_t row = rr.r0 + threadIdx.x / SPLIT; row < rr.r1; row += RPP) {
+    double ax[PQ], aw[PQ];
+#pragma unroll
+    for (int j = 0; j < PQ; ++j) {
+      ax[j] = 0.0;
+      aw[j] = 0.0;
+    }
+    constexpr int RU = PQ <= 6 ? 8 : (PQ <= 12 ? 4 : 2);
+    int i = 0;
+    for (; i + RU <= g; i += RU) {
+      double vv[RU], ww[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        vv[u] = __ldg(v + row + (int64_t)(i + u) * ldv);
+        ww[u] = __ldg(w + row + (int64_t)(i + u) * ldw);
+      }
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const double2 *yrow = reinterpret_cast<const double2 *>(ysh + (i + u) * PT + j0);
+#pragma unroll
+        for (int j = 0; j < PQ / 2; ++j) {
+          double2 cf = yrow[j];
+          ax[2 * j] = fma(vv[u], cf.x, ax[2 * j]);
+          aw[2 * j] = fma(ww[u], cf.x, aw[2 * j]);
+          ax[2 * j + 1] = fma(vv[u], cf.y, ax[2 * j + 1]);
+          aw[2 * j + 1] = fma(ww[u], cf.y, aw[2 * j + 1]);
+        }
+      }
+    }
+    for (; i < g; ++i) {
+      double vv = __ldg(v + row + (int64_t)i * ldv);
+      double ww = __ldg(w + row + (int64_t)i * ldw);
+      const double2 *yrow = reinterpret_cast<const double2 *>(ysh + i * PT + j0);
+#pragma unroll
+      for (int j = 0; j < PQ / 2; ++j) {
+        double2 cf = yrow[j];
+        ax[2 * j] = fma(vv, cf.x, ax[2 * j]);
+        aw[2 * j] = fma(ww, cf.x, aw[2 * j]);
+        ax[2 * j + 1] = fma(vv, cf.y, ax[2 * j + 1]);
+        aw[2 * j + 1] = fma(ww, cf.y, aw[2 * j + 1]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PQ; ++j) {
+      if (j0 + j < p) {
+        double res = aw[j] - ax[j] * lsh[j0 + j];
+        r[row + (int64_t)(j0 + j) * ldr] = res;
+        if (xo) xo[row + (int64_t)(j0 + j) * ldx] = ax[j];
+        if (oxo) oxo[row + (int64_t)(j0 + j) * ldox] = aw[j];
+        nacc[j] = fma(res, res, nacc[j]);
+      }
+    }
+  }
+  pdl_trigger();
+  // per-candidate CTA sums: lanes of equal `part` reduced with xor shuffles
+  // (lane % SPLIT is preserved by xor offsets >= SPLIT), then across warps
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < PQ; ++j) {
+    double t = nacc[j];
+#pragma unroll
+    for (int off = 16; off >= SPLIT; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (lane < SPLIT) red[wid][lane * PQ + j] = t;
+  }
+  __syncthreads();
+  double *pp = partials + (int64_t)blockIdx.x * PT;
+  for (int k = threadIdx.x; k < PT; k += kThreads) {
+    double t = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) t += red[ww][k];
+    pp[k] = t;
+  }
+  if (!last_cta(ticket)) return;
+  fold_parts(partials, gridDim.x, PT, p, [&](int j, int, int, double t) { rn2[j] = t; });
+  if (so.host != nullptr) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < so.gn + p + 8; i += blockDim.x)
+      so.host[i] = i < so.gn ? so.lams[i] : (i < so.gn + p ? rn2[i - so.gn] : so.st[i - so.gn - p]);
+    __threadfence_system();
+  }
 }
 
 // Y = alpha X C + beta Y, two rows per thread, s <= ST.
@@ -1124,7 +1248,17 @@ extern "C" {
 
 int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs, const int *cols,
                const double *y, int64_t ldy, int b, double *c, int64_t ldc, double *norms2, void *stream) {
+  return svdsb::gram_impl(ctx, dim, nblk, xs, ldxs, cols, y, ldy, b, c, ldc, norms2, stream, svdsb::HInsert{});
+}
+
+}  // extern "C"
+
+namespace svdsb {
+
+int gram_impl(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs, const int *cols,
+              const double *y, int64_t ldy, int b, double *c, int64_t ldc, double *norms2, void *stream, HInsert hi) {
   SVDSB_CHECK_ARG(ctx != nullptr, "svdsb_gram: NULL ctx");
+  SVDSB_CHECK_ARG(hi.h == nullptr || b == 1, "gram_impl: the H epilogue is for one column");
   ColSet s;
   int rc = make_colset(s, nblk, xs, ldxs, cols);
   if (rc) return rc;
@@ -1140,7 +1274,7 @@ int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, c
     if (s.total <= 16) {
       dim3 grid(grid_for(gram1_vec_kernel<16>, dim, 0), 1, 1);
       SVDSB_LAUNCH_PDL(gram1_vec_kernel<16>, grid, kThreads, 0, st, dim, s, y, c, norms2, ctx->partials,
-                       take_ticket(ctx), nullptr);
+                       take_ticket(ctx), nullptr, hi);
     } else {
       constexpr int AT = 40;
       // latency-bound sizes (L2-scale N): one CTA per SM halves the partials
@@ -1149,7 +1283,7 @@ int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, c
       if (dim <= (1 << 18) && gxv > kNumSMs) gxv = kNumSMs;
       dim3 grid(gxv, (s.total + AT - 1) / AT, 1);
       SVDSB_LAUNCH_PDL(gram1_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, y, c, norms2, ctx->partials,
-                       take_ticket(ctx), nullptr);
+                       take_ticket(ctx), nullptr, hi);
     }
     return SVDSB_OK;
   } else if (b == 4 && colset_vec_ok(s) && aligned16(y) && ldy % 2 == 0) {
@@ -1166,6 +1300,7 @@ int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, c
     }
     return SVDSB_OK;
   } else if (b == 1) {
+    SVDSB_CHECK_ARG(hi.h == nullptr, "gram_impl: the H epilogue needs 16-byte aligned operands");
     constexpr int AT = 32, BT = 1;
     dim3 grid(gx, (s.total + AT - 1) / AT, 1);
     SVDSB_CHECK_ARG((int64_t)grid.x * grid.y * (AT * BT + BT) <= kMaxPartials, "gram: workspace too small");
@@ -1181,6 +1316,10 @@ int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, c
   SVDSB_LAUNCHED();
   return SVDSB_OK;
 }
+
+}  // namespace svdsb
+
+extern "C" {
 
 int svdsb_project_out(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs,
                       const int *cols, const double *c, int64_t ldc, double *y, int64_t ldy, int b, double *norms2,
@@ -1261,16 +1400,56 @@ int svdsb_ts_gemm(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx, int
 int svdsb_ritz_residual(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const double *w, int64_t ldw,
                         int g, const double *yc, int64_t ldyc, const double *lam, int p, double *r, int64_t ldr,
                         double *x, int64_t ldx, double *ox, int64_t ldox, double *rn2, void *stream) {
+  return svdsb::ritz_impl(ctx, dim, v, ldv, w, ldw, g, yc, ldyc, lam, p, r, ldr, x, ldx, ox, ldox, rn2, stream,
+                          svdsb::StatusOut{});
+}
+
+}  // extern "C"
+
+namespace svdsb {
+
+int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const double *w, int64_t ldw, int g,
+              const double *yc, int64_t ldyc, const double *lam, int p, double *r, int64_t ldr, double *x,
+              int64_t ldx, double *ox, int64_t ldox, double *rn2, void *stream, StatusOut so) {
   SVDSB_CHECK_ARG(ctx != nullptr, "svdsb_ritz_residual: NULL ctx");
+  SVDSB_CHECK_ARG(so.host == nullptr || (p <= 32 && rn2 != nullptr), "ritz_impl: status epilogue needs p <= 32");
   if (p <= 0) return SVDSB_OK;
   SVDSB_CHECK_ARG(g >= 1 && g <= 256, "svdsb_ritz_residual: g out of range");
   cudaStream_t st = as_stream(stream);
+  if (p > 16 && p <= 32 && g_tune[3] != 1) {
+    // two threads per row, 12 or 16 candidates each (config 4, p = 24:
+    // 336 -> 295 us; for p <= 16 the one-thread kernel is faster -- config
+    // 3, p = 11: 637 vs 716 us; g_tune[3] = 2 forces the split there too)
+    auto *tk = take_ticket(ctx);
+#define SVDSB_RITZ_SPLIT(PQ)                                                                                   \
+  SVDSB_LAUNCH_PDL(ritz_split_kernel<PQ, 2>, grid_for(ritz_split_kernel<PQ, 2>, dim, sizeof(double) * g * 2 * PQ), \
+                   kThreads, sizeof(double) * g * 2 * PQ, st, dim, v, ldv, w, ldw, g, yc, ldyc, lam, p, r, ldr, x,  \
+                   ldx, ox, ldox, rn2, ctx->partials, tk, so)
+    if (p <= 24)
+      SVDSB_RITZ_SPLIT(12);
+    else
+      SVDSB_RITZ_SPLIT(16);
+#undef SVDSB_RITZ_SPLIT
+    return SVDSB_OK;
+  }
+  if (p > 8 && p <= 16 && g_tune[3] == 2) {
+    auto *tk = take_ticket(ctx);
+    if (p <= 12)
+      SVDSB_LAUNCH_PDL(ritz_split_kernel<6, 2>, grid_for(ritz_split_kernel<6, 2>, dim, sizeof(double) * g * 12),
+                       kThreads, sizeof(double) * g * 12, st, dim, v, ldv, w, ldw, g, yc, ldyc, lam, p, r, ldr, x, ldx,
+                       ox, ldox, rn2, ctx->partials, tk, so);
+    else
+      SVDSB_LAUNCH_PDL(ritz_split_kernel<8, 2>, grid_for(ritz_split_kernel<8, 2>, dim, sizeof(double) * g * 16),
+                       kThreads, sizeof(double) * g * 16, st, dim, v, ldv, w, ldw, g, yc, ldyc, lam, p, r, ldr, x, ldx,
+                       ox, ldox, rn2, ctx->partials, tk, so);
+    return SVDSB_OK;
+  }
   if (p <= 32) {
     auto *tk = take_ticket(ctx);
 #define SVDSB_RITZ_WIDE(PTV)                                                                                  \
   SVDSB_LAUNCH_PDL(ritz_wide_kernel<PTV>, grid_for(ritz_wide_kernel<PTV>, dim, sizeof(double) * g * PTV), kThreads,  \
                    sizeof(double) * g * PTV, st, dim, v, ldv, w, ldw, g, yc, ldyc, lam, p, r, ldr, x, ldx, ox, ldox, \
-                   rn2, ctx->partials, tk)
+                   rn2, ctx->partials, tk, so)
     if (p <= 4)
       SVDSB_RITZ_WIDE(4);
     else if (p <= 8)
@@ -1294,6 +1473,10 @@ int svdsb_ritz_residual(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ld
   SVDSB_LAUNCHED();
   return SVDSB_OK;
 }
+
+}  // namespace svdsb
+
+extern "C" {
 
 int svdsb_col_norms2(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx, int b, double *out, void *stream) {
   return svdsb_col_dots(ctx, dim, x, ldx, x, ldx, b, out, stream);
@@ -1424,12 +1607,12 @@ int svdsb_cgs_pass(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *x
   if (s.total <= 16) {
     dim3 grid(grid_for(gram1_vec_kernel<16>, dim, 0), 1, 1);
     SVDSB_LAUNCH_PDL(gram1_vec_kernel<16>, grid, kThreads, 0, st, dim, s, v, cwork, n0, ctx->partials,
-                     take_ticket(ctx), state);
+                     take_ticket(ctx), state, HInsert{});
   } else {
     constexpr int AT = 40;
     dim3 grid(grid_for(gram1_vec_kernel<AT>, dim, 0), (s.total + AT - 1) / AT, 1);
     SVDSB_LAUNCH_PDL(gram1_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, v, cwork, n0, ctx->partials,
-                     take_ticket(ctx), state);
+                     take_ticket(ctx), state, HInsert{});
   }
   size_t sh = sizeof(double) * s.total;
   SVDSB_LAUNCH_PDL(project1_vec_kernel, grid_for(project1_vec_kernel, dim, sh), kThreads, sh, st, dim, s, cwork, v,

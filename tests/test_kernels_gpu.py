@@ -142,6 +142,37 @@ def test_gram_b4_grid_orders(order, rng):
     assert np.allclose(nrm.cpu().numpy(), (y ** 2).sum(0), rtol=1e-13)
 
 
+@pytest.mark.parametrize("p", [6, 11, 16, 20, 24, 32])
+def test_ritz_residual_variants(p, rng):
+    """Ritz residuals R = W Y - V Y diag(lam) and |R_j|^2 for one and two
+    threads per row (svdsb_tune_set key 3): R bit-identical between the
+    variants (same fma order), both against fp64 numpy."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    dim, g = 30011, 35
+    vh, wh = rng.standard_normal((dim, g)), rng.standard_normal((dim, g))
+    yh = np.linalg.qr(rng.standard_normal((g, g)))[0][:, :p]
+    lh = rng.standard_normal(p)
+    V, W, Y = dv.to_device_block(vh), dv.to_device_block(wh), dv.to_device_block(yh)
+    lam = torch.from_numpy(lh).to(ctx.device)
+    want = wh @ yh - (vh @ yh) * lh
+    outs = []
+    try:
+        for variant in (1, 2, 0):
+            _lib.call("svdsb_tune_set", 3, variant)
+            R = dv.new_block(dim, p)
+            rn2 = torch.zeros(p, dtype=torch.float64, device=ctx.device)
+            dv.ritz_residual(ctx, V, W, Y, lam, R, rn2=rn2)
+            outs.append((dv.to_host(R), rn2.cpu().numpy()))
+    finally:
+        _lib.call("svdsb_tune_set", 3, 0)
+    for got, n2 in outs:
+        assert np.array_equal(got, outs[0][0])
+        assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+        assert np.allclose(n2, (want ** 2).sum(0), rtol=1e-12)
+
+
 def test_spmv_bulk_copy_path_bit_exact(rng):
     """Matrices of >= 64 MB stream through the cp.async.bulk tile ring
     (csr_tile_bulk_kernel); it must reproduce the reference's summation
