@@ -119,6 +119,7 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // otherwise; 1: always one; 2: two also for 8 < p <= 16).
 // Key 4: native GD+k iteration (0 H-column / status epilogues, 1 separate
 // h_insert and status_pack launches).
+// Key 5: transposed b = 4 SpMV (0 length-sorted sliced ELL, 1 CSR tiles).
 constexpr int kTuneKeys = 8;
 inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0};
 

@@ -59,6 +59,10 @@ struct CsrPart {
   // sell_ptr[slice] + 32 j + t) for the b = 4 forward product; built on
   // first use
   int64_t nslice = 0;
+  int64_t nsell = 0;            // rows in the sliced copy
+  int *sell_perm = nullptr;     // transpose parts: sliced position -> row (rows sorted by length)
+  int nmid = 0;                 // transpose parts: rows between kSellTMax and a tile's nonzeros
+  int *mid_rows = nullptr;
   int64_t *sell_ptr = nullptr;  // nslice + 1
   int *sell_col = nullptr;
   double *sell_val = nullptr;
@@ -895,13 +899,15 @@ csr_sell4w_kernel(int64_t nrows, int64_t nslice, const int *__restrict__ row_ptr
   pdl_trigger();
 }
 
-__global__ void sell_fill_kernel(int64_t nrows, const int *__restrict__ row_ptr, const int *__restrict__ col,
-                                 const double *__restrict__ val, const int64_t *__restrict__ sell_ptr,
-                                 int *__restrict__ scol, double *__restrict__ sval) {
-  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (row >= nrows) return;
-  const int64_t sl = row >> 5;
-  const int t = (int)(row & 31);
+__global__ void sell_fill_kernel(int64_t nrows, const int *__restrict__ perm, const int *__restrict__ row_ptr,
+                                 const int *__restrict__ col, const double *__restrict__ val,
+                                 const int64_t *__restrict__ sell_ptr, int *__restrict__ scol,
+                                 double *__restrict__ sval) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nrows) return;
+  const int64_t row = perm ? perm[q] : q;
+  const int64_t sl = q >> 5;
+  const int t = (int)(q & 31);
   const int k0 = row_ptr[row], k1 = row_ptr[row + 1];
   const int64_t base = sell_ptr[sl] + t;
   const int w = (int)((sell_ptr[sl + 1] - sell_ptr[sl]) >> 5);
@@ -911,6 +917,101 @@ __global__ void sell_fill_kernel(int64_t nrows, const int *__restrict__ row_ptr,
     sval[base + 32 * (int64_t)j] = in ? val[k0 + j] : 0.0;
   }
 }
+
+// Transposed b = 4 rows of kSellTMax..kTileNnz nonzeros ("mid" rows), one
+// warp per row: lanes load 32 values / column ids at a time (coalesced) and
+// gather their x rows; four lanes (one per block column) then add the 32
+// products left to right -- np.add.at's order, bit-identical.
+constexpr int kSellTMax = 64;
+
+// One warp, one mid row (called by csr_sell4t_kernel).
+__device__ __forceinline__ void warprow4t(int64_t row, const int *__restrict__ row_ptr, const int *__restrict__ col,
+                                          const double *__restrict__ val, const double *__restrict__ x,
+                                          double *__restrict__ y, int64_t ldy, int yrow, int acc,
+                                          double (*prod)[33]) {
+  const int lane = threadIdx.x & 31;
+  const int k0 = __ldg(row_ptr + row), k1 = __ldg(row_ptr + row + 1);
+  const int cc = lane & 3;
+  double sacc = 0.0;
+  if (acc && lane < 4) sacc = yrow ? y[row * 4 + cc] : y[row + cc * ldy];
+  for (int k = k0; k < k1; k += 32) {
+    const int e = k + lane;
+    const bool ok = e < k1;
+    const int c = ok ? ld_stream(col + e) : 0;
+    const double v = ok ? ld_stream(val + e) : 0.0;
+    double xv[4];
+    gather4(x, c, xv);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) prod[q][lane] = dmul(v, xv[q]);
+    __syncwarp();
+    if (lane < 4) {
+      const int n = min(32, k1 - k);
+      for (int t = 0; t < n; ++t) sacc = dadd(sacc, prod[cc][t]);
+    }
+    __syncwarp();
+  }
+  if (lane < 4) {
+    if (yrow)
+      y[row * 4 + cc] = sacc;
+    else
+      y[row + cc * ldy] = sacc;
+  }
+}
+
+// Transposed b = 4 product on a sliced-ELL copy whose rows are sorted by
+// length (so slices carry almost no padding despite config 4's Zipf row
+// lengths): lane q of the sorted order owns row perm[q] and sums its
+// products left to right with no FMA, continuing from y when accumulating
+// over column blocks -- np.add.at's order, bit-identical to the CSR
+// kernels.  Rows longer than a tile are not in the copy (chunk path).
+template <int YROW>
+__global__ void __launch_bounds__(kTileThreads, 2)
+csr_sell4t_kernel(int64_t nq, int64_t nslice, const int *__restrict__ perm, const int *__restrict__ row_ptr,
+                  const int64_t *__restrict__ sell_ptr, const int *__restrict__ scol, const double *__restrict__ sval,
+                  int nmid, const int *__restrict__ mid, const int *__restrict__ col, const double *__restrict__ val,
+                  const double *__restrict__ x, double *__restrict__ y, int64_t ldy, int acc) {
+  __shared__ double prod[kTileThreads / 32][4][33];
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * (kTileThreads / 32);
+  pdl_wait();
+  // warp work items: the mid rows first (longest work), then the slices
+  for (int64_t it = blockIdx.x * (int64_t)(kTileThreads / 32) + (threadIdx.x >> 5); it < nmid + nslice;
+       it += wstride) {
+    if (it < nmid) {
+      warprow4t(__ldg(mid + it), row_ptr, col, val, x, y, ldy, YROW, acc, prod[threadIdx.x >> 5]);
+      continue;
+    }
+    const int64_t sl = it - nmid;
+    const int64_t q = (sl << 5) + lane;
+    if (q >= nq) continue;
+    const int64_t row = __ldg(perm + q);
+    const int len = __ldg(row_ptr + row + 1) - __ldg(row_ptr + row);
+    const int64_t base = __ldg(sell_ptr + sl) + lane;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    if (acc) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) s[c] = YROW ? y[row * 4 + c] : y[row + c * ldy];
+    }
+    for (int j0 = 0; j0 < len; j0 += 4) {
+      double xv[4][4], vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = min(j0 + u, len - 1);
+        vv[u] = ld_stream(sval + base + 32 * (int64_t)j);
+        gather4(x, ld_stream(scol + base + 32 * (int64_t)j), xv[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j0 + u < len) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) s[c] = dadd(s[c], dmul(vv[u], xv[u][c]));
+        }
+    }
+    store_row4<YROW>(y, ldy, row, s);
+  }
+  pdl_trigger();
+}
+
 
 static bool rowlane_on() {
   static int on = -1;
@@ -1305,6 +1406,8 @@ static void free_part(CsrPart &p) {
   pfree(p.chunk_nz, nullptr);
   pfree(p.chunk_part, nullptr);
   pfree(p.sell_ptr, nullptr);
+  pfree(p.sell_perm, nullptr);
+  pfree(p.mid_rows, nullptr);
   pfree(p.sell_col, nullptr);
   pfree(p.sell_val, nullptr);
   p = CsrPart();
@@ -1322,33 +1425,65 @@ static int upload(T **dst, const std::vector<T> &src, cudaStream_t st) {
 // Sliced ELL copy of a part (see csr_sell4_kernel): slice widths from the
 // host row pointer, device fill.  Padding entries (column 0, value 0) are
 // never read: a lane stops at its row's length.
-static int build_sell(CsrPart &p, cudaStream_t st) {
+static int build_sell(CsrPart &p, cudaStream_t st, bool sorted = false) {
   const std::vector<int> &rp = p.host_row_ptr;
-  const int64_t ns = (p.rows + 31) / 32;
+  // sorted: rows of at most kSellTMax nonzeros, longest first (stable);
+  // rows up to a tile go to the warp-per-row kernel (mid_rows), longer ones
+  // stay on the chunk path
+  std::vector<int> order;
+  if (sorted) {
+    order.reserve(p.rows);
+    std::vector<int> mid;
+    for (int64_t r = 0; r < p.rows; ++r) {
+      const int len = rp[r + 1] - rp[r];
+      if (len <= kSellTMax)
+        order.push_back((int)r);
+      else if (len <= kTileNnz)
+        mid.push_back((int)r);
+    }
+    int *dmid = nullptr;
+    int rcm = upload(&dmid, mid, st);
+    if (rcm) return rcm;
+    p.nmid = (int)mid.size();
+    p.mid_rows = dmid;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
+  }
+  const int64_t nq = sorted ? (int64_t)order.size() : p.rows;
+  auto row_of = [&](int64_t q) -> int64_t { return sorted ? order[q] : q; };
+  const int64_t ns = (nq + 31) / 32;
   std::vector<int64_t> sp(ns + 1, 0);
   for (int64_t sl = 0; sl < ns; ++sl) {
     int w = 0;
-    for (int64_t r = 32 * sl; r < std::min(p.rows, 32 * sl + 32); ++r) w = std::max(w, rp[r + 1] - rp[r]);
+    for (int64_t q = 32 * sl; q < std::min(nq, 32 * sl + 32); ++q) w = std::max(w, rp[row_of(q) + 1] - rp[row_of(q)]);
     sp[sl + 1] = sp[sl] + 32 * (int64_t)w;
   }
   int64_t *dsp = nullptr;
+  int *dperm = nullptr;
   int rc;
   if ((rc = upload(&dsp, sp, st))) return rc;
+  if (sorted && (rc = upload(&dperm, order, st))) {
+    pfree(dsp, st);
+    return rc;
+  }
   int *scol = nullptr;
   double *sval = nullptr;
   if (alloc_pad(&scol, std::max<int64_t>(sp[ns], 1), st) != cudaSuccess ||
       alloc_pad(&sval, std::max<int64_t>(sp[ns], 1), st) != cudaSuccess) {
     pfree(dsp, st);
+    pfree(dperm, st);
     pfree(scol, st);
     set_error("sliced-ELL allocation failed");
     return SVDSB_ERR_ALLOC;
   }
-  if (p.rows > 0) {
-    sell_fill_kernel<<<(unsigned)((p.rows + 255) / 256), 256, 0, st>>>(p.rows, p.row_ptr, p.col, p.val, dsp, scol,
-                                                                       sval);
+  if (nq > 0) {
+    sell_fill_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(nq, dperm, p.row_ptr, p.col, p.val, dsp, scol,
+                                                                   sval);
     SVDSB_LAUNCHED();
   }
   p.nslice = ns;
+  p.nsell = nq;
+  p.sell_perm = dperm;
   p.sell_ptr = dsp;
   p.sell_col = scol;
   p.sell_val = sval;
@@ -1434,14 +1569,14 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
         int rc = build_sell(const_cast<CsrPart &>(p), st);
         if (rc) return rc;
       }
-      if (p.sell_val && p.maxlen <= kSellW && g_tune[2] == 1) {  // measured slower (register spills)
+      if (p.sell_val && !p.sell_perm && p.maxlen <= kSellW && g_tune[2] == 1) {  // measured slower (register spills)
         auto k = yrow ? csr_sell4w_kernel<1> : csr_sell4w_kernel<0>;
         const int g = (int)std::min<int64_t>((p.nslice + 7) / 8, pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
         SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.rows, p.nslice, p.row_ptr, p.sell_ptr, p.sell_col, p.sell_val, x,
                          y, ldy);
         return SVDSB_OK;
       }
-      if (p.sell_val) {
+      if (p.sell_val && !p.sell_perm) {
         auto k = yrow ? csr_sell4_kernel<1> : csr_sell4_kernel<0>;
         const int g = (int)std::min<int64_t>((p.nslice + 7) / 8, pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
         SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.rows, p.nslice, p.row_ptr, p.sell_ptr, p.sell_col, p.sell_val, x,
@@ -1473,7 +1608,27 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
         SVDSB_LAUNCH_PDL(csr_rowlane4_kernel<0>, g, kTileThreads, 0, st, p.rows, p.row_ptr, p.col, p.val, x, y, ldy);
       return SVDSB_OK;
     }
-    if (p.ntile > 0 && xrow) {
+    bool short_done = false;
+    if (ORDER == 1 && b == 4 && xrow && p.ntile > 0 && g_tune[5] == 0) {
+      // rows up to a tile on a length-sorted sliced-ELL copy (built on the
+      // first uncaptured call); long rows below on the chunk path
+      if (!p.sell_val && !capturing(st)) {
+        int rc = build_sell(const_cast<CsrPart &>(p), st, true);
+        if (rc) return rc;
+      }
+      if (p.sell_val && p.sell_perm) {
+        if (p.nslice + p.nmid > 0) {
+          auto k = yrow ? csr_sell4t_kernel<1> : csr_sell4t_kernel<0>;
+          const int g = (int)std::min<int64_t>((p.nslice + p.nmid + 7) / 8,
+                                               pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
+          SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.nsell, p.nslice, p.sell_perm, p.row_ptr, p.sell_ptr, p.sell_col,
+                           p.sell_val, p.nmid, p.mid_rows, p.col, p.val, x, y, ldy, acc);
+        }
+        short_done = true;
+      }
+    }
+    if (short_done) {
+    } else if (p.ntile > 0 && xrow) {
       const size_t sm = sizeof(double) * 4 * kTileNnz + sizeof(int) * (kTileRows + 1);
       if (yrow) {
         auto k = csr_tile_pipe_rows_kernel<ORDER, 1>;

@@ -173,6 +173,36 @@ def test_ritz_residual_variants(p, rng):
         assert np.allclose(n2, (want ** 2).sum(0), rtol=1e-12)
 
 
+@pytest.mark.parametrize("variant", [0, 1])
+def test_spmv_transpose_b4_variants(variant, rng):
+    """Transposed b = 4 products (svdsb_tune_set key 5: length-sorted sliced
+    ELL for rows <= 64 + one warp per row up to 2048, or the CSR tiles)
+    against the oracle: bit-exact on rows up to a tile, chunked rows
+    (> 2048) within rounding, empty rows zero."""
+    from paper_1607_01404_b200 import _lib
+    m, n = 9000, 700
+    cols = np.concatenate([rng.integers(0, n, 20000),          # short rows of A^T
+                           rng.integers(0, 40, 15000),         # ~375-nonzero rows
+                           np.full(2600, 650), np.full(3000, 651)])  # beyond a tile
+    cols[cols == 699] = 698                                    # one empty row
+    rows = rng.integers(0, m, cols.size)
+    vals = rng.standard_normal(cols.size) * 10.0 ** rng.uniform(-3, 3, cols.size)
+    a, (rp, ci, va) = _csr(m, n, rows, cols, vals)
+    y = rng.standard_normal((m, 4))
+    try:
+        _lib.call("svdsb_tune_set", 5, variant)
+        got = _spmv_dev(a, y, True)
+    finally:
+        _lib.call("svdsb_tune_set", 5, 0)
+    want = ocsr.spmv(m, n, rp, ci, va, y, transpose=True)
+    t_rp = ocsr.csr_transpose(m, n, rp, ci, va)[0]
+    lens = np.diff(t_rp)
+    assert lens.max() > 2048 and ((lens > 64) & (lens <= 2048)).any() and (lens == 0).any()
+    ok = lens <= 2048
+    assert np.array_equal(got[ok], want[ok])
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
 def test_spmv_bulk_copy_path_bit_exact(rng):
     """Matrices of >= 64 MB stream through the cp.async.bulk tile ring
     (csr_tile_bulk_kernel); it must reproduce the reference's summation

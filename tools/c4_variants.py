@@ -49,12 +49,19 @@ b = 4
 x = dv.to_device_block(np.random.default_rng(0).standard_normal((n, b)))
 op = make_normal_operator(SvdOperator.from_csr(a, check=False))
 out = {}
-ref_y = ref_z = None
+ref_y = ref_z = ref_a = None
 for val in values:
     _lib.call("svdsb_tune_set", key, val)
     y = dv.new_block(m, b)
     t = timeit(lambda: dev.matvec(x, y, False))
     byt = 12 * nnz + 4 * (m + 1) + 8 * b * (m + n)
+    yy = dv.to_device_block(np.random.default_rng(1).standard_normal((m, b)))
+    za = dv.new_block(n, b)
+    ta = timeit(lambda: dev.matvec(yy, za, True))
+    same_a = ref_a is None or bool(torch.equal(za, ref_a))
+    if ref_a is None:
+        ref_a = za.clone()
+    ba = 12 * nnz + 4 * (n + 1) + 8 * b * (m + n)
     z = dv.new_block(n, b)
     tn = timeit(lambda: op.apply_into(x, z))
     bn = 2 * (12 * nnz) + 4 * (m + n + 2) + 2 * 8 * b * (m + n)
@@ -75,6 +82,7 @@ for val in values:
     bp = 8 * n * (g + 2 * b)
     extra = {"gram_b4_us": tg * 1e6, "gram_frac": bg / tg / 1e9 / peak, "project_b4_us": tp * 1e6,
              "project_frac": bp / tp / 1e9 / peak, "C_head": float(C[0, 0])}
+    extra.update({"adj_b4_us": ta * 1e6, "adj_frac": ba / ta / 1e9 / peak, "adj_bit_equal": same_a})
     out[val] = {**extra, "fwd_b4_us": t * 1e6, "fwd_frac": byt / t / 1e9 / peak, "normal_b4_us": tn * 1e6,
                 "normal_frac": bn / tn / 1e9 / peak, "fwd_bit_equal": same_y, "normal_bit_equal": same_z}
     print("tune[%d]=%d" % (key, val), json.dumps(out[val]), flush=True)
