@@ -2,7 +2,7 @@
 config 3 (N = 4.1 M, p = 11), config 4 (N = 1 M, p = 24), config 2
 (N = 100 k, p = 6) with g = 35 (25 for config 2); svdsb_tune_set key 3.
 
-python tools/ritz_variants.py
+python tools/ritz_variants.py [key]
 """
 import json
 import sys
@@ -36,6 +36,7 @@ def timeit(fn, reps=10):
 
 
 ctx = dv.context()
+KEY = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 for name, N, g, p in (("c3", 4096000, 35, 11), ("c4", 1000000, 35, 24), ("c2", 100000, 25, 6), ("c4p20", 1000000, 35, 20)):
     gen = torch.Generator(device='cuda').manual_seed(0)
     V = dv.new_block(N, g)
@@ -46,7 +47,7 @@ for name, N, g, p in (("c3", 4096000, 35, 11), ("c4", 1000000, 35, 24), ("c2", 1
     lam = torch.randn(g, dtype=torch.float64, device='cuda', generator=gen)
     ref = None
     for val in (1, 0):
-        _lib.call("svdsb_tune_set", 3, val)
+        _lib.call("svdsb_tune_set", KEY, val)
         R = dv.new_block(N, p)
         rn2 = torch.zeros(p, dtype=torch.float64, device='cuda')
         t = timeit(lambda: dv.ritz_residual(ctx, V, W, Y[:, :p], lam[:p], R, rn2=rn2))
@@ -57,7 +58,7 @@ for name, N, g, p in (("c3", 4096000, 35, 11), ("c4", 1000000, 35, 24), ("c2", 1
         else:
             same = bool(torch.equal(R, ref[0]))
             rel = float(((rn2 - ref[1]).abs() / ref[1]).max())
-        print(name, "tune[3]=%d" % val, json.dumps({"us": round(t * 1e6, 1), "frac": round(byt / t / 1e9 / peak, 3),
+        print(name, "tune[%d]=%d" % (KEY, val), json.dumps({"us": round(t * 1e6, 1), "frac": round(byt / t / 1e9 / peak, 3),
                                                     "R_bit_equal": same,
                                                     "rn2_rel": None if same is None else rel}), flush=True)
-    _lib.call("svdsb_tune_set", 3, 0)
+    _lib.call("svdsb_tune_set", KEY, 0)
