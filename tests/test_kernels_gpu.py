@@ -657,3 +657,49 @@ def test_cgs_fused_matches_pass_by_pass(dim, g, precond, rng):
     assert np.abs(xf - xr).max() <= 1e-12
     assert abs(np.linalg.norm(xf) - 1.0) <= 1e-13
     assert np.abs(q.T @ xf).max() <= 1e-13
+
+
+def test_config4_shape_b4_products_at_hbm_scale(rng):
+    """Config 4's generator at a fifth of its size (2 M x 200 k, ~35 M nnz,
+    every operand larger than L2): the sliced-ELL forward b = 4 product
+    against the oracle bit for bit, and the transposed b = 4 product on the
+    length-sorted sliced ELL against the CSR-tile kernel bit for bit (the
+    oracle's add.at is too slow at this size), with the C-apply passing the
+    adjoint identity <A x, A x> = <x, A^T A x>."""
+    from paper_1607_01404_b200 import SparseMatrixCsr, SvdOperator, _lib, make_normal_operator, workloads
+    dv = _dev()
+    m, n, r, c, v = workloads.c4_coo(m=2_000_000, n=200_000)
+    rp, ci, va = ocsr.csr_from_coo(m, n, r, c, v)
+    del r, c, v
+    a = SparseMatrixCsr(m, n, rp, ci, va)
+    x = rng.standard_normal((n, 4))
+    assert np.array_equal(_spmv_dev(a, x, False), ocsr.spmv(m, n, rp, ci, va, x))
+    y = rng.standard_normal((m, 4))
+    try:
+        _lib.call("svdsb_tune_set", 5, 1)
+        ref_t = _spmv_dev(a, y, True)
+    finally:
+        _lib.call("svdsb_tune_set", 5, 0)
+    assert np.array_equal(_spmv_dev(a, y, True), ref_t)
+    op = make_normal_operator(SvdOperator.from_csr(a, check=False))
+    cx = dv.to_host(op.apply(dv.to_device_block(x)))
+    ax = ocsr.spmv(m, n, rp, ci, va, x)
+    lhs, rhs = (ax * ax).sum(0), (x * cx).sum(0)
+    assert np.all(np.abs(lhs - rhs) <= 1e-11 * np.abs(lhs))
+
+
+def test_config3_full_size_adjoint_identity(rng):
+    """Config 3 at its full size (160^3, 28.5 M nnz): A x bit-exact against
+    the oracle and <A x, y> = <x, A^T y> within rounding."""
+    from paper_1607_01404_b200 import SparseMatrixCsr, workloads
+    m, n, r, c, v = workloads.c3_coo()
+    rp, ci, va = ocsr.csr_from_coo(m, n, r, c, v)
+    del r, c, v
+    a = SparseMatrixCsr(m, n, rp, ci, va)
+    x = rng.standard_normal((n, 1))
+    y = rng.standard_normal((m, 1))
+    ax = _spmv_dev(a, x, False)
+    assert np.array_equal(ax, ocsr.spmv(m, n, rp, ci, va, x))
+    aty = _spmv_dev(a, y, True)
+    lhs, rhs = float((ax * y).sum()), float((x * aty).sum())
+    assert abs(lhs - rhs) <= 1e-12 * np.sqrt(n) * np.abs(ax).max() * np.abs(y).max()
