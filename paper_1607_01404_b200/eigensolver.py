@@ -646,13 +646,26 @@ class DavidsonSolver:
                 self._update_h_full()
                 return
         j = g0 - 1
+        skip_apply = False
+        if (self.spec_fill and self.speculate and self.q is None and not self.comm.distributed
+                and getattr(self.ctx, "handle", None) is not None and init_target - j >= 2
+                and self._budget_left() >= init_target - j):
+            # the whole Krylov fill with device-decided DGKS, one host sync
+            resume = self._krylov_fill_speculative(j, init_target)
+            if resume is None:
+                self.g = init_target
+                self._update_h_full()
+                return
+            j, skip_apply = resume, True
         while True:
             if self._budget_left() < 1:
                 self.status = "budget"
                 self.g = j
                 self._update_h_full()
                 return
-            self._apply_op(self.v[:, j:j + 1], self.w[:, j:j + 1])
+            if not skip_apply:
+                self._apply_op(self.v[:, j:j + 1], self.w[:, j:j + 1])
+            skip_apply = False
             if j + 1 >= init_target:
                 break
             dv.axpby(self.ctx, 1.0, self.w[:, j:j + 1], 0.0, self.v[:, j + 1:j + 2])
@@ -660,6 +673,63 @@ class DavidsonSolver:
             j += 1
         self.g = init_target
         self._update_h_full()
+
+    def _krylov_fill_speculative(self, j0, target):
+        """Krylov fill of eigensolver.py:320-346 (v_{j+1} = orthonormalised
+        Op v_j) with every column's DGKS passes decided on the device and a
+        single status read at the end.  Returns None when every column was
+        accepted, else the column j whose successor must be redone on the
+        host path (W[:, j] is valid and counted; later products are
+        uncounted)."""
+        nspec = target - 1 - j0
+        states = torch.zeros((nspec, 8), dtype=DTYPE, device=self.ctx.device)
+        for k in range(nspec):
+            jj = j0 + k
+            self._apply_op(self.v[:, jj:jj + 1], self.w[:, jj:jj + 1])
+            prior = self._against() + [self.v[:, :jj + 1]]
+            self._spec_cgs(prior, self.w[:, jj:jj + 1], self.v[:, jj + 1:jj + 2], states[k])
+        self._apply_op(self.v[:, target - 1:target], self.w[:, target - 1:target])
+        st = states.cpu().numpy()
+        self.stats.syncs += 1
+        for k in range(nspec):
+            if not (st[k, 0] == 0.0 and st[k, 5] > 0.0):
+                self._uncount_products(target - 1 - (j0 + k))
+                return j0 + k
+        return None
+
+    def _uncount_products(self, ncols):
+        """Undo the matvec accounting of ncols discarded operator columns."""
+        self.stats.matvecs -= ncols
+        self.op.n_applies -= ncols
+        svd_op = getattr(self.op, "svd_op", None)
+        if svd_op is not None:
+            getattr(svd_op, "base", svd_op).n_matvecs -= 2 * ncols
+
+    def _spec_cgs(self, prior, src, dst, st, d=None):
+        """dst = src (./ d) orthonormalised against the prior blocks with
+        device-decided DGKS passes (state into st, no host sync): the one
+        launch of the graphed iterations while the basis is L2-resident,
+        else the pass-by-pass kernels."""
+        total = sum(b.shape[1] for b in prior)
+        ws = self._ws
+        if (ws is not None and self._use_fused_cgs(total) and len(prior) <= _lib.MAX_BLOCKS):
+            n, ptrs, lds, cols, _ = dv._blk_args(prior)
+            blk = dv.as_block(src)
+            _lib.call("svdsb_cgs_fused", self.ctx.handle, self.n, n, ptrs, lds, cols, dv.P(blk), dv.ld_of(blk),
+                      dv.P(ws.zero_i), None if d is None else dv.P(d), dv.P(dst), None, 1, total, 1, None, 1,
+                      self.SPEC_PASSES, dv.P(st), self.ctx.stream)
+            return
+        if d is not None:
+            _lib.call("svdsb_diag_solve", dst.shape[0], dv.P(d), dv.P(src), dv.ld_of(src), dv.P(dst), dv.ld_of(dst),
+                      1, self.ctx.stream)
+        else:
+            dv.axpby(self.ctx, 1.0, src, 0.0, dst)
+        _lib.call("svdsb_dgks_begin", dv.P(st), self.ctx.stream)
+        n, ptrs, lds, cols, _ = dv._blk_args(prior)
+        for p in range(self.SPEC_PASSES):
+            _lib.call("svdsb_cgs_pass", self.ctx.handle, self.n, n, ptrs, lds, cols, dv.P(dst),
+                      dv.P(self.ortho.c), dv.P(st), 1 if p == 0 else 0, self.ctx.stream)
+        dv.scale_cols(self.ctx, dst, st[5:6], dv.SCALE_DIV)
 
     def _update_h_full(self):
         """H = sym(V^T W) (eigensolver.py:349-352)."""
@@ -1301,6 +1371,8 @@ class DavidsonSolver:
     # counters are only advanced when the queued iteration is accepted.
 
     run_ahead = os.environ.get("SVDSB_AHEAD", "1") != "0"
+    # Krylov fill of the initial basis with device-decided DGKS (SVDSB_SPEC_FILL=0: host-driven)
+    spec_fill = os.environ.get("SVDSB_SPEC_FILL", "1") != "0"
     fused_cgs = os.environ.get("SVDSB_CGS_FUSED", "1") != "0"
 
     def _graph_ok(self, b):
