@@ -243,7 +243,7 @@ def run_ours(args):
                    "converged": bool(res.converged.all()), "status": res.status,
                    "stage1_matvecs": res.stats.stage1_matvecs, "stage2_matvecs": res.stats.stage2_matvecs,
                    "outer_iterations": res.stats.outer_iterations, "host_syncs": res.stats.syncs},
-        "spmv_eager_events": {"kernel": "csr_tile_pipe_kernel (CSR SpMV, b=%d), launches outside the graphed "
+        "spmv_eager_events": {"kernel": "CSR SpMV kernels (b=%d), launches outside the graphed "
                                         "iterations (init, restarts, finalisation)" % wl.block,
                               "achieved_gbs": achieved, "frac": achieved / peak, "launches_timed": nl,
                               "avg_launch_us": tot_ms / nl * 1e3 if nl else None, "traffic": traffic},
@@ -256,7 +256,9 @@ def run_ours(args):
         line["roofline"] = roof
         line["iteration_kernels"] = table
     else:
-        line["roofline"] = {"kernel": "csr_tile_pipe_kernel (CSR SpMV, b=%d)" % wl.block, "bound": "hbm",
+        spmv_names = ("csr_sell4_kernel + csr_sell4t_kernel (sliced-ELL CSR SpMV, b=4)" if wl.block == 4 else
+                      "csr_tile_pipe / csr_tile_bulk kernels (CSR SpMV, b=%d)" % wl.block)
+        line["roofline"] = {"kernel": spmv_names, "bound": "hbm",
                             "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
                             "frac": achieved / peak, "traffic": traffic,
                             "algorithmic_bytes_per_launch": tot_bytes / nl if nl else None,
