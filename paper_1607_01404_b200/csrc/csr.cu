@@ -1904,15 +1904,24 @@ __global__ void seg_bounds_kernel(int64_t n, const int *__restrict__ rp, const i
   len_out[j] = b - a;
 }
 
-__global__ void seg_copy_kernel(int64_t n, const int *__restrict__ col, const double *__restrict__ val,
+// One thread per nonzero of the block (a thread per row serialised the
+// Zipf head rows: 1 s for config 4): the row of output q is the last j
+// with rpk[j] <= q.
+__global__ void seg_copy_kernel(int64_t n, int64_t nnzk, const int *__restrict__ col, const double *__restrict__ val,
                                 const int *__restrict__ lo, const int *__restrict__ rpk, int r0, int *__restrict__ colk,
                                 double *__restrict__ valk) {
-  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const int src = lo[j], dst = rpk[j], len = rpk[j + 1] - rpk[j];
-  for (int i = 0; i < len; ++i) {
-    colk[dst + i] = col[src + i] - r0;
-    valk[dst + i] = val[src + i];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnzk; q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = 0, b = n;  // rpk[a] <= q < rpk[b]
+    while (b - a > 1) {
+      const int64_t mid = (a + b) >> 1;
+      if (rpk[mid] <= q)
+        a = mid;
+      else
+        b = mid;
+    }
+    const int64_t src = lo[a] + (q - rpk[a]);
+    colk[q] = col[src] - r0;
+    valk[q] = val[src];
   }
 }
 
@@ -1950,8 +1959,11 @@ static int build_blocked_transpose(svdsb_csr *h, cudaStream_t st) {
     p.nnz = p.host_row_ptr[n];
     SVDSB_CUDA(alloc_pad(&p.col, std::max<int64_t>(p.nnz, 1), st));
     SVDSB_CUDA(alloc_pad(&p.val, std::max<int64_t>(p.nnz, 1), st));
-    seg_copy_kernel<<<grid1(n), 256, 0, st>>>(n, at.col, at.val, lo, p.row_ptr, (int)r0, p.col, p.val);
-    SVDSB_LAUNCHED();
+    if (p.nnz > 0) {
+      seg_copy_kernel<<<(unsigned)std::min<int64_t>((p.nnz + 255) / 256, 16 * kNumSMs), 256, 0, st>>>(
+          n, p.nnz, at.col, at.val, lo, p.row_ptr, (int)r0, p.col, p.val);
+      SVDSB_LAUNCHED();
+    }
     int rc = build_partition(p, st);
     if (rc) return rc;
     h->atb.push_back(std::move(p));

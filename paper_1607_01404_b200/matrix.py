@@ -192,12 +192,19 @@ class SparseMatrixCsr:
         values = t(values, np.float64)
         if not (rows.shape == cols.shape == values.shape):
             raise ValueError("triplet arrays must have equal length")
+        ctx = context(device)
+        rows = rows.to(device=ctx.device, dtype=torch.int64, non_blocking=True)
+        cols = cols.to(device=ctx.device, dtype=torch.int64, non_blocking=True)
+        values = values.to(device=ctx.device, dtype=torch.float64, non_blocking=True)
         if rows.numel():
-            if int(rows.min()) < 0 or int(rows.max()) >= m:
+            # range checks (matio.py:41-52) on the device copies: one
+            # read-back of four extremes instead of four host passes
+            ext = torch.stack([rows.min(), rows.max(), cols.min(), cols.max()]).cpu()
+            if int(ext[0]) < 0 or int(ext[1]) >= m:
                 raise ValueError("row index out of range")
-            if int(cols.min()) < 0 or int(cols.max()) >= n:
+            if int(ext[2]) < 0 or int(ext[3]) >= n:
                 raise ValueError("column index out of range")
-        dev = DeviceCsr.from_coo_device(m, n, rows, cols, values, device=device)
+        dev = DeviceCsr.from_coo_device(m, n, rows, cols, values, device=ctx.device)
         return cls._from_device(dev)
 
     @classmethod

@@ -703,3 +703,20 @@ def test_config3_full_size_adjoint_identity(rng):
     aty = _spmv_dev(a, y, True)
     lhs, rhs = float((ax * y).sum()), float((x * aty).sum())
     assert abs(lhs - rhs) <= 1e-12 * np.sqrt(n) * np.abs(ax).max() * np.abs(y).max()
+
+
+def test_from_coo_range_checks():
+    """Index validation of SparseMatrixCsr.from_coo (matio.py:41-52), done on
+    the device copies: ValueError for rows >= m, negative columns, columns
+    >= n; equal-length check on the host."""
+    from paper_1607_01404_b200 import SparseMatrixCsr
+    ok = (np.array([0, 1]), np.array([0, 2]), np.array([1.0, 2.0]))
+    SparseMatrixCsr.from_coo(2, 3, *ok)
+    with pytest.raises(ValueError, match="row index"):
+        SparseMatrixCsr.from_coo(2, 3, np.array([0, 2]), ok[1], ok[2])
+    with pytest.raises(ValueError, match="column index"):
+        SparseMatrixCsr.from_coo(2, 3, ok[0], np.array([-1, 0]), ok[2])
+    with pytest.raises(ValueError, match="column index"):
+        SparseMatrixCsr.from_coo(2, 3, ok[0], np.array([0, 3]), ok[2])
+    with pytest.raises(ValueError, match="equal length"):
+        SparseMatrixCsr.from_coo(2, 3, ok[0], ok[1], np.array([1.0]))
