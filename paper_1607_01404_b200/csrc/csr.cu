@@ -1446,8 +1446,13 @@ static int build_sell(CsrPart &p, cudaStream_t st, bool sorted = false) {
     if (rcm) return rcm;
     p.nmid = (int)mid.size();
     p.mid_rows = dmid;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int a, int b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
+    // stable counting sort by length, longest first (lengths <= kSellTMax)
+    std::vector<int64_t> start(kSellTMax + 2, 0);
+    for (int r : order) start[kSellTMax - (rp[r + 1] - rp[r]) + 1]++;
+    for (int k = 1; k <= kSellTMax + 1; ++k) start[k] += start[k - 1];
+    std::vector<int> sorted_rows(order.size());
+    for (int r : order) sorted_rows[start[kSellTMax - (rp[r + 1] - rp[r])]++] = r;
+    order.swap(sorted_rows);
   }
   const int64_t nq = sorted ? (int64_t)order.size() : p.rows;
   auto row_of = [&](int64_t q) -> int64_t { return sorted ? order[q] : q; };
