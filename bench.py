@@ -247,6 +247,7 @@ def run_ours(args):
                                         "iterations (init, restarts, finalisation)" % wl.block,
                               "achieved_gbs": achieved, "frac": achieved / peak, "launches_timed": nl,
                               "avg_launch_us": tot_ms / nl * 1e3 if nl else None, "traffic": traffic},
+        "per_step_ms": [round(t, 3) for t in step_ms],
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
