@@ -148,7 +148,57 @@ def solves():
     dump("solves.json", out)
 
 
+# Full-size config 2 (the benchmarked solve) and mid-scale instances of the
+# config 3-largest and config 4 generators, solved by the reference.  Besides
+# sigma / stats / residuals this records sha256 digests of the reference's
+# fp64 U and V (the oracle restatement must reproduce them bit for bit) and a
+# float32 copy of V (npz next to this file) for the principal-angle checks of
+# the device solves: float32 rounding keeps the angle floor near 1e-7.
+BIG = {
+    "c2_full": ("c2", {}),
+    "c3L_40": ("c3L", {"nx": 40}),
+    "c4_mid": ("c4", {"m": 500_000, "n": 50_000}),
+}
+
+
+def big(keys=None):
+    path = os.path.join(HERE, "big_solves.json")
+    out = {}
+    if os.path.exists(path):
+        with open(path) as f:
+            out = json.load(f)
+    for name, (key, kw) in BIG.items():
+        if keys and name not in keys:
+            continue
+        wl = workloads.CONFIGS[key]
+        m, n, r, c, v = wl.build(**kw)
+        a = SparseMatrixCsr.from_coo(m, n, r, c, v)
+        pre = itersvd.jacobi_precond_on_normal(a, side="auto") if wl.precond else None
+        cfg = itersvd.SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0)
+        t0 = time.perf_counter()
+        res = itersvd.svds_solve(a, precond=pre, cfg=cfg)
+        sec = time.perf_counter() - t0
+        s = res.stats
+        rec = {"sigma": res.sigma.tolist(), "rnorms": res.rnorms.tolist(),
+               "converged": [bool(x) for x in res.converged], "status": res.status,
+               "stage1_matvecs": s.stage1_matvecs, "stage2_matvecs": s.stage2_matvecs,
+               "precond_applies": s.precond_applies, "restarts": s.restarts, "resets": s.resets,
+               "seconds": sec, "config": key, "kwargs": kw, "m": m, "n": n, "nnz": int(a.nnz),
+               "csr": csr_digest(a), "u_digest": digest(np.asfortranarray(res.u)),
+               "v_digest": digest(np.asfortranarray(res.v)), "a_norm_fro": float(np.linalg.norm(a.values))}
+        np.savez_compressed(os.path.join(HERE, "vectors_%s.npz" % name), v=res.v.astype(np.float32),
+                            sigma=res.sigma)
+        out[name] = rec
+        print(name, "%.1f s" % sec, rec["stage1_matvecs"], rec["stage2_matvecs"], rec["status"], flush=True)
+        with open(path, "w") as f:
+            json.dump(out, f, indent=1)
+    print("wrote big_solves.json")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:2] == ["big"]:
+        big(sys.argv[2:])
+        sys.exit(0)
     what = sys.argv[1:] or ["fixtures", "generators", "spmv", "solves"]
     for w in what:
         globals()[w]()

@@ -126,3 +126,32 @@ def test_port_matches_reference_fixture_values():
         for target in ("largest", "smallest"):
             out = phsvds.svds(mat, 5, target, 1e-12, seed=seed)
             assert np.abs(out["sigma"] - np.array(rec[target + "5"])).max() <= rec["sigma_max"] * 1e-11
+
+
+def _big_case(name):
+    from paper_1607_01404_b200 import workloads
+    gold = load_golden("big_solves.json")[name]
+    wl = workloads.CONFIGS[gold["config"]]
+    m, n, r, c, v = wl.build(**gold["kwargs"])
+    mat = phsvds.Csr(m, n, *ocsr.csr_from_coo(m, n, r, c, v))
+    return gold, wl, mat
+
+
+@pytest.mark.parametrize("name", ["c2_full", "c3L_40",
+                                  pytest.param("c4_mid", marks=pytest.mark.skipif(
+                                      not __import__("os").environ.get("SVDSB_SLOW_TESTS"),
+                                      reason="~3 min of CPU: set SVDSB_SLOW_TESTS=1"))])
+def test_port_reproduces_reference_big_solves(name):
+    """Full-size config 2 (the benchmarked solve) and mid-scale configs 3L /
+    4: the port returns the reference's sigma, U and V bit for bit
+    (big_solves.json digests, made by tests/golden/make_golden.py big)."""
+    gold, wl, mat = _big_case(name)
+    assert ogen.csr_digest(mat.row_ptr, mat.col_idx, mat.values) == gold["csr"]
+    pre = phsvds.Jacobi(mat, "auto") if wl.precond else None
+    out = phsvds.svds(mat, wl.k, wl.which, wl.tol, seed=0, block=wl.block, precond=pre)
+    assert np.array_equal(out["sigma"], np.array(gold["sigma"]))
+    assert out["stage1_matvecs"] == gold["stage1_matvecs"]
+    assert out["stage2_matvecs"] == gold["stage2_matvecs"]
+    assert out["restarts"] == gold["restarts"]
+    assert _digest(np.asfortranarray(out["u"])) == gold["u_digest"]
+    assert _digest(np.asfortranarray(out["v"])) == gold["v_digest"]
