@@ -1,31 +1,45 @@
-"""Benchmark: time-to-k-triplets of the device PHSVDS solve on BASELINE
-config 2 (200,000 x 100,000 random sparse, 8 N(0,1) per row + unit
-diagonal, k=5 smallest, tol 1e-10, point-Jacobi preconditioner).
+"""Benchmark: time-to-k-triplets of the device PHSVDS solve.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2]
+                    [--config c4|c2|c1|c3L|c3S|c5] [--budget MATVECS]
+
+Default workload: BASELINE config 4 (10,000,000 x 1,000,000 Zipf(1.1)
+power-law sparse, 20 draws per row, k = 20 largest, tol 1e-6, block 4) --
+the largest BASELINE configuration that fits one B200.  ``--config c2``
+selects config 2 (200,000 x 100,000 random sparse, k = 5 smallest, tol
+1e-10, point-Jacobi), the configuration of the round-1 headline.
 
 One "step" is one full svds_solve (both stages as needed) with the matrix
-and preconditioner already resident in HBM; value = mean seconds per solve
-(max over ranks; lower is better).  ``e2e`` is the same solve through the
-reference-facing binding (pysvds.svds) from host COO arrays, host->device
-and device->host copies included.  ``roofline`` is the dominant kernel of
-the graphed iteration (``iteration_kernels`` lists every kernel with its
-per-launch time -- a CUDA graph of 100 back-to-back launches on this
-workload's matrix, timed with CUDA events on the launching stream -- and
-its share of the step); ``kernels_at_hbm_scale`` repeats the hot kernels at
-config-3 size where every operand streams from HBM.  ``cpu_baseline`` is the CPU
-oracle port (oracle/phsvds.py, bit-identical to the reference) on a
-bounded sample of the same workload.
+(and preconditioner) already resident in HBM; ``value`` = mean seconds per
+solve (max over ranks; lower is better).  ``e2e`` is the same solve through
+the reference-facing binding (pysvds.svds) from host COO triplets in pinned
+memory: host->device copy, device CSR assembly, solve and device->host read
+of (sigma, U, V, rnorms) inside the timed region.
 
-With --gpus N > 1 (torchrun) the same solve runs row-sharded over the N
-ranks (nnz-balanced row blocks, NCCL collectives):
-total work fixed, so scaling is "strong".
+``roofline``: on config 4 the dominant operation of the step is the
+normal-operator apply C X = A^T (A X) at b = 4 (sliced-ELL forward product
+plus the column-blocked transposed products); its algorithmic bytes
+ over its average duration, measured with CUDA events on
+the launching stream around every C-apply inside the timed steps.  On the
+b = 1 configurations (c1, c2) it is the dominant kernel of the graphed
+iteration.  ``cpu_baseline``: the CPU oracle (oracle/phsvds.py, bit-identical
+to the reference) on a bounded sample of the same workload.
+
+``--budget MATVECS`` runs a fixed-budget solve (SURVEY 8(d) protocol for
+configs that do not converge in practical time: c3S, c5) and reports time
+per outer iteration and per matvec beside the solve time.
+
+With --gpus N > 1 the script re-launches itself under torch.distributed.run
+(one rank per GPU, NCCL) unless it already runs under it; every rank
+assembles only its nnz-balanced row block of A (dist.py) and the same solve
+runs row-sharded: total work fixed, so scaling is "strong" (c5 grows with
+N: "weak").
 """
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -40,8 +54,11 @@ METRIC = "time-to-k-triplets"
 UNIT = "s"
 PEAKS_FILE = os.path.join(REPO, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0
-REF_SAMPLE_MATVECS = 150     # budget of one bounded reference step
-CPU_BASELINE_MATVECS = 300   # budget of the cpu_baseline sample
+# matvecs of the full solves: the reference's own count where it ran (c1, c2
+# at full size: tests/golden/solves.json, big_solves.json); for configs the
+# reference cannot finish in practical time, the device solve's count
+FULL_MATVECS = {"c1": 1792, "c2": 950, "c3L": 5316, "c4": 956}
+FULL_SOLVE_REF = ("c1", "c2")        # reference arm times the full solve per step
 
 
 def parse():
@@ -50,7 +67,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--budget", type=int, default=None, help="fixed max_matvecs per solve (SURVEY 8(d))")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-scale", action="store_true", help="skip the config-3 kernel roofline section")
@@ -66,21 +84,52 @@ def dist_env():
     return world, rank, local
 
 
-def workload(key):
-    from paper_1607_01404_b200 import workloads
-    wl = workloads.CONFIGS[key]
-    return wl, wl.build()
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
-def config_json(wl, m, n, nnz, world):
-    return {"workload": "BASELINE config %s: %s" % (wl.name[1], wl.note), "m": m, "n": n, "nnz": nnz,
-            "k": wl.k, "which": wl.which, "tol": wl.tol, "block": wl.block,
-            "precond": "jacobi" if wl.precond else None, "seed_matrix": int(wl.name[1]), "seed_solver": 0,
-            "parallelism": "row-sharded x%d (NCCL all-reduce / all-gather / reduce-scatter)" % world
-            if world > 1 else "single",
-            "l2": "flushed before every timed step (256 MiB write); the solve's working set (CSR A + A^T "
-                  "41 MB, basis V/W 56 MB, ...) does not stay L2-resident: warm-cache ncu shows the basis "
-                  "kernels reading their algorithmic bytes from DRAM (profiles/r01_warm_c2.json)"}
+def maybe_spawn(args):
+    """--gpus N: run as N ranks.  Under torchrun WORLD_SIZE must equal N;
+    otherwise re-exec this script under torch.distributed.run (one process
+    per GPU).  Fails loudly instead of silently timing one GPU."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
+        return
+    if args.gpus <= 1:
+        return
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit("bench.py: --gpus %d but only %d CUDA device(s) visible" % (args.gpus, have))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def config_json(wl, m, n, nnz, world, budget=None):
+    out = {"workload": "BASELINE config %s: %s" % (wl.name[1:], wl.note), "m": m, "n": n, "nnz": nnz,
+           "k": wl.k, "which": wl.which, "tol": wl.tol, "block": wl.block,
+           "precond": "jacobi" if wl.precond else None, "seed_matrix": int(wl.name[1]), "seed_solver": 0,
+           "parallelism": ("row-sharded x%d (nnz-balanced row blocks; NCCL all-reduce / all-gather or halo / "
+                           "reduce-scatter)" % world) if world > 1 else "single"}
+    if budget:
+        out["max_matvecs"] = budget
+    if wl.name == "c2":
+        out["l2"] = ("flushed before every timed step (256 MiB write); the solve's working set (CSR A + A^T "
+                     "41 MB, basis V/W 56 MB, ...) does not stay L2-resident: warm-cache ncu shows the basis "
+                     "kernels reading their algorithmic bytes from DRAM (profiles/r01_warm_c2.json)")
+    else:
+        out["l2"] = ("inputs larger than L2 (CSR of A and A^T %.1f GB, basis blocks of %d rows) and L2 flushed "
+                     "before every timed step" % (24e-9 * nnz, n))
+    return out
 
 
 # ------------------------------------------------------------------ clocks
@@ -140,39 +189,60 @@ def spmv_bytes(m, n, nnz, b, transpose):
 def peak_hbm():
     try:
         with open(PEAKS_FILE) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return FALLBACK_HBM, "fallback"
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(key):
+    """ncu dram read+write bytes per launch (profiles/traffic_<cfg>.json)."""
+    tf = os.path.join(REPO, "profiles", "traffic_%s.json" % key)
+    if not os.path.exists(tf):
+        return {}
+    with open(tf) as f:
+        return json.load(f).get("dram_bytes_per_launch", {})
+
+
+def build_problem(wl, world, rank, dev):
+    """Host COO of the workload (c5 scaled by the world size) and the
+    operator: one device CSR on a single GPU, this rank's row block
+    otherwise (each rank assembles only its own rows)."""
+    from paper_1607_01404_b200 import SparseMatrixCsr, jacobi_precond_on_normal
+    kw = {"gpus": world} if wl.name == "c5" else {}
+    m, n, r, c, v = wl.build(**kw)
+    if world > 1:
+        from paper_1607_01404_b200.dist import Comm, DistSvdOperator, dist_jacobi
+        comm = Comm()
+        a = DistSvdOperator.from_coo(comm, m, n, r, c, v, device=dev)
+        pre = dist_jacobi(a) if wl.precond else None
+        return (m, n, r, c, v), a, pre, a.nnz_global
+    a = SparseMatrixCsr.from_coo(m, n, r, c, v)
+    pre = jacobi_precond_on_normal(a, side="auto") if wl.precond else None
+    return (m, n, r, c, v), a, pre, a.nnz
 
 
 def run_ours(args):
     import torch
     import torch.distributed as tdist
 
-    from paper_1607_01404_b200 import (SparseMatrixCsr, SvdsConfig, _lib, jacobi_precond_on_normal, matrix,
-                                       svds_solve)
-    from paper_1607_01404_b200 import pysvds
+    from paper_1607_01404_b200 import SvdsConfig, _lib, matrix, pysvds, svds_solve, workloads
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     for kv in args.tune:
         key, val = kv.split("=")
         _lib.call("svdsb_tune_set", int(key), int(val))
     if world > 1:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    wl, (m, n, r, c, v) = workload(args.config)
-    a = SparseMatrixCsr.from_coo(m, n, r, c, v)
-    pre = jacobi_precond_on_normal(a, side="auto") if wl.precond else None
-    if world > 1:
-        # row-sharded solve over NCCL: each rank keeps
-        # its nnz-balanced row block of A (and its transpose)
-        from paper_1607_01404_b200.dist import Comm, DistSvdOperator, local_jacobi
-        comm = Comm()
-        full = a
-        a = DistSvdOperator.from_host_csr(comm, m, n, full.row_ptr, full.col_idx, full.values, device=dev)
-        pre = local_jacobi(a, full) if wl.precond else None
-    cfg = lambda: SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0)  # noqa
+        tdist.init_process_group("nccl", device_id=dev)
+    wl = workloads.CONFIGS[args.config]
+    t0 = time.perf_counter()
+    (m, n, r, c, v), a, pre, nnz = build_problem(wl, world, rank, dev)
+    setup_s = time.perf_counter() - t0
+
+    def cfg():
+        return SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0,
+                          max_matvecs=args.budget)
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
@@ -209,75 +279,152 @@ def run_ours(args):
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
 
-    # SpMV roofline from the events recorded around every launch
-    tot_bytes, tot_ms, nl = 0.0, 0.0, 0
-    nnz_r = a.local_csr.nnz if world > 1 else a.nnz
+    # SpMV / C-apply events recorded around every eager launch of the timed
+    # steps (on the solver's stream)
     m_r = a.m_loc if world > 1 else m
+    nnz_r = a.local_nnz if world > 1 else nnz
+    by_kind = {}
     for prof in prof_all:
         for kind, b, s0, s1 in prof:
             if kind == "normal":
                 byt = spmv_bytes(m_r, n, nnz_r, b, False) + spmv_bytes(m_r, n, nnz_r, b, True)
-                nl += 2
             else:
                 byt = spmv_bytes(m_r, n, nnz_r, b, kind == "adj")
-                nl += 1
-            tot_bytes += byt
-            tot_ms += s0.elapsed_time(s1)
-    nnz = full.nnz if world > 1 else a.nnz
+            key = (kind, b)
+            tb, tm, cnt = by_kind.get(key, (0.0, 0.0, 0))
+            by_kind[key] = (tb + byt, tm + s0.elapsed_time(s1), cnt + 1)
     peak, peak_kind = peak_hbm()
-    achieved = (tot_bytes / nl) / (tot_ms / nl * 1e-3) / 1e9 if nl else 0.0
-    spmv_share = tot_ms / float(np.sum(step_ms)) if step_ms else 0.0
-    traffic = None
-    tf = os.path.join(REPO, "profiles", "spmv_traffic_%s.json" % args.config)
-    if os.path.exists(tf):
-        with open(tf) as f:
-            traffic = json.load(f).get("bytes_per_launch")
+    total_step_ms = float(np.sum(step_ms))
+    spmv_live = [{"op": "%s b=%d" % k, "launches": cnt, "avg_us": tm / cnt * 1e3,
+                  "algorithmic_bytes_per_launch": tb / cnt, "gbs": tb / (tm * 1e-3) / 1e9,
+                  "frac": tb / (tm * 1e-3) / 1e9 / peak, "share_of_step": tm / total_step_ms}
+                 for k, (tb, tm, cnt) in sorted(by_kind.items(), key=lambda kv: -kv[1][1])]
 
+    iters = res.stats.outer_iterations
+    mv = res.stats.stage1_matvecs + res.stats.stage2_matvecs
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "strong" if world > 1 else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator of BASELINE config %s)" %
-        wl.name[1], "config": config_json(wl, m, n, nnz, world),
+        "scaling": ("weak" if wl.name == "c5" else "strong") if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator of BASELINE config %s; random draws, no dataset)" % wl.name[1:],
+        "config": config_json(wl, m, n, nnz, world, args.budget),
         "result": {"sigma": [float(s) for s in res.sigma], "rnorms_max": float(res.rnorms.max()),
-                   "converged": bool(res.converged.all()), "status": res.status,
+                   "converged": int(res.converged.sum()), "status": res.status,
                    "stage1_matvecs": res.stats.stage1_matvecs, "stage2_matvecs": res.stats.stage2_matvecs,
-                   "outer_iterations": res.stats.outer_iterations, "host_syncs": res.stats.syncs},
-        "spmv_eager_events": {"kernel": "CSR SpMV kernels (b=%d), launches outside the graphed "
-                                        "iterations (init, restarts, finalisation)" % wl.block,
-                              "achieved_gbs": achieved, "frac": achieved / peak, "launches_timed": nl,
-                              "avg_launch_us": tot_ms / nl * 1e3 if nl else None, "traffic": traffic},
+                   "outer_iterations": iters, "restarts": getattr(res.stats, "restarts", None),
+                   "host_syncs": res.stats.syncs},
         "per_step_ms": [round(t, 3) for t in step_ms],
+        "per_iteration_ms": ms / max(iters, 1), "per_matvec_us": ms * 1e3 / max(mv, 1),
+        "setup_s": setup_s, "spmv_live_events": spmv_live,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    traffic = load_traffic(wl.name)
     if world == 1 and wl.block == 1:
-        roof, table = iteration_kernels(a, pre, wl, peak, res.stats.outer_iterations, step_ms)
+        roof, table = iteration_kernels(a, pre, wl, peak, iters, step_ms)
         roof["peak_source"] = peak_kind
         line["roofline"] = roof
         line["iteration_kernels"] = table
     else:
-        spmv_names = ("csr_sell4_kernel + csr_sell4t_kernel (sliced-ELL CSR SpMV, b=4)" if wl.block == 4 else
-                      "csr_tile_pipe / csr_tile_bulk kernels (CSR SpMV, b=%d)" % wl.block)
-        line["roofline"] = {"kernel": spmv_names, "bound": "hbm",
-                            "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
-                            "frac": achieved / peak, "traffic": traffic,
-                            "algorithmic_bytes_per_launch": tot_bytes / nl if nl else None,
-                            "avg_launch_us": tot_ms / nl * 1e3 if nl else None, "share_of_step": spmv_share,
-                            "method": "CUDA events around every eagerly launched SpMV of the timed steps"}
-
-    if not args.no_e2e and world == 1:
-        line["e2e"] = e2e(args, wl, m, n, r, c, v, pysvds, barrier)
+        key = ("normal", wl.block)
+        tb, tm, cnt = by_kind.get(key, (0.0, 0.0, 0))
+        if not cnt:
+            key = max(by_kind, key=lambda k: by_kind[k][1])
+            tb, tm, cnt = by_kind[key]
+        achieved = tb / (tm * 1e-3) / 1e9
+        line["roofline"] = {
+            "kernel": "C-apply A^T(A X), b=%d: sliced-ELL forward + column-blocked transposed SpMV kernels "
+                      "(csr_sell*, csr_chunk, csr_long_fixup; the dominant operation of the step)" % wl.block,
+            "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic.get("normal_b%d" % wl.block),
+            "algorithmic_bytes_per_launch": tb / cnt, "avg_launch_us": tm / cnt * 1e3, "launches": cnt,
+            "share_of_step": tm / total_step_ms,
+            "method": "CUDA events on the solver's stream around every C-apply of the %d timed steps; "
+                      "algorithmic bytes = A.X + A^T.Y per SURVEY 8(d) (the m x b intermediate counted "
+                      "written and read)" % args.steps}
+        if world == 1:
+            line["block_kernels"] = block_kernels(a, wl, peak, traffic)
+    if not args.no_e2e:
+        line["e2e"] = e2e(args, wl, (m, n, r, c, v), pysvds, barrier, world, rank, dev)
     if world == 1 and not args.no_scale:
         line["kernels_at_hbm_scale"] = kernels_at_scale(peak)
-    if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(wl, m, n, r, c, v, res.stats.stage1_matvecs + res.stats.stage2_matvecs,
-                                            CPU_BASELINE_MATVECS)
+    if rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(wl, a if world == 1 else None, (m, n, r, c, v), pre is not None,
+                                            res.stats.stage1_matvecs + res.stats.stage2_matvecs, args.budget)
     if world > 1:
         tdist.barrier()
         tdist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def block_kernels(a, wl, peak, traffic):
+    """Per-launch device time of the block (b = 4) kernels on this
+    workload's matrix: forward / transposed SpMV, the C-apply, and the
+    tall-skinny basis kernels at N = n with g = 35, p = k + b (every operand
+    larger than L2 on config 4; L2 flushed before each timed launch)."""
+    import torch
+    from paper_1607_01404_b200 import SvdOperator, make_normal_operator
+    from paper_1607_01404_b200 import device as dv
+    m, n, nnz, b = a.m, a.n, a.nnz, wl.block
+    dcsr = a.device_csr()
+    ctx = dv.context()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    def timed(fn, reps=10):
+        for _ in range(2):
+            fn()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        return float(np.median(ts))
+
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    x = dv.new_block(n, b)
+    x.copy_(torch.randn(b, n, dtype=torch.float64, device="cuda", generator=gen).t())
+    y = dv.new_block(m, b)
+    y.copy_(torch.randn(b, m, dtype=torch.float64, device="cuda", generator=gen).t())
+    yo = dv.new_block(m, b)
+    z = dv.new_block(n, b)
+    op = make_normal_operator(SvdOperator.from_csr(a, check=False))
+    g, p, s = 35, min(wl.k + b, 35), 15
+    V = dv.new_block(n, g)
+    V.copy_(torch.randn(g, n, dtype=torch.float64, device="cuda", generator=gen).t())
+    W = dv.new_block(n, g)
+    W.copy_(torch.randn(g, n, dtype=torch.float64, device="cuda", generator=gen).t())
+    Y = dv.to_device_block(np.linalg.qr(np.random.default_rng(2).standard_normal((g, g)))[0])
+    lam = torch.randn(g, dtype=torch.float64, device="cuda", generator=gen)
+    R = dv.new_block(n, p)
+    rn2 = torch.zeros(p, dtype=torch.float64, device="cuda")
+    C = dv.small_matrix(g, b)
+    nr = torch.zeros(b, dtype=torch.float64, device="cuda")
+    V2 = dv.new_block(n, s)
+    cases = [
+        ("spmv_fwd_b%d" % b, lambda: dcsr.matvec(x, yo, False), spmv_bytes(m, n, nnz, b, False)),
+        ("spmv_adj_b%d" % b, lambda: dcsr.matvec(y, z, True), spmv_bytes(m, n, nnz, b, True)),
+        ("normal_b%d" % b, lambda: op.apply_into(x, z),
+         spmv_bytes(m, n, nnz, b, False) + spmv_bytes(m, n, nnz, b, True)),
+        ("gram_b%d_g35" % b, lambda: dv.gram(ctx, n, [V], x, C, norms2=nr), 8 * n * (g + b)),
+        ("project_b%d_g35" % b, lambda: dv.project_out(ctx, n, [V], C, x, norms2=nr), 8 * n * (g + 2 * b)),
+        ("ritz_residual_g35_p%d" % p, lambda: dv.ritz_residual(ctx, V, W, Y[:, :p], lam[:p], R, rn2=rn2),
+         8 * n * (2 * g + p)),
+        ("restart_ts_gemm_35to15", lambda: dv.ts_gemm(ctx, V, Y[:, :s], V2), 8 * n * (g + s)),
+    ]
+    out = {"workload": "this workload's matrix (m=%d, n=%d, nnz=%d), basis g=%d" % (m, n, nnz, g),
+           "peak_gbs": peak, "method": "CUDA events on the launching stream, L2 flushed, median of 10"}
+    for name, fn, byt in cases:
+        t = timed(fn)
+        out[name] = {"us": t * 1e6, "gbs": byt / t / 1e9, "frac": byt / t / 1e9 / peak,
+                     "algorithmic_bytes": byt, "ncu_dram_bytes": traffic.get(name)}
+    return out
 
 
 def iteration_kernels(a, pre, wl, peak, iters, step_ms, g=25):
@@ -497,106 +644,184 @@ def kernels_at_scale(peak):
     return out
 
 
-def e2e(args, wl, m, n, r, c, v, pysvds, barrier):
-    """Same solve through the reference-facing binding from host COO:
-    pysvds.svds((rows, cols, vals, shape), ...) with the Jacobi
-    preconditioner; host->device copy of the triplets, device CSR assembly,
-    the solve and the device->host read of (sigma, u, v, rnorms) inside the
-    timed region."""
+def e2e(args, wl, coo, pysvds, barrier, world, rank, dev):
+    """Same solve through the public API from host COO triplets in pinned
+    memory: host->device copy of the triplets, device CSR assembly, the
+    solve and the device->host read of (sigma, u, v, rnorms) inside the
+    timed region.  One GPU: pysvds.svds (the reference binding's entry
+    point) on SparseMatrixCsr.from_coo.  N ranks: each rank copies only its
+    own row block's triplets, assembles it (DistSvdOperator.from_coo) and
+    reads back its rows of U / V after svds_solve."""
     import torch
-    from paper_1607_01404_b200 import SparseMatrixCsr, jacobi_precond_on_normal
-    rows_p = torch.from_numpy(r).pin_memory()
-    cols_p = torch.from_numpy(c).pin_memory()
-    vals_p = torch.from_numpy(v).pin_memory()
+    from paper_1607_01404_b200 import SparseMatrixCsr, SvdsConfig, jacobi_precond_on_normal, svds_solve
+    m, n, r, c, v = coo
     times = []
-    h2d = int(r.nbytes + c.nbytes + v.nbytes)
+    if world > 1:
+        from paper_1607_01404_b200.dist import Comm, DistSvdOperator, dist_jacobi, partition_coo
+        comm = Comm()
+        sel, _, _ = partition_coo(comm, m, n, r)
+        r, c, v = r[sel], c[sel], v[sel]
+    rows_p = torch.from_numpy(np.ascontiguousarray(r)).pin_memory()
+    cols_p = torch.from_numpy(np.ascontiguousarray(c)).pin_memory()
+    vals_p = torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+    h2d = int(rows_p.numel() * 8 * 3)
     d2h = 0
     warm = 2  # the first two fresh matrices grow the device memory pool (two live at once)
     for i in range(max(args.steps, 15) + warm):
         barrier()
         t0 = time.perf_counter()
-        a = SparseMatrixCsr.from_coo(m, n, rows_p, cols_p, vals_p)
-        pre = jacobi_precond_on_normal(a, side="auto") if wl.precond else None
-        sigma, u, vv, rn, stats = pysvds.svds(a, k=wl.k, which="S" if wl.which == "smallest" else "L",
-                                              tol=wl.tol, seed=0, precond=pre, max_block_size=wl.block)
+        if world > 1:
+            a = DistSvdOperator.from_coo(comm, m, n, rows_p, cols_p, vals_p, device=dev, presharded=True)
+            pre = dist_jacobi(a) if wl.precond else None
+            res = svds_solve(a, precond=pre, cfg=SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol,
+                                                             max_block_size=wl.block, seed=0,
+                                                             max_matvecs=args.budget))
+            sigma, u, vv, rn = res.sigma, res.u, res.v, res.rnorms
+        else:
+            a = SparseMatrixCsr.from_coo(m, n, rows_p, cols_p, vals_p)
+            pre = jacobi_precond_on_normal(a, side="auto") if wl.precond else None
+            sigma, u, vv, rn, _ = pysvds.svds(a, k=wl.k, which="S" if wl.which == "smallest" else "L",
+                                              tol=wl.tol, seed=0, precond=pre, max_block_size=wl.block,
+                                              max_matvecs=args.budget)
         barrier()
         dt = time.perf_counter() - t0
         d2h = int(sigma.nbytes + u.nbytes + vv.nbytes + rn.nbytes)
+        del a, pre
         if i >= warm:
             times.append(dt)
+    if world > 1:
+        import torch.distributed as tdist
+        tt = torch.tensor(times, dtype=torch.float64, device=dev)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        times = tt.cpu().tolist()
     # median over at least 15 steps: on the GPU boxes a step occasionally
-    # stalls for 0.02-0.5 s in host Python code outside the library (whole
-    # process paused: no CPU time, no page faults, no throttling; the
-    # library's own phases stay fast -- tools/coo_stall_probe.py with
-    # SVDSB_TRACE); mean and max are reported beside it
-    return {"value": float(np.median(times)), "stat": "median", "mean": float(np.mean(times)),
-            "max": float(np.max(times)), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+    # stalls for 0.02-0.5 s in host Python code outside the library (DESIGN
+    # section 5); mean and max are reported beside it
+    return {"value": float(np.median(times)), "stat": "median (max over ranks per step)" if world > 1 else "median",
+            "mean": float(np.mean(times)), "max": float(np.max(times)), "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "per_step_s": [round(t, 4) for t in times],
-            "api": "paper_1607_01404_b200.pysvds.svds(SparseMatrixCsr.from_coo(host COO), precond=jacobi)",
+            "api": ("svds_solve(DistSvdOperator.from_coo(this rank's host COO rows))" if world > 1 else
+                    "paper_1607_01404_b200.pysvds.svds(SparseMatrixCsr.from_coo(host COO))"),
             "steps": len(times)}
 
 
 # ----------------------------------------------------------- CPU oracle
 
-def _oracle_solve(wl, m, n, r, c, v, budget):
+def _oracle_csr(wl, coo, dev_csr=None):
+    """Host CSR of the workload for the oracle.  On our arm the device
+    assembly (bit-identical to from_coo, tests/test_kernels_gpu.py) is
+    exported; the reference arm assembles with the oracle itself."""
     from oracle import csr as ocsr
     from oracle import phsvds
-    rp, ci, va = ocsr.csr_from_coo(m, n, r, c, v)
-    mat = phsvds.Csr(m, n, rp, ci, va)
-    pre = phsvds.Jacobi(mat, "auto") if wl.precond else None
+    m, n, r, c, v = coo
+    if dev_csr is not None:
+        rp, ci, va = dev_csr.export()
+    else:
+        rp, ci, va = ocsr.csr_from_coo(m, n, r, c, v)
+    return phsvds.Csr(m, n, rp, ci, va)
+
+
+def _oracle_full_solve(wl, mat, precond, budget=None):
+    from oracle import phsvds
+    pre = phsvds.Jacobi(mat, "auto") if precond else None
     t0 = time.perf_counter()
     out = phsvds.svds(mat, wl.k, wl.which, wl.tol, seed=0, block=wl.block, precond=pre, max_matvecs=budget)
     return time.perf_counter() - t0, out
 
 
-def cpu_baseline(wl, m, n, r, c, v, full_matvecs, budget):
-    sec, out = _oracle_solve(wl, m, n, r, c, v, budget)
-    used = out["stage1_matvecs"] + out["stage2_matvecs"]
-    return {"value": sec * full_matvecs / used, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": "oracle/phsvds.py (bit-identical restatement of the reference) on the full config-%s matrix "
-                      "with max_matvecs=%d: %.2f s for %d matvecs, scaled to the %d matvecs of the full solve "
-                      "(single-threaded NumPy SpMV, OpenBLAS on up to %d threads for dense ops)"
-                      % (wl.name[1], budget, sec, used, full_matvecs, os.cpu_count())}
+def _oracle_capply(mat, seed=0):
+    """One b = 1 normal-operator apply with the oracle's NumPy SpMV
+    (matio.py:141-155 restated): y = A x (np.add.reduceat order), then
+    z = A^T y (np.add.at order) -- 2 matvecs."""
+    from oracle import csr as ocsr
+    x = np.random.default_rng(seed).standard_normal((mat.n, 1))
+    t0 = time.perf_counter()
+    y = ocsr.spmv(mat.m, mat.n, mat.row_ptr, mat.col_idx, mat.values, x)
+    ocsr.spmv(mat.m, mat.n, mat.row_ptr, mat.col_idx, mat.values, y, transpose=True)
+    return time.perf_counter() - t0
 
 
-FULL_MATVECS = {"c2": 950, "c1": 1792}
+def cpu_baseline(wl, a, coo, precond, our_matvecs, budget):
+    """The oracle port (bit-identical to the reference) on the host cores,
+    bounded sample: the full solve for configs 1-2 (~17 s for config 2),
+    one b = 1 C-apply (2 matvecs) elsewhere, scaled to the solve's matvecs."""
+    mat = _oracle_csr(wl, coo, a.device_csr() if a is not None else None)
+    cores = os.cpu_count()
+    if wl.name in FULL_SOLVE_REF and not budget:
+        sec, out = _oracle_full_solve(wl, mat, precond)
+        return {"value": sec, "unit": UNIT, "cores": cores, "kind": "port", "extrapolated": False,
+                "sample": "oracle/phsvds.py full solve of the full config-%s matrix: %d matvecs, status %s "
+                          "(single-threaded NumPy SpMV, OpenBLAS on up to %d threads for dense ops)"
+                          % (wl.name[1:], out["stage1_matvecs"] + out["stage2_matvecs"], out["status"], cores)}
+    sec = _oracle_capply(mat)
+    full = budget or FULL_MATVECS.get(wl.name, our_matvecs)
+    return {"value": sec * full / 2.0, "unit": UNIT, "cores": 1, "kind": "port", "extrapolated": True,
+            "cpu_s_per_matvec": sec / 2.0, "multiplier": full / 2.0,
+            "sample": "one b=1 C-apply (A x then A^T y, 2 matvecs) with the oracle's NumPy SpMV on the full "
+                      "config-%s matrix: %.2f s; x %d/2 C-applies = the SpMV time alone of a %d-matvec solve "
+                      "(a lower bound: dense ops excluded)" % (wl.name[1:], sec, full, full)}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU algorithm (the oracle port)
-    on the host cores, rank 0 only, each step a bounded sample."""
+    """--impl reference: the reference's CPU algorithm (the oracle port,
+    bit-identical to the reference) on the host cores, rank 0 only.
+    Configs 1 and 2: each step is one full solve.  Others (the reference
+    needs hours): each step is one b = 1 C-apply on the full matrix,
+    extrapolated to the solve's matvec count and labelled as such."""
     world, rank, local = dist_env()
     if rank != 0:
         return
-    wl, (m, n, r, c, v) = workload(args.config)
-    full = FULL_MATVECS.get(args.config)
-    from oracle import csr as ocsr
-    nnz_dedup = int(ocsr.csr_from_coo(m, n, r, c, v)[0][-1])
-    vals = []
-    samples = []
+    from paper_1607_01404_b200 import workloads
+    wl = workloads.CONFIGS[args.config]
+    kw = {"gpus": world} if wl.name == "c5" else {}
+    coo = wl.build(**kw)
+    m, n = coo[0], coo[1]
+    t0 = time.perf_counter()
+    mat = _oracle_csr(wl, coo)
+    setup = time.perf_counter() - t0
+    nnz = int(mat.row_ptr[-1])
+    full_solve = wl.name in FULL_SOLVE_REF and not args.budget
+    vals, outs = [], []
     for i in range(args.warmup + args.steps):
-        sec, out = _oracle_solve(wl, m, n, r, c, v, REF_SAMPLE_MATVECS)
-        used = out["stage1_matvecs"] + out["stage2_matvecs"]
-        est = sec * (full if full else used) / used
+        if full_solve:
+            sec, out = _oracle_full_solve(wl, mat, wl.precond)
+            est = sec
+            outs.append(out)
+        else:
+            sec = _oracle_capply(mat, seed=i)
+            full = args.budget or FULL_MATVECS.get(wl.name)
+            est = sec * full / 2.0
         if i >= args.warmup:
             vals.append(est)
-            samples.append((sec, used))
     value = float(np.mean(vals))
+    cores = os.cpu_count()
+    if full_solve:
+        out = outs[-1]
+        cpu = {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "extrapolated": False,
+               "sample": "each step: oracle/phsvds.py full solve of the full matrix (%d matvecs, status %s); "
+                         "single-threaded NumPy SpMV, OpenBLAS on up to %d threads" %
+                         (out["stage1_matvecs"] + out["stage2_matvecs"], out["status"], cores)}
+    else:
+        full = args.budget or FULL_MATVECS.get(wl.name)
+        cpu = {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "extrapolated": True,
+               "cpu_s_per_matvec": value / full, "multiplier": full / 2.0,
+               "sample": "each step: one b=1 C-apply (A x then A^T y, 2 matvecs) with the oracle's NumPy SpMV "
+                         "on the full matrix, x %d/2 = the SpMV time alone of a %d-matvec solve (lower bound: "
+                         "dense ops excluded; the full reference solve needs hours)" % (full, full)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator of BASELINE config %s)"
-            % wl.name[1], "config": config_json(wl, m, n, nnz_dedup, 1), "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                             "sample": "each step: oracle/phsvds.py on the full matrix with max_matvecs=%d "
-                                       "(mean %.2f s for %d matvecs), scaled to the full solve's %s matvecs"
-                                       % (REF_SAMPLE_MATVECS, float(np.mean([s for s, _ in samples])),
-                                          samples[0][1], full)},
+            "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator of BASELINE config %s)" % wl.name[1:],
+            "config": config_json(wl, m, n, nnz, 1, args.budget), "impl": "reference",
+            "extrapolated": not full_solve, "setup_s": setup, "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def main():
     args = parse()
+    maybe_spawn(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -152,6 +152,11 @@ int svdsb_apply_augmented(svdsb_ctx *ctx, const svdsb_csr *a, const double *x,
  * below at EPS * max.  d has n (side 0) or m (side 1) entries. Bit-exact. */
 int svdsb_precond_diag(svdsb_ctx *ctx, const svdsb_csr *a, int side,
                        double *d, void *stream);
+/* The unclamped squared norms of svdsb_precond_diag (column_sq_norms /
+ * row_sq_norms, matio.py:115-123): the per-rank partial of the sharded
+ * Jacobi diagonal, summed over ranks and clamped by the caller (dist.py). */
+int svdsb_row_sq(svdsb_ctx *ctx, const svdsb_csr *a, int side, double *d,
+                 void *stream);
 /* y = x ./ d (applyPreconditioner; the lambda at
  * operators.py:249).  y may alias x. */
 int svdsb_diag_solve(int64_t dim, const double *d, const double *x,

@@ -49,6 +49,7 @@ _PROTOS = [
     ("svdsb_apply_augmented", i32, [vp, vp, vp, i64, vp, i64, i32, vp]),
     ("svdsb_precond_diag", i32, [vp, vp, i32, vp, vp]),
     ("svdsb_diag_solve", i32, [i64, vp, vp, i64, vp, i64, i32, vp]),
+    ("svdsb_row_sq", i32, [vp, vp, i32, vp, vp]),
     ("svdsb_gram", i32, [vp, i64, i32, vp, vp, vp, vp, i64, i32, vp, i64, vp, vp]),
     ("svdsb_project_out", i32, [vp, i64, i32, vp, vp, vp, vp, i64, vp, i64, i32, vp, vp]),
     ("svdsb_ts_gemm", i32, [vp, i64, vp, i64, i32, vp, i64, i32, f64, f64, vp, i64, vp]),

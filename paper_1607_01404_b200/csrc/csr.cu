@@ -2365,6 +2365,17 @@ int svdsb_precond_diag(svdsb_ctx *ctx, const svdsb_csr *a, int side, double *d, 
   return SVDSB_OK;
 }
 
+int svdsb_row_sq(svdsb_ctx *ctx, const svdsb_csr *a, int side, double *d, void *stream) {
+  SVDSB_CHECK_ARG(ctx && a && d, "svdsb_row_sq: NULL argument");
+  SVDSB_CHECK_ARG(side == 0 || side == 1, "side must be 0 (cols) or 1 (rows)");
+  SVDSB_CHECK_ARG(side == 1 || a->has_t, "column norms need CSR(A^T)");
+  const CsrPart *p = side == 0 ? &a->at : &a->a;
+  if (p->rows == 0) return SVDSB_OK;
+  row_sq_kernel<<<grid1(p->rows), 256, 0, as_stream(stream)>>>(p->rows, p->row_ptr, p->val, d);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
 int svdsb_diag_solve(int64_t dim, const double *d, const double *x, int64_t ldx, double *y, int64_t ldy, int block,
                      void *stream) {
   if (dim == 0 || block == 0) return SVDSB_OK;

@@ -8,7 +8,15 @@ PAPER.md:584-599, 645-657).
 * n-space vectors (stage 1) are split evenly (``even_split``); stage-2
   stacked vectors [v; u] hold the rank's v chunk followed by its u rows.
 * A C-apply is: all-gather x (n x b) -> local A_p x -> local A_p^T y_p ->
-  reduce-scatter of the partial n x b result (``DistSvdOperator``).
+  reduce-scatter of the partial n x b result (``DistSvdOperator``).  When
+  every rank's rows only touch columns of its own chunk and its two
+  neighbours' (grid stencils: configs 3 and 5, square, column chunks = row
+  blocks) the all-gather becomes a halo exchange (x rows [lo, c0) from
+  rank-1, [c1, hi) from rank+1, P2P sends) and the reduce-scatter a
+  reverse halo (the partial sums of the neighbours' rows travel back and
+  are added): O(halo) bytes per C-apply instead of O(n).
+* ``DistSvdOperator.from_coo``: each rank selects and assembles only its
+  own row block's triplets on its device (``partition_coo``).
 * Every Gram / norm partial is finished by ``Comm.allreduce_`` -- PRIMME's
   globalSumDouble -- over NCCL on the kernels' stream.
   Small state is replicated and all-reduce returns identical bits on every
@@ -33,6 +41,28 @@ def partition_rows(row_ptr, parts):
     bounds[0] = 0
     bounds[parts] = m
     return np.minimum(bounds, m)
+
+
+def partition_coo(comm, m, n, rows):
+    """Row blocks balanced by the triplet counts of the rows (for a
+    duplicate-free COO -- every BASELINE generator but config 4 -- these are
+    the CSR row pointers, so the bounds equal ``partition_rows``'; with
+    duplicates the balance is by triplets; host int64, deterministic).
+    Square matrices split their columns like their rows (so a grid
+    stencil's coupling stays between neighbouring ranks), tall ones evenly.
+    Returns (this rank's triplet selection, row bounds, column bounds)."""
+    rows = np.asarray(rows)
+    counts = np.bincount(rows, minlength=m).astype(np.int64) if rows.size else np.zeros(m, np.int64)
+    rp = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(counts, out=rp[1:])
+    rb = partition_rows(rp, comm.world)
+    cb = rb.copy() if m == n else even_split(n, comm.world)
+    r0, r1 = int(rb[comm.rank]), int(rb[comm.rank + 1])
+    if rows.size and bool(np.all(rows[1:] >= rows[:-1])):
+        sel = slice(int(np.searchsorted(rows, r0, "left")), int(np.searchsorted(rows, r1, "left")))
+    else:
+        sel = np.flatnonzero((rows >= r0) & (rows < r1))
+    return sel, rb, cb
 
 
 def even_split(n, parts):
@@ -98,6 +128,69 @@ class Comm:
         out.copy_(mine.t())
         return out
 
+    def _exchange(self, ops):
+        if ops:
+            for req in tdist.batch_isend_irecv(ops):
+                req.wait()
+
+    def halo_gather(self, x_loc, col_bounds, ext, ext_all, out):
+        """out (rows [lo, hi) of the global vector) = own chunk + the halo
+        rows from the two neighbours.  ext = (lo, hi) of this rank,
+        ext_all[p] = (lo_p, hi_p) of every rank."""
+        r, world = self.rank, self.world
+        lo, hi = ext
+        c0, c1 = int(col_bounds[r]), int(col_bounds[r + 1])
+        out[c0 - lo:c1 - lo].copy_(x_loc)
+        b = x_loc.shape[1]
+        ops, recvs = [], []
+        if r > 0 and lo < c0:
+            t = torch.empty((b, c0 - lo), dtype=x_loc.dtype, device=x_loc.device)
+            ops.append(tdist.P2POp(tdist.irecv, t, r - 1, self.group))
+            recvs.append((t, 0, c0 - lo))
+        if r + 1 < world and hi > c1:
+            t = torch.empty((b, hi - c1), dtype=x_loc.dtype, device=x_loc.device)
+            ops.append(tdist.P2POp(tdist.irecv, t, r + 1, self.group))
+            recvs.append((t, c1 - lo, hi - lo))
+        # what the neighbours need from this chunk
+        if r > 0 and int(ext_all[r - 1][1]) > c0:
+            k1 = int(ext_all[r - 1][1])
+            ops.append(tdist.P2POp(tdist.isend, x_loc[0:k1 - c0].t().contiguous(), r - 1, self.group))
+        if r + 1 < world and int(ext_all[r + 1][0]) < c1:
+            k0 = int(ext_all[r + 1][0])
+            ops.append(tdist.P2POp(tdist.isend, x_loc[k0 - c0:c1 - c0].t().contiguous(), r + 1, self.group))
+        self._exchange(ops)
+        for t, a, bnd in recvs:
+            out[a:bnd].copy_(t.t())
+        return out
+
+    def halo_reduce(self, z_ext, col_bounds, ext, ext_all, out):
+        """out (this rank's chunk) = own partial sums + the neighbours'
+        partial sums of this chunk's rows (the reverse of halo_gather)."""
+        r, world = self.rank, self.world
+        lo, hi = ext
+        c0, c1 = int(col_bounds[r]), int(col_bounds[r + 1])
+        out.copy_(z_ext[c0 - lo:c1 - lo])
+        b = z_ext.shape[1]
+        ops, recvs = [], []
+        if r > 0 and lo < c0:
+            ops.append(tdist.P2POp(tdist.isend, z_ext[0:c0 - lo].t().contiguous(), r - 1, self.group))
+        if r + 1 < world and hi > c1:
+            ops.append(tdist.P2POp(tdist.isend, z_ext[c1 - lo:hi - lo].t().contiguous(), r + 1, self.group))
+        if r > 0 and int(ext_all[r - 1][1]) > c0:
+            k1 = int(ext_all[r - 1][1])
+            t = torch.empty((b, k1 - c0), dtype=z_ext.dtype, device=z_ext.device)
+            ops.append(tdist.P2POp(tdist.irecv, t, r - 1, self.group))
+            recvs.append((t, 0, k1 - c0))
+        if r + 1 < world and int(ext_all[r + 1][0]) < c1:
+            k0 = int(ext_all[r + 1][0])
+            t = torch.empty((b, c1 - k0), dtype=z_ext.dtype, device=z_ext.device)
+            ops.append(tdist.P2POp(tdist.irecv, t, r + 1, self.group))
+            recvs.append((t, k0 - c0, c1 - c0))
+        self._exchange(ops)
+        for t, a, bnd in recvs:
+            out[a:bnd] += t.t()
+        return out
+
     def allgather_host(self, arr):
         """Concatenate host numpy arrays (rows) from all ranks in rank order."""
         if self.world == 1:
@@ -120,7 +213,7 @@ class DistSvdOperator:
     of the global vector, m-space blocks rows [row_bounds[r], row_bounds[r+1]).
     """
 
-    def __init__(self, comm, m, n, row_bounds, col_bounds, local_fwd, local_adj, alloc=None):
+    def __init__(self, comm, m, n, row_bounds, col_bounds, local_fwd, local_adj, alloc=None, halo=None):
         if m < n:
             raise ValueError("DistSvdOperator expects an oriented (tall) matrix")
         self.comm = comm
@@ -133,6 +226,10 @@ class DistSvdOperator:
         self.m_loc, self.n_loc = self.r1 - self.r0, self.c1 - self.c0
         self._fwd, self._adj = local_fwd, local_adj
         self._alloc = alloc
+        # halo = (ext, ext_all): the global column range [lo, hi) this rank's
+        # rows touch, and every rank's; local products then work on rows
+        # [lo, hi) of x / z instead of all n
+        self.halo = halo
         self._bufs = {}
         self.n_matvecs = 0
         self.explicit = None
@@ -160,6 +257,12 @@ class DistSvdOperator:
         """y_loc = (A x)[r0:r1] from the local n-chunk of x."""
         b = x_loc.shape[1]
         self.n_matvecs += b
+        if self.halo is not None:
+            (lo, hi), ext_all = self.halo
+            x_ext = self._buf("xext", hi - lo, b, x_loc)
+            self.comm.halo_gather(x_loc, self.col_bounds, (lo, hi), ext_all, x_ext)
+            self._fwd(x_ext, y_loc)
+            return y_loc
         x_full = self._buf("xfull", self.n, b, x_loc)
         self.comm.allgather_rows(x_loc, self.col_bounds, x_full)
         self._fwd(x_full, y_loc)
@@ -169,6 +272,12 @@ class DistSvdOperator:
         """z_loc = (A^T y)[c0:c1] from the local m-rows of y."""
         b = y_loc.shape[1]
         self.n_matvecs += b
+        if self.halo is not None:
+            (lo, hi), ext_all = self.halo
+            z_ext = self._buf("zext", hi - lo, b, y_loc)
+            self._adj(y_loc, z_ext)
+            self.comm.halo_reduce(z_ext, self.col_bounds, (lo, hi), ext_all, z_loc)
+            return z_loc
         z_full = self._buf("zfull", self.n, b, y_loc)
         self._adj(y_loc, z_full)
         self.comm.reduce_scatter_rows(z_full, self.col_bounds, z_loc)
@@ -206,6 +315,106 @@ class DistSvdOperator:
         op = cls(comm, m, n, rb, cb, fwd, adj, alloc=lambda rows, b: dv.new_block(rows, b, device=device))
         op.local_csr = local
         return op
+
+
+def column_extent(comm, col_bounds, cols):
+    """(lo, hi) of the global columns this rank's triplets touch (its own
+    chunk always included), every rank's extents, and whether a halo
+    exchange covers them (each extent within the neighbours' chunks)."""
+    r = comm.rank
+    c0, c1 = int(col_bounds[r]), int(col_bounds[r + 1])
+    if len(cols):
+        cmin = int(cols.min()) if not isinstance(cols, torch.Tensor) else int(cols.min().item())
+        cmax = int(cols.max()) if not isinstance(cols, torch.Tensor) else int(cols.max().item())
+        lo, hi = min(c0, cmin), max(c1, cmax + 1)
+    else:
+        lo, hi = c0, c1
+    ext = np.array([[lo, hi]], dtype=np.int64)
+    ext_all = comm.allgather_host(ext) if comm.distributed else ext
+    ok = True
+    for p in range(comm.world):
+        plo, phi = int(ext_all[p][0]), int(ext_all[p][1])
+        lo_lim = int(col_bounds[max(p - 1, 0)])
+        hi_lim = int(col_bounds[min(p + 2, comm.world)])
+        ok &= lo_lim <= plo and phi <= hi_lim
+    return (lo, hi), [tuple(int(v) for v in e) for e in ext_all], ok
+
+
+def _from_coo(cls, comm, m, n, rows, cols, vals, device=None, bounds=None):
+    from .matrix import SparseMatrixCsr
+    from . import device as dv
+    if bounds is None:
+        sel, rb, cb = partition_coo(comm, m, n, np.asarray(rows))
+        rows, cols, vals = rows[sel], cols[sel], vals[sel]
+    else:
+        rb, cb = bounds
+    r0, r1 = int(rb[comm.rank]), int(rb[comm.rank + 1])
+    (lo, hi), ext_all, use_halo = column_extent(comm, cb, cols)
+    shift = lo if use_halo else 0
+    ncols = (hi - lo) if use_halo else n
+    local = SparseMatrixCsr.from_coo(r1 - r0, ncols, rows - r0, cols - shift if shift else cols, vals,
+                                     device=device).device_csr(device)
+
+    def fwd(x, y_loc):
+        local.matvec(x, y_loc, transpose=False)
+
+    def adj(y_loc, z):
+        local.matvec(y_loc, z, transpose=True)
+
+    op = cls(comm, m, n, rb, cb, fwd, adj, alloc=lambda nr, b: dv.new_block(nr, b, device=device),
+             halo=((lo, hi), ext_all) if use_halo else None)
+    op.local_csr = local
+    op.local_nnz = local.nnz
+    tot = torch.tensor([local.nnz], dtype=torch.int64)
+    if comm.distributed and tdist.get_backend(comm.group) == "nccl":
+        tot = tot.to(local.ctx.device)
+    op.nnz_global = int(comm.allreduce_(tot).item())
+    return op
+
+
+DistSvdOperator.from_coo = classmethod(_from_coo)
+
+
+def dist_jacobi_diag(op, part):
+    """This rank's chunk of the Jacobi diagonal from its rows' partial
+    squared column norms ``part`` (length hi - lo with a halo, n otherwise):
+    summed over the ranks sharing a column, clamped below at EPS times the
+    global maximum (operators.py:225-249)."""
+    part = part.reshape(-1, 1)
+    d = torch.zeros((1, op.n_loc), dtype=part.dtype, device=part.device).t()
+    if op.halo is not None:
+        (lo, hi), ext_all = op.halo
+        op.comm.halo_reduce(part, op.col_bounds, (lo, hi), ext_all, d)
+    else:
+        op.comm.reduce_scatter_rows(part, op.col_bounds, d)
+    mx = d.max().reshape(1) if d.numel() else torch.zeros(1, dtype=d.dtype, device=d.device)
+    if op.comm.distributed:
+        tdist.all_reduce(mx, op=tdist.ReduceOp.MAX, group=op.comm.group)
+    eps = float(np.finfo(np.float64).eps)
+    return torch.maximum(d[:, 0], mx * eps).contiguous()
+
+
+def dist_jacobi(op):
+    """Point-Jacobi preconditioner of the sharded normal operator: squared
+    column norms of this rank's rows on device (svdsb_row_sq), reduced over
+    ranks by ``dist_jacobi_diag`` -- no rank holds the whole matrix.  The
+    cross-rank additions round differently from the single-GPU bincount
+    order (not bit-exact with it)."""
+    from . import _lib
+    from . import device as dv
+    from .operators import Preconditioner
+    local = op.local_csr
+    part = dv.new_block(local.n, 1, device=local.ctx.device)
+    local.col_sq_norms(part[:, 0])
+    d = dist_jacobi_diag(op, part[:, 0])
+
+    def into(x, y):
+        _lib.call("svdsb_diag_solve", x.shape[0], dv.P(d), dv.P(x), dv.ld_of(x), dv.P(y), dv.ld_of(y), x.shape[1],
+                  dv.context(x.device).stream)
+
+    pre = Preconditioner("AtA", into=into)
+    pre.diagonal = d
+    return pre
 
 
 def local_jacobi(op, csr):

@@ -124,6 +124,11 @@ class DeviceCsr:
             setattr(self, attr, buf)
         return buf[:, :cols]
 
+    def col_sq_norms(self, out):
+        """Unclamped squared column norms (matio.py:115-118) into out[n]."""
+        from .device import P
+        _lib.call("svdsb_row_sq", self.ctx.handle, self.handle, 0, P(out), self.ctx.stream)
+
     def precond_diag(self, side, out):
         from .device import P
         _lib.call("svdsb_precond_diag", self.ctx.handle, self.handle, int(side), P(out),
