@@ -257,7 +257,9 @@ int svdsb_split_stats(svdsb_ctx *ctx, int64_t dim, int64_t nsplit,
  * svdsb_cgs_pass and x /= final norm; `state` receives the DGKS record
  * (svdsb_dgks_begin layout).  Replaces the orthonormalize / _expand
  * sequence of eigensolver.py:666-700 + kernels.py:54-133 for one column.
- * Uses a software grid barrier: the grid is at most one CTA per SM. */
+ * Uses a software grid barrier: the grid is at most one CTA per SM
+ * (queried, not assumed) and the launch is cooperative, so it fails with
+ * SVDSB_ERR_CUDA instead of hanging when the CTAs cannot be co-resident. */
 int svdsb_cgs_fused(svdsb_ctx *ctx, int64_t dim, int nblk,
                     const double *const *xs, const int64_t *ldxs,
                     const int *cols, const double *rsrc, int64_t ldr,
@@ -265,6 +267,9 @@ int svdsb_cgs_fused(svdsb_ctx *ctx, int64_t dim, int nblk,
                     const double *yin, int64_t ldyin, int g, int kk,
                     double *prev, int64_t ldprev, int passes, double *state,
                     void *stream);
+/* 1 when svdsb_cgs_fused can run on the current device (cooperative launch
+ * supported, kernel fits an SM); callers use svdsb_cgs_pass otherwise. */
+int svdsb_cgs_fused_supported(void);
 /* Device-resident iterated CGS for ONE new column v (kernels.py:54-133
  * without the host round trip).  state: 8 doubles [active, pass,
  * collapses, orig, prev, final, |v|^2 before, |v|^2 after];

@@ -66,6 +66,7 @@ _PROTOS = [
     ("svdsb_dgks_begin", i32, [vp, vp]),
     ("svdsb_cgs_fused", i32, [vp, i64, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp, i64, i32, i32, vp, i64, i32,
                               vp, vp]),
+    ("svdsb_cgs_fused_supported", i32, []),
     ("svdsb_cgs_pass", i32, [vp, i64, i32, vp, vp, vp, vp, vp, vp, i32, vp]),
     ("svdsb_split_residual",i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp, vp, vp]),
     ("svdsb_syev_small", i32, [i32, vp, i64, i32, f64, vp, vp, i64, vp]),
@@ -152,6 +153,18 @@ def check(rc, what=""):
 def call(name, *args):
     rc = getattr(load(), name)(*args)
     check(rc, name)
+
+
+_coop = {}
+
+
+def cgs_fused_supported():
+    """svdsb_cgs_fused needs a co-resident grid (cooperative launch)."""
+    import torch
+    dev = torch.cuda.current_device()
+    if dev not in _coop:
+        _coop[dev] = bool(load().svdsb_cgs_fused_supported())
+    return _coop[dev]
 
 
 def launch_count():

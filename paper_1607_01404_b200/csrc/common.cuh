@@ -13,7 +13,10 @@
 namespace svdsb {
 
 constexpr double kEps = 2.220446049250313e-16;  // kernels.py:20
-constexpr int kNumSMs = 148;                     // B200
+// SM count of the current device (148 on B200), queried once per device:
+// grids sized in multiples of it, and the co-residency bound of the
+// grid-barrier kernel, follow the part the library actually runs on.
+int num_sms();
 
 void set_error(const char *fmt, ...);
 int64_t bump_launches(int n = 1);
@@ -79,6 +82,27 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// As launch_k, plus the cooperative attribute: the launch fails instead of
+// deadlocking when the grid cannot be co-resident (kernels with a software
+// grid barrier).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                               Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_on() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <mutex>
 #include <vector>
 
 #include <stdlib.h>
@@ -66,6 +67,7 @@ struct CsrPart {
   int64_t *sell_ptr = nullptr;  // nslice + 1
   int *sell_col = nullptr;
   double *sell_val = nullptr;
+  bool sell_failed = false;     // the copy could not be built: CSR kernels (same bits)
 };
 
 constexpr int kMaxB = 64;   // largest block handled by one matvec call
@@ -1177,10 +1179,10 @@ static int pipe_rows_grid(const void *kernel, size_t smem, bool bulk = false) {
   for (int i = 0; i < 8; ++i)
     if (!which[i]) {
       which[i] = kernel;
-      cap[i] = occ * kNumSMs;
+      cap[i] = occ * num_sms();
       break;
     }
-  return occ * kNumSMs;
+  return occ * num_sms();
 }
 
 static int pipe_grid(const void *kernel) {
@@ -1194,10 +1196,10 @@ static int pipe_grid(const void *kernel) {
   for (int i = 0; i < 8; ++i)
     if (!which[i]) {
       which[i] = kernel;
-      cap[i] = occ * kNumSMs;
+      cap[i] = occ * num_sms();
       break;
     }
-  return occ * kNumSMs;
+  return occ * num_sms();
 }
 
 // column-major (ld) -> row-major (stride b) and back
@@ -1500,6 +1502,29 @@ static bool capturing(cudaStream_t st) {
   return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
 }
 
+// The sliced-ELL copy of a part, built once on the first uncaptured b = 4
+// call (serialised: handles may be shared between host threads).  If it
+// cannot be built (out of memory) the part keeps using the CSR kernels,
+// which give the same bits, and the solve carries on.
+static std::mutex g_sell_mu;
+static bool ensure_sell(const CsrPart &cp, cudaStream_t st, bool sorted) {
+  if (cp.sell_val) return true;
+  if (cp.sell_failed || capturing(st)) return false;
+  std::lock_guard<std::mutex> lk(g_sell_mu);
+  CsrPart &p = const_cast<CsrPart &>(cp);  // cache fields only; the matrix itself is immutable
+  if (p.sell_val || p.sell_failed) return p.sell_val != nullptr;
+  if (build_sell(p, st, sorted) != SVDSB_OK) {
+    p.sell_failed = true;
+    pfree(p.mid_rows, st);
+    p.mid_rows = nullptr;
+    p.nmid = 0;
+    cudaGetLastError();
+    set_error("");
+    return false;
+  }
+  return true;
+}
+
 // Tile the rows (host; row_ptr already on host in p.host_row_ptr).
 static int build_partition(CsrPart &p, cudaStream_t st) {
   const std::vector<int> &rp = p.host_row_ptr;
@@ -1570,10 +1595,7 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
     if (ORDER == 0 && b == 4 && xrow && !acc && p.nlong == 0 && p.maxlen <= 129 && rowlane_on() &&
         g_tune[0] == 0) {
       // sliced-ELL copy, built on the first uncaptured call
-      if (!p.sell_val && !capturing(st)) {
-        int rc = build_sell(const_cast<CsrPart &>(p), st);
-        if (rc) return rc;
-      }
+      ensure_sell(p, st, false);
       if (p.sell_val && !p.sell_perm && p.maxlen <= kSellW && g_tune[2] == 1) {  // measured slower (register spills)
         auto k = yrow ? csr_sell4w_kernel<1> : csr_sell4w_kernel<0>;
         const int g = (int)std::min<int64_t>((p.nslice + 7) / 8, pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
@@ -1606,7 +1628,7 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
       return SVDSB_OK;
     }
     if (ORDER == 0 && b == 4 && xrow && !acc && p.nlong == 0 && p.maxlen <= 129 && rowlane_on()) {
-      const int g = (int)std::min<int64_t>((p.rows + kTileThreads - 1) / kTileThreads, 2 * kNumSMs * 4);
+      const int g = (int)std::min<int64_t>((p.rows + kTileThreads - 1) / kTileThreads, 2 * num_sms() * 4);
       if (yrow)
         SVDSB_LAUNCH_PDL(csr_rowlane4_kernel<1>, g, kTileThreads, 0, st, p.rows, p.row_ptr, p.col, p.val, x, y, ldy);
       else
@@ -1617,10 +1639,7 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
     if (ORDER == 1 && b == 4 && xrow && p.ntile > 0 && g_tune[5] == 0) {
       // rows up to a tile on a length-sorted sliced-ELL copy (built on the
       // first uncaptured call); long rows below on the chunk path
-      if (!p.sell_val && !capturing(st)) {
-        int rc = build_sell(const_cast<CsrPart &>(p), st, true);
-        if (rc) return rc;
-      }
+      ensure_sell(p, st, true);
       if (p.sell_val && p.sell_perm) {
         if (p.nslice + p.nmid > 0) {
           auto k = yrow ? csr_sell4t_kernel<1> : csr_sell4t_kernel<0>;
@@ -1821,12 +1840,18 @@ static int build_transpose(const CsrPart &a, CsrPart &at, cudaStream_t st) {
 
 // ---------------------------------------------------------------- COO build
 
-__global__ void coo_keys_kernel(int64_t nt, int64_t n, const int64_t *__restrict__ r,
+// Sort key of each triplet, with the from_coo range check (matio.py:41-52)
+// folded in: an out-of-range index raises *bad and gets key 0, so nothing
+// downstream indexes outside the row counters before the caller reads *bad.
+__global__ void coo_keys_kernel(int64_t nt, int64_t m, int64_t n, const int64_t *__restrict__ r,
                                 const int64_t *__restrict__ c, unsigned long long *__restrict__ key,
-                                int *__restrict__ idx) {
+                                int *__restrict__ idx, int *__restrict__ bad) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nt) return;
-  key[i] = (unsigned long long)(r[i] * n + c[i]);
+  const int64_t ri = r[i], cj = c[i];
+  const bool ok = ri >= 0 && ri < m && cj >= 0 && cj < n;
+  if (!ok) atomicOr(bad, 1);
+  key[i] = ok ? (unsigned long long)(ri * n + cj) : 0ull;
   idx[i] = (int)i;
 }
 
@@ -1857,6 +1882,22 @@ __global__ void coo_sum_kernel(int64_t nt, int64_t n, const unsigned long long *
   val[o] = s;
   atomicAdd(rowcnt + r, 1);
 }
+
+// Temporary pool allocations of a build step, released (stream-ordered) on
+// every return path.
+struct StreamTemps {
+  cudaStream_t st;
+  std::vector<void *> v;
+  ~StreamTemps() {
+    for (void *q : v) pfree(q, st);
+  }
+  template <typename T>
+  cudaError_t get(T **q, size_t bytes) {
+    cudaError_t e = palloc(q, bytes, st);
+    if (e == cudaSuccess) v.push_back(*q);
+    return e;
+  }
+};
 
 }  // namespace svdsb
 
@@ -1940,16 +1981,26 @@ static int build_blocked_transpose(svdsb_csr *h, cudaStream_t st) {
     forced = true;
   }
   if (!forced && !(m > block_rows && m >= 4 * n)) return SVDSB_OK;
+  StreamTemps temps{st, {}};
   int *lo = nullptr, *len = nullptr;
-  SVDSB_CUDA(palloc(&lo, sizeof(int) * (n + 1), st));
-  SVDSB_CUDA(palloc(&len, sizeof(int) * (n + 1), st));
+  SVDSB_CUDA(temps.get(&lo, sizeof(int) * (n + 1)));
+  SVDSB_CUDA(temps.get(&len, sizeof(int) * (n + 1)));
   size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, len, lo, (int)(n + 1), st);
   void *scan_tmp = nullptr;
-  SVDSB_CUDA(palloc(&scan_tmp, scan_bytes, st));
+  SVDSB_CUDA(temps.get(&scan_tmp, scan_bytes));
   for (int64_t r0 = 0; r0 < m; r0 += block_rows) {
     const int64_t r1 = std::min(m, r0 + block_rows);
     CsrPart p;
+    struct PartGuard {  // a block that fails half-built is freed here
+      CsrPart *p;
+      ~PartGuard() {
+        if (p) {
+          cudaDeviceSynchronize();
+          free_part(*p);
+        }
+      }
+    } pguard{&p};
     p.rows = n;
     p.cols = r1 - r0;
     SVDSB_CUDA(alloc_pad(&p.row_ptr, n + 1, st));
@@ -1965,19 +2016,17 @@ static int build_blocked_transpose(svdsb_csr *h, cudaStream_t st) {
     SVDSB_CUDA(alloc_pad(&p.col, std::max<int64_t>(p.nnz, 1), st));
     SVDSB_CUDA(alloc_pad(&p.val, std::max<int64_t>(p.nnz, 1), st));
     if (p.nnz > 0) {
-      seg_copy_kernel<<<(unsigned)std::min<int64_t>((p.nnz + 255) / 256, 16 * kNumSMs), 256, 0, st>>>(
+      seg_copy_kernel<<<(unsigned)std::min<int64_t>((p.nnz + 255) / 256, 16 * num_sms()), 256, 0, st>>>(
           n, p.nnz, at.col, at.val, lo, p.row_ptr, (int)r0, p.col, p.val);
       SVDSB_LAUNCHED();
     }
     int rc = build_partition(p, st);
     if (rc) return rc;
+    pguard.p = nullptr;
     h->atb.push_back(std::move(p));
     h->atb_r0.push_back(r0);
   }
   SVDSB_CUDA(cudaStreamSynchronize(st));
-  pfree(lo, st);
-  pfree(len, st);
-  pfree(scan_tmp, st);
   return SVDSB_OK;
 }
 
@@ -2073,7 +2122,15 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
   CreateTrace trace;
   g_trace = &trace;
   struct Unset { ~Unset() { g_trace = nullptr; } } unset_trace;
-  svdsb_csr *h = new svdsb_csr();
+  // every early return below frees the handle and the temporaries
+  StreamTemps tmp_bufs{st, {}};
+  struct Guard {
+    svdsb_csr *h;
+    ~Guard() {
+      if (h) svdsb_csr_destroy(h);
+    }
+  } guard{new svdsb_csr()};
+  svdsb_csr *h = guard.h;
   cudaGetDevice(&h->device);
   h->has_t = false;
   CsrPart &p = h->a;
@@ -2085,22 +2142,25 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
   if (nt > 0) {
     unsigned long long *key = nullptr, *key_s = nullptr;
     int *idx = nullptr, *perm = nullptr, *first = nullptr, *seg = nullptr, *rowcnt = nullptr;
-    SVDSB_CUDA(palloc(&key, 8 * nt, st));
-    SVDSB_CUDA(palloc(&key_s, 8 * nt, st));
-    SVDSB_CUDA(palloc(&idx, 4 * nt, st));
-    SVDSB_CUDA(palloc(&perm, 4 * nt, st));
-    SVDSB_CUDA(palloc(&first, 4 * nt, st));
-    SVDSB_CUDA(palloc(&seg, 4 * (nt + 1), st));
-    SVDSB_CUDA(palloc(&rowcnt, 4 * (m + 1), st));
+    SVDSB_CUDA(tmp_bufs.get(&key, 8 * nt));
+    SVDSB_CUDA(tmp_bufs.get(&key_s, 8 * nt));
+    SVDSB_CUDA(tmp_bufs.get(&idx, 4 * nt));
+    SVDSB_CUDA(tmp_bufs.get(&perm, 4 * nt));
+    SVDSB_CUDA(tmp_bufs.get(&first, 4 * nt));
+    SVDSB_CUDA(tmp_bufs.get(&seg, 4 * (nt + 1)));
+    SVDSB_CUDA(tmp_bufs.get(&rowcnt, 4 * (m + 1)));
+    int *bad = nullptr;
+    SVDSB_CUDA(tmp_bufs.get(&bad, 4));
     SVDSB_CUDA(cudaMemsetAsync(rowcnt, 0, 4 * (m + 1), st));
+    SVDSB_CUDA(cudaMemsetAsync(bad, 0, 4, st));
     tmark("alloc");
-    coo_keys_kernel<<<grid1(nt), 256, 0, st>>>(nt, n, rows, cols, key, idx);
+    coo_keys_kernel<<<grid1(nt), 256, 0, st>>>(nt, m, n, rows, cols, key, idx, bad);
     SVDSB_LAUNCHED();
     int nbits = bits_for(std::max<int64_t>(m * n, 2));
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key_s, idx, perm, (int)nt, 0, nbits, st);
     void *tmp = nullptr;
-    SVDSB_CUDA(palloc(&tmp, tb, st));
+    SVDSB_CUDA(tmp_bufs.get(&tmp, tb));
     SVDSB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key_s, idx, perm, (int)nt, 0, nbits, st));
     bump_launches();
     coo_first_kernel<<<grid1(nt), 256, 0, st>>>(nt, key_s, first);
@@ -2108,14 +2168,19 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     size_t sb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb, first, seg, (int)nt, st);
     void *stmp = nullptr;
-    SVDSB_CUDA(palloc(&stmp, sb, st));
+    SVDSB_CUDA(tmp_bufs.get(&stmp, sb));
     SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(stmp, sb, first, seg, (int)nt, st));
     bump_launches();
-    int last_seg = 0, last_first = 0;
+    int last_seg = 0, last_first = 0, any_bad = 0;
     tmark("sort+scan launch");
     SVDSB_CUDA(cudaMemcpyAsync(&last_seg, seg + nt - 1, 4, cudaMemcpyDeviceToHost, st));
     SVDSB_CUDA(cudaMemcpyAsync(&last_first, first + nt - 1, 4, cudaMemcpyDeviceToHost, st));
+    SVDSB_CUDA(cudaMemcpyAsync(&any_bad, bad, 4, cudaMemcpyDeviceToHost, st));
     SVDSB_CUDA(cudaStreamSynchronize(st));
+    if (any_bad) {
+      set_error("COO index out of range for a %lld x %lld matrix", (long long)m, (long long)n);
+      return SVDSB_ERR_ARG;
+    }
     nnz = (int64_t)last_seg + last_first;
     tmark("sync nnz");
     SVDSB_CUDA(alloc_pad(&p.col, std::max<int64_t>(nnz, 1), st));
@@ -2125,22 +2190,12 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     size_t sb2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb2, rowcnt, p.row_ptr, (int)(m + 1), st);
     void *stmp2 = nullptr;
-    SVDSB_CUDA(palloc(&stmp2, sb2, st));
+    SVDSB_CUDA(tmp_bufs.get(&stmp2, sb2));
     SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(stmp2, sb2, rowcnt, p.row_ptr, (int)(m + 1), st));
     bump_launches();
     tmark("sum+scan launch");
     SVDSB_CUDA(cudaStreamSynchronize(st));
     tmark("sum sync");
-    pfree(key, st);
-    pfree(key_s, st);
-    pfree(idx, st);
-    pfree(perm, st);
-    pfree(first, st);
-    pfree(seg, st);
-    pfree(rowcnt, st);
-    pfree(tmp, st);
-    pfree(stmp, st);
-    pfree(stmp2, st);
   } else {
     SVDSB_CUDA(palloc(&p.col, 4, st));
     SVDSB_CUDA(palloc(&p.val, 8, st));
@@ -2152,10 +2207,8 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
   SVDSB_CUDA(cudaStreamSynchronize(st));
   tmark("row_ptr d2h");
   int rc = finish_create(h, flags, st);
-  if (rc) {
-    svdsb_csr_destroy(h);
-    return rc;
-  }
+  if (rc) return rc;  // the guard destroys h
+  guard.h = nullptr;
   *out = h;
   return SVDSB_OK;
 }
@@ -2356,7 +2409,7 @@ int svdsb_precond_diag(svdsb_ctx *ctx, const svdsb_csr *a, int side, double *d, 
   cudaStream_t st = as_stream(stream);
   row_sq_kernel<<<grid1(p->rows), 256, 0, st>>>(p->rows, p->row_ptr, p->val, d);
   SVDSB_LAUNCHED();
-  int g = (int)std::min<int64_t>(grid1(p->rows), 2 * kNumSMs);
+  int g = (int)std::min<int64_t>(grid1(p->rows), 2 * num_sms());
   double *mx = ctx->partials + kMaxPartials - 1;
   max_kernel<<<g, 256, 0, st>>>(p->rows, d, mx, take_ticket(ctx), ctx->partials);
   SVDSB_LAUNCHED();

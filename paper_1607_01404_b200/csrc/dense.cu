@@ -21,7 +21,6 @@ namespace svdsb {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxCtas = 8 * kNumSMs;
 constexpr int kMinRowsPerCta = 256;
 
 struct ColSet {
@@ -71,7 +70,7 @@ __device__ __forceinline__ void cta_fold(double (&acc)[NACC], int nvalid, double
   }
 }
 
-static inline int grid_rows(int64_t dim) { return stream_grid(dim, kMinRowsPerCta, kMaxCtas); }
+static inline int grid_rows(int64_t dim) { return stream_grid(dim, kMinRowsPerCta, 8 * num_sms()); }
 
 // Persistent-style grid: one wave of resident CTAs (occupancy x 148 SMs),
 // each looping over its contiguous row range.  Cached per (kernel, smem).
@@ -91,7 +90,7 @@ static int grid_for(K kernel, int64_t dim, size_t smem) {
   if (cap == 0) {
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
-    cap = occ * kNumSMs;
+    cap = occ * num_sms();
     if (ncache < 64) cache[ncache++] = {kp, smem, cap};
   }
   return stream_grid(dim, kMinRowsPerCta, cap);
@@ -1280,7 +1279,7 @@ int gram_impl(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, co
       // latency-bound sizes (L2-scale N): one CTA per SM halves the partials
       // the last CTA folds (measured 12.4 -> 9.9 us on config 2)
       int gxv = grid_for(gram1_vec_kernel<AT>, dim, 0);
-      if (dim <= (1 << 18) && gxv > kNumSMs) gxv = kNumSMs;
+      if (dim <= (1 << 18) && gxv > num_sms()) gxv = num_sms();
       dim3 grid(gxv, (s.total + AT - 1) / AT, 1);
       SVDSB_LAUNCH_PDL(gram1_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, y, c, norms2, ctx->partials,
                        take_ticket(ctx), nullptr, hi);
@@ -1577,21 +1576,36 @@ int svdsb_cgs_fused(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *
   SVDSB_CHECK_ARG(colset_vec_ok(s) && aligned16(x), "svdsb_cgs_fused: operands must be 16-byte aligned");
   SVDSB_CHECK_ARG(passes >= 1 && passes <= 6, "svdsb_cgs_fused: 1..6 passes");
   if (dim == 0) return SVDSB_OK;
-  static int cap = 0;
-  if (cap == 0) {
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cgs_fused_kernel, kCgsThreads, 0) != cudaSuccess ||
-        occ < 1) {
-      set_error("svdsb_cgs_fused: kernel does not fit on an SM");
-      return SVDSB_ERR_CUDA;
-    }
-    cap = kNumSMs;  // one CTA per SM: all resident for the grid barrier
+  if (!svdsb_cgs_fused_supported()) {
+    set_error("svdsb_cgs_fused: cooperative launch unavailable on this device (use svdsb_cgs_pass)");
+    return SVDSB_ERR_CUDA;
   }
-  const int grid = stream_grid(dim, 2 * kCgsThreads, cap);
+  // one CTA per SM: all resident for the grid barrier; the cooperative
+  // attribute makes the launch fail rather than hang if they cannot be
+  const int grid = stream_grid(dim, 2 * kCgsThreads, num_sms());
   SVDSB_CHECK_ARG((int64_t)grid * (kCgsMaxCols + 2) <= kMaxPartials, "svdsb_cgs_fused: workspace too small");
-  SVDSB_LAUNCH_PDL(cgs_fused_kernel, grid, kCgsThreads, 0, as_stream(stream), dim, s, rsrc, ldr, ci, d, x, yin,
-                   ldyin, g, kk, prev, ldprev, passes, state, ctx->partials, ctx->gbar);
+  cudaError_t e = launch_coop(cgs_fused_kernel, grid, kCgsThreads, 0, as_stream(stream), dim, s, rsrc, ldr, ci, d,
+                              x, yin, ldyin, g, kk, prev, ldprev, passes, state, ctx->partials, ctx->gbar);
+  if (e != cudaSuccess) {
+    set_error("svdsb_cgs_fused: cooperative launch of %d CTAs failed: %s", grid, cudaGetErrorString(e));
+    return SVDSB_ERR_CUDA;
+  }
+  bump_launches();
   return SVDSB_OK;
+}
+
+int svdsb_cgs_fused_supported(void) {
+  static int ok[64] = {0};  // 0 unknown, 1 yes, -1 no
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  if (ok[dev] == 0) {
+    int coop = 0, occ = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cgs_fused_kernel, kCgsThreads, 0) != cudaSuccess)
+      occ = 0;
+    ok[dev] = (coop && occ >= 1) ? 1 : -1;
+  }
+  return ok[dev] == 1;
 }
 
 int svdsb_cgs_pass(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs,

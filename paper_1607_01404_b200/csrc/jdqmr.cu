@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(jd::kThreads) jd_k4_kernel(
 }
 
 // the setup (beta = 0) applies the same kernel: d = P z
-static int jd_grid(int64_t n) { return stream_grid(n, jd::kThreads * 4, kNumSMs * 4); }
+static int jd_grid(int64_t n) { return stream_grid(n, jd::kThreads * 4, num_sms() * 4); }
 
 template <int QB>
 static int jd_step_q(svdsb_ctx *ctx, int phase, int64_t n, const svdsb_jd_vecs *v, const double *q, int64_t ldq,

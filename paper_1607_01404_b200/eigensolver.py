@@ -1259,7 +1259,8 @@ class DavidsonSolver:
         """The one-launch CGS wins while the basis is L2-resident (latency
         bound: configs 1 and 2); HBM-streamed bases run the separate
         Gram / projection kernels, which stream at 82-86 % of HBM."""
-        return self.fused_cgs and cols <= 40 and 8 * self.n * cols <= (64 << 20)
+        return (self.fused_cgs and cols <= 40 and 8 * self.n * cols <= (64 << 20)
+                and _lib.cgs_fused_supported())
 
     def _expand_speculative(self, block, precondition=True):
         g = self.g
