@@ -233,6 +233,19 @@ int svdsb_gather_cols(int64_t dim, const double *x, int64_t ldx,
  * eigensolver.py:563-607). */
 int svdsb_status_pack(const double *lams, int gn, const double *rn2, int p,
                       const double *state, double *host_dst, void *stream);
+/* As svdsb_status_pack with nstate consecutive 8-double DGKS records (one
+ * per column of a block expansion): host_dst receives gn + p + 8*nstate. */
+int svdsb_status_pack_n(const double *lams, int gn, const double *rn2, int p,
+                        const double *state, int nstate, double *host_dst,
+                        void *stream);
+/* Standard-normal block out[r + c*ldo] (r < rows, c < cols) for global rows
+ * row0 .. row0+rows-1 of a cols-wide block: element (R, c) is a pure
+ * function of (seed, R*cols + c) (Philox4x32-10 counter RNG, Box-Muller), so
+ * a row-partitioned caller gets the slices of one global block.  Replaces
+ * the host draw rng.standard_normal((N, cols)) of eigensolver.py:283-292
+ * for large N (a different stream: same distribution, not the same bits). */
+int svdsb_randn(uint64_t seed, int64_t row0, int64_t rows, int cols,
+                double *out, int64_t ldo, void *stream);
 /* *dst = v on the stream (stream-ordered scalar update for the above). */
 int svdsb_set_int(int *dst, int v, void *stream);
 /* Stage-2 split statistics of candidate vectors on the stacked layout

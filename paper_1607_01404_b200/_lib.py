@@ -61,7 +61,9 @@ _PROTOS = [
     ("svdsb_axpby", i32, [i64, i32, f64, vp, i64, f64, vp, i64, vp]),
     ("svdsb_gather_cols", i32, [i64, vp, i64, vp, i32, i32, vp, vp, i64, vp]),
     ("svdsb_set_int", i32, [vp, i32, vp]),
+    ("svdsb_randn", i32, [ctypes.c_uint64, i64, i64, i32, vp, i64, vp]),
     ("svdsb_status_pack", i32, [vp, i32, vp, i32, vp, vp, vp]),
+    ("svdsb_status_pack_n", i32, [vp, i32, vp, i32, vp, i32, vp, vp]),
     ("svdsb_split_stats",i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp]),
     ("svdsb_dgks_begin", i32, [vp, vp]),
     ("svdsb_cgs_fused", i32, [vp, i64, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp, i64, i32, i32, vp, i64, i32,

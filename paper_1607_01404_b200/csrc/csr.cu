@@ -2261,6 +2261,16 @@ static int pack(const double *x, int64_t rows, int64_t ldx, int b, double *xr, c
 }
 
 static inline bool packed_block(int b) { return b >= 2 && b <= 4; }
+// Width of the next column chunk of a wide block: fours, with the
+// remainder spread so no chunk is a lone column (5 -> 3+2, 6 -> 3+3,
+// 9 -> 4+3+2, ...) while at least 4 remain.
+static inline int chunk_cols(int left) {
+  if (left <= 4) return left;
+  if (left == 5) return 3;
+  if (left == 6) return 3;
+  if (left == 7) return 4;
+  return 4;
+}
 
 int svdsb_matvec(svdsb_ctx *ctx, const svdsb_csr *a, int transpose, const double *x, int64_t ldx, double *y,
                  int64_t ldy, int block, void *stream) {
@@ -2272,6 +2282,19 @@ int svdsb_matvec(svdsb_ctx *ctx, const svdsb_csr *a, int transpose, const double
   SVDSB_CHECK_ARG(!transpose || a->has_t, "svdsb_matvec: transpose requested but CSR(A^T) was not built");
   const CsrPart &p = transpose ? a->at : a->a;
   SVDSB_CHECK_ARG(ldx >= p.cols && ldy >= p.rows, "svdsb_matvec: leading dimension too small");
+  if (block > 4) {
+    // wide blocks (initial basis, soft-lock finalisation) in chunks of at
+    // most four columns through the packed kernels: every column's sum order
+    // is independent of the block width, so the bits are those of the
+    // narrow products
+    for (int c0 = 0; c0 < block;) {
+      const int nb = chunk_cols(block - c0);
+      int rc = svdsb_matvec(ctx, a, transpose, x + c0 * ldx, ldx, y + c0 * ldy, ldy, nb, stream);
+      if (rc) return rc;
+      c0 += nb;
+    }
+    return SVDSB_OK;
+  }
   if (packed_block(block)) {
     double *xr = scratch_get(a, 0, (size_t)p.cols * block);
     if (!xr) {
@@ -2297,6 +2320,15 @@ int svdsb_apply_normal(svdsb_ctx *ctx, const svdsb_csr *a, int side, const doubl
   cudaStream_t st = as_stream(stream);
   const CsrPart &first = side == 0 ? a->a : a->at;    // inner product
   const CsrPart &second = side == 0 ? a->at : a->a;
+  if (block > 4) {  // as svdsb_matvec: chunks of at most four columns
+    for (int c0 = 0; c0 < block;) {
+      const int nb = chunk_cols(block - c0);
+      int rc = svdsb_apply_normal(ctx, a, side, x + c0 * ldx, ldx, y + c0 * ldy, ldy, nb, tmp, ldtmp, stream);
+      if (rc) return rc;
+      c0 += nb;
+    }
+    return SVDSB_OK;
+  }
   if (packed_block(block)) {
     // x packed once; the inner result stays row-major for the second gather
     double *xr = scratch_get(a, 0, (size_t)first.cols * block);

@@ -432,9 +432,9 @@ __global__ void gather_cols_kernel(int64_t dim, const double *x, int64_t ldx, co
 // Replaces three small device->host copies at the end of every graphed
 // iteration.
 __global__ void status_pack_kernel(const double *__restrict__ lams, int gn, const double *__restrict__ rn2, int p,
-                                   const double *__restrict__ st, double *host) {
+                                   const double *__restrict__ st, int nst, double *host) {
   pdl_wait();
-  for (int i = threadIdx.x; i < gn + p + 8; i += blockDim.x) {
+  for (int i = threadIdx.x; i < gn + p + 8 * nst; i += blockDim.x) {
     double v;
     if (i < gn)
       v = lams[i];
@@ -445,6 +445,41 @@ __global__ void status_pack_kernel(const double *__restrict__ lams, int gn, cons
     host[i] = v;
   }
   __threadfence_system();
+}
+
+// Counter-based standard normals (Philox4x32-10 + Box-Muller) for the
+// initial basis block of large problems: element (R, c) of a grows x cols
+// block is a pure function of (seed, R * cols + c), so every row partition
+// draws the same global block and reruns are bit-reproducible.
+__device__ __forceinline__ void philox_round(uint32_t (&c)[4], uint32_t k0, uint32_t k1) {
+  const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+  const uint32_t h0 = (uint32_t)(p0 >> 32), l0 = (uint32_t)p0, h1 = (uint32_t)(p1 >> 32), l1 = (uint32_t)p1;
+  c[0] = h1 ^ c[1] ^ k0;
+  c[1] = l1;
+  c[2] = h0 ^ c[3] ^ k1;
+  c[3] = l0;
+}
+
+__global__ void randn_kernel(uint64_t seed, int64_t row0, int64_t rows, int cols, double *__restrict__ out,
+                             int64_t ldo) {
+  pdl_wait();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * cols) return;
+  const int64_t r = i % rows, c = i / rows;          // column-major walk: coalesced stores
+  const uint64_t e = (uint64_t)(row0 + r) * (uint64_t)cols + (uint64_t)c;
+  uint32_t x[4] = {(uint32_t)e, (uint32_t)(e >> 32), 0x5fd0u, 0u};
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int t = 0; t < 10; ++t) {
+    philox_round(x, k0, k1);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  const uint64_t a = ((uint64_t)x[0] << 21) ^ (uint64_t)x[1];   // 53 bits used below
+  const uint64_t b = ((uint64_t)x[2] << 21) ^ (uint64_t)x[3];
+  const double u1 = ((double)(a & ((1ull << 53) - 1)) + 0.5) * 0x1p-53;   // (0, 1)
+  const double u2 = (double)(b & ((1ull << 53) - 1)) * 0x1p-53;           // [0, 1)
+  out[r + c * ldo] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
 }
 
 __global__ void set_int_kernel(int *dst, int v) {
@@ -1544,11 +1579,27 @@ int svdsb_gather_cols(int64_t dim, const double *x, int64_t ldx, const int *firs
   return SVDSB_OK;
 }
 
-int svdsb_status_pack(const double *lams, int gn, const double *rn2, int p, const double *state,
-                       double *host_dst, void *stream) {
+int svdsb_status_pack_n(const double *lams, int gn, const double *rn2, int p, const double *state, int nstate,
+                        double *host_dst, void *stream) {
   SVDSB_CHECK_ARG(lams != nullptr && rn2 != nullptr && state != nullptr && host_dst != nullptr,
                   "svdsb_status_pack: NULL argument");
-  SVDSB_LAUNCH_PDL(status_pack_kernel, 1, 128, 0, as_stream(stream), lams, gn, rn2, p, state, host_dst);
+  SVDSB_CHECK_ARG(nstate >= 1 && nstate <= 64, "svdsb_status_pack: 1..64 DGKS records");
+  SVDSB_LAUNCH_PDL(status_pack_kernel, 1, 128, 0, as_stream(stream), lams, gn, rn2, p, state, nstate, host_dst);
+  return SVDSB_OK;
+}
+
+int svdsb_status_pack(const double *lams, int gn, const double *rn2, int p, const double *state,
+                      double *host_dst, void *stream) {
+  return svdsb_status_pack_n(lams, gn, rn2, p, state, 1, host_dst, stream);
+}
+
+int svdsb_randn(uint64_t seed, int64_t row0, int64_t rows, int cols, double *out, int64_t ldo, void *stream) {
+  SVDSB_CHECK_ARG(out != nullptr && rows >= 0 && cols >= 0 && row0 >= 0 && (cols == 0 || ldo >= rows),
+                  "svdsb_randn: bad arguments");
+  const int64_t tot = rows * cols;
+  if (tot == 0) return SVDSB_OK;
+  SVDSB_LAUNCH_PDL(randn_kernel, (unsigned)((tot + 255) / 256), 256, 0, as_stream(stream), seed, row0, rows, cols,
+                   out, ldo);
   return SVDSB_OK;
 }
 

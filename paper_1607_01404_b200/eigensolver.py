@@ -119,6 +119,7 @@ class EigStats:
     graphs_captured: int = 0
     inner_iterations: int = 0
     inner_solves: int = 0
+    device_rng: bool = False   # initial block from svdsb_randn (not the reference's numpy stream)
 
 
 @dataclass
@@ -344,15 +345,20 @@ class _Workspace:
         self.y = [dv.small_matrix(gm, gm) for _ in range(2)]
         self.rbuf = [dv.new_block(n, pmax) for _ in range(2)]
         self.stat = [torch.zeros(8 * pmax + 4, dtype=DTYPE, device=dev) for _ in range(2)]
-        self.dgks = [torch.zeros(8, dtype=DTYPE, device=dev) for _ in range(2)]
-        self.status = [torch.zeros(2 * gm + 32, dtype=DTYPE, pin_memory=True) for _ in range(2)]
+        # one 8-double DGKS record per column of a block expansion
+        self.dgks = [torch.zeros(8 * max(bs, 1), dtype=DTYPE, device=dev) for _ in range(2)]
+        self.status = [torch.zeros(2 * gm + 8 * max(bs, 1) + 32, dtype=DTYPE, pin_memory=True) for _ in range(2)]
+        # preconditioned expansion block of a speculative block expansion
+        # (kept so a rejected speculation can be redone on the host path)
+        self.src = [dv.new_block(n, bs) for _ in range(2)] if bs > 1 else None
+        self.hcb = dv.small_matrix(gm + bs, bs)
         self.events = [torch.cuda.Event() for _ in range(2)]
         self.coefs = dv.small_matrix(gm, gm)
         self.count = torch.zeros(1, dtype=torch.int32, device=dev)
         self.prev = dv.small_matrix(gm, max(plus_k, 1))
         self.yref = torch.zeros(gm, dtype=DTYPE, device=dev)
         self.excl = torch.zeros(gm, dtype=DTYPE, device=dev)
-        self.dgks_eager = torch.zeros(8, dtype=DTYPE, device=dev)
+        self.dgks_eager = torch.zeros(8 * max(bs, 1), dtype=DTYPE, device=dev)
         self.hc1 = dv.small_matrix(gm + 1, 1)
         self.ci = torch.zeros(1, dtype=torch.int32, device=dev)   # selected candidate (device copy)
         self.zero_i = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -495,8 +501,8 @@ class DavidsonSolver:
         self.warm_start = True
         self.speculate = True       # device-decided DGKS for single-column expansions
         self._spec = None
-        self._dgks_state = self._ws.dgks_eager if self._ws is not None else torch.zeros(8, dtype=DTYPE,
-                                                                                         device=ctx.device)
+        self._dgks_state = self._ws.dgks_eager if self._ws is not None else torch.zeros(
+            8 * max(bs, 1), dtype=DTYPE, device=ctx.device)
 
         need_v1, split1 = _test_needs(cfg.convergence_test)
         need_v2, split2 = _test_needs(cfg.practical_test)
@@ -590,6 +596,28 @@ class DavidsonSolver:
         stream on every rank), this rank's rows."""
         return self._local_rows(self.rng.standard_normal((self.n_global, cols)))
 
+    # Initial blocks of at least this many draws come from the device
+    # counter RNG (svdsb_randn) instead of the host draw of the reference's
+    # numpy stream: a 10 M x 20 host draw alone costs ~0.2 s (config 4).
+    # Smaller problems keep the reference's stream, so their iterates and
+    # matvec counts match the reference's; SVDSB_DEVICE_RNG_MIN overrides.
+    device_rng_min = int(os.environ.get("SVDSB_DEVICE_RNG_MIN", str(1 << 22)))
+
+    def _draw_into(self, block, cols):
+        """block[:, :cols] = the initial standard-normal block
+        (eigensolver.py:283-292)."""
+        row0 = 0
+        if self.comm.distributed:
+            row0 = getattr(self.op, "local_row0", None)
+        if (row0 is not None and getattr(self.ctx, "handle", None) is not None
+                and self.n_global * cols >= self.device_rng_min):
+            seed = (int(self.cfg.seed) * 0x9E3779B97F4A7C15 + 0x5FD) & ((1 << 64) - 1)
+            blk = block[:, :cols]
+            _lib.call("svdsb_randn", seed, int(row0), self.n, int(cols), dv.P(blk), dv.ld_of(blk), self.ctx.stream)
+            self.stats.device_rng = True
+            return
+        self._upload_normal(block[:, :cols], self._draw(cols))
+
     def _red(self, *tensors):
         """Finish local partial sums across ranks (globalSum)."""
         if self.comm.distributed:
@@ -628,7 +656,7 @@ class DavidsonSolver:
             g0 = take
         if g0 == 0:
             b0 = min(max(cfg.max_block_size, cfg.num_evals), self.gmax - 1)
-            self._upload_normal(self.v[:, :b0], self._draw(b0))
+            self._draw_into(self.v, b0)
             self.orthonormalize(self.v[:, :b0], against=self._against())
             g0 = b0
         if cfg.deactivate_krylov_init:
@@ -1026,7 +1054,7 @@ class DavidsonSolver:
             self._use_slot(pend["slot"])
             lams_d, y_d = self.lams_d[:g], self.y_d[:g, :g]
             r, x, ox, split = self.rbuf[:, :p], None, None, None
-            got = self._wait_status(g, p, pend["slot"])
+            got = self._wait_status(g, p, pend["slot"], pend["b"])
             st = got.pop()
             if not self._resolve_speculation(st):
                 # the queued next iteration was built on the collapsed column
@@ -1252,7 +1280,8 @@ class DavidsonSolver:
     SPEC_PASSES = 3
 
     def _can_speculate(self, b):
-        return (b == 1 and self.speculate and self.q is None and not self.comm.distributed
+        return ((b == 1 or (self._ws is not None and self._ws.src is not None and b <= self.cfg.max_block_size))
+                and self.speculate and self.q is None and not self.comm.distributed
                 and self.g >= 1 and getattr(self.ctx, "handle", None) is not None)
 
     def _use_fused_cgs(self, cols):
@@ -1263,6 +1292,9 @@ class DavidsonSolver:
                 and _lib.cgs_fused_supported())
 
     def _expand_speculative(self, block, precondition=True):
+        if block.shape[1] > 1:
+            self._expand_speculative_block(block, precondition)
+            return
         g = self.g
         dst = self.v[:, g:g + 1]
         prior = [b for b in self._against()] + [self.v[:, :g]]
@@ -1309,10 +1341,67 @@ class DavidsonSolver:
         self._spec = {"g0": g}
         self.g = g + 1
 
+    def _expand_speculative_block(self, block, precondition=True, slot=None):
+        """Block expansion (eigensolver.py:666-700 with b > 1) with every
+        column's DGKS passes decided on the device: column j is
+        orthonormalised against the basis and the new columns before it, as
+        the reference's column loop does, with no host round trip; the b
+        DGKS records ride along with the next status read."""
+        g = self.g
+        b = block.shape[1]
+        ws = self._ws
+        src = ws.src[self._slot if slot is None else slot][:, :b]
+        if self.precond is not None and precondition:
+            self.precond.apply_into(block, src)
+            self.stats.precond_applies += b
+        else:
+            dv.axpby(self.ctx, 1.0, block, 0.0, src)
+        st = self._dgks_state
+        for j in range(b):
+            prior = self._against() + [self.v[:, :g + j]]
+            self._spec_cgs(prior, src[:, j:j + 1], self.v[:, g + j:g + j + 1], st[8 * j:8 * j + 8])
+        self._apply_op(self.v[:, g:g + b], self.w[:, g:g + b])
+        hc = ws.hcb[:g + b, :b]
+        dv.gram(self.ctx, self.n, [self.v[:, :g + b]], self.w[:, g:g + b], hc)
+        dv.h_insert(self.ctx, g, b, hc, self.h)
+        self._spec = {"g0": g, "b": b, "src": src}
+        self.g = g + b
+
+    def _resolve_block(self, spec, st):
+        """Resolve a speculative block expansion: it stands when every
+        column was accepted by DGKS within SPEC_PASSES; otherwise the whole
+        block is redone on the host path from the kept preconditioned
+        directions (the reference's column loop, random replacement
+        included)."""
+        g, b, src = spec["g0"], spec["b"], spec["src"]
+        rec = np.asarray(st[:8 * b]).reshape(b, 8)
+        if np.all(rec[:, 0] == 0.0) and np.all(rec[:, 5] > 0.0):
+            self.collapse_streak = 0
+            return True
+        self.g = g
+        self._uncount_products(b)
+        dv.axpby(self.ctx, 1.0, src, 0.0, self.v[:, g:g + b])
+        replaced = self.orthonormalize(self.v[:, :g + b], against=self._against(), start_col=g)
+        if len(replaced) == b:
+            self.collapse_streak += 1
+            if self.collapse_streak >= 3:
+                raise BasisCollapseError("no independent expansion direction after 3 retries")
+        else:
+            self.collapse_streak = 0
+        self._apply_op(self.v[:, g:g + b], self.w[:, g:g + b])
+        hc = dv.small_matrix(g + b, b)
+        dv.gram(self.ctx, self.n, [self.v[:, :g + b]], self.w[:, g:g + b], hc)
+        dv.h_insert(self.ctx, g, b, hc, self.h)
+        self.g = g + b
+        self._warm = None
+        return False
+
     def _resolve_speculation(self, st):
         """Called with the fetched DGKS state; True if the speculative
         expansion stands, else it has been redone on the host path."""
         spec, self._spec = self._spec, None
+        if spec.get("b", 1) > 1:
+            return self._resolve_block(spec, st)
         if st[0] == 0.0 and st[5] > 0.0:
             self.collapse_streak = 0
             return True
@@ -1387,12 +1476,16 @@ class DavidsonSolver:
                 and self._split_n is None and not self._need_vecs and self.cfg.iteration_hook is None
                 and not self.ext and getattr(self.op, "graph_key", None) is not None
                 and (self.precond is None or getattr(self.precond, "diagonal", None) is not None))
-        return (static and b == 1 and self.speculate and self.q is None and self.g >= 1 and self.warm_start
+        return (static and (b == 1 or (self._ws.src is not None and b <= self.cfg.max_block_size))
+                and self.speculate and self.q is None and self.g >= 1 and self.warm_start
                 and self._warm is not None and self.locked_vecs.shape[1] == 0)
 
-    def _iter_device(self, g, kind, g0, p, order, shift, sin, sout):
+    def _iter_device(self, g, kind, g0, p, order, shift, sin, sout, b=1):
         """Launch-only body of a graphed iteration (no host bookkeeping):
         expand with candidate *ws.ci of slot sin, extract into slot sout."""
+        if b > 1:
+            self._iter_device_block(g, kind, g0, p, order, shift, sin, sout, b)
+            return
         ctx = self.ctx
         ws = self._ws
         dst = self.v[:, g:g + 1]
@@ -1454,6 +1547,37 @@ class DavidsonSolver:
         _lib.call("svdsb_status_pack", dv.P(l_out), gn, dv.P(s_out), p, dv.P(st), ws.status[sout].data_ptr(),
                   ctx.stream)
 
+    def _iter_device_block(self, g, kind, g0, p, order, shift, sin, sout, b):
+        """_iter_device for a block expansion of b columns (candidates
+        *ws.ci .. *ws.ci + b - 1): the +k copy, the preconditioned residual
+        block, device-decided CGS column by column, the b-column operator
+        product, the H border, the warm b-border RR update, the candidate
+        residuals and the status record with b DGKS records."""
+        ctx = self.ctx
+        ws = self._ws
+        y_in, l_in = ws.y[sin], ws.lams[sin]
+        y_out, l_out, r_out, s_out = ws.y[sout], ws.lams[sout], ws.rbuf[sout], ws.stat[sout]
+        kk = max(self.cfg.plus_k, 1)
+        d = self.precond.diagonal if self.precond is not None else None
+        st = ws.dgks[sout]
+        src = ws.src[sout][:, :b]
+        dv.gather_cols(ctx, y_in[:g, :g], ws.ci, kk, g, self.prev_d[:g, :kk])
+        dv.gather_cols(ctx, ws.rbuf[sin], ws.ci, b, self.pmax, src, d=d)
+        for j in range(b):
+            self._spec_cgs([self.v[:, :g + j]], src[:, j:j + 1], self.v[:, g + j:g + j + 1], st[8 * j:8 * j + 8])
+        self.op.raw_into(self.v[:, g:g + b], self.w[:, g:g + b])
+        hc = ws.hcb[:g + b, :b]
+        dv.gram(ctx, self.n, [self.v[:, :g + b]], self.w[:, g:g + b], hc)
+        dv.h_insert(ctx, g, b, hc, self.h)
+        gn = g + b
+        y0 = y_in[:g0, :g0] if kind == "prev" else None
+        l0 = l_in[:g0] if kind == "prev" else None
+        dv.syev_update(ctx, self.h, g0, gn - g0, y0, l0, order, shift, l_out[:gn], y_out[:gn, :gn])
+        dv.ritz_residual(ctx, self.v[:, :gn], self.w[:, :gn], y_out[:gn, :p], l_out[:p],
+                         r_out[:, :p], rn2=s_out[:p])
+        _lib.call("svdsb_status_pack_n", dv.P(l_out), gn, dv.P(s_out), p, dv.P(st), b, ws.status[sout].data_ptr(),
+                  ctx.stream)
+
     def _capture(self, fn, reuse=None):
         """Record fn's libsvdsb launches as a CUDA graph on a side stream
         (capture needs a non-default stream) and instantiate it -- or, with
@@ -1482,20 +1606,20 @@ class DavidsonSolver:
             reuse.exec = None   # ownership moves to the returned graph
         return _NativeGraph(ex.value)
 
-    def _launch_iter(self, g, kind, g0, sin, ci):
+    def _launch_iter(self, g, kind, g0, sin, ci, b=1):
         """Replay (capturing on first use) the iteration graph that expands
-        a basis of size g from slot sin; returns the queued-iteration
-        record."""
+        a basis of size g by b columns from slot sin; returns the
+        queued-iteration record."""
         ws = self._ws
         sout = 1 - sin
-        p = min(self.wanted + self.cfg.max_block_size, g + 1)
+        p = min(self.wanted + self.cfg.max_block_size, g + b)
         order, shift = self._order_mode()
         base = self._graph_base
         if base is None:
             # operator / preconditioner identity: fixed for the solve
             base = self._graph_base = (self.op.graph_key(),
                                        None if self.precond is None else self.precond.diagonal.data_ptr())
-        key = (self.v.data_ptr(), self.w.data_ptr(), kind, g0, g, p, sin, order, shift, base)
+        key = (self.v.data_ptr(), self.w.data_ptr(), kind, g0, g, b, p, sin, order, shift, base)
         entry = ws.graphs.get(key)
         if entry is None:
             # one graph per iteration shape: the one captured for another
@@ -1504,7 +1628,7 @@ class DavidsonSolver:
             old_key = ws.graph_shape.get(skey)
             old = ws.graphs.pop(old_key, None) if old_key is not None else None
             before = _lib.launch_count()
-            graph = self._capture(lambda: self._iter_device(g, kind, g0, p, order, shift, sin, sout),
+            graph = self._capture(lambda: self._iter_device(g, kind, g0, p, order, shift, sin, sout, b),
                                   reuse=None if old is None else old[0])
             entry = (graph, _lib.launch_count() - before)
             ws.graphs[key] = entry
@@ -1513,16 +1637,24 @@ class DavidsonSolver:
         entry[0].replay(self.ctx._stream)
         ws.events[sout].record(self.ctx.torch_stream)
         _lib.load().svdsb_note_launches(entry[1])
-        return {"p": p, "slot": sout, "sin": sin, "g": g, "ci": ci}
+        return {"p": p, "slot": sout, "sin": sin, "g": g, "ci": ci, "b": b}
 
-    def _expand_graphed(self, ci):
+    def _block_width(self, ci, g):
+        """Columns of the expansion that follows an extraction at basis size
+        g with candidate ci (eigensolver.py:650-656: the residual block
+        res[:, ci:ci+b] of p candidates, cut to the free basis columns)."""
+        bs = self.cfg.max_block_size
+        p = min(self.wanted + bs, g)
+        return min(min(ci + bs, p) - ci, self.gmax - g)
+
+    def _expand_graphed(self, ci, b=1):
         ws = self._ws
         g = self.g
         sin = self._slot
         ahead, self._ahead = self._ahead, None
         self._ahead_used = True
         if ahead is not None and ahead["g"] == g and ahead["ci"] == ci and ahead["sin"] == sin \
-                and self._warm == ("prev", g):
+                and ahead["b"] == b and self._warm == ("prev", g):
             pend = ahead          # already running: the guess was right
         else:
             if ws.ci_host != ci:
@@ -1533,33 +1665,35 @@ class DavidsonSolver:
                 # a restart cycle always starts from slot 0 (the diag-warm
                 # iteration reads only the chosen residual), so each basis
                 # size maps to one slot and half as many graphs get captured
-                dv.axpby(self.ctx, 1.0, ws.rbuf[1][:, ci:ci + 1], 0.0, ws.rbuf[0][:, ci:ci + 1])
+                dv.axpby(self.ctx, 1.0, ws.rbuf[1][:, ci:ci + b], 0.0, ws.rbuf[0][:, ci:ci + b])
                 sin = 0
-            pend = self._launch_iter(g, kind, g0, sin, ci)
+            pend = self._launch_iter(g, kind, g0, sin, ci, b)
         # host bookkeeping of what the graph does
         if self.precond is not None:
-            self.precond.n_applies += 1
-            self.stats.precond_applies += 1
-        self.stats.matvecs += 1
-        self.op.n_applies += 1
-        self.op.count_svd_matvecs(1)
-        self._spec = {"g0": g}
-        self.g = g + 1
-        self._warm = ("prev", g + 1)
+            self.precond.n_applies += b
+            self.stats.precond_applies += b
+        self.stats.matvecs += b
+        self.op.n_applies += b
+        self.op.count_svd_matvecs(b)
+        self._spec = {"g0": g, "b": b, "src": ws.src[pend["slot"]][:, :b] if b > 1 else None}
+        self.g = g + b
+        self._warm = ("prev", g + b)
         self._pending = pend
         # queue the next iteration on the usual decision; with a full basis
-        # the host would restart instead, so only while g + 1 < gmax
-        if self.run_ahead and g + 1 < self.gmax:
-            self._ahead = self._launch_iter(g + 1, "prev", g + 1, pend["slot"], ci)
+        # the host would restart instead, so only while g + b < gmax
+        if self.run_ahead and g + b < self.gmax:
+            b_next = self._block_width(ci, g + b)
+            if b_next >= 1:
+                self._ahead = self._launch_iter(g + b, "prev", g + b, pend["slot"], ci, b_next)
 
-    def _wait_status(self, g, p, slot):
+    def _wait_status(self, g, p, slot, b=1):
         """Wait for the queued iteration that writes `slot` (not for a
         later one queued behind it) and read its status."""
         ws = self._ws
         ws.events[slot].synchronize()
         self.stats.syncs += 1
         host = ws.status[slot].numpy()
-        return [host[:g].copy(), host[g:g + p].copy(), host[g + p:g + p + 8].copy()]
+        return [host[:g].copy(), host[g:g + p].copy(), host[g + p:g + p + 8 * b].copy()]
 
     def _expand(self, res_block, ci=0, graph=True, precondition=True):
         """eigensolver.py:666-700.  precondition=False: the block is already
@@ -1568,7 +1702,7 @@ class DavidsonSolver:
         if b <= 0:
             return
         if graph and precondition and self._graph_ok(b):
-            self._expand_graphed(ci)
+            self._expand_graphed(ci, b)
             return
         block = res_block[:, :b]
         if self._can_speculate(b):

@@ -263,6 +263,7 @@ def make_normal_operator(a):
         op.comm = a.comm
         op.dim_global = a.n
         op.local_slice = a.n_slice
+        op.local_row0 = a.c0
         return op
     base = a.base if isinstance(a, _TransposedSvdOperator) else a
     dev = getattr(base, "_csr_dev", None)
