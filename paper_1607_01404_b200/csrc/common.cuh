@@ -144,6 +144,8 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // Key 4: native GD+k iteration (0 H-column / status epilogues, 1 separate
 // h_insert and status_pack launches).
 // Key 5: transposed b = 4 SpMV (0 length-sorted sliced ELL, 1 CSR tiles).
+// Key 6: 2- and 3-column products of short-row matrices (0 zero-padded to
+// the 4-column kernels, 1 the b-column CSR tile kernels).
 constexpr int kTuneKeys = 8;
 inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0};
 

@@ -80,8 +80,8 @@ struct svdsb_csr {
   bool has_t;
   // row-major staging for block products (2 <= b <= 4): packed input and
   // the inner product of the normal operator; grown on demand
-  double *scratch[2] = {nullptr, nullptr};
-  size_t scratch_cap[2] = {0, 0};
+  double *scratch[3] = {nullptr, nullptr, nullptr};
+  size_t scratch_cap[3] = {0, 0, 0};
   // A^T split by row blocks of A (tall, scattered matrices): local column
   // ids, block k covers rows [atb_r0[k], atb_r0[k+1]) of A
   std::vector<svdsb::CsrPart> atb;
@@ -1212,6 +1212,26 @@ __global__ void pack_rows_kernel(int64_t rows, int b, const double *__restrict__
   xr[i] = x[r + cc * ldx];
 }
 
+// Row-major copy of a b-column block with stride bp >= b (columns b..bp-1
+// zero): 2- and 3-column products run the 4-column kernels.
+__global__ void pack_pad_kernel(int64_t rows, int b, int bp, const double *__restrict__ x, int64_t ldx,
+                                double *__restrict__ xr) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * bp) return;
+  int64_t r = i / bp;
+  int cc = (int)(i - r * bp);
+  xr[i] = cc < b ? x[r + cc * ldx] : 0.0;
+}
+
+__global__ void unpack_pad_kernel(int64_t rows, int b, int bp, const double *__restrict__ xr, double *__restrict__ y,
+                                  int64_t ldy) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * b) return;
+  int64_t r = i % rows;
+  int cc = (int)(i / rows);
+  y[r + cc * ldy] = xr[r * bp + cc];
+}
+
 __global__ void unpack_rows_kernel(int64_t rows, int b, const double *__restrict__ xr, double *__restrict__ y,
                                    int64_t ldy) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1911,8 +1931,7 @@ int svdsb_csr_destroy(svdsb_csr *a) {
   free_part(a->a);
   free_part(a->at);
   for (auto &p : a->atb) free_part(p);
-  cudaFree(a->scratch[0]);
-  cudaFree(a->scratch[1]);
+  for (double *sp : a->scratch) cudaFree(sp);
   delete a;
   return SVDSB_OK;
 }
@@ -2261,6 +2280,30 @@ static int pack(const double *x, int64_t rows, int64_t ldx, int b, double *xr, c
 }
 
 static inline bool packed_block(int b) { return b >= 2 && b <= 4; }
+
+static int pack_pad(const double *x, int64_t rows, int64_t ldx, int b, int bp, double *xr, cudaStream_t st) {
+  const int64_t tot = rows * bp;
+  if (tot == 0) return SVDSB_OK;
+  pack_pad_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(rows, b, bp, x, ldx, xr);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+static int unpack_pad(const double *xr, int64_t rows, int b, int bp, double *y, int64_t ldy, cudaStream_t st) {
+  const int64_t tot = rows * b;
+  if (tot == 0) return SVDSB_OK;
+  unpack_pad_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(rows, b, bp, xr, y, ldy);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+// 2- and 3-column products of short-row matrices go through the 4-column
+// sliced-ELL kernels with a zero-padded operand (a zero column changes no
+// other column's bits; a 24-byte gather costs the same 32-byte sector).
+static inline bool pad_to4(const svdsb_csr *a, int b) {
+  return (b == 2 || b == 3) && a->a.nlong == 0 && a->a.maxlen <= 129 && a->has_t && a->at.ntile > 0 &&
+         g_tune[6] == 0;
+}
 // Width of the next column chunk of a wide block: fours, with the
 // remainder spread so no chunk is a lone column (5 -> 3+2, 6 -> 3+3,
 // 9 -> 4+3+2, ...) while at least 4 remain.
@@ -2295,6 +2338,22 @@ int svdsb_matvec(svdsb_ctx *ctx, const svdsb_csr *a, int transpose, const double
     }
     return SVDSB_OK;
   }
+  if (pad_to4(a, block)) {
+    double *xr = scratch_get(a, 0, (size_t)p.cols * 4);
+    double *yr = scratch_get(a, 2, (size_t)p.rows * 4);
+    if (!xr || !yr) {
+      set_error("svdsb_matvec: scratch allocation failed");
+      return SVDSB_ERR_ALLOC;
+    }
+    int rc = pack_pad(x, p.cols, ldx, block, 4, xr, st);
+    if (rc) return rc;
+    if (transpose && !a->atb.empty())
+      rc = blocked_adj<1>(a, xr, 4, yr, 4, 1, 4, st);
+    else
+      rc = transpose ? part_matvec<1>(p, xr, 4, 1, yr, 4, 1, 4, st) : part_matvec<0>(p, xr, 4, 1, yr, 4, 1, 4, st);
+    if (rc) return rc;
+    return unpack_pad(yr, p.rows, block, 4, y, ldy, st);
+  }
   if (packed_block(block)) {
     double *xr = scratch_get(a, 0, (size_t)p.cols * block);
     if (!xr) {
@@ -2328,6 +2387,26 @@ int svdsb_apply_normal(svdsb_ctx *ctx, const svdsb_csr *a, int side, const doubl
       c0 += nb;
     }
     return SVDSB_OK;
+  }
+  if (pad_to4(a, block)) {
+    double *xr = scratch_get(a, 0, (size_t)first.cols * 4);
+    double *tr = scratch_get(a, 1, (size_t)first.rows * 4);
+    double *yr = scratch_get(a, 2, (size_t)second.rows * 4);
+    if (!xr || !tr || !yr) {
+      set_error("svdsb_apply_normal: scratch allocation failed");
+      return SVDSB_ERR_ALLOC;
+    }
+    int rc = pack_pad(x, first.cols, ldx, block, 4, xr, st);
+    if (rc) return rc;
+    rc = side == 0 ? part_matvec<0>(first, xr, 4, 1, tr, 4, 1, 4, st) : part_matvec<1>(first, xr, 4, 1, tr, 4, 1, 4, st);
+    if (rc) return rc;
+    if (side == 0 && !a->atb.empty())
+      rc = blocked_adj<1>(a, tr, 4, yr, 4, 1, 4, st);
+    else
+      rc = side == 0 ? part_matvec<1>(second, tr, 4, 1, yr, 4, 1, 4, st)
+                     : part_matvec<0>(second, tr, 4, 1, yr, 4, 1, 4, st);
+    if (rc) return rc;
+    return unpack_pad(yr, second.rows, block, 4, y, ldy, st);
   }
   if (packed_block(block)) {
     // x packed once; the inner result stays row-major for the second gather

@@ -580,7 +580,7 @@ gram1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, double *c
 template <int AT>
 __global__ void __launch_bounds__(kThreads)
 gram4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t ldy, double *c, int64_t ldc,
-                 double *norms2, double *partials, unsigned int *ticket, int ny) {
+                 double *norms2, double *partials, unsigned int *ticket, int ny, int nb) {
   pdl_wait();
   __shared__ const double *xp[AT];
   // ny > 0: one-dimensional grid with the ny column groups of a row range
@@ -603,7 +603,7 @@ gram4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t l
   for (; r + 1 < rr.r1; r += 2 * kThreads) {
     double2 yv[4], xv[AT];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) yv[j] = ldg2(y + r + (int64_t)j * ldy);
+    for (int j = 0; j < 4; ++j) yv[j] = ldg2(y + r + (int64_t)min(j, nb - 1) * ldy);  // nb < 4: re-read, unused
 #pragma unroll
     for (int i = 0; i < AT; ++i) xv[i] = ldg2(xp[i] + r);  // columns past na re-read the last one
 #pragma unroll
@@ -618,7 +618,7 @@ gram4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t l
   if (r < rr.r1) {  // odd tail row
     double yv[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) yv[j] = __ldg(y + r + (int64_t)j * ldy);
+    for (int j = 0; j < 4; ++j) yv[j] = __ldg(y + r + (int64_t)min(j, nb - 1) * ldy);
 #pragma unroll
     for (int i = 0; i < AT; ++i) {
       const double xv = __ldg(xp[i] + r);
@@ -637,8 +637,8 @@ gram4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t l
   fold_parts(partials, nx, NOUT, nty * NOUT, [&](int, int t, int k, double sum) {
     if (k < AT * 4) {
       const int i = t * AT + k / 4, j = k % 4;
-      if (k / 4 < min(AT, xs.total - t * AT)) c[i + (int64_t)j * ldc] = sum;
-    } else if (norms2 != nullptr && t == 0) {
+      if (k / 4 < min(AT, xs.total - t * AT) && j < nb) c[i + (int64_t)j * ldc] = sum;
+    } else if (norms2 != nullptr && t == 0 && k - AT * 4 < nb) {
       norms2[k - AT * 4] = sum;
     }
   });
@@ -1320,17 +1320,25 @@ int gram_impl(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, co
                        take_ticket(ctx), nullptr, hi);
     }
     return SVDSB_OK;
-  } else if (b == 4 && colset_vec_ok(s) && aligned16(y) && ldy % 2 == 0) {
+  } else if (b >= 2 && b <= 4 && colset_vec_ok(s) && aligned16(y) && ldy % 2 == 0) {
+    // up to four columns of y (2 or 3: the kernel masks the rest); wider
+    // blocks (full H rebuilds) read X once in the generic kernel below
     constexpr int AT = 8;
     const int ny = (s.total + AT - 1) / AT;
     dim3 grid(grid_for(gram4_vec_kernel<AT>, dim, 0), ny, 1);
     SVDSB_CHECK_ARG((int64_t)grid.x * grid.y * (AT * 4 + 4) <= kMaxPartials, "gram: workspace too small");
-    if (g_tune[1] != 2) {  // 2: column groups outermost (the slower order)
-      SVDSB_LAUNCH_PDL(gram4_vec_kernel<AT>, dim3(grid.x * ny, 1, 1), kThreads, 0, st, dim, s, y, ldy, c, ldc, norms2,
-                       ctx->partials, take_ticket(ctx), ny);
-    } else {
-      SVDSB_LAUNCH_PDL(gram4_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, y, ldy, c, ldc, norms2, ctx->partials,
-                       take_ticket(ctx), 0);
+    for (int j0 = 0; j0 < b; j0 += 4) {
+      const int nb = std::min(4, b - j0);
+      const double *yj = y + (int64_t)j0 * ldy;
+      double *cj = c + (int64_t)j0 * ldc;
+      double *nj = norms2 ? norms2 + j0 : nullptr;
+      if (g_tune[1] != 2) {  // 2: column groups outermost (the slower order)
+        SVDSB_LAUNCH_PDL(gram4_vec_kernel<AT>, dim3(grid.x * ny, 1, 1), kThreads, 0, st, dim, s, yj, ldy, cj, ldc, nj,
+                         ctx->partials, take_ticket(ctx), ny, nb);
+      } else {
+        SVDSB_LAUNCH_PDL(gram4_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, yj, ldy, cj, ldc, nj, ctx->partials,
+                         take_ticket(ctx), 0, nb);
+      }
     }
     return SVDSB_OK;
   } else if (b == 1) {

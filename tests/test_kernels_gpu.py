@@ -203,6 +203,41 @@ def test_spmv_transpose_b4_variants(variant, rng):
     assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
 
 
+@pytest.mark.parametrize("b", [2, 3])
+def test_spmv_b23_padded_to_b4(b, rng):
+    """2- and 3-column products of short-row matrices run the 4-column
+    sliced-ELL kernels on a zero-padded operand (svdsb_tune_set key 6 = 0)
+    or the b-column CSR tiles (key 6 = 1): bit-identical to each other, to
+    the oracle for rows up to a tile, and so is the normal operator."""
+    from paper_1607_01404_b200 import _lib, make_normal_operator, SvdOperator
+    dv = _dev()
+    m, n = 9000, 700
+    cols = np.concatenate([rng.integers(0, n, 60000), rng.integers(0, 40, 15000), np.full(2600, 650)])
+    rows = np.concatenate([np.arange(m).repeat(6), rng.integers(0, m, cols.size - 6 * m)])
+    vals = rng.standard_normal(cols.size)
+    a, (rp, ci, va) = _csr(m, n, rows, cols, vals)
+    x = rng.standard_normal((n, b))
+    y = rng.standard_normal((m, b))
+    op = make_normal_operator(SvdOperator.from_csr(a, check=False))
+    out = {}
+    for key in (0, 1):
+        try:
+            _lib.call("svdsb_tune_set", 6, key)
+            z = dv.new_block(n, b)
+            op.apply_into(dv.to_device_block(x), z)
+            out[key] = (_spmv_dev(a, x, False), _spmv_dev(a, y, True), dv.to_host(z))
+        finally:
+            _lib.call("svdsb_tune_set", 6, 0)
+    for u, v in zip(out[0], out[1]):
+        assert np.array_equal(u, v)
+    assert np.array_equal(out[0][0], ocsr.spmv(m, n, rp, ci, va, x))
+    want_t = ocsr.spmv(m, n, rp, ci, va, y, transpose=True)
+    lens = np.diff(ocsr.csr_transpose(m, n, rp, ci, va)[0])
+    ok = lens <= 2048
+    assert np.array_equal(out[0][1][ok], want_t[ok])
+    assert np.abs(out[0][1] - want_t).max() <= 1e-12 * np.abs(want_t).max()
+
+
 def test_spmv_bulk_copy_path_bit_exact(rng):
     """Matrices of >= 64 MB stream through the cp.async.bulk tile ring
     (csr_tile_bulk_kernel); it must reproduce the reference's summation
