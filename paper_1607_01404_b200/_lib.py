@@ -11,7 +11,10 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsvdsb.so")
+# SVDSB_LIB_VARIANT=<name>: load _lib/libsvdsb_<name>.so instead (A/B builds of
+# the same sources for kernel experiments; never set in tests or the bench)
+_VARIANT = os.environ.get("SVDSB_LIB_VARIANT", "")
+LIB_PATH = os.path.join(_HERE, "_lib", "libsvdsb%s.so" % ("_" + _VARIANT if _VARIANT else ""))
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 c_int64_p = ctypes.POINTER(ctypes.c_int64)

@@ -40,16 +40,25 @@ def up_to_date():
     return all(os.path.getmtime(f) <= t for f in _inputs())
 
 
-def build(force=False, verbose=False):
-    """Compile every .cu to an object, then link the shared library."""
-    if not force and up_to_date():
+def build(force=False, verbose=False, variant=None, overrides=None):
+    """Compile every .cu to an object, then link the shared library.
+
+    variant / overrides (kernel experiments only): link
+    _lib/libsvdsb_<variant>.so with some sources replaced by other files
+    (overrides: {"dense.cu": "/path/to/dense.cu"}); loaded when
+    SVDSB_LIB_VARIANT=<variant> is set."""
+    overrides = overrides or {}
+    lib = LIB if variant is None else os.path.join(OUT_DIR, "libsvdsb_%s.so" % variant)
+    if variant is None and not force and up_to_date():
         return LIB
-    os.makedirs(OUT_DIR, exist_ok=True)
+    odir = OUT_DIR if variant is None else os.path.join(OUT_DIR, "var_" + variant)
+    os.makedirs(odir, exist_ok=True)
     objs = []
     for src in SOURCES:
-        obj = os.path.join(OUT_DIR, os.path.splitext(src)[0] + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(REPO, "include"),
-               "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(odir, os.path.splitext(src)[0] + ".o")
+        path = overrides.get(src, os.path.join(CSRC, src))
+        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(REPO, "include"), "-I", CSRC,
+               "-c", path, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
@@ -57,20 +66,23 @@ def build(force=False, verbose=False):
         if verbose:
             sys.stderr.write(res.stderr)
         objs.append(obj)
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
-    return LIB
+    return lib
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("--override", action="append", default=[], metavar="SRC=PATH")
     args = ap.parse_args()
-    print(build(force=args.force, verbose=args.verbose))
+    ov = dict(o.split("=", 1) for o in args.override)
+    print(build(force=args.force, verbose=args.verbose, variant=args.variant, overrides=ov))
 
 
 if __name__ == "__main__":

@@ -187,6 +187,23 @@ __device__ __forceinline__ int ld_stream(const int *p) {
   asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+// The same for matrices that stream from HBM (config 3/4 scale): L2
+// evict-first, so the gathered operand block keeps its L2 residency.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double ld_ef(const double *p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_evict_first()));
+  return v;
+}
+__device__ __forceinline__ int ld_ef(const int *p) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_evict_first()));
+  return v;
+}
 
 // XROW: x is row-major with row stride b (one 8*b-byte gather per nonzero);
 // otherwise column-major with leading dimension ldx.  YROW likewise for y.
@@ -495,9 +512,16 @@ csr_tile_pipe_rows_kernel(int ntile, const int4 *__restrict__ info, const int *_
 // fold_row<0> -- p0 + numpy pairwise(rest): the first 8 tail products seed 8
 // accumulators, whole blocks of 8 follow, the remainder is added to the
 // tree sum -- for the four columns as independent chains.
+// One 32-byte x row (256-bit load, L2 evict-last: the gathered block stays
+// resident while the matrix streams past it).
 __device__ __forceinline__ void gather4(const double *x, int c, double (&o)[4]) {
-  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
-      : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(x + (int64_t)c * 4));
+  unsigned long long a, b, d, e;
+  asm("ld.global.nc.L2::evict_last.v4.b64 {%0, %1, %2, %3}, [%4];"
+      : "=l"(a), "=l"(b), "=l"(d), "=l"(e) : "l"(x + (int64_t)c * 4));
+  o[0] = __longlong_as_double(a);
+  o[1] = __longlong_as_double(b);
+  o[2] = __longlong_as_double(d);
+  o[3] = __longlong_as_double(e);
 }
 
 // One row's four products in the exact fold_row<0> order; `src` supplies
@@ -789,8 +813,8 @@ struct SellRowSrc {
   const double *__restrict__ val;
   const int *__restrict__ col;
   int64_t base;  // slice base + t - 32 k0 (element k sits at base + 32 k)
-  __device__ __forceinline__ double v(int k) const { return ld_stream(val + base + 32 * (int64_t)k); }
-  __device__ __forceinline__ int c(int k) const { return ld_stream(col + base + 32 * (int64_t)k); }
+  __device__ __forceinline__ double v(int k) const { return ld_ef(val + base + 32 * (int64_t)k); }
+  __device__ __forceinline__ int c(int k) const { return ld_ef(col + base + 32 * (int64_t)k); }
 };
 
 template <int YROW>
@@ -939,8 +963,8 @@ __device__ __forceinline__ void warprow4t(int64_t row, const int *__restrict__ r
   for (int k = k0; k < k1; k += 32) {
     const int e = k + lane;
     const bool ok = e < k1;
-    const int c = ok ? ld_stream(col + e) : 0;
-    const double v = ok ? ld_stream(val + e) : 0.0;
+    const int c = ok ? ld_ef(col + e) : 0;
+    const double v = ok ? ld_ef(val + e) : 0.0;
     double xv[4];
     gather4(x, c, xv);
 #pragma unroll
@@ -999,8 +1023,8 @@ csr_sell4t_kernel(int64_t nq, int64_t nslice, const int *__restrict__ perm, cons
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int j = min(j0 + u, len - 1);
-        vv[u] = ld_stream(sval + base + 32 * (int64_t)j);
-        gather4(x, ld_stream(scol + base + 32 * (int64_t)j), xv[u]);
+        vv[u] = ld_ef(sval + base + 32 * (int64_t)j);
+        gather4(x, ld_ef(scol + base + 32 * (int64_t)j), xv[u]);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -1245,7 +1269,13 @@ __global__ void unpack_rows_kernel(int64_t rows, int b, const double *__restrict
 __device__ __forceinline__ void gather_acc(const double *xr, int b, double v, double (&s)[4]) {
   if (b == 4) {
     double x0, x1, x2, x3;
-    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(x0), "=d"(x1), "=d"(x2), "=d"(x3) : "l"(xr));
+    unsigned long long a0, a1, a2, a3;
+    asm("ld.global.nc.L2::evict_last.v4.b64 {%0, %1, %2, %3}, [%4];"
+        : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3) : "l"(xr));
+    x0 = __longlong_as_double(a0);
+    x1 = __longlong_as_double(a1);
+    x2 = __longlong_as_double(a2);
+    x3 = __longlong_as_double(a3);
     s[0] = fma(v, x0, s[0]);
     s[1] = fma(v, x1, s[1]);
     s[2] = fma(v, x2, s[2]);
@@ -1273,18 +1303,18 @@ csr_chunk_kernel(const int *__restrict__ chunk_nz, const int *__restrict__ col,
     double s[4] = {0.0, 0.0, 0.0, 0.0};
     int k = nz0 + t;
     for (; k + 3 * kTileThreads < nz1; k += 4 * kTileThreads) {
-      int64_t c0 = ld_stream(col + k), c1 = ld_stream(col + k + kTileThreads);
-      int64_t c2 = ld_stream(col + k + 2 * kTileThreads), c3 = ld_stream(col + k + 3 * kTileThreads);
-      double v0 = ld_stream(val + k), v1 = ld_stream(val + k + kTileThreads);
-      double v2 = ld_stream(val + k + 2 * kTileThreads), v3 = ld_stream(val + k + 3 * kTileThreads);
+      int64_t c0 = ld_ef(col + k), c1 = ld_ef(col + k + kTileThreads);
+      int64_t c2 = ld_ef(col + k + 2 * kTileThreads), c3 = ld_ef(col + k + 3 * kTileThreads);
+      double v0 = ld_ef(val + k), v1 = ld_ef(val + k + kTileThreads);
+      double v2 = ld_ef(val + k + 2 * kTileThreads), v3 = ld_ef(val + k + 3 * kTileThreads);
       gather_acc(x + c0 * b, b, v0, s);
       gather_acc(x + c1 * b, b, v1, s);
       gather_acc(x + c2 * b, b, v2, s);
       gather_acc(x + c3 * b, b, v3, s);
     }
     for (; k < nz1; k += kTileThreads) {
-      int64_t c0 = ld_stream(col + k);
-      double v0 = ld_stream(val + k);
+      int64_t c0 = ld_ef(col + k);
+      double v0 = ld_ef(val + k);
       gather_acc(x + c0 * b, b, v0, s);
     }
 #pragma unroll
@@ -1303,9 +1333,9 @@ csr_chunk_kernel(const int *__restrict__ chunk_nz, const int *__restrict__ col,
   for (int cc = 0; cc < b; ++cc) {
     double s = 0.0;
     for (int k = nz0 + t; k < nz1; k += kTileThreads) {
-      int64_t cix = ld_stream(col + k);
+      int64_t cix = ld_ef(col + k);
       double xv = xrow ? __ldg(x + cix * b + cc) : __ldg(x + cix + cc * ldx);
-      s = fma(ld_stream(val + k), xv, s);
+      s = fma(ld_ef(val + k), xv, s);
     }
     s = warp_sum(s);
     if ((t & 31) == 0) red[t >> 5][0] = s;

@@ -577,10 +577,11 @@ gram1_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, double *c
 // b = 4 Gram C = X^T Y (+ |Y_j|^2): two rows per thread with 16-byte loads,
 // AT basis columns per CTA row of the grid; every load of a row pair is
 // issued before its FMAs (the generic gram_kernel keeps ~4 in flight).
-template <int AT>
+template <int AT, int NB>
 __global__ void __launch_bounds__(kThreads)
 gram4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t ldy, double *c, int64_t ldc,
-                 double *norms2, double *partials, unsigned int *ticket, int ny, int nb) {
+                 double *norms2, double *partials, unsigned int *ticket, int ny) {
+  constexpr int nb = NB;  // valid columns of y (2 or 3: the rest re-read column NB-1, unused)
   pdl_wait();
   __shared__ const double *xp[AT];
   // ny > 0: one-dimensional grid with the ny column groups of a row range
@@ -1320,24 +1321,26 @@ int gram_impl(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, co
                        take_ticket(ctx), nullptr, hi);
     }
     return SVDSB_OK;
-  } else if (b >= 2 && b <= 4 && colset_vec_ok(s) && aligned16(y) && ldy % 2 == 0) {
-    // up to four columns of y (2 or 3: the kernel masks the rest); wider
-    // blocks (full H rebuilds) read X once in the generic kernel below
+  } else if (b >= 2 && colset_vec_ok(s) && aligned16(y) && ldy % 2 == 0) {
+    // four columns of y per launch (a 2- or 3-column tail masks the rest);
+    // wide blocks (full H rebuilds) in chunks of four: 4x faster than one
+    // generic launch at g = 14..35
     constexpr int AT = 8;
     const int ny = (s.total + AT - 1) / AT;
-    dim3 grid(grid_for(gram4_vec_kernel<AT>, dim, 0), ny, 1);
+    dim3 grid(grid_for(gram4_vec_kernel<AT, 4>, dim, 0), ny, 1);
     SVDSB_CHECK_ARG((int64_t)grid.x * grid.y * (AT * 4 + 4) <= kMaxPartials, "gram: workspace too small");
     for (int j0 = 0; j0 < b; j0 += 4) {
       const int nb = std::min(4, b - j0);
       const double *yj = y + (int64_t)j0 * ldy;
       double *cj = c + (int64_t)j0 * ldc;
       double *nj = norms2 ? norms2 + j0 : nullptr;
+      auto k = nb == 4 ? gram4_vec_kernel<AT, 4> : nb == 3 ? gram4_vec_kernel<AT, 3>
+             : nb == 2 ? gram4_vec_kernel<AT, 2> : gram4_vec_kernel<AT, 1>;
       if (g_tune[1] != 2) {  // 2: column groups outermost (the slower order)
-        SVDSB_LAUNCH_PDL(gram4_vec_kernel<AT>, dim3(grid.x * ny, 1, 1), kThreads, 0, st, dim, s, yj, ldy, cj, ldc, nj,
-                         ctx->partials, take_ticket(ctx), ny, nb);
+        SVDSB_LAUNCH_PDL(k, dim3(grid.x * ny, 1, 1), kThreads, 0, st, dim, s, yj, ldy, cj, ldc, nj, ctx->partials,
+                         take_ticket(ctx), ny);
       } else {
-        SVDSB_LAUNCH_PDL(gram4_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, yj, ldy, cj, ldc, nj, ctx->partials,
-                         take_ticket(ctx), 0, nb);
+        SVDSB_LAUNCH_PDL(k, grid, kThreads, 0, st, dim, s, yj, ldy, cj, ldc, nj, ctx->partials, take_ticket(ctx), 0);
       }
     }
     return SVDSB_OK;
