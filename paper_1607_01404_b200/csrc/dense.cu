@@ -269,7 +269,7 @@ ritz_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const double
 #pragma unroll
     for (int j = 0; j < PT; ++j) {
       if (j < np) {
-        double res = aw[j] - ax[j] * lsh[j];
+        double res = __dsub_rn(aw[j], __dmul_rn(ax[j], lsh[j]));  // R = OpX - X*lam, two roundings (no fma), eigensolver.py:392
         r[row + (int64_t)(j0 + j) * ldr] = res;
         if (xo) xo[row + (int64_t)(j0 + j) * ldx] = ax[j];
         if (oxo) oxo[row + (int64_t)(j0 + j) * ldox] = aw[j];
@@ -871,7 +871,7 @@ ritz_wide_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const d
 #pragma unroll
     for (int j = 0; j < PT; ++j) {
       if (j < p) {
-        double res = aw[j] - ax[j] * lsh[j];
+        double res = __dsub_rn(aw[j], __dmul_rn(ax[j], lsh[j]));  // R = OpX - X*lam, two roundings (no fma), eigensolver.py:392
         r[row + (int64_t)j * ldr] = res;
         if (xo) xo[row + (int64_t)j * ldx] = ax[j];
         if (oxo) oxo[row + (int64_t)j * ldox] = aw[j];
@@ -967,7 +967,7 @@ ritz_split_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const 
 #pragma unroll
     for (int j = 0; j < PQ; ++j) {
       if (j0 + j < p) {
-        double res = aw[j] - ax[j] * lsh[j0 + j];
+        double res = __dsub_rn(aw[j], __dmul_rn(ax[j], lsh[j0 + j]));  // as ritz_wide_kernel
         r[row + (int64_t)(j0 + j) * ldr] = res;
         if (xo) xo[row + (int64_t)(j0 + j) * ldx] = ax[j];
         if (oxo) oxo[row + (int64_t)(j0 + j) * ldox] = aw[j];
