@@ -694,6 +694,58 @@ def test_cgs_fused_matches_pass_by_pass(dim, g, precond, rng):
     assert np.abs(q.T @ xf).max() <= 1e-13
 
 
+def test_grid_barrier_and_ticket_reductions_stress(rng):
+    """Race evidence for the synchronisation the kernels build themselves
+    (compute-sanitizer is closed on the GPU pool): the software grid
+    barrier of svdsb_cgs_fused and the last-CTA ticket folds of the Gram /
+    projection / Ritz kernels, 300 times each while a second stream keeps
+    the SMs busy with independent work (so CTA scheduling and completion
+    order vary between repetitions).  Every repetition must give the same
+    bits: a lost update, a stale partial or a barrier passed early shows up
+    as a different result."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    dim, g = 300_000, 33
+    q, _ = np.linalg.qr(rng.standard_normal((dim, g)))
+    V = dv.to_device_block(q)
+    W = dv.to_device_block(rng.standard_normal((dim, g)))
+    R = dv.to_device_block(rng.standard_normal((dim, 3)) + 0.5 * q[:, :1])
+    Y = dv.to_device_block(np.linalg.qr(rng.standard_normal((g, g)))[0])
+    lam = torch.from_numpy(rng.standard_normal(g)).cuda()
+    ci = torch.tensor([1], dtype=torch.int32, device="cuda")
+    n_, ptrs, lds, cols, _ = dv._blk_args([V])
+    noise = torch.randn(1 << 24, device="cuda")
+    side = torch.cuda.Stream()
+    ref = None
+    for rep in range(300):
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                noise.mul_(1.0000001).add_(1e-7)
+        x = dv.new_block(dim, 1)
+        prev = dv.small_matrix(g, 2)
+        st = torch.zeros(8, dtype=torch.float64, device="cuda")
+        _lib.call("svdsb_cgs_fused", ctx.handle, dim, n_, ptrs, lds, cols, dv.P(R), dv.ld_of(R), dv.P(ci), None,
+                  dv.P(x), dv.P(Y), dv.ld_of(Y), g, 2, dv.P(prev), dv.ld_of(prev), 3, dv.P(st), ctx.stream)
+        c = dv.small_matrix(g, 4)
+        nr = torch.zeros(4, dtype=torch.float64, device="cuda")
+        dv.gram(ctx, dim, [V], W[:, :4], c, norms2=nr)
+        y4 = W[:, 4:8].clone()
+        dv.project_out(ctx, dim, [V], c, y4)
+        r = dv.new_block(dim, 12)
+        rn2 = torch.zeros(12, dtype=torch.float64, device="cuda")
+        dv.ritz_residual(ctx, V, W, Y[:, :12], lam[:12], r, rn2=rn2)
+        got = [t.cpu().numpy().copy() for t in (x, st, c, nr, y4, rn2)] + [float(r.sum())]
+        if ref is None:
+            ref = got
+            assert ref[1][0] == 0.0 and ref[1][5] > 0.0
+        else:
+            for a, b in zip(ref[:-1], got[:-1]):
+                assert np.array_equal(a, b), rep
+            assert ref[-1] == got[-1], rep
+    torch.cuda.synchronize()
+
+
 def test_config4_shape_b4_products_at_hbm_scale(rng):
     """Config 4's generator at a fifth of its size (2 M x 200 k, ~35 M nnz,
     every operand larger than L2): the sliced-ELL forward b = 4 product
