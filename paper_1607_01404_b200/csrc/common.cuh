@@ -146,6 +146,9 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // Key 5: transposed b = 4 SpMV (0 length-sorted sliced ELL, 1 CSR tiles).
 // Key 6: 2- and 3-column products of short-row matrices (0 zero-padded to
 // the 4-column kernels, 1 the b-column CSR tile kernels).
+// Key 7: b = 4 sliced ELL (0 TMA-staged ring for the forward product,
+// csr_sell4s_kernel, rows <= 20 nonzeros; 1 the direct-load kernels both
+// ways; 2 the TMA-staged ring both ways, csr_sell4ts_kernel transposed).
 constexpr int kTuneKeys = 8;
 inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0};
 

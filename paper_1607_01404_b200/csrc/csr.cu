@@ -67,6 +67,7 @@ struct CsrPart {
   int64_t *sell_ptr = nullptr;  // nslice + 1
   int *sell_col = nullptr;
   double *sell_val = nullptr;
+  uint8_t *sell_len = nullptr;  // forward copy: row length of each sliced position (0 past the end)
   bool sell_failed = false;     // the copy could not be built: CSR kernels (same bits)
 };
 
@@ -925,16 +926,171 @@ csr_sell4w_kernel(int64_t nrows, int64_t nslice, const int *__restrict__ row_ptr
   pdl_trigger();
 }
 
+// TMA-staged sliced-ELL forward product for b = 4 (rows of at most
+// kSell4sW nonzeros: config 4's A).  One persistent CTA of kS4Warps warps
+// per SM; each warp owns every kS4Warps*gridDim.x-th slice and streams its
+// slices through a private two-stage shared-memory ring filled by
+// cp.async.bulk (values, column ids and the slice's row lengths; L2
+// evict-first), so no lane ever waits on DRAM for its indices: the only
+// latency left in a row is the x gathers, issued eight (plus p0) at a time
+// from indices already on chip.  The fold is row4_fold's order, so the
+// result is bit-identical to the other b = 4 kernels.
+constexpr int kSell4sW = 20;                  // widest slice staged
+constexpr int kS4Warps = 12;                  // warps per CTA (1 CTA / SM)
+constexpr int kS4Stage = 32 * kSell4sW * 12 + 32 + 96;   // vals + cols + lens, padded to 128 B
+static_assert(kS4Stage % 128 == 0, "stage alignment");
+constexpr size_t kS4Smem = (size_t)kS4Warps * 2 * kS4Stage;
+
+__device__ __forceinline__ void s4_fold(const double *__restrict__ sv, const int *__restrict__ sc, int lane, int len,
+                                        const double *__restrict__ x, double (&out)[4]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) out[c] = 0.0;
+  if (len == 0) return;
+  const int n = len - 1;  // tail length
+  double p0[4], xg[8][4];
+  {
+    double g0[4];
+    gather4(x, sc[lane], g0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) gather4(x, sc[(n == 0 ? 0 : 1 + min(u, n - 1)) * 32 + lane], xg[u]);
+    const double v0 = sv[lane];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) p0[c] = dmul(v0, g0[c]);
+  }
+  if (n < 8) {
+    double r[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int u = 0; u < 7; ++u)
+      if (u < n) {
+        const double vu = sv[(1 + u) * 32 + lane];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) r[c] = dadd(r[c], dmul(vu, xg[u][c]));
+      }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) out[c] = n == 0 ? p0[c] : dadd(p0[c], r[c]);
+    return;
+  }
+  double acc[4][8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double vu = sv[(1 + u) * 32 + lane];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[c][u] = dmul(vu, xg[u][c]);
+  }
+  const int nb = n - (n % 8);
+  for (int b0 = 8; b0 < nb; b0 += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) gather4(x, sc[(1 + b0 + u) * 32 + lane], xg[u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double vu = sv[(1 + b0 + u) * 32 + lane];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c][u] = dadd(acc[c][u], dmul(vu, xg[u][c]));
+    }
+  }
+  double res[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double *a = acc[c];
+    res[c] = dadd(dadd(dadd(a[0], a[1]), dadd(a[2], a[3])), dadd(dadd(a[4], a[5]), dadd(a[6], a[7])));
+  }
+  if (nb < n) {
+#pragma unroll
+    for (int u = 0; u < 7; ++u) gather4(x, sc[(1 + nb + min(u, n - nb - 1)) * 32 + lane], xg[u]);
+#pragma unroll
+    for (int u = 0; u < 7; ++u)
+      if (nb + u < n) {
+        const double vu = sv[(1 + nb + u) * 32 + lane];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) res[c] = dadd(res[c], dmul(vu, xg[u][c]));
+      }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) out[c] = dadd(p0[c], res[c]);
+}
+
+template <int YROW>
+__global__ void __launch_bounds__(kS4Warps * 32, 1)
+csr_sell4s_kernel(int64_t nrows, int64_t nslice, const int64_t *__restrict__ sell_ptr, const int *__restrict__ scol,
+                  const double *__restrict__ sval, const uint8_t *__restrict__ slen, const double *__restrict__ x,
+                  double *__restrict__ y, int64_t ldy) {
+  extern __shared__ __align__(128) unsigned char s4_smem[];
+  __shared__ __align__(8) uint64_t bar[kS4Warps][2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned char *ring = s4_smem + (size_t)w * 2 * kS4Stage;
+  const int64_t gw = (int64_t)blockIdx.x * kS4Warps + w, nw = (int64_t)gridDim.x * kS4Warps;
+  if (lane == 0) {
+    mbar_init(&bar[w][0], 1);
+    mbar_init(&bar[w][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint64_t policy = 0;
+  if (lane == 0) policy = evict_first_policy();
+  // lane 0: slice sl (entries [e0, e1)) into stage k (values, column ids,
+  // lengths; one mbarrier).  The slice pointers are loaded one issue ahead
+  // so lane 0 never stalls the warp on them.
+  auto issue = [&](int64_t sl, int k, int64_t e0, int64_t e1) {
+    const int wd = (int)((e1 - e0) >> 5);
+    unsigned char *st = ring + (size_t)k * kS4Stage;
+    mbar_expect_tx(&bar[w][k], 32u * wd * 12u + 32u);
+    if (wd > 0) {
+      bulk_g2s(st, sval + e0, 256u * wd, &bar[w][k], policy);
+      bulk_g2s(st + 32 * kSell4sW * 8, scol + e0, 128u * wd, &bar[w][k], policy);
+    }
+    bulk_g2s(st + 32 * kSell4sW * 12, slen + 32 * sl, 32u, &bar[w][k], policy);
+  };
+  // the matrix is immutable: start streaming before the producer of x ends
+  int64_t pe0 = 0, pe1 = 0;   // pointers of slice gw + 2 nw (the next to issue)
+  if (lane == 0) {
+    if (gw < nslice) issue(gw, 0, __ldg(sell_ptr + gw), __ldg(sell_ptr + gw + 1));
+    if (gw + nw < nslice) issue(gw + nw, 1, __ldg(sell_ptr + gw + nw), __ldg(sell_ptr + gw + nw + 1));
+    if (gw + 2 * nw < nslice) {
+      pe0 = __ldg(sell_ptr + gw + 2 * nw);
+      pe1 = __ldg(sell_ptr + gw + 2 * nw + 1);
+    }
+  }
+  pdl_wait();
+  int k = 0;
+  unsigned phase = 0;
+  for (int64_t sl = gw; sl < nslice; sl += nw) {
+    mbar_wait(&bar[w][k], phase);
+    const unsigned char *st = ring + (size_t)k * kS4Stage;
+    const double *sv = reinterpret_cast<const double *>(st);
+    const int *sc = reinterpret_cast<const int *>(st + 32 * kSell4sW * 8);
+    const int len = st[32 * kSell4sW * 12 + lane];
+    const int64_t row = (sl << 5) + lane;
+    double out[4];
+    s4_fold(sv, sc, lane, len, x, out);
+    if (row < nrows) store_row4<YROW>(y, ldy, row, out);
+    __syncwarp();
+    if (lane == 0 && sl + 2 * nw < nslice) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(sl + 2 * nw, k, pe0, pe1);
+      if (sl + 3 * nw < nslice) {
+        pe0 = __ldg(sell_ptr + sl + 3 * nw);
+        pe1 = __ldg(sell_ptr + sl + 3 * nw + 1);
+      }
+    }
+    if (++k == 2) {
+      k = 0;
+      phase ^= 1u;
+    }
+  }
+  pdl_trigger();
+}
+
 __global__ void sell_fill_kernel(int64_t nrows, const int *__restrict__ perm, const int *__restrict__ row_ptr,
                                  const int *__restrict__ col, const double *__restrict__ val,
                                  const int64_t *__restrict__ sell_ptr, int *__restrict__ scol,
-                                 double *__restrict__ sval) {
+                                 double *__restrict__ sval, uint8_t *__restrict__ slen) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= nrows) return;
   const int64_t row = perm ? perm[q] : q;
   const int64_t sl = q >> 5;
   const int t = (int)(q & 31);
   const int k0 = row_ptr[row], k1 = row_ptr[row + 1];
+  if (slen) slen[q] = (uint8_t)min(k1 - k0, 255);
   const int64_t base = sell_ptr[sl] + t;
   const int w = (int)((sell_ptr[sl + 1] - sell_ptr[sl]) >> 5);
   for (int j = 0; j < w; ++j) {
@@ -1034,6 +1190,133 @@ csr_sell4t_kernel(int64_t nq, int64_t nslice, const int *__restrict__ perm, cons
         }
     }
     store_row4<YROW>(y, ldy, row, s);
+  }
+  pdl_trigger();
+}
+
+
+// TMA-staged transposed b = 4 product on the length-sorted sliced-ELL copy
+// (rows of at most kSellTMax nonzeros; the mid rows stay on
+// csr_sell4t_kernel, long rows on the chunk path).  As csr_sell4s_kernel:
+// one persistent CTA of kS4Warps warps per SM, each warp streaming its
+// slices through a private ring of kT4Stages stages, each stage one chunk
+// of up to kT4Chunk columns of a slice (values, column ids; the slice's
+// row permutation and lengths ride with its first chunk), filled by
+// cp.async.bulk kT4Stages chunks ahead.  A lane sums its row left to right
+// with no FMA, continuing from y when accumulating: np.add.at's order,
+// bit-identical to csr_sell4t_kernel.
+constexpr int kT4Chunk = 8;
+constexpr int kT4Stages = 4;
+constexpr int kT4Stage = 32 * kT4Chunk * 12 + 128 + 32 + 96;
+static_assert(kT4Stage % 128 == 0, "stage alignment");
+constexpr size_t kT4Smem = (size_t)kS4Warps * kT4Stages * kT4Stage;
+
+template <int YROW>
+__global__ void __launch_bounds__(kS4Warps * 32, 1)
+csr_sell4ts_kernel(int64_t nq, int64_t nslice, const int *__restrict__ perm, const uint8_t *__restrict__ slen,
+                   const int64_t *__restrict__ sell_ptr, const int *__restrict__ scol,
+                   const double *__restrict__ sval, const double *__restrict__ x, double *__restrict__ y,
+                   int64_t ldy, int acc) {
+  extern __shared__ __align__(128) unsigned char t4_smem[];
+  __shared__ __align__(8) uint64_t bar[kS4Warps][kT4Stages];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned char *ring = t4_smem + (size_t)w * kT4Stages * kT4Stage;
+  const int64_t gw = (int64_t)blockIdx.x * kS4Warps + w, nw = (int64_t)gridDim.x * kS4Warps;
+  if (lane == 0) {
+    for (int k = 0; k < kT4Stages; ++k) mbar_init(&bar[w][k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // producer cursor (lane 0): chunk pj0 of slice psl (width pw, first entry sp0)
+  // (nsp0, nsp1: pointers of slice psl + nw, loaded one slice ahead)
+  uint64_t policy = 0;
+  int64_t psl = gw, sp0 = 0, nsp0 = 0, nsp1 = 0;
+  int pw = 0, pj0 = 0;
+  if (lane == 0) {
+    policy = evict_first_policy();
+    if (psl < nslice) {
+      sp0 = __ldg(sell_ptr + psl);
+      pw = (int)((__ldg(sell_ptr + psl + 1) - sp0) >> 5);
+    }
+    if (psl + nw < nslice) {
+      nsp0 = __ldg(sell_ptr + psl + nw);
+      nsp1 = __ldg(sell_ptr + psl + nw + 1);
+    }
+  }
+  auto issue_next = [&](int k) {
+    if (psl >= nslice) return;
+    unsigned char *st = ring + (size_t)k * kT4Stage;
+    const int cw = max(0, min(kT4Chunk, pw - pj0));
+    mbar_expect_tx(&bar[w][k], 384u * cw + (pj0 == 0 ? 160u : 0u));
+    if (cw > 0) {
+      bulk_g2s(st, sval + sp0 + 32 * pj0, 256u * cw, &bar[w][k], policy);
+      bulk_g2s(st + 32 * kT4Chunk * 8, scol + sp0 + 32 * pj0, 128u * cw, &bar[w][k], policy);
+    }
+    if (pj0 == 0) {
+      bulk_g2s(st + 32 * kT4Chunk * 12, perm + 32 * psl, 128u, &bar[w][k], policy);
+      bulk_g2s(st + 32 * kT4Chunk * 12 + 128, slen + 32 * psl, 32u, &bar[w][k], policy);
+    }
+    pj0 += kT4Chunk;
+    if (pj0 >= pw) {
+      pj0 = 0;
+      psl += nw;
+      sp0 = nsp0;
+      pw = (int)((nsp1 - nsp0) >> 5);
+      if (psl + nw < nslice) {
+        nsp0 = __ldg(sell_ptr + psl + nw);
+        nsp1 = __ldg(sell_ptr + psl + nw + 1);
+      }
+    }
+  };
+  if (lane == 0)
+    for (int k = 0; k < kT4Stages; ++k) issue_next(k);
+  pdl_wait();
+  int k = 0;
+  unsigned phase = 0;
+  for (int64_t sl = gw; sl < nslice; sl += nw) {
+    const int64_t q = (sl << 5) + lane;
+    int64_t row = 0;
+    int len = 0, wd = 0;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j0 = 0;; j0 += kT4Chunk) {
+      mbar_wait(&bar[w][k], phase);
+      const unsigned char *st = ring + (size_t)k * kT4Stage;
+      if (j0 == 0) {
+        row = reinterpret_cast<const int *>(st + 32 * kT4Chunk * 12)[lane];
+        len = st[32 * kT4Chunk * 12 + 128 + lane];
+        wd = __shfl_sync(0xffffffffu, len, 0);   // lane 0 holds the slice's longest row
+        if (acc && q < nq) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) s[c] = YROW ? y[row * 4 + c] : y[row + c * ldy];
+        }
+      }
+      const double *sv = reinterpret_cast<const double *>(st);
+      const int *sc = reinterpret_cast<const int *>(st + 32 * kT4Chunk * 8);
+      const int jl = min(len, j0 + kT4Chunk);
+      if (j0 < jl) {
+        double xv[kT4Chunk][4];
+#pragma unroll
+        for (int u = 0; u < kT4Chunk; ++u) gather4(x, sc[(min(j0 + u, jl - 1) - j0) * 32 + lane], xv[u]);
+#pragma unroll
+        for (int u = 0; u < kT4Chunk; ++u)
+          if (j0 + u < jl) {
+            const double v = sv[u * 32 + lane];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) s[c] = dadd(s[c], dmul(v, xv[u][c]));
+          }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_next(k);
+      }
+      if (++k == kT4Stages) {
+        k = 0;
+        phase ^= 1u;
+      }
+      if (j0 + kT4Chunk >= wd) break;
+    }
+    if (q < nq) store_row4<YROW>(y, ldy, row, s);
   }
   pdl_trigger();
 }
@@ -1462,6 +1745,7 @@ static void free_part(CsrPart &p) {
   pfree(p.mid_rows, nullptr);
   pfree(p.sell_col, nullptr);
   pfree(p.sell_val, nullptr);
+  pfree(p.sell_len, nullptr);
   p = CsrPart();
 }
 
@@ -1519,23 +1803,33 @@ static int build_sell(CsrPart &p, cudaStream_t st, bool sorted = false) {
   int *dperm = nullptr;
   int rc;
   if ((rc = upload(&dsp, sp, st))) return rc;
-  if (sorted && (rc = upload(&dperm, order, st))) {
+  std::vector<int> perm_pad;
+  if (sorted) {
+    perm_pad = order;
+    perm_pad.resize(32 * ns, 0);  // whole slices: the staged kernel copies 32 entries per slice
+  }
+  if (sorted && (rc = upload(&dperm, perm_pad, st))) {
     pfree(dsp, st);
     return rc;
   }
   int *scol = nullptr;
   double *sval = nullptr;
+  uint8_t *slen = nullptr;
   if (alloc_pad(&scol, std::max<int64_t>(sp[ns], 1), st) != cudaSuccess ||
-      alloc_pad(&sval, std::max<int64_t>(sp[ns], 1), st) != cudaSuccess) {
+      alloc_pad(&sval, std::max<int64_t>(sp[ns], 1), st) != cudaSuccess ||
+      alloc_pad(&slen, std::max<int64_t>(32 * ns, 32), st) != cudaSuccess ||
+      cudaMemsetAsync(slen, 0, std::max<int64_t>(32 * ns, 32), st) != cudaSuccess) {
     pfree(dsp, st);
     pfree(dperm, st);
     pfree(scol, st);
+    pfree(sval, st);
+    pfree(slen, st);
     set_error("sliced-ELL allocation failed");
     return SVDSB_ERR_ALLOC;
   }
   if (nq > 0) {
     sell_fill_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(nq, dperm, p.row_ptr, p.col, p.val, dsp, scol,
-                                                                   sval);
+                                                                   sval, slen);
     SVDSB_LAUNCHED();
   }
   p.nslice = ns;
@@ -1544,6 +1838,7 @@ static int build_sell(CsrPart &p, cudaStream_t st, bool sorted = false) {
   p.sell_ptr = dsp;
   p.sell_col = scol;
   p.sell_val = sval;
+  p.sell_len = slen;
   return SVDSB_OK;
 }
 
@@ -1653,6 +1948,19 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
                          y, ldy);
         return SVDSB_OK;
       }
+      if (p.sell_val && p.sell_len && p.maxlen <= kSell4sW && g_tune[7] != 1) {
+        auto k = yrow ? csr_sell4s_kernel<1> : csr_sell4s_kernel<0>;
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(csr_sell4s_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kS4Smem);
+          cudaFuncSetAttribute(csr_sell4s_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kS4Smem);
+          attr = true;
+        }
+        const int g = (int)std::min<int64_t>(num_sms(), (p.nslice + kS4Warps - 1) / kS4Warps);
+        SVDSB_LAUNCH_PDL(k, g, kS4Warps * 32, kS4Smem, st, p.rows, p.nslice, p.sell_ptr, p.sell_col, p.sell_val,
+                         p.sell_len, x, y, ldy);
+        return SVDSB_OK;
+      }
       if (p.sell_val && !p.sell_perm) {
         auto k = yrow ? csr_sell4_kernel<1> : csr_sell4_kernel<0>;
         const int g = (int)std::min<int64_t>((p.nslice + 7) / 8, pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
@@ -1690,7 +1998,27 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
       // rows up to a tile on a length-sorted sliced-ELL copy (built on the
       // first uncaptured call); long rows below on the chunk path
       ensure_sell(p, st, true);
-      if (p.sell_val && p.sell_perm) {
+      if (p.sell_val && p.sell_perm && p.sell_len && g_tune[7] == 2) {
+        if (p.nmid > 0) {  // mid rows: one warp per row (csr_sell4t_kernel with no slices)
+          auto k = yrow ? csr_sell4t_kernel<1> : csr_sell4t_kernel<0>;
+          const int g = (int)std::min<int64_t>((p.nmid + 7) / 8, pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
+          SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.nsell, (int64_t)0, p.sell_perm, p.row_ptr, p.sell_ptr,
+                           p.sell_col, p.sell_val, p.nmid, p.mid_rows, p.col, p.val, x, y, ldy, acc);
+        }
+        if (p.nslice > 0) {
+          auto k = yrow ? csr_sell4ts_kernel<1> : csr_sell4ts_kernel<0>;
+          static bool attr = false;
+          if (!attr) {
+            cudaFuncSetAttribute(csr_sell4ts_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT4Smem);
+            cudaFuncSetAttribute(csr_sell4ts_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT4Smem);
+            attr = true;
+          }
+          const int g = (int)std::min<int64_t>(num_sms(), (p.nslice + kS4Warps - 1) / kS4Warps);
+          SVDSB_LAUNCH_PDL(k, g, kS4Warps * 32, kT4Smem, st, p.nsell, p.nslice, p.sell_perm, p.sell_len, p.sell_ptr,
+                           p.sell_col, p.sell_val, x, y, ldy, acc);
+        }
+        short_done = true;
+      } else if (p.sell_val && p.sell_perm) {
         if (p.nslice + p.nmid > 0) {
           auto k = yrow ? csr_sell4t_kernel<1> : csr_sell4t_kernel<0>;
           const int g = (int)std::min<int64_t>((p.nslice + p.nmid + 7) / 8,

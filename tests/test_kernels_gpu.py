@@ -203,6 +203,78 @@ def test_spmv_transpose_b4_variants(variant, rng):
     assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
 
 
+@pytest.mark.parametrize("m", [1, 31, 33, 70_001])
+def test_spmv_forward_b4_tma_ring_bit_exact(m, rng):
+    """The TMA-staged sliced-ELL forward b = 4 kernel (rows <= 20 nonzeros,
+    svdsb_tune_set key 7 = 0) against the direct-load sliced-ELL kernel
+    (key 7 = 1) and the oracle, bit for bit: ragged rows of 0..20 nonzeros
+    (every tail length below, at and above numpy's 8-term block), empty
+    rows, slices of width 1, row counts around the 32-row slice, and enough
+    slices per warp to wrap the two-stage ring many times."""
+    from paper_1607_01404_b200 import _lib
+    n = 5000
+    lens = rng.integers(0, 21, m)
+    lens[rng.random(m) < 0.05] = 0
+    if m >= 64:
+        lens[32:64] = rng.integers(0, 2, 32)        # a slice of width <= 1
+    rows = np.repeat(np.arange(m), lens)
+    cols = rng.integers(0, n, rows.size)
+    vals = rng.standard_normal(rows.size) * 10.0 ** rng.uniform(-3, 3, rows.size)
+    a, (rp, ci, va) = _csr(m, n, rows, cols, vals)
+    assert np.diff(rp).max() <= 20
+    x = rng.standard_normal((n, 4)) * 10.0 ** rng.uniform(-3, 3, (n, 4))
+    want = ocsr.spmv(m, n, rp, ci, va, x)
+    got = {}
+    for key in (0, 1):
+        try:
+            _lib.call("svdsb_tune_set", 7, key)
+            got[key] = _spmv_dev(a, x, False)
+        finally:
+            _lib.call("svdsb_tune_set", 7, 0)
+    assert np.array_equal(got[0], want)
+    assert np.array_equal(got[1], want)
+
+
+@pytest.mark.parametrize("variant", [0, 2])
+def test_spmv_transpose_b4_tma_ring(variant, rng):
+    """The TMA-staged transposed b = 4 kernel (svdsb_tune_set key 7 = 2:
+    length-sorted slices streamed in 8-column chunks, mid rows one warp per
+    row) against the direct-load kernel and the oracle: bit-exact up to a
+    tile, chunked rows within rounding, empty rows zero; both with a fresh
+    output and accumulating over the column blocks of a tall matrix."""
+    import os
+    from paper_1607_01404_b200 import _lib
+    m, n = 9000, 700
+    cols = np.concatenate([rng.integers(0, n, 20000), rng.integers(0, 40, 15000),
+                           np.full(2600, 650), np.full(3000, 651)])
+    cols[cols == 699] = 698
+    rows = rng.integers(0, m, cols.size)
+    vals = rng.standard_normal(cols.size) * 10.0 ** rng.uniform(-3, 3, cols.size)
+    y = rng.standard_normal((m, 4))
+    want = ocsr.spmv(m, n, *ocsr.csr_from_coo(m, n, rows, cols, vals), y, transpose=True)
+    old = os.environ.get("SVDSB_T_BLOCK_ROWS")
+    got = {}
+    try:
+        for blocked in (False, True):
+            if blocked:
+                os.environ["SVDSB_T_BLOCK_ROWS"] = "2500"     # 4 column blocks: accumulating path
+            a, (rp, ci, va) = _csr(m, n, rows, cols, vals)
+            _lib.call("svdsb_tune_set", 7, variant)
+            got[blocked] = _spmv_dev(a, y, True)
+            _lib.call("svdsb_tune_set", 7, 0)
+    finally:
+        _lib.call("svdsb_tune_set", 7, 0)
+        if old is None:
+            os.environ.pop("SVDSB_T_BLOCK_ROWS", None)
+        else:
+            os.environ["SVDSB_T_BLOCK_ROWS"] = old
+    lens = np.diff(ocsr.csr_transpose(m, n, rp, ci, va)[0])
+    ok = lens <= 2048
+    for g in got.values():
+        assert np.array_equal(g[ok], want[ok])
+        assert np.abs(g - want).max() <= 1e-12 * np.abs(want).max()
+
+
 @pytest.mark.parametrize("b", [2, 3])
 def test_spmv_b23_padded_to_b4(b, rng):
     """2- and 3-column products of short-row matrices run the 4-column
