@@ -40,7 +40,7 @@ def up_to_date():
     return all(os.path.getmtime(f) <= t for f in _inputs())
 
 
-def build(force=False, verbose=False, variant=None, overrides=None):
+def build(force=False, verbose=False, variant=None, overrides=None, defines=()):
     """Compile every .cu to an object, then link the shared library.
 
     variant / overrides (kernel experiments only): link
@@ -57,7 +57,7 @@ def build(force=False, verbose=False, variant=None, overrides=None):
     for src in SOURCES:
         obj = os.path.join(odir, os.path.splitext(src)[0] + ".o")
         path = overrides.get(src, os.path.join(CSRC, src))
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(REPO, "include"), "-I", CSRC,
+        cmd = [NVCC, *ARCH, *FLAGS, *["-D" + d for d in defines], "-I", os.path.join(REPO, "include"), "-I", CSRC,
                "-c", path, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
@@ -80,9 +80,10 @@ def main():
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--variant", default=None)
     ap.add_argument("--override", action="append", default=[], metavar="SRC=PATH")
+    ap.add_argument("--define", action="append", default=[], metavar="NAME=VALUE")
     args = ap.parse_args()
     ov = dict(o.split("=", 1) for o in args.override)
-    print(build(force=args.force, verbose=args.verbose, variant=args.variant, overrides=ov))
+    print(build(force=args.force, verbose=args.verbose, variant=args.variant, overrides=ov, defines=args.define))
 
 
 if __name__ == "__main__":

@@ -142,7 +142,8 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // Key 3: Ritz residual (0: two threads per row for 16 < p <= 32, one
 // otherwise; 1: always one; 2: two also for 8 < p <= 16).
 // Key 4: native GD+k iteration (0 H-column / status epilogues, 1 separate
-// h_insert and status_pack launches).
+// h_insert and status_pack launches); 2 also selects the generic 32-column
+// in-place restart product instead of ts_gemm_inplace_vec_kernel.
 // Key 5: transposed b = 4 SpMV (0 length-sorted sliced ELL, 1 CSR tiles).
 // Key 6: 2- and 3-column products of short-row matrices (0 zero-padded to
 // the 4-column kernels, 1 the b-column CSR tile kernels).

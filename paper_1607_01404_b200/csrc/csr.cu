@@ -1205,23 +1205,30 @@ csr_sell4t_kernel(int64_t nq, int64_t nslice, const int *__restrict__ perm, cons
 // cp.async.bulk kT4Stages chunks ahead.  A lane sums its row left to right
 // with no FMA, continuing from y when accumulating: np.add.at's order,
 // bit-identical to csr_sell4t_kernel.
+#ifndef SVDSB_T4_WARPS
+#define SVDSB_T4_WARPS 12
+#endif
+#ifndef SVDSB_T4_STAGES
+#define SVDSB_T4_STAGES 4
+#endif
 constexpr int kT4Chunk = 8;
-constexpr int kT4Stages = 4;
+constexpr int kT4Stages = SVDSB_T4_STAGES;
+constexpr int kT4Warps = SVDSB_T4_WARPS;
 constexpr int kT4Stage = 32 * kT4Chunk * 12 + 128 + 32 + 96;
 static_assert(kT4Stage % 128 == 0, "stage alignment");
-constexpr size_t kT4Smem = (size_t)kS4Warps * kT4Stages * kT4Stage;
+constexpr size_t kT4Smem = (size_t)kT4Warps * kT4Stages * kT4Stage;
 
 template <int YROW>
-__global__ void __launch_bounds__(kS4Warps * 32, 1)
+__global__ void __launch_bounds__(kT4Warps * 32, 1)
 csr_sell4ts_kernel(int64_t nq, int64_t nslice, const int *__restrict__ perm, const uint8_t *__restrict__ slen,
                    const int64_t *__restrict__ sell_ptr, const int *__restrict__ scol,
                    const double *__restrict__ sval, const double *__restrict__ x, double *__restrict__ y,
                    int64_t ldy, int acc) {
   extern __shared__ __align__(128) unsigned char t4_smem[];
-  __shared__ __align__(8) uint64_t bar[kS4Warps][kT4Stages];
+  __shared__ __align__(8) uint64_t bar[kT4Warps][kT4Stages];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   unsigned char *ring = t4_smem + (size_t)w * kT4Stages * kT4Stage;
-  const int64_t gw = (int64_t)blockIdx.x * kS4Warps + w, nw = (int64_t)gridDim.x * kS4Warps;
+  const int64_t gw = (int64_t)blockIdx.x * kT4Warps + w, nw = (int64_t)gridDim.x * kT4Warps;
   if (lane == 0) {
     for (int k = 0; k < kT4Stages; ++k) mbar_init(&bar[w][k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -2013,8 +2020,8 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
             cudaFuncSetAttribute(csr_sell4ts_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT4Smem);
             attr = true;
           }
-          const int g = (int)std::min<int64_t>(num_sms(), (p.nslice + kS4Warps - 1) / kS4Warps);
-          SVDSB_LAUNCH_PDL(k, g, kS4Warps * 32, kT4Smem, st, p.nsell, p.nslice, p.sell_perm, p.sell_len, p.sell_ptr,
+          const int g = (int)std::min<int64_t>(num_sms(), (p.nslice + kT4Warps - 1) / kT4Warps);
+          SVDSB_LAUNCH_PDL(k, g, kT4Warps * 32, kT4Smem, st, p.nsell, p.nslice, p.sell_perm, p.sell_len, p.sell_ptr,
                            p.sell_col, p.sell_val, x, y, ldy, acc);
         }
         short_done = true;
@@ -2289,7 +2296,7 @@ int svdsb_csr_destroy(svdsb_csr *a) {
   free_part(a->a);
   free_part(a->at);
   for (auto &p : a->atb) free_part(p);
-  for (double *sp : a->scratch) cudaFree(sp);
+  for (double *sp : a->scratch) pfree(sp, nullptr);  // pool memory: cheap to return
   delete a;
   return SVDSB_OK;
 }
@@ -2620,10 +2627,14 @@ int svdsb_csr_device_arrays(const svdsb_csr *a, int transpose, const int **row_p
 static double *scratch_get(const svdsb_csr *ca, int slot, size_t n) {
   svdsb_csr *a = const_cast<svdsb_csr *>(ca);
   if (a->scratch_cap[slot] < n) {
-    cudaFree(a->scratch[slot]);
+    // stream-ordered pool memory (legacy stream: the handle may be used on
+    // any stream after this call returns; the matrix destructor synchronises)
+    if (a->scratch[slot]) cudaDeviceSynchronize();
+    pfree(a->scratch[slot], nullptr);
     a->scratch[slot] = nullptr;
     a->scratch_cap[slot] = 0;
-    if (cudaMalloc(&a->scratch[slot], n * sizeof(double)) != cudaSuccess) return nullptr;
+    if (palloc(&a->scratch[slot], n * sizeof(double), nullptr) != cudaSuccess) return nullptr;
+    cudaStreamSynchronize(nullptr);
     a->scratch_cap[slot] = n;
   }
   return a->scratch[slot];

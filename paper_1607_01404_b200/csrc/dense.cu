@@ -1101,6 +1101,67 @@ ts_gemm_inplace_kernel(int64_t dim, double *x, int64_t ldx, int g, const double 
 }
 
 
+// In-place V <- V C for 16-byte aligned bases with even leading dimension:
+// two rows per thread with 16-byte loads, basis columns in groups of eight
+// whose loads precede their FMAs, and only ST >= s accumulators (the
+// generic kernel above always carries 32).  Per element the same fma chain
+// over i = 0..g-1 as ts_gemm_inplace_kernel, so the bits are identical.
+template <int ST>
+__global__ void __launch_bounds__(kThreads)
+ts_gemm_inplace_vec_kernel(int64_t dim, double *x, int64_t ldx, int g, const double *__restrict__ cmat,
+                           int64_t ldc, int s) {
+  extern __shared__ double csh[];  // g x ST
+  for (int k = threadIdx.x; k < g * ST; k += kThreads) {
+    int i = k / ST, j = k % ST;
+    csh[k] = (j < s) ? cmat[i + (int64_t)j * ldc] : 0.0;
+  }
+  __syncthreads();
+  constexpr int GU = ST <= 16 ? 8 : 4;   // basis columns loaded per group
+  RowRange rr = cta_rows_even(dim);
+  int64_t r = rr.r0 + 2 * threadIdx.x;
+  for (; r + 1 < rr.r1; r += 2 * kThreads) {
+    double2 acc[ST];
+#pragma unroll
+    for (int j = 0; j < ST; ++j) acc[j] = make_double2(0.0, 0.0);
+    for (int i0 = 0; i0 < g; i0 += GU) {
+      double2 xv[GU];
+#pragma unroll
+      for (int u = 0; u < GU; ++u)   // coherent loads: x is rewritten in place by this kernel
+        xv[u] = *reinterpret_cast<const double2 *>(x + r + (int64_t)min(i0 + u, g - 1) * ldx);
+#pragma unroll
+      for (int u = 0; u < GU; ++u) {
+        if (i0 + u < g) {
+          const double2 *crow = reinterpret_cast<const double2 *>(csh + (i0 + u) * ST);
+#pragma unroll
+          for (int j = 0; j < ST / 2; ++j) {
+            const double2 cf = crow[j];
+            acc[2 * j].x = fma(xv[u].x, cf.x, acc[2 * j].x);
+            acc[2 * j].y = fma(xv[u].y, cf.x, acc[2 * j].y);
+            acc[2 * j + 1].x = fma(xv[u].x, cf.y, acc[2 * j + 1].x);
+            acc[2 * j + 1].y = fma(xv[u].y, cf.y, acc[2 * j + 1].y);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < ST; ++j)
+      if (j < s) *reinterpret_cast<double2 *>(x + r + (int64_t)j * ldx) = acc[j];
+  }
+  if (r < rr.r1) {  // odd tail row
+    double acc[ST];
+#pragma unroll
+    for (int j = 0; j < ST; ++j) acc[j] = 0.0;
+    for (int i = 0; i < g; ++i) {
+      const double xv = x[r + (int64_t)i * ldx];
+#pragma unroll
+      for (int j = 0; j < ST; ++j) acc[j] = fma(xv, csh[i * ST + j], acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < ST; ++j)
+      if (j < s) x[r + (int64_t)j * ldx] = acc[j];
+  }
+}
+
 // ------------------------------------------------ fused single-column CGS
 // The whole orthonormalisation of one expansion vector in ONE launch, for a
 // basis of <= 40 columns: select the residual column by the device index and
@@ -1417,6 +1478,23 @@ int svdsb_ts_gemm(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx, int
   if (x == y) {
     SVDSB_CHECK_ARG(ldx == ldy && s <= g && s <= 32 && alpha == 1.0 && beta == 0.0,
                     "svdsb_ts_gemm: in-place needs ldy == ldx, s <= min(g, 32), alpha 1, beta 0");
+    if (aligned16(y) && !(ldy & 1) && g_tune[4] != 2) {
+      auto k = s <= 8 ? ts_gemm_inplace_vec_kernel<8> : s <= 16 ? ts_gemm_inplace_vec_kernel<16>
+             : s <= 24 ? ts_gemm_inplace_vec_kernel<24> : ts_gemm_inplace_vec_kernel<32>;
+      const int st_cols = s <= 8 ? 8 : s <= 16 ? 16 : s <= 24 ? 24 : 32;
+      const size_t shv = sizeof(double) * g * st_cols;
+      static bool attrv = false;
+      if (!attrv) {
+        for (auto kk : {ts_gemm_inplace_vec_kernel<8>, ts_gemm_inplace_vec_kernel<16>,
+                        ts_gemm_inplace_vec_kernel<24>, ts_gemm_inplace_vec_kernel<32>})
+          SVDSB_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(sizeof(double) * 256 * 32)));
+        attrv = true;
+      }
+      k<<<grid_for(k, dim, shv), kThreads, shv, st>>>(dim, y, ldy, g, c, ldc, s);
+      SVDSB_LAUNCHED();
+      return SVDSB_OK;
+    }
     size_t sh = sizeof(double) * g * 32;
     static bool attr = false;
     if (!attr) {

@@ -139,9 +139,72 @@ def to_device_block(x, device=None):
 
 def to_host(t):
     """Device block -> F-ordered numpy array (the reference's result
-    layout, hybrid.py:603-605)."""
-    a = t.detach().to("cpu").numpy()
-    return np.asfortranarray(a)
+    layout, hybrid.py:603-605).  A column-major block (strides (1, ld)) is
+    packed to (cols, rows) on the device and read back with one contiguous
+    copy, whose transpose is the F-ordered result -- no host-side transpose
+    (config 4's 10 M x 20 U: 0.8 s -> ~0.1 s)."""
+    t = t.detach()
+    if t.dim() == 2 and t.stride(0) == 1 and t.shape[0] > 1 and t.is_cuda:
+        rows, cols = t.shape
+        packed = t.t().contiguous()                     # (cols, rows): F order of the result
+        out = np.empty((rows, cols), dtype=np.float64, order="F")
+        if packed.numel() * 8 < (8 << 20):
+            out.T[...] = packed.cpu().numpy()
+            return out
+        _read_back(packed.view(-1), out.T.reshape(-1))
+        return out
+    return np.asfortranarray(t.cpu().numpy())
+
+
+_STAGE = {}
+_COPY_THREADS = 8
+
+
+def _read_back(src, dst):
+    """Device vector -> host numpy vector through a cached pinned staging
+    buffer: chunks of 64 MB alternate between two pinned slots, each copied
+    to the destination by host threads while the next chunk's device->host
+    copy runs (a pageable copy of config 4's U ran at ~2 GB/s)."""
+    from concurrent.futures import ThreadPoolExecutor
+    chunk = 8 << 20                                     # doubles per chunk (64 MB)
+    st = _STAGE.get(src.device)
+    if st is None:
+        slots = [torch.empty(chunk, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        st = _STAGE[src.device] = {"slots": slots, "events": [torch.cuda.Event(), torch.cuda.Event()],
+                                   "pool": ThreadPoolExecutor(_COPY_THREADS), "stream": torch.cuda.Stream(src.device)}
+    slots, events, pool, stream = st["slots"], st["events"], st["pool"], st["stream"]
+    n = src.numel()
+    stream.wait_stream(torch.cuda.current_stream(src.device))
+    pending = [None, None]
+
+    def host_copy(slot, off, cnt):
+        view = slots[slot].numpy()[:cnt]
+        parts = max(1, min(_COPY_THREADS, cnt // (1 << 18)))
+        step = (cnt + parts - 1) // parts
+        futs = [pool.submit(np.copyto, dst[off + i:off + min(i + step, cnt)], view[i:min(i + step, cnt)])
+                for i in range(0, cnt, step)]
+        for f in futs:
+            f.result()
+
+    k = 0
+    for off in range(0, n, chunk):
+        cnt = min(chunk, n - off)
+        if pending[k] is not None:                      # the slot's previous chunk must be on the host
+            host_copy(*pending[k])
+            pending[k] = None
+        with torch.cuda.stream(stream):
+            slots[k][:cnt].copy_(src[off:off + cnt], non_blocking=True)
+            events[k].record(stream)
+        prev = 1 - k
+        if pending[prev] is not None:
+            host_copy(*pending[prev])
+            pending[prev] = None
+        events[k].synchronize()
+        pending[k] = (k, off, cnt)
+        k = 1 - k
+    for p in pending:
+        if p is not None:
+            host_copy(*p)
 
 
 # ------------------------------------------------------- kernel wrappers

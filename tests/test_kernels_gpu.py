@@ -766,6 +766,34 @@ def test_cgs_fused_matches_pass_by_pass(dim, g, precond, rng):
     assert np.abs(q.T @ xf).max() <= 1e-13
 
 
+@pytest.mark.parametrize("g,s", [(20, 3), (35, 8), (35, 15), (35, 20), (40, 32)])
+def test_restart_inplace_product_variants(g, s, rng):
+    """Thick-restart V <- V C in place: the vectorised kernel
+    (ts_gemm_inplace_vec_kernel) and the generic one (svdsb_tune_set key
+    4 = 2) give the same bits, equal to X C within rounding, on an odd row
+    count; the columns past s are untouched."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    dim = 200_001
+    x0 = rng.standard_normal((dim, g))
+    c = rng.standard_normal((g, s))
+    outs = []
+    for key in (0, 2):
+        X = dv.to_device_block(x0)
+        C = dv.to_device_block(c)
+        try:
+            _lib.call("svdsb_tune_set", 4, key)
+            dv.ts_gemm(ctx, X, C, X[:, :s])
+        finally:
+            _lib.call("svdsb_tune_set", 4, 0)
+        outs.append(dv.to_host(X))
+    assert np.array_equal(outs[0], outs[1])
+    want = x0 @ c
+    assert np.abs(outs[0][:, :s] - want).max() <= 1e-13 * np.abs(want).max() * g
+    assert np.array_equal(outs[0][:, s:], x0[:, s:])
+
+
 def test_grid_barrier_and_ticket_reductions_stress(rng):
     """Race evidence for the synchronisation the kernels build themselves
     (compute-sanitizer is closed on the GPU pool): the software grid
