@@ -280,6 +280,22 @@ int svdsb_cgs_fused(svdsb_ctx *ctx, int64_t dim, int nblk,
                     const double *yin, int64_t ldyin, int g, int kk,
                     double *prev, int64_t ldprev, int passes, double *state,
                     void *stream);
+/* Device-decided iterated CGS of a block of b new columns v (in place, on
+ * entry the preconditioned expansion directions, on exit orthonormal),
+ * the reference's column loop (kernels.py:54-133, eigensolver.py:666-700)
+ * with its first pass split: the projection against the prior blocks runs
+ * for all b columns at once (one Gram + one projection over the basis
+ * instead of b of each), then column j finishes pass 1 against the block's
+ * columns 0..j-1 and takes up to passes-1 further passes against
+ * [prior, v[:, :j]] as svdsb_cgs_pass; the DGKS decision of pass 1 uses
+ * |v_j| before the batched projection.  state: b 8-double records
+ * (svdsb_cgs_pass layout); a column still active or collapsed after
+ * `passes` (state[0] != 0 or state[5] == 0) must be redone by the caller.
+ * cwork >= total*b + 3*b + total doubles (total = prior columns). */
+int svdsb_cgs_block(svdsb_ctx *ctx, int64_t dim, int nblk,
+                    const double *const *xs, const int64_t *ldxs,
+                    const int *cols, double *v, int64_t ldv, int b,
+                    double *cwork, double *state, int passes, void *stream);
 /* 1 when svdsb_cgs_fused can run on the current device (cooperative launch
  * supported, kernel fits an SM); callers use svdsb_cgs_pass otherwise. */
 int svdsb_cgs_fused_supported(void);

@@ -72,6 +72,7 @@ _PROTOS = [
     ("svdsb_cgs_fused", i32, [vp, i64, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp, i64, i32, i32, vp, i64, i32,
                               vp, vp]),
     ("svdsb_cgs_fused_supported", i32, []),
+    ("svdsb_cgs_block", i32, [vp, i64, i32, vp, vp, vp, vp, i64, i32, vp, vp, i32, vp]),
     ("svdsb_cgs_pass", i32, [vp, i64, i32, vp, vp, vp, vp, vp, vp, i32, vp]),
     ("svdsb_split_residual",i32, [vp, i64, i64, vp, i64, vp, i64, i32, vp, vp, vp, vp]),
     ("svdsb_syev_small", i32, [i32, vp, i64, i32, f64, vp, vp, i64, vp]),

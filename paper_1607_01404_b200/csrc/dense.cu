@@ -743,6 +743,23 @@ __device__ __forceinline__ void dgks_decide(double *st) {
   st[5] = fin;
 }
 
+// Arm b DGKS records after the batched first projection of a block
+// (svdsb_cgs_block): record j gets |v_j|^2 before (pass 1 started from the
+// original column); column 0, whose pass 1 is complete, also gets its
+// after-norm and the decision.
+__global__ void dgks_seed_kernel(double *st, int b, const double *before2, const double *after2) {
+  pdl_wait();
+  pdl_trigger();
+  const int j = threadIdx.x;
+  if (j >= b) return;
+  double *r = st + 8 * j;
+  r[0] = 1.0;
+  r[1] = r[2] = r[3] = r[4] = r[5] = 0.0;
+  r[6] = before2[j];
+  r[7] = after2[j];
+  if (j == 0) dgks_decide(r);
+}
+
 __global__ void dgks_begin_kernel(double *st) {
   pdl_wait();
   pdl_trigger();
@@ -1746,6 +1763,57 @@ int svdsb_cgs_fused_supported(void) {
     ok[dev] = (coop && occ >= 1) ? 1 : -1;
   }
   return ok[dev] == 1;
+}
+
+int svdsb_cgs_block(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs,
+                    const int *cols, double *v, int64_t ldv, int b, double *cwork, double *state, int passes,
+                    void *stream) {
+  SVDSB_CHECK_ARG(ctx != nullptr && v != nullptr && cwork != nullptr && state != nullptr,
+                  "svdsb_cgs_block: NULL argument");
+  SVDSB_CHECK_ARG(b >= 1 && b <= 32 && passes >= 1 && passes <= 6, "svdsb_cgs_block: 1..32 columns, 1..6 passes");
+  SVDSB_CHECK_ARG(nblk >= 1 && nblk < SVDSB_MAX_BLOCKS, "svdsb_cgs_block: 1..MAX_BLOCKS-1 prior blocks");
+  ColSet s;
+  int rc = make_colset(s, nblk, xs, ldxs, cols);
+  if (rc) return rc;
+  SVDSB_CHECK_ARG(s.total >= 1 && s.total + b <= 256, "svdsb_cgs_block: 1..256 prior columns");
+  if (dim == 0) return SVDSB_OK;
+  // cwork: C (total x b) | before2 (b) | after2 (b)
+  double *c = cwork, *before2 = cwork + (int64_t)s.total * b, *after2 = before2 + b;
+  // pass 1, old part, all columns at once: C = X^T V (norms before), V -= X C (norms after)
+  if ((rc = svdsb_gram(ctx, dim, nblk, xs, ldxs, cols, v, ldv, b, c, s.total, before2, stream))) return rc;
+  if ((rc = svdsb_project_out(ctx, dim, nblk, xs, ldxs, cols, c, s.total, v, ldv, b, after2, stream))) return rc;
+  SVDSB_LAUNCH_PDL(dgks_seed_kernel, 1, 32, 0, as_stream(stream), state, b, (const double *)before2,
+                   (const double *)after2);
+  const double *xs2[SVDSB_MAX_BLOCKS];
+  int64_t ld2[SVDSB_MAX_BLOCKS];
+  int cols2[SVDSB_MAX_BLOCKS];
+  for (int k = 0; k < nblk; ++k) {
+    xs2[k] = xs[k];
+    ld2[k] = ldxs[k];
+    cols2[k] = cols[k];
+  }
+  xs2[nblk] = v;
+  ld2[nblk] = ldv;
+  for (int j = 0; j < b; ++j) {
+    double *vj = v + (int64_t)j * ldv, *st = state + 8 * j;
+    if (j > 0) {
+      // pass 1, new part: against the finished columns 0..j-1 of the block;
+      // the projection's last CTA applies the DGKS decision of the pass
+      const double *nb[1] = {v};
+      const int64_t nl[1] = {ldv};
+      const int nc[1] = {j};
+      if ((rc = svdsb_cgs_pass(ctx, dim, 1, nb, nl, nc, vj, cwork + (int64_t)s.total * b + 2 * b, st, 0, stream)))
+        return rc;
+    }
+    cols2[nblk] = j;
+    const int nb2 = j > 0 ? nblk + 1 : nblk;
+    for (int p = 1; p < passes; ++p)
+      if ((rc = svdsb_cgs_pass(ctx, dim, nb2, xs2, ld2, cols2, vj, cwork + (int64_t)s.total * b + 2 * b, st, 0,
+                               stream)))
+        return rc;
+    if ((rc = svdsb_scale_cols(dim, vj, ldv, 1, st + 5, 1 /* divide */, vj, ldv, stream))) return rc;
+  }
+  return SVDSB_OK;
 }
 
 int svdsb_cgs_pass(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs,

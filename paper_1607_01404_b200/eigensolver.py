@@ -1357,15 +1357,35 @@ class DavidsonSolver:
         else:
             dv.axpby(self.ctx, 1.0, block, 0.0, src)
         st = self._dgks_state
-        for j in range(b):
-            prior = self._against() + [self.v[:, :g + j]]
-            self._spec_cgs(prior, src[:, j:j + 1], self.v[:, g + j:g + j + 1], st[8 * j:8 * j + 8])
+        self._block_cgs(self._against() + [self.v[:, :g]], src, self.v[:, g:g + b], st)
         self._apply_op(self.v[:, g:g + b], self.w[:, g:g + b])
         hc = ws.hcb[:g + b, :b]
         dv.gram(self.ctx, self.n, [self.v[:, :g + b]], self.w[:, g:g + b], hc)
         dv.h_insert(self.ctx, g, b, hc, self.h)
         self._spec = {"g0": g, "b": b, "src": src}
         self.g = g + b
+
+    # block CGS: batched first pass (svdsb_cgs_block); SVDSB_BLOCK_CGS=0 runs
+    # the columns one by one through _spec_cgs instead
+    block_cgs = os.environ.get("SVDSB_BLOCK_CGS", "1") != "0"
+
+    def _block_cgs(self, prior, src, dst, st):
+        """dst = src orthonormalised column by column against the prior
+        blocks and the block's earlier columns, DGKS decided on the device
+        (b records in st)."""
+        b = dst.shape[1]
+        total = sum(p_.shape[1] for p_ in prior)
+        if (not self.block_cgs or len(prior) + 1 >= _lib.MAX_BLOCKS
+                or total * b + 3 * b + total > self.ortho.c.numel() or total + b > 256):
+            g0 = prior[-1].shape[1]
+            for j in range(b):
+                self._spec_cgs(prior[:-1] + [self.v[:, :g0 + j]], src[:, j:j + 1], dst[:, j:j + 1],
+                               st[8 * j:8 * j + 8])
+            return
+        dv.axpby(self.ctx, 1.0, src, 0.0, dst)
+        n, ptrs, lds, cols, _ = dv._blk_args(prior)
+        _lib.call("svdsb_cgs_block", self.ctx.handle, self.n, n, ptrs, lds, cols, dv.P(dst), dv.ld_of(dst), b,
+                  dv.P(self.ortho.c), dv.P(st), self.SPEC_PASSES, self.ctx.stream)
 
     def _resolve_block(self, spec, st):
         """Resolve a speculative block expansion: it stands when every
@@ -1563,8 +1583,7 @@ class DavidsonSolver:
         src = ws.src[sout][:, :b]
         dv.gather_cols(ctx, y_in[:g, :g], ws.ci, kk, g, self.prev_d[:g, :kk])
         dv.gather_cols(ctx, ws.rbuf[sin], ws.ci, b, self.pmax, src, d=d)
-        for j in range(b):
-            self._spec_cgs([self.v[:, :g + j]], src[:, j:j + 1], self.v[:, g + j:g + j + 1], st[8 * j:8 * j + 8])
+        self._block_cgs([self.v[:, :g]], src, self.v[:, g:g + b], st)
         self.op.raw_into(self.v[:, g:g + b], self.w[:, g:g + b])
         hc = ws.hcb[:g + b, :b]
         dv.gram(ctx, self.n, [self.v[:, :g + b]], self.w[:, g:g + b], hc)

@@ -794,6 +794,67 @@ def test_restart_inplace_product_variants(g, s, rng):
     assert np.array_equal(outs[0][:, s:], x0[:, s:])
 
 
+@pytest.mark.parametrize("b", [2, 3, 4])
+def test_cgs_block_matches_column_loop(b, rng):
+    """svdsb_cgs_block (first CGS pass batched over the block's columns)
+    against the reference's column loop run on the host with NumPy
+    (kernels.py:54-133): the same DGKS pass counts, the same vectors to
+    rounding, an orthonormal block orthogonal to the basis; a column that
+    repeats an earlier one is reported collapsed (state[5] == 0) so the
+    solver redoes the block on the host path."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    dim, g = 400_000, 27
+    q, _ = np.linalg.qr(rng.standard_normal((dim, g)))
+    S = rng.standard_normal((dim, b)) + q[:, :b] * 3.0
+    V = dv.to_device_block(q)
+    n_, ptrs, lds, cols, _ = dv._blk_args([V])
+    for collapse in (False, True):
+        src = S.copy()
+        if collapse:
+            src[:, b - 1] = src[:, 0]
+        X = dv.to_device_block(src)
+        st = torch.zeros(8 * b, dtype=torch.float64, device="cuda")
+        cw = torch.zeros(1024, dtype=torch.float64, device="cuda")
+        _lib.call("svdsb_cgs_block", ctx.handle, dim, n_, ptrs, lds, cols, dv.P(X), dv.ld_of(X), b, dv.P(cw),
+                  dv.P(st), 3, ctx.stream)
+        got, rec = dv.to_host(X), st.cpu().numpy().reshape(b, 8)
+        # host column loop (the reference's algorithm)
+        want = src.copy()
+        passes = []
+        for j in range(b):
+            prior = np.concatenate([q, want[:, :j]], axis=1)
+            v = want[:, j]
+            orig = prev = np.linalg.norm(v)
+            hits, npass, final = 0, 0, 0.0
+            for _ in range(3):
+                v -= prior @ (prior.T @ v)
+                npass += 1
+                cur = np.linalg.norm(v)
+                if cur < 1e-14 * orig:
+                    hits += 1
+                    if hits >= 2:
+                        break
+                elif cur > 2 ** -0.5 * prev:
+                    final = cur
+                    break
+                else:
+                    hits = 0
+                prev = cur
+            passes.append(npass)
+            if final > 0:
+                v /= final
+        if not collapse:
+            assert (rec[:, 0] == 0.0).all() and (rec[:, 5] > 0.0).all()
+            assert list(rec[:, 1].astype(int)) == passes
+            assert np.abs(got - want).max() <= 1e-12
+            assert np.abs(got.T @ got - np.eye(b)).max() <= 1e-13
+            assert np.abs(q.T @ got).max() <= 1e-13
+        else:
+            assert rec[b - 1, 5] == 0.0 or rec[b - 1, 0] != 0.0
+
+
 def test_grid_barrier_and_ticket_reductions_stress(rng):
     """Race evidence for the synchronisation the kernels build themselves
     (compute-sanitizer is closed on the GPU pool): the software grid
