@@ -140,7 +140,8 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // Key 2: sliced-ELL b = 4 (0 grouped loads, 1 whole-row prefetch for rows
 // <= 20; slower on config 4).
 // Key 3: Ritz residual (0: two threads per row for 16 < p <= 32, one
-// otherwise; 1: always one; 2: two also for 8 < p <= 16).
+// otherwise; 1: always one; 2: two also for 8 < p <= 16; 4: two threads per
+// row with two rows each for 16 < p <= 24 -- slower on config 4).
 // Key 4: native GD+k iteration (0 H-column / status epilogues, 1 separate
 // h_insert and status_pack launches); 2 also selects the generic 32-column
 // in-place restart product instead of ts_gemm_inplace_vec_kernel.

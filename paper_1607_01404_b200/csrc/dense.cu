@@ -1021,6 +1021,148 @@ ritz_split_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const 
   }
 }
 
+template <int PQ>
+__global__ void __launch_bounds__(kThreads, 2)
+ritz_split_r2_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const double *__restrict__ w, int64_t ldw,
+                  int g, const double *__restrict__ yc, int64_t ldyc, const double *__restrict__ lam, int p,
+                  double *__restrict__ r, int64_t ldr, double *__restrict__ xo, int64_t ldx, double *__restrict__ oxo,
+                  int64_t ldox, double *rn2, double *partials, unsigned int *ticket, StatusOut so) {
+  constexpr int SPLIT = 2;
+  constexpr int PT = PQ * SPLIT;
+  pdl_wait();
+  extern __shared__ double ysh[];  // g x PT
+  __shared__ double lsh[PT];
+  __shared__ double red[kWarps][PT];
+  for (int k = threadIdx.x; k < g * PT; k += kThreads) {
+    int i = k / PT, j = k % PT;
+    ysh[k] = (j < p) ? yc[i + (int64_t)j * ldyc] : 0.0;
+  }
+  if (threadIdx.x < PT) lsh[threadIdx.x] = ((int)threadIdx.x < p) ? lam[threadIdx.x] : 0.0;
+  __syncthreads();
+  const int part = threadIdx.x % SPLIT;
+  const int j0 = part * PQ;
+  // per-thread candidate norms in shared memory ([j][thread]: conflict
+  // free), so the 48 accumulators of the two rows fit the register budget
+  __shared__ double nsh[PQ][kThreads];
+#pragma unroll
+  for (int j = 0; j < PQ; ++j) nsh[j][threadIdx.x] = 0.0;
+  // two adjacent rows per thread pair member: every shared-memory
+  // coefficient feeds four FMAs instead of two (the one-row kernel is bound
+  // by shared-memory bandwidth at ~half the fp64 FMA rate); 16-byte loads
+  // and stores; per element the same fma chain, so R is bit-identical
+  RowRange rr = cta_rows_even(dim);
+  constexpr int RPP = kThreads;  // rows per pass of the CTA (kThreads/2 pairs x 2 rows)
+  for (int64_t row = rr.r0 + 2 * (threadIdx.x / SPLIT); row < rr.r1; row += RPP) {
+    const bool two = row + 1 < rr.r1;
+    double2 ax[PQ], aw[PQ];
+#pragma unroll
+    for (int j = 0; j < PQ; ++j) {
+      ax[j] = make_double2(0.0, 0.0);
+      aw[j] = make_double2(0.0, 0.0);
+    }
+    constexpr int RU = 1;
+    int i = 0;
+    for (; i + RU <= g; i += RU) {
+      double2 vv[RU], ww[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        if (two) {
+          vv[u] = ldg2(v + row + (int64_t)(i + u) * ldv);
+          ww[u] = ldg2(w + row + (int64_t)(i + u) * ldw);
+        } else {
+          vv[u] = make_double2(__ldg(v + row + (int64_t)(i + u) * ldv), 0.0);
+          ww[u] = make_double2(__ldg(w + row + (int64_t)(i + u) * ldw), 0.0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const double2 *yrow = reinterpret_cast<const double2 *>(ysh + (i + u) * PT + j0);
+#pragma unroll
+        for (int j = 0; j < PQ / 2; ++j) {
+          const double2 cf = yrow[j];
+          ax[2 * j].x = fma(vv[u].x, cf.x, ax[2 * j].x);
+          ax[2 * j].y = fma(vv[u].y, cf.x, ax[2 * j].y);
+          aw[2 * j].x = fma(ww[u].x, cf.x, aw[2 * j].x);
+          aw[2 * j].y = fma(ww[u].y, cf.x, aw[2 * j].y);
+          ax[2 * j + 1].x = fma(vv[u].x, cf.y, ax[2 * j + 1].x);
+          ax[2 * j + 1].y = fma(vv[u].y, cf.y, ax[2 * j + 1].y);
+          aw[2 * j + 1].x = fma(ww[u].x, cf.y, aw[2 * j + 1].x);
+          aw[2 * j + 1].y = fma(ww[u].y, cf.y, aw[2 * j + 1].y);
+        }
+      }
+    }
+    for (; i < g; ++i) {
+      double2 vv, ww;
+      if (two) {
+        vv = ldg2(v + row + (int64_t)i * ldv);
+        ww = ldg2(w + row + (int64_t)i * ldw);
+      } else {
+        vv = make_double2(__ldg(v + row + (int64_t)i * ldv), 0.0);
+        ww = make_double2(__ldg(w + row + (int64_t)i * ldw), 0.0);
+      }
+      const double2 *yrow = reinterpret_cast<const double2 *>(ysh + i * PT + j0);
+#pragma unroll
+      for (int j = 0; j < PQ / 2; ++j) {
+        const double2 cf = yrow[j];
+        ax[2 * j].x = fma(vv.x, cf.x, ax[2 * j].x);
+        ax[2 * j].y = fma(vv.y, cf.x, ax[2 * j].y);
+        aw[2 * j].x = fma(ww.x, cf.x, aw[2 * j].x);
+        aw[2 * j].y = fma(ww.y, cf.x, aw[2 * j].y);
+        ax[2 * j + 1].x = fma(vv.x, cf.y, ax[2 * j + 1].x);
+        ax[2 * j + 1].y = fma(vv.y, cf.y, ax[2 * j + 1].y);
+        aw[2 * j + 1].x = fma(ww.x, cf.y, aw[2 * j + 1].x);
+        aw[2 * j + 1].y = fma(ww.y, cf.y, aw[2 * j + 1].y);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PQ; ++j) {
+      if (j0 + j < p) {
+        const double l = lsh[j0 + j];
+        const double2 res = make_double2(__dsub_rn(aw[j].x, __dmul_rn(ax[j].x, l)),
+                                         __dsub_rn(aw[j].y, __dmul_rn(ax[j].y, l)));
+        if (two) {
+          *reinterpret_cast<double2 *>(r + row + (int64_t)(j0 + j) * ldr) = res;
+          if (xo) *reinterpret_cast<double2 *>(xo + row + (int64_t)(j0 + j) * ldx) = ax[j];
+          if (oxo) *reinterpret_cast<double2 *>(oxo + row + (int64_t)(j0 + j) * ldox) = aw[j];
+          nsh[j][threadIdx.x] = fma(res.y, res.y, fma(res.x, res.x, nsh[j][threadIdx.x]));
+        } else {
+          r[row + (int64_t)(j0 + j) * ldr] = res.x;
+          if (xo) xo[row + (int64_t)(j0 + j) * ldx] = ax[j].x;
+          if (oxo) oxo[row + (int64_t)(j0 + j) * ldox] = aw[j].x;
+          nsh[j][threadIdx.x] = fma(res.x, res.x, nsh[j][threadIdx.x]);
+        }
+      }
+    }
+  }
+  pdl_trigger();
+  // per-candidate CTA sums: lanes of equal `part` reduced with xor shuffles
+  // (lane % SPLIT is preserved by xor offsets >= SPLIT), then across warps
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < PQ; ++j) {
+    double t = nsh[j][threadIdx.x];
+#pragma unroll
+    for (int off = 16; off >= SPLIT; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (lane < SPLIT) red[wid][lane * PQ + j] = t;
+  }
+  __syncthreads();
+  double *pp = partials + (int64_t)blockIdx.x * PT;
+  for (int k = threadIdx.x; k < PT; k += kThreads) {
+    double t = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) t += red[ww][k];
+    pp[k] = t;
+  }
+  if (!last_cta(ticket)) return;
+  fold_parts(partials, gridDim.x, PT, p, [&](int j, int, int, double t) { rn2[j] = t; });
+  if (so.host != nullptr) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < so.gn + p + 8; i += blockDim.x)
+      so.host[i] = i < so.gn ? so.lams[i] : (i < so.gn + p ? rn2[i - so.gn] : so.st[i - so.gn - p]);
+    __threadfence_system();
+  }
+}
+
 // Y = alpha X C + beta Y, two rows per thread, s <= ST.
 template <int ST>
 __global__ void __launch_bounds__(kThreads)
@@ -1565,6 +1707,17 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
   SVDSB_LAUNCH_PDL(ritz_split_kernel<PQ, 2>, grid_for(ritz_split_kernel<PQ, 2>, dim, sizeof(double) * g * 2 * PQ), \
                    kThreads, sizeof(double) * g * 2 * PQ, st, dim, v, ldv, w, ldw, g, yc, ldyc, lam, p, r, ldr, x,  \
                    ldx, ox, ldox, rn2, ctx->partials, tk, so)
+    const bool vec = aligned16(v) && aligned16(w) && aligned16(r) && !(ldv & 1) && !(ldw & 1) && !(ldr & 1) &&
+                     (x == nullptr || (aligned16(x) && !(ldx & 1))) && (ox == nullptr || (aligned16(ox) && !(ldox & 1)));
+    if (vec && p <= 24 && g_tune[3] == 4) {  // measured slower on config 4 (386 vs 296 us); PQ = 16 would spill
+#define SVDSB_RITZ_R2(PQ)                                                                                      \
+  SVDSB_LAUNCH_PDL(ritz_split_r2_kernel<PQ>, grid_for(ritz_split_r2_kernel<PQ>, dim, sizeof(double) * g * 2 * PQ),  \
+                   kThreads, sizeof(double) * g * 2 * PQ, st, dim, v, ldv, w, ldw, g, yc, ldyc, lam, p, r, ldr, x,  \
+                   ldx, ox, ldox, rn2, ctx->partials, tk, so)
+      SVDSB_RITZ_R2(12);
+#undef SVDSB_RITZ_R2
+      return SVDSB_OK;
+    }
     if (p <= 24)
       SVDSB_RITZ_SPLIT(12);
     else

@@ -145,8 +145,9 @@ def test_gram_b4_grid_orders(order, rng):
 @pytest.mark.parametrize("p", [6, 11, 16, 20, 24, 32])
 def test_ritz_residual_variants(p, rng):
     """Ritz residuals R = W Y - V Y diag(lam) and |R_j|^2 for one and two
-    threads per row (svdsb_tune_set key 3): R bit-identical between the
-    variants (same fma order), both against fp64 numpy."""
+    threads per row, the latter with one or two rows per thread
+    (svdsb_tune_set key 3; dim odd so a pair tail exists): R bit-identical
+    between the variants (same fma order), all against fp64 numpy."""
     from paper_1607_01404_b200 import _lib
     dv = _dev()
     ctx = dv.context()
@@ -159,7 +160,7 @@ def test_ritz_residual_variants(p, rng):
     want = wh @ yh - (vh @ yh) * lh
     outs = []
     try:
-        for variant in (1, 2, 0):
+        for variant in (1, 2, 4, 0):
             _lib.call("svdsb_tune_set", 3, variant)
             R = dv.new_block(dim, p)
             rn2 = torch.zeros(p, dtype=torch.float64, device=ctx.device)
