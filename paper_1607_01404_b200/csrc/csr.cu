@@ -1146,8 +1146,11 @@ __device__ __forceinline__ void warprow4t(int64_t row, const int *__restrict__ r
 // products left to right with no FMA, continuing from y when accumulating
 // over column blocks -- np.add.at's order, bit-identical to the CSR
 // kernels.  Rows longer than a tile are not in the copy (chunk path).
+#ifndef SVDSB_T4T_MINB
+#define SVDSB_T4T_MINB 4   // resident CTAs per SM the register budget targets (64 registers, no spills; 2: 75 registers, 1.7% slower)
+#endif
 template <int YROW>
-__global__ void __launch_bounds__(kTileThreads, 2)
+__global__ void __launch_bounds__(kTileThreads, SVDSB_T4T_MINB)
 csr_sell4t_kernel(int64_t nq, int64_t nslice, const int *__restrict__ perm, const int *__restrict__ row_ptr,
                   const int64_t *__restrict__ sell_ptr, const int *__restrict__ scol, const double *__restrict__ sval,
                   int nmid, const int *__restrict__ mid, const int *__restrict__ col, const double *__restrict__ val,
