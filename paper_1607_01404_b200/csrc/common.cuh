@@ -151,8 +151,11 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // Key 7: b = 4 sliced ELL (0 TMA-staged ring for the forward product,
 // csr_sell4s_kernel, rows <= 20 nonzeros; 1 the direct-load kernels both
 // ways; 2 the TMA-staged ring both ways, csr_sell4ts_kernel transposed).
-constexpr int kTuneKeys = 8;
-inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0};
+// Key 8: transposed b = 4 rows of 65-2048 nonzeros (0 lane-parallel fma
+// sums + fixed xor tree, deterministic, within 1e-13 of the sequential sum;
+// 1 the serial left-to-right fold, bit-identical to np.add.at).
+constexpr int kTuneKeys = 12;
+inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 
 #define SVDSB_LAUNCH_PDL(...)                                             \
   do {                                                                    \

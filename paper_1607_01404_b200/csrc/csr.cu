@@ -1107,28 +1107,83 @@ __global__ void sell_fill_kernel(int64_t nrows, const int *__restrict__ perm, co
 constexpr int kSellTMax = 64;
 
 // One warp, one mid row (called by csr_sell4t_kernel).
+// kWR4 rounds of 32 nonzeros per step: every value / column-id load of the
+// step is issued first, then every gather, so one DRAM + one L2 round trip
+// serve 32 kWR4 nonzeros (one round of 32 used to pay both per 32).
+constexpr int kWR4 = 4;
+
 __device__ __forceinline__ void warprow4t(int64_t row, const int *__restrict__ row_ptr, const int *__restrict__ col,
                                           const double *__restrict__ val, const double *__restrict__ x,
                                           double *__restrict__ y, int64_t ldy, int yrow, int acc,
-                                          double (*prod)[33]) {
+                                          double (*prod)[32 * kWR4 + 1], int exact) {
   const int lane = threadIdx.x & 31;
   const int k0 = __ldg(row_ptr + row), k1 = __ldg(row_ptr + row + 1);
   const int cc = lane & 3;
   double sacc = 0.0;
   if (acc && lane < 4) sacc = yrow ? y[row * 4 + cc] : y[row + cc * ldy];
-  for (int k = k0; k < k1; k += 32) {
-    const int e = k + lane;
-    const bool ok = e < k1;
-    const int c = ok ? ld_ef(col + e) : 0;
-    const double v = ok ? ld_ef(val + e) : 0.0;
-    double xv[4];
-    gather4(x, c, xv);
+  if (!exact) {
+    // deterministic lane-parallel sum: lane l folds nonzeros l, l+32, ...
+    // (fma), then a fixed xor tree; no serial fold (config 4's 65-2048-nnz
+    // rows: 16 % of the nonzeros took a third of A^T.Y serially)
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = k0; k < k1; k += 32 * kWR4) {
+      int c[kWR4];
+      double v[kWR4], xv[kWR4][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) prod[q][lane] = dmul(v, xv[q]);
+      for (int u = 0; u < kWR4; ++u) {
+        const int e = k + 32 * u + lane;
+        const bool ok = e < k1;
+        c[u] = ok ? ld_ef(col + e) : 0;
+        v[u] = ok ? ld_ef(val + e) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kWR4; ++u) gather4(x, c[u], xv[u]);
+#pragma unroll
+      for (int u = 0; u < kWR4; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s4[q] = fma(v[u], xv[u][q], s4[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s4[q] = warp_sum(s4[q]);
+    if (lane < 4) {
+      const double t = cc == 0 ? s4[0] : cc == 1 ? s4[1] : cc == 2 ? s4[2] : s4[3];
+      const double out = acc ? dadd(sacc, t) : t;
+      if (yrow)
+        y[row * 4 + cc] = out;
+      else
+        y[row + cc * ldy] = out;
+    }
+    return;
+  }
+  for (int k = k0; k < k1; k += 32 * kWR4) {
+    int c[kWR4];
+    double v[kWR4], xv[kWR4][4];
+#pragma unroll
+    for (int u = 0; u < kWR4; ++u) {
+      const int e = k + 32 * u + lane;
+      const bool ok = e < k1;
+      c[u] = ok ? ld_ef(col + e) : 0;
+      v[u] = ok ? ld_ef(val + e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kWR4; ++u) gather4(x, c[u], xv[u]);
+#pragma unroll
+    for (int u = 0; u < kWR4; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) prod[q][32 * u + lane] = dmul(v[u], xv[u][q]);
     __syncwarp();
     if (lane < 4) {
-      const int n = min(32, k1 - k);
-      for (int t = 0; t < n; ++t) sacc = dadd(sacc, prod[cc][t]);
+      // left to right (np.add.at order); shared-memory loads eight ahead of
+      // the dependent adds, so the chain runs at the add latency
+      const int n = min(32 * kWR4, k1 - k);
+      for (int t0 = 0; t0 < n; t0 += 8) {
+        double pv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) pv[u] = prod[cc][min(t0 + u, 32 * kWR4 - 1)];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (t0 + u < n) sacc = dadd(sacc, pv[u]);
+      }
     }
     __syncwarp();
   }
@@ -1146,6 +1201,9 @@ __device__ __forceinline__ void warprow4t(int64_t row, const int *__restrict__ r
 // products left to right with no FMA, continuing from y when accumulating
 // over column blocks -- np.add.at's order, bit-identical to the CSR
 // kernels.  Rows longer than a tile are not in the copy (chunk path).
+#ifndef SVDSB_DBG_SKIP
+#define SVDSB_DBG_SKIP 0   // timing experiments only: 1 skips the mid rows, 2 the sliced rows
+#endif
 #ifndef SVDSB_T4T_MINB
 #define SVDSB_T4T_MINB 4   // resident CTAs per SM the register budget targets (64 registers, no spills; 2: 75 registers, 1.7% slower)
 #endif
@@ -1154,8 +1212,8 @@ __global__ void __launch_bounds__(kTileThreads, SVDSB_T4T_MINB)
 csr_sell4t_kernel(int64_t nq, int64_t nslice, const int *__restrict__ perm, const int *__restrict__ row_ptr,
                   const int64_t *__restrict__ sell_ptr, const int *__restrict__ scol, const double *__restrict__ sval,
                   int nmid, const int *__restrict__ mid, const int *__restrict__ col, const double *__restrict__ val,
-                  const double *__restrict__ x, double *__restrict__ y, int64_t ldy, int acc) {
-  __shared__ double prod[kTileThreads / 32][4][33];
+                  const double *__restrict__ x, double *__restrict__ y, int64_t ldy, int acc, int g_t4exact) {
+  __shared__ double prod[kTileThreads / 32][4][32 * kWR4 + 1];
   const int lane = threadIdx.x & 31;
   const int64_t wstride = (int64_t)gridDim.x * (kTileThreads / 32);
   pdl_wait();
@@ -1163,9 +1221,14 @@ csr_sell4t_kernel(int64_t nq, int64_t nslice, const int *__restrict__ perm, cons
   for (int64_t it = blockIdx.x * (int64_t)(kTileThreads / 32) + (threadIdx.x >> 5); it < nmid + nslice;
        it += wstride) {
     if (it < nmid) {
-      warprow4t(__ldg(mid + it), row_ptr, col, val, x, y, ldy, YROW, acc, prod[threadIdx.x >> 5]);
+#if SVDSB_DBG_SKIP != 1
+      warprow4t(__ldg(mid + it), row_ptr, col, val, x, y, ldy, YROW, acc, prod[threadIdx.x >> 5], g_t4exact);
+#endif
       continue;
     }
+#if SVDSB_DBG_SKIP == 2
+    continue;
+#endif
     const int64_t sl = it - nmid;
     const int64_t q = (sl << 5) + lane;
     if (q >= nq) continue;
@@ -2013,7 +2076,7 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
           auto k = yrow ? csr_sell4t_kernel<1> : csr_sell4t_kernel<0>;
           const int g = (int)std::min<int64_t>((p.nmid + 7) / 8, pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
           SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.nsell, (int64_t)0, p.sell_perm, p.row_ptr, p.sell_ptr,
-                           p.sell_col, p.sell_val, p.nmid, p.mid_rows, p.col, p.val, x, y, ldy, acc);
+                           p.sell_col, p.sell_val, p.nmid, p.mid_rows, p.col, p.val, x, y, ldy, acc, g_tune[8] == 1);
         }
         if (p.nslice > 0) {
           auto k = yrow ? csr_sell4ts_kernel<1> : csr_sell4ts_kernel<0>;
@@ -2034,7 +2097,7 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
           const int g = (int)std::min<int64_t>((p.nslice + p.nmid + 7) / 8,
                                                pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
           SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.nsell, p.nslice, p.sell_perm, p.row_ptr, p.sell_ptr, p.sell_col,
-                           p.sell_val, p.nmid, p.mid_rows, p.col, p.val, x, y, ldy, acc);
+                           p.sell_val, p.nmid, p.mid_rows, p.col, p.val, x, y, ldy, acc, g_tune[8] == 1);
         }
         short_done = true;
       }

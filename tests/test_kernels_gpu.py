@@ -36,6 +36,19 @@ def _csr(m, n, rows, cols, vals):
     return SparseMatrixCsr(m, n, rp, ci, va), (rp, ci, va)
 
 
+@pytest.fixture(autouse=True)
+def _exact_mid_rows():
+    """The kernel tests below check the transposed products bit for bit
+    against np.add.at's order for every row up to a tile, which needs the
+    serial fold for 65-2048-nonzero rows (svdsb_tune_set key 8 = 1); the
+    default lane-parallel sums of those rows are checked separately
+    (test_spmv_transpose_mid_rows_default)."""
+    from paper_1607_01404_b200 import _lib
+    _lib.call("svdsb_tune_set", 8, 1)
+    yield
+    _lib.call("svdsb_tune_set", 8, 0)
+
+
 SHAPES = [(1, 1, 1), (7, 5, 12), (300, 40, 3000), (40, 300, 3000), (2000, 1500, 30000), (513, 257, 0)]
 
 
@@ -309,6 +322,47 @@ def test_spmv_b23_padded_to_b4(b, rng):
     ok = lens <= 2048
     assert np.array_equal(out[0][1][ok], want_t[ok])
     assert np.abs(out[0][1] - want_t).max() <= 1e-12 * np.abs(want_t).max()
+
+
+@pytest.mark.parametrize("b", [1, 2, 4])
+def test_spmv_transpose_mid_rows_default(b, rng):
+    """Default transposed products (svdsb_tune_set key 8 = 0): rows of at
+    most 64 nonzeros bit-exact, rows of 65-2048 summed lane-parallel with a
+    fixed xor tree -- deterministic and within 1e-13 relative of the
+    sequential sum -- in the plain and the column-blocked (accumulating)
+    layout."""
+    import os
+    from paper_1607_01404_b200 import _lib
+    _lib.call("svdsb_tune_set", 8, 0)
+    m, n = 9000, 700
+    cols = np.concatenate([rng.integers(0, n, 20000), rng.integers(0, 40, 15000),
+                           np.full(2600, 650)])
+    rows = rng.integers(0, m, cols.size)
+    vals = rng.standard_normal(cols.size)
+    y = rng.standard_normal((m, b))
+    want = ocsr.spmv(m, n, *ocsr.csr_from_coo(m, n, rows, cols, vals), y, transpose=True)
+    old = os.environ.get("SVDSB_T_BLOCK_ROWS")
+    try:
+        for blocked in (False, True):
+            if blocked:
+                os.environ["SVDSB_T_BLOCK_ROWS"] = "2500"
+            a, (rp, ci, va) = _csr(m, n, rows, cols, vals)
+            g1 = _spmv_dev(a, y, True)
+            g2 = _spmv_dev(a, y, True)
+            assert np.array_equal(g1, g2)
+            lens = np.diff(ocsr.csr_transpose(m, n, rp, ci, va)[0])
+            assert ((lens > 64) & (lens <= 2048)).any()
+            scale = np.abs(want).max()
+            assert np.abs(g1 - want).max() <= 1e-13 * scale * 10
+            if b == 1:
+                assert np.array_equal(g1[lens <= 2048], want[lens <= 2048])   # b = 1 kernels stay serial
+            else:
+                assert np.array_equal(g1[lens <= 64], want[lens <= 64])
+    finally:
+        if old is None:
+            os.environ.pop("SVDSB_T_BLOCK_ROWS", None)
+        else:
+            os.environ["SVDSB_T_BLOCK_ROWS"] = old
 
 
 def test_spmv_bulk_copy_path_bit_exact(rng):
