@@ -163,6 +163,18 @@ def call(name, *args):
 
 _coop = {}
 
+# > 0 while an iteration graph is being captured: device frees are deferred
+# (matrix.DeviceCsr.__del__) so a finaliser cannot invalidate the capture
+CAPTURING = [0]
+DEFERRED = []
+
+
+def flush_deferred():
+    while DEFERRED and not CAPTURING[0]:
+        h = DEFERRED.pop()
+        if _lib is not None:
+            _lib.svdsb_csr_destroy(h)
+
 
 def cgs_fused_supported():
     """svdsb_cgs_fused needs a co-resident grid (cooperative launch)."""

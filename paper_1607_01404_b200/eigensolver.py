@@ -16,6 +16,7 @@ reference so trajectories track it.
 """
 
 import ctypes
+import gc
 import os
 from dataclasses import dataclass
 
@@ -1609,17 +1610,29 @@ class DavidsonSolver:
             cap = ctx.capture_stream = torch.cuda.Stream(ctx.device)
         old = ctx._stream
         lib = _lib.load()
-        _lib.check(lib.svdsb_graph_begin(cap.cuda_stream), "svdsb_graph_begin")
         ex = ctypes.c_void_p()
+        # no cyclic garbage collection while capturing: a finaliser that
+        # frees device memory (a previous matrix) would invalidate the
+        # capture; matrix finalisers run anyway are deferred (_lib.CAPTURING)
+        gc_on = gc.isenabled()
+        gc.disable()
+        _lib.CAPTURING[0] += 1
         try:
-            ctx._stream = cap.cuda_stream
-            fn()
+            _lib.check(lib.svdsb_graph_begin(cap.cuda_stream), "svdsb_graph_begin")
+            try:
+                ctx._stream = cap.cuda_stream
+                fn()
+            finally:
+                ctx._stream = old
+                if reuse is None:
+                    rc = lib.svdsb_graph_end(cap.cuda_stream, ctypes.byref(ex))
+                else:
+                    rc = lib.svdsb_graph_end_update(cap.cuda_stream, reuse.exec, ctypes.byref(ex))
         finally:
-            ctx._stream = old
-            if reuse is None:
-                rc = lib.svdsb_graph_end(cap.cuda_stream, ctypes.byref(ex))
-            else:
-                rc = lib.svdsb_graph_end_update(cap.cuda_stream, reuse.exec, ctypes.byref(ex))
+            _lib.CAPTURING[0] -= 1
+            if gc_on:
+                gc.enable()
+            _lib.flush_deferred()
         _lib.check(rc, "svdsb_graph_end")
         if reuse is not None and ex.value == reuse.exec:
             reuse.exec = None   # ownership moves to the returned graph

@@ -27,6 +27,7 @@ improvement, or at ``max_inner_iterations``.
 """
 
 import ctypes
+import gc
 
 import numpy as np
 import torch
@@ -127,16 +128,25 @@ class JdqmrInner:
         cap.wait_stream(ctx.torch_stream)
         l0 = _lib.launch_count()
         cond = ctypes.c_uint64()
-        _lib.check(lib.svdsb_while_begin(cap.cuda_stream, ctypes.byref(cond)), "svdsb_while_begin")
         ex = ctypes.c_void_p()
         old = ctx._stream
+        gc_on = gc.isenabled()   # as DavidsonSolver._capture: no finalisers inside a capture
+        gc.disable()
+        _lib.CAPTURING[0] += 1
         try:
-            ctx._stream = cap.cuda_stream
-            self._apply(raw=True)
-            self._phase(1, nq, cond.value)
+            _lib.check(lib.svdsb_while_begin(cap.cuda_stream, ctypes.byref(cond)), "svdsb_while_begin")
+            try:
+                ctx._stream = cap.cuda_stream
+                self._apply(raw=True)
+                self._phase(1, nq, cond.value)
+            finally:
+                ctx._stream = old
+                rc = lib.svdsb_while_end(cap.cuda_stream, ctypes.byref(ex))
         finally:
-            ctx._stream = old
-            rc = lib.svdsb_while_end(cap.cuda_stream, ctypes.byref(ex))
+            _lib.CAPTURING[0] -= 1
+            if gc_on:
+                gc.enable()
+            _lib.flush_deferred()
         _lib.check(rc, "svdsb_while_end")
         from .eigensolver import _NativeGraph
         return _NativeGraph(ex.value), _lib.launch_count() - l0

@@ -137,7 +137,11 @@ class DeviceCsr:
     def __del__(self):
         try:
             if getattr(self, "handle", None) and _lib._lib is not None:
-                _lib._lib.svdsb_csr_destroy(self.handle)
+                if _lib.CAPTURING[0]:
+                    _lib.DEFERRED.append(self.handle)   # destroyed after the capture
+                else:
+                    _lib._lib.svdsb_csr_destroy(self.handle)
+                    _lib.flush_deferred()
         except Exception:
             pass
 
