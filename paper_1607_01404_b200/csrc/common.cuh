@@ -154,6 +154,10 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // Key 8: transposed b = 4 rows of 65-2048 nonzeros (0 lane-parallel fma
 // sums + fixed xor tree, deterministic, within 1e-13 of the sequential sum;
 // 1 the serial left-to-right fold, bit-identical to np.add.at).
+// Key 9: long rows of transposed b = 4 products (0 the 8192-nonzero chunks
+// gathering from L2, csr_chunk_kernel; 1 head tiles: the operand staged in
+// shared memory tile by tile, csr_headtile4_kernel -- 3.2x slower on config
+// 4: ~470 small pieces per 2048-row tile, each a latency-bound reduction).
 constexpr int kTuneKeys = 12;
 inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 

@@ -69,6 +69,15 @@ struct CsrPart {
   double *sell_val = nullptr;
   uint8_t *sell_len = nullptr;  // forward copy: row length of each sliced position (0 past the end)
   bool sell_failed = false;     // the copy could not be built: CSR kernels (same bits)
+  // head tiles of the long rows (b = 4 transposed products, built on first
+  // use): pieces of <= kHeadPiece nonzeros of one long row inside one
+  // kHeadTile-row tile of the operand, listed tile by tile
+  int nhtile = 0;
+  int *htp = nullptr;           // nhtile + 1: piece range of each tile
+  int4 *hpiece = nullptr;       // {k0, k1, output slot, -}
+  int *hcptr = nullptr;         // nlong + 1: slot range of each long row (tile order)
+  double *hpart = nullptr;      // slots x 4 partial sums
+  bool head_failed = false;
 };
 
 constexpr int kMaxB = 64;   // largest block handled by one matvec call
@@ -1705,19 +1714,98 @@ csr_chunk_kernel(const int *__restrict__ chunk_nz, const int *__restrict__ col,
   }
 }
 
+
+// Long rows of a transposed b = 4 product (the Zipf head of config 4's
+// A^T: 70 % of the nonzeros) by operand tiles: one CTA per kHeadTile rows
+// of the row-major operand x stages the tile in shared memory with
+// coalesced loads, then its warps sum the pieces -- at most kHeadPiece
+// consecutive nonzeros of one long row that fall in the tile -- against
+// shared memory (lane-parallel fma, fixed xor tree), one partial per piece.
+// Every x row is read from L2 once per tile instead of once per nonzero;
+// csr_long_fixup_kernel then adds each long row's partials in tile order
+// (deterministic; within rounding of the sequential sum, like the chunks).
+constexpr int kHeadTile = 2048;
+constexpr int kHeadPiece = 256;
+
+__global__ void __launch_bounds__(kTileThreads)
+csr_headtile4_kernel(int ntile, int64_t xrows, const int *__restrict__ htp, const int4 *__restrict__ pieces,
+                     const int *__restrict__ col, const double *__restrict__ val, const double *__restrict__ x,
+                     double *__restrict__ part) {
+  extern __shared__ __align__(16) double ys[];  // kHeadTile x 4
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  pdl_wait();
+  for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+    const int64_t r0 = (int64_t)t * kHeadTile;
+    const int nr = (int)min((int64_t)kHeadTile, xrows - r0);
+    const double2 *src = reinterpret_cast<const double2 *>(x + r0 * 4);
+    double2 *dst = reinterpret_cast<double2 *>(ys);
+    for (int i = threadIdx.x; i < 2 * nr; i += kTileThreads) dst[i] = __ldg(src + i);
+    __syncthreads();
+    const int p1 = __ldg(htp + t + 1);
+    for (int pc = __ldg(htp + t) + w; pc < p1; pc += kTileThreads / 32) {
+      const int4 pi = __ldg(pieces + pc);
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = pi.x + lane; k < pi.y; k += 32 * 4) {
+        int c[4];
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = k + 32 * u;
+          const bool ok = e < pi.y;
+          c[u] = ok ? ld_ef(col + e) - (int)r0 : 0;
+          v[u] = ok ? ld_ef(val + e) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double2 lo = dst[2 * c[u]], hi = dst[2 * c[u] + 1];
+          s4[0] = fma(v[u], lo.x, s4[0]);
+          s4[1] = fma(v[u], lo.y, s4[1]);
+          s4[2] = fma(v[u], hi.x, s4[2]);
+          s4[3] = fma(v[u], hi.y, s4[3]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s4[q] = warp_sum(s4[q]);
+      if (lane < 4) part[(int64_t)pi.z * 4 + lane] = lane == 0 ? s4[0] : lane == 1 ? s4[1] : lane == 2 ? s4[2] : s4[3];
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+}
+
+// seg[li * (ntile + 1) + t] = first nonzero of long row li at or past tile t
+__global__ void head_bounds_kernel(int nlong, int ntile, const int *__restrict__ long_row,
+                                   const int *__restrict__ row_ptr, const int *__restrict__ col, int *__restrict__ seg) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nlong * (ntile + 1)) return;
+  const int li = (int)(i / (ntile + 1)), t = (int)(i % (ntile + 1));
+  const int r = long_row[li];
+  int lo = row_ptr[r], hi = row_ptr[r + 1];
+  const int64_t key = (int64_t)t * kHeadTile;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (col[mid] < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  seg[i] = lo;
+}
+
 // One warp per (long row, column): lanes take chunks l, l+32, ... and a
 // fixed shuffle tree combines them (deterministic for a given chunking).
 __global__ void csr_long_fixup_kernel(int nlong, const int *__restrict__ long_row,
                                       const int *__restrict__ long_cptr,
                                       const double *__restrict__ part, int b,
-                                      double *__restrict__ y, int64_t ldy, int yrow, int accumulate) {
+                                      double *__restrict__ y, int64_t ldy, int yrow, int accumulate,
+                                      int pstride) {
   pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= nlong * b) return;
   const int li = warp / b, cc = warp % b;
   double s = 0.0;
-  for (int ch = long_cptr[li] + lane; ch < long_cptr[li + 1]; ch += 32) s += part[(int64_t)ch * kMaxB + cc];
+  for (int ch = long_cptr[li] + lane; ch < long_cptr[li + 1]; ch += 32) s += part[(int64_t)ch * pstride + cc];
   s = warp_sum(s);
   if (lane == 0) {
     int64_t r = long_row[li];
@@ -1796,6 +1884,22 @@ static void pfree(void *p, cudaStream_t st) {
   if (p) cudaFreeAsync(p, st);
 }
 
+// Temporary pool allocations of a build step, released (stream-ordered) on
+// every return path.
+struct StreamTemps {
+  cudaStream_t st;
+  std::vector<void *> v;
+  ~StreamTemps() {
+    for (void *q : v) pfree(q, st);
+  }
+  template <typename T>
+  cudaError_t get(T **q, size_t bytes) {
+    cudaError_t e = palloc(q, bytes, st);
+    if (e == cudaSuccess) v.push_back(*q);
+    return e;
+  }
+};
+
 template <typename T>
 static cudaError_t alloc_pad(T **dst, size_t n, cudaStream_t st) {
   return palloc(dst, n * sizeof(T) + kAllocPad, st);
@@ -1819,6 +1923,10 @@ static void free_part(CsrPart &p) {
   pfree(p.sell_col, nullptr);
   pfree(p.sell_val, nullptr);
   pfree(p.sell_len, nullptr);
+  pfree(p.htp, nullptr);
+  pfree(p.hpiece, nullptr);
+  pfree(p.hcptr, nullptr);
+  pfree(p.hpart, nullptr);
   p = CsrPart();
 }
 
@@ -1998,6 +2106,83 @@ static int build_partition(CsrPart &p, cudaStream_t st) {
   return SVDSB_OK;
 }
 
+// Head tiles of a part's long rows (see csr_headtile4_kernel): tile
+// boundaries inside every long row by binary search on the device, the
+// piece lists on the host.  Serialised and built once, like the sliced-ELL
+// copies; a part whose build fails keeps the chunk path (same semantics).
+static int build_head(CsrPart &p, cudaStream_t st) {
+  const int ntile = (int)((p.cols + kHeadTile - 1) / kHeadTile);
+  const int64_t nseg = (int64_t)p.nlong * (ntile + 1);
+  StreamTemps temps{st, {}};
+  int *dseg = nullptr;
+  SVDSB_CUDA(temps.get(&dseg, sizeof(int) * nseg));
+  head_bounds_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, st>>>(p.nlong, ntile, p.long_row, p.row_ptr, p.col,
+                                                                    dseg);
+  SVDSB_LAUNCHED();
+  std::vector<int> seg(nseg);
+  SVDSB_CUDA(cudaMemcpyAsync(seg.data(), dseg, sizeof(int) * nseg, cudaMemcpyDeviceToHost, st));
+  SVDSB_CUDA(cudaStreamSynchronize(st));
+  auto npieces = [&](int li, int t) {
+    const int len = seg[(int64_t)li * (ntile + 1) + t + 1] - seg[(int64_t)li * (ntile + 1) + t];
+    return (len + kHeadPiece - 1) / kHeadPiece;
+  };
+  // slots long row by long row (tile order inside), pieces tile by tile
+  std::vector<int> hcptr(p.nlong + 1, 0), base((int64_t)p.nlong * ntile);
+  for (int li = 0; li < p.nlong; ++li) {
+    int acc = hcptr[li];
+    for (int t = 0; t < ntile; ++t) {
+      base[(int64_t)li * ntile + t] = acc;
+      acc += npieces(li, t);
+    }
+    hcptr[li + 1] = acc;
+  }
+  std::vector<int> htp(ntile + 1, 0);
+  std::vector<int> pcs;
+  pcs.reserve(4 * (size_t)hcptr[p.nlong]);
+  for (int t = 0; t < ntile; ++t) {
+    htp[t] = (int)(pcs.size() / 4);
+    for (int li = 0; li < p.nlong; ++li) {
+      const int k0 = seg[(int64_t)li * (ntile + 1) + t], k1 = seg[(int64_t)li * (ntile + 1) + t + 1];
+      int slot = base[(int64_t)li * ntile + t];
+      for (int k = k0; k < k1; k += kHeadPiece, ++slot) {
+        pcs.push_back(k);
+        pcs.push_back(std::min(k + kHeadPiece, k1));
+        pcs.push_back(slot);
+        pcs.push_back(0);
+      }
+    }
+  }
+  htp[ntile] = (int)(pcs.size() / 4);
+  int rc;
+  if ((rc = upload(&p.htp, htp, st)) || (rc = upload(reinterpret_cast<int **>(&p.hpiece), pcs, st)) ||
+      (rc = upload(&p.hcptr, hcptr, st)))
+    return rc;
+  SVDSB_CUDA(palloc(&p.hpart, sizeof(double) * 4 * std::max(hcptr[p.nlong], 1), st));
+  p.nhtile = ntile;
+  return SVDSB_OK;
+}
+
+static std::mutex g_head_mu;
+static bool ensure_head(const CsrPart &cp, cudaStream_t st) {
+  if (cp.hpart) return true;
+  if (cp.head_failed || cp.nlong == 0 || capturing(st)) return false;
+  std::lock_guard<std::mutex> lk(g_head_mu);
+  CsrPart &p = const_cast<CsrPart &>(cp);  // cache fields only
+  if (p.hpart || p.head_failed) return p.hpart != nullptr;
+  if (build_head(p, st) != SVDSB_OK) {
+    p.head_failed = true;
+    pfree(p.htp, st);
+    pfree(p.hpiece, st);
+    pfree(p.hcptr, st);
+    p.htp = p.hcptr = nullptr;
+    p.hpiece = nullptr;
+    cudaGetLastError();
+    set_error("");
+    return false;
+  }
+  return true;
+}
+
 // y = P x for one orientation.  xrow / yrow: operands row-major with
 // stride b (only for 2 <= b <= 4); otherwise column-major with ld.
 template <int ORDER>
@@ -2123,12 +2308,25 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
                                                                        ldy, b);
       SVDSB_LAUNCHED();
     }
-    if (p.nlong > 0) {
+    if (p.nlong > 0 && ORDER == 1 && b == 4 && xrow && g_tune[9] == 1 && ensure_head(p, st)) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(csr_headtile4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * 4 * kHeadTile));
+        attr = true;
+      }
+      const size_t sm = sizeof(double) * 4 * kHeadTile;
+      SVDSB_LAUNCH_PDL(csr_headtile4_kernel, p.nhtile, kTileThreads, sm, st, p.nhtile, p.cols, p.htp, p.hpiece,
+                       p.col, p.val, x, p.hpart);
+      int tot = p.nlong * b;
+      SVDSB_LAUNCH_PDL(csr_long_fixup_kernel, (tot * 32 + 255) / 256, 256, 0, st, p.nlong, p.long_row, p.hcptr,
+                       p.hpart, b, y, ldy, yrow, acc, 4);
+    } else if (p.nlong > 0) {
       SVDSB_LAUNCH_PDL(csr_chunk_kernel, p.nchunk, kTileThreads, 0, st, p.chunk_nz, p.col, p.val, x, ldx, xrow, b,
                        p.chunk_part);
       int tot = p.nlong * b;
       SVDSB_LAUNCH_PDL(csr_long_fixup_kernel, (tot * 32 + 255) / 256, 256, 0, st, p.nlong, p.long_row, p.long_cptr,
-                       p.chunk_part, b, y, ldy, yrow, acc);
+                       p.chunk_part, b, y, ldy, yrow, acc, kMaxB);
     }
     return SVDSB_OK;
   }
@@ -2170,7 +2368,7 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
                        p.chunk_part);
       int tot = p.nlong * bb;
       SVDSB_LAUNCH_PDL(csr_long_fixup_kernel, (tot * 32 + 255) / 256, 256, 0, st, p.nlong, p.long_row, p.long_cptr,
-                       p.chunk_part, bb, yc, ldy, 0, acc);
+                       p.chunk_part, bb, yc, ldy, 0, acc, kMaxB);
     }
   }
   return SVDSB_OK;
@@ -2334,21 +2532,6 @@ __global__ void coo_sum_kernel(int64_t nt, int64_t n, const unsigned long long *
   atomicAdd(rowcnt + r, 1);
 }
 
-// Temporary pool allocations of a build step, released (stream-ordered) on
-// every return path.
-struct StreamTemps {
-  cudaStream_t st;
-  std::vector<void *> v;
-  ~StreamTemps() {
-    for (void *q : v) pfree(q, st);
-  }
-  template <typename T>
-  cudaError_t get(T **q, size_t bytes) {
-    cudaError_t e = palloc(q, bytes, st);
-    if (e == cudaSuccess) v.push_back(*q);
-    return e;
-  }
-};
 
 }  // namespace svdsb
 

@@ -365,6 +365,49 @@ def test_spmv_transpose_mid_rows_default(b, rng):
             os.environ["SVDSB_T_BLOCK_ROWS"] = old
 
 
+@pytest.mark.parametrize("blocked", [False, True])
+def test_spmv_transpose_long_rows_head_tiles(blocked, rng):
+    """Long rows (> 2048 nonzeros) of transposed b = 4 products: operand
+    tiles staged in shared memory (svdsb_tune_set key 9 = 1, several tiles
+    and pieces per row, a row count that is not a tile multiple) against the
+    L2-gathering chunks (key 9 = 1) and the oracle: deterministic, within
+    1e-13 relative of the sequential sum, short rows untouched (bit-exact)."""
+    import os
+    from paper_1607_01404_b200 import _lib
+    m, n = 11000, 300
+    cols = np.concatenate([rng.integers(0, n, 30000), np.full(9000, 7), np.full(4000, 123),
+                           rng.integers(0, 3, 9000)])
+    rows = rng.integers(0, m, cols.size)
+    vals = rng.standard_normal(cols.size)
+    y = rng.standard_normal((m, 4))
+    rp_, ci_, va_ = ocsr.csr_from_coo(m, n, rows, cols, vals)
+    want = ocsr.spmv(m, n, rp_, ci_, va_, y, transpose=True)
+    lens = np.diff(ocsr.csr_transpose(m, n, rp_, ci_, va_)[0])
+    assert (lens > 2048).sum() >= 3
+    old = os.environ.get("SVDSB_T_BLOCK_ROWS")
+    got = {}
+    try:
+        if blocked:
+            os.environ["SVDSB_T_BLOCK_ROWS"] = "3001"
+        a, _ = _csr(m, n, rows, cols, vals)
+        for key in (0, 1, 1):
+            _lib.call("svdsb_tune_set", 9, key)
+            g = _spmv_dev(a, y, True)
+            if key in got:
+                assert np.array_equal(g, got[key])       # deterministic
+            got[key] = g
+    finally:
+        _lib.call("svdsb_tune_set", 9, 0)
+        if old is None:
+            os.environ.pop("SVDSB_T_BLOCK_ROWS", None)
+        else:
+            os.environ["SVDSB_T_BLOCK_ROWS"] = old
+    scale = np.abs(want).max()
+    for g in got.values():
+        assert np.abs(g - want).max() <= 1e-13 * scale * 10
+        assert np.array_equal(g[lens <= 64], want[lens <= 64])
+
+
 def test_spmv_bulk_copy_path_bit_exact(rng):
     """Matrices of >= 64 MB stream through the cp.async.bulk tile ring
     (csr_tile_bulk_kernel); it must reproduce the reference's summation
