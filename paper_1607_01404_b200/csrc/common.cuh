@@ -158,6 +158,7 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // gathering from L2, csr_chunk_kernel; 1 head tiles: the operand staged in
 // shared memory tile by tile, csr_headtile4_kernel -- 3.2x slower on config
 // 4: ~470 small pieces per 2048-row tile, each a latency-bound reduction).
+// Key 10: sliced-ELL copies built on the device (0) or on the host (1).
 constexpr int kTuneKeys = 12;
 inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 

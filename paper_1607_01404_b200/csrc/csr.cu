@@ -1089,6 +1089,38 @@ csr_sell4s_kernel(int64_t nrows, int64_t nslice, const int64_t *__restrict__ sel
   pdl_trigger();
 }
 
+constexpr int kSellTMax = 64;  // transposed sliced-ELL rows (longer: one warp per row)
+
+// ---- device build of the sliced-ELL copies (build_sell_device)
+struct RowLenIn {
+  const int *rp;
+  int lo, hi;  // lo < length <= hi
+  __host__ __device__ bool operator()(const int &r) const {
+    const int l = rp[r + 1] - rp[r];
+    return l > lo && l <= hi;
+  }
+};
+
+__global__ void sell_keys_kernel(int64_t n, const int *__restrict__ rows, const int *__restrict__ rp,
+                                 unsigned *__restrict__ key) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) key[i] = (unsigned)(kSellTMax - (rp[rows[i] + 1] - rp[rows[i]]));  // longest first
+}
+
+// w[s + 1] = 32 * (longest row of slice s); w[0] = 0
+__global__ void sell_width_kernel(int64_t nq, int64_t ns, const int *__restrict__ perm, const int *__restrict__ rp,
+                                  int64_t *__restrict__ w) {
+  const int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (sl == 0) w[0] = 0;
+  if (sl >= ns) return;
+  int m = 0;
+  for (int64_t q = 32 * sl; q < min(nq, 32 * sl + 32); ++q) {
+    const int64_t r = perm ? perm[q] : q;
+    m = max(m, rp[r + 1] - rp[r]);
+  }
+  w[sl + 1] = 32 * (int64_t)m;
+}
+
 __global__ void sell_fill_kernel(int64_t nrows, const int *__restrict__ perm, const int *__restrict__ row_ptr,
                                  const int *__restrict__ col, const double *__restrict__ val,
                                  const int64_t *__restrict__ sell_ptr, int *__restrict__ scol,
@@ -1113,7 +1145,6 @@ __global__ void sell_fill_kernel(int64_t nrows, const int *__restrict__ perm, co
 // warp per row: lanes load 32 values / column ids at a time (coalesced) and
 // gather their x rows; four lanes (one per block column) then add the 32
 // products left to right -- np.add.at's order, bit-identical.
-constexpr int kSellTMax = 64;
 
 // One warp, one mid row (called by csr_sell4t_kernel).
 // kWR4 rounds of 32 nonzeros per step: every value / column-id load of the
@@ -2023,6 +2054,108 @@ static int build_sell(CsrPart &p, cudaStream_t st, bool sorted = false) {
   return SVDSB_OK;
 }
 
+// The sliced-ELL copy built on the device (CUB select / stable radix sort
+// by length / scan); the same layout and bits as the host build above, a
+// few ms instead of tens for config 4's parts (e2e: every new matrix
+// builds its copies).
+static int build_sell_device(CsrPart &p, cudaStream_t st, bool sorted) {
+  StreamTemps temps{st, {}};
+  int *dperm = nullptr, *dmid = nullptr;
+  int64_t nq = p.rows;
+  int nmid = 0;
+  if (sorted) {
+    int *sel = nullptr, *cnt = nullptr, *order = nullptr;
+    unsigned *key = nullptr, *key_s = nullptr;
+    SVDSB_CUDA(temps.get(&sel, sizeof(int) * std::max<int64_t>(p.rows, 1)));
+    SVDSB_CUDA(temps.get(&cnt, sizeof(int) * 2));
+    cub::CountingInputIterator<int> rows(0);
+    size_t tb = 0, tb2 = 0;
+    cub::DeviceSelect::If(nullptr, tb, rows, sel, cnt, (int)p.rows, RowLenIn{p.row_ptr, -1, kSellTMax}, st);
+    cub::DeviceSelect::If(nullptr, tb2, rows, sel, cnt + 1, (int)p.rows, RowLenIn{p.row_ptr, kSellTMax, kTileNnz},
+                          st);
+    void *tmp = nullptr;
+    SVDSB_CUDA(temps.get(&tmp, std::max(tb, tb2)));
+    // mid rows first (into sel), copied out, then the short rows
+    SVDSB_CUDA(cub::DeviceSelect::If(tmp, tb2, rows, sel, cnt + 1, (int)p.rows,
+                                     RowLenIn{p.row_ptr, kSellTMax, kTileNnz}, st));
+    int hc[2] = {0, 0};
+    SVDSB_CUDA(cudaMemcpyAsync(&hc[1], cnt + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SVDSB_CUDA(cudaStreamSynchronize(st));
+    nmid = hc[1];
+    if (nmid > 0) {
+      SVDSB_CUDA(palloc(&dmid, sizeof(int) * nmid, st));
+      SVDSB_CUDA(cudaMemcpyAsync(dmid, sel, sizeof(int) * nmid, cudaMemcpyDeviceToDevice, st));
+    }
+    SVDSB_CUDA(cub::DeviceSelect::If(tmp, tb, rows, sel, cnt, (int)p.rows, RowLenIn{p.row_ptr, -1, kSellTMax}, st));
+    SVDSB_CUDA(cudaMemcpyAsync(&hc[0], cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SVDSB_CUDA(cudaStreamSynchronize(st));
+    nq = hc[0];
+    const int64_t nsq = (nq + 31) / 32;
+    SVDSB_CUDA(palloc(&dperm, sizeof(int) * std::max<int64_t>(32 * nsq, 1) + kAllocPad, st));
+    SVDSB_CUDA(cudaMemsetAsync(dperm, 0, sizeof(int) * std::max<int64_t>(32 * nsq, 1), st));
+    if (nq > 0) {
+      SVDSB_CUDA(temps.get(&key, sizeof(unsigned) * nq));
+      SVDSB_CUDA(temps.get(&key_s, sizeof(unsigned) * nq));
+      SVDSB_CUDA(temps.get(&order, sizeof(int) * nq));
+      sell_keys_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(nq, sel, p.row_ptr, key);
+      SVDSB_LAUNCHED();
+      size_t tbs = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tbs, key, key_s, sel, dperm, (int)nq, 0, 7, st);
+      void *tmps = nullptr;
+      SVDSB_CUDA(temps.get(&tmps, tbs));
+      SVDSB_CUDA(cub::DeviceRadixSort::SortPairs(tmps, tbs, key, key_s, sel, dperm, (int)nq, 0, 7, st));
+      bump_launches();
+    }
+  }
+  const int64_t ns = (nq + 31) / 32;
+  int64_t *dsp = nullptr;
+  SVDSB_CUDA(palloc(&dsp, sizeof(int64_t) * (ns + 1) + kAllocPad, st));
+  sell_width_kernel<<<(unsigned)((ns + 256) / 256), 256, 0, st>>>(nq, ns, dperm, p.row_ptr, dsp);
+  SVDSB_LAUNCHED();
+  if (ns > 0) {
+    size_t tbw = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tbw, dsp + 1, dsp + 1, (int)ns, st);
+    void *tmpw = nullptr;
+    SVDSB_CUDA(temps.get(&tmpw, tbw));
+    SVDSB_CUDA(cub::DeviceScan::InclusiveSum(tmpw, tbw, dsp + 1, dsp + 1, (int)ns, st));
+    bump_launches();
+  }
+  int64_t total = 0;
+  SVDSB_CUDA(cudaMemcpyAsync(&total, dsp + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SVDSB_CUDA(cudaStreamSynchronize(st));
+  int *scol = nullptr;
+  double *sval = nullptr;
+  uint8_t *slen = nullptr;
+  if (alloc_pad(&scol, std::max<int64_t>(total, 1), st) != cudaSuccess ||
+      alloc_pad(&sval, std::max<int64_t>(total, 1), st) != cudaSuccess ||
+      alloc_pad(&slen, std::max<int64_t>(32 * ns, 32), st) != cudaSuccess ||
+      cudaMemsetAsync(slen, 0, std::max<int64_t>(32 * ns, 32), st) != cudaSuccess) {
+    pfree(dsp, st);
+    pfree(dperm, st);
+    pfree(dmid, st);
+    pfree(scol, st);
+    pfree(sval, st);
+    pfree(slen, st);
+    set_error("sliced-ELL allocation failed");
+    return SVDSB_ERR_ALLOC;
+  }
+  if (nq > 0) {
+    sell_fill_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(nq, dperm, p.row_ptr, p.col, p.val, dsp, scol,
+                                                                   sval, slen);
+    SVDSB_LAUNCHED();
+  }
+  p.nmid = nmid;
+  p.mid_rows = dmid;
+  p.nslice = ns;
+  p.nsell = nq;
+  p.sell_perm = dperm;
+  p.sell_ptr = dsp;
+  p.sell_col = scol;
+  p.sell_val = sval;
+  p.sell_len = slen;
+  return SVDSB_OK;
+}
+
 static bool capturing(cudaStream_t st) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
@@ -2039,7 +2172,8 @@ static bool ensure_sell(const CsrPart &cp, cudaStream_t st, bool sorted) {
   std::lock_guard<std::mutex> lk(g_sell_mu);
   CsrPart &p = const_cast<CsrPart &>(cp);  // cache fields only; the matrix itself is immutable
   if (p.sell_val || p.sell_failed) return p.sell_val != nullptr;
-  if (build_sell(p, st, sorted) != SVDSB_OK) {
+  const int rc = g_tune[10] == 1 ? build_sell(p, st, sorted) : build_sell_device(p, st, sorted);
+  if (rc != SVDSB_OK) {
     p.sell_failed = true;
     pfree(p.mid_rows, st);
     p.mid_rows = nullptr;

@@ -408,6 +408,31 @@ def test_spmv_transpose_long_rows_head_tiles(blocked, rng):
         assert np.array_equal(g[lens <= 64], want[lens <= 64])
 
 
+def test_sell_copies_device_build_matches_host(rng):
+    """The sliced-ELL copies built on the device (CUB select / stable radix
+    sort by length / scan; svdsb_tune_set key 10 = 0) and on the host (key
+    10 = 1) give the same products bit for bit, forward and transposed, on
+    ragged rows: short, mid (65-2048) and long rows, empty rows."""
+    from paper_1607_01404_b200 import _lib
+    m, n = 7000, 500
+    cols = np.concatenate([rng.integers(0, n, 30000), rng.integers(0, 30, 6000), np.full(2500, 400)])
+    cols[cols == 499] = 498
+    rows = np.concatenate([np.repeat(np.arange(m), 2), rng.integers(0, m, cols.size - 2 * m)])
+    vals = rng.standard_normal(cols.size)
+    x = rng.standard_normal((n, 4))
+    y = rng.standard_normal((m, 4))
+    out = {}
+    try:
+        for key in (1, 0):
+            _lib.call("svdsb_tune_set", 10, key)
+            a, _ = _csr(m, n, rows, cols, vals)           # a fresh matrix: copies built under this key
+            out[key] = (_spmv_dev(a, x, False), _spmv_dev(a, y, True))
+    finally:
+        _lib.call("svdsb_tune_set", 10, 0)
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+
+
 def test_spmv_bulk_copy_path_bit_exact(rng):
     """Matrices of >= 64 MB stream through the cp.async.bulk tile ring
     (csr_tile_bulk_kernel); it must reproduce the reference's summation
