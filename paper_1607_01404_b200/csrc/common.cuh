@@ -159,6 +159,9 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // shared memory tile by tile, csr_headtile4_kernel -- 3.2x slower on config
 // 4: ~470 small pieces per 2048-row tile, each a latency-bound reduction).
 // Key 10: sliced-ELL copies built on the device (0) or on the host (1).
+// Key 11: Ritz residuals with FMAs (0, ritz_wide / ritz_split) or on the
+// fp64 tensor cores (1, ritz_dmma_kernel: DMMA m8n8k4 with Y in registers;
+// slower on B200 -- config 3: 910 vs 639 us).
 constexpr int kTuneKeys = 12;
 inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 

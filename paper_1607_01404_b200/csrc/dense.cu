@@ -909,6 +909,130 @@ ritz_wide_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const d
   }
 }
 
+// Ritz residuals on the fp64 tensor cores (DMMA m8n8k4): X = V Y and
+// OpX = W Y are dense (N x g) x (g x p) contractions, so each warp takes 8
+// rows at a time and runs ceil(g/4) x NT DMMAs per operand with Y's
+// fragments held in registers for the whole kernel -- no shared-memory
+// coefficient traffic, which bounds the FMA kernels (ritz_wide reads every
+// coefficient from shared memory once per row).  The epilogue is the
+// reference's R = OpX - X*lam with two roundings (eigensolver.py:392), the
+// squared norms fold deterministically (lane shuffles, warps in order,
+// last-CTA fold).  DMMA accumulates in its own order, so R matches the FMA
+// kernels to rounding, not bit for bit.
+constexpr int kDmmaMaxK = 10;   // g <= 40
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads)
+ritz_dmma_kernel(int64_t dim, const double *__restrict__ v, int64_t ldv, const double *__restrict__ w, int64_t ldw,
+                 int g, const double *__restrict__ yc, int64_t ldyc, const double *__restrict__ lam, int p,
+                 double *__restrict__ r, int64_t ldr, double *__restrict__ xo, int64_t ldx, double *__restrict__ oxo,
+                 int64_t ldox, double *rn2, double *partials, unsigned int *ticket, StatusOut so) {
+  constexpr int PT = 8 * NT;
+  pdl_wait();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gi = lane >> 2, ti = lane & 3;          // fragment row / k (or column pair)
+  const int ks = (g + 3) >> 2;
+  // B fragments: Y[k = 4s + ti][j = 8t + gi]
+  double bf[kDmmaMaxK][NT];
+#pragma unroll
+  for (int s2 = 0; s2 < kDmmaMaxK; ++s2)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int k = 4 * s2 + ti, j = 8 * t + gi;
+      bf[s2][t] = (s2 < ks && k < g && j < p) ? yc[k + (int64_t)j * ldyc] : 0.0;
+    }
+  double lv[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = 8 * t + 2 * ti + e;
+      lv[t][e] = j < p ? lam[j] : 0.0;
+    }
+  double nacc[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) nacc[t][0] = nacc[t][1] = 0.0;
+  const int64_t ngroups = (dim + 7) >> 3;
+  const int64_t gstride = (int64_t)gridDim.x * (kThreads / 32);
+  for (int64_t grp = blockIdx.x * (int64_t)(kThreads / 32) + wid; grp < ngroups; grp += gstride) {
+    const int64_t r0 = grp << 3;
+    const int64_t ra = r0 + gi;                     // A-fragment row of this lane
+    const bool rok = ra < dim;
+    double av[kDmmaMaxK], aw[kDmmaMaxK];
+#pragma unroll
+    for (int s2 = 0; s2 < kDmmaMaxK; ++s2) {
+      const int k = 4 * s2 + ti;
+      const bool ok = rok && s2 < ks && k < g;
+      av[s2] = ok ? __ldg(v + ra + (int64_t)k * ldv) : 0.0;
+      aw[s2] = ok ? __ldg(w + ra + (int64_t)k * ldw) : 0.0;
+    }
+    double cx[NT][2], cw[NT][2];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) cx[t][0] = cx[t][1] = cw[t][0] = cw[t][1] = 0.0;
+#pragma unroll
+    for (int s2 = 0; s2 < kDmmaMaxK; ++s2) {
+      if (s2 < ks) {
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          dmma884(cx[t], av[s2], bf[s2][t]);
+          dmma884(cw[t], aw[s2], bf[s2][t]);
+        }
+      }
+    }
+    // C fragment: row r0 + gi, columns 8t + 2ti + e
+    const int64_t row = r0 + gi;
+    if (row < dim) {
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 8 * t + 2 * ti + e;
+          if (j < p) {
+            const double res = __dsub_rn(cw[t][e], __dmul_rn(cx[t][e], lv[t][e]));
+            r[row + (int64_t)j * ldr] = res;
+            if (xo) xo[row + (int64_t)j * ldx] = cx[t][e];
+            if (oxo) oxo[row + (int64_t)j * ldox] = cw[t][e];
+            nacc[t][e] = fma(res, res, nacc[t][e]);
+          }
+        }
+    }
+  }
+  pdl_trigger();
+  // lanes with equal ti hold the same columns: xor over the row bits
+  __shared__ double red[kThreads / 32][PT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double x = nacc[t][e];
+      x += __shfl_xor_sync(0xffffffffu, x, 4);
+      x += __shfl_xor_sync(0xffffffffu, x, 8);
+      x += __shfl_xor_sync(0xffffffffu, x, 16);
+      if (gi == 0) red[wid][8 * t + 2 * ti + e] = x;
+    }
+  __syncthreads();
+  double *pp = partials + (int64_t)blockIdx.x * PT;
+  for (int k = threadIdx.x; k < PT; k += kThreads) {
+    double x = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kThreads / 32; ++ww) x += red[ww][k];
+    pp[k] = x;
+  }
+  if (!last_cta(ticket)) return;
+  fold_parts(partials, gridDim.x, PT, p, [&](int j, int, int, double x) { rn2[j] = x; });
+  if (so.host != nullptr) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < so.gn + p + 8; i += blockDim.x)
+      so.host[i] = i < so.gn ? so.lams[i] : (i < so.gn + p ? rn2[i - so.gn] : so.st[i - so.gn - p]);
+    __threadfence_system();
+  }
+}
+
 // Ritz residuals with SPLIT threads per row, each owning PQ consecutive
 // candidates: the same per-element fma order as ritz_wide_kernel (basis
 // index ascending), so R is bit-identical; fewer accumulators per thread
@@ -1698,6 +1822,24 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
   if (p <= 0) return SVDSB_OK;
   SVDSB_CHECK_ARG(g >= 1 && g <= 256, "svdsb_ritz_residual: g out of range");
   cudaStream_t st = as_stream(stream);
+  if (g <= 4 * kDmmaMaxK && p <= 32 && g_tune[11] == 1) {
+    // fp64 tensor-core variant: measured slower than the FMA kernels at
+    // config-3 size (g = 35, p = 11: 910 vs 639 us, ~10 TFLOP/s of DMMA)
+    auto *tk = take_ticket(ctx);
+#define SVDSB_RITZ_DMMA(NT)                                                                                    \
+  SVDSB_LAUNCH_PDL(ritz_dmma_kernel<NT>, grid_for(ritz_dmma_kernel<NT>, dim, 0), kThreads, 0, st, dim, v, ldv, w,  \
+                   ldw, g, yc, ldyc, lam, p, r, ldr, x, ldx, ox, ldox, rn2, ctx->partials, tk, so)
+    if (p <= 8)
+      SVDSB_RITZ_DMMA(1);
+    else if (p <= 16)
+      SVDSB_RITZ_DMMA(2);
+    else if (p <= 24)
+      SVDSB_RITZ_DMMA(3);
+    else
+      SVDSB_RITZ_DMMA(4);
+#undef SVDSB_RITZ_DMMA
+    return SVDSB_OK;
+  }
   if (p > 16 && p <= 32 && g_tune[3] != 1) {
     // two threads per row, 12 or 16 candidates each (config 4, p = 24:
     // 336 -> 295 us; for p <= 16 the one-thread kernel is faster -- config

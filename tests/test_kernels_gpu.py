@@ -187,6 +187,45 @@ def test_ritz_residual_variants(p, rng):
         assert np.allclose(n2, (want ** 2).sum(0), rtol=1e-12)
 
 
+@pytest.mark.parametrize("g,p", [(35, 6), (35, 11), (26, 16), (35, 24), (40, 32), (5, 3)])
+def test_ritz_residual_dmma(g, p, rng):
+    """Ritz residuals of an HBM-scale basis (N >= 2^20 rows) on the fp64
+    tensor cores (DMMA m8n8k4, svdsb_tune_set key 11 = 1) against fp64
+    NumPy and the FMA kernels (key 11 = 0, the default): R to rounding (the tensor cores
+    accumulate in their own order), the squared norms, the x / W y outputs;
+    a row count that is not a multiple of the 8-row fragment."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    dim = (1 << 20) + 13
+    vh, wh = rng.standard_normal((dim, g)), rng.standard_normal((dim, g))
+    yh = np.linalg.qr(rng.standard_normal((g, g)))[0][:, :p]
+    lh = rng.standard_normal(p)
+    V, W, Y = dv.to_device_block(vh), dv.to_device_block(wh), dv.to_device_block(yh)
+    lam = torch.from_numpy(lh).to(ctx.device)
+    xw = vh @ yh
+    ow = wh @ yh
+    want = ow - xw * lh
+    outs = []
+    try:
+        for key in (1, 0):
+            _lib.call("svdsb_tune_set", 11, key)
+            R, X, OX = dv.new_block(dim, p), dv.new_block(dim, p), dv.new_block(dim, p)
+            rn2 = torch.zeros(p, dtype=torch.float64, device=ctx.device)
+            dv.ritz_residual(ctx, V, W, Y, lam, R, X, OX, rn2)
+            outs.append((dv.to_host(R), dv.to_host(X), dv.to_host(OX), rn2.cpu().numpy()))
+    finally:
+        _lib.call("svdsb_tune_set", 11, 0)
+    (r0, x0, o0, n0), (r1, x1, o1, n1) = outs
+    scale = np.abs(want).max()
+    assert np.abs(r0 - want).max() <= 1e-12 * scale
+    assert np.abs(r0 - r1).max() <= 1e-13 * scale
+    assert np.abs(x0 - xw).max() <= 1e-13 * np.abs(xw).max()
+    assert np.abs(o0 - ow).max() <= 1e-13 * np.abs(ow).max()
+    assert np.allclose(n0, (want ** 2).sum(0), rtol=1e-12)
+    assert np.allclose(n0, n1, rtol=1e-12)
+
+
 @pytest.mark.parametrize("variant", [0, 1])
 def test_spmv_transpose_b4_variants(variant, rng):
     """Transposed b = 4 products (svdsb_tune_set key 5: length-sorted sliced
