@@ -150,7 +150,10 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // the 4-column kernels, 1 the b-column CSR tile kernels).
 // Key 7: b = 4 sliced ELL (0 TMA-staged ring for the forward product,
 // csr_sell4s_kernel, rows <= 20 nonzeros; 1 the direct-load kernels both
-// ways; 2 the TMA-staged ring both ways, csr_sell4ts_kernel transposed).
+// ways; 2 the TMA-staged ring both ways, csr_sell4ts_kernel transposed;
+// 4 the forward ring staging only column ids and lengths, 4 slices deep,
+// values loaded with the gathers, csr_sell4sb_kernel: 810-825 us, the same
+// as key 0; 6 slices deep 950 us).
 // Key 8: transposed b = 4 rows of 65-2048 nonzeros (0 lane-parallel fma
 // sums + fixed xor tree, deterministic, within 1e-13 of the sequential sum;
 // 1 the serial left-to-right fold, bit-identical to np.add.at).

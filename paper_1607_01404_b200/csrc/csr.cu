@@ -950,7 +950,18 @@ constexpr int kS4Stage = 32 * kSell4sW * 12 + 32 + 96;   // vals + cols + lens, 
 static_assert(kS4Stage % 128 == 0, "stage alignment");
 constexpr size_t kS4Smem = (size_t)kS4Warps * 2 * kS4Stage;
 
-__device__ __forceinline__ void s4_fold(const double *__restrict__ sv, const int *__restrict__ sc, int lane, int len,
+// value sources of s4_fold: element k of this lane's row
+struct S4SmemVals {
+  const double *p;  // stage + lane
+  __device__ __forceinline__ double v(int k) const { return p[32 * k]; }
+};
+struct S4GlobalVals {
+  const double *p;  // sval + slice start + lane
+  __device__ __forceinline__ double v(int k) const { return ld_ef(p + 32 * k); }
+};
+
+template <typename VS>
+__device__ __forceinline__ void s4_fold(const VS sv, const int *__restrict__ sc, int lane, int len,
                                         const double *__restrict__ x, double (&out)[4]) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) out[c] = 0.0;
@@ -962,7 +973,7 @@ __device__ __forceinline__ void s4_fold(const double *__restrict__ sv, const int
     gather4(x, sc[lane], g0);
 #pragma unroll
     for (int u = 0; u < 8; ++u) gather4(x, sc[(n == 0 ? 0 : 1 + min(u, n - 1)) * 32 + lane], xg[u]);
-    const double v0 = sv[lane];
+    const double v0 = sv.v(0);
 #pragma unroll
     for (int c = 0; c < 4; ++c) p0[c] = dmul(v0, g0[c]);
   }
@@ -971,7 +982,7 @@ __device__ __forceinline__ void s4_fold(const double *__restrict__ sv, const int
 #pragma unroll
     for (int u = 0; u < 7; ++u)
       if (u < n) {
-        const double vu = sv[(1 + u) * 32 + lane];
+        const double vu = sv.v(1 + u);
 #pragma unroll
         for (int c = 0; c < 4; ++c) r[c] = dadd(r[c], dmul(vu, xg[u][c]));
       }
@@ -982,7 +993,7 @@ __device__ __forceinline__ void s4_fold(const double *__restrict__ sv, const int
   double acc[4][8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    const double vu = sv[(1 + u) * 32 + lane];
+    const double vu = sv.v(1 + u);
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[c][u] = dmul(vu, xg[u][c]);
   }
@@ -992,7 +1003,7 @@ __device__ __forceinline__ void s4_fold(const double *__restrict__ sv, const int
     for (int u = 0; u < 8; ++u) gather4(x, sc[(1 + b0 + u) * 32 + lane], xg[u]);
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const double vu = sv[(1 + b0 + u) * 32 + lane];
+      const double vu = sv.v(1 + b0 + u);
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[c][u] = dadd(acc[c][u], dmul(vu, xg[u][c]));
     }
@@ -1009,7 +1020,7 @@ __device__ __forceinline__ void s4_fold(const double *__restrict__ sv, const int
 #pragma unroll
     for (int u = 0; u < 7; ++u)
       if (nb + u < n) {
-        const double vu = sv[(1 + nb + u) * 32 + lane];
+        const double vu = sv.v(1 + nb + u);
 #pragma unroll
         for (int c = 0; c < 4; ++c) res[c] = dadd(res[c], dmul(vu, xg[u][c]));
       }
@@ -1070,7 +1081,7 @@ csr_sell4s_kernel(int64_t nrows, int64_t nslice, const int64_t *__restrict__ sel
     const int len = st[32 * kSell4sW * 12 + lane];
     const int64_t row = (sl << 5) + lane;
     double out[4];
-    s4_fold(sv, sc, lane, len, x, out);
+    s4_fold(S4SmemVals{sv + lane}, sc, lane, len, x, out);
     if (row < nrows) store_row4<YROW>(y, ldy, row, out);
     __syncwarp();
     if (lane == 0 && sl + 2 * nw < nslice) {
@@ -1082,6 +1093,86 @@ csr_sell4s_kernel(int64_t nrows, int64_t nslice, const int64_t *__restrict__ sel
       }
     }
     if (++k == 2) {
+      k = 0;
+      phase ^= 1u;
+    }
+  }
+  pdl_trigger();
+}
+
+// Variant of csr_sell4s_kernel (key 7 = 4): only the column ids and lengths
+// are staged, kS4bStages slices deep (a 2.7 KB stage instead of 7.8 KB);
+// the values are loaded from global memory together with the gathers
+// (independent loads, so their latency overlaps).
+#ifndef SVDSB_S4B_STAGES
+#define SVDSB_S4B_STAGES 4
+#endif
+constexpr int kS4bStages = SVDSB_S4B_STAGES;
+constexpr int kS4bStage = 32 * kSell4sW * 4 + 32 + 16 + 80;   // cols + lens + slice start, 128-B multiple
+static_assert(kS4bStage % 128 == 0, "stage alignment");
+constexpr size_t kS4bSmem = (size_t)kS4Warps * kS4bStages * kS4bStage;
+
+template <int YROW>
+__global__ void __launch_bounds__(kS4Warps * 32, 1)
+csr_sell4sb_kernel(int64_t nrows, int64_t nslice, const int64_t *__restrict__ sell_ptr, const int *__restrict__ scol,
+                   const double *__restrict__ sval, const uint8_t *__restrict__ slen, const double *__restrict__ x,
+                   double *__restrict__ y, int64_t ldy) {
+  extern __shared__ __align__(128) unsigned char s4b_smem[];
+  __shared__ __align__(8) uint64_t bar[kS4Warps][kS4bStages];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned char *ring = s4b_smem + (size_t)w * kS4bStages * kS4bStage;
+  const int64_t gw = (int64_t)blockIdx.x * kS4Warps + w, nw = (int64_t)gridDim.x * kS4Warps;
+  if (lane == 0) {
+    for (int k = 0; k < kS4bStages; ++k) mbar_init(&bar[w][k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint64_t policy = 0;
+  if (lane == 0) policy = evict_first_policy();
+  auto issue = [&](int64_t sl, int k, int64_t e0, int64_t e1) {
+    const int wd = (int)((e1 - e0) >> 5);
+    unsigned char *st = ring + (size_t)k * kS4bStage;
+    *reinterpret_cast<int64_t *>(st + 32 * kSell4sW * 4 + 32) = e0;   // seen after the mbarrier wait
+    mbar_expect_tx(&bar[w][k], 128u * wd + 32u);
+    if (wd > 0) bulk_g2s(st, scol + e0, 128u * wd, &bar[w][k], policy);
+    bulk_g2s(st + 32 * kSell4sW * 4, slen + 32 * sl, 32u, &bar[w][k], policy);
+  };
+  // pointers of the next slice to issue, loaded one issue ahead
+  int64_t pe0 = 0, pe1 = 0;
+  if (lane == 0) {
+    for (int k = 0; k < kS4bStages; ++k) {
+      const int64_t sl = gw + k * nw;
+      if (sl < nslice) issue(sl, k, __ldg(sell_ptr + sl), __ldg(sell_ptr + sl + 1));
+    }
+    if (gw + kS4bStages * nw < nslice) {
+      pe0 = __ldg(sell_ptr + gw + kS4bStages * nw);
+      pe1 = __ldg(sell_ptr + gw + kS4bStages * nw + 1);
+    }
+  }
+  pdl_wait();
+  int k = 0;
+  unsigned phase = 0;
+  for (int64_t sl = gw; sl < nslice; sl += nw) {
+    mbar_wait(&bar[w][k], phase);
+    const unsigned char *st = ring + (size_t)k * kS4bStage;
+    const int *sc = reinterpret_cast<const int *>(st);
+    const int len = st[32 * kSell4sW * 4 + lane];
+    const int64_t e0 = *reinterpret_cast<const int64_t *>(st + 32 * kSell4sW * 4 + 32);
+    const int64_t row = (sl << 5) + lane;
+    double out[4];
+    s4_fold(S4GlobalVals{sval + e0 + lane}, sc, lane, len, x, out);
+    if (row < nrows) store_row4<YROW>(y, ldy, row, out);
+    __syncwarp();
+    const int64_t nx = sl + kS4bStages * nw;
+    if (lane == 0 && nx < nslice) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(nx, k, pe0, pe1);
+      if (nx + nw < nslice) {
+        pe0 = __ldg(sell_ptr + nx + nw);
+        pe1 = __ldg(sell_ptr + nx + nw + 1);
+      }
+    }
+    if (++k == kS4bStages) {
       k = 0;
       phase ^= 1u;
     }
@@ -2338,6 +2429,19 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
         const int g = (int)std::min<int64_t>((p.nslice + 7) / 8, pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
         SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.rows, p.nslice, p.row_ptr, p.sell_ptr, p.sell_col, p.sell_val, x,
                          y, ldy);
+        return SVDSB_OK;
+      }
+      if (p.sell_val && p.sell_len && p.maxlen <= kSell4sW && g_tune[7] == 4) {
+        auto k = yrow ? csr_sell4sb_kernel<1> : csr_sell4sb_kernel<0>;
+        static bool attrb = false;
+        if (!attrb) {
+          cudaFuncSetAttribute(csr_sell4sb_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kS4bSmem);
+          cudaFuncSetAttribute(csr_sell4sb_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kS4bSmem);
+          attrb = true;
+        }
+        const int g = (int)std::min<int64_t>(num_sms(), (p.nslice + kS4Warps - 1) / kS4Warps);
+        SVDSB_LAUNCH_PDL(k, g, kS4Warps * 32, kS4bSmem, st, p.rows, p.nslice, p.sell_ptr, p.sell_col, p.sell_val,
+                         p.sell_len, x, y, ldy);
         return SVDSB_OK;
       }
       if (p.sell_val && p.sell_len && p.maxlen <= kSell4sW && g_tune[7] != 1) {
