@@ -2736,8 +2736,9 @@ __global__ void coo_keys_kernel(int64_t nt, int64_t m, int64_t n, const int64_t 
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nt) return;
   const int64_t ri = r[i], cj = c[i];
-  const bool ok = ri >= 0 && ri < m && cj >= 0 && cj < n;
-  if (!ok) atomicOr(bad, 1);
+  const bool rok = ri >= 0 && ri < m, cok = cj >= 0 && cj < n;
+  const bool ok = rok && cok;
+  if (!ok) atomicOr(bad, (rok ? 0 : 1) | (cok ? 0 : 2));
   key[i] = ok ? (unsigned long long)(ri * n + cj) : 0ull;
   idx[i] = (int)i;
 }
@@ -3048,8 +3049,8 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     SVDSB_CUDA(cudaMemcpyAsync(&last_first, first + nt - 1, 4, cudaMemcpyDeviceToHost, st));
     SVDSB_CUDA(cudaMemcpyAsync(&any_bad, bad, 4, cudaMemcpyDeviceToHost, st));
     SVDSB_CUDA(cudaStreamSynchronize(st));
-    if (any_bad) {
-      set_error("COO index out of range for a %lld x %lld matrix", (long long)m, (long long)n);
+    if (any_bad) {  // the reference's messages and order of checks (matio.py:74-78)
+      set_error((any_bad & 1) ? "row index out of range" : "column index out of range");
       return SVDSB_ERR_ARG;
     }
     nnz = (int64_t)last_seg + last_first;

@@ -205,14 +205,8 @@ class SparseMatrixCsr:
         rows = rows.to(device=ctx.device, dtype=torch.int64, non_blocking=True)
         cols = cols.to(device=ctx.device, dtype=torch.int64, non_blocking=True)
         values = values.to(device=ctx.device, dtype=torch.float64, non_blocking=True)
-        if rows.numel():
-            # range checks (matio.py:41-52) on the device copies: one
-            # read-back of four extremes instead of four host passes
-            ext = torch.stack([rows.min(), rows.max(), cols.min(), cols.max()]).cpu()
-            if int(ext[0]) < 0 or int(ext[1]) >= m:
-                raise ValueError("row index out of range")
-            if int(ext[2]) < 0 or int(ext[3]) >= n:
-                raise ValueError("column index out of range")
+        # the range checks of matio.py:74-78 run inside the device assembly
+        # (svdsb_csr_create_coo_device: same messages, ValueError)
         dev = DeviceCsr.from_coo_device(m, n, rows, cols, values, device=ctx.device)
         return cls._from_device(dev)
 
