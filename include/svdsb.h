@@ -53,7 +53,7 @@ int64_t svdsb_launch_count(void);
 /* Adds n to that counter: a CUDA-graph replay of n captured library kernels
  * is n launches the host no longer makes one by one. */
 int64_t svdsb_note_launches(int64_t n);
-/* Kernel-variant knob for measurement tools (key < 8; value 0 = default
+/* Kernel-variant knob for measurement tools (key < 15; value 0 = default
  * dispatch).  Not part of the reference interface. */
 int svdsb_tune_set(int key, int value);
 
@@ -108,6 +108,12 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n,
                                 int flags, void *stream, svdsb_csr **out);
 int svdsb_csr_destroy(svdsb_csr *a);
 int svdsb_csr_shape(const svdsb_csr *a, int64_t *m, int64_t *n, int64_t *nnz);
+/* Derived device layouts of a handle (tests / tools; not part of the
+ * reference interface).  key 0: slices of the forward sliced-ELL copy (0
+ * until a 2..4-column product built it); 1: operand rows the forward b = 4
+ * kernel keeps in shared memory (0: hot-column copy not built); 2: column
+ * blocks of the stored transpose. */
+int svdsb_csr_layout_info(const svdsb_csr *a, int key, int64_t *out);
 /* Copy CSR(A) (transpose = 0) or CSR(A^T) (transpose = 1) back to host in
  * the reference's int64/fp64 layout (bit-exactness checks).  Synchronous. */
 int svdsb_csr_export_host(const svdsb_csr *a, int transpose,

@@ -165,8 +165,18 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // Key 11: Ritz residuals with FMAs (0, ritz_wide / ritz_split) or on the
 // fp64 tensor cores (1, ritz_dmma_kernel: DMMA m8n8k4 with Y in registers;
 // slower on B200 -- config 3: 910 vs 639 us).
-constexpr int kTuneKeys = 12;
-inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+// Key 12: hot operand rows of the forward b = 4 ring kernel (0: every gather
+// from global memory; 1: the part's 1280 most referenced columns are read
+// from a shared-memory copy when they carry at least a fifth of the nonzeros
+// -- set before the first block product of a matrix; config 4: 992 vs 820 us,
+// L1-wavefront-bound either way, see csr_sell4s_kernel).
+// Key 13: running sums of the column-blocked A^T product of a packed block
+// (0: in the column-major result; 1: in a row-major scratch block unpacked
+// at the end -- 25 us slower on config 4).
+// Key 14: work items of csr_sell4t_kernel (0: handed out by a device
+// counter after each warp's first; 1: fixed stride).
+constexpr int kTuneKeys = 15;
+inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 
 #define SVDSB_LAUNCH_PDL(...)                                             \
   do {                                                                    \

@@ -69,6 +69,12 @@ struct CsrPart {
   double *sell_val = nullptr;
   uint8_t *sell_len = nullptr;  // forward copy: row length of each sliced position (0 past the end)
   bool sell_failed = false;     // the copy could not be built: CSR kernels (same bits)
+  // hot-encoded column ids of the forward copy (csr_sell4s_kernel<.., 1>):
+  // ~slot for the sell_nhot most referenced columns (listed in sell_hot)
+  int *sell_colh = nullptr;
+  int *sell_hot = nullptr;
+  int sell_nhot = 0;
+  unsigned *work_ctr = nullptr; // transpose parts: {next work item, warps done} of csr_sell4t_kernel
   // head tiles of the long rows (b = 4 transposed products, built on first
   // use): pieces of <= kHeadPiece nonzeros of one long row inside one
   // kHeadTile-row tile of the operand, listed tile by tile
@@ -949,6 +955,9 @@ constexpr int kS4Warps = 12;                  // warps per CTA (1 CTA / SM)
 constexpr int kS4Stage = 32 * kSell4sW * 12 + 32 + 96;   // vals + cols + lens, padded to 128 B
 static_assert(kS4Stage % 128 == 0, "stage alignment");
 constexpr size_t kS4Smem = (size_t)kS4Warps * 2 * kS4Stage;
+constexpr int kS4Hot = 1280;                  // operand rows kept in shared memory (hot variant)
+constexpr size_t kS4HotBytes = (size_t)kS4Hot * 32;
+static_assert(kS4Smem + kS4HotBytes + 256 <= 232448, "hot rows + ring exceed the 227 KB of a CTA");
 
 // value sources of s4_fold: element k of this lane's row
 struct S4SmemVals {
@@ -960,9 +969,34 @@ struct S4GlobalVals {
   __device__ __forceinline__ double v(int k) const { return ld_ef(p + 32 * k); }
 };
 
-template <typename VS>
+// gather sources of s4_fold: the operand row of column id c
+struct S4GlobalX {
+  const double *x;
+  __device__ __forceinline__ void load(int c, double (&o)[4]) const { gather4(x, c, o); }
+};
+// hot rows (ids < 0: ~slot) from the CTA's shared copy, the rest from global
+// memory: a warp-wide gather of 32 scattered rows costs the L1 one wavefront
+// per distinct 128-byte line, a shared-memory read 8 per 32 rows
+struct S4HotX {
+  const double *x;
+  const double *xs;   // kS4Hot x 4 doubles in shared memory
+  __device__ __forceinline__ void load(int c, double (&o)[4]) const {
+    if (c < 0) {
+      const double2 a = *reinterpret_cast<const double2 *>(xs + 4 * (~c));
+      const double2 b = *reinterpret_cast<const double2 *>(xs + 4 * (~c) + 2);
+      o[0] = a.x;
+      o[1] = a.y;
+      o[2] = b.x;
+      o[3] = b.y;
+    } else {
+      gather4(x, c, o);
+    }
+  }
+};
+
+template <typename VS, typename GX>
 __device__ __forceinline__ void s4_fold(const VS sv, const int *__restrict__ sc, int lane, int len,
-                                        const double *__restrict__ x, double (&out)[4]) {
+                                        const GX x, double (&out)[4]) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) out[c] = 0.0;
   if (len == 0) return;
@@ -970,9 +1004,9 @@ __device__ __forceinline__ void s4_fold(const VS sv, const int *__restrict__ sc,
   double p0[4], xg[8][4];
   {
     double g0[4];
-    gather4(x, sc[lane], g0);
+    x.load(sc[lane], g0);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) gather4(x, sc[(n == 0 ? 0 : 1 + min(u, n - 1)) * 32 + lane], xg[u]);
+    for (int u = 0; u < 8; ++u) x.load(sc[(n == 0 ? 0 : 1 + min(u, n - 1)) * 32 + lane], xg[u]);
     const double v0 = sv.v(0);
 #pragma unroll
     for (int c = 0; c < 4; ++c) p0[c] = dmul(v0, g0[c]);
@@ -1000,7 +1034,7 @@ __device__ __forceinline__ void s4_fold(const VS sv, const int *__restrict__ sc,
   const int nb = n - (n % 8);
   for (int b0 = 8; b0 < nb; b0 += 8) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) gather4(x, sc[(1 + b0 + u) * 32 + lane], xg[u]);
+    for (int u = 0; u < 8; ++u) x.load(sc[(1 + b0 + u) * 32 + lane], xg[u]);
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const double vu = sv.v(1 + b0 + u);
@@ -1016,7 +1050,7 @@ __device__ __forceinline__ void s4_fold(const VS sv, const int *__restrict__ sc,
   }
   if (nb < n) {
 #pragma unroll
-    for (int u = 0; u < 7; ++u) gather4(x, sc[(1 + nb + min(u, n - nb - 1)) * 32 + lane], xg[u]);
+    for (int u = 0; u < 7; ++u) x.load(sc[(1 + nb + min(u, n - nb - 1)) * 32 + lane], xg[u]);
 #pragma unroll
     for (int u = 0; u < 7; ++u)
       if (nb + u < n) {
@@ -1029,15 +1063,26 @@ __device__ __forceinline__ void s4_fold(const VS sv, const int *__restrict__ sc,
   for (int c = 0; c < 4; ++c) out[c] = dadd(p0[c], res[c]);
 }
 
-template <int YROW>
+// HOT = 1: the column ids are the hot-encoded copy (sell_colh: ~slot for
+// the part's kS4Hot most referenced columns) and the CTA first copies those
+// operand rows into shared memory.  Config 4's Zipf columns: 1280 rows
+// serve two thirds of the gathers.  Same values, same fold: bit-identical.
+// Measured SLOWER on config 4 (992 vs 820 us): the kernel is bound by L1
+// wavefronts (one per distinct 128-byte line of a gather), config 4's hot
+// columns are adjacent ids that already share lines, and the two LDS.128 of
+// a hot row cost as many wavefronts as they save while the larger carve-out
+// shrinks L1.  Opt-in (svdsb_tune_set key 12 = 1) for matrices whose hot
+// columns are scattered.
+template <int YROW, int HOT>
 __global__ void __launch_bounds__(kS4Warps * 32, 1)
 csr_sell4s_kernel(int64_t nrows, int64_t nslice, const int64_t *__restrict__ sell_ptr, const int *__restrict__ scol,
                   const double *__restrict__ sval, const uint8_t *__restrict__ slen, const double *__restrict__ x,
-                  double *__restrict__ y, int64_t ldy) {
+                  double *__restrict__ y, int64_t ldy, const int *__restrict__ hot_cols, int nhot) {
   extern __shared__ __align__(128) unsigned char s4_smem[];
   __shared__ __align__(8) uint64_t bar[kS4Warps][2];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned char *ring = s4_smem + (size_t)w * 2 * kS4Stage;
+  unsigned char *ring = s4_smem + (HOT ? kS4HotBytes : 0) + (size_t)w * 2 * kS4Stage;
+  double *xs = reinterpret_cast<double *>(s4_smem);
   const int64_t gw = (int64_t)blockIdx.x * kS4Warps + w, nw = (int64_t)gridDim.x * kS4Warps;
   if (lane == 0) {
     mbar_init(&bar[w][0], 1);
@@ -1071,6 +1116,15 @@ csr_sell4s_kernel(int64_t nrows, int64_t nslice, const int64_t *__restrict__ sel
     }
   }
   pdl_wait();
+  if (HOT) {
+    for (int s = threadIdx.x; s < nhot; s += kS4Warps * 32) {
+      double r[4];
+      gather4(x, __ldg(hot_cols + s), r);
+      *reinterpret_cast<double2 *>(xs + 4 * s) = make_double2(r[0], r[1]);
+      *reinterpret_cast<double2 *>(xs + 4 * s + 2) = make_double2(r[2], r[3]);
+    }
+    __syncthreads();
+  }
   int k = 0;
   unsigned phase = 0;
   for (int64_t sl = gw; sl < nslice; sl += nw) {
@@ -1081,7 +1135,10 @@ csr_sell4s_kernel(int64_t nrows, int64_t nslice, const int64_t *__restrict__ sel
     const int len = st[32 * kSell4sW * 12 + lane];
     const int64_t row = (sl << 5) + lane;
     double out[4];
-    s4_fold(S4SmemVals{sv + lane}, sc, lane, len, x, out);
+    if (HOT)
+      s4_fold(S4SmemVals{sv + lane}, sc, lane, len, S4HotX{x, xs}, out);
+    else
+      s4_fold(S4SmemVals{sv + lane}, sc, lane, len, S4GlobalX{x}, out);
     if (row < nrows) store_row4<YROW>(y, ldy, row, out);
     __syncwarp();
     if (lane == 0 && sl + 2 * nw < nslice) {
@@ -1160,7 +1217,7 @@ csr_sell4sb_kernel(int64_t nrows, int64_t nslice, const int64_t *__restrict__ se
     const int64_t e0 = *reinterpret_cast<const int64_t *>(st + 32 * kSell4sW * 4 + 32);
     const int64_t row = (sl << 5) + lane;
     double out[4];
-    s4_fold(S4GlobalVals{sval + e0 + lane}, sc, lane, len, x, out);
+    s4_fold(S4GlobalVals{sval + e0 + lane}, sc, lane, len, S4GlobalX{x}, out);
     if (row < nrows) store_row4<YROW>(y, ldy, row, out);
     __syncwarp();
     const int64_t nx = sl + kS4bStages * nw;
@@ -1341,52 +1398,77 @@ __device__ __forceinline__ void warprow4t(int64_t row, const int *__restrict__ r
 template <int YROW>
 __global__ void __launch_bounds__(kTileThreads, SVDSB_T4T_MINB)
 csr_sell4t_kernel(int64_t nq, int64_t nslice, const int *__restrict__ perm, const int *__restrict__ row_ptr,
-                  const int64_t *__restrict__ sell_ptr, const int *__restrict__ scol, const double *__restrict__ sval,
-                  int nmid, const int *__restrict__ mid, const int *__restrict__ col, const double *__restrict__ val,
-                  const double *__restrict__ x, double *__restrict__ y, int64_t ldy, int acc, int g_t4exact) {
+                  const uint8_t *__restrict__ slen, const int64_t *__restrict__ sell_ptr,
+                  const int *__restrict__ scol, const double *__restrict__ sval, int nmid,
+                  const int *__restrict__ mid, const int *__restrict__ col, const double *__restrict__ val,
+                  const double *__restrict__ x, double *__restrict__ y, int64_t ldy, int acc, int g_t4exact,
+                  unsigned *__restrict__ ctr) {
   __shared__ double prod[kTileThreads / 32][4][32 * kWR4 + 1];
   const int lane = threadIdx.x & 31;
-  const int64_t wstride = (int64_t)gridDim.x * (kTileThreads / 32);
+  const unsigned nwarps = gridDim.x * (kTileThreads / 32);
+  const unsigned nitems = (unsigned)(nmid + nslice);
   pdl_wait();
-  // warp work items: the mid rows first (longest work), then the slices
-  for (int64_t it = blockIdx.x * (int64_t)(kTileThreads / 32) + (threadIdx.x >> 5); it < nmid + nslice;
-       it += wstride) {
-    if (it < nmid) {
+  // Warp work items: the mid rows first (longest work), then the slices.
+  // A warp's first item is its own index; the rest come from a counter
+  // (ctr[0]; fetched one item ahead so the atomic's round trip hides behind
+  // the current item), so a warp that drew long mid rows (65-2048 nonzeros)
+  // takes fewer items (config 4: 1370 -> 1360 us per product; the kernel is
+  // bound by L1 wavefronts, not by the tail).  Each item is owned by exactly
+  // one warp and writes its own rows, so the assignment does not touch the
+  // sums.  ctr == nullptr keeps the fixed stride.
+  unsigned it = blockIdx.x * (kTileThreads / 32) + (threadIdx.x >> 5);
+  while (it < nitems) {
+    unsigned nxt = it + nwarps;
+    if (ctr != nullptr && lane == 0) nxt = nwarps + atomicAdd(ctr, 1u);
+    if (it < (unsigned)nmid) {
 #if SVDSB_DBG_SKIP != 1
       warprow4t(__ldg(mid + it), row_ptr, col, val, x, y, ldy, YROW, acc, prod[threadIdx.x >> 5], g_t4exact);
 #endif
-      continue;
-    }
-#if SVDSB_DBG_SKIP == 2
-    continue;
-#endif
-    const int64_t sl = it - nmid;
-    const int64_t q = (sl << 5) + lane;
-    if (q >= nq) continue;
-    const int64_t row = __ldg(perm + q);
-    const int len = __ldg(row_ptr + row + 1) - __ldg(row_ptr + row);
-    const int64_t base = __ldg(sell_ptr + sl) + lane;
-    double s[4] = {0.0, 0.0, 0.0, 0.0};
-    if (acc) {
+    } else {
+#if SVDSB_DBG_SKIP != 2
+      const int64_t sl = (int64_t)it - nmid;
+      const int64_t q = (sl << 5) + lane;
+      // the stored length of this sliced position (one coalesced byte load;
+      // row_ptr[perm[q]] was two scattered ones).  An empty row of an
+      // accumulating block keeps its running sum: nothing to read or write.
+      const int len = q < nq ? (int)__ldg(slen + q) : 0;
+      if (q < nq && !(acc && len == 0)) {
+        const int64_t row = __ldg(perm + q);
+        const int64_t base = __ldg(sell_ptr + sl) + lane;
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
+        if (acc) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) s[c] = YROW ? y[row * 4 + c] : y[row + c * ldy];
-    }
-    for (int j0 = 0; j0 < len; j0 += 4) {
-      double xv[4][4], vv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = min(j0 + u, len - 1);
-        vv[u] = ld_ef(sval + base + 32 * (int64_t)j);
-        gather4(x, ld_ef(scol + base + 32 * (int64_t)j), xv[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (j0 + u < len) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) s[c] = dadd(s[c], dmul(vv[u], xv[u][c]));
+          for (int c = 0; c < 4; ++c) s[c] = YROW ? y[row * 4 + c] : y[row + c * ldy];
         }
+        for (int j0 = 0; j0 < len; j0 += 4) {
+          double xv[4][4], vv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = min(j0 + u, len - 1);
+            vv[u] = ld_ef(sval + base + 32 * (int64_t)j);
+            gather4(x, ld_ef(scol + base + 32 * (int64_t)j), xv[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (j0 + u < len) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) s[c] = dadd(s[c], dmul(vv[u], xv[u][c]));
+            }
+        }
+        store_row4<YROW>(y, ldy, row, s);
+      }
+#endif
     }
-    store_row4<YROW>(y, ldy, row, s);
+    it = ctr != nullptr ? __shfl_sync(0xffffffffu, nxt, 0) : nxt;
+  }
+  // the last warp out rearms the counter for the next launch on this part
+  if (ctr != nullptr && lane == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1u) == nwarps - 1) {
+      ctr[0] = 0u;
+      ctr[1] = 0u;
+      __threadfence();
+    }
   }
   pdl_trigger();
 }
@@ -2043,6 +2125,9 @@ static void free_part(CsrPart &p) {
   pfree(p.sell_perm, nullptr);
   pfree(p.mid_rows, nullptr);
   pfree(p.sell_col, nullptr);
+  pfree(p.sell_colh, nullptr);
+  pfree(p.sell_hot, nullptr);
+  pfree(p.work_ctr, nullptr);
   pfree(p.sell_val, nullptr);
   pfree(p.sell_len, nullptr);
   pfree(p.htp, nullptr);
@@ -2247,6 +2332,84 @@ static int build_sell_device(CsrPart &p, cudaStream_t st, bool sorted) {
   return SVDSB_OK;
 }
 
+// Hot-encoded column ids for the forward ring kernel: the kS4Hot columns
+// with the most nonzeros (stable descending radix sort of the column
+// counts, ties by ascending id) get slots 0..; an entry of a hot column
+// stores ~slot.  Skipped (sell_nhot = 0) when those columns carry less than
+// a fifth of the nonzeros or the matrix is small.
+__global__ void iota_kernel(int64_t n, int *__restrict__ out);
+
+__global__ void count_agg_kernel(int64_t nnz, const int *__restrict__ keys, int *__restrict__ counts) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  const int c = keys[i];
+  const unsigned peers = __match_any_sync(__activemask(), c);
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + c, __popc(peers));
+}
+
+__global__ void hot_slot_kernel(int nhot, const int *__restrict__ hot, int *__restrict__ slot) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nhot) slot[hot[s]] = s;
+}
+
+__global__ void hot_encode_kernel(int64_t n, const int *__restrict__ scol, const int *__restrict__ slot,
+                                  int *__restrict__ colh) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = scol[e];
+    const int s = slot[c];
+    colh[e] = s >= 0 ? ~s : c;
+  }
+}
+
+static int build_sell_hot(CsrPart &p, cudaStream_t st) {
+  if (p.cols <= 4 * kS4Hot || p.nnz < 32 * kS4Hot || !p.sell_col) return SVDSB_OK;
+  StreamTemps temps{st, {}};
+  int *cnt = nullptr, *cnt_s = nullptr, *ids = nullptr, *ids_s = nullptr, *slot = nullptr;
+  SVDSB_CUDA(temps.get(&cnt, sizeof(int) * p.cols));
+  SVDSB_CUDA(temps.get(&cnt_s, sizeof(int) * p.cols));
+  SVDSB_CUDA(temps.get(&ids, sizeof(int) * p.cols));
+  SVDSB_CUDA(temps.get(&ids_s, sizeof(int) * p.cols));
+  SVDSB_CUDA(temps.get(&slot, sizeof(int) * p.cols));
+  SVDSB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * p.cols, st));
+  SVDSB_CUDA(cudaMemsetAsync(slot, 0xff, sizeof(int) * p.cols, st));
+  count_agg_kernel<<<(unsigned)((p.nnz + 255) / 256), 256, 0, st>>>(p.nnz, p.col, cnt);
+  SVDSB_LAUNCHED();
+  iota_kernel<<<(unsigned)((p.cols + 255) / 256), 256, 0, st>>>(p.cols, ids);
+  SVDSB_LAUNCHED();
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt, cnt_s, ids, ids_s, (int)p.cols, 0, 32, st);
+  void *tmp = nullptr;
+  SVDSB_CUDA(temps.get(&tmp, tb));
+  SVDSB_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, cnt, cnt_s, ids, ids_s, (int)p.cols, 0, 32, st));
+  bump_launches();
+  std::vector<int> top(kS4Hot);
+  int64_t total = 0;
+  SVDSB_CUDA(cudaMemcpyAsync(top.data(), cnt_s, sizeof(int) * kS4Hot, cudaMemcpyDeviceToHost, st));
+  SVDSB_CUDA(cudaMemcpyAsync(&total, p.sell_ptr + p.nslice, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SVDSB_CUDA(cudaStreamSynchronize(st));
+  int64_t covered = 0;
+  for (int c : top) covered += c;
+  if (5 * covered < p.nnz || total <= 0) return SVDSB_OK;
+  int *hot = nullptr, *colh = nullptr;
+  if (palloc(&hot, sizeof(int) * kS4Hot, st) != cudaSuccess || alloc_pad(&colh, total, st) != cudaSuccess) {
+    pfree(hot, st);
+    pfree(colh, st);
+    cudaGetLastError();
+    return SVDSB_OK;   // no room for the copy: the plain ring kernel gives the same bits
+  }
+  SVDSB_CUDA(cudaMemcpyAsync(hot, ids_s, sizeof(int) * kS4Hot, cudaMemcpyDeviceToDevice, st));
+  hot_slot_kernel<<<(kS4Hot + 255) / 256, 256, 0, st>>>(kS4Hot, hot, slot);
+  SVDSB_LAUNCHED();
+  hot_encode_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 32 * num_sms()), 256, 0, st>>>(
+      total, p.sell_col, slot, colh);
+  SVDSB_LAUNCHED();
+  SVDSB_CUDA(cudaStreamSynchronize(st));   // the temporaries are released on return
+  p.sell_hot = hot;
+  p.sell_colh = colh;
+  p.sell_nhot = kS4Hot;
+  return SVDSB_OK;
+}
+
 static bool capturing(cudaStream_t st) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
@@ -2272,6 +2435,18 @@ static bool ensure_sell(const CsrPart &cp, cudaStream_t st, bool sorted) {
     cudaGetLastError();
     set_error("");
     return false;
+  }
+  if (sorted && !p.work_ctr) {
+    if (palloc(&p.work_ctr, 2 * sizeof(unsigned), st) == cudaSuccess) {
+      cudaMemsetAsync(p.work_ctr, 0, 2 * sizeof(unsigned), st);
+    } else {
+      p.work_ctr = nullptr;   // fixed-stride assignment
+      cudaGetLastError();
+    }
+  }
+  if (!sorted && p.sell_len && p.maxlen <= kSell4sW && g_tune[12] == 1 && build_sell_hot(p, st) != SVDSB_OK) {
+    cudaGetLastError();   // the hot copy is optional
+    set_error("");
   }
   return true;
 }
@@ -2445,16 +2620,26 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
         return SVDSB_OK;
       }
       if (p.sell_val && p.sell_len && p.maxlen <= kSell4sW && g_tune[7] != 1) {
-        auto k = yrow ? csr_sell4s_kernel<1> : csr_sell4s_kernel<0>;
         static bool attr = false;
         if (!attr) {
-          cudaFuncSetAttribute(csr_sell4s_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kS4Smem);
-          cudaFuncSetAttribute(csr_sell4s_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kS4Smem);
+          cudaFuncSetAttribute(csr_sell4s_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kS4Smem);
+          cudaFuncSetAttribute(csr_sell4s_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kS4Smem);
+          cudaFuncSetAttribute(csr_sell4s_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(kS4Smem + kS4HotBytes));
+          cudaFuncSetAttribute(csr_sell4s_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(kS4Smem + kS4HotBytes));
           attr = true;
         }
         const int g = (int)std::min<int64_t>(num_sms(), (p.nslice + kS4Warps - 1) / kS4Warps);
+        if (p.sell_colh && g_tune[12] == 1) {
+          auto k = yrow ? csr_sell4s_kernel<1, 1> : csr_sell4s_kernel<0, 1>;
+          SVDSB_LAUNCH_PDL(k, g, kS4Warps * 32, kS4Smem + kS4HotBytes, st, p.rows, p.nslice, p.sell_ptr, p.sell_colh,
+                           p.sell_val, p.sell_len, x, y, ldy, (const int *)p.sell_hot, p.sell_nhot);
+          return SVDSB_OK;
+        }
+        auto k = yrow ? csr_sell4s_kernel<1, 0> : csr_sell4s_kernel<0, 0>;
         SVDSB_LAUNCH_PDL(k, g, kS4Warps * 32, kS4Smem, st, p.rows, p.nslice, p.sell_ptr, p.sell_col, p.sell_val,
-                         p.sell_len, x, y, ldy);
+                         p.sell_len, x, y, ldy, (const int *)nullptr, 0);
         return SVDSB_OK;
       }
       if (p.sell_val && !p.sell_perm) {
@@ -2498,8 +2683,9 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
         if (p.nmid > 0) {  // mid rows: one warp per row (csr_sell4t_kernel with no slices)
           auto k = yrow ? csr_sell4t_kernel<1> : csr_sell4t_kernel<0>;
           const int g = (int)std::min<int64_t>((p.nmid + 7) / 8, pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
-          SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.nsell, (int64_t)0, p.sell_perm, p.row_ptr, p.sell_ptr,
-                           p.sell_col, p.sell_val, p.nmid, p.mid_rows, p.col, p.val, x, y, ldy, acc, g_tune[8] == 1);
+          SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.nsell, (int64_t)0, p.sell_perm, p.row_ptr,
+                           (const uint8_t *)p.sell_len, p.sell_ptr, p.sell_col, p.sell_val, p.nmid, p.mid_rows, p.col,
+                           p.val, x, y, ldy, acc, g_tune[8] == 1, g_tune[14] == 1 ? (unsigned *)nullptr : p.work_ctr);
         }
         if (p.nslice > 0) {
           auto k = yrow ? csr_sell4ts_kernel<1> : csr_sell4ts_kernel<0>;
@@ -2514,13 +2700,14 @@ static int part_matvec(const CsrPart &p, const double *x, int64_t ldx, int xrow,
                            p.sell_col, p.sell_val, x, y, ldy, acc);
         }
         short_done = true;
-      } else if (p.sell_val && p.sell_perm) {
+      } else if (p.sell_val && p.sell_perm && p.sell_len) {
         if (p.nslice + p.nmid > 0) {
           auto k = yrow ? csr_sell4t_kernel<1> : csr_sell4t_kernel<0>;
           const int g = (int)std::min<int64_t>((p.nslice + p.nmid + 7) / 8,
                                                pipe_rows_grid(reinterpret_cast<const void *>(k), 0));
-          SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.nsell, p.nslice, p.sell_perm, p.row_ptr, p.sell_ptr, p.sell_col,
-                           p.sell_val, p.nmid, p.mid_rows, p.col, p.val, x, y, ldy, acc, g_tune[8] == 1);
+          SVDSB_LAUNCH_PDL(k, g, kTileThreads, 0, st, p.nsell, p.nslice, p.sell_perm, p.row_ptr,
+                           (const uint8_t *)p.sell_len, p.sell_ptr, p.sell_col, p.sell_val, p.nmid, p.mid_rows, p.col,
+                           p.val, x, y, ldy, acc, g_tune[8] == 1, g_tune[14] == 1 ? (unsigned *)nullptr : p.work_ctr);
         }
         short_done = true;
       }
@@ -2794,6 +2981,17 @@ int svdsb_csr_shape(const svdsb_csr *a, int64_t *m, int64_t *n, int64_t *nnz) {
   if (m) *m = a->a.rows;
   if (n) *n = a->a.cols;
   if (nnz) *nnz = a->a.nnz;
+  return SVDSB_OK;
+}
+
+int svdsb_csr_layout_info(const svdsb_csr *a, int key, int64_t *out) {
+  SVDSB_CHECK_ARG(a != nullptr && out != nullptr, "svdsb_csr_layout_info: NULL argument");
+  switch (key) {
+    case 0: *out = a->a.sell_val ? a->a.nslice : 0; break;
+    case 1: *out = a->a.sell_colh ? a->a.sell_nhot : 0; break;
+    case 2: *out = (int64_t)a->atb.size(); break;
+    default: set_error("svdsb_csr_layout_info: unknown key %d", key); return SVDSB_ERR_ARG;
+  }
   return SVDSB_OK;
 }
 
@@ -3138,6 +3336,35 @@ static int pack(const double *x, int64_t rows, int64_t ldx, int b, double *xr, c
 
 static inline bool packed_block(int b) { return b >= 2 && b <= 4; }
 
+static int unpack(const double *xr, int64_t rows, int b, double *y, int64_t ldy, cudaStream_t st) {
+  const int64_t tot = rows * b;
+  if (tot == 0) return SVDSB_OK;
+  unpack_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(rows, b, xr, y, ldy);
+  SVDSB_LAUNCHED();
+  return SVDSB_OK;
+}
+
+// Column-blocked A^T product of a packed (row-major) operand into a
+// column-major result.  svdsb_tune_set key 13 = 1 keeps the running sums of
+// the blocks in a row-major scratch block (one 32-byte access per row and
+// block instead of four scattered 8-byte ones) and unpacks once at the end:
+// measured 25 us SLOWER on config 4 (1362 vs 1337 us per product) -- the
+// kernels are bound by the gathers' L1 wavefronts (one per nonzero), the
+// read-modify-write is a few percent of them and the unpack costs more than
+// it saves.  Same sums in the same order either way, bit-identical.
+static int blocked_adj_packed(const svdsb_csr *a, const double *xr, int b, double *y, int64_t ldy,
+                              cudaStream_t st) {
+  if (g_tune[13] != 1) return blocked_adj<1>(a, xr, b, y, ldy, 0, b, st);
+  double *yr = scratch_get(a, 2, (size_t)a->at.rows * b);
+  if (!yr) {
+    set_error("blocked A^T product: scratch allocation failed");
+    return SVDSB_ERR_ALLOC;
+  }
+  int rc = blocked_adj<1>(a, xr, b, yr, b, 1, b, st);
+  if (rc) return rc;
+  return unpack(yr, a->at.rows, b, y, ldy, st);
+}
+
 static int pack_pad(const double *x, int64_t rows, int64_t ldx, int b, int bp, double *xr, cudaStream_t st) {
   const int64_t tot = rows * bp;
   if (tot == 0) return SVDSB_OK;
@@ -3219,7 +3446,7 @@ int svdsb_matvec(svdsb_ctx *ctx, const svdsb_csr *a, int transpose, const double
     }
     int rc = pack(x, p.cols, ldx, block, xr, st);
     if (rc) return rc;
-    if (transpose && !a->atb.empty()) return blocked_adj<1>(a, xr, block, y, ldy, 0, block, st);
+    if (transpose && !a->atb.empty()) return blocked_adj_packed(a, xr, block, y, ldy, st);
     return transpose ? part_matvec<1>(p, xr, block, 1, y, ldy, 0, block, st)
                      : part_matvec<0>(p, xr, block, 1, y, ldy, 0, block, st);
   }
@@ -3278,7 +3505,7 @@ int svdsb_apply_normal(svdsb_ctx *ctx, const svdsb_csr *a, int side, const doubl
     rc = side == 0 ? part_matvec<0>(first, xr, block, 1, tr, block, 1, block, st)
                    : part_matvec<1>(first, xr, block, 1, tr, block, 1, block, st);
     if (rc) return rc;
-    if (side == 0 && !a->atb.empty()) return blocked_adj<1>(a, tr, block, y, ldy, 0, block, st);
+    if (side == 0 && !a->atb.empty()) return blocked_adj_packed(a, tr, block, y, ldy, st);
     return side == 0 ? part_matvec<1>(second, tr, block, 1, y, ldy, 0, block, st)
                      : part_matvec<0>(second, tr, block, 1, y, ldy, 0, block, st);
   }

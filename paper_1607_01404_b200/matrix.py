@@ -68,6 +68,12 @@ class DeviceCsr:
         _lib.call("svdsb_csr_shape", h, None, None, ctypes.byref(nnz))
         return cls(h, ctx, m, n, nnz.value)
 
+    def layout_info(self, key):
+        """Derived-layout counters (svdsb_csr_layout_info; tests and tools)."""
+        out = ctypes.c_int64()
+        _lib.call("svdsb_csr_layout_info", self.handle, int(key), ctypes.byref(out))
+        return out.value
+
     def export(self, transpose=False):
         """(row_ptr, col_idx, values) of A (or A^T) in the reference layout."""
         rows = self.n if transpose else self.m

@@ -288,6 +288,44 @@ def test_spmv_forward_b4_tma_ring_bit_exact(m, rng):
         assert np.array_equal(got[key], want), key
 
 
+@pytest.mark.parametrize("m", [33, 70_001])
+def test_spmv_forward_b4_hot_rows_bit_exact(m, rng):
+    """The forward b = 4 ring kernel with the part's 1280 most referenced
+    columns read from a shared-memory copy of their operand rows
+    (svdsb_tune_set key 12 = 1; built when those columns carry at least a
+    fifth of the nonzeros) against the all-global kernel (key 12 = 0) and
+    the oracle, bit for bit: Zipf-like column ids whose hot set is not the
+    lowest indices, ties in the column counts, rows of 0..20 nonzeros."""
+    from paper_1607_01404_b200 import _lib
+    n = 30_000
+    lens = rng.integers(0, 21, m)
+    rows = np.repeat(np.arange(m), lens)
+    scramble = rng.permutation(n)
+    cols = scramble[np.minimum(rng.zipf(1.2, rows.size) - 1, n - 1)]
+    vals = rng.standard_normal(rows.size) * 10.0 ** rng.uniform(-3, 3, rows.size)
+    x = rng.standard_normal((n, 4)) * 10.0 ** rng.uniform(-3, 3, (n, 4))
+    rp, ci, va = ocsr.csr_from_coo(m, n, rows, cols, vals)
+    want = ocsr.spmv(m, n, rp, ci, va, x)
+    for key, nhot in ((1, 1280 if rows.size >= 32 * 1280 else 0), (0, 0)):
+        try:
+            _lib.call("svdsb_tune_set", 12, key)
+            a, _ = _csr(m, n, rows, cols, vals)        # a fresh handle: the copies are built on first use
+            got = _spmv_dev(a, x, False)
+            assert a.device_csr().layout_info(1) == nhot
+        finally:
+            _lib.call("svdsb_tune_set", 12, 0)
+        assert np.array_equal(got, want), key
+    # uniform columns: the hot copy is not worth building
+    try:
+        _lib.call("svdsb_tune_set", 12, 1)
+        a, (rp, ci, va) = _csr(m, n, rows, rng.integers(0, n, rows.size), vals)
+        got = _spmv_dev(a, x, False)
+        assert a.device_csr().layout_info(1) == 0
+    finally:
+        _lib.call("svdsb_tune_set", 12, 0)
+    assert np.array_equal(got, ocsr.spmv(m, n, rp, ci, va, x))
+
+
 @pytest.mark.parametrize("variant", [0, 2])
 def test_spmv_transpose_b4_tma_ring(variant, rng):
     """The TMA-staged transposed b = 4 kernel (svdsb_tune_set key 7 = 2:
@@ -828,21 +866,36 @@ def test_syev_update_matches_eigh(g0, b, kind, rng):
         assert np.abs(h @ got_y - got_y * got_w).max() <= 1e-13 * scale * g
 
 
+@pytest.mark.parametrize("accum", [0, 1])
 @pytest.mark.parametrize("b", [1, 2, 4])
-def test_column_blocked_transpose(b, rng, monkeypatch):
+def test_column_blocked_transpose(b, accum, rng, monkeypatch):
     """A^T through row blocks of A (tall scattered matrices) keeps the
     reference's left-to-right order across blocks: bit-exact for short rows,
-    deterministic within rounding for long (chunked) rows."""
+    deterministic within rounding for long (chunked) rows.  Running sums in
+    the result (svdsb_tune_set key 13 = 0) or in the row-major scratch block
+    (1); columns that occur in one block only (their rows are empty in the
+    other blocks and must keep their sums) and columns that never occur."""
     monkeypatch.setenv("SVDSB_T_BLOCK_ROWS", "997")
-    from paper_1607_01404_b200 import SparseMatrixCsr, SvdOperator, make_normal_operator
-    m, n = 5000, 300
-    rows = np.concatenate([np.repeat(np.arange(m), 3), rng.integers(0, m, 6000)])
-    cols = np.concatenate([rng.integers(0, n, 3 * m), rng.integers(0, 3, 6000)])  # 3 heavy columns
+    from paper_1607_01404_b200 import SparseMatrixCsr, SvdOperator, make_normal_operator, _lib
+    m, n = 5000, 320
+    rows = np.concatenate([np.repeat(np.arange(m), 3), rng.integers(0, m, 6000), rng.integers(1000, 1500, 40)])
+    cols = np.concatenate([rng.integers(0, 300, 3 * m), rng.integers(0, 3, 6000),   # 3 heavy columns
+                           rng.integers(300, 310, 40)])                             # one-block columns
     vals = rng.standard_normal(rows.size)
     rp, ci, va = ocsr.csr_from_coo(m, n, rows, cols, vals)
     a = SparseMatrixCsr(m, n, rp, ci, va)
     y = rng.standard_normal((m, b))
-    got = _spmv_dev(a, y, True)
+    _lib.call("svdsb_tune_set", 13, accum)
+    try:
+        got = _spmv_dev(a, y, True)
+        assert a.device_csr().layout_info(2) == 6
+        _test_column_blocked_rest(a, rp, ci, va, m, n, b, y, got, rng)
+    finally:
+        _lib.call("svdsb_tune_set", 13, 0)
+
+
+def _test_column_blocked_rest(a, rp, ci, va, m, n, b, y, got, rng):
+    from paper_1607_01404_b200 import SvdOperator, make_normal_operator
     want = ocsr.spmv(m, n, rp, ci, va, y, transpose=True)
     t_rp = ocsr.csr_transpose(m, n, rp, ci, va)[0]
     long_rows = np.flatnonzero(np.diff(t_rp) > 2048)
