@@ -175,8 +175,12 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // at the end -- 25 us slower on config 4).
 // Key 14: work items of csr_sell4t_kernel (0: handed out by a device
 // counter after each warp's first; 1: fixed stride).
-constexpr int kTuneKeys = 15;
-inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+// Key 15: tall-skinny Gram / Ritz residual / restart product of bases beyond
+// L2 scale (0: streamed through a cp.async.bulk shared-memory ring by one
+// persistent CTA per SM when the operand has >= 2^18 rows, dense_stream.cuh;
+// 1: always the register-tiled kernels; 2: always the streamed kernels).
+constexpr int kTuneKeys = 16;
+inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 
 #define SVDSB_LAUNCH_PDL(...)                                             \
   do {                                                                    \

@@ -13,6 +13,7 @@
 // :104-111 (norms), :497-499 (qr_append projection), eigensolver.py:349-352
 // (V^T W), :385-394 (_candidates), :526-527 (restart V @ coefs),
 // :690 (H column), hybrid.py:226-241 (stage-2 split residual).
+#include <cuda.h>
 #include <algorithm>
 
 #include "common.cuh"
@@ -1445,6 +1446,8 @@ ts_gemm_inplace_vec_kernel(int64_t dim, double *x, int64_t ldx, int g, const dou
   }
 }
 
+#include "dense_stream.cuh"
+
 // ------------------------------------------------ fused single-column CGS
 // The whole orthonormalisation of one expansion vector in ONE launch, for a
 // basis of <= 40 columns: select the residual column by the device index and
@@ -1598,6 +1601,66 @@ static bool colset_vec_ok(const ColSet &s) {
   return true;
 }
 
+// Streamed (shared-memory ring) kernels of dense_stream.cuh: the default for
+// bases beyond L2 scale; tune key 15 = 1 keeps the register-tiled kernels,
+// 2 takes the streamed ones at every size.
+static bool stream_ok(int64_t dim) {
+  if (g_tune[15] == 1) return false;
+  if (g_tune[15] == 2) return dim >= 1;
+  return dim >= (int64_t)1 << 18;
+}
+
+static int stream_grid_tiles(int64_t dim, int rows) {
+  const int64_t nt = (dim + rows - 1) / rows;
+  return (int)std::min<int64_t>(num_sms(), std::max<int64_t>(nt, 1));
+}
+
+// L2 evict-first for operands that cannot stay resident anyway
+static int stream_evict_first(int64_t dim, int cols) { return (double)dim * cols * 8.0 > 48e6 ? 1 : 0; }
+
+template <typename K>
+static cudaError_t stream_attr(K kernel, size_t smem) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+// Tensor map of a column-major fp64 block (rows innermost) for the streamed
+// kernels' tile loads; cuTensorMapEncodeTiled through the runtime's driver
+// entry point (no link against libcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+static bool make_map2d(CUtensorMap *m, const double *base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                       int box_cols) {
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (fn == nullptr || rows < 1 || cols < 1 || !aligned16(base) || (ld & 1) || rows >= ((int64_t)1 << 31)) return false;
+  const cuuint64_t gdim[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  const cuuint64_t gstr[1] = {(cuuint64_t)ld * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), gdim, gstr, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr int kTsMaxG = 64;  // basis columns the streamed Ritz / restart kernels take (coefficients in shared memory)
+
+static size_t ts_stream_smem(int nin, int g, int pt) {
+  return sizeof(double) * ((size_t)kTsStages * nin * ts_kc(nin) * kTsRows + (size_t)g * pt);
+}
+
 static int make_colset(ColSet &s, int nblk, const double *const *xs, const int64_t *ldxs, const int *cols) {
   SVDSB_CHECK_ARG(nblk >= 1 && nblk <= SVDSB_MAX_BLOCKS, "between 1 and SVDSB_MAX_BLOCKS column blocks");
   s.nblk = 0;
@@ -1634,6 +1697,43 @@ int svdsb_gram(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, c
 
 namespace svdsb {
 
+// b >= 2 Gram through gram_stream_kernel (one persistent CTA per SM, tiles
+// by TMA); false when a tensor map cannot be built (the caller falls back).
+static bool gram_stream(svdsb_ctx *ctx, int64_t dim, const ColSet &s, const double *y, int64_t ldy, int b, double *c,
+                        int64_t ldc, double *norms2, cudaStream_t st) {
+  GramMaps maps;
+  int cap = 4;
+  for (int k = 0; k < s.nblk; ++k) {
+    if (!make_map2d(&maps.x[k], s.base[k], dim, s.cols[k], s.ld[k], kGsRows, kGsBox)) return false;
+    cap += (s.cols[k] + kGsBox - 1) / kGsBox * kGsBox;
+  }
+  for (int k = s.nblk; k < SVDSB_MAX_BLOCKS; ++k) maps.x[k] = maps.x[0];
+  if (cap > kGsCap) return false;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(gram_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * kGsStages * kGsCap * kGsRows)) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    attr = true;
+  }
+  const int gxs = stream_grid_tiles(dim, kGsRows);
+  const size_t sh = sizeof(double) * (size_t)kGsStages * cap * kGsRows;
+  for (int j0 = 0; j0 < b; j0 += 4) {
+    const int nb = std::min(4, b - j0);
+    if (!make_map2d(&maps.y, y + (int64_t)j0 * ldy, dim, nb, ldy, kGsRows, 4)) return false;
+    if (launch_k(gram_stream_kernel, dim3(gxs, 1, 1), dim3(kStreamThreads, 1, 1), sh, st, maps, dim, s, nb,
+                 c + (int64_t)j0 * ldc, ldc, norms2 ? norms2 + j0 : (double *)nullptr, ctx->partials, take_ticket(ctx),
+                 stream_evict_first(dim, s.total)) != cudaSuccess) {
+      cudaGetLastError();
+      return false;  // nothing written yet for this chunk: the register-tiled kernels redo the whole Gram
+    }
+    bump_launches();
+  }
+  return true;
+}
+
 int gram_impl(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, const int64_t *ldxs, const int *cols,
               const double *y, int64_t ldy, int b, double *c, int64_t ldc, double *norms2, void *stream, HInsert hi) {
   SVDSB_CHECK_ARG(ctx != nullptr, "svdsb_gram: NULL ctx");
@@ -1664,6 +1764,9 @@ int gram_impl(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, co
       SVDSB_LAUNCH_PDL(gram1_vec_kernel<AT>, grid, kThreads, 0, st, dim, s, y, c, norms2, ctx->partials,
                        take_ticket(ctx), nullptr, hi);
     }
+    return SVDSB_OK;
+  } else if (b >= 2 && colset_vec_ok(s) && aligned16(y) && ldy % 2 == 0 && s.total <= kGsMaxX && stream_ok(dim) &&
+             gram_stream(ctx, dim, s, y, ldy, b, c, ldc, norms2, st)) {
     return SVDSB_OK;
   } else if (b >= 2 && colset_vec_ok(s) && aligned16(y) && ldy % 2 == 0) {
     // four columns of y per launch (a 2- or 3-column tail masks the rest);
@@ -1761,6 +1864,29 @@ int svdsb_ts_gemm(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx, int
   if (x == y) {
     SVDSB_CHECK_ARG(ldx == ldy && s <= g && s <= 32 && alpha == 1.0 && beta == 0.0,
                     "svdsb_ts_gemm: in-place needs ldy == ldx, s <= min(g, 32), alpha 1, beta 0");
+    if (aligned16(y) && !(ldy & 1) && g_tune[4] != 2 && g <= kTsMaxG && stream_ok(dim)) {
+      const int pt = s <= 8 ? 8 : s <= 16 ? 16 : s <= 24 ? 24 : 32;
+      const size_t shs = ts_stream_smem(1, g, pt);
+      static bool attrs = false;
+      if (!attrs) {
+        const size_t mx = ts_stream_smem(1, kTsMaxG, 32);
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 2, 4, false>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 2, 8, false>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 4, 6, false>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 4, 8, false>, mx));
+        attrs = true;
+      }
+      auto ks = pt == 8 ? ts_stream_kernel<1, 2, 4, false> : pt == 16 ? ts_stream_kernel<1, 2, 8, false>
+              : pt == 24 ? ts_stream_kernel<1, 4, 6, false> : ts_stream_kernel<1, 4, 8, false>;
+      CUtensorMap mx;
+      if (make_map2d(&mx, y, dim, g, ldy, kTsRows, ts_kc(1))) {
+        ks<<<stream_grid_tiles(dim, kTsRows), kTsThreads, shs, st>>>(
+            mx, mx, dim, g, c, ldc, nullptr, s, y, ldy, nullptr, 0, nullptr, 0, nullptr, nullptr, nullptr, StatusOut{},
+            stream_evict_first(dim, g));
+        SVDSB_LAUNCHED();
+        return SVDSB_OK;
+      }
+    }
     if (aligned16(y) && !(ldy & 1) && g_tune[4] != 2) {
       auto k = s <= 8 ? ts_gemm_inplace_vec_kernel<8> : s <= 16 ? ts_gemm_inplace_vec_kernel<16>
              : s <= 24 ? ts_gemm_inplace_vec_kernel<24> : ts_gemm_inplace_vec_kernel<32>;
@@ -1839,6 +1965,45 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
       SVDSB_RITZ_DMMA(4);
 #undef SVDSB_RITZ_DMMA
     return SVDSB_OK;
+  }
+  {
+    const bool vec = aligned16(v) && aligned16(w) && aligned16(r) && !(ldv & 1) && !(ldw & 1) && !(ldr & 1) &&
+                     (x == nullptr || (aligned16(x) && !(ldx & 1))) && (ox == nullptr || (aligned16(ox) && !(ldox & 1)));
+    if (vec && p <= 32 && g <= kTsMaxG && stream_ok(dim)) {
+      const int pt = p <= 8 ? 8 : p <= 12 ? 12 : p <= 16 ? 16 : p <= 24 ? 24 : 32;
+      const size_t shs = ts_stream_smem(2, g, pt);
+      static bool attrs = false;
+      if (!attrs) {
+        const size_t mx = ts_stream_smem(2, kTsMaxG, 32);
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 2, 4, true>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 2, 6, true>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 2, 8, true>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 4, 6, true>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 4, 8, true>, mx));
+        attrs = true;
+      }
+      CUtensorMap mv, mw;
+      if (make_map2d(&mv, v, dim, g, ldv, kTsRows, ts_kc(2)) && make_map2d(&mw, w, dim, g, ldw, kTsRows, ts_kc(2))) {
+        auto *tk = take_ticket(ctx);
+        const dim3 grid(stream_grid_tiles(dim, kTsRows), 1, 1);
+        const int ef = stream_evict_first(dim, 2 * g);
+#define SVDSB_RITZ_STREAM(RPT, PQV)                                                                            \
+  SVDSB_LAUNCH_PDL(ts_stream_kernel<2, RPT, PQV, true>, grid, kTsThreads, shs, st, mv, mw, dim, g, yc, ldyc, lam, p, r, \
+                   ldr, x, ldx, ox, ldox, rn2, ctx->partials, tk, so, ef)
+        if (pt == 8)
+          SVDSB_RITZ_STREAM(2, 4);
+        else if (pt == 12)
+          SVDSB_RITZ_STREAM(2, 6);
+        else if (pt == 16)
+          SVDSB_RITZ_STREAM(2, 8);
+        else if (pt == 24)
+          SVDSB_RITZ_STREAM(4, 6);
+        else
+          SVDSB_RITZ_STREAM(4, 8);
+        return SVDSB_OK;
+      }
+#undef SVDSB_RITZ_STREAM
+    }
   }
   if (p > 16 && p <= 32 && g_tune[3] != 1) {
     // two threads per row, 12 or 16 candidates each (config 4, p = 24:

@@ -1183,3 +1183,95 @@ def test_from_coo_range_checks():
         SparseMatrixCsr.from_coo(2, 3, ok[0], np.array([0, 3]), ok[2])
     with pytest.raises(ValueError, match="equal length"):
         SparseMatrixCsr.from_coo(2, 3, ok[0], ok[1], np.array([1.0]))
+
+
+# ---------------------------------------------------------------- streamed
+# (cp.async.bulk ring) tall-skinny kernels, svdsb_tune_set key 15
+
+
+@pytest.mark.parametrize("dim", [1, 255, 257, 70_001, 300_002])
+@pytest.mark.parametrize("g,p", [(35, 24), (35, 11), (8, 3), (40, 32), (17, 16), (5, 7)])
+def test_ritz_residual_streamed_bit_identical(dim, g, p, rng):
+    """ts_stream_kernel<2, PQ, true> against the register-tiled Ritz kernels:
+    R, X = V Y and OpX = W Y bit for bit (same fma chain), |R_j|^2 to
+    rounding, on odd / sub-tile / multi-tile row counts and partial column
+    chunks; the status copy is exercised by the solver tests."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    vh, wh = rng.standard_normal((dim, g)), rng.standard_normal((dim, g))
+    yh = rng.standard_normal((g, p))
+    lh = rng.standard_normal(p)
+    V, W, Y = dv.to_device_block(vh), dv.to_device_block(wh), dv.to_device_block(yh)
+    lam = torch.from_numpy(lh).to(ctx.device)
+    outs = []
+    try:
+        for key in (1, 2):
+            _lib.call("svdsb_tune_set", 15, key)
+            R, X, OX = dv.new_block(dim, p), dv.new_block(dim, p), dv.new_block(dim, p)
+            rn2 = torch.zeros(p, dtype=torch.float64, device=ctx.device)
+            dv.ritz_residual(ctx, V, W, Y, lam, R, x=X, ox=OX, rn2=rn2)
+            outs.append((dv.to_host(R), dv.to_host(X), dv.to_host(OX), rn2.cpu().numpy()))
+    finally:
+        _lib.call("svdsb_tune_set", 15, 0)
+    for k in range(3):
+        assert np.array_equal(outs[0][k], outs[1][k])
+    want = wh @ yh - (vh @ yh) * lh
+    assert np.abs(outs[1][0] - want).max() <= 1e-12 * max(np.abs(want).max(), 1.0)
+    assert np.allclose(outs[1][3], (want ** 2).sum(0), rtol=1e-12)
+
+
+@pytest.mark.parametrize("dim", [1, 257, 200_001])
+@pytest.mark.parametrize("g,s", [(20, 3), (35, 15), (35, 20), (40, 32), (9, 9)])
+def test_restart_inplace_streamed_bit_identical(dim, g, s, rng):
+    """In-place V <- V C through the streamed kernel equals the vectorised
+    register kernel bit for bit; columns past s untouched."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    x0 = rng.standard_normal((dim, g))
+    c = rng.standard_normal((g, s))
+    outs = []
+    for key in (1, 2):
+        X = dv.to_device_block(x0)
+        C = dv.to_device_block(c)
+        try:
+            _lib.call("svdsb_tune_set", 15, key)
+            dv.ts_gemm(ctx, X, C, X[:, :s])
+        finally:
+            _lib.call("svdsb_tune_set", 15, 0)
+        outs.append(dv.to_host(X))
+    assert np.array_equal(outs[0], outs[1])
+    want = x0 @ c
+    assert np.abs(outs[1][:, :s] - want).max() <= 1e-13 * np.abs(want).max() * g
+    assert np.array_equal(outs[1][:, s:], x0[:, s:])
+
+
+@pytest.mark.parametrize("dim", [1, 127, 129, 70_001, 300_002])
+@pytest.mark.parametrize("g,b", [(35, 4), (40, 4), (7, 2), (20, 3), (1, 4), (33, 7)])
+def test_gram_streamed(dim, g, b, rng):
+    """gram_stream_kernel against fp64 numpy and the register-tiled kernel
+    (different summation trees: rounding-level agreement), norms included;
+    two calls give identical bits (fixed tile ranges and trees)."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    a = rng.standard_normal((dim, g))
+    y = rng.standard_normal((dim, b))
+    X, Y = dv.to_device_block(a), dv.to_device_block(y)
+    outs = []
+    try:
+        for key in (1, 2, 2):
+            _lib.call("svdsb_tune_set", 15, key)
+            C = dv.small_matrix(g, b)
+            nrm = torch.zeros(b, dtype=torch.float64, device=ctx.device)
+            dv.gram(ctx, dim, [X], Y, C, norms2=nrm)
+            outs.append((dv.to_host(C), nrm.cpu().numpy()))
+    finally:
+        _lib.call("svdsb_tune_set", 15, 0)
+    want = a.T @ y
+    tol = 1e-13 * max(np.abs(want).max(), 1.0) * np.sqrt(dim)
+    for got, n2 in outs:
+        assert np.abs(got - want).max() <= tol
+        assert np.allclose(n2, (y ** 2).sum(0), rtol=1e-13)
+    assert np.array_equal(outs[1][0], outs[2][0]) and np.array_equal(outs[1][1], outs[2][1])
