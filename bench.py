@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4")
     ap.add_argument("--budget", type=int, default=None, help="fixed max_matvecs per solve (SURVEY 8(d))")
+    ap.add_argument("--stage1-method", default=None, choices=["GD+k", "JDQMR"],
+                    help="stage-1 eigensolver (SvdsConfig.stage1_opts['method']); JDQMR converges config "
+                         "3-smallest, where GD+k stalls")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-scale", action="store_true", help="skip the config-3 kernel roofline section")
@@ -241,8 +244,9 @@ def run_ours(args):
     setup_s = time.perf_counter() - t0
 
     def cfg():
+        extra = {"stage1_opts": {"method": args.stage1_method}} if args.stage1_method else {}
         return SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block, seed=0,
-                          max_matvecs=args.budget)
+                          max_matvecs=args.budget, **extra)
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
@@ -308,11 +312,13 @@ def run_ours(args):
         "scaling": ("weak" if wl.name == "c5" else "strong") if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator of BASELINE config %s; random draws, no dataset)" % wl.name[1:],
-        "config": config_json(wl, m, n, nnz, world, args.budget),
+        "config": dict(config_json(wl, m, n, nnz, world, args.budget),
+                       **({"stage1_method": args.stage1_method} if args.stage1_method else {})),
         "result": {"sigma": [float(s) for s in res.sigma], "rnorms_max": float(res.rnorms.max()),
                    "converged": int(res.converged.sum()), "status": res.status,
                    "stage1_matvecs": res.stats.stage1_matvecs, "stage2_matvecs": res.stats.stage2_matvecs,
-                   "outer_iterations": iters, "restarts": getattr(res.stats, "restarts", None),
+                   "outer_iterations": iters, "inner_iterations": getattr(res.stats, "inner_iterations", 0),
+                   "restarts": getattr(res.stats, "restarts", None),
                    "host_syncs": res.stats.syncs},
         "per_step_ms": [round(t, 3) for t in step_ms],
         "per_iteration_ms": ms / max(iters, 1), "per_matvec_us": ms * 1e3 / max(mv, 1),
@@ -357,6 +363,17 @@ def run_ours(args):
                           "step = (stage-1 matvecs / 2 - eager wide-block columns) / b; algorithmic bytes = "
                           "A.X + A^T.Y per SURVEY 8(d); traffic = ncu DRAM read+write of the same C-apply "
                           "(cold L2, profiles/traffic_%s.json)" % (per_step, wl.name)}
+            gp = gather_ceiling()
+            if gp:
+                # every nonzero of a b = 4 product fetches one 32-byte operand row; the SMs deliver
+                # at most `rows_per_s` such rows (profiles/r02_gather_probe.jsonl), whatever HBM does
+                floor_us = 2.0 * nnz / gp * 1e6
+                line["roofline"]["sm_gather_ceiling"] = {
+                    "rows_per_s": gp, "floor_us_per_c_apply": floor_us,
+                    "hbm_frac_at_floor": nb["algorithmic_bytes"] / (floor_us * 1e-6) / 1e9 / peak,
+                    "achieved_frac_of_floor": floor_us / nb["us"],
+                    "source": "tools/probes/gather_probe.cu on this pool's B200: 1.00 cycle per gathered "
+                              "32-byte row per SM, independent of lanes per row, occupancy and table size"}
         else:
             if not cnt:
                 key = max(by_kind, key=lambda k: by_kind[k][1])
@@ -384,6 +401,23 @@ def run_ours(args):
         tdist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def gather_ceiling():
+    """Measured 32-byte-row gather rate of the chip (rows/s), uniform
+    addresses, one lane per row -- the best case of the probe."""
+    path = os.path.join(REPO, "profiles", "r02_gather_probe.jsonl")
+    if not os.path.exists(path):
+        return None
+    best = 0.0
+    for ln in open(path):
+        try:
+            rec = json.loads(ln)
+        except ValueError:
+            continue
+        if rec.get("zipf") == 0:
+            best = max(best, rec["grows_per_s"] * 1e9)
+    return best or None
 
 
 def block_kernels(a, wl, peak, traffic):
@@ -433,7 +467,7 @@ def block_kernels(a, wl, peak, traffic):
     rn2 = torch.zeros(p, dtype=torch.float64, device="cuda")
     C = dv.small_matrix(g, b)
     nr = torch.zeros(b, dtype=torch.float64, device="cuda")
-    V2 = dv.new_block(n, s)
+    s2 = min(wl.k + b, 32)
     cases = [
         ("spmv_fwd_b%d" % b, lambda: dcsr.matvec(x, yo, False), spmv_bytes(m, n, nnz, b, False)),
         ("spmv_adj_b%d" % b, lambda: dcsr.matvec(y, z, True), spmv_bytes(m, n, nnz, b, True)),
@@ -443,7 +477,9 @@ def block_kernels(a, wl, peak, traffic):
         ("project_b%d_g35" % b, lambda: dv.project_out(ctx, n, [V], C, x, norms2=nr), 8 * n * (g + 2 * b)),
         ("ritz_residual_g35_p%d" % p, lambda: dv.ritz_residual(ctx, V, W, Y[:, :p], lam[:p], R, rn2=rn2),
          8 * n * (2 * g + p)),
-        ("restart_ts_gemm_35to15", lambda: dv.ts_gemm(ctx, V, Y[:, :s], V2), 8 * n * (g + s)),
+        # the thick restart V <- V C in place, as DavidsonSolver._swap_basis runs it (Y orthonormal: V stays bounded)
+        ("restart_inplace_35to%d" % s, lambda: dv.ts_gemm(ctx, V, Y[:, :s], V[:, :s]), 8 * n * (g + s)),
+        ("restart_inplace_35to%d" % s2, lambda: dv.ts_gemm(ctx, V, Y[:, :s2], V[:, :s2]), 8 * n * (g + s2)),
     ]
     out = {"workload": "this workload's matrix (m=%d, n=%d, nnz=%d), basis g=%d" % (m, n, nnz, g),
            "peak_gbs": peak, "method": "CUDA events on the launching stream, L2 flushed, median of 10"}

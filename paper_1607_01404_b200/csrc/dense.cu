@@ -646,26 +646,29 @@ gram4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ y, int64_t l
   });
 }
 
-// b = 4 projection Y -= X C (+ |Y_j|^2 after): two rows per thread with
+// b = NB <= 4 projection Y -= X C (+ |Y_j|^2 after): two rows per thread with
 // 16-byte loads, basis columns in chunks of 8 whose loads precede their
 // FMAs; per element the same fma order as project_kernel (bit-identical).
+template <int NB>
 __global__ void __launch_bounds__(kThreads)
 project4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ cmat, int64_t ldc, double *y, int64_t ldy,
                     double *norms2, double *partials, unsigned int *ticket) {
   pdl_wait();
-  extern __shared__ double csh4[];  // na x 4
+  extern __shared__ double csh4[];  // na x NB
   __shared__ const double *xp[256];
   const int na = xs.total;
   for (int i = threadIdx.x; i < na; i += kThreads) xp[i] = colset_ptr(xs, i);
-  for (int k = threadIdx.x; k < na * 4; k += kThreads) csh4[k] = cmat[k / 4 + (int64_t)(k % 4) * ldc];
+  for (int k = threadIdx.x; k < na * NB; k += kThreads) csh4[k] = cmat[k / NB + (int64_t)(k % NB) * ldc];
   __syncthreads();
-  double nacc[4] = {0.0, 0.0, 0.0, 0.0};
+  double nacc[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) nacc[j] = 0.0;
   RowRange rr = cta_rows_even(dim);
   int64_t r = rr.r0 + 2 * threadIdx.x;
   for (; r + 1 < rr.r1; r += 2 * kThreads) {
-    double2 yv[4];
+    double2 yv[NB];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) yv[j] = *reinterpret_cast<const double2 *>(y + r + (int64_t)j * ldy);
+    for (int j = 0; j < NB; ++j) yv[j] = *reinterpret_cast<const double2 *>(y + r + (int64_t)j * ldy);
     for (int i0 = 0; i0 < na; i0 += 8) {
       double2 xv[8];
 #pragma unroll
@@ -673,9 +676,9 @@ project4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ cmat, int
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         if (i0 + u < na) {
-          const double *cr = csh4 + (i0 + u) * 4;
+          const double *cr = csh4 + (i0 + u) * NB;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < NB; ++j) {
             yv[j].x = fma(-xv[u].x, cr[j], yv[j].x);
             yv[j].y = fma(-xv[u].y, cr[j], yv[j].y);
           }
@@ -683,32 +686,32 @@ project4_vec_kernel(int64_t dim, ColSet xs, const double *__restrict__ cmat, int
       }
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NB; ++j) {
       *reinterpret_cast<double2 *>(y + r + (int64_t)j * ldy) = yv[j];
       nacc[j] = fma(yv[j].x, yv[j].x, nacc[j]);
       nacc[j] = fma(yv[j].y, yv[j].y, nacc[j]);
     }
   }
   if (r < rr.r1) {
-    double yv[4];
+    double yv[NB];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) yv[j] = y[r + (int64_t)j * ldy];
+    for (int j = 0; j < NB; ++j) yv[j] = y[r + (int64_t)j * ldy];
     for (int i = 0; i < na; ++i) {
       const double xv = __ldg(xp[i] + r);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) yv[j] = fma(-xv, csh4[i * 4 + j], yv[j]);
+      for (int j = 0; j < NB; ++j) yv[j] = fma(-xv, csh4[i * NB + j], yv[j]);
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NB; ++j) {
       y[r + (int64_t)j * ldy] = yv[j];
       nacc[j] = fma(yv[j], yv[j], nacc[j]);
     }
   }
   pdl_trigger();
   if (norms2 == nullptr) return;
-  cta_fold<4>(nacc, 4, partials + (int64_t)blockIdx.x * 4);
+  cta_fold<NB>(nacc, NB, partials + (int64_t)blockIdx.x * NB);
   if (!last_cta(ticket)) return;
-  fold_parts(partials, gridDim.x, 4, 4, [&](int j, int, int, double sum) { norms2[j] = sum; });
+  fold_parts(partials, gridDim.x, NB, NB, [&](int j, int, int, double sum) { norms2[j] = sum; });
 }
 
 // One step of the iterated-CGS decision of kernels.py:115-127, on device.
@@ -1834,10 +1837,12 @@ int svdsb_project_out(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const
       SVDSB_LAUNCH_PDL(project1_vec_kernel, grid_for(project1_vec_kernel, dim, sh), kThreads, sh, st, dim, s, cc, yy,
                        nn, ctx->partials, take_ticket(ctx), (double *)nullptr);
       continue;
-    } else if (bb == 4 && colset_vec_ok(s) && aligned16(yy) && ldy % 2 == 0) {
-      size_t sh = sizeof(double) * std::max(s.total, 1) * 4;
-      SVDSB_LAUNCH_PDL(project4_vec_kernel, grid_for(project4_vec_kernel, dim, sh), kThreads, sh, st, dim, s, cc,
-                       ldc, yy, ldy, nn, ctx->partials, take_ticket(ctx));
+    } else if (bb >= 2 && bb <= 4 && colset_vec_ok(s) && aligned16(yy) && ldy % 2 == 0) {
+      // (2 and 3 columns went through the generic kernel: 209 vs 78 us at N = 1 M, g = 35)
+      size_t sh = sizeof(double) * std::max(s.total, 1) * bb;
+      auto k = bb == 4 ? project4_vec_kernel<4> : bb == 3 ? project4_vec_kernel<3> : project4_vec_kernel<2>;
+      SVDSB_LAUNCH_PDL(k, grid_for(k, dim, sh), kThreads, sh, st, dim, s, cc, ldc, yy, ldy, nn, ctx->partials,
+                       take_ticket(ctx));
       continue;
     } else if (bb == 1) {
       size_t sh = sizeof(double) * std::max(s.total, 1) * 1;

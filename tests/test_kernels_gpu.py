@@ -613,7 +613,7 @@ def test_gram_project_tsgemm(dim, rng):
     a2 = rng.standard_normal((dim, 30))
     y = rng.standard_normal((dim, 4))
     X1, X2, Y = dv.to_device_block(a1), dv.to_device_block(a2), dv.to_device_block(y)
-    for b in (1, 4):
+    for b in (1, 2, 3, 4):
         C = dv.small_matrix(37, b)
         nrm = torch.zeros(b, dtype=torch.float64, device=ctx.device)
         dv.gram(ctx, dim, [X1, X2], Y[:, :b], C, norms2=nrm)

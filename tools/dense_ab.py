@@ -32,12 +32,16 @@ for N in (1_000_000, 4_096_000):
     for key in (1, 2):
         _lib.call("svdsb_tune_set", 15, key)
         tag = {1: "reg", 2: "stream"}[key]
-        for b in (4, 2):
+        for b in (4, 2, 1):
             Y = dv.new_block(N, b); Y.normal_()
             C = dv.small_matrix(g, b); nrm = torch.zeros(b, dtype=torch.float64, device=ctx.device)
             t = timeit(lambda: dv.gram(ctx, N, [V], Y, C, norms2=nrm))
             byt = 8 * N * (g + b)
             out[f"N{N}_gram_b{b}_{tag}"] = dict(us=t * 1e6, gbs=byt / t / 1e9, frac=byt / t / 1e9 / PEAK)
+            C.mul_(1e-3)
+            t = timeit(lambda: dv.project_out(ctx, N, [V], C, Y, norms2=nrm))
+            byt = 8 * N * (g + 2 * b)
+            out[f"N{N}_project_b{b}_{tag}"] = dict(us=t * 1e6, gbs=byt / t / 1e9, frac=byt / t / 1e9 / PEAK)
         for p in (24, 11, 5):
             Yc = dv.small_matrix(g, p); Yc.normal_()
             lam = torch.randn(p, dtype=torch.float64, device=ctx.device)

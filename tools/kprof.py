@@ -32,6 +32,7 @@ b = wl.block
 N, g = n, 35
 p = min(wl.k + b, g)
 s = 15
+s2 = min(wl.k + b, 32)
 gen = torch.Generator(device="cuda")
 gen.manual_seed(5)
 
@@ -69,7 +70,8 @@ ops = [
     ("cgs_project_b1_g35", lambda: dv.project_out(ctx, N, [V], C1, y1, norms2=nr1), 8 * N * (g + 2)),
     ("ritz_residual_g35_p%d" % p, lambda: dv.ritz_residual(ctx, V, W, Y[:, :p], lam[:p], R, rn2=rn2),
      8 * N * (2 * g + p)),
-    ("restart_ts_gemm_35to15", lambda: dv.ts_gemm(ctx, V2, Y[:, :s], V2[:, :s]), 8 * N * (g + s)),
+    ("restart_inplace_35to%d" % s, lambda: dv.ts_gemm(ctx, V2, Y[:, :s], V2[:, :s]), 8 * N * (g + s)),
+    ("restart_inplace_35to%d" % s2, lambda: dv.ts_gemm(ctx, V2, Y[:, :s2], V2[:, :s2]), 8 * N * (g + s2)),
 ]
 for _ in range(2):
     for _, fn, _ in ops:
