@@ -33,11 +33,32 @@ def _inputs():
     return files
 
 
+STAMP = LIB + ".srchash"
+
+
+def source_hash():
+    """SHA-256 over the compiler version, flags and every input file's
+    contents: the library is reused only when it was built from exactly
+    these sources (file times say nothing after a checkout or a copy)."""
+    import hashlib
+    h = hashlib.sha256()
+    try:
+        h.update(subprocess.run([NVCC, "--version"], capture_output=True).stdout)
+    except OSError:
+        pass
+    h.update(" ".join(ARCH + FLAGS).encode())
+    for f in sorted(_inputs()):
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def up_to_date():
-    if not os.path.exists(LIB):
+    if not (os.path.exists(LIB) and os.path.exists(STAMP)):
         return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(f) <= t for f in _inputs())
+    with open(STAMP) as fh:
+        return fh.read().strip() == source_hash()
 
 
 def build(force=False, verbose=False, variant=None, overrides=None, defines=()):
@@ -71,6 +92,9 @@ def build(force=False, verbose=False, variant=None, overrides=None, defines=()):
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
+    if variant is None and not overrides and not defines:
+        with open(STAMP, "w") as fh:
+            fh.write(source_hash() + "\n")
     return lib
 
 
