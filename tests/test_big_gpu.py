@@ -149,3 +149,33 @@ def test_full_size_certified(key):
     # orthonormal singular vectors
     assert np.abs(res.v.T @ res.v - np.eye(wl.k)).max() <= 1e-8
     assert np.abs(res.u.T @ res.u - np.eye(wl.k)).max() <= 1e-8
+
+
+@pytest.mark.skipif(not os.environ.get("SVDSB_LONG_TESTS"),
+                    reason="two minutes of GPU time: set SVDSB_LONG_TESTS=1 (profiles/r02_c3S_certified.log holds a run)")
+def test_config3_smallest_full_size_jdqmr_certified():
+    """BASELINE config 3, k = 10 SMALLEST triplets of the 160^3 operator at
+    tol 1e-8: GD+k stalls (residual 0.0245 after 400 000 matvecs), JDQMR in
+    stage 1 converges (~4.2e5 matvecs, ~2 min).  Certified like the other
+    full-size solves: host Eq. (7) of every triplet <= tol ||A||, with ||A||
+    from an independent scipy estimate."""
+    import scipy.sparse.linalg as spla
+    from paper_1607_01404_b200 import SparseMatrixCsr, SvdsConfig, svds_solve, workloads
+    wl = workloads.CONFIGS["c3S"]
+    m, n, r, c, v = wl.build()
+    a = SparseMatrixCsr.from_coo(m, n, r, c, v)
+    res = svds_solve(a, cfg=SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol, max_block_size=wl.block,
+                                       seed=0, stage1_opts={"method": "JDQMR"}))
+    del a
+    assert res.converged.all(), (res.rnorms, res.status)
+    assert res.status == "ok"
+    ha = _host_csr(m, n, r, c, v)
+    del r, c, v
+    a_norm = float(spla.svds(ha, k=1, return_singular_vectors=False, tol=1e-6)[0])
+    r7 = _eq7(ha, res.sigma, res.u, res.v)
+    print("c3S sigma", res.sigma, "max Eq7 %.3e (tol*||A|| %.3e)" % (r7.max(), wl.tol * a_norm),
+          "matvecs", res.stats.stage1_matvecs, res.stats.stage2_matvecs, "inner", res.stats.inner_iterations)
+    assert r7.max() <= wl.tol * a_norm, r7
+    assert np.all(np.diff(res.sigma) >= 0) or np.all(np.diff(res.sigma) <= 0)
+    assert np.abs(res.v.T @ res.v - np.eye(wl.k)).max() <= 1e-8
+    assert np.abs(res.u.T @ res.u - np.eye(wl.k)).max() <= 1e-8
