@@ -178,7 +178,10 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // Key 15: tall-skinny Gram / Ritz residual / restart product of bases beyond
 // L2 scale (0: streamed through a cp.async.bulk shared-memory ring by one
 // persistent CTA per SM when the operand has >= 2^18 rows, dense_stream.cuh;
-// 1: always the register-tiled kernels; 2: always the streamed kernels).
+// 1: always the register-tiled kernels; 2: always the streamed kernels; 3: as 2
+// with the twelve-warp Ritz variant for 16 < p <= 24 -- two rows x six
+// candidates per thread, more shared-memory loads per FMA: 219 vs 195 us at
+// N = 1 M, kept for measurement).
 constexpr int kTuneKeys = 16;
 inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 

@@ -1609,7 +1609,7 @@ static bool colset_vec_ok(const ColSet &s) {
 // 2 takes the streamed ones at every size.
 static bool stream_ok(int64_t dim) {
   if (g_tune[15] == 1) return false;
-  if (g_tune[15] == 2) return dim >= 1;
+  if (g_tune[15] >= 2) return dim >= 1;
   return dim >= (int64_t)1 << 18;
 }
 
@@ -1660,8 +1660,8 @@ static bool make_map2d(CUtensorMap *m, const double *base, int64_t rows, int64_t
 
 constexpr int kTsMaxG = 64;  // basis columns the streamed Ritz / restart kernels take (coefficients in shared memory)
 
-static size_t ts_stream_smem(int nin, int g, int pt) {
-  return sizeof(double) * ((size_t)kTsStages * nin * ts_kc(nin) * kTsRows + (size_t)g * pt);
+static size_t ts_stream_smem(int nin, int g, int pt, int rows = kTsRows) {
+  return sizeof(double) * ((size_t)kTsStages * nin * ts_kc(nin) * rows + (size_t)g * pt);
 }
 
 static int make_colset(ColSet &s, int nblk, const double *const *xs, const int64_t *ldxs, const int *cols) {
@@ -1875,14 +1875,14 @@ int svdsb_ts_gemm(svdsb_ctx *ctx, int64_t dim, const double *x, int64_t ldx, int
       static bool attrs = false;
       if (!attrs) {
         const size_t mx = ts_stream_smem(1, kTsMaxG, 32);
-        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 2, 4, false>, mx));
-        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 2, 8, false>, mx));
-        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 4, 6, false>, mx));
-        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 4, 8, false>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 256, 2, 2, 4, false>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 256, 2, 2, 8, false>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 256, 4, 4, 6, false>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<1, 256, 4, 4, 8, false>, mx));
         attrs = true;
       }
-      auto ks = pt == 8 ? ts_stream_kernel<1, 2, 4, false> : pt == 16 ? ts_stream_kernel<1, 2, 8, false>
-              : pt == 24 ? ts_stream_kernel<1, 4, 6, false> : ts_stream_kernel<1, 4, 8, false>;
+      auto ks = pt == 8 ? ts_stream_kernel<1, 256, 2, 2, 4, false> : pt == 16 ? ts_stream_kernel<1, 256, 2, 2, 8, false>
+              : pt == 24 ? ts_stream_kernel<1, 256, 4, 4, 6, false> : ts_stream_kernel<1, 256, 4, 4, 8, false>;
       CUtensorMap mx;
       if (make_map2d(&mx, y, dim, g, ldy, kTsRows, ts_kc(1))) {
         ks<<<stream_grid_tiles(dim, kTsRows), kTsThreads, shs, st>>>(
@@ -1980,12 +1980,24 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
       static bool attrs = false;
       if (!attrs) {
         const size_t mx = ts_stream_smem(2, kTsMaxG, 32);
-        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 2, 4, true>, mx));
-        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 2, 6, true>, mx));
-        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 2, 8, true>, mx));
-        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 4, 6, true>, mx));
-        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 4, 8, true>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 256, 2, 2, 4, true>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 256, 2, 2, 6, true>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 256, 2, 2, 8, true>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 256, 4, 4, 6, true>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 256, 4, 4, 8, true>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 384, 2, 4, 6, true>, mx));
         attrs = true;
+      }
+      if (pt == 24 && g_tune[15] == 3) {
+        // twelve warps of two rows x six candidates (3 per sub-partition, <= 168 registers)
+        constexpr int rows = ts_rows(384, 2, 4);
+        CUtensorMap mv, mw;
+        if (make_map2d(&mv, v, dim, g, ldv, rows, ts_kc(2)) && make_map2d(&mw, w, dim, g, ldw, rows, ts_kc(2))) {
+          SVDSB_LAUNCH_PDL(ts_stream_kernel<2, 384, 2, 4, 6, true>, dim3(stream_grid_tiles(dim, rows), 1, 1), 384,
+                           ts_stream_smem(2, g, pt, rows), st, mv, mw, dim, g, yc, ldyc, lam, p, r, ldr, x, ldx, ox, ldox,
+                           rn2, ctx->partials, take_ticket(ctx), so, stream_evict_first(dim, 2 * g));
+          return SVDSB_OK;
+        }
       }
       CUtensorMap mv, mw;
       if (make_map2d(&mv, v, dim, g, ldv, kTsRows, ts_kc(2)) && make_map2d(&mw, w, dim, g, ldw, kTsRows, ts_kc(2))) {
@@ -1993,8 +2005,8 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
         const dim3 grid(stream_grid_tiles(dim, kTsRows), 1, 1);
         const int ef = stream_evict_first(dim, 2 * g);
 #define SVDSB_RITZ_STREAM(RPT, PQV)                                                                            \
-  SVDSB_LAUNCH_PDL(ts_stream_kernel<2, RPT, PQV, true>, grid, kTsThreads, shs, st, mv, mw, dim, g, yc, ldyc, lam, p, r, \
-                   ldr, x, ldx, ox, ldox, rn2, ctx->partials, tk, so, ef)
+  SVDSB_LAUNCH_PDL(ts_stream_kernel<2, 256, RPT, RPT, PQV, true>, grid, kTsThreads, shs, st, mv, mw, dim, g, yc, ldyc, \
+                   lam, p, r, ldr, x, ldx, ox, ldox, rn2, ctx->partials, tk, so, ef)
         if (pt == 8)
           SVDSB_RITZ_STREAM(2, 4);
         else if (pt == 12)

@@ -63,6 +63,7 @@ constexpr int kTsThreads = 256;
 constexpr int kTsLead = SVDSB_TS_LEAD;      // a stage is refilled this many items after its use
 
 __host__ __device__ constexpr int ts_kc(int nin) { return 16 / nin; }  // basis columns per stage
+__host__ __device__ constexpr int ts_rows(int nt, int rpt, int split) { return nt / split * rpt; }  // rows per tile
 
 // NIN = 2, RITZ: R[:, j] = (W y_j) - (V y_j) * lam_j for j < p (two roundings,
 //   eigensolver.py:392), optional X = V Y and OpX = W Y, |R_j|^2 folded by the
@@ -78,15 +79,15 @@ __host__ __device__ constexpr int ts_kc(int nin) { return 16 / nin; }  // basis 
 // for wide Y: a k-step of a warp then reads 7 shared-memory wavefronts for
 // its 48 fp64 FMAs per lane where RPT = 2 reads 10-16 (the shared-memory pipe
 // and the FMA pipe were both about half busy).
-template <int NIN, int RPT, int PQ, bool RITZ>
-__global__ void __launch_bounds__(kTsThreads, 1)
+template <int NIN, int NT, int RPT, int SPLIT, int PQ, bool RITZ>
+__global__ void __launch_bounds__(NT, 1)
 ts_stream_kernel(const __grid_constant__ CUtensorMap mapv, const __grid_constant__ CUtensorMap mapw, int64_t dim, int g,
                  const double *__restrict__ yc, int64_t ldyc, const double *__restrict__ lam, int p, double *r,
                  int64_t ldr, double *xo, int64_t ldx, double *oxo, int64_t ldox, double *rn2, double *partials,
                  unsigned int *ticket, StatusOut so, int evict_first) {
-  constexpr int SPLIT = RPT, PT = PQ * SPLIT, R = kTsRows, KC = ts_kc(NIN), NS = kTsStages, NW = kTsThreads / 32;
+  constexpr int PT = PQ * SPLIT, R = ts_rows(NT, RPT, SPLIT), KC = ts_kc(NIN), NS = kTsStages, NW = NT / 32;
   constexpr int STAGE_D = NIN * KC * R;
-  static_assert(R == kTsThreads / SPLIT * RPT && (RPT == 2 || RPT == 4) && PQ % 2 == 0, "tile shape");
+  static_assert((RPT == 2 || RPT == 4) && (SPLIT == 2 || SPLIT == 4) && PQ % 2 == 0 && R <= 256, "tile shape");
   extern __shared__ __align__(1024) double ts_dyn[];
   double *ysh = ts_dyn + NS * STAGE_D;  // g x PT
   __shared__ uint64_t full[NS], empty[NS];
@@ -101,7 +102,7 @@ ts_stream_kernel(const __grid_constant__ CUtensorMap mapv, const __grid_constant
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   pdl_wait();
-  for (int k = tid; k < g * PT; k += kTsThreads) {
+  for (int k = tid; k < g * PT; k += NT) {
     const int i = k / PT, j = k % PT;
     ysh[k] = (j < p) ? yc[i + (int64_t)j * ldyc] : 0.0;
   }
@@ -234,7 +235,7 @@ ts_stream_kernel(const __grid_constant__ CUtensorMap mapv, const __grid_constant
   }
   __syncthreads();
   double *pp = partials + (int64_t)blockIdx.x * PT;
-  for (int k = tid; k < PT; k += kTsThreads) {
+  for (int k = tid; k < PT; k += NT) {
     double t = 0.0;
 #pragma unroll
     for (int ww = 0; ww < NW; ++ww) t += red[ww][k];

@@ -29,9 +29,18 @@ for N in (1_000_000, 4_096_000):
     g = 35
     V = dv.new_block(N, g); W = dv.new_block(N, g)
     V.normal_(); W.normal_()
-    for key in (1, 2):
+    for key in (1, 2, 3):
         _lib.call("svdsb_tune_set", 15, key)
-        tag = {1: "reg", 2: "stream"}[key]
+        tag = {1: "reg", 2: "stream", 3: "stream12w"}[key]
+        if key == 3:
+            p = 24
+            Yc = dv.small_matrix(g, p); Yc.normal_()
+            lam = torch.randn(p, dtype=torch.float64, device=ctx.device)
+            R = dv.new_block(N, p); rn2 = torch.zeros(p, dtype=torch.float64, device=ctx.device)
+            t = timeit(lambda: dv.ritz_residual(ctx, V, W, Yc, lam, R, rn2=rn2))
+            byt = 8 * N * (2 * g + p)
+            out[f"N{N}_ritz_p{p}_{tag}"] = dict(us=t * 1e6, gbs=byt / t / 1e9, frac=byt / t / 1e9 / PEAK)
+            continue
         for b in (4, 2, 1):
             Y = dv.new_block(N, b); Y.normal_()
             C = dv.small_matrix(g, b); nrm = torch.zeros(b, dtype=torch.float64, device=ctx.device)
