@@ -67,6 +67,68 @@ __global__ void __launch_bounds__(256) gather_kernel(const Row *tab, uint32_t ma
   if (acc == 1.2345e300) out[0] = acc;
 }
 
+// The same gathers through the TMA unit instead of the LSU: every lane issues
+// a 32-byte cp.async.bulk of its row into a shared-memory slot (one mbarrier
+// per warp and stage, two stages), then reads the previous stage's slot.
+__device__ __forceinline__ unsigned s32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) tma_gather_kernel(const Row *tab, uint32_t mask, int steps, double *out) {
+  __shared__ __align__(128) Row buf[WARPS][2][32];
+  __shared__ uint64_t bar[WARPS][2];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(s32(&bar[w][k])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t s = mix((blockIdx.x * blockDim.x + threadIdx.x) * 2654435761U + 777U);
+  double acc = 0.0;
+  auto issue = [&](int k) {
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(s32(&bar[w][k])), "r"(32u * 32u) : "memory");
+    __syncwarp();
+    s = mix(s + 0x9e3779b9U);
+    const Row *src = tab + (s & mask);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 32, [%2];"
+                 :: "r"(s32(&buf[w][k][lane])), "l"(src), "r"(s32(&bar[w][k])) : "memory");
+  };
+  issue(0);
+  for (int it = 0; it < steps; ++it) {
+    const int k = it & 1;
+    if (it + 1 < steps) issue(k ^ 1);
+    const unsigned parity = (it >> 1) & 1;
+    asm volatile("{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}"
+                 :: "r"(s32(&bar[w][k])), "r"(parity) : "memory");
+    const Row r = buf[w][k][lane];
+    acc += r.v[0] + r.v[1] + r.v[2] + r.v[3];
+    __syncwarp();
+  }
+  if (acc == 1.2345e300) out[0] = acc;
+}
+
+template <int WARPS>
+static void run_tma(const Row *tab, uint32_t rows, int ctas_per_sm, double *out) {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int grid = sms * ctas_per_sm, steps = 512;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  tma_gather_kernel<WARPS><<<grid, WARPS * 32>>>(tab, rows - 1, steps, out);
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(e0));
+  tma_gather_kernel<WARPS><<<grid, WARPS * 32>>>(tab, rows - 1, steps, out);
+  CK(cudaEventRecord(e1));
+  CK(cudaDeviceSynchronize());
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  const double gathers = (double)grid * WARPS * 32 * steps;
+  printf("{\"case\": \"tma_bulk_32B\", \"table_mb\": %u, \"zipf\": 0, \"warps_per_cta\": %d, \"ctas_per_sm\": %d, "
+         "\"grows_per_s\": %.1f, \"cycles_per_row_per_sm\": %.2f, \"us_for_173M\": %.0f}\n",
+         rows / 32768, WARPS, ctas_per_sm, gathers / ms / 1e6, 1.92e9 * sms / (gathers / (ms * 1e-3)),
+         172.93e6 / (gathers / ms) * 1e3);
+}
+
 template <int LANES, int U>
 static void run(const char *name, const Row *tab, uint32_t rows, int zipf, int ctas_per_sm, double *out) {
   int sms = 0;
@@ -108,5 +170,9 @@ int main() {
       run<4, 8>("four_lanes", tab, rows, zipf, 8, out);
     }
   }
+  run_tma<8>(tab, 1u << 20, 1, out);
+  run_tma<8>(tab, 1u << 20, 4, out);
+  run_tma<16>(tab, 1u << 20, 4, out);
+  run_tma<8>(tab, 1u << 21, 4, out);
   return 0;
 }
