@@ -147,9 +147,14 @@ ts_stream_kernel(const __grid_constant__ CUtensorMap mapv, const __grid_constant
         if (NIN == 2) aw[j][e] = 0.0;
       }
     for (int c = 0; c < nch; ++c, ++it) {
+#ifndef SVDSB_TS_NOLOAD   // timing experiment: 1 = compute on stale stages after the first ring fill
       if (tid == 0 && it >= kTsLead && it - kTsLead + NS < nitems) issue(it - kTsLead + NS);
       __syncwarp();
+#endif
       const int s = (int)(it % NS);
+#ifdef SVDSB_TS_NOLOAD
+      if (it < NS)
+#endif
       mbar_wait(&full[s], (unsigned)((it / NS) & 1));
       const double *sv = ts_dyn + s * STAGE_D + RPT * q;
       const double *yb = ysh + (c * KC) * PT + j0;
