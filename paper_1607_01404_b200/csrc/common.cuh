@@ -181,7 +181,8 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // 1: always the register-tiled kernels; 2: always the streamed kernels; 3: as 2
 // with the twelve-warp Ritz variant for 16 < p <= 24 -- two rows x six
 // candidates per thread, more shared-memory loads per FMA: 219 vs 195 us at
-// N = 1 M, kept for measurement).
+// N = 1 M, kept for measurement; 4: sixteen warps of the same shape, <= 128
+// registers: 215 us).
 constexpr int kTuneKeys = 16;
 inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 

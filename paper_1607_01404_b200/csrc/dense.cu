@@ -1986,7 +1986,19 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
         SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 256, 4, 4, 6, true>, mx));
         SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 256, 4, 4, 8, true>, mx));
         SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 384, 2, 4, 6, true>, mx));
+        SVDSB_CUDA(stream_attr(ts_stream_kernel<2, 512, 2, 4, 6, true>, mx));
         attrs = true;
+      }
+      if (pt == 24 && g_tune[15] == 4) {
+        // sixteen warps of two rows x six candidates (4 per sub-partition, <= 128 registers)
+        constexpr int rows = ts_rows(512, 2, 4);
+        CUtensorMap mv, mw;
+        if (make_map2d(&mv, v, dim, g, ldv, rows, ts_kc(2)) && make_map2d(&mw, w, dim, g, ldw, rows, ts_kc(2))) {
+          SVDSB_LAUNCH_PDL(ts_stream_kernel<2, 512, 2, 4, 6, true>, dim3(stream_grid_tiles(dim, rows), 1, 1), 512,
+                           ts_stream_smem(2, g, pt, rows), st, mv, mw, dim, g, yc, ldyc, lam, p, r, ldr, x, ldx, ox, ldox,
+                           rn2, ctx->partials, take_ticket(ctx), so, stream_evict_first(dim, 2 * g));
+          return SVDSB_OK;
+        }
       }
       if (pt == 24 && g_tune[15] == 3) {
         // twelve warps of two rows x six candidates (3 per sub-partition, <= 168 registers)

@@ -1206,7 +1206,7 @@ def test_ritz_residual_streamed_bit_identical(dim, g, p, rng):
     lam = torch.from_numpy(lh).to(ctx.device)
     outs = []
     try:
-        for key in (1, 2, 3):   # 3: the twelve-warp variant for 16 < p <= 24
+        for key in (1, 2, 3, 4):   # 3 / 4: the twelve- / sixteen-warp variants for 16 < p <= 24
             _lib.call("svdsb_tune_set", 15, key)
             R, X, OX = dv.new_block(dim, p), dv.new_block(dim, p), dv.new_block(dim, p)
             rn2 = torch.zeros(p, dtype=torch.float64, device=ctx.device)
@@ -1217,7 +1217,9 @@ def test_ritz_residual_streamed_bit_identical(dim, g, p, rng):
     for k in range(3):
         assert np.array_equal(outs[0][k], outs[1][k])
         assert np.array_equal(outs[0][k], outs[2][k])
+        assert np.array_equal(outs[0][k], outs[3][k])
     assert np.allclose(outs[2][3], outs[1][3], rtol=1e-12)
+    assert np.allclose(outs[3][3], outs[1][3], rtol=1e-12)
     want = wh @ yh - (vh @ yh) * lh
     assert np.abs(outs[1][0] - want).max() <= 1e-12 * max(np.abs(want).max(), 1.0)
     assert np.allclose(outs[1][3], (want ** 2).sum(0), rtol=1e-12)

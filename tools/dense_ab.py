@@ -29,10 +29,10 @@ for N in (1_000_000, 4_096_000):
     g = 35
     V = dv.new_block(N, g); W = dv.new_block(N, g)
     V.normal_(); W.normal_()
-    for key in (1, 2, 3):
+    for key in (1, 2, 3, 4):
         _lib.call("svdsb_tune_set", 15, key)
-        tag = {1: "reg", 2: "stream", 3: "stream12w"}[key]
-        if key == 3:
+        tag = {1: "reg", 2: "stream", 3: "stream12w", 4: "stream16w"}[key]
+        if key >= 3:
             p = 24
             Yc = dv.small_matrix(g, p); Yc.normal_()
             lam = torch.randn(p, dtype=torch.float64, device=ctx.device)
