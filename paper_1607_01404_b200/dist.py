@@ -107,6 +107,16 @@ class Comm:
             return out
         b = local.shape[1]
         sizes = [int(bounds[p + 1] - bounds[p]) for p in range(self.world)]
+        cols_ok = all(t[:, j].is_contiguous() for t in (local, out) for j in range(b))
+        if cols_ok and b <= 4:
+            # column-major blocks: every column of the result is one contiguous
+            # vector, so each rank's slice of it is gathered in place (no
+            # slab transposes or staging copies; b collectives of rows*8 bytes)
+            for j in range(b):
+                col = out[:, j]
+                views = [col[int(bounds[p]):int(bounds[p + 1])] for p in range(self.world)]
+                tdist.all_gather(views, local[:, j], group=self.group)
+            return out
         # gather contiguous (b, rows_p) row-major slabs, then place them
         mine = local.t().contiguous()
         slabs = [torch.empty((b, s), dtype=local.dtype, device=local.device) for s in sizes]
@@ -122,6 +132,15 @@ class Comm:
             out.copy_(full)
             return out
         b = full.shape[1]
+        cols_ok = all(t[:, j].is_contiguous() for t in (full, out) for j in range(b))
+        if cols_ok and b <= 4:
+            # as allgather_rows: slices of contiguous columns reduced straight
+            # into this rank's column (no transposes or staging copies)
+            for j in range(b):
+                col = full[:, j]
+                views = [col[int(bounds[p]):int(bounds[p + 1])] for p in range(self.world)]
+                tdist.reduce_scatter(out[:, j], views, op=tdist.ReduceOp.SUM, group=self.group)
+            return out
         slabs = [full[int(bounds[p]):int(bounds[p + 1]), :].t().contiguous() for p in range(self.world)]
         mine = torch.empty_like(slabs[self.rank])
         tdist.reduce_scatter(mine, slabs, op=tdist.ReduceOp.SUM, group=self.group)

@@ -356,3 +356,36 @@ def test_four_rank_gloo_solve(tmp_path, key, kw, k, target, eps, gold, stage2):
         want = np.sort(np.linalg.svd(dense, compute_uv=False))[:k]
         assert np.abs(o["sigma"] - want).max() <= max(10 * eps, 1e-12) * max(1.0, want.max()) * 10
     assert (int(o["mv2"]) > 0) == stage2
+
+
+def _collective_worker(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1607_01404_b200.dist import Comm
+        comm = Comm()
+        rows = 6 * world
+        bounds = np.arange(world + 1) * 6          # gloo gathers equal slices only; NCCL takes uneven ones
+        for b in (1, 4, 6):                        # 1, 4: per-column in-place path; 6: slab path
+            loc = torch.zeros((b, 6), dtype=torch.float64).t()   # column-major, as device blocks
+            loc.copy_(torch.arange(6 * b, dtype=torch.float64).reshape(6, b) + 100 * rank)
+            full = torch.zeros((b, rows), dtype=torch.float64).t()
+            comm.allgather_rows(loc, bounds, full)
+            want = torch.cat([torch.arange(6 * b, dtype=torch.float64).reshape(6, b) + 100 * p for p in range(world)])
+            assert torch.equal(full, want), (rank, b)
+            part = torch.zeros((b, rows), dtype=torch.float64).t()
+            part.copy_(torch.arange(rows * b, dtype=torch.float64).reshape(rows, b) * (rank + 1))
+            out = torch.zeros((b, 6), dtype=torch.float64).t()
+            comm.reduce_scatter_rows(part, bounds, out)
+            tot = torch.arange(rows * b, dtype=torch.float64).reshape(rows, b) * (world * (world + 1) // 2)
+            assert torch.equal(out, tot[6 * rank:6 * rank + 6]), (rank, b)
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_row_collectives_in_place_columns():
+    """allgather_rows / reduce_scatter_rows on column-major blocks: the
+    per-column in-place path (b <= 4, no staging copies) and the slab path
+    give the concatenation / the summed slice, 3 gloo ranks."""
+    mp.spawn(_collective_worker, args=(3, _free_port()), nprocs=3, join=True)
