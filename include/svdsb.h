@@ -54,7 +54,9 @@ int64_t svdsb_launch_count(void);
  * is n launches the host no longer makes one by one. */
 int64_t svdsb_note_launches(int64_t n);
 /* Kernel-variant knob for measurement tools (key < 16; value 0 = default
- * dispatch).  Not part of the reference interface. */
+ * dispatch).  Not part of the reference interface.  Set it before the
+ * first solve: CUDA graphs captured earlier keep the kernels they were
+ * captured with. */
 int svdsb_tune_set(int key, int value);
 
 /* Status plumbing: asynchronous device->host copy on `stream` (dst should be

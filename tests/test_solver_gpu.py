@@ -225,3 +225,52 @@ def test_graph_cache_across_matrices_and_repeats():
         want_sig, want_mv = plain[i % 2]
         assert mv == want_mv
         assert np.array_equal(sig, want_sig)
+
+
+@pytest.mark.parametrize("key", ["c4", "c2"])
+def test_streamed_kernels_inside_iteration_graphs(key):
+    """The TMA-streamed Gram / Ritz / restart kernels (forced at every size
+    with svdsb_tune_set key 15 = 2; the default takes them from 2^18 rows)
+    inside the captured block (c4 generator, b = 4) and single-column (c2)
+    iterations: the graphed solve equals the graph-free one bit for bit, and
+    both agree with the register-tiled kernels' solve within the tolerance
+    (the streamed Gram sums in a different, fixed order)."""
+    from paper_1607_01404_b200 import SparseMatrixCsr, SvdsConfig, _lib, jacobi_precond_on_normal, svds_solve, workloads
+    from paper_1607_01404_b200.eigensolver import DavidsonSolver
+    wl = workloads.CONFIGS[key]
+    m, n, r, c, v = wl.build(**workloads.SMALL[key])
+    a = SparseMatrixCsr.from_coo(m, n, r, c, v)
+    pre = jacobi_precond_on_normal(a, side="auto") if wl.precond else None
+
+    def solve():
+        res = svds_solve(a, precond=pre, cfg=SvdsConfig(num_svals=wl.k, target=wl.which, eps=wl.tol,
+                                                        max_block_size=wl.block, seed=0))
+        assert res.converged.all(), (res.status, res.rnorms)
+        return res.sigma.copy(), res.stats.stage1_matvecs, res.stats.graphs_captured
+
+    from paper_1607_01404_b200 import eigensolver as es
+    saved = DavidsonSolver.use_graphs
+    try:
+        # cached workspaces keep the iteration graphs they captured, kernels
+        # included: drop them whenever the variant changes
+        es._POOL.clear()
+        _lib.call("svdsb_tune_set", 15, 1)
+        ref_sig, ref_mv, _ = solve()
+        es._POOL.clear()
+        _lib.call("svdsb_tune_set", 15, 2)
+        sig_g, mv_g, graphs = solve()
+        DavidsonSolver.use_graphs = False
+        sig_p, mv_p, _ = solve()
+    finally:
+        DavidsonSolver.use_graphs = saved
+        _lib.call("svdsb_tune_set", 15, 0)
+        es._POOL.clear()
+    assert graphs > 0
+    assert mv_g == mv_p and np.array_equal(sig_g, sig_p)
+    a_norm = float(max(ref_sig.max(), sig_g.max())) if wl.which == "largest" else None
+    if a_norm is None:
+        import scipy.sparse as sp
+        import scipy.sparse.linalg as spla
+        a_norm = float(spla.svds(sp.csr_matrix((v, (r, c)), shape=(m, n)), k=1, return_singular_vectors=False)[0])
+    assert np.abs(sig_g - ref_sig).max() <= max(wl.tol * a_norm, 1e-10 * ref_sig.max())
+    assert abs(mv_g - ref_mv) <= 0.2 * ref_mv + 8
