@@ -1,7 +1,7 @@
 """A/B of the tall-skinny kernels (register-tiled vs streamed, svdsb_tune_set
 key 15) at config-4 (N = 1 M) and config-3 (N = 4.1 M) basis sizes.
 python tools/dense_ab.py [out.json]"""
-import sys, json
+import os, sys, json
 import numpy as np, torch
 sys.path.insert(0, '.')
 from paper_1607_01404_b200 import _lib
@@ -25,7 +25,8 @@ def timeit(fn, reps=15):
 
 ctx = dv.context()
 out = {}
-for N in (1_000_000, 4_096_000):
+SIZES = [int(x) for x in os.environ.get('DENSE_AB_N', '1000000,4096000').split(',')]
+for N in SIZES:
     g = 35
     V = dv.new_block(N, g); W = dv.new_block(N, g)
     V.normal_(); W.normal_()
