@@ -53,7 +53,7 @@ int64_t svdsb_launch_count(void);
 /* Adds n to that counter: a CUDA-graph replay of n captured library kernels
  * is n launches the host no longer makes one by one. */
 int64_t svdsb_note_launches(int64_t n);
-/* Kernel-variant knob for measurement tools (key < 16; value 0 = default
+/* Kernel-variant knob for measurement tools (key < 17; value 0 = default
  * dispatch).  Not part of the reference interface.  Set it before the
  * first solve: CUDA graphs captured earlier keep the kernels they were
  * captured with. */

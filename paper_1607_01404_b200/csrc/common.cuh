@@ -183,8 +183,11 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // candidates per thread, more shared-memory loads per FMA: 219 vs 195 us at
 // N = 1 M, kept for measurement; 4: sixteen warps of the same shape, <= 128
 // registers: 215 us).
-constexpr int kTuneKeys = 16;
-inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+// Key 16: kernel order of a transposed b = 4 part (0: short rows first; 1:
+// long rows, chunk path, first -- they stream the operand block into L2 for
+// the short rows' scattered gathers; no gain on config 4).
+constexpr int kTuneKeys = 17;
+inline int g_tune[kTuneKeys] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 
 #define SVDSB_LAUNCH_PDL(...)                                             \
   do {                                                                    \

@@ -894,6 +894,30 @@ def test_column_blocked_transpose(b, accum, rng, monkeypatch):
         _lib.call("svdsb_tune_set", 13, 0)
 
 
+def test_column_blocked_transpose_long_rows_first(rng, monkeypatch):
+    """Kernel order of a transposed b = 4 part (svdsb_tune_set key 16): long
+    rows before short rows gives the same bits (disjoint rows per part)."""
+    monkeypatch.setenv("SVDSB_T_BLOCK_ROWS", "997")
+    from paper_1607_01404_b200 import SparseMatrixCsr, _lib
+    m, n, b = 5000, 320, 4
+    rows = np.concatenate([np.repeat(np.arange(m), 3), rng.integers(0, m, 9000)])
+    cols = np.concatenate([rng.integers(0, 300, 3 * m), rng.integers(0, 3, 9000)])   # 3 heavy (chunked) columns
+    vals = rng.standard_normal(rows.size)
+    rp, ci, va = ocsr.csr_from_coo(m, n, rows, cols, vals)
+    y = rng.standard_normal((m, b))
+    outs = []
+    for key in (0, 1):
+        a = SparseMatrixCsr(m, n, rp, ci, va)
+        _lib.call("svdsb_tune_set", 16, key)
+        try:
+            outs.append(_spmv_dev(a, y, True))
+        finally:
+            _lib.call("svdsb_tune_set", 16, 0)
+    assert np.array_equal(outs[0], outs[1])
+    want = ocsr.spmv(m, n, rp, ci, va, y, transpose=True)
+    assert np.abs(outs[1] - want).max() <= 1e-12 * np.abs(want).max()
+
+
 def _test_column_blocked_rest(a, rp, ci, va, m, n, b, y, got, rng):
     from paper_1607_01404_b200 import SvdOperator, make_normal_operator
     want = ocsr.spmv(m, n, rp, ci, va, y, transpose=True)
