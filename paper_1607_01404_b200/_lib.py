@@ -139,6 +139,11 @@ def load():
         fn.restype = res
         fn.argtypes = args
     _lib = lib
+    # measurement knob: SVDSB_TUNE="15=2,7=1" presets svdsb_tune_set keys at load
+    for kv in filter(None, os.environ.get("SVDSB_TUNE", "").split(",")):
+        key, val = kv.split("=")
+        if lib.svdsb_tune_set(int(key), int(val)) != 0:
+            raise ValueError("SVDSB_TUNE: bad entry %r" % kv)
     return lib
 
 
