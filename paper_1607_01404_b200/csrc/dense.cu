@@ -1703,7 +1703,9 @@ namespace svdsb {
 // b >= 2 Gram through gram_stream_kernel (one persistent CTA per SM, tiles
 // by TMA); false when a tensor map cannot be built (the caller falls back).
 static bool gram_stream(svdsb_ctx *ctx, int64_t dim, const ColSet &s, const double *y, int64_t ldy, int b, double *c,
-                        int64_t ldc, double *norms2, cudaStream_t st) {
+                        int64_t ldc, double *norms2, cudaStream_t st, const double *gate = nullptr,
+                        HInsert hi = HInsert{}) {
+  if (b == 1) ldy = (dim + 1) & ~(int64_t)1;  // one column: the stride is never used, the map wants it even
   GramMaps maps;
   int cap = 4;
   for (int k = 0; k < s.nblk; ++k) {
@@ -1728,12 +1730,61 @@ static bool gram_stream(svdsb_ctx *ctx, int64_t dim, const ColSet &s, const doub
     if (!make_map2d(&maps.y, y + (int64_t)j0 * ldy, dim, nb, ldy, kGsRows, 4)) return false;
     if (launch_k(gram_stream_kernel, dim3(gxs, 1, 1), dim3(kStreamThreads, 1, 1), sh, st, maps, dim, s, nb,
                  c + (int64_t)j0 * ldc, ldc, norms2 ? norms2 + j0 : (double *)nullptr, ctx->partials, take_ticket(ctx),
-                 stream_evict_first(dim, s.total)) != cudaSuccess) {
+                 stream_evict_first(dim, s.total), gate, hi) != cudaSuccess) {
       cudaGetLastError();
       return false;  // nothing written yet for this chunk: the register-tiled kernels redo the whole Gram
     }
     bump_launches();
   }
+  return true;
+}
+
+constexpr int kPsCap = 52;  // stage capacity in columns of project_stream_kernel (2 stages of 256 rows)
+
+// b <= 4 projection through project_stream_kernel; false when it does not
+// apply (the caller falls back to the register kernels; nothing was written).
+static bool project_stream(svdsb_ctx *ctx, int64_t dim, const ColSet &s, const double *c, int64_t ldc, double *y,
+                           int64_t ldy, int nb, double *norms2, cudaStream_t st, double *dgks = nullptr) {
+  if (nb < 1 || nb > 4 || s.total < 1 || s.total > kGsMaxX || !aligned16(y) || (nb > 1 && (ldy & 1))) return false;
+  ProjMaps maps;
+  int cap = 4;
+  for (int k = 0; k < s.nblk; ++k) {
+    if (!make_map2d(&maps.x[k], s.base[k], dim, s.cols[k], s.ld[k], kPsRows, kGsBox)) return false;
+    cap += (s.cols[k] + kGsBox - 1) / kGsBox * kGsBox;
+  }
+  for (int k = s.nblk; k < SVDSB_MAX_BLOCKS; ++k) maps.x[k] = maps.x[0];
+  if (cap > kPsCap) return false;
+  if (!make_map2d(&maps.y, y, dim, nb, nb == 1 ? ((dim + 1) & ~(int64_t)1) : ldy, kPsRows, 4)) return false;
+  static bool attr = false;
+  if (!attr) {
+    const int mx = (int)(sizeof(double) * kPsStages * kPsCap * kPsRows);
+    if (cudaFuncSetAttribute(project_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+        cudaFuncSetAttribute(project_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+        cudaFuncSetAttribute(project_stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+        cudaFuncSetAttribute(project_stream_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    attr = true;
+  }
+  const size_t sh = sizeof(double) * (size_t)kPsStages * cap * kPsRows;
+  const dim3 grid(stream_grid_tiles(dim, kPsRows), 1, 1), block(kStreamThreads, 1, 1);
+  const int ef = stream_evict_first(dim, s.total);
+  auto *tk = take_ticket(ctx);
+  cudaError_t e;
+  if (nb == 1)
+    e = launch_k(project_stream_kernel<1>, grid, block, sh, st, maps, dim, s, c, ldc, y, ldy, norms2, ctx->partials, tk, ef, dgks);
+  else if (nb == 2)
+    e = launch_k(project_stream_kernel<2>, grid, block, sh, st, maps, dim, s, c, ldc, y, ldy, norms2, ctx->partials, tk, ef, dgks);
+  else if (nb == 3)
+    e = launch_k(project_stream_kernel<3>, grid, block, sh, st, maps, dim, s, c, ldc, y, ldy, norms2, ctx->partials, tk, ef, dgks);
+  else
+    e = launch_k(project_stream_kernel<4>, grid, block, sh, st, maps, dim, s, c, ldc, y, ldy, norms2, ctx->partials, tk, ef, dgks);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  bump_launches();
   return true;
 }
 
@@ -1750,6 +1801,10 @@ int gram_impl(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, co
   const int gx = grid_rows(dim);
   if (s.total == 0) {
     if (norms2) return svdsb_col_norms2(ctx, dim, y, ldy, b, norms2, stream);
+    return SVDSB_OK;
+  }
+  if (b == 1 && colset_vec_ok(s) && aligned16(y) && s.total <= kGsMaxX && stream_ok(dim) && g_tune[15] != 5 &&
+      gram_stream(ctx, dim, s, y, ldy, 1, c, ldc, norms2, st, nullptr, hi)) {
     return SVDSB_OK;
   }
   if (b == 1 && colset_vec_ok(s) && aligned16(y)) {
@@ -1832,6 +1887,12 @@ int svdsb_project_out(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const
     double *yy = y + (int64_t)j0 * ldy;
     const double *cc = c + (int64_t)j0 * ldc;
     double *nn = norms2 ? norms2 + j0 : nullptr;
+    // one and two columns (measured: 70 -> 59 us and 74 -> 64 us at N = 1 M, 94 % of HBM at
+    // 4.1 M; four columns are faster on project4_vec_kernel: 78 vs 88 us); key 15 = 2 forces all
+    if ((bb <= 2 || (bb <= 4 && g_tune[15] == 2)) && colset_vec_ok(s) && stream_ok(dim) && g_tune[15] != 5 &&
+        project_stream(ctx, dim, s, cc, ldc, yy, ldy, bb, nn, st)) {
+      continue;
+    }
     if (bb == 1 && colset_vec_ok(s) && aligned16(yy)) {
       size_t sh = sizeof(double) * std::max(s.total, 1);
       SVDSB_LAUNCH_PDL(project1_vec_kernel, grid_for(project1_vec_kernel, dim, sh), kThreads, sh, st, dim, s, cc, yy,
@@ -2315,6 +2376,20 @@ int svdsb_cgs_pass(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *x
   SVDSB_CHECK_ARG(colset_vec_ok(s) && aligned16(v), "svdsb_cgs_pass: operands must be 16-byte aligned");
   cudaStream_t st = as_stream(stream);
   double *n0 = first_pass ? state + 6 : nullptr;
+  if (s.total <= kGsMaxX && stream_ok(dim) && g_tune[15] != 5) {
+    // both halves of the pass on the streamed kernels (or neither: a pass
+    // whose Gram ran must be followed by its projection)
+    ProjMaps probe;
+    bool ok = aligned16(v);
+    for (int k = 0; ok && k < s.nblk; ++k) ok = make_map2d(&probe.x[0], s.base[k], dim, s.cols[k], s.ld[k], kPsRows, kGsBox);
+    int cap = 4;
+    for (int k = 0; k < s.nblk; ++k) cap += (s.cols[k] + kGsBox - 1) / kGsBox * kGsBox;
+    if (ok && cap <= kPsCap && gram_stream(ctx, dim, s, v, 0, 1, cwork, s.total, n0, st, state, HInsert{})) {
+      if (project_stream(ctx, dim, s, cwork, s.total, v, 0, 1, state + 7, st, state)) return SVDSB_OK;
+      set_error("svdsb_cgs_pass: streamed projection failed after its Gram");
+      return SVDSB_ERR_CUDA;
+    }
+  }
   if (s.total <= 16) {
     dim3 grid(grid_for(gram1_vec_kernel<16>, dim, 0), 1, 1);
     SVDSB_LAUNCH_PDL(gram1_vec_kernel<16>, grid, kThreads, 0, st, dim, s, v, cwork, n0, ctx->partials,

@@ -275,7 +275,8 @@ struct GramMaps {
 // warp w owns basis columns w, w + 8, ..., each lane two row pairs of a tile.
 __global__ void __launch_bounds__(kStreamThreads, 1)
 gram_stream_kernel(const __grid_constant__ GramMaps maps, int64_t dim, ColSet xs, int nb, double *c, int64_t ldc,
-                   double *norms2, double *partials, unsigned int *ticket, int evict_first) {
+                   double *norms2, double *partials, unsigned int *ticket, int evict_first, const double *gate,
+                   HInsert hi) {
   constexpr int R = kGsRows, NS = kGsStages, MC = kGsMaxX / 8, NW = kStreamConsumers / 32;
   extern __shared__ __align__(1024) double gs_dyn[];
   __shared__ uint64_t full[NS], empty[NS];
@@ -298,6 +299,7 @@ gram_stream_kernel(const __grid_constant__ GramMaps maps, int64_t dim, ColSet xs
     }
   }
   pdl_wait();
+  if (gate != nullptr && gate[0] == 0.0) return;  // device-side DGKS: column already final (every thread leaves)
   __syncthreads();
   const int64_t ntile = (dim + R - 1) / R;
   int64_t t0, t1;
@@ -383,9 +385,142 @@ gram_stream_kernel(const __grid_constant__ GramMaps maps, int64_t dim, ColSet xs
   fold_parts(partials, gridDim.x, kGsOut, kGsOut, [&](int, int, int k, double sum) {
     if (k < kGsMaxX * 4) {
       const int i = k / 4, j = k % 4;
-      if (i < na && j < nb) c[i + (int64_t)j * ldc] = sum;
+      if (i < na && j < nb) {
+        c[i + (int64_t)j * ldc] = sum;
+        if (hi.h != nullptr && j == 0 && i <= hi.g) {  // one column: H(i, g) = H(g, i), as gram1_vec_kernel
+          hi.h[i + (int64_t)hi.g * hi.ldh] = sum;
+          hi.h[hi.g + (int64_t)i * hi.ldh] = sum;
+        }
+      }
     } else if (norms2 != nullptr && k - kGsMaxX * 4 < nb) {
       norms2[k - kGsMaxX * 4] = sum;
     }
+  });
+}
+
+
+constexpr int kPsRows = 256;   // rows per tile: one per consumer thread
+constexpr int kPsStages = 2;
+
+// Y -= X C (+ |Y_j|^2 after) for NB <= 4 columns of Y and up to 40 basis
+// columns: stage layout as gram_stream_kernel with 256-row tiles, one row
+// per consumer thread; per element the fma chain of project_kernel (basis
+// index ascending), so Y is bit-identical to the register kernels.  NB = 1
+// carries the device-side DGKS gate and decision of project1_vec_kernel.
+struct ProjMaps {
+  CUtensorMap x[SVDSB_MAX_BLOCKS];  // box kPsRows x kGsBox
+  CUtensorMap y;                    // box kPsRows x 4, extent dim x NB
+};
+
+template <int NB>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+project_stream_kernel(const __grid_constant__ ProjMaps maps, int64_t dim, ColSet xs, const double *__restrict__ cmat,
+                      int64_t ldc, double *y, int64_t ldy, double *norms2, double *partials, unsigned int *ticket,
+                      int evict_first, double *dgks) {
+  constexpr int R = kPsRows, NS = kPsStages, NW = kStreamConsumers / 32;
+  extern __shared__ __align__(1024) double ps_dyn[];
+  __shared__ uint64_t full[NS], empty[NS];
+  __shared__ int scol[kGsMaxX];
+  __shared__ double csh[kGsMaxX * NB];
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int na = xs.total;
+  int ycol = 0;
+  for (int k = 0; k < xs.nblk; ++k) ycol += (xs.cols[k] + kGsBox - 1) / kGsBox * kGsBox;
+  const int stage_d = (ycol + 4) * R;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    int i = 0, off = 0;
+    for (int k = 0; k < xs.nblk; ++k) {
+      for (int q = 0; q < xs.cols[k]; ++q) scol[i++] = off + q;
+      off += (xs.cols[k] + kGsBox - 1) / kGsBox * kGsBox;
+    }
+  }
+  pdl_wait();
+  if (dgks != nullptr && dgks[0] == 0.0) return;
+  for (int k = tid; k < na * NB; k += kStreamThreads) csh[k] = cmat[k / NB + (int64_t)(k % NB) * ldc];
+  __syncthreads();
+  const int64_t ntile = (dim + R - 1) / R;
+  int64_t t0, t1;
+  stream_tiles(ntile, blockIdx.x, gridDim.x, t0, t1);
+  double nacc[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) nacc[j] = 0.0;
+
+  if (wid == NW) {
+    if (lane == 0) {
+      const uint64_t policy = evict_first_policy();
+      const bool ef = evict_first != 0;
+      int64_t it = 0;
+      for (int64_t t = t0; t < t1; ++t, ++it) {
+        const int s = (int)(it % NS);
+        const int64_t k = it / NS;
+        if (k > 0) mbar_wait(&empty[s], (unsigned)((k - 1) & 1));
+        double *st = ps_dyn + (size_t)s * stage_d;
+        mbar_expect_tx(&full[s], (unsigned)(stage_d * sizeof(double)));
+        int off = 0;
+        for (int kb = 0; kb < xs.nblk; ++kb)
+          for (int q = 0; q < xs.cols[kb]; q += kGsBox, off += kGsBox)
+            tma_tile_2d(st + off * R, &maps.x[kb], (int)(t * R), q, &full[s], ef, policy);
+        tma_tile_2d(st + off * R, &maps.y, (int)(t * R), 0, &full[s], false, policy);
+      }
+    }
+  } else {
+    int64_t it = 0;
+    for (int64_t t = t0; t < t1; ++t, ++it) {
+      const int s = (int)(it % NS);
+      mbar_wait(&full[s], (unsigned)((it / NS) & 1));
+      const double *st = ps_dyn + (size_t)s * stage_d + tid;
+      const int64_t row = t * R + tid;
+      double yv[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) yv[j] = st[(ycol + j) * R];
+      for (int i0 = 0; i0 < na; i0 += 8) {
+        double xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = st[scol[min(i0 + u, na - 1)] * R];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (i0 + u < na) {
+#pragma unroll
+            for (int j = 0; j < NB; ++j) yv[j] = fma(-xv[u], csh[(i0 + u) * NB + j], yv[j]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (row < dim) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          y[row + (int64_t)j * ldy] = yv[j];
+          nacc[j] = fma(yv[j], yv[j], nacc[j]);
+        }
+      }
+    }
+  }
+  pdl_trigger();
+  if (norms2 == nullptr) return;
+  __shared__ double red[NW][NB];
+  if (wid < NW) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const double sum = warp_sum(nacc[j]);
+      if (lane == 0) red[wid][j] = sum;
+    }
+  }
+  __syncthreads();
+  if (tid < NB) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += red[w][tid];
+    partials[(int64_t)blockIdx.x * NB + tid] = t;
+  }
+  if (!last_cta(ticket)) return;
+  fold_parts(partials, gridDim.x, NB, NB, [&](int j, int, int, double sum) {
+    norms2[j] = sum;
+    if (NB == 1 && dgks != nullptr) dgks_decide(dgks);
   });
 }

@@ -1276,7 +1276,7 @@ def test_restart_inplace_streamed_bit_identical(dim, g, s, rng):
 
 
 @pytest.mark.parametrize("dim", [1, 127, 129, 70_001, 300_002])
-@pytest.mark.parametrize("g,b", [(35, 4), (40, 4), (7, 2), (20, 3), (1, 4), (33, 7)])
+@pytest.mark.parametrize("g,b", [(35, 4), (40, 4), (7, 2), (20, 3), (1, 4), (33, 7), (35, 1), (3, 1)])
 def test_gram_streamed(dim, g, b, rng):
     """gram_stream_kernel against fp64 numpy and the register-tiled kernel
     (different summation trees: rounding-level agreement), norms included;
@@ -1303,3 +1303,36 @@ def test_gram_streamed(dim, g, b, rng):
         assert np.abs(got - want).max() <= tol
         assert np.allclose(n2, (y ** 2).sum(0), rtol=1e-13)
     assert np.array_equal(outs[1][0], outs[2][0]) and np.array_equal(outs[1][1], outs[2][1])
+
+
+@pytest.mark.parametrize("dim", [1, 255, 257, 70_001, 300_002])
+@pytest.mark.parametrize("g1,g2,b", [(35, 0, 1), (7, 30, 4), (40, 0, 2), (3, 5, 3), (1, 0, 1), (20, 13, 6)])
+def test_project_streamed_bit_identical(dim, g1, g2, b, rng):
+    """project_stream_kernel against the register kernels: Y -= X C bit for
+    bit (same fma chain, basis index ascending, one or two basis blocks),
+    |Y_j|^2 to rounding; b = 6 runs as 4 + 2 columns."""
+    from paper_1607_01404_b200 import _lib
+    dv = _dev()
+    ctx = dv.context()
+    a1 = rng.standard_normal((dim, g1))
+    a2 = rng.standard_normal((dim, max(g2, 1)))
+    y = rng.standard_normal((dim, b))
+    c = rng.standard_normal((g1 + g2, b)) * 0.1
+    X1, X2 = dv.to_device_block(a1), dv.to_device_block(a2)
+    blocks = [X1, X2] if g2 else [X1]
+    outs = []
+    try:
+        for key in (1, 2):
+            _lib.call("svdsb_tune_set", 15, key)
+            Y = dv.to_device_block(y)
+            C = dv.to_device_block(c)
+            nrm = torch.zeros(b, dtype=torch.float64, device=ctx.device)
+            dv.project_out(ctx, dim, blocks, C, Y, norms2=nrm)
+            outs.append((dv.to_host(Y), nrm.cpu().numpy()))
+    finally:
+        _lib.call("svdsb_tune_set", 15, 0)
+    assert np.array_equal(outs[0][0], outs[1][0])
+    want = y - np.hstack([a1, a2[:, :g2]]) @ c
+    assert np.abs(outs[1][0] - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+    assert np.allclose(outs[1][1], (want ** 2).sum(0), rtol=1e-12, atol=1e-300)
+    assert np.allclose(outs[1][1], outs[0][1], rtol=1e-12, atol=1e-300)
