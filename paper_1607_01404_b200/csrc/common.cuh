@@ -182,8 +182,9 @@ int ritz_impl(svdsb_ctx *ctx, int64_t dim, const double *v, int64_t ldv, const d
 // with the twelve-warp Ritz variant for 16 < p <= 24 -- two rows x six
 // candidates per thread, more shared-memory loads per FMA: 219 vs 195 us at
 // N = 1 M, kept for measurement; 4: sixteen warps of the same shape, <= 128
-// registers: 215 us; 5: streamed b >= 2 Gram / Ritz / restart only, the
-// one-column Gram and the projections on the register kernels).
+// registers: 215 us; 5: no streamed projection; 6: as 0 plus the one-column
+// Gram / projection / CGS pass on the streamed kernels -- faster alone,
+// slower inside the solves, see stream_one_col in dense.cu).
 // Key 16: kernel order of a transposed b = 4 part (0: short rows first; 1:
 // long rows, chunk path, first -- they stream the operand block into L2 for
 // the short rows' scattered gathers; no gain on config 4).

@@ -1613,6 +1613,15 @@ static bool stream_ok(int64_t dim) {
   return dim >= (int64_t)1 << 18;
 }
 
+// One-column Gram / projection / CGS pass on the streamed kernels: opt-in
+// (key 15 = 2 or 6).  Alone they are faster at g = 35 (N = 1 M: 78 -> 68 us
+// and 71 -> 59 us; 87 % / 94 % of HBM at 4.1 M) but inside the solves they
+// lose: most CGS passes of a block iteration are gated off on the device,
+// and a gated streamed launch (288 threads, 180 KB of shared memory) costs
+// more than a gated register launch -- config 4: 0.376 -> 0.387 s; config 3
+// at g = 25: H-column Gram 153 -> 161 us.
+static bool stream_one_col(int64_t dim) { return (g_tune[15] == 2 || g_tune[15] == 6) && stream_ok(dim); }
+
 static int stream_grid_tiles(int64_t dim, int rows) {
   const int64_t nt = (dim + rows - 1) / rows;
   return (int)std::min<int64_t>(num_sms(), std::max<int64_t>(nt, 1));
@@ -1803,7 +1812,7 @@ int gram_impl(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *xs, co
     if (norms2) return svdsb_col_norms2(ctx, dim, y, ldy, b, norms2, stream);
     return SVDSB_OK;
   }
-  if (b == 1 && colset_vec_ok(s) && aligned16(y) && s.total <= kGsMaxX && stream_ok(dim) && g_tune[15] != 5 &&
+  if (b == 1 && colset_vec_ok(s) && aligned16(y) && s.total <= kGsMaxX && stream_one_col(dim) &&
       gram_stream(ctx, dim, s, y, ldy, 1, c, ldc, norms2, st, nullptr, hi)) {
     return SVDSB_OK;
   }
@@ -1887,9 +1896,10 @@ int svdsb_project_out(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const
     double *yy = y + (int64_t)j0 * ldy;
     const double *cc = c + (int64_t)j0 * ldc;
     double *nn = norms2 ? norms2 + j0 : nullptr;
-    // one and two columns (measured: 70 -> 59 us and 74 -> 64 us at N = 1 M, 94 % of HBM at
-    // 4.1 M; four columns are faster on project4_vec_kernel: 78 vs 88 us); key 15 = 2 forces all
-    if ((bb <= 2 || (bb <= 4 && g_tune[15] == 2)) && colset_vec_ok(s) && stream_ok(dim) && g_tune[15] != 5 &&
+    // two columns: 74 -> 64 us at N = 1 M (four are faster on project4_vec_kernel: 78 vs 88 us;
+    // one column is opt-in, see stream_one_col); key 15 = 2 forces every width
+    if (((bb == 2 && stream_ok(dim) && g_tune[15] != 5) || (bb <= 4 && g_tune[15] == 2) || (bb == 1 && stream_one_col(dim))) &&
+        colset_vec_ok(s) &&
         project_stream(ctx, dim, s, cc, ldc, yy, ldy, bb, nn, st)) {
       continue;
     }
@@ -2376,7 +2386,7 @@ int svdsb_cgs_pass(svdsb_ctx *ctx, int64_t dim, int nblk, const double *const *x
   SVDSB_CHECK_ARG(colset_vec_ok(s) && aligned16(v), "svdsb_cgs_pass: operands must be 16-byte aligned");
   cudaStream_t st = as_stream(stream);
   double *n0 = first_pass ? state + 6 : nullptr;
-  if (s.total <= kGsMaxX && stream_ok(dim) && g_tune[15] != 5) {
+  if (s.total <= kGsMaxX && stream_one_col(dim)) {
     // both halves of the pass on the streamed kernels (or neither: a pass
     // whose Gram ran must be followed by its projection)
     ProjMaps probe;
