@@ -2840,9 +2840,18 @@ __global__ void iota_kernel(int64_t n, int *__restrict__ out) {
   if (i < n) out[i] = (int)i;
 }
 
-__global__ void count_kernel(int64_t nnz, const int *__restrict__ keys, int *__restrict__ counts) {
+// row_ptr from SORTED keys: row_ptr[c] = number of keys < c, written by the
+// thread at the first position whose key is >= c (thread nnz closes the
+// tail).  The same values as a histogram + exclusive scan, without the
+// histogram's atomics: on config 4 a fifth of the 173 M nonzeros share ten
+// columns and the atomic counts took 25 ms.
+__global__ void bounds_from_sorted_kernel(int64_t nnz, const int *__restrict__ keys, int nrows,
+                                          int *__restrict__ row_ptr) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < nnz) atomicAdd(counts + keys[i], 1);
+  if (i > nnz) return;
+  const int lo = i == 0 ? 0 : keys[i - 1] + 1;
+  const int hi = i == nnz ? nrows : keys[i];
+  for (int c = lo; c <= hi; ++c) row_ptr[c] = (int)i;
 }
 
 __global__ void gather_t_kernel(int64_t nnz, const int *__restrict__ perm, const int *__restrict__ rows,
@@ -2876,13 +2885,11 @@ static int build_transpose(const CsrPart &a, CsrPart &at, cudaStream_t st) {
   SVDSB_CUDA(alloc_pad(&at.val, std::max<int64_t>(nnz, 1), st));
   SVDSB_CUDA(cudaMemsetAsync(at.row_ptr, 0, sizeof(int) * (at.rows + 1), st));
   if (nnz > 0) {
-    int *rows = nullptr, *idx = nullptr, *keys_out = nullptr, *perm = nullptr, *counts = nullptr;
+    int *rows = nullptr, *idx = nullptr, *keys_out = nullptr, *perm = nullptr;
     SVDSB_CUDA(palloc(&rows, sizeof(int) * nnz, st));
     SVDSB_CUDA(palloc(&idx, sizeof(int) * nnz, st));
     SVDSB_CUDA(palloc(&keys_out, sizeof(int) * nnz, st));
     SVDSB_CUDA(palloc(&perm, sizeof(int) * nnz, st));
-    SVDSB_CUDA(palloc(&counts, sizeof(int) * (at.rows + 1), st));
-    SVDSB_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * (at.rows + 1), st));
     expand_rows_kernel<<<grid1(a.rows), 256, 0, st>>>(a.rows, a.row_ptr, rows);
     SVDSB_LAUNCHED();
     iota_kernel<<<grid1(nnz), 256, 0, st>>>(nnz, idx);
@@ -2897,15 +2904,9 @@ static int build_transpose(const CsrPart &a, CsrPart &at, cudaStream_t st) {
     bump_launches();
     gather_t_kernel<<<grid1(nnz), 256, 0, st>>>(nnz, perm, rows, a.val, at.col, at.val);
     SVDSB_LAUNCHED();
-    // row_ptr of A^T: counts per column, exclusive scan into [0, rows]
-    count_kernel<<<grid1(nnz), 256, 0, st>>>(nnz, a.col, counts);
+    // row_ptr of A^T from the sorted column keys
+    bounds_from_sorted_kernel<<<grid1(nnz + 1), 256, 0, st>>>(nnz, keys_out, (int)at.rows, at.row_ptr);
     SVDSB_LAUNCHED();
-    size_t scan_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts, at.row_ptr, (int)(at.rows + 1), st);
-    void *scan_tmp = nullptr;
-    SVDSB_CUDA(palloc(&scan_tmp, scan_bytes, st));
-    SVDSB_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, at.row_ptr, (int)(at.rows + 1), st));
-    bump_launches();
     tmark("T launch");
     SVDSB_CUDA(cudaStreamSynchronize(st));
     tmark("T sync");
@@ -2913,9 +2914,7 @@ static int build_transpose(const CsrPart &a, CsrPart &at, cudaStream_t st) {
     pfree(idx, st);
     pfree(keys_out, st);
     pfree(perm, st);
-    pfree(counts, st);
     pfree(tmp, st);
-    pfree(scan_tmp, st);
   }
   at.host_row_ptr.resize(at.rows + 1);
   SVDSB_CUDA(cudaMemcpyAsync(at.host_row_ptr.data(), at.row_ptr, sizeof(int) * (at.rows + 1),
