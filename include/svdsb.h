@@ -108,6 +108,16 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n,
                                 int64_t ntrip, const int64_t *rows,
                                 const int64_t *cols, const double *vals,
                                 int flags, void *stream, svdsb_csr **out);
+/* As above, with the values possibly still being copied to the device on
+ * another stream: `vals_ready` (a cudaEvent_t recorded after that copy, or
+ * NULL) is waited on by `stream` just before the duplicate sums, the first
+ * use of `vals` -- the key build, sort and scans of the indices overlap the
+ * copy (SparseMatrixCsr.from_coo from host arrays, matio.py:63-92). */
+int svdsb_csr_create_coo_device_ev(svdsb_ctx *ctx, int64_t m, int64_t n,
+                                   int64_t ntrip, const int64_t *rows,
+                                   const int64_t *cols, const double *vals,
+                                   void *vals_ready, int flags, void *stream,
+                                   svdsb_csr **out);
 int svdsb_csr_destroy(svdsb_csr *a);
 int svdsb_csr_shape(const svdsb_csr *a, int64_t *m, int64_t *n, int64_t *nnz);
 /* Derived device layouts of a handle (tests / tools; not part of the

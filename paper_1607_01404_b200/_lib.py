@@ -43,6 +43,7 @@ _PROTOS = [
     ("svdsb_ctx_destroy", i32, [vp]),
     ("svdsb_csr_create_host", i32, [vp, i64, i64, i64, vp, vp, vp, i32, vp, ctypes.POINTER(vp)]),
     ("svdsb_csr_create_coo_device", i32, [vp, i64, i64, i64, vp, vp, vp, i32, vp, ctypes.POINTER(vp)]),
+    ("svdsb_csr_create_coo_device_ev", i32, [vp, i64, i64, i64, vp, vp, vp, vp, i32, vp, ctypes.POINTER(vp)]),
     ("svdsb_csr_destroy", i32, [vp]),
     ("svdsb_csr_shape", i32, [vp, c_int64_p, c_int64_p, c_int64_p]),
     ("svdsb_csr_layout_info", i32, [vp, i32, c_int64_p]),

@@ -3193,6 +3193,12 @@ int svdsb_csr_create_host(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nnz, con
 int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt, const int64_t *rows,
                                 const int64_t *cols, const double *vals, int flags, void *stream,
                                 svdsb_csr **out) {
+  return svdsb_csr_create_coo_device_ev(ctx, m, n, nt, rows, cols, vals, nullptr, flags, stream, out);
+}
+
+int svdsb_csr_create_coo_device_ev(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt, const int64_t *rows,
+                                   const int64_t *cols, const double *vals, void *vals_ready, int flags,
+                                   void *stream, svdsb_csr **out) {
   (void)ctx;
   SVDSB_CHECK_ARG(out != nullptr, "svdsb_csr_create_coo_device: out is NULL");
   SVDSB_CHECK_ARG(m >= 0 && n >= 0 && nt >= 0, "negative size");
@@ -3267,6 +3273,9 @@ int svdsb_csr_create_coo_device(svdsb_ctx *ctx, int64_t m, int64_t n, int64_t nt
     tmark("sync nnz");
     SVDSB_CUDA(alloc_pad(&p.col, std::max<int64_t>(nnz, 1), st));
     SVDSB_CUDA(alloc_pad(&p.val, std::max<int64_t>(nnz, 1), st));
+    // the values are first needed here: a copy still in flight on another
+    // stream has had the key build, sort and scans to finish
+    if (vals_ready != nullptr) SVDSB_CUDA(cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(vals_ready), 0));
     coo_sum_kernel<<<grid1(nt), 256, 0, st>>>(nt, n, key_s, perm, first, seg, vals, p.col, p.val, rowcnt);
     SVDSB_LAUNCHED();
     size_t sb2 = 0;

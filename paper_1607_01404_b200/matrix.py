@@ -26,6 +26,18 @@ SPMV_PROFILER = None
 _UIDS = itertools.count(1)
 
 
+_SIDE = {}
+
+
+def _side_stream(device):
+    """One extra stream per device for copies that overlap the assembly."""
+    key = torch.device(device).index
+    st = _SIDE.get(key)
+    if st is None:
+        st = _SIDE[key] = torch.cuda.Stream(device=device)
+    return st
+
+
 class DeviceCsr:
     """Owning handle to a libsvdsb CSR (A and A^T) on one device."""
 
@@ -52,8 +64,10 @@ class DeviceCsr:
         return cls(h, ctx, m, n, va.shape[0])
 
     @classmethod
-    def from_coo_device(cls, m, n, rows, cols, vals, device=None, transpose=True):
-        """rows/cols int64, vals fp64, all torch device tensors."""
+    def from_coo_device(cls, m, n, rows, cols, vals, device=None, transpose=True, vals_ready=None):
+        """rows/cols int64, vals fp64, all torch device tensors.  vals_ready:
+        a recorded torch.cuda.Event after which `vals` is complete (its copy
+        may still run on another stream while the indices are sorted)."""
         ctx = context(device)
         rows = rows.to(device=ctx.device, dtype=torch.int64).contiguous()
         cols = cols.to(device=ctx.device, dtype=torch.int64).contiguous()
@@ -61,9 +75,10 @@ class DeviceCsr:
         h = ctypes.c_void_p()
         flags = _lib.SVDSB_CSR_TRANSPOSE if transpose else 0
         with torch.cuda.device(ctx.device):
-            _lib.call("svdsb_csr_create_coo_device", ctx.handle, int(m), int(n), int(rows.numel()),
+            ev = ctypes.c_void_p(vals_ready.cuda_event) if vals_ready is not None else None
+            _lib.call("svdsb_csr_create_coo_device_ev", ctx.handle, int(m), int(n), int(rows.numel()),
                       ctypes.c_void_p(rows.data_ptr()), ctypes.c_void_p(cols.data_ptr()),
-                      ctypes.c_void_p(vals.data_ptr()), flags, ctx.stream, ctypes.byref(h))
+                      ctypes.c_void_p(vals.data_ptr()), ev, flags, ctx.stream, ctypes.byref(h))
         nnz = ctypes.c_int64()
         _lib.call("svdsb_csr_shape", h, None, None, ctypes.byref(nnz))
         return cls(h, ctx, m, n, nnz.value)
@@ -210,10 +225,24 @@ class SparseMatrixCsr:
         ctx = context(device)
         rows = rows.to(device=ctx.device, dtype=torch.int64, non_blocking=True)
         cols = cols.to(device=ctx.device, dtype=torch.int64, non_blocking=True)
-        values = values.to(device=ctx.device, dtype=torch.float64, non_blocking=True)
+        ready = None
+        if values.device.type == "cpu" and values.dtype == torch.float64 and values.numel() >= (1 << 22):
+            # large host value arrays: copied on a side stream behind the index
+            # copies, so the transfer overlaps the key build / sort / scans of
+            # the assembly, which waits for it only before the duplicate sums
+            main = torch.cuda.current_stream(ctx.device)
+            side = _side_stream(ctx.device)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                values = values.to(device=ctx.device, non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(side)
+            values.record_stream(main)
+        else:
+            values = values.to(device=ctx.device, dtype=torch.float64, non_blocking=True)
         # the range checks of matio.py:74-78 run inside the device assembly
         # (svdsb_csr_create_coo_device: same messages, ValueError)
-        dev = DeviceCsr.from_coo_device(m, n, rows, cols, values, device=ctx.device)
+        dev = DeviceCsr.from_coo_device(m, n, rows, cols, values, device=ctx.device, vals_ready=ready)
         return cls._from_device(dev)
 
     @classmethod

@@ -1336,3 +1336,27 @@ def test_project_streamed_bit_identical(dim, g1, g2, b, rng):
     assert np.abs(outs[1][0] - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
     assert np.allclose(outs[1][1], (want ** 2).sum(0), rtol=1e-12, atol=1e-300)
     assert np.allclose(outs[1][1], outs[0][1], rtol=1e-12, atol=1e-300)
+
+
+def test_from_coo_values_copied_on_side_stream(rng):
+    """from_coo of large host arrays copies the values on a side stream
+    while the indices are sorted (svdsb_csr_create_coo_device_ev waits for
+    the copy's event before the duplicate sums): the assembled CSR and its
+    stored transpose equal the oracle's bit for bit, pinned or pageable
+    inputs, three times in a row (the side stream and buffers get reused)."""
+    from paper_1607_01404_b200 import SparseMatrixCsr
+    m, n, nt = 200_000, 50_000, (1 << 22) + 12_345
+    rows = rng.integers(0, m, nt)
+    cols = rng.integers(0, n, nt)
+    cols[: nt // 8] = rng.integers(0, 4, nt // 8)          # hot columns: duplicates to sum, long A^T rows
+    vals = rng.standard_normal(nt)
+    rp, ci, va = ocsr.csr_from_coo(m, n, rows, cols, vals)
+    trp, tci, tva = ocsr.csr_from_coo(n, m, cols, rows, vals)
+    pinned = [torch.from_numpy(a).pin_memory() for a in (rows, cols, vals)]
+    for rep in range(3):
+        src = pinned if rep != 1 else (rows, cols, vals)
+        a = SparseMatrixCsr.from_coo(m, n, *src)
+        grp, gci, gva = a.device_csr().export()
+        assert np.array_equal(grp, rp) and np.array_equal(gci, ci) and np.array_equal(gva, va)
+        g2 = a.device_csr().export(transpose=True)
+        assert np.array_equal(g2[0], trp) and np.array_equal(g2[1], tci) and np.array_equal(g2[2], tva)
