@@ -1392,6 +1392,10 @@ __device__ __forceinline__ void warprow4t(int64_t row, const int *__restrict__ r
 #ifndef SVDSB_DBG_SKIP
 #define SVDSB_DBG_SKIP 0   // timing experiments only: 1 skips the mid rows, 2 the sliced rows
 #endif
+#ifndef SVDSB_EARLY_TRIGGER
+#define SVDSB_EARLY_TRIGGER 0   // timing experiment: 1 lets the transposed b = 4 kernels release their dependants at the start
+                                // (slower: the waiting dependants take slots from the running grid -- A^T.Y 1330 -> 1397 us)
+#endif
 #ifndef SVDSB_T4T_MINB
 #define SVDSB_T4T_MINB 4   // resident CTAs per SM the register budget targets (64 registers, no spills; 2: 75 registers, 1.7% slower)
 #endif
@@ -1417,6 +1421,9 @@ csr_sell4t_kernel(int64_t nq, int64_t nslice, const int *__restrict__ perm, cons
   // one warp and writes its own rows, so the assignment does not touch the
   // sums.  ctr == nullptr keeps the fixed stride.
   unsigned it = blockIdx.x * (kTileThreads / 32) + (threadIdx.x >> 5);
+#if SVDSB_EARLY_TRIGGER
+  pdl_trigger();
+#endif
   while (it < nitems) {
     unsigned nxt = it + nwarps;
     if (ctr != nullptr && lane == 0) nxt = nwarps + atomicAdd(ctr, 1u);
@@ -1863,6 +1870,9 @@ csr_chunk_kernel(const int *__restrict__ chunk_nz, const int *__restrict__ col,
                  const double *__restrict__ val, const double *__restrict__ x,
                  int64_t ldx, int xrow, int b, double *__restrict__ part) {
   pdl_wait();
+#if SVDSB_EARLY_TRIGGER
+  pdl_trigger();  // dependants (the fix-up kernel) may be scheduled under this grid's tail; they still wait for its completion
+#endif
   __shared__ double red[kTileThreads / 32][4];
   const int nz0 = chunk_nz[2 * blockIdx.x], nz1 = chunk_nz[2 * blockIdx.x + 1];
   const int t = threadIdx.x;
